@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""AM-QFT benchmark (BASELINE.json config 2 by default).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+One step = one pass of the hot path over one batch: a batched complex fp32
+forward DFT, N=4096, batch=65536 (2 GiB in + 2 GiB out, interleaved re/im,
+iid N(0,1) from a seed), AM-QFT variant 4 (the improved QFT) by default.
+Inputs are resident in HBM when the timed region starts and are 16x larger
+than L2, so no flush is needed between steps.  Multi-GPU (torchrun): every
+rank runs its own 65536-transform shard (weak scaling, no communication);
+time = max over ranks of the CUDA-event time.
+
+--impl reference times the reference's own CPU implementation
+(oracle/_ref/libamqft_ref.so: the unmodified reference library compiled from
+its sources) on the host cores over a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "AM-QFT transforms/s (CDFT N=4096 fp32, batch 65536)"
+UNIT = "transforms/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--variant", type=int, default=4)
+    p.add_argument("--n", type=int, default=4096)
+    p.add_argument("--batch", type=int, default=65536)
+    p.add_argument("--dtype", default="f32")
+    p.add_argument("--order", choices=["fast", "exact"], default="fast")
+    p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--all-variants", action="store_true",
+                   help="also time variants 1..8 (extra 'variants' key)")
+    return p.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons DURING the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [s.strip() for s in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(args, seconds_target=10.0):
+    """Reference CPU path (oracle/_ref) on the host cores, bounded sample of the
+    same workload (fp32 inputs widened to double: the reference is fp64-only)."""
+    import numpy as np
+    from oracle import oracle as O
+    ref = O.reference()
+    kind = "reference"
+    if ref is None:  # reference never compiled: the C restatement stands in
+        ref = O.restatement()
+        kind = "port"
+    threads = os.cpu_count() or 1
+    n = args.n
+    rng = np.random.default_rng(1234)
+
+    def run(rows):
+        x = rng.standard_normal((rows, 2 * n)).astype(np.float32).astype(np.float64)
+        t0 = time.perf_counter()
+        if kind == "reference":
+            ref.execute_rows(args.variant, O.CDFT, n, x, threads)
+        else:
+            for r in range(rows):
+                ref.execute(args.variant, O.F_CDFT, n, x[r])
+        return time.perf_counter() - t0
+
+    probe = max(threads, 8)
+    dt = run(probe)
+    rate = probe / dt
+    rows = int(min(max(probe, rate * seconds_target), 200000))
+    dt = run(rows)
+    value = rows / dt
+    used = threads if kind == "reference" else 1
+    return {"value": value, "unit": UNIT, "cores": used, "kind": kind,
+            "sample": f"{rows} rows of CDFT N={n} (variant {args.variant}), fp32 data widened to fp64, "
+                      f"{used} threads, {dt:.1f} s",
+            "gbs_fp32_bytes": value * 16 * n / 1e9}
+
+
+def bench_reference(args, rank):
+    """--impl reference: the reference's own CPU implementation, rank 0 only."""
+    if rank != 0:
+        return None
+    cb = None
+    times = []
+    for _ in range(args.warmup):
+        cpu_baseline(args, seconds_target=1.0)
+    for _ in range(args.steps):
+        cb = cpu_baseline(args, seconds_target=3.0)
+        times.append(cb["value"])
+    value = statistics.median(times)
+    cb["value"] = value
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * args.batch / value, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic N(0,1) (seeded), fp32 values widened to fp64",
+        "config": {"workload": f"config 2: batched CDFT N={args.n} x {args.batch}, variant {args.variant}",
+                   "n": args.n, "batch": args.batch, "variant": args.variant,
+                   "parallelism": "host threads"},
+        "cpu_baseline": cb,
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    return line
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        line = bench_reference(args, rank)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_1404_1810_b200 as amqft
+
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    n, batch = args.n, args.batch
+    dtype = torch.float32 if args.dtype == "f32" else torch.float64
+    esize = 4 if args.dtype == "f32" else 8
+    order = amqft.Order.Fast if args.order == "fast" else amqft.Order.Exact
+    plan = amqft.Plan(args.variant, amqft.FunctionId.Cdft, n, batch, dtype=args.dtype,
+                      order=order, device=local)
+    path, launches = plan.path()
+    g = torch.Generator(device=dev)
+    g.manual_seed(20260 + rank)
+    x = torch.randn(batch, 2 * n, generator=g, device=dev, dtype=dtype)
+    y = torch.empty_like(x)
+    stream = torch.cuda.current_stream(dev)
+
+    for _ in range(max(args.warmup, 3)):
+        plan.forward(x, y, stream=stream)
+    torch.cuda.synchronize(dev)
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        plan.forward(x, y, stream=stream)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = world * batch * args.steps / (ms / 1000.0)
+
+    # Dominant-kernel roofline: the exec call is one kernel on path 0/2;
+    # per-launch duration from CUDA events on the launching stream.
+    hbm, hbm_src = peaks()
+    alg_bytes = 2 * (2 * n * esize) * batch  # one read + one write per transform
+    kernel_ms = ms_per_step / max(1, launches) if path != 1 else ms_per_step
+    achieved = alg_bytes / (kernel_ms / 1000.0) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm, "traffic": None,
+            "peak_source": hbm_src, "algorithmic_bytes_per_launch": alg_bytes,
+            "kernel_ms": kernel_ms}
+
+    # Parity of what was timed: a few rows against the CPU oracle (checker).
+    parity = None
+    try:
+        from oracle import oracle as O
+        r = O.restatement()
+        errs = []
+        for row in (0, batch // 2, batch - 1):
+            xin = x[row].double().cpu().numpy()
+            want = r.execute(args.variant, O.F_CDFT, n, xin)
+            errs.append(r.rel_l2(y[row].double().cpu().numpy(), want))
+        parity = max(errs)
+    except Exception as e:  # noqa: BLE001
+        parity = f"unavailable: {e}"
+
+    # End to end through the public API with HOST buffers (pinned): H2D of the
+    # step's input, the transform, D2H of the result, every step.
+    e2e = None
+    if args.e2e_steps > 0:
+        hx = torch.empty(batch, 2 * n, dtype=dtype, pin_memory=True)
+        hx.copy_(x)
+        hy = torch.empty_like(hx, pin_memory=True)
+        plan.forward(x, y, stream=stream)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(args.e2e_steps):
+            x.copy_(hx, non_blocking=True)
+            plan.forward(x, y, stream=stream)
+            hy.copy_(y, non_blocking=True)
+        s1.record(stream)
+        torch.cuda.synchronize(dev)
+        ems = torch.tensor([s0.elapsed_time(s1)], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * batch * args.e2e_steps / (float(ems.item()) / 1000.0), "unit": UNIT,
+               "h2d_bytes_per_step": batch * 2 * n * esize, "d2h_bytes_per_step": batch * 2 * n * esize,
+               "steps": args.e2e_steps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(args)
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                   "sample": f"failed: {e}"}
+
+    variants = None
+    if args.all_variants:
+        variants = {}
+        for v in range(1, 9):
+            pv = amqft.Plan(v, amqft.FunctionId.Cdft, n, batch, dtype=args.dtype, order=order,
+                            device=local)
+            for _ in range(3):
+                pv.forward(x, y, stream=stream)
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(args.steps):
+                pv.forward(x, y, stream=stream)
+            b.record(stream)
+            torch.cuda.synchronize(dev)
+            vms = a.elapsed_time(b) / args.steps
+            variants[str(v)] = {"transforms_per_s": batch / (vms / 1000.0), "ms": vms,
+                                "gbs": alg_bytes / (vms / 1000.0) / 1e9}
+            pv.close()
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": args.dtype, "data": "synthetic: iid N(0,1) from a seed (torch.Generator)",
+            "config": {"workload": f"config 2: batched complex forward DFT N={n}, batch {batch} per GPU, "
+                                   f"interleaved re/im, AM-QFT variant {args.variant}",
+                       "n": n, "batch_per_gpu": batch, "variant": args.variant,
+                       "order": args.order, "path": path, "launches_per_step": launches,
+                       "l2": "inputs 2 GiB per GPU > 126 MB L2; no flush",
+                       "parallelism": f"batch-sharded x{world}, no communication"},
+            "gbs": alg_bytes * world / (ms_per_step / 1000.0) / 1e9,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clocks,
+            "gpu_launches": launches * args.steps,
+            "parity_rel_l2_vs_cpu_same_variant": parity,
+        }
+        if variants:
+            line["variants"] = variants
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,158 @@
+/*
+ * amqft_b200.h -- C ABI of the B200 AM-QFT library (libamqft_b200.so).
+ *
+ * Drop-in boundary for the reference's transform entry point
+ *   SignalBuffer amqft::execute(VariantId, FunctionId, const SignalBuffer&,
+ *                               const TrigSource&, OpMeter*)
+ *   (/root/reference/proj/include/amqft/variants.hpp:148-153,
+ *    src/variants.cpp:404-442)
+ * and its constant-table plugin
+ *   TrigTable(VariantId, max_periodization, TrigMode)
+ *   (include/amqft/variants.hpp:111-141, src/variants.cpp:248-299).
+ * The C++ header amqft_b200.hpp keeps the reference names on top of this.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Device pointers are caller-owned and
+ *    must stay valid until the stream work completes.  `stream` is a
+ *    cudaStream_t passed as void* (NULL = legacy default stream).
+ *  - Cell layout per transform is the reference SignalBuffer layout
+ *    (include/amqft/signal.hpp:110-146): CDFT = 2N interleaved re/im reals,
+ *    RDFT = N reals (packed spectrum Re S(j), j <= N/2, then Im S(j)),
+ *    DCT = N/2+1, DST = N/2-1, restricted types per their stored ranges.
+ *    Batches are row-major: row r starts at r * cells.
+ *  - Transforms are unnormalised forward sums with kernel e^{-2 pi i nk/N}
+ *    (src/oracle.cpp:69-84).  amqft_exec_inverse (CDFT only) is the
+ *    builder-defined inverse x = swap(DFT(swap(X))) / N, exact in its swap
+ *    and power-of-two scale.
+ *  - Errors mirror the reference's std::invalid_argument cases
+ *    (variants.cpp:404-421, signal.cpp:138-147) as AMQFT_EINVAL;
+ *    amqft_last_error() returns the message (thread-local).
+ *  - There is no CPU fallback: without a usable CUDA device every exec
+ *    call returns AMQFT_ECUDA.
+ */
+#ifndef AMQFT_B200_H
+#define AMQFT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  AMQFT_OK = 0,
+  AMQFT_EINVAL = 1, /* reference: std::invalid_argument */
+  AMQFT_ECUDA = 2,
+  AMQFT_ENCCL = 3,
+  AMQFT_ENOMEM = 4
+} amqft_status;
+
+/* FunctionId, same order as include/amqft/variants.hpp:55-66. */
+typedef enum {
+  AMQFT_FN_CDFT = 0,
+  AMQFT_FN_RDFT = 1,
+  AMQFT_FN_DCT = 2,
+  AMQFT_FN_DST = 3,
+  AMQFT_FN_DCT_ODD_TIME = 4,
+  AMQFT_FN_DST_ODD_TIME = 5,
+  AMQFT_FN_DCT_ODD_HARM = 6,
+  AMQFT_FN_DST_ODD_HARM = 7,
+  AMQFT_FN_DCT_ODD_ODD = 8,
+  AMQFT_FN_DST_ODD_ODD = 9
+} amqft_function;
+
+typedef enum { AMQFT_F32 = 0, AMQFT_F64 = 1 } amqft_dtype;
+
+/* TrigMode (variants.hpp:108): TABLE = Precomputed (host long-double
+ * constants, bitwise the reference's); ONTHEFLY = computed on the device
+ * with sincospi in the plan's dtype (close to, not bitwise, the table). */
+typedef enum { AMQFT_TRIG_TABLE = 0, AMQFT_TRIG_ONTHEFLY = 1 } amqft_trig_mode;
+
+/* Execution order.  EXACT: every node's operations in the reference's
+ * operand order and association, no FMA contraction, serial M1/M3/M5/M7
+ * recurrences -> bitwise equal to amqft::execute in F64.  FAST: the
+ * specialised fused kernels (same DAG; recurrences may be evaluated as
+ * parallel scans; F32 and F64). */
+typedef enum { AMQFT_ORDER_EXACT = 0, AMQFT_ORDER_FAST = 1 } amqft_order;
+
+typedef struct amqft_plan_s* amqft_plan;
+
+typedef struct {
+  int variant;          /* 1..8 (VariantId) */
+  int function;         /* amqft_function */
+  size_t n;             /* periodization, power of two >= the function base */
+  size_t batch;         /* rows per exec call */
+  int dtype;            /* amqft_dtype */
+  int trig_mode;        /* amqft_trig_mode */
+  int order;            /* amqft_order */
+  int device;           /* CUDA device ordinal */
+  size_t table_max_n;   /* TrigTable max periodization; 0 = max(n, 8) */
+  int corrupt_constants;/* TrigTable::corrupt_for_testing (variants.cpp:301) */
+} amqft_plan_desc;
+
+/* Plan lifecycle.  Creation compiles the schedule, uploads it and the
+ * constant table, and sizes the workspace; exec allocates nothing. */
+amqft_status amqft_plan_create(amqft_plan* out, const amqft_plan_desc* desc);
+amqft_status amqft_plan_destroy(amqft_plan plan);
+
+/* Cells per row of the plan's operand (cell_count, signal.cpp:254-258). */
+size_t amqft_plan_cells(amqft_plan plan);
+
+/* Forward transform of `plan->batch` rows: d_in -> d_out (may alias). */
+amqft_status amqft_exec_forward(amqft_plan plan, const void* d_in, void* d_out,
+                                void* stream);
+
+/* Inverse CDFT of `batch` rows (swap trick; CDFT plans only). */
+amqft_status amqft_exec_inverse(amqft_plan plan, const void* d_in, void* d_out,
+                                void* stream);
+
+/* Forward / inverse with an explicit row count <= plan batch. */
+amqft_status amqft_exec_rows(amqft_plan plan, const void* d_in, void* d_out,
+                             size_t rows, int inverse, void* stream);
+
+/* Convenience mirror of amqft::execute: one signal, HOST buffers (upload,
+ * run on the device, download, synchronise).  meter3 (nullable) receives
+ * {adds, muls, binary translations} of the executed schedule. */
+amqft_status amqft_execute_host(int variant, int function, size_t n,
+                                const double* in, double* out, int trig_mode,
+                                size_t table_max_n, int corrupt_constants,
+                                uint64_t* meter3);
+
+/* Arithmetic performed per row by the compiled schedule (OpMeter,
+ * include/amqft/opmeter.hpp:13-29): {adds, muls, binary translations}. */
+amqft_status amqft_plan_op_counts(amqft_plan plan, uint64_t* out3);
+
+/* Which kernel path the plan uses: 0 generic single-CTA schedule,
+ * 1 generic multi-pass, 2 fused fast kernel.  Number of kernel launches
+ * per exec call in *launches. */
+amqft_status amqft_plan_path(amqft_plan plan, int* path, int* launches);
+
+/* Serialise the compiled schedule for host-side inspection (tests):
+ * writes up to cap 16-byte elaboration records {op,lens,flags,am,n,off,aux}
+ * of program `prog` (0 = root) and returns the record count in *count;
+ * stage boundaries (pairs begin,end) go to stages (cap2 pairs). */
+amqft_status amqft_plan_dump(amqft_plan plan, int prog, void* records,
+                             size_t cap, size_t* count, uint32_t* stages,
+                             size_t cap2, size_t* nstages);
+
+/* Host-only schedule compilation (no device needed): compiles (variant,
+ * function, n) for a CTA capacity of `capacity_cells` and serialises the
+ * single-CTA stage program as amqft_plan_dump does.  Returns AMQFT_EINVAL
+ * for requests the reference rejects.  ops3 (nullable) receives the
+ * schedule's {adds, muls, binary translations}. */
+amqft_status amqft_schedule_dump(int variant, int function, size_t n,
+                                 size_t capacity_cells, void* records,
+                                 size_t cap, size_t* count, uint32_t* stages,
+                                 size_t cap2, size_t* nstages, uint64_t* ops3);
+
+/* Device synchronisation helper and error text. */
+amqft_status amqft_device_synchronize(int device);
+const char* amqft_last_error(void);
+const char* amqft_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* AMQFT_B200_H */

@@ -1,0 +1,431 @@
+// engine.cu -- plan objects, kernel launches and the C ABI (amqft_b200.h).
+//
+// Execution paths (chosen at plan creation, no runtime fallback):
+//   path 0  generic single-CTA: one CTA per row runs the whole compiled
+//           stage program out of shared memory (k_prog).
+//   path 1  generic multi-pass: nodes whose operand exceeds the CTA
+//           capacity run as grid-wide stages over two HBM arenas (k_stage),
+//           the subtrees below as per-CTA jobs (k_prog).  This keeps the
+//           reference recursion (and fp64 bitwise parity) at any N.
+//   path 2  fused fast kernels (fast.cuh) for the CDFT hot path.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/amqft_b200.h"
+#include "fast.cuh"
+#include "generic_exec.hpp"
+#include "plan.hpp"
+#include "trig.hpp"
+
+using namespace amqft_b200;
+
+namespace {
+
+thread_local std::string g_err;
+
+}  // namespace
+
+namespace amqft_b200 {
+void set_last_error(const std::string& m) { g_err = m; }
+}  // namespace amqft_b200
+
+namespace {
+
+amqft_status set_err(amqft_status s, const std::string& m) {
+  g_err = m;
+  return s;
+}
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// Kernels and launchers live in generic_kernels.cuh (instantiated per dtype
+// in generic_f32.cu / generic_f64.cu so the build parallelises).
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Plan object.
+
+struct amqft_plan_s {
+  amqft_plan_desc d{};
+  Compiled c;
+  int path = 0;
+  int T = 256, K = 1;
+  size_t smem = 0;
+  size_t capacity = 0;
+  size_t esize = 8;
+  uint32_t nmax = 8;
+  // device arrays
+  void* d_trig = nullptr;
+  EI* d_eis = nullptr;
+  uint32_t* d_prefix = nullptr;
+  Stage* d_stages = nullptr;
+  ProgInfo* d_progs = nullptr;
+  JobDev* d_jobs = nullptr;   // multi-pass jobs; for path 0 a single job
+  uint32_t njobs = 0;
+  EI* d_geis = nullptr;       // global EIs
+  uint32_t* d_gprefix = nullptr;
+  void* bufA = nullptr;
+  void* bufB = nullptr;
+  std::unique_ptr<FastPlan> fast;
+  int launches = 0;
+  int sms = 148;
+
+  ~amqft_plan_s() {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(d.device);
+    for (void* p : {static_cast<void*>(d_trig), static_cast<void*>(d_eis),
+                    static_cast<void*>(d_prefix), static_cast<void*>(d_stages),
+                    static_cast<void*>(d_progs), static_cast<void*>(d_jobs),
+                    static_cast<void*>(d_geis), static_cast<void*>(d_gprefix),
+                    bufA, bufB})
+      if (p) cudaFree(p);
+    fast.reset();
+    cudaSetDevice(cur);
+  }
+};
+
+namespace {
+
+template <typename Tv>
+Tv* upload(const std::vector<Tv>& v) {
+  if (v.empty()) return nullptr;
+  Tv* p = nullptr;
+  ck(cudaMalloc(&p, v.size() * sizeof(Tv)), "cudaMalloc");
+  ck(cudaMemcpy(p, v.data(), v.size() * sizeof(Tv), cudaMemcpyHostToDevice), "cudaMemcpy");
+  return p;
+}
+
+int pick_k(uint32_t per_thread) {
+  int k = 1;
+  while (k < static_cast<int>(per_thread)) k *= 2;
+  return k;
+}
+
+void build_generic(amqft_plan_s* P) {
+  const Compiled& c = P->c;
+  // Concatenate programs.
+  std::vector<EI> eis;
+  std::vector<uint32_t> prefix;
+  std::vector<Stage> stages;
+  std::vector<ProgInfo> infos;
+  uint32_t max_items = 0, max_cells = 0;
+  for (const SubProgram& sp : c.progs) {
+    ProgInfo pi;
+    pi.ei_base = static_cast<uint32_t>(eis.size());
+    pi.stage_base = static_cast<uint32_t>(stages.size());
+    pi.nstages = static_cast<uint32_t>(sp.stages.size());
+    pi.cells = static_cast<uint32_t>(sp.cells);
+    eis.insert(eis.end(), sp.eis.begin(), sp.eis.end());
+    prefix.insert(prefix.end(), sp.prefix.begin(), sp.prefix.end());
+    stages.insert(stages.end(), sp.stages.begin(), sp.stages.end());
+    infos.push_back(pi);
+    max_items = std::max(max_items, sp.max_items);
+    max_cells = std::max(max_cells, static_cast<uint32_t>(sp.cells));
+  }
+  P->T = max_items > 1024 ? 512 : 256;
+  P->K = pick_k((max_items + P->T - 1) / P->T);
+  if (P->K > 32) throw std::invalid_argument("subtree too large for one CTA");
+  P->smem = std::max<size_t>(16, max_cells * P->esize);
+  P->d_eis = upload(eis);
+  P->d_prefix = upload(prefix);
+  P->d_stages = upload(stages);
+  P->d_progs = upload(infos);
+  std::vector<JobDev> jobs;
+  if (c.single) {
+    jobs.push_back(JobDev{0, 0, 0, 0});
+  } else {
+    for (const Job& j : c.jobs) jobs.push_back(JobDev{j.prog, j.off, j.src, j.dst});
+    std::vector<uint32_t> gp(c.global_eis.size());
+    for (const auto* sv : {&c.fwd_stages, &c.bwd_stages})
+      for (const Stage& st : *sv) {
+        uint32_t acc = 0;
+        for (uint32_t k = st.ei_begin; k < st.ei_end; ++k) {
+          gp[k] = acc;
+          acc += ei_items(c.global_eis[k]);
+        }
+      }
+    P->d_geis = upload(c.global_eis);
+    P->d_gprefix = upload(gp);
+    const size_t bytes = P->d.batch * c.cells * P->esize;
+    ck(cudaMalloc(&P->bufA, bytes), "cudaMalloc arena A");
+    ck(cudaMalloc(&P->bufB, bytes), "cudaMalloc arena B");
+  }
+  P->njobs = static_cast<uint32_t>(jobs.size());
+  P->d_jobs = upload(jobs);
+  P->launches = c.single ? 1
+                         : static_cast<int>(2 + c.fwd_stages.size() + c.bwd_stages.size() + 1);
+}
+
+template <typename R>
+void exec_generic(amqft_plan_s* P, const void* in, void* out, size_t rows,
+                  int inverse, cudaStream_t st) {
+  const Compiled& c = P->c;
+  TrigRef trig{P->d_trig, P->nmax, static_cast<uint32_t>(modulation_kind(P->d.variant)),
+               static_cast<uint32_t>(P->d.trig_mode == AMQFT_TRIG_ONTHEFLY)};
+  const double scale = 1.0 / static_cast<double>(P->d.n);
+  const size_t sms = static_cast<size_t>(P->sms);
+  const int swap = inverse ? 1 : 0;
+  ProgLaunch L{};
+  L.eis = P->d_eis;
+  L.prefix = P->d_prefix;
+  L.stages = P->d_stages;
+  L.progs = P->d_progs;
+  L.jobs = P->d_jobs;
+  L.trig = trig;
+  L.smem = P->smem;
+  L.T = P->T;
+  L.K = P->K;
+  L.stream = st;
+  L.arena = c.cells;
+  L.rows = rows;
+  if (c.single) {
+    L.njobs = 1;
+    L.srcA = in;
+    L.dstA = out;
+    L.swap_in = L.swap_out = swap;
+    L.scale = scale;
+    L.grid = static_cast<unsigned>(std::min<size_t>(rows, sms * 32));
+    ck(launch_prog<R>(L), "k_prog launch");
+    return;
+  }
+  void* A = P->bufA;
+  void* B = P->bufB;
+  const size_t total = rows * c.cells;
+  const unsigned cgrid = static_cast<unsigned>(std::min<size_t>((total + 255) / 256, sms * 64));
+  ck(launch_copy<R>(in, c.root_src ? B : A, total, swap, 1.0, cgrid, st), "k_copy_rows");
+  auto stage_run = [&](const Stage& s) {
+    const size_t work = static_cast<size_t>(s.items) * rows;
+    const unsigned g = static_cast<unsigned>(std::min<size_t>((work + 255) / 256, sms * 64));
+    ck(launch_stage<R>(P->d_geis, P->d_gprefix, s, A, B, c.cells, rows, trig, g, st), "k_stage");
+  };
+  for (const Stage& s : c.fwd_stages) stage_run(s);
+  L.njobs = P->njobs;
+  L.srcA = A;
+  L.srcB = B;
+  L.dstA = A;
+  L.dstB = B;
+  L.swap_in = L.swap_out = 0;
+  L.scale = 1.0;
+  L.grid = static_cast<unsigned>(std::min<size_t>(rows * P->njobs, sms * 32));
+  ck(launch_prog<R>(L), "k_prog jobs launch");
+  for (const Stage& s : c.bwd_stages) stage_run(s);
+  ck(launch_copy<R>(c.root_dst ? B : A, out, total, swap, scale, cgrid, st), "k_copy_rows");
+}
+
+amqft_status validate_desc(const amqft_plan_desc* d) {
+  if (!d) return set_err(AMQFT_EINVAL, "null plan descriptor");
+  if (d->variant < 1 || d->variant > 8) return set_err(AMQFT_EINVAL, "variant number must be in 1..8");
+  if (d->function < 0 || d->function >= kNumFn) return set_err(AMQFT_EINVAL, "unknown function");
+  if (d->dtype != AMQFT_F32 && d->dtype != AMQFT_F64) return set_err(AMQFT_EINVAL, "dtype must be F32 or F64");
+  if (d->trig_mode != AMQFT_TRIG_TABLE && d->trig_mode != AMQFT_TRIG_ONTHEFLY)
+    return set_err(AMQFT_EINVAL, "unknown trig mode");
+  if (d->order != AMQFT_ORDER_EXACT && d->order != AMQFT_ORDER_FAST)
+    return set_err(AMQFT_EINVAL, "unknown execution order");
+  if (d->batch == 0) return set_err(AMQFT_EINVAL, "batch must be >= 1");
+  return AMQFT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* amqft_last_error(void) { return g_err.c_str(); }
+const char* amqft_version(void) { return "amqft_b200 0.1 (sm_100a)"; }
+
+amqft_status amqft_plan_create(amqft_plan* out, const amqft_plan_desc* desc) {
+  if (!out) return set_err(AMQFT_EINVAL, "null plan pointer");
+  *out = nullptr;
+  const amqft_status vs = validate_desc(desc);
+  if (vs != AMQFT_OK) return vs;
+  std::unique_ptr<amqft_plan_s> P(new amqft_plan_s());
+  P->d = *desc;
+  try {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      return set_err(AMQFT_ECUDA, "no CUDA device: the AM-QFT library has no CPU path");
+    if (desc->device < 0 || desc->device >= ndev)
+      return set_err(AMQFT_EINVAL, "device ordinal out of range");
+    ck(cudaSetDevice(desc->device), "cudaSetDevice");
+    cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, desc->device);
+    P->esize = desc->dtype == AMQFT_F64 ? 8 : 4;
+    const size_t n = desc->n;
+    const size_t tmax = desc->table_max_n ? desc->table_max_n : std::max<size_t>(n, 8);
+    if (tmax < n || (tmax & (tmax - 1)) != 0 || tmax < 8)
+      return set_err(AMQFT_EINVAL, "constant table needs a power-of-two max periodization >= max(n, 8)");
+    P->nmax = static_cast<uint32_t>(tmax);
+    // Constant table (TrigTable::constants layout), host long double.
+    const std::vector<double> tab =
+        trig_table(desc->variant, tmax, desc->corrupt_constants != 0);
+    if (desc->dtype == AMQFT_F64) {
+      P->d_trig = upload(tab);
+    } else {
+      std::vector<float> tf(tab.begin(), tab.end());
+      P->d_trig = upload(tf);
+    }
+    // Fast fused path where one exists for this request.
+    if (desc->order == AMQFT_ORDER_FAST) {
+      P->fast = make_fast_plan(*desc, P->d_trig, P->nmax);
+      if (P->fast) {
+        P->path = 2;
+        P->c.variant = desc->variant;
+        P->c.fn = desc->function;
+        P->c.n = n;
+        P->c.cells = fn_cells(desc->function, n);
+        P->c.ops = fast_op_counts(*desc);
+        P->launches = P->fast->launches;
+        *out = P.release();
+        return AMQFT_OK;
+      }
+    }
+    P->capacity = desc->dtype == AMQFT_F64 ? 8192 : 16384;
+    P->c = compile(desc->variant, desc->function, n, P->capacity);
+    P->path = P->c.single ? 0 : 1;
+    build_generic(P.get());
+  } catch (const std::invalid_argument& e) {
+    return set_err(AMQFT_EINVAL, e.what());
+  } catch (const CudaError& e) {
+    return set_err(AMQFT_ECUDA, e.what());
+  } catch (const std::bad_alloc&) {
+    return set_err(AMQFT_ENOMEM, "host allocation failed");
+  }
+  *out = P.release();
+  return AMQFT_OK;
+}
+
+amqft_status amqft_plan_destroy(amqft_plan plan) {
+  delete plan;
+  return AMQFT_OK;
+}
+
+size_t amqft_plan_cells(amqft_plan plan) { return plan ? plan->c.cells : 0; }
+
+amqft_status amqft_exec_rows(amqft_plan P, const void* in, void* out, size_t rows,
+                             int inverse, void* stream) {
+  if (!P) return set_err(AMQFT_EINVAL, "null plan");
+  if (rows > P->d.batch) return set_err(AMQFT_EINVAL, "rows exceed the plan batch");
+  if (inverse && P->d.function != AMQFT_FN_CDFT)
+    return set_err(AMQFT_EINVAL, "the inverse is defined for CDFT plans only");
+  if (rows == 0) return AMQFT_OK;
+  if (!in || !out) return set_err(AMQFT_EINVAL, "null data pointer");
+  try {
+    ck(cudaSetDevice(P->d.device), "cudaSetDevice");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (P->path == 2) {
+      P->fast->exec(in, out, rows, inverse, st);
+    } else if (P->d.dtype == AMQFT_F64) {
+      exec_generic<double>(P, in, out, rows, inverse, st);
+    } else {
+      exec_generic<float>(P, in, out, rows, inverse, st);
+    }
+  } catch (const std::invalid_argument& e) {
+    return set_err(AMQFT_EINVAL, e.what());
+  } catch (const CudaError& e) {
+    return set_err(AMQFT_ECUDA, e.what());
+  }
+  return AMQFT_OK;
+}
+
+amqft_status amqft_exec_forward(amqft_plan P, const void* in, void* out, void* stream) {
+  return amqft_exec_rows(P, in, out, P ? P->d.batch : 0, 0, stream);
+}
+
+amqft_status amqft_exec_inverse(amqft_plan P, const void* in, void* out, void* stream) {
+  return amqft_exec_rows(P, in, out, P ? P->d.batch : 0, 1, stream);
+}
+
+amqft_status amqft_plan_op_counts(amqft_plan P, uint64_t* out3) {
+  if (!P || !out3) return set_err(AMQFT_EINVAL, "null argument");
+  out3[0] = P->c.ops.adds;
+  out3[1] = P->c.ops.muls;
+  out3[2] = P->c.ops.bt;
+  return AMQFT_OK;
+}
+
+amqft_status amqft_plan_path(amqft_plan P, int* path, int* launches) {
+  if (!P) return set_err(AMQFT_EINVAL, "null plan");
+  if (path) *path = P->path;
+  if (launches) *launches = P->launches;
+  return AMQFT_OK;
+}
+
+amqft_status amqft_plan_dump(amqft_plan P, int prog, void* records, size_t cap,
+                             size_t* count, uint32_t* stages, size_t cap2,
+                             size_t* nstages) {
+  if (!P) return set_err(AMQFT_EINVAL, "null plan");
+  if (P->path == 2) return set_err(AMQFT_EINVAL, "fused plans carry no stage program");
+  if (prog < 0 || static_cast<size_t>(prog) >= P->c.progs.size())
+    return set_err(AMQFT_EINVAL, "no such program");
+  const SubProgram& sp = P->c.progs[prog];
+  if (count) *count = sp.eis.size();
+  if (records) std::memcpy(records, sp.eis.data(), std::min(cap, sp.eis.size()) * sizeof(EI));
+  if (nstages) *nstages = sp.stages.size();
+  if (stages)
+    for (size_t s = 0; s < std::min(cap2, sp.stages.size()); ++s) {
+      stages[2 * s] = sp.stages[s].ei_begin;
+      stages[2 * s + 1] = sp.stages[s].ei_end;
+    }
+  return AMQFT_OK;
+}
+
+amqft_status amqft_execute_host(int variant, int function, size_t n, const double* in,
+                                double* out, int trig_mode, size_t table_max_n,
+                                int corrupt_constants, uint64_t* meter3) {
+  amqft_plan_desc d{};
+  d.variant = variant;
+  d.function = function;
+  d.n = n;
+  d.batch = 1;
+  d.dtype = AMQFT_F64;
+  d.trig_mode = trig_mode;
+  d.order = AMQFT_ORDER_EXACT;
+  d.device = 0;
+  cudaGetDevice(&d.device);
+  d.table_max_n = table_max_n;
+  d.corrupt_constants = corrupt_constants;
+  amqft_plan P = nullptr;
+  amqft_status s = amqft_plan_create(&P, &d);
+  if (s != AMQFT_OK) return s;
+  const size_t bytes = P->c.cells * sizeof(double);
+  void *din = nullptr, *dout = nullptr;
+  try {
+    ck(cudaMalloc(&din, bytes), "cudaMalloc");
+    ck(cudaMalloc(&dout, bytes), "cudaMalloc");
+    ck(cudaMemcpy(din, in, bytes, cudaMemcpyHostToDevice), "cudaMemcpy H2D");
+    s = amqft_exec_rows(P, din, dout, 1, 0, nullptr);
+    if (s == AMQFT_OK) {
+      ck(cudaMemcpy(out, dout, bytes, cudaMemcpyDeviceToHost), "cudaMemcpy D2H");
+      if (meter3) amqft_plan_op_counts(P, meter3);
+    }
+  } catch (const CudaError& e) {
+    s = set_err(AMQFT_ECUDA, e.what());
+  }
+  cudaFree(din);
+  cudaFree(dout);
+  amqft_plan_destroy(P);
+  return s;
+}
+
+amqft_status amqft_device_synchronize(int device) {
+  if (cudaSetDevice(device) != cudaSuccess) return set_err(AMQFT_ECUDA, "cudaSetDevice failed");
+  const cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return set_err(AMQFT_ECUDA, cudaGetErrorString(e));
+  return AMQFT_OK;
+}
+
+}  // extern "C"
