@@ -37,7 +37,7 @@ def test_exact_fp64_every_function_bitwise(oracle, restatement, v):
         n = O.FUNCTION_BASE[f]
         while n <= 4096:
             t = O.FUNCTION_OPERAND[f]
-            rows = [r.uniform(r.mix_seed(77, v, f, n, row), r.cell_count(t, n)) for row in range(3)]
+            rows = [r.uniform(r.mix_seed(77, v, f, 8 * n + row), r.cell_count(t, n)) for row in range(3)]
             plan = amqft.Plan(v, f, n, 3, dtype="f64", order=amqft.Order.Exact)
             got = run_plan(plan, rows)
             for row in range(3):
