@@ -1,0 +1,418 @@
+#!/usr/bin/env python3
+"""Generates csrc/fast_gen.cuh: straight-line per-thread code for the
+bottom of the AM-QFT recursion (see tests/fast_model.py for the proven
+formulation and csrc/fast.cu for the kernel that calls these functions).
+
+Per variant family:
+  time-major (1,4,5,8)
+    tmB  one index-space segment [a, a+LB]: remaining mirror folds (forward),
+         then the spectra of every block inside (AM_B neighbour ops / serial
+         recurrences), scattered to the frequency layout.
+    tmS  the cells at multiples of LB (small top blocks + Dct(2)/Dst(4)):
+         their backward and the chain recombination up to Dct/Dst(N/LB).
+  harmonic-major (2,3,6,7)
+    hmB  one frequency-space segment: gathers + AM_F of the blocks inside
+         (read from the temporal layout), then the bottom mirror levels.
+    hmS  the small top blocks: chain folds up to N/LB, their forward, leaves
+         placed at multiples of LB, and the Dct(2)/Dst(4) bases.
+
+Every emitted operation is one of the reference's add/sub/mul on the
+reference's operands (AR::add/sub/mul = __fadd_rn/__dadd_rn..., never
+contracted), so the fp64 instantiation is bitwise the reference recursion.
+
+  python3 paper_1404_1810_b200/codegen/gen_fast.py > paper_1404_1810_b200/csrc/fast_gen.cuh
+"""
+from __future__ import annotations
+
+import sys
+
+TM = (1, 4, 5, 8)
+HM = (2, 3, 6, 7)
+
+
+class Emitter:
+    def __init__(self):
+        self.lines = []
+        self.tmp = 0
+
+    def emit(self, s):
+        self.lines.append("  " + s)
+
+    def new(self, expr):
+        self.tmp += 1
+        name = f"t{self.tmp}"
+        self.emit(f"const R {name} = {expr};")
+        return name
+
+
+def add(a, b):
+    return f"AR::add({a}, {b})"
+
+
+def sub(a, b):
+    return f"AR::sub({a}, {b})"
+
+
+def mul(a, b):
+    return f"AR::mul({a}, {b})"
+
+
+def half(a):
+    return f"AR::mul(R(0.5), {a})"
+
+
+def const_expr(v, L):
+    """AM constant f(pi v / L): table slot v*nmax/(2L) (variants.cpp:281)."""
+    if v == L // 4:
+        return "base"
+    lg = (2 * L).bit_length() - 1
+    return f"__ldg(tab + ({v} * (nmax >> {lg}) - 1))"
+
+
+# --------------------------------------------------------------- time-major
+def am_b_tm(em, v, lens, C):
+    q = len(C)
+    O = [None] * q
+    if v == 4:
+        if lens == 0:
+            for j in range(q - 1):
+                O[j] = em.new(add(C[j], C[j + 1]))
+            O[q - 1] = C[q - 1]
+        else:
+            O[0] = C[0]
+            for j in range(1, q):
+                O[j] = em.new(add(C[j - 1], C[j]))
+    elif v == 8:
+        if lens == 0:
+            O[0] = C[0]
+            for j in range(1, q):
+                O[j] = em.new(sub(C[j], C[j - 1]))
+        else:
+            for j in range(q - 1):
+                O[j] = em.new(sub(C[j], C[j + 1]))
+            O[q - 1] = C[q - 1]
+    elif v == 1:
+        if lens == 0:
+            O[0] = em.new(half(C[0]))
+            for j in range(1, q):
+                O[j] = em.new(sub(C[j], O[j - 1]))
+        else:
+            O[q - 1] = em.new(half(C[q - 1]))
+            for j in range(q - 2, -1, -1):
+                O[j] = em.new(sub(C[j], O[j + 1]))
+    elif v == 5:
+        if lens == 0:
+            O[q - 1] = em.new(half(C[q - 1]))
+            for j in range(q - 2, -1, -1):
+                O[j] = em.new(add(C[j], O[j + 1]))
+        else:
+            O[0] = em.new(half(C[0]))
+            for j in range(1, q):
+                O[j] = em.new(add(C[j], O[j - 1]))
+    return O
+
+
+def interleave(lens, E, O):
+    out = []
+    for e, o in zip(E, O):
+        out += [e, o] if lens == 0 else [o, e]
+    return out
+
+
+def mnet_fwd(em, x, a, L, rho, lens, sine):
+    if L < 4:
+        return
+    for v in range(1, L // 2):
+        lo, hi = a + v, a + L - v
+        j, m = (lo, hi) if rho == 0 else (hi, lo)
+        p, q = x[j], x[m]
+        s, d = add(p, q), sub(p, q)
+        e_expr, o_expr = (s, d) if lens == 0 else (d, s)
+        e_name = em.new(e_expr)
+        o_name = em.new(mul(o_expr, const_expr(v, L)))
+        x[j], x[m] = e_name, o_name
+    lo_l = lens if rho == 0 else lens ^ sine
+    hi_l = lens ^ sine if rho == 0 else lens
+    mnet_fwd(em, x, a, L // 2, 0, lo_l, sine)
+    mnet_fwd(em, x, a + L // 2, L // 2, 1, hi_l, sine)
+
+
+def spectrum_tm(em, v, x, a, L, rho, lens, sine, tcls):
+    m = L >> (tcls + 1)
+    if m == 1:
+        return [x[a + L // 2]]
+    lower, upper = (a, L // 2, 0), (a + L // 2, L // 2, 1)
+    es, os_ = (lower, upper) if rho == 0 else (upper, lower)
+    E = spectrum_tm(em, v, x, *es, lens, sine, tcls)
+    C = spectrum_tm(em, v, x, *os_, lens ^ sine, sine, tcls)
+    O = am_b_tm(em, v, lens, C) if m > 2 else C
+    return interleave(lens, E, O)
+
+
+def gen_tmB(v, LB, rho, lam):
+    sine = 1 if v >= 5 else 0
+    lg = LB.bit_length() - 1
+    em = Emitter()
+    x = {u: f"x{u}" for u in range(1, LB)}
+    for u in range(1, LB):
+        em.emit(f"const R x{u} = T[PH(a + {u})];")
+    x = dict(x)
+    mnet_fwd(em, x, 0, LB, rho, lam, sine)
+    for t in range(lg):
+        sp = spectrum_tm(em, v, x, 0, LB, rho, lam, sine, t)
+        em.emit(f"{{ const int hi = (N >> {t + 1}) - dsto - r;")
+        for p, name in enumerate(sp):
+            em.emit(f"  F[PH(hi - ({p} << D))] = {name};")
+        em.emit("}")
+    sig = (f"template <typename R, typename AR, int LOGLB>\n__device__ __forceinline__ void "
+           f"tmB_v{v}_lb{LB}_r{rho}_l{lam}(const R* __restrict__ T, R* __restrict__ F, int a, "
+           f"const R* __restrict__ tab, int nmax, R base, int N, int D, int r, int dsto)")
+    return sig + " {\n" + "\n".join(em.lines) + "\n}\n"
+
+
+def gen_tmS(v, HP, LB, lam):
+    """Small chain: cells k*LB, k = 0..HP (Dct) / 1..HP-1 (Dst)."""
+    sine = 1 if v >= 5 else 0
+    em = Emitter()
+    y = {}
+    ks = range(0, HP + 1) if lam == 0 else range(1, HP)
+    for k in ks:
+        em.emit(f"const R y{k} = T[PH({k} * {LB})];")
+        y[k] = f"y{k}"
+    G = [None] * (HP + 1)
+    lg = HP.bit_length() - 1
+    ntop = lg if lam == 0 else lg - 1
+    Np = 2 * HP
+    for t in range(ntop):
+        sp = spectrum_tm(em, v, y, 0, HP, 0, lam, sine, t)
+        hi = Np >> (t + 1)
+        for p, name in enumerate(sp):
+            G[hi - p - lam] = name
+    if lam == 0:
+        G[0] = em.new(add(y[0], y[HP]))
+        G[1] = em.new(sub(y[0], y[HP]))
+        n = 4
+    else:
+        G[1] = y[HP // 2]
+        n = 8
+    while n <= Np:
+        if lam == 0:
+            for k in range(n // 4):
+                e, o = G[k], G[n // 2 - k]
+                G[k], G[n // 2 - k] = em.new(add(e, o)), em.new(sub(e, o))
+        else:
+            for k in range(1, n // 4):
+                e, o = G[k], G[n // 2 - k]
+                G[k], G[n // 2 - k] = em.new(add(o, e)), em.new(sub(o, e))
+        n *= 2
+    for k in ks:
+        em.emit(f"F[PH({k})] = {G[k]};")
+    sig = (f"template <typename R, typename AR, int LOGLB>\n__device__ __forceinline__ void "
+           f"tmS_v{v}_hp{HP}_l{lam}(const R* __restrict__ T, R* __restrict__ F, R base)")
+    return sig + " {\n" + "\n".join(em.lines) + "\n}\n"
+
+
+# ----------------------------------------------------------- harmonic-major
+def am_f_hm(em, v, lens, A):
+    q = len(A)
+    C = [None] * q
+    if v == 2:
+        if lens == 0:
+            C[0] = A[0]
+            for j in range(1, q):
+                C[j] = em.new(add(A[j], A[j - 1]))
+        else:
+            C[q - 1] = A[q - 1]
+            for j in range(q - 1):
+                C[j] = em.new(add(A[j + 1], A[j]))
+    elif v == 6:
+        if lens == 0:
+            C[q - 1] = A[q - 1]
+            for j in range(q - 1):
+                C[j] = em.new(sub(A[j], A[j + 1]))
+        else:
+            C[0] = A[0]
+            for j in range(1, q):
+                C[j] = em.new(sub(A[j], A[j - 1]))
+    elif v == 3:
+        if lens == 0:
+            C[q - 1] = A[q - 1]
+            for j in range(q - 2, 0, -1):
+                C[j] = em.new(sub(A[j], C[j + 1]))
+            C[0] = em.new(half(sub(A[0], C[1])))
+        else:
+            C[0] = A[0]
+            for j in range(1, q - 1):
+                C[j] = em.new(sub(A[j], C[j - 1]))
+            C[q - 1] = em.new(half(sub(A[q - 1], C[q - 2])))
+    elif v == 7:
+        if lens == 0:
+            C[0] = A[0]
+            for j in range(1, q - 1):
+                C[j] = em.new(add(A[j], C[j - 1]))
+            C[q - 1] = em.new(half(add(A[q - 1], C[q - 2])))
+        else:
+            C[q - 1] = A[q - 1]
+            for j in range(q - 2, 0, -1):
+                C[j] = em.new(add(A[j], C[j + 1]))
+            C[0] = em.new(half(add(A[0], C[1])))
+    return C
+
+
+def place_hm(em, v, vals, lens, sine, x, a, L, rho):
+    m = len(vals)
+    if m == 1:
+        x[a + L // 2] = vals[0]
+        return
+    if lens == 0:
+        E, A = vals[0::2], vals[1::2]
+    else:
+        E, A = vals[1::2], vals[0::2]
+    C = am_f_hm(em, v, lens, A) if m > 2 else A
+    lower, upper = (a, L // 2, 0), (a + L // 2, L // 2, 1)
+    es, os_ = (lower, upper) if rho == 0 else (upper, lower)
+    place_hm(em, v, E, lens, sine, x, *es)
+    place_hm(em, v, C, lens ^ sine, sine, x, *os_)
+
+
+def mnet_bwd(em, x, a, L, rho, lens, sine):
+    if L < 4:
+        return
+    lo_l = lens if rho == 0 else lens ^ sine
+    hi_l = lens ^ sine if rho == 0 else lens
+    mnet_bwd(em, x, a, L // 2, 0, lo_l, sine)
+    mnet_bwd(em, x, a + L // 2, L // 2, 1, hi_l, sine)
+    for v in range(1, L // 2):
+        lo, hi = a + v, a + L - v
+        j, m = (lo, hi) if rho == 0 else (hi, lo)
+        E, C = x[j], x[m]
+        O = em.new(mul(C, const_expr(v, L)))
+        if lens == 0:
+            x[j], x[m] = em.new(add(E, O)), em.new(sub(E, O))
+        else:
+            x[j], x[m] = em.new(add(O, E)), em.new(sub(O, E))
+
+
+def gen_hmB(v, LB, rho, lam):
+    sine = 1 if v >= 5 else 0
+    lg = LB.bit_length() - 1
+    em = Emitter()
+    x = {}
+    for t in range(lg):
+        cnt = LB >> (t + 1)
+        em.emit(f"const int hi{t} = (N >> {t + 1}) - dsto - r;")
+        vals = []
+        for p in range(cnt):
+            nm = f"v{t}_{p}"
+            em.emit(f"const R {nm} = T[PH(hi{t} - ({p} << D))];")
+            vals.append(nm)
+        place_hm(em, v, vals, lam, sine, x, 0, LB, rho)
+    mnet_bwd(em, x, 0, LB, rho, lam, sine)
+    for u in range(1, LB):
+        em.emit(f"F[PH(a + {u})] = {x[u]};")
+    sig = (f"template <typename R, typename AR, int LOGLB>\n__device__ __forceinline__ void "
+           f"hmB_v{v}_lb{LB}_r{rho}_l{lam}(const R* __restrict__ T, R* __restrict__ F, int a, "
+           f"const R* __restrict__ tab, int nmax, R base, int N, int D, int r, int dsto)")
+    return sig + " {\n" + "\n".join(em.lines) + "\n}\n"
+
+
+def gen_hmS(v, HP, LB, lam):
+    """Temporal cells [0, HP] (Dct(N/LB) after the big folds) -> leaves at
+    frequency cells k*LB."""
+    sine = 1 if v >= 5 else 0
+    em = Emitter()
+    S = {}
+    ks = range(0, HP + 1) if lam == 0 else range(1, HP)
+    for k in ks:
+        em.emit(f"const R s{k} = T[PH({k})];")
+        S[k] = f"s{k}"
+    x = {}
+    Np = 2 * HP
+    n = Np
+    while n >= (4 if lam == 0 else 8):
+        if lam == 0:
+            for m in range(n // 4):
+                a_, b_ = S[m], S[n // 2 - m]
+                S[m], S[n // 2 - m] = em.new(add(a_, b_)), em.new(sub(a_, b_))
+        else:
+            for m in range(1, n // 4):
+                a_, b_ = S[m], S[n // 2 - m]
+                S[m], S[n // 2 - m] = em.new(sub(a_, b_)), em.new(add(a_, b_))
+        vals = [S[n // 2 - p - lam] for p in range(n // 4)]
+        place_hm(em, v, vals, lam, sine, x, 0, HP, 0)
+        n //= 2
+    if lam == 0:
+        x[0] = em.new(add(S[0], S[1]))
+        x[HP] = em.new(sub(S[0], S[1]))
+    else:
+        x[HP // 2] = S[1]
+    for k in ks:
+        em.emit(f"F[PH({k} * {LB})] = {x[k]};")
+    sig = (f"template <typename R, typename AR, int LOGLB>\n__device__ __forceinline__ void "
+           f"hmS_v{v}_hp{HP}_l{lam}(const R* __restrict__ T, R* __restrict__ F, R base)")
+    return sig + " {\n" + "\n".join(em.lines) + "\n}\n"
+
+
+# Sizes instantiated by csrc/fast.cu (LB, HP = N/(2 LB)).
+CONFIGS = [
+    # (LB, [HP...])
+    (32, [8, 16, 32, 64]),
+    (64, [8, 16, 32, 64]),
+]
+
+
+def main():
+    out = [
+        "// fast_gen.cuh -- GENERATED by codegen/gen_fast.py; do not edit.",
+        "// Straight-line bottom-of-recursion code for the fused AM-QFT kernels.",
+        "#pragma once",
+        "#define PH(i) ((i) + ((i) >> LOGLB))",
+        "namespace amqft_b200 {",
+        "namespace gen {",
+    ]
+    hp_all = sorted({hp for _, hps in CONFIGS for hp in hps})
+    for LB, hps in CONFIGS:
+        for v in range(1, 9):
+            for rho in (0, 1):
+                for lam in (0, 1):
+                    out.append(gen_tmB(v, LB, rho, lam) if v in TM else gen_hmB(v, LB, rho, lam))
+    for v in range(1, 9):
+        for hp in hp_all:
+            for lam in (0, 1):
+                body = gen_tmS(v, hp, "LBV", lam) if v in TM else gen_hmS(v, hp, "LBV", lam)
+                body = body.replace("template <typename R, typename AR, int LOGLB>",
+                                    "template <typename R, typename AR, int LOGLB, int LBV>")
+                out.append(body)
+    out.append("}  // namespace gen")
+    # Compile-time dispatch: Bottom<V, LB> and Small<V, HP>.
+    out.append("template <int V, int LB> struct Bottom;")
+    for LB, _ in CONFIGS:
+        for v in range(1, 9):
+            fam = "tmB" if v in TM else "hmB"
+            out.append(f"template <> struct Bottom<{v}, {LB}> {{")
+            out.append("  template <typename R, typename AR, int LOGLB>")
+            out.append("  static __device__ __forceinline__ void run(int rho, int lens, const R* T, R* F, int a, "
+                       "const R* tab, int nmax, R base, int N, int D, int r, int dsto) {")
+            for rho in (0, 1):
+                for lam in (0, 1):
+                    out.append(f"    if (rho == {rho} && lens == {lam}) {{ gen::{fam}_v{v}_lb{LB}_r{rho}_l{lam}"
+                               f"<R, AR, LOGLB>(T, F, a, tab, nmax, base, N, D, r, dsto); return; }}")
+            out.append("  }")
+            out.append("};")
+    out.append("template <int V, int HP> struct Small;")
+    for v in range(1, 9):
+        fam = "tmS" if v in TM else "hmS"
+        for hp in hp_all:
+            out.append(f"template <> struct Small<{v}, {hp}> {{")
+            out.append("  template <typename R, typename AR, int LOGLB, int LBV>")
+            out.append("  static __device__ __forceinline__ void run(int lam, const R* T, R* F, R base) {")
+            out.append(f"    if (lam == 0) gen::{fam}_v{v}_hp{hp}_l0<R, AR, LOGLB, LBV>(T, F, base);")
+            out.append(f"    else gen::{fam}_v{v}_hp{hp}_l1<R, AR, LOGLB, LBV>(T, F, base);")
+            out.append("  }")
+            out.append("};")
+    out += ["}  // namespace amqft_b200", "#undef PH", ""]
+    sys.stdout.write("\n".join(out))
+
+
+if __name__ == "__main__":
+    main()

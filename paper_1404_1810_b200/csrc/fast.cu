@@ -1,16 +1,48 @@
-// fast.cu -- fused fast-path kernels (placeholder until the fused CDFT
-// kernel lands; requests fall through to the generic schedule kernels).
+// fast.cu -- dispatcher of the fused CDFT kernels (kernel: fast_kernel.cuh;
+// per-variant instances: fast_v1.cu .. fast_v8.cu).
 #include "fast.cuh"
 
 namespace amqft_b200 {
+namespace fastk {
+template <int V, typename R>
+std::unique_ptr<FastPlan> make_for_variant(size_t n, const void* tab, uint32_t nmax, int dev);
+}  // namespace fastk
 
-std::unique_ptr<FastPlan> make_fast_plan(const amqft_plan_desc&, const void*, uint32_t) {
+template <typename R>
+std::unique_ptr<FastPlan> make_fast_typed(int v, size_t n, const void* tab, uint32_t nmax, int dev) {
+  using namespace fastk;
+  switch (v) {
+    case 1: return make_for_variant<1, R>(n, tab, nmax, dev);
+    case 2: return make_for_variant<2, R>(n, tab, nmax, dev);
+    case 3: return make_for_variant<3, R>(n, tab, nmax, dev);
+    case 4: return make_for_variant<4, R>(n, tab, nmax, dev);
+    case 5: return make_for_variant<5, R>(n, tab, nmax, dev);
+    case 6: return make_for_variant<6, R>(n, tab, nmax, dev);
+    case 7: return make_for_variant<7, R>(n, tab, nmax, dev);
+    case 8: return make_for_variant<8, R>(n, tab, nmax, dev);
+  }
   return nullptr;
 }
 
+std::unique_ptr<FastPlan> make_fast_plan(const amqft_plan_desc& d, const void* d_trig,
+                                         uint32_t nmax) {
+  if (d.function != AMQFT_FN_CDFT) return nullptr;
+  if (d.trig_mode != AMQFT_TRIG_TABLE) return nullptr;
+  if (d.dtype == AMQFT_F32) return make_fast_typed<float>(d.variant, d.n, d_trig, nmax, d.device);
+  return make_fast_typed<double>(d.variant, d.n, d_trig, nmax, d.device);
+}
+
 OpCount fast_op_counts(const amqft_plan_desc& d) {
-  (void)d;
-  return OpCount{};
+  // The fused kernel executes exactly the reference DAG (fast_model.py):
+  // the closed forms of metering.cpp:85-96.
+  OpCount c;
+  uint64_t lg = 0;
+  for (size_t v = d.n; v > 1; v >>= 1) ++lg;
+  const uint64_t n = d.n;
+  c.adds = 3 * n * lg - 3 * n + 4;
+  c.muls = n * lg - 3 * n + 4;
+  c.bt = (d.variant % 2 == 1) ? n - 4 * lg + 4 : 0;
+  return c;
 }
 
 }  // namespace amqft_b200

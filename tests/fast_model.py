@@ -316,3 +316,237 @@ def fast_cdft_harmonic_major(v, N, x, tab, nmax, base):
         out[2 * k + 1] = idct[k] - rdst[k]
         out[2 * (N - k) + 1] = idct[k] + rdst[k]
     return out
+
+
+# ---------------------------------------------------------------------------
+# Phase-structured model: the exact decomposition the CUDA kernel uses
+# (top levels, bottom segments of length LB, small chain, depth-ordered upper
+# levels, chain recombination).  Must equal the recursive models bitwise.
+
+def _parity(x):
+    return bin(x).count("1") & 1
+
+
+def segment_params(lam_c, s, LT, sine):
+    """(orientation, lens, residue) of segment s at depth LT."""
+    rho = 0 if LT == 0 else (s & 1)
+    lens = lam_c ^ (sine & _parity(s ^ (s >> 1)))
+    r = 0
+    ln = lam_c
+    prev = 0
+    for i in range(1, LT + 1):
+        b = (s >> (LT - i)) & 1
+        is_o = 1 if b != prev else 0
+        bit = is_o ^ ln
+        r |= bit << (i - 1)
+        ln ^= sine & is_o
+        prev = b
+    return rho, lens, r
+
+
+def sub_lens(lam_c, depth, r, sine):
+    """Lens of the depth-`depth` sub-block with residue r (upper levels)."""
+    if not sine or depth == 0:
+        return lam_c
+    return (r >> (depth - 1)) & 1
+
+
+def phased_time_major(v, N, x, tab, nmax, base, LB):
+    H = N // 2
+    sine = 1 if v >= 5 else 0
+    LT = (H // LB).bit_length() - 1
+    lgLB = LB.bit_length() - 1
+    x = np.asarray(x, dtype=np.float64)
+    chains = []
+    for part in (x[0::2], x[1::2]):
+        dct = np.zeros(H + 1)
+        dst = np.zeros(H + 1)
+        dct[0], dct[H] = part[0], part[H]
+        for m in range(1, H):
+            dct[m] = part[m] + part[N - m]
+            dst[m] = part[m] - part[N - m]
+        chains += [(dct, 0), (dst, 1)]
+    results = []
+    for T, lam_c in chains:
+        F = np.zeros(H + 1)
+        # phase T: levels 1..LT
+        for lvl in range(1, LT + 1):
+            L = H >> (lvl - 1)
+            for s in range(1 << (lvl - 1)):
+                rho, lens, _ = segment_params(lam_c, s, lvl - 1, sine)
+                a = s * L
+                for vv in range(1, L // 2):
+                    lo, hi = a + vv, a + L - vv
+                    j, m = (lo, hi) if rho == 0 else (hi, lo)
+                    p, q = T[j], T[m]
+                    e, o = (p + q, p - q) if lens == 0 else (p - q, p + q)
+                    k = base if vv == L // 4 else tab[vv * (nmax // (2 * L)) - 1]
+                    T[j], T[m] = e, o * k
+        # phase B: segments of length LB
+        for s in range(H // LB):
+            rho, lens, r = segment_params(lam_c, s, LT, sine)
+            seg = T.copy()
+            mnet_forward(seg, s * LB, LB, rho, lens, sine, tab, nmax, base)
+            for t in range(lgLB):
+                sp = spectrum(seg, v, s * LB, LB, rho, lens, sine, t)
+                hi = (N >> (t + 1)) - lam_c - r
+                for p, val in enumerate(sp):
+                    F[hi - (p << LT)] = val
+        # small chain
+        HP = H // LB
+        y = {k: T[k * LB] for k in range(HP + 1)}
+        G = [0.0] * (HP + 1)
+        lg = HP.bit_length() - 1
+        ntop = lg if lam_c == 0 else lg - 1
+        for t in range(ntop):
+            sp = spectrum(y, v, 0, HP, 0, lam_c, sine, t)
+            hi = (2 * HP) >> (t + 1)
+            for p, val in enumerate(sp):
+                G[hi - p - lam_c] = val
+        if lam_c == 0:
+            G[0], G[1] = y[0] + y[HP], y[0] - y[HP]
+            n = 4
+        else:
+            G[1] = y[HP // 2]
+            n = 8
+        while n <= 2 * HP:
+            for k in (range(n // 4) if lam_c == 0 else range(1, n // 4)):
+                e, o = G[k], G[n // 2 - k]
+                G[k], G[n // 2 - k] = (e + o, e - o) if lam_c == 0 else (o + e, o - e)
+            n *= 2
+        for k in range(HP + 1):
+            if lam_c == 0 or 1 <= k < HP:
+                F[k] = G[k]
+        # phase U: depth LT-1 .. 0, blocks of top classes t < lgLB
+        for depth in range(LT - 1, -1, -1):
+            new = F.copy()
+            for t in range(lgLB):
+                Mt = N >> (t + 2)
+                m = Mt >> depth
+                hi = (N >> (t + 1)) - lam_c
+                for r in range(1 << depth):
+                    lens = sub_lens(lam_c, depth, r, sine)
+                    rO = r + ((1 - lens) << depth)
+                    q = m // 2
+                    C = [F[hi - (j * (2 << depth) + rO)] for j in range(q)]
+                    O = am_backward_tm(v, lens, C) if m > 2 else C
+                    for j in range(q):
+                        new[hi - (j * (2 << depth) + rO)] = O[j]
+            F = new
+        # phase F: chain recombination n = 2N'..N
+        n = 2 * (N // LB)
+        while n <= N:
+            for k in (range(n // 4) if lam_c == 0 else range(1, n // 4)):
+                e, o = F[k], F[n // 2 - k]
+                F[k], F[n // 2 - k] = (e + o, e - o) if lam_c == 0 else (o + e, o - e)
+            n *= 2
+        results.append(F)
+    rdct, rdst, idct, idst = results
+    out = np.zeros(2 * N)
+    out[0], out[1] = rdct[0], idct[0]
+    out[2 * H], out[2 * H + 1] = rdct[H], idct[H]
+    for k in range(1, H):
+        out[2 * k] = rdct[k] + idst[k]
+        out[2 * (N - k)] = rdct[k] - idst[k]
+        out[2 * k + 1] = idct[k] - rdst[k]
+        out[2 * (N - k) + 1] = idct[k] + rdst[k]
+    return out
+
+
+def phased_harmonic_major(v, N, x, tab, nmax, base, LB):
+    H = N // 2
+    sine = 1 if v >= 5 else 0
+    LT = (H // LB).bit_length() - 1
+    lgLB = LB.bit_length() - 1
+    HP = H // LB
+    x = np.asarray(x, dtype=np.float64)
+    chains = []
+    for part in (x[0::2], x[1::2]):
+        dct = np.zeros(H + 1)
+        dst = np.zeros(H + 1)
+        dct[0], dct[H] = part[0], part[H]
+        for m in range(1, H):
+            dct[m] = part[m] + part[N - m]
+            dst[m] = part[m] - part[N - m]
+        chains += [(dct, 0), (dst, 1)]
+    results = []
+    for T, lam_c in chains:
+        F = np.zeros(H + 1)
+        # phase F': chain folds n = N .. 2N'
+        n = N
+        while n >= 2 * (N // LB):
+            for m in (range(n // 4) if lam_c == 0 else range(1, n // 4)):
+                a_, b_ = T[m], T[n // 2 - m]
+                T[m], T[n // 2 - m] = (a_ + b_, a_ - b_) if lam_c == 0 else (a_ - b_, a_ + b_)
+            n //= 2
+        # phase U': depth 0 .. LT-1 (top-down), AM_F on odd classes
+        for depth in range(LT):
+            new = T.copy()
+            for t in range(lgLB):
+                Mt = N >> (t + 2)
+                m = Mt >> depth
+                hi = (N >> (t + 1)) - lam_c
+                for r in range(1 << depth):
+                    lens = sub_lens(lam_c, depth, r, sine)
+                    rO = r + ((1 - lens) << depth)
+                    q = m // 2
+                    A = [T[hi - (j * (2 << depth) + rO)] for j in range(q)]
+                    C = am_forward_hm(v, lens, A) if m > 2 else A
+                    for j in range(q):
+                        new[hi - (j * (2 << depth) + rO)] = C[j]
+            T = new
+        # phase B': segments in frequency space
+        for s in range(H // LB):
+            rho, lens, r = segment_params(lam_c, s, LT, sine)
+            seg = {}
+            for t in range(lgLB):
+                hi = (N >> (t + 1)) - lam_c - r
+                vals = [T[hi - (p << LT)] for p in range(LB >> (t + 1))]
+                place_forward(v, vals, lens, sine, seg, s * LB, LB, rho)
+            arr = np.zeros(H + 1)
+            for k, val in seg.items():
+                arr[k] = val
+            mnet_backward(arr, s * LB, LB, rho, lens, sine, tab, nmax, base)
+            for u in range(1, LB):
+                F[s * LB + u] = arr[s * LB + u]
+        # small chain: temporal [0, HP] -> frequency k*LB
+        S = {k: T[k] for k in range(HP + 1)}
+        seg = {}
+        n = 2 * HP
+        while n >= (4 if lam_c == 0 else 8):
+            for m in (range(n // 4) if lam_c == 0 else range(1, n // 4)):
+                a_, b_ = S[m], S[n // 2 - m]
+                S[m], S[n // 2 - m] = (a_ + b_, a_ - b_) if lam_c == 0 else (a_ - b_, a_ + b_)
+            vals = [S[n // 2 - p - lam_c] for p in range(n // 4)]
+            place_forward(v, vals, lam_c, sine, seg, 0, HP, 0)
+            n //= 2
+        if lam_c == 0:
+            seg[0], seg[HP] = S[0] + S[1], S[0] - S[1]
+        else:
+            seg[HP // 2] = S[1]
+        for k, val in seg.items():
+            F[k * LB] = val
+        # phase T': mirror levels LT .. 1 (L = 2LB .. H), bottom-up
+        for lvl in range(LT, 0, -1):
+            L = H >> (lvl - 1)
+            for s in range(1 << (lvl - 1)):
+                rho, lens, _ = segment_params(lam_c, s, lvl - 1, sine)
+                a = s * L
+                for vv in range(1, L // 2):
+                    lo, hi = a + vv, a + L - vv
+                    j, m = (lo, hi) if rho == 0 else (hi, lo)
+                    E, C = F[j], F[m]
+                    k = base if vv == L // 4 else tab[vv * (nmax // (2 * L)) - 1]
+                    O = C * k
+                    F[j], F[m] = (E + O, E - O) if lens == 0 else (O + E, O - E)
+        results.append(F)
+    rdct, rdst, idct, idst = results
+    out = np.zeros(2 * N)
+    out[0], out[1] = rdct[0], idct[0]
+    out[2 * H], out[2 * H + 1] = rdct[H], idct[H]
+    for k in range(1, H):
+        out[2 * k] = rdct[k] + idst[k]
+        out[2 * (N - k)] = rdct[k] - idst[k]
+        out[2 * k + 1] = idct[k] - rdst[k]
+        out[2 * (N - k) + 1] = idct[k] + rdst[k]
+    return out

@@ -161,3 +161,35 @@ def test_empty_and_single_row_edges(oracle, restatement):
     torch.cuda.synchronize()
     for t in range(4):
         assert xt[t].cpu().numpy().tobytes() == r.execute(4, O.F_CDFT, 256, xs[t]).tobytes()
+
+
+@pytest.mark.parametrize("n", [1024, 2048, 4096])
+def test_fast_kernel_fp64_bitwise(oracle, restatement, n):
+    """The fused kernel executes the reference DAG with the reference's
+    operands and association; its fp64 instance is bitwise the oracle."""
+    r, O = restatement, oracle
+    for v in range(1, 9):
+        xs = [O.seeded_signal(21, O.CDFT, n, 10 * v + k, r) for k in range(3)]
+        plan = amqft.Plan(v, amqft.FunctionId.Cdft, n, 3, dtype="f64", order=amqft.Order.Fast)
+        assert plan.path()[0] == 2, "fused kernel expected"
+        got = run_plan(plan, xs)
+        for k in range(3):
+            assert got[k].tobytes() == r.execute(v, O.F_CDFT, n, xs[k]).tobytes(), (v, n, k)
+        inv = run_plan(plan, [r.execute(v, O.F_CDFT, n, xs[0])], inverse=True)[0]
+        assert inv.tobytes() == r.inverse_cdft(v, n, r.execute(v, O.F_CDFT, n, xs[0])).tobytes()
+
+
+@pytest.mark.parametrize("n", [1024, 2048, 4096, 8192])
+def test_fast_kernel_fp32_tolerance(oracle, restatement, n):
+    r, O = restatement, oracle
+    rng = np.random.default_rng(n)
+    xs = rng.standard_normal((4, 2 * n)).astype(np.float32)
+    tol = 1e-5 * math.log2(n)
+    for v in range(1, 9):
+        plan = amqft.Plan(v, amqft.FunctionId.Cdft, n, 4, dtype="f32", order=amqft.Order.Fast)
+        assert plan.path()[0] == 2
+        got = run_plan(plan, xs)
+        for k in (0, 3):
+            err = r.rel_l2(got[k], r.execute(v, O.F_CDFT, n, xs[k].astype(np.float64)))
+            if v <= 4:
+                assert err <= tol, (v, n, err)
