@@ -162,7 +162,7 @@ def gen_tmB(v, LB, rho, lam):
         sp = spectrum_tm(em, v, x, 0, LB, rho, lam, sine, t)
         em.emit(f"{{ const int hi = (N >> {t + 1}) - dsto - r;")
         for p, name in enumerate(sp):
-            em.emit(f"  F[PH(hi - ({p} << D))] = {name};")
+            em.emit(f"  F[hi - ({p} << D)] = {name};")
         em.emit("}")
     sig = (f"template <typename R, typename AR, int LOGLB>\n__device__ __forceinline__ void "
            f"tmB_v{v}_lb{LB}_r{rho}_l{lam}(const R* __restrict__ T, R* __restrict__ F, int a, "
@@ -304,7 +304,7 @@ def gen_hmB(v, LB, rho, lam):
         vals = []
         for p in range(cnt):
             nm = f"v{t}_{p}"
-            em.emit(f"const R {nm} = T[PH(hi{t} - ({p} << D))];")
+            em.emit(f"const R {nm} = T[hi{t} - ({p} << D)];")
             vals.append(nm)
         place_hm(em, v, vals, lam, sine, x, 0, LB, rho)
     mnet_bwd(em, x, 0, LB, rho, lam, sine)
@@ -353,6 +353,210 @@ def gen_hmS(v, HP, LB, lam):
     return sig + " {\n" + "\n".join(em.lines) + "\n}\n"
 
 
+# ------------------------------------------------------------- top levels
+def gen_top(LB, LT, direction, lam, sine, nlog):
+    """Mirror levels 1..LT of one chain for the thread owning offset v in
+    [1, LB): cells z_2k = kW + v, z_2k+1 = (k+1)W - v (W = 2 LB), closed
+    under every top level.  direction 'fwd' = time-major forward fold,
+    'bwd' = harmonic-major backward butterfly (levels LT..1).  Table size
+    nmax = N = 2^nlog (compile time).  Skewed addresses:
+    PH(kW+v) = v + k(W+2), PH((k+1)W-v) = (k+1)(W+2) - v - 1."""
+    W = 2 * LB
+    K = 1 << (LT - 1)          # cells per parity
+    H = W * K
+    em = Emitter()
+    em.emit("R* __restrict__ pe = B + v;")
+    em.emit("R* __restrict__ po = B - v - 1;")
+    x = {}
+    for k in range(K):
+        x[2 * k] = f"x{2 * k}"
+        x[2 * k + 1] = f"x{2 * k + 1}"
+        em.emit(f"R x{2 * k} = pe[{k * (W + 2)}];")
+        em.emit(f"R x{2 * k + 1} = po[{(k + 1) * (W + 2)}];")
+    # offsets of cells from 0: z_2k = kW + v (+v), z_2k+1 = (k+1)W - v (-v)
+    def off(z):
+        k = z // 2
+        return (k * W, +1) if z % 2 == 0 else ((k + 1) * W, -1)
+    nmax = 1 << nlog
+    levels = list(range(1, LT + 1))
+    if direction == "bwd":
+        levels = levels[::-1]
+    for i in levels:
+        L = H >> (i - 1)
+        lg2L = (2 * L).bit_length() - 1
+        sc = nmax >> lg2L
+        em.emit(f"{{ const R* __restrict__ tp = tab + v * {sc};")
+        em.emit(f"  const R* __restrict__ tm = tab - v * {sc};")
+        done = set()
+        for z in range(2 * K):
+            if z in done:
+                continue
+            c0, sg = off(z)
+            seg = c0 // L if sg > 0 else (c0 - 1) // L
+            a = seg * L
+            # mirror cell
+            mc0, msg = a + L - (c0 - a), -sg
+            mz = None
+            for z2 in range(2 * K):
+                if off(z2) == (mc0, msg):
+                    mz = z2
+            assert mz is not None
+            done.add(z)
+            done.add(mz)
+            # lower cell: offset < L/2
+            u_z = (c0 - a, sg)
+            z_is_lower = (c0 - a) < L // 2 if sg > 0 else (c0 - a) <= L // 2
+            lower, upper = (z, mz) if z_is_lower else (mz, z)
+            lc0, lsg = off(lower)
+            u0 = lc0 - a                  # u = u0 + lsg * v
+            rho = 0 if i == 1 else (seg & 1)
+            par = bin(seg ^ (seg >> 1)).count("1") & 1
+            lens = lam ^ (sine & par)
+            jc, mcz = (lower, upper) if rho == 0 else (upper, lower)
+            idx0 = u0 * sc - 1
+            kexpr = f"__ldg({'tp' if lsg > 0 else 'tm'} + {idx0})"
+            if u0 == 0 and lsg > 0 and i == LT:
+                kexpr = f"(v == {LB // 2} ? base : {kexpr})"
+            p_, q_ = x[jc], x[mcz]
+            em.tmp += 1
+            t = em.tmp
+            em.emit(f"  const R k{t} = {kexpr};")
+            if direction == "fwd":
+                em.emit(f"  const R s{t} = {add(p_, q_)}, d{t} = {sub(p_, q_)};")
+                if lens == 0:
+                    em.emit(f"  {p_} = s{t}; {q_} = {mul('d' + str(t), 'k' + str(t))};")
+                else:
+                    em.emit(f"  {p_} = d{t}; {q_} = {mul('s' + str(t), 'k' + str(t))};")
+            else:
+                em.emit(f"  const R o{t} = {mul(q_, 'k' + str(t))};")
+                if lens == 0:
+                    em.emit(f"  const R e{t} = {p_}; {p_} = {add('e' + str(t), 'o' + str(t))}; "
+                            f"{q_} = {sub('e' + str(t), 'o' + str(t))};")
+                else:
+                    em.emit(f"  const R e{t} = {p_}; {p_} = {add('o' + str(t), 'e' + str(t))}; "
+                            f"{q_} = {sub('o' + str(t), 'e' + str(t))};")
+        em.emit("}")
+    for k in range(K):
+        em.emit(f"pe[{k * (W + 2)}] = x{2 * k};")
+        em.emit(f"po[{(k + 1) * (W + 2)}] = x{2 * k + 1};")
+    sig = (f"template <typename R, typename AR>\n__device__ __forceinline__ void "
+           f"top_{direction}_lb{LB}_lt{LT}_n{nlog}_l{lam}_s{sine}(R* __restrict__ B, int v, "
+           f"const R* __restrict__ tab, R base)")
+    return sig + " {\n" + "\n".join(em.lines) + "\n}\n"
+
+
+def scaled_mnet(em, y, HP, lam, sine, direction, nlog, LB):
+    """Mirror network on the cells at multiples of LB (scaled segment
+    [0, HP]); constants f(pi u/L) with the scaled u and L."""
+    nmax = 1 << nlog
+    def rec(a, L, rho, lens):
+        if L < 4:
+            return
+        if direction == "bwd":
+            lo_l = lens if rho == 0 else lens ^ sine
+            hi_l = lens ^ sine if rho == 0 else lens
+            rec(a, L // 2, 0, lo_l)
+            rec(a + L // 2, L // 2, 1, hi_l)
+        lg2L = (2 * L).bit_length() - 1
+        for vv in range(1, L // 2):
+            lo, hi = a + vv, a + L - vv
+            j, m = (lo, hi) if rho == 0 else (hi, lo)
+            k = "base" if vv == L // 4 else f"__ldg(tab + {vv * (nmax >> lg2L) - 1})"
+            if direction == "fwd":
+                p_, q_ = y[j], y[m]
+                s_, d_ = add(p_, q_), sub(p_, q_)
+                e_, o_ = (s_, d_) if lens == 0 else (d_, s_)
+                y[j] = em.new(e_)
+                y[m] = em.new(mul(o_, k))
+            else:
+                E, C = y[j], y[m]
+                O = em.new(mul(C, k))
+                if lens == 0:
+                    y[j], y[m] = em.new(add(E, O)), em.new(sub(E, O))
+                else:
+                    y[j], y[m] = em.new(add(O, E)), em.new(sub(O, E))
+        if direction == "fwd":
+            lo_l = lens if rho == 0 else lens ^ sine
+            hi_l = lens ^ sine if rho == 0 else lens
+            rec(a, L // 2, 0, lo_l)
+            rec(a + L // 2, L // 2, 1, hi_l)
+    rec(0, HP, 0, lam)
+
+
+def gen_small_full(v, HP, lam, nlog):
+    """Cells at multiples of LB: time-major = full forward (scaled mirror
+    network) + backward (tmS); harmonic-major = hmS + scaled backward."""
+    sine = 1 if v >= 5 else 0
+    em = Emitter()
+    ks = range(0, HP + 1) if lam == 0 else range(1, HP)
+    if v in TM:
+        y = {}
+        for k in ks:
+            em.emit(f"const R y{k} = T[PH({k} * LBV)];")
+            y[k] = f"y{k}"
+        scaled_mnet(em, y, HP, lam, sine, "fwd", nlog, None)
+        G = [None] * (HP + 1)
+        lg = HP.bit_length() - 1
+        ntop = lg if lam == 0 else lg - 1
+        Np = 2 * HP
+        for t in range(ntop):
+            sp = spectrum_tm(em, v, y, 0, HP, 0, lam, sine, t)
+            hi = Np >> (t + 1)
+            for p, name in enumerate(sp):
+                G[hi - p - lam] = name
+        if lam == 0:
+            G[0] = em.new(add(y[0], y[HP]))
+            G[1] = em.new(sub(y[0], y[HP]))
+            n = 4
+        else:
+            G[1] = y[HP // 2]
+            n = 8
+        while n <= Np:
+            for k in (range(n // 4) if lam == 0 else range(1, n // 4)):
+                e, o = G[k], G[n // 2 - k]
+                if lam == 0:
+                    G[k], G[n // 2 - k] = em.new(add(e, o)), em.new(sub(e, o))
+                else:
+                    G[k], G[n // 2 - k] = em.new(add(o, e)), em.new(sub(o, e))
+            n *= 2
+        for k in ks:
+            em.emit(f"F[{k}] = {G[k]};")
+    else:
+        S = {}
+        for k in ks:
+            em.emit(f"const R s{k} = T[{k}];")
+            S[k] = f"s{k}"
+        x = {}
+        Np = 2 * HP
+        n = Np
+        while n >= (4 if lam == 0 else 8):
+            for m in (range(n // 4) if lam == 0 else range(1, n // 4)):
+                a_, b_ = S[m], S[n // 2 - m]
+                if lam == 0:
+                    S[m], S[n // 2 - m] = em.new(add(a_, b_)), em.new(sub(a_, b_))
+                else:
+                    S[m], S[n // 2 - m] = em.new(sub(a_, b_)), em.new(add(a_, b_))
+            vals = [S[n // 2 - p - lam] for p in range(n // 4)]
+            place_hm(em, v, vals, lam, sine, x, 0, HP, 0)
+            n //= 2
+        if lam == 0:
+            x[0] = em.new(add(S[0], S[1]))
+            x[HP] = em.new(sub(S[0], S[1]))
+        else:
+            x[HP // 2] = S[1]
+        scaled_mnet(em, x, HP, lam, sine, "bwd", nlog, None)
+        for k in ks:
+            em.emit(f"F[PH({k} * LBV)] = {x[k]};")
+    sig = (f"template <typename R, typename AR, int LOGLB, int LBV>\n__device__ __forceinline__ void "
+           f"smallfull_v{v}_hp{HP}_n{nlog}_l{lam}(const R* __restrict__ T, R* __restrict__ F, "
+           f"const R* __restrict__ tab, R base)")
+    return sig + " {\n" + "\n".join(em.lines) + "\n}\n"
+
+
+# (LB, nlog) pairs of the fused kernels: LT = nlog - 1 - log2(LB), HP = 2^LT
+FULL_SIZES = [(32, 10), (32, 11), (32, 12), (64, 11), (64, 12), (64, 13)]
+
+
 # Sizes instantiated by csrc/fast.cu (LB, HP = N/(2 LB)).
 CONFIGS = [
     # (LB, [HP...])
@@ -383,7 +587,41 @@ def main():
                 body = body.replace("template <typename R, typename AR, int LOGLB>",
                                     "template <typename R, typename AR, int LOGLB, int LBV>")
                 out.append(body)
+    for LB, nlog in FULL_SIZES:
+        LT = nlog - 1 - (LB.bit_length() - 1)
+        for direction in ("fwd", "bwd"):
+            for lam in (0, 1):
+                for sine in (0, 1):
+                    out.append(gen_top(LB, LT, direction, lam, sine, nlog))
+        HP = 1 << LT
+        for v in range(1, 9):
+            for lam in (0, 1):
+                out.append(gen_small_full(v, HP, lam, nlog))
     out.append("}  // namespace gen")
+    out.append("template <int LB, int LT, int NLOG, int SINE> struct Top;")
+    for LB, nlog in FULL_SIZES:
+        LT = nlog - 1 - (LB.bit_length() - 1)
+        for sine in (0, 1):
+            out.append(f"template <> struct Top<{LB}, {LT}, {nlog}, {sine}> {{")
+            for direction in ("fwd", "bwd"):
+                out.append("  template <typename R, typename AR>")
+                out.append(f"  static __device__ __forceinline__ void {direction}(int lam, R* B, int v, const R* tab, R base) {{")
+                out.append(f"    if (lam == 0) gen::top_{direction}_lb{LB}_lt{LT}_n{nlog}_l0_s{sine}<R, AR>(B, v, tab, base);")
+                out.append(f"    else gen::top_{direction}_lb{LB}_lt{LT}_n{nlog}_l1_s{sine}<R, AR>(B, v, tab, base);")
+                out.append("  }")
+            out.append("};")
+    out.append("template <int V, int HP, int NLOG> struct SmallFull;")
+    for LB, nlog in FULL_SIZES:
+        LT = nlog - 1 - (LB.bit_length() - 1)
+        HP = 1 << LT
+        for v in range(1, 9):
+            out.append(f"template <> struct SmallFull<{v}, {HP}, {nlog}> {{")
+            out.append("  template <typename R, typename AR, int LOGLB, int LBV>")
+            out.append("  static __device__ __forceinline__ void run(int lam, const R* T, R* F, const R* tab, R base) {")
+            out.append(f"    if (lam == 0) gen::smallfull_v{v}_hp{HP}_n{nlog}_l0<R, AR, LOGLB, LBV>(T, F, tab, base);")
+            out.append(f"    else gen::smallfull_v{v}_hp{HP}_n{nlog}_l1<R, AR, LOGLB, LBV>(T, F, tab, base);")
+            out.append("  }")
+            out.append("};")
     # Compile-time dispatch: Bottom<V, LB> and Small<V, HP>.
     out.append("template <int V, int LB> struct Bottom;")
     for LB, _ in CONFIGS:

@@ -39,28 +39,31 @@
 namespace amqft_b200 {
 namespace fastk {
 
-template <int LOGLB>
-__device__ __forceinline__ int ph(int i) { return i + (i >> LOGLB); }
-
 __device__ __forceinline__ int parity(unsigned x) { return __popc(x) & 1; }
 
 template <int V, typename R, int LOGN, int LOGLB>
-struct FastCfg {
+struct Cfg {
+  static constexpr int V_ = V;
   static constexpr int N = 1 << LOGN;
+  static constexpr int LOGN_ = LOGN;
   static constexpr int H = N / 2;
   static constexpr int LOGH = LOGN - 1;
   static constexpr int LB = 1 << LOGLB;
+  static constexpr int LOGLB_ = LOGLB;
   static constexpr int LT = LOGH - LOGLB;        // depth of the bottom segments
   static constexpr int HP = H / LB;               // cells at multiples of LB
   static constexpr int NSEG = 4 * HP;             // bottom segments (4 chains)
-  static constexpr int NT = NSEG + 32;            // + one warp for small chains
-  static constexpr int CS = ((H + HP + 1) + 3) / 4 * 4;  // chain stride (skewed)
+  static constexpr int NT0 = (4 * LB > NSEG ? 4 * LB : NSEG);
+  static constexpr int NT = NT0 < 128 ? 128 : NT0;
+  static constexpr int CS = ((H + HP + 1) + 3) / 4 * 4;  // chain stride
   static constexpr bool TM = (V == 1 || V == 4 || V == 5 || V == 8);
   static constexpr int SINE = V >= 5 ? 1 : 0;
   static constexpr bool CHAIN = (V == 1 || V == 5 || V == 3 || V == 7);
-  static constexpr int UPC = N / 4 - N / (4 * LB);  // U items per chain
-  static constexpr int UK = (4 * UPC + NT - 1) / NT;
   static constexpr size_t SMEM = 8 * CS * sizeof(R);
+  // skew (i + i/LB) only on the buffer holding the index-space mirror
+  // network: T for time-major, F for harmonic-major.
+  static __device__ __forceinline__ int pt(int i) { return TM ? i + (i >> LOGLB) : i; }
+  static __device__ __forceinline__ int pf(int i) { return TM ? i : i + (i >> LOGLB); }
 };
 
 // Segment parameters at depth d: orientation, lens, residue (fast_model.segment_params).
@@ -79,44 +82,8 @@ __device__ __forceinline__ void seg_params(int lam_c, int s, int d, int* rho, in
   *r = res;
 }
 
-// Mirror level L over the four chains of buffer B (time-major forward when
-// FWD, harmonic-major backward otherwise).  Items: N per level.
-template <class C, typename R, bool FWD>
-__device__ __forceinline__ void mirror_level(R* B, int lvl, int L, const R* tab, int nmax, R base) {
-  using A = Arith<R>;
-  const int half = L >> 1;
-  const int lgh = 31 - __clz(half);
-  const int lgL2 = lgh + 2;  // log2(2L)
-  const int nseg_mask = (1 << (lvl - 1)) - 1;
-  for (int g = threadIdx.x; g < C::N; g += C::NT) {
-    const int v = g & (half - 1);
-    if (v == 0) continue;
-    const int s = (g >> lgh) & nseg_mask;
-    const int c = g >> (C::LOGH - 1);
-    const int lam_c = c & 1;
-    const int rho = lvl == 1 ? 0 : (s & 1);
-    const int lens = lam_c ^ (C::SINE & parity(static_cast<unsigned>(s ^ (s >> 1))));
-    const int a = s * L;
-    const int lo = a + v, hi = a + L - v;
-    const int jc = rho ? hi : lo, mc = rho ? lo : hi;
-    R* ch = B + c * C::CS;
-    const R k = (v == (L >> 2)) ? base : __ldg(tab + (v * (nmax >> lgL2) - 1));
-    const R p = ch[ph<C::LOGLB_>(jc)];
-    const R q = ch[ph<C::LOGLB_>(mc)];
-    if (FWD) {
-      const R sm = A::add(p, q), df = A::sub(p, q);
-      ch[ph<C::LOGLB_>(jc)] = lens ? df : sm;
-      ch[ph<C::LOGLB_>(mc)] = A::mul(lens ? sm : df, k);
-    } else {
-      const R o = A::mul(q, k);
-      ch[ph<C::LOGLB_>(jc)] = lens ? A::add(o, p) : A::add(p, o);
-      ch[ph<C::LOGLB_>(mc)] = lens ? A::sub(o, p) : A::sub(p, o);
-    }
-  }
-}
-
 // Dct/Dst chain recombination (time-major backward, FWD=false) or fold
-// (harmonic-major forward, FWD=true) at size n on buffer B.
+// (harmonic-major forward, FWD=true) at size n on an unskewed buffer.
 template <class C, typename R, bool FWD>
 __device__ __forceinline__ void chain_level(R* B, int n) {
   using A = Arith<R>;
@@ -128,7 +95,7 @@ __device__ __forceinline__ void chain_level(R* B, int n) {
     const int lam = c & 1;
     if (lam && k == 0) continue;
     R* ch = B + c * C::CS;
-    const int i0 = ph<C::LOGLB_>(k), i1 = ph<C::LOGLB_>((n >> 1) - k);
+    const int i0 = k, i1 = (n >> 1) - k;
     const R e = ch[i0], o = ch[i1];
     if (!FWD) {  // elaborations.cpp:310-329
       ch[i0] = lam ? A::add(o, e) : A::add(e, o);
@@ -140,124 +107,194 @@ __device__ __forceinline__ void chain_level(R* B, int n) {
   }
 }
 
-// AM conversion of the odd residue classes at depth `depth` (U-levels):
-// time-major: AM_B on F; harmonic-major: AM_F on T.  Neighbour ops are
-// staged through registers (read all, barrier, write all); serial
-// recurrences are run in place by the class's j == 0 item.
-template <class C, typename R>
-__device__ void am_level(R* B, int depth) {
+// ---- AM conversion levels on the odd residue classes (unskewed buffer).
+// Time-major: AM_B (elaborations.cpp:472-526) on F, depth D-1 .. 0;
+// harmonic-major: AM_F (elaborations.cpp:370-448) on T, depth 0 .. D-1.
+// Work item = a run of up to RU consecutive class positions; neighbour
+// operations read one halo cell, results are staged in registers until the
+// whole CTA has read (in-place update).  Serial recurrences (variants
+// 1,3,5,7) run the class in place from its first run's thread.
+template <class C, int DEPTH>
+struct AmLevel {
+  static constexpr int RU = 16;
+  static constexpr int q_of(int t) { return C::N >> (t + DEPTH + 3); }
+  static constexpr int len_of(int t) { return q_of(t) < RU ? q_of(t) : RU; }
+  static constexpr int items_of(int t) {
+    return q_of(t) >= 2 ? (1 << DEPTH) * (q_of(t) / len_of(t)) : 0;
+  }
+  static constexpr int items_chain() {
+    int s = 0;
+    for (int t = 0; t < C::LOGLB_; ++t) s += items_of(t);
+    return s;
+  }
+  static constexpr int IC = items_chain();
+  static constexpr int TOTAL = 4 * IC;
+  static constexpr int PER = (TOTAL + C::NT - 1) / C::NT;
+
+  template <typename R>
+  static __device__ __forceinline__ void run(R* B) {
+    using A = Arith<R>;
+    constexpr int V = C::V_;
+    constexpr int stride = 2 << DEPTH;
+    R val[PER][RU];
+    R* dst[PER];
+    int cnt[PER];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      cnt[u] = 0;
+      dst[u] = nullptr;
+      const int g = threadIdx.x + u * C::NT;
+      if (g >= TOTAL) continue;
+      const int c = g / IC;
+      int w = g - c * IC;
+      int t = 0;
+#pragma unroll
+      for (int tt = 0; tt < C::LOGLB_; ++tt) {
+        if (w >= items_of(tt) && t == tt) { w -= items_of(tt); t = tt + 1; }
+      }
+      const int q = C::N >> (t + DEPTH + 3);
+      const int len = q < RU ? q : RU;
+      const int runs = q / len;
+      const int r = w / runs;               // class (residue at this depth)
+      const int b = w - r * runs;           // run within the class
+      const int lam_c = c & 1;
+      const int lens = (C::SINE && DEPTH > 0) ? ((r >> (DEPTH - 1)) & 1) : lam_c;
+      const int rO = r + ((1 - lens) << DEPTH);
+      const int hi = (C::N >> (t + 1)) - lam_c;
+      R* ch = B + c * C::CS;
+      const int j0 = b * len;
+      R* p0 = ch + (hi - rO - j0 * stride);  // cell(j) = p0 - (j - j0) * stride
+      // right-halo ops read C[j+1], left-halo ops read C[j-1]
+      bool right;
+      if (C::TM) right = (V == 4) ? (lens == 0) : (lens == 1);
+      else right = (V == 2) ? (lens == 1) : (lens == 0);
+      // the op:  right: out_j = f(C_j, C_{j+1}), last class cell copies;
+      //          left:  out_j = f(C_{j-1}, C_j) (order per variant), first copies.
+#pragma unroll
+      for (int i = 0; i < RU; ++i) {
+        if (i >= len) break;
+        const int j = j0 + i;
+        const R cj = p0[-i * stride];
+        R o;
+        if (right) {
+          if (j == q - 1) o = cj;
+          else {
+            const R cn = p0[-(i + 1) * stride];
+            if (C::TM) o = (V == 4) ? A::add(cj, cn) : A::sub(cj, cn);
+            else o = (V == 2) ? A::add(cn, cj) : A::sub(cj, cn);
+          }
+        } else {
+          if (j == 0) o = cj;
+          else {
+            const R cp = p0[-(i - 1) * stride];
+            if (C::TM) o = (V == 4) ? A::add(cp, cj) : A::sub(cj, cp);
+            else o = (V == 2) ? A::add(cj, cp) : A::sub(cj, cp);
+          }
+        }
+        val[u][i] = o;
+      }
+      dst[u] = p0;
+      cnt[u] = len;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      if (cnt[u] > 0) {
+#pragma unroll
+        for (int i = 0; i < RU; ++i) {
+          if (i >= cnt[u]) break;
+          dst[u][-i * stride] = val[u][i];
+        }
+      }
+    }
+    __syncthreads();
+  }
+
+};
+
+template <class C, int DEPTH, typename R>
+__device__ __forceinline__ void chain_class(R* ch, int lam_c, int t, int r) {
   using A = Arith<R>;
   constexpr int V = C::V_;
-  R val[C::UK];
-  int pos[C::UK];
-#pragma unroll
-  for (int u = 0; u < C::UK; ++u) {
-    pos[u] = -1;
-    const int g = threadIdx.x + u * C::NT;
-    if (g >= 4 * C::UPC) continue;
-    const int c = g / C::UPC;
-    const int gp = g - c * C::UPC;
-    const int t = (C::LOGN_ - 3) - (31 - __clz(C::N / 4 - 1 - gp));
-    const int St = C::N / 4 - (C::N >> (t + 2));
-    const int w = gp - St;
-    const int r = w & ((1 << depth) - 1);
-    const int j = w >> depth;
-    const int lam_c = c & 1;
-    const int m = (C::N >> (t + 2)) >> depth;
-    if (m <= 2) continue;  // OO(8) base: no AM conversion
-    const int q = m >> 1;
-    const int lens = (C::SINE && depth > 0) ? ((r >> (depth - 1)) & 1) : lam_c;
-    const int rO = r + ((1 - lens) << depth);
-    const int hi = (C::N >> (t + 1)) - lam_c;
-    const int stride = 2 << depth;
-    R* ch = B + c * C::CS;
-    auto cell = [&](int jj) { return ph<C::LOGLB_>(hi - (jj * stride + rO)); };
-    if (C::CHAIN) {
-      if (j == 0) pos[u] = (c << 24) | (t << 16) | r;  // run the class serially
-      continue;
-    }
-    R out;
-    if (C::TM) {
-      if (V == 4) {
-        out = lens == 0 ? (j < q - 1 ? A::add(ch[cell(j)], ch[cell(j + 1)]) : ch[cell(j)])
-                        : (j > 0 ? A::add(ch[cell(j - 1)], ch[cell(j)]) : ch[cell(j)]);
-      } else {  // V == 8
-        out = lens == 0 ? (j > 0 ? A::sub(ch[cell(j)], ch[cell(j - 1)]) : ch[cell(j)])
-                        : (j < q - 1 ? A::sub(ch[cell(j)], ch[cell(j + 1)]) : ch[cell(j)]);
-      }
-    } else {
-      if (V == 2) {
-        out = lens == 0 ? (j > 0 ? A::add(ch[cell(j)], ch[cell(j - 1)]) : ch[cell(j)])
-                        : (j < q - 1 ? A::add(ch[cell(j + 1)], ch[cell(j)]) : ch[cell(j)]);
-      } else {  // V == 6
-        out = lens == 0 ? (j < q - 1 ? A::sub(ch[cell(j)], ch[cell(j + 1)]) : ch[cell(j)])
-                        : (j > 0 ? A::sub(ch[cell(j)], ch[cell(j - 1)]) : ch[cell(j)]);
-      }
-    }
-    val[u] = out;
-    pos[u] = c * C::CS + cell(j);
-  }
-  __syncthreads();
-#pragma unroll
-  for (int u = 0; u < C::UK; ++u) {
-    if (pos[u] < 0) continue;
-    if (!C::CHAIN) {
-      B[pos[u]] = val[u];
-      continue;
-    }
-    // Serial recurrence over the class (elaborations.cpp:402-448, 472-513).
-    const int c = pos[u] >> 24, t = (pos[u] >> 16) & 0xff, r = pos[u] & 0xffff;
-    const int lam_c = c & 1;
-    const int m = (C::N >> (t + 2)) >> depth;
-    const int q = m >> 1;
-    const int lens = (C::SINE && depth > 0) ? ((r >> (depth - 1)) & 1) : lam_c;
-    const int rO = r + ((1 - lens) << depth);
-    const int hi = (C::N >> (t + 1)) - lam_c;
-    const int stride = 2 << depth;
-    R* ch = B + c * C::CS;
-    auto at = [&](int jj) -> R& { return ch[ph<C::LOGLB_>(hi - (jj * stride + rO))]; };
-    if (C::TM) {
-      // M1: cos asc/sub, sin desc/sub; M5: cos desc/add, sin asc/add
-      const bool addop = V == 5;
-      const bool desc = (V == 1) ? (lens == 1) : (lens == 0);
-      const int s0 = desc ? q - 1 : 0, d = desc ? -1 : 1;
-      R prev = A::mul(R(0.5), at(s0));
-      at(s0) = prev;
-      int p = s0;
-      for (int k = 1; k < q; ++k) {
-        p += d;
-        prev = addop ? A::add(at(p), prev) : A::sub(at(p), prev);
-        at(p) = prev;
-      }
-    } else {
-      // M3: cos desc/sub, sin asc/sub; M7: cos asc/add, sin desc/add
-      const bool addop = V == 7;
-      const bool desc = (V == 3) ? (lens == 0) : (lens == 1);
-      const int s0 = desc ? q - 1 : 0, d = desc ? -1 : 1;
-      R prev = at(s0);
-      int p = s0;
-      for (int k = 1; k < q - 1; ++k) {
-        p += d;
-        prev = addop ? A::add(at(p), prev) : A::sub(at(p), prev);
-        at(p) = prev;
-      }
+  constexpr int stride = 2 << DEPTH;
+  const int q = C::N >> (t + DEPTH + 3);
+  const int lens = (C::SINE && DEPTH > 0) ? ((r >> (DEPTH - 1)) & 1) : lam_c;
+  const int rO = r + ((1 - lens) << DEPTH);
+  const int hi = (C::N >> (t + 1)) - lam_c;
+  R* p0 = ch + (hi - rO);
+  auto at = [&](int jj) -> R& { return p0[-jj * stride]; };
+  if (C::TM) {
+    // M1: cos asc/sub, sin desc/sub; M5: cos desc/add, sin asc/add
+    const bool addop = V == 5;
+    const bool desc = (V == 1) ? (lens == 1) : (lens == 0);
+    const int s0 = desc ? q - 1 : 0, d = desc ? -1 : 1;
+    R prev = A::mul(R(0.5), at(s0));
+    at(s0) = prev;
+    int p = s0;
+    for (int k = 1; k < q; ++k) {
       p += d;
-      const R tt = addop ? A::add(at(p), prev) : A::sub(at(p), prev);
-      at(p) = A::mul(R(0.5), tt);
+      prev = addop ? A::add(at(p), prev) : A::sub(at(p), prev);
+      at(p) = prev;
     }
+  } else {
+    // M3: cos desc/sub, sin asc/sub; M7: cos asc/add, sin desc/add
+    const bool addop = V == 7;
+    const bool desc = (V == 3) ? (lens == 0) : (lens == 1);
+    const int s0 = desc ? q - 1 : 0, d = desc ? -1 : 1;
+    R prev = at(s0);
+    int p = s0;
+    for (int k = 1; k < q - 1; ++k) {
+      p += d;
+      prev = addop ? A::add(at(p), prev) : A::sub(at(p), prev);
+      at(p) = prev;
+    }
+    p += d;
+    const R tt = addop ? A::add(at(p), prev) : A::sub(at(p), prev);
+    at(p) = A::mul(R(0.5), tt);
+  }
+}
+
+template <class C, int DEPTH, typename R>
+__device__ __forceinline__ void am_chains(R* B) {
+  // one thread per odd class (serial recurrence); classes with m <= 2 skip
+  int idx = threadIdx.x;
+  constexpr int classes = 1 << DEPTH;
+  for (int g = idx; g < 4 * C::LOGLB_ * classes; g += C::NT) {
+    const int c = g / (C::LOGLB_ * classes);
+    const int rem = g - c * (C::LOGLB_ * classes);
+    const int t = rem / classes;
+    const int r = rem - t * classes;
+    const int q = C::N >> (t + DEPTH + 3);
+    if (q < 2) continue;
+    chain_class<C, DEPTH, R>(B + c * C::CS, c & 1, t, r);
   }
   __syncthreads();
 }
 
-template <int V, typename R, int LOGN, int LOGLB>
-struct Cfg : FastCfg<V, R, LOGN, LOGLB> {
-  static constexpr int V_ = V;
-  static constexpr int LOGLB_ = LOGLB;
-  static constexpr int LOGN_ = LOGN;
-};
+template <class C, int DEPTH, typename R>
+__device__ __forceinline__ void am_level(R* B) {
+  if constexpr (C::CHAIN) am_chains<C, DEPTH, R>(B);
+  else AmLevel<C, DEPTH>::template run<R>(B);
+}
+
+// Depth loops unrolled at compile time.
+template <class C, typename R, int D>
+__device__ __forceinline__ void am_levels_desc(R* B) {  // D-1 .. 0
+  if constexpr (D > 0) {
+    am_level<C, D - 1, R>(B);
+    am_levels_desc<C, R, D - 1>(B);
+  }
+}
+template <class C, typename R, int D, int I = 0>
+__device__ __forceinline__ void am_levels_asc(R* B) {  // 0 .. D-1
+  if constexpr (I < D) {
+    am_level<C, I, R>(B);
+    am_levels_asc<C, R, D, I + 1>(B);
+  }
+}
 
 template <int V, typename R, int LOGN, int LOGLB>
-__global__ void __launch_bounds__(Cfg<V, R, LOGN, LOGLB>::NT)
+__global__ void __launch_bounds__(Cfg<V, R, LOGN, LOGLB>::NT, (sizeof(R) == 4 ? 2 : 1))
 k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
        const R* __restrict__ tab, int nmax, int inverse, R scale) {
   using C = Cfg<V, R, LOGN, LOGLB>;
@@ -277,24 +314,29 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       V2 a = x[m];
       if (inverse) { const R tmp = a.x; a.x = a.y; a.y = tmp; }
       if (m == 0 || m == H) {
-        Tb[0 * C::CS + ph<LOGLB>(m)] = a.x;
-        Tb[2 * C::CS + ph<LOGLB>(m)] = a.y;
+        Tb[0 * C::CS + C::pt(m)] = a.x;
+        Tb[2 * C::CS + C::pt(m)] = a.y;
       } else {
         V2 b = x[N - m];
         if (inverse) { const R tmp = b.x; b.x = b.y; b.y = tmp; }
-        Tb[0 * C::CS + ph<LOGLB>(m)] = A::add(a.x, b.x);
-        Tb[1 * C::CS + ph<LOGLB>(m)] = A::sub(a.x, b.x);
-        Tb[2 * C::CS + ph<LOGLB>(m)] = A::add(a.y, b.y);
-        Tb[3 * C::CS + ph<LOGLB>(m)] = A::sub(a.y, b.y);
+        Tb[0 * C::CS + C::pt(m)] = A::add(a.x, b.x);
+        Tb[1 * C::CS + C::pt(m)] = A::sub(a.x, b.x);
+        Tb[2 * C::CS + C::pt(m)] = A::add(a.y, b.y);
+        Tb[3 * C::CS + C::pt(m)] = A::sub(a.y, b.y);
       }
     }
     __syncthreads();
 
-    if (C::TM) {
-#pragma unroll 1
-      for (int lvl = 1; lvl <= C::LT; ++lvl) {
-        mirror_level<C, R, true>(Tb, lvl, H >> (lvl - 1), tab, nmax, base);
-        __syncthreads();
+    if constexpr (C::TM) {
+      // top mirror levels (generated, 2^LT cells per thread) || small chains
+      if (tid < 4 * C::LB) {
+        const int c = tid >> LOGLB, v = tid & (C::LB - 1);
+        if (v > 0) {
+          Top<C::LB, C::LT, LOGN, C::SINE>::template fwd<R, A>(c & 1, Tb + c * C::CS, v, tab, base);
+        } else {
+          SmallFull<V, C::HP, LOGN>::template run<R, A, LOGLB, C::LB>(c & 1, Tb + c * C::CS,
+                                                                      Fb + c * C::CS, tab, base);
+        }
       }
     } else {
 #pragma unroll 1
@@ -302,11 +344,11 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
         chain_level<C, R, true>(Tb, n);
         __syncthreads();
       }
-#pragma unroll 1
-      for (int depth = 0; depth < C::LT; ++depth) am_level<C, R>(Tb, depth);
+      am_levels_asc<C, R, C::LT>(Tb);
     }
+    __syncthreads();
 
-    // ---- bottom: T -> F
+    // ---- bottom: T -> F (generated, one LB-segment per thread)
     if (tid < C::NSEG) {
       const int half = C::HP / 2;
       const int h = tid % half;
@@ -319,41 +361,44 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       Bottom<V, C::LB>::template run<R, A, LOGLB>(rho, lens, Tb + c * C::CS, Fb + c * C::CS,
                                                   s * C::LB, tab, nmax, base, N, C::LT, r,
                                                   lam_bit);
-    } else if (tid < C::NSEG + 4) {
-      const int c = tid - C::NSEG;
-      Small<V, C::HP>::template run<R, A, LOGLB, C::LB>(c & 1, Tb + c * C::CS, Fb + c * C::CS,
-                                                        base);
+    }
+    if constexpr (!C::TM) {
+      if (tid >= C::NT - 4) {
+        const int c = tid - (C::NT - 4);
+        SmallFull<V, C::HP, LOGN>::template run<R, A, LOGLB, C::LB>(c & 1, Tb + c * C::CS,
+                                                                    Fb + c * C::CS, tab, base);
+      }
     }
     __syncthreads();
 
-    if (C::TM) {
-#pragma unroll 1
-      for (int depth = C::LT - 1; depth >= 0; --depth) am_level<C, R>(Fb, depth);
+    if constexpr (C::TM) {
+      am_levels_desc<C, R, C::LT>(Fb);
 #pragma unroll 1
       for (int n = 2 * (N / C::LB); n <= N; n <<= 1) {
         chain_level<C, R, false>(Fb, n);
         __syncthreads();
       }
     } else {
-#pragma unroll 1
-      for (int lvl = C::LT; lvl >= 1; --lvl) {
-        mirror_level<C, R, false>(Fb, lvl, H >> (lvl - 1), tab, nmax, base);
-        __syncthreads();
+      if (tid < 4 * C::LB) {
+        const int c = tid >> LOGLB, v = tid & (C::LB - 1);
+        if (v > 0) Top<C::LB, C::LT, LOGN, C::SINE>::template bwd<R, A>(c & 1, Fb + c * C::CS, v, tab, base);
       }
+      __syncthreads();
     }
 
     // ---- store: SplitReal bwd (elab.cpp:199-208) + SplitComplex bwd (162-183)
     V2* y = reinterpret_cast<V2*>(out + row * 2 * N);
     for (int k = tid; k <= H; k += C::NT) {
-      const R rd = Fb[0 * C::CS + ph<LOGLB>(k)];
-      const R id = Fb[2 * C::CS + ph<LOGLB>(k)];
+      const R rd = Fb[0 * C::CS + C::pf(k)];
+      const R id = Fb[2 * C::CS + C::pf(k)];
       V2 lo, hi;
       if (k == 0 || k == H) {
         lo.x = rd;
         lo.y = id;
+        hi = lo;
       } else {
-        const R rs = Fb[1 * C::CS + ph<LOGLB>(k)];
-        const R is = Fb[3 * C::CS + ph<LOGLB>(k)];
+        const R rs = Fb[1 * C::CS + C::pf(k)];
+        const R is = Fb[3 * C::CS + C::pf(k)];
         lo.x = A::add(rd, is);
         lo.y = A::sub(id, rs);
         hi.x = A::sub(rd, is);

@@ -1,0 +1,98 @@
+// gen_host.cpp -- TEST HARNESS: compiles the generated device code
+// (paper_1404_1810_b200/csrc/fast_gen.cuh) as host C++ so the CPU test
+// suite can check every generated function against the fast-kernel model
+// (tests/fast_model.py) without a GPU.  fp64, -ffp-contract=off.
+#define __device__
+#define __forceinline__ inline
+#define __ldg(p) (*(p))
+#include "../../paper_1404_1810_b200/csrc/fast_gen.cuh"
+
+namespace {
+struct HA {
+  static double add(double a, double b) { return a + b; }
+  static double sub(double a, double b) { return a - b; }
+  static double mul(double a, double b) { return a * b; }
+};
+using namespace amqft_b200;
+}  // namespace
+
+template <int V>
+int bottom_v(int LB, int rho, int lens, const double* T, double* F, int a, const double* tab,
+             int nmax, double base, int N, int D, int r, int dsto) {
+  if (LB == 32) { Bottom<V, 32>::template run<double, HA, 5>(rho, lens, T, F, a, tab, nmax, base, N, D, r, dsto); return 0; }
+  if (LB == 64) { Bottom<V, 64>::template run<double, HA, 6>(rho, lens, T, F, a, tab, nmax, base, N, D, r, dsto); return 0; }
+  return -1;
+}
+
+template <int V, int HP, int NL>
+int small_vh(int LB, int lam, const double* T, double* F, const double* tab, double base) {
+  if (LB == 32) { SmallFull<V, HP, NL>::template run<double, HA, 5, 32>(lam, T, F, tab, base); return 0; }
+  if (LB == 64) { SmallFull<V, HP, NL>::template run<double, HA, 6, 64>(lam, T, F, tab, base); return 0; }
+  return -1;
+}
+
+template <int V>
+int small_v(int HP, int nlog, int LB, int lam, const double* T, double* F, const double* tab,
+            double base) {
+  if (HP == 16 && nlog == 10) return small_vh<V, 16, 10>(LB, lam, T, F, tab, base);
+  if (HP == 32 && nlog == 11) return small_vh<V, 32, 11>(LB, lam, T, F, tab, base);
+  if (HP == 64 && nlog == 12) return small_vh<V, 64, 12>(LB, lam, T, F, tab, base);
+  if (HP == 16 && nlog == 11) return small_vh<V, 16, 11>(LB, lam, T, F, tab, base);
+  if (HP == 32 && nlog == 12) return small_vh<V, 32, 12>(LB, lam, T, F, tab, base);
+  if (HP == 64 && nlog == 13) return small_vh<V, 64, 13>(LB, lam, T, F, tab, base);
+  return -1;
+}
+
+
+extern "C" {
+
+int host_top(int LB, int LT, int nlog, int sine, int bwd, int lam, double* B, int v,
+             const double* tab, double base) {
+#define TOPCASE(lb, lt, nl)                                                        \
+  if (LB == lb && LT == lt && nlog == nl) {                                         \
+    if (sine) {                                                                     \
+      if (bwd) Top<lb, lt, nl, 1>::bwd<double, HA>(lam, B, v, tab, base);           \
+      else Top<lb, lt, nl, 1>::fwd<double, HA>(lam, B, v, tab, base);               \
+    } else {                                                                        \
+      if (bwd) Top<lb, lt, nl, 0>::bwd<double, HA>(lam, B, v, tab, base);           \
+      else Top<lb, lt, nl, 0>::fwd<double, HA>(lam, B, v, tab, base);               \
+    }                                                                               \
+    return 0;                                                                       \
+  }
+  TOPCASE(32, 4, 10) TOPCASE(32, 5, 11) TOPCASE(32, 6, 12)
+  TOPCASE(64, 4, 11) TOPCASE(64, 5, 12) TOPCASE(64, 6, 13)
+#undef TOPCASE
+  return -1;
+}
+
+int host_bottom(int V, int LB, int rho, int lens, const double* T, double* F, int a,
+                const double* tab, int nmax, double base, int N, int D, int r, int dsto) {
+  switch (V) {
+    case 1: return bottom_v<1>(LB, rho, lens, T, F, a, tab, nmax, base, N, D, r, dsto);
+    case 2: return bottom_v<2>(LB, rho, lens, T, F, a, tab, nmax, base, N, D, r, dsto);
+    case 3: return bottom_v<3>(LB, rho, lens, T, F, a, tab, nmax, base, N, D, r, dsto);
+    case 4: return bottom_v<4>(LB, rho, lens, T, F, a, tab, nmax, base, N, D, r, dsto);
+    case 5: return bottom_v<5>(LB, rho, lens, T, F, a, tab, nmax, base, N, D, r, dsto);
+    case 6: return bottom_v<6>(LB, rho, lens, T, F, a, tab, nmax, base, N, D, r, dsto);
+    case 7: return bottom_v<7>(LB, rho, lens, T, F, a, tab, nmax, base, N, D, r, dsto);
+    case 8: return bottom_v<8>(LB, rho, lens, T, F, a, tab, nmax, base, N, D, r, dsto);
+  }
+  return -1;
+}
+
+int host_small(int V, int HP, int nlog, int LB, int lam, const double* T, double* F,
+               const double* tab, double base) {
+  switch (V) {
+    case 1: return small_v<1>(HP, nlog, LB, lam, T, F, tab, base);
+    case 2: return small_v<2>(HP, nlog, LB, lam, T, F, tab, base);
+    case 3: return small_v<3>(HP, nlog, LB, lam, T, F, tab, base);
+    case 4: return small_v<4>(HP, nlog, LB, lam, T, F, tab, base);
+    case 5: return small_v<5>(HP, nlog, LB, lam, T, F, tab, base);
+    case 6: return small_v<6>(HP, nlog, LB, lam, T, F, tab, base);
+    case 7: return small_v<7>(HP, nlog, LB, lam, T, F, tab, base);
+    case 8: return small_v<8>(HP, nlog, LB, lam, T, F, tab, base);
+  }
+  return -1;
+}
+
+}  // extern "C"
