@@ -162,7 +162,7 @@ def gen_tmB(v, LB, rho, lam):
         sp = spectrum_tm(em, v, x, 0, LB, rho, lam, sine, t)
         em.emit(f"{{ const int hi = (N >> {t + 1}) - dsto - r;")
         for p, name in enumerate(sp):
-            em.emit(f"  F[hi - ({p} << D)] = {name};")
+            em.emit(f"  F[SW(hi - ({p} << D))] = {name};")
         em.emit("}")
     sig = (f"template <typename R, typename AR, int LOGLB>\n__device__ __forceinline__ void "
            f"tmB_v{v}_lb{LB}_r{rho}_l{lam}(const R* __restrict__ T, R* __restrict__ F, int a, "
@@ -304,7 +304,7 @@ def gen_hmB(v, LB, rho, lam):
         vals = []
         for p in range(cnt):
             nm = f"v{t}_{p}"
-            em.emit(f"const R {nm} = T[hi{t} - ({p} << D)];")
+            em.emit(f"const R {nm} = T[SW(hi{t} - ({p} << D))];")
             vals.append(nm)
         place_hm(em, v, vals, lam, sine, x, 0, LB, rho)
     mnet_bwd(em, x, 0, LB, rho, lam, sine)
@@ -520,11 +520,11 @@ def gen_small_full(v, HP, lam, nlog):
                     G[k], G[n // 2 - k] = em.new(add(o, e)), em.new(sub(o, e))
             n *= 2
         for k in ks:
-            em.emit(f"F[{k}] = {G[k]};")
+            em.emit(f"F[SW({k})] = {G[k]};")
     else:
         S = {}
         for k in ks:
-            em.emit(f"const R s{k} = T[{k}];")
+            em.emit(f"const R s{k} = T[SW({k})];")
             S[k] = f"s{k}"
         x = {}
         Np = 2 * HP
@@ -554,13 +554,12 @@ def gen_small_full(v, HP, lam, nlog):
 
 
 # (LB, nlog) pairs of the fused kernels: LT = nlog - 1 - log2(LB), HP = 2^LT
-FULL_SIZES = [(32, 10), (32, 11), (32, 12), (64, 11), (64, 12), (64, 13)]
+FULL_SIZES = [(64, 10), (64, 11), (64, 12), (64, 13)]
 
 
 # Sizes instantiated by csrc/fast.cu (LB, HP = N/(2 LB)).
 CONFIGS = [
     # (LB, [HP...])
-    (32, [8, 16, 32, 64]),
     (64, [8, 16, 32, 64]),
 ]
 
@@ -571,6 +570,7 @@ def main():
         "// Straight-line bottom-of-recursion code for the fused AM-QFT kernels.",
         "#pragma once",
         "#define PH(i) ((i) + ((i) >> LOGLB))",
+        "#define SW(i) ((i) ^ (((i) >> 5) & 31))",
         "namespace amqft_b200 {",
         "namespace gen {",
     ]
@@ -648,7 +648,7 @@ def main():
             out.append(f"    else gen::{fam}_v{v}_hp{hp}_l1<R, AR, LOGLB, LBV>(T, F, base);")
             out.append("  }")
             out.append("};")
-    out += ["}  // namespace amqft_b200", "#undef PH", ""]
+    out += ["}  // namespace amqft_b200", "#undef PH", "#undef SW", ""]
     sys.stdout.write("\n".join(out))
 
 

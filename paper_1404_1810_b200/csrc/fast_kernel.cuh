@@ -55,15 +55,20 @@ struct Cfg {
   static constexpr int NSEG = 4 * HP;             // bottom segments (4 chains)
   static constexpr int NT0 = (4 * LB > NSEG ? 4 * LB : NSEG);
   static constexpr int NT = NT0 < 128 ? 128 : NT0;
-  static constexpr int CS = ((H + HP + 1) + 3) / 4 * 4;  // chain stride
+  // chain stride: holds the skewed (H + H/LB + 1) and the swizzled
+  // (32-aligned blocks up to H) layouts; +16 staggers the chains' banks.
+  static constexpr int CS = ((H + HP + 1 > H + 32 ? H + HP + 1 : H + 32) + 31) / 32 * 32 + 16;
   static constexpr bool TM = (V == 1 || V == 4 || V == 5 || V == 8);
   static constexpr int SINE = V >= 5 ? 1 : 0;
   static constexpr bool CHAIN = (V == 1 || V == 5 || V == 3 || V == 7);
   static constexpr size_t SMEM = 8 * CS * sizeof(R);
-  // skew (i + i/LB) only on the buffer holding the index-space mirror
-  // network: T for time-major, F for harmonic-major.
-  static __device__ __forceinline__ int pt(int i) { return TM ? i + (i >> LOGLB) : i; }
-  static __device__ __forceinline__ int pf(int i) { return TM ? i : i + (i >> LOGLB); }
+  // Bank-conflict layouts: skew (i + i/LB) on the buffer holding the
+  // index-space mirror network (T for time-major, F for harmonic-major);
+  // XOR swizzle (i ^ (i/32 mod 32)) on the other one (strided class runs).
+  static __device__ __forceinline__ int skew(int i) { return i + (i >> LOGLB); }
+  static __device__ __forceinline__ int swz(int i) { return i ^ ((i >> 5) & 31); }
+  static __device__ __forceinline__ int pt(int i) { return TM ? skew(i) : swz(i); }
+  static __device__ __forceinline__ int pf(int i) { return TM ? swz(i) : skew(i); }
 };
 
 // Segment parameters at depth d: orientation, lens, residue (fast_model.segment_params).
@@ -95,7 +100,7 @@ __device__ __forceinline__ void chain_level(R* B, int n) {
     const int lam = c & 1;
     if (lam && k == 0) continue;
     R* ch = B + c * C::CS;
-    const int i0 = k, i1 = (n >> 1) - k;
+    const int i0 = C::swz(k), i1 = C::swz((n >> 1) - k);
     const R e = ch[i0], o = ch[i1];
     if (!FWD) {  // elaborations.cpp:310-329
       ch[i0] = lam ? A::add(o, e) : A::add(e, o);
@@ -107,111 +112,9 @@ __device__ __forceinline__ void chain_level(R* B, int n) {
   }
 }
 
-// ---- AM conversion levels on the odd residue classes (unskewed buffer).
-// Time-major: AM_B (elaborations.cpp:472-526) on F, depth D-1 .. 0;
-// harmonic-major: AM_F (elaborations.cpp:370-448) on T, depth 0 .. D-1.
-// Work item = a run of up to RU consecutive class positions; neighbour
-// operations read one halo cell, results are staged in registers until the
-// whole CTA has read (in-place update).  Serial recurrences (variants
-// 1,3,5,7) run the class in place from its first run's thread.
-template <class C, int DEPTH>
-struct AmLevel {
-  static constexpr int RU = 16;
-  static constexpr int q_of(int t) { return C::N >> (t + DEPTH + 3); }
-  static constexpr int len_of(int t) { return q_of(t) < RU ? q_of(t) : RU; }
-  static constexpr int items_of(int t) {
-    return q_of(t) >= 2 ? (1 << DEPTH) * (q_of(t) / len_of(t)) : 0;
-  }
-  static constexpr int items_chain() {
-    int s = 0;
-    for (int t = 0; t < C::LOGLB_; ++t) s += items_of(t);
-    return s;
-  }
-  static constexpr int IC = items_chain();
-  static constexpr int TOTAL = 4 * IC;
-  static constexpr int PER = (TOTAL + C::NT - 1) / C::NT;
-
-  template <typename R>
-  static __device__ __forceinline__ void run(R* B) {
-    using A = Arith<R>;
-    constexpr int V = C::V_;
-    constexpr int stride = 2 << DEPTH;
-    R val[PER][RU];
-    R* dst[PER];
-    int cnt[PER];
-#pragma unroll
-    for (int u = 0; u < PER; ++u) {
-      cnt[u] = 0;
-      dst[u] = nullptr;
-      const int g = threadIdx.x + u * C::NT;
-      if (g >= TOTAL) continue;
-      const int c = g / IC;
-      int w = g - c * IC;
-      int t = 0;
-#pragma unroll
-      for (int tt = 0; tt < C::LOGLB_; ++tt) {
-        if (w >= items_of(tt) && t == tt) { w -= items_of(tt); t = tt + 1; }
-      }
-      const int q = C::N >> (t + DEPTH + 3);
-      const int len = q < RU ? q : RU;
-      const int runs = q / len;
-      const int r = w / runs;               // class (residue at this depth)
-      const int b = w - r * runs;           // run within the class
-      const int lam_c = c & 1;
-      const int lens = (C::SINE && DEPTH > 0) ? ((r >> (DEPTH - 1)) & 1) : lam_c;
-      const int rO = r + ((1 - lens) << DEPTH);
-      const int hi = (C::N >> (t + 1)) - lam_c;
-      R* ch = B + c * C::CS;
-      const int j0 = b * len;
-      R* p0 = ch + (hi - rO - j0 * stride);  // cell(j) = p0 - (j - j0) * stride
-      // right-halo ops read C[j+1], left-halo ops read C[j-1]
-      bool right;
-      if (C::TM) right = (V == 4) ? (lens == 0) : (lens == 1);
-      else right = (V == 2) ? (lens == 1) : (lens == 0);
-      // the op:  right: out_j = f(C_j, C_{j+1}), last class cell copies;
-      //          left:  out_j = f(C_{j-1}, C_j) (order per variant), first copies.
-#pragma unroll
-      for (int i = 0; i < RU; ++i) {
-        if (i >= len) break;
-        const int j = j0 + i;
-        const R cj = p0[-i * stride];
-        R o;
-        if (right) {
-          if (j == q - 1) o = cj;
-          else {
-            const R cn = p0[-(i + 1) * stride];
-            if (C::TM) o = (V == 4) ? A::add(cj, cn) : A::sub(cj, cn);
-            else o = (V == 2) ? A::add(cn, cj) : A::sub(cj, cn);
-          }
-        } else {
-          if (j == 0) o = cj;
-          else {
-            const R cp = p0[-(i - 1) * stride];
-            if (C::TM) o = (V == 4) ? A::add(cp, cj) : A::sub(cj, cp);
-            else o = (V == 2) ? A::add(cj, cp) : A::sub(cj, cp);
-          }
-        }
-        val[u][i] = o;
-      }
-      dst[u] = p0;
-      cnt[u] = len;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < PER; ++u) {
-      if (cnt[u] > 0) {
-#pragma unroll
-        for (int i = 0; i < RU; ++i) {
-          if (i >= cnt[u]) break;
-          dst[u][-i * stride] = val[u][i];
-        }
-      }
-    }
-    __syncthreads();
-  }
-
-};
-
+// ---- Serial AM recurrences (variants 1,3,5,7): AM_B M1/M5
+// (elaborations.cpp:472-513) or AM_F M3/M7 (402-448) along each odd class
+// of the big top blocks, one thread per class, in place (swizzled buffer).
 template <class C, int DEPTH, typename R>
 __device__ __forceinline__ void chain_class(R* ch, int lam_c, int t, int r) {
   using A = Arith<R>;
@@ -221,8 +124,8 @@ __device__ __forceinline__ void chain_class(R* ch, int lam_c, int t, int r) {
   const int lens = (C::SINE && DEPTH > 0) ? ((r >> (DEPTH - 1)) & 1) : lam_c;
   const int rO = r + ((1 - lens) << DEPTH);
   const int hi = (C::N >> (t + 1)) - lam_c;
-  R* p0 = ch + (hi - rO);
-  auto at = [&](int jj) -> R& { return p0[-jj * stride]; };
+  const int c0 = hi - rO;
+  auto at = [&](int jj) -> R& { return ch[C::swz(c0 - jj * stride)]; };
   if (C::TM) {
     // M1: cos asc/sub, sin desc/sub; M5: cos desc/add, sin asc/add
     const bool addop = V == 5;
@@ -273,8 +176,7 @@ __device__ __forceinline__ void am_chains(R* B) {
 
 template <class C, int DEPTH, typename R>
 __device__ __forceinline__ void am_level(R* B) {
-  if constexpr (C::CHAIN) am_chains<C, DEPTH, R>(B);
-  else AmLevel<C, DEPTH>::template run<R>(B);
+  am_chains<C, DEPTH, R>(B);
 }
 
 // Depth loops unrolled at compile time.
@@ -293,10 +195,141 @@ __device__ __forceinline__ void am_levels_asc(R* B) {  // 0 .. D-1
   }
 }
 
+// ---- Register-resident AM phase (non-recurrent variants 2,4,6,8).
+// Every odd-class neighbour operation of every depth for the big top
+// blocks (t < log2 LB) runs out of registers: warp pair (2c, 2c+1) owns
+// chain c; top block 0 is one warp, blocks 1.. share the second warp; each
+// lane owns RR = N/128 consecutive positions of its block (natural order,
+// cell(p) = hi - p).  Halo values cross lanes with warp shuffles; the last
+// lane of a block takes the class-end copy, so segment boundaries inside a
+// warp never consume foreign data.
+template <class C, typename R, bool BWD, int LAM, int D>
+__device__ __forceinline__ void am_depth(R (&x)[C::N / 128], bool last_lane, bool first_lane,
+                                         bool blk_ok) {
+  using A = Arith<R>;
+  constexpr int V = C::V_;
+  constexpr int RR = C::N / 128;
+  constexpr int S = 2 << D;
+  static_assert(S <= RR, "class stride must fit a lane's run");
+  R hr[S], hl[S];
+#pragma unroll
+  for (int h = 0; h < S; ++h) {
+    hr[h] = __shfl_down_sync(0xffffffffu, x[h], 1);
+    hl[h] = __shfl_up_sync(0xffffffffu, x[RR - 1 - h], 1);
+  }
+  R y[RR];
+#pragma unroll
+  for (int l = 0; l < RR; ++l) {
+    // low bits of the block position p = i*RR + l are those of l (S <= RR)
+    const int obit = (l >> D) & 1;
+    const int lens = (C::SINE && D > 0) ? ((l >> (D - 1)) & 1) : LAM;
+    const bool is_o = obit == 1 - lens;
+    y[l] = x[l];
+    if (!is_o) continue;
+    bool right;
+    if (BWD) right = (V == 4) ? (lens == 0) : (lens == 1);   // AM_B M4 / M8
+    else right = (V == 2) ? (lens == 1) : (lens == 0);       // AM_F M2 / M6
+    const R cj = x[l];
+    R cn;
+    bool edge;
+    if (right) {
+      cn = (l + S < RR) ? x[l + S] : hr[l + S - RR];
+      edge = (l + S >= RR) && last_lane;     // class end: copy
+    } else {
+      cn = (l - S >= 0) ? x[l - S] : hl[S - 1 - l];
+      edge = (l - S < 0) && first_lane;      // class start: copy
+    }
+    R o;
+    const bool addop = BWD ? (V == 4) : (V == 2);
+    if (addop) o = A::add(cj, cn);
+    else o = right ? (BWD ? A::sub(cj, cn) : A::sub(cj, cn)) : A::sub(cj, cn);
+    y[l] = (edge || !blk_ok) ? cj : o;
+  }
+#pragma unroll
+  for (int l = 0; l < RR; ++l) x[l] = y[l];
+}
+
+template <class C, typename R, bool BWD, int LAM>
+__device__ __forceinline__ void am_depths(R (&x)[C::N / 128], bool last_lane, bool first_lane,
+                                          int Mt) {
+  auto step = [&](auto dtag) {
+    constexpr int D = decltype(dtag)::value;
+    am_depth<C, R, BWD, LAM, D>(x, last_lane, first_lane, (Mt >> (D + 1)) >= 2);
+  };
+  static_assert(C::LT <= 6, "depth range");
+  if constexpr (BWD) {
+    if constexpr (C::LT > 5) step(std::integral_constant<int, 5>());
+    if constexpr (C::LT > 4) step(std::integral_constant<int, 4>());
+    if constexpr (C::LT > 3) step(std::integral_constant<int, 3>());
+    if constexpr (C::LT > 2) step(std::integral_constant<int, 2>());
+    if constexpr (C::LT > 1) step(std::integral_constant<int, 1>());
+    step(std::integral_constant<int, 0>());
+  } else {
+    step(std::integral_constant<int, 0>());
+    if constexpr (C::LT > 1) step(std::integral_constant<int, 1>());
+    if constexpr (C::LT > 2) step(std::integral_constant<int, 2>());
+    if constexpr (C::LT > 3) step(std::integral_constant<int, 3>());
+    if constexpr (C::LT > 4) step(std::integral_constant<int, 4>());
+    if constexpr (C::LT > 5) step(std::integral_constant<int, 5>());
+  }
+}
+
+template <class C, typename R, bool BWD>
+__device__ __forceinline__ void am_phase_regs(R* B) {
+  constexpr int RR = C::N / 128;
+  constexpr int LOGR = C::LOGN_ - 7;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = warp >> 1;
+  int t, i;
+  if ((warp & 1) == 0) {
+    t = 0;
+    i = lane;
+  } else {
+    t = 1 + (lane >= 16) + (lane >= 24) + (lane >= 28) + (lane >= 30) + (lane >= 31);
+    i = lane - (32 - (64 >> t));
+  }
+  const bool active = warp < 8 && t < C::LOGLB_;
+  const int tt = active ? t : 0;
+  const int lam_c = c & 1;
+  const int Mt = C::N >> (tt + 2);
+  const int nl = 32 >> tt;                       // lanes of this block
+  R* chb = B + (c & 3) * C::CS;
+  const int cell0 = (C::N >> (tt + 1)) - lam_c - (i << LOGR);
+  R x[RR];
+#pragma unroll
+  for (int l = 0; l < RR; ++l) x[l] = active ? chb[C::swz(cell0 - l)] : R(0);
+  const bool last_lane = i == nl - 1, first_lane = i == 0;
+  if (lam_c) am_depths<C, R, BWD, 1>(x, last_lane, first_lane, Mt);
+  else am_depths<C, R, BWD, 0>(x, last_lane, first_lane, Mt);
+  if (active) {
+#pragma unroll
+    for (int l = 0; l < RR; ++l) chb[C::swz(cell0 - l)] = x[l];
+  }
+}
+
+#ifdef AMQFT_PHASE_TIMING
+// Instrumented build only (tools/phase_timing): CTA 0 accumulates the
+// cycles spent between phase boundaries.
+__device__ unsigned long long g_phase_cycles[16];
+#define PHASE_MARK(k)                                                          \
+  do {                                                                         \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                                 \
+      const long long now = clock64();                                         \
+      if ((k) > 0) atomicAdd(&g_phase_cycles[(k) - 1], (unsigned long long)(now - t_prev)); \
+      t_prev = now;                                                            \
+    }                                                                          \
+  } while (0)
+#else
+#define PHASE_MARK(k) do {} while (0)
+#endif
+
 template <int V, typename R, int LOGN, int LOGLB>
 __global__ void __launch_bounds__(Cfg<V, R, LOGN, LOGLB>::NT, (sizeof(R) == 4 ? 2 : 1))
 k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
        const R* __restrict__ tab, int nmax, int inverse, R scale) {
+#ifdef AMQFT_PHASE_TIMING
+  long long t_prev = 0;
+#endif
   using C = Cfg<V, R, LOGN, LOGLB>;
   using A = Arith<R>;
   using V2 = typename std::conditional<sizeof(R) == 4, float2, double2>::type;
@@ -308,6 +341,7 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
   constexpr int N = C::N, H = C::H;
 
   for (size_t row = blockIdx.x; row < rows; row += gridDim.x) {
+    PHASE_MARK(0);
     // ---- load: SplitComplex (elab.cpp:152-155) + SplitReal (185-197)
     const V2* x = reinterpret_cast<const V2*>(in + row * 2 * N);
     for (int m = tid; m <= H; m += C::NT) {
@@ -326,6 +360,7 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       }
     }
     __syncthreads();
+    PHASE_MARK(1);
 
     if constexpr (C::TM) {
       // top mirror levels (generated, 2^LT cells per thread) || small chains
@@ -344,9 +379,11 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
         chain_level<C, R, true>(Tb, n);
         __syncthreads();
       }
-      am_levels_asc<C, R, C::LT>(Tb);
+      if constexpr (C::CHAIN) am_levels_asc<C, R, C::LT>(Tb);
+      else am_phase_regs<C, R, false>(Tb);
     }
     __syncthreads();
+    PHASE_MARK(2);
 
     // ---- bottom: T -> F (generated, one LB-segment per thread)
     if (tid < C::NSEG) {
@@ -370,9 +407,15 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       }
     }
     __syncthreads();
+    PHASE_MARK(3);
 
     if constexpr (C::TM) {
-      am_levels_desc<C, R, C::LT>(Fb);
+      if constexpr (C::CHAIN) am_levels_desc<C, R, C::LT>(Fb);
+      else {
+        am_phase_regs<C, R, true>(Fb);
+        __syncthreads();
+      }
+      PHASE_MARK(4);
 #pragma unroll 1
       for (int n = 2 * (N / C::LB); n <= N; n <<= 1) {
         chain_level<C, R, false>(Fb, n);
@@ -385,6 +428,7 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       }
       __syncthreads();
     }
+    PHASE_MARK(5);
 
     // ---- store: SplitReal bwd (elab.cpp:199-208) + SplitComplex bwd (162-183)
     V2* y = reinterpret_cast<V2*>(out + row * 2 * N);
@@ -412,6 +456,7 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       if (k != 0 && k != H) y[N - k] = hi;
     }
     __syncthreads();
+    PHASE_MARK(6);
   }
 }
 
@@ -451,19 +496,13 @@ class FastPlanImpl final : public FastPlan {
 
 template <int V, typename R>
 std::unique_ptr<FastPlan> make_for_variant(size_t n, const void* tab, uint32_t nmax, int dev) {
-  if constexpr (sizeof(R) == 4) {
-    switch (n) {
-      case 1024: return std::make_unique<FastPlanImpl<V, R, 10, 5>>(tab, nmax, dev);
-      case 2048: return std::make_unique<FastPlanImpl<V, R, 11, 6>>(tab, nmax, dev);
-      case 4096: return std::make_unique<FastPlanImpl<V, R, 12, 6>>(tab, nmax, dev);
-      case 8192: return std::make_unique<FastPlanImpl<V, R, 13, 6>>(tab, nmax, dev);
-    }
-  } else {
-    switch (n) {
-      case 1024: return std::make_unique<FastPlanImpl<V, R, 10, 5>>(tab, nmax, dev);
-      case 2048: return std::make_unique<FastPlanImpl<V, R, 11, 5>>(tab, nmax, dev);
-      case 4096: return std::make_unique<FastPlanImpl<V, R, 12, 5>>(tab, nmax, dev);
-    }
+  switch (n) {
+    case 1024: return std::make_unique<FastPlanImpl<V, R, 10, 6>>(tab, nmax, dev);
+    case 2048: return std::make_unique<FastPlanImpl<V, R, 11, 6>>(tab, nmax, dev);
+    case 4096: return std::make_unique<FastPlanImpl<V, R, 12, 6>>(tab, nmax, dev);
+    case 8192:
+      if constexpr (sizeof(R) == 4) return std::make_unique<FastPlanImpl<V, R, 13, 6>>(tab, nmax, dev);
+      break;
   }
   return nullptr;
 }

@@ -39,6 +39,10 @@ def lib():
     return _lib
 
 
+def _swz(i):
+    return i ^ ((i >> 5) & 31)
+
+
 def _par(x):
     return bin(x).count("1") & 1
 
@@ -71,8 +75,7 @@ def _am_level(B, CS, N, LOGLB, depth, v, sine, tm):
             for r in range(1 << depth):
                 lens = ((r >> (depth - 1)) & 1) if (sine and depth > 0) else lam_c
                 rO = r + ((1 - lens) << depth)
-                base = c * CS + hi - rO
-                cells = [base - j * stride for j in range(q)]
+                cells = [c * CS + _swz(hi - rO - j * stride) for j in range(q)]
                 Cv = [B[p] for p in cells]
                 if chain:
                     out = _chain(v, tm, lens, Cv)
@@ -141,7 +144,7 @@ def _chain_level(B, CS, n, fwd):
         for k in range(q):
             if lam and k == 0:
                 continue
-            i0, i1 = c * CS + k, c * CS + (n >> 1) - k
+            i0, i1 = c * CS + _swz(k), c * CS + _swz((n >> 1) - k)
             e, o = B[i0], B[i1]
             if not fwd:
                 B[i0], B[i1] = (o + e, o - e) if lam else (e + o, e - o)
@@ -158,11 +161,13 @@ def emulate(v, N, LB, x, tab, base):
     HP = H // LB
     NSEG = 4 * HP
     NT = max(4 * LB, NSEG, 128)
-    CS = ((H + HP + 1) + 3) // 4 * 4
+    CS = (max(H + HP + 1, H + 32) + 31) // 32 * 32 + 16
     TM = v in (1, 4, 5, 8)
     SINE = 1 if v >= 5 else 0
-    pt = (lambda i: i + (i >> LOGLB)) if TM else (lambda i: i)
-    pf = (lambda i: i) if TM else (lambda i: i + (i >> LOGLB))
+    skew = lambda i: i + (i >> LOGLB)  # noqa: E731
+    swz = lambda i: i ^ ((i >> 5) & 31)  # noqa: E731
+    pt = skew if TM else swz
+    pf = swz if TM else skew
     T = np.zeros(4 * CS + 8)
     F = np.zeros(4 * CS + 8)
     tab = np.ascontiguousarray(tab, dtype=np.float64)
@@ -189,8 +194,11 @@ def emulate(v, N, LB, x, tab, base):
         while n >= 2 * (N // LB):
             _chain_level(T, CS, n, True)
             n >>= 1
-        for depth in range(LT):
-            _am_level(T, CS, N, LOGLB, depth, v, SINE, False)
+        if v in (3, 7):
+            for depth in range(LT):
+                _am_level(T, CS, N, LOGLB, depth, v, SINE, False)
+        else:
+            am_phase_regs(T, CS, N, LOGLB, LT, v, SINE, False)
     half = HP // 2
     for tid in range(NSEG):
         h = tid % half
@@ -205,8 +213,11 @@ def emulate(v, N, LB, x, tab, base):
         for c in range(4):
             assert L.host_small(v, HP, LOGN, LB, c & 1, Tp + 8 * c * CS, Fp + 8 * c * CS, tp, base) == 0
     if TM:
-        for depth in range(LT - 1, -1, -1):
-            _am_level(F, CS, N, LOGLB, depth, v, SINE, True)
+        if v in (1, 5):
+            for depth in range(LT - 1, -1, -1):
+                _am_level(F, CS, N, LOGLB, depth, v, SINE, True)
+        else:
+            am_phase_regs(F, CS, N, LOGLB, LT, v, SINE, True)
         n = 2 * (N // LB)
         while n <= N:
             _chain_level(F, CS, n, False)
@@ -225,3 +236,72 @@ def emulate(v, N, LB, x, tab, base):
             out[2 * k], out[2 * k + 1] = rd + is_, idd - rs
             out[2 * (N - k)], out[2 * (N - k) + 1] = rd - is_, idd + rs
     return out
+
+
+def am_phase_regs(B, CS, N, LOGLB, LT, v, sine, bwd):
+    """Mirror of fast_kernel.cuh am_phase_regs: per-lane runs of RR cells,
+    halo exchange between adjacent lanes of the same warp (shuffles)."""
+    RR = N // 128
+    LOGR = RR.bit_length() - 1
+    lanes = []  # (warp, lane, c, t, i, active)
+    for warp in range(8):
+        for lane in range(32):
+            c = warp >> 1
+            if warp % 2 == 0:
+                t, i = 0, lane
+            else:
+                t = 1 + (lane >= 16) + (lane >= 24) + (lane >= 28) + (lane >= 30) + (lane >= 31)
+                i = lane - (32 - (64 >> t))
+            active = t < LOGLB
+            lanes.append((warp, lane, c, t if active else 0, i, active))
+    X = {}
+    for (warp, lane, c, t, i, active) in lanes:
+        lam_c = c & 1
+        basep = (N >> (t + 1)) - lam_c - (i << LOGR)
+        X[(warp, lane)] = [B[c * CS + _swz(basep - l)] if active else 0.0 for l in range(RR)]
+    depths = list(range(LT - 1, -1, -1)) if bwd else list(range(LT))
+    for D in depths:
+        S = 2 << D
+        new = {}
+        for (warp, lane, c, t, i, active) in lanes:
+            lam_c = c & 1
+            Mt = N >> (t + 2)
+            blk_ok = (Mt >> (D + 1)) >= 2
+            x = X[(warp, lane)]
+            xr = X[(warp, lane + 1)] if lane < 31 else x     # shfl_down (lane 31 keeps own)
+            xl = X[(warp, lane - 1)] if lane > 0 else x      # shfl_up (lane 0 keeps own)
+            y = []
+            for l in range(RR):
+                p = (i << LOGR) + l
+                obit = (p >> D) & 1
+                lens = ((p >> (D - 1)) & 1) if (sine and D > 0) else lam_c
+                is_o = blk_ok and (obit == 1 - lens)
+                if bwd:
+                    right = (lens == 0) if v == 4 else (lens == 1)
+                else:
+                    right = (lens == 1) if v == 2 else (lens == 0)
+                cj = x[l]
+                if right:
+                    cn = x[l + S] if l + S < RR else (xr[l + S - RR] if S <= RR else cj)
+                    edge = p + S >= Mt
+                else:
+                    cn = x[l - S] if l - S >= 0 else (xl[l - S + RR] if S <= RR else cj)
+                    edge = p - S < 0
+                o = cj
+                if not edge:
+                    if bwd:
+                        o = ((cj + cn) if v == 4 else (cj - cn)) if right else \
+                            ((cn + cj) if v == 4 else (cj - cn))
+                    else:
+                        o = ((cn + cj) if v == 2 else (cj - cn)) if right else \
+                            ((cj + cn) if v == 2 else (cj - cn))
+                y.append(o if is_o else cj)
+            new[(warp, lane)] = y
+        X = new
+    for (warp, lane, c, t, i, active) in lanes:
+        if not active:
+            continue
+        lam_c = c & 1
+        basep = (N >> (t + 1)) - lam_c - (i << LOGR)
+        for l in range(RR):
+            B[c * CS + _swz(basep - l)] = X[(warp, lane)][l]

@@ -19,14 +19,12 @@ using namespace amqft_b200;
 template <int V>
 int bottom_v(int LB, int rho, int lens, const double* T, double* F, int a, const double* tab,
              int nmax, double base, int N, int D, int r, int dsto) {
-  if (LB == 32) { Bottom<V, 32>::template run<double, HA, 5>(rho, lens, T, F, a, tab, nmax, base, N, D, r, dsto); return 0; }
   if (LB == 64) { Bottom<V, 64>::template run<double, HA, 6>(rho, lens, T, F, a, tab, nmax, base, N, D, r, dsto); return 0; }
   return -1;
 }
 
 template <int V, int HP, int NL>
 int small_vh(int LB, int lam, const double* T, double* F, const double* tab, double base) {
-  if (LB == 32) { SmallFull<V, HP, NL>::template run<double, HA, 5, 32>(lam, T, F, tab, base); return 0; }
   if (LB == 64) { SmallFull<V, HP, NL>::template run<double, HA, 6, 64>(lam, T, F, tab, base); return 0; }
   return -1;
 }
@@ -34,9 +32,7 @@ int small_vh(int LB, int lam, const double* T, double* F, const double* tab, dou
 template <int V>
 int small_v(int HP, int nlog, int LB, int lam, const double* T, double* F, const double* tab,
             double base) {
-  if (HP == 16 && nlog == 10) return small_vh<V, 16, 10>(LB, lam, T, F, tab, base);
-  if (HP == 32 && nlog == 11) return small_vh<V, 32, 11>(LB, lam, T, F, tab, base);
-  if (HP == 64 && nlog == 12) return small_vh<V, 64, 12>(LB, lam, T, F, tab, base);
+  if (HP == 8 && nlog == 10) return small_vh<V, 8, 10>(LB, lam, T, F, tab, base);
   if (HP == 16 && nlog == 11) return small_vh<V, 16, 11>(LB, lam, T, F, tab, base);
   if (HP == 32 && nlog == 12) return small_vh<V, 32, 12>(LB, lam, T, F, tab, base);
   if (HP == 64 && nlog == 13) return small_vh<V, 64, 13>(LB, lam, T, F, tab, base);
@@ -59,8 +55,7 @@ int host_top(int LB, int LT, int nlog, int sine, int bwd, int lam, double* B, in
     }                                                                               \
     return 0;                                                                       \
   }
-  TOPCASE(32, 4, 10) TOPCASE(32, 5, 11) TOPCASE(32, 6, 12)
-  TOPCASE(64, 4, 11) TOPCASE(64, 5, 12) TOPCASE(64, 6, 13)
+  TOPCASE(64, 3, 10) TOPCASE(64, 4, 11) TOPCASE(64, 5, 12) TOPCASE(64, 6, 13)
 #undef TOPCASE
   return -1;
 }

@@ -29,7 +29,7 @@ def test_models_bitwise(oracle, restatement, v):
 
 
 @pytest.mark.parametrize("v", range(1, 9))
-@pytest.mark.parametrize("n,lb", [(1024, 32), (2048, 32), (2048, 64), (4096, 64)])
+@pytest.mark.parametrize("n,lb", [(1024, 64), (2048, 64), (4096, 64), (8192, 64)])
 def test_kernel_emulator_bitwise(oracle, restatement, v, n, lb):
     r, O = restatement, oracle
     x = O.seeded_signal(9, O.CDFT, n, 100 + v, r)

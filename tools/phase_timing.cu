@@ -1,0 +1,32 @@
+// phase_timing.cu -- DIAGNOSTIC build of the fused kernel with per-phase
+// clock64() accounting (CTA 0).  Not part of the product library.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -shared -Xcompiler -fPIC \
+//        -o tools/libphase_timing.so tools/phase_timing.cu
+#define AMQFT_PHASE_TIMING
+#include "../paper_1404_1810_b200/csrc/fast_kernel.cuh"
+
+using namespace amqft_b200::fastk;
+
+template <int V>
+static int run_v(const float* in, float* out, size_t rows, const float* tab, int nmax,
+                 unsigned long long* cyc, int grid) {
+  using C = Cfg<V, float, 12, 6>;
+  auto fn = k_fast<V, float, 12, 6>;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+  unsigned long long z[16] = {0};
+  cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
+  fn<<<grid, C::NT, C::SMEM>>>(in, out, rows, tab, nmax, 0, 1.0f / 4096);
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(cyc, g_phase_cycles, sizeof(z));
+  return (int)cudaGetLastError();
+}
+
+extern "C" int pt_run(int v, const float* in, float* out, size_t rows, const float* tab,
+                      int nmax, unsigned long long* cyc, int grid) {
+  switch (v) {
+    case 1: return run_v<1>(in, out, rows, tab, nmax, cyc, grid);
+    case 2: return run_v<2>(in, out, rows, tab, nmax, cyc, grid);
+    case 4: return run_v<4>(in, out, rows, tab, nmax, cyc, grid);
+  }
+  return -1;
+}
