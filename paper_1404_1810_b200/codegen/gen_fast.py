@@ -119,10 +119,16 @@ def interleave(lens, E, O):
     return out
 
 
-def mnet_fwd(em, x, a, L, rho, lens, sine):
+def tz(u):
+    return (u & -u).bit_length() - 1
+
+
+def mnet_fwd(em, x, a, L, rho, lens, sine, cls=None):
     if L < 4:
         return
     for v in range(1, L // 2):
+        if cls is not None and tz(v) != cls:
+            continue
         lo, hi = a + v, a + L - v
         j, m = (lo, hi) if rho == 0 else (hi, lo)
         p, q = x[j], x[m]
@@ -133,8 +139,8 @@ def mnet_fwd(em, x, a, L, rho, lens, sine):
         x[j], x[m] = e_name, o_name
     lo_l = lens if rho == 0 else lens ^ sine
     hi_l = lens ^ sine if rho == 0 else lens
-    mnet_fwd(em, x, a, L // 2, 0, lo_l, sine)
-    mnet_fwd(em, x, a + L // 2, L // 2, 1, hi_l, sine)
+    mnet_fwd(em, x, a, L // 2, 0, lo_l, sine, cls)
+    mnet_fwd(em, x, a + L // 2, L // 2, 1, hi_l, sine, cls)
 
 
 def spectrum_tm(em, v, x, a, L, rho, lens, sine, tcls):
@@ -150,20 +156,25 @@ def spectrum_tm(em, v, x, a, L, rho, lens, sine, tcls):
 
 
 def gen_tmB(v, LB, rho, lam):
+    """Class by class: mirror folds never mix trailing-zero classes
+    (tz(v) == tz(L - v)), so each class is loaded, transformed and stored
+    on its own -- small live register set."""
     sine = 1 if v >= 5 else 0
     lg = LB.bit_length() - 1
     em = Emitter()
-    x = {u: f"x{u}" for u in range(1, LB)}
-    for u in range(1, LB):
-        em.emit(f"const R x{u} = T[PH(a + {u})];")
-    x = dict(x)
-    mnet_fwd(em, x, 0, LB, rho, lam, sine)
     for t in range(lg):
+        x = {}
+        for u in range(1, LB):
+            if tz(u) == t:
+                em.emit(f"const R x{u} = T[PH(a + {u})];")
+                x[u] = f"x{u}"
+        mnet_fwd(em, x, 0, LB, rho, lam, sine, cls=t)
         sp = spectrum_tm(em, v, x, 0, LB, rho, lam, sine, t)
         em.emit(f"{{ const int hi = (N >> {t + 1}) - dsto - r;")
         for p, name in enumerate(sp):
             em.emit(f"  F[SW(hi - ({p} << D))] = {name};")
         em.emit("}")
+        em.emit('asm volatile("" ::: "memory");  // keep classes apart (register pressure)')
     sig = (f"template <typename R, typename AR, int LOGLB>\n__device__ __forceinline__ void "
            f"tmB_v{v}_lb{LB}_r{rho}_l{lam}(const R* __restrict__ T, R* __restrict__ F, int a, "
            f"const R* __restrict__ tab, int nmax, R base, int N, int D, int r, int dsto)")
@@ -275,14 +286,16 @@ def place_hm(em, v, vals, lens, sine, x, a, L, rho):
     place_hm(em, v, C, lens ^ sine, sine, x, *os_)
 
 
-def mnet_bwd(em, x, a, L, rho, lens, sine):
+def mnet_bwd(em, x, a, L, rho, lens, sine, cls=None):
     if L < 4:
         return
     lo_l = lens if rho == 0 else lens ^ sine
     hi_l = lens ^ sine if rho == 0 else lens
-    mnet_bwd(em, x, a, L // 2, 0, lo_l, sine)
-    mnet_bwd(em, x, a + L // 2, L // 2, 1, hi_l, sine)
+    mnet_bwd(em, x, a, L // 2, 0, lo_l, sine, cls)
+    mnet_bwd(em, x, a + L // 2, L // 2, 1, hi_l, sine, cls)
     for v in range(1, L // 2):
+        if cls is not None and tz(v) != cls:
+            continue
         lo, hi = a + v, a + L - v
         j, m = (lo, hi) if rho == 0 else (hi, lo)
         E, C = x[j], x[m]
@@ -294,22 +307,25 @@ def mnet_bwd(em, x, a, L, rho, lens, sine):
 
 
 def gen_hmB(v, LB, rho, lam):
+    """Class by class (see gen_tmB)."""
     sine = 1 if v >= 5 else 0
     lg = LB.bit_length() - 1
     em = Emitter()
-    x = {}
     for t in range(lg):
+        x = {}
         cnt = LB >> (t + 1)
-        em.emit(f"const int hi{t} = (N >> {t + 1}) - dsto - r;")
+        em.emit(f"{{ const int hi{t} = (N >> {t + 1}) - dsto - r;")
         vals = []
         for p in range(cnt):
             nm = f"v{t}_{p}"
             em.emit(f"const R {nm} = T[SW(hi{t} - ({p} << D))];")
             vals.append(nm)
         place_hm(em, v, vals, lam, sine, x, 0, LB, rho)
-    mnet_bwd(em, x, 0, LB, rho, lam, sine)
-    for u in range(1, LB):
-        em.emit(f"F[PH(a + {u})] = {x[u]};")
+        mnet_bwd(em, x, 0, LB, rho, lam, sine, cls=t)
+        for u in sorted(x):
+            em.emit(f"F[PH(a + {u})] = {x[u]};")
+        em.emit("}")
+        em.emit('asm volatile("" ::: "memory");  // keep classes apart (register pressure)')
     sig = (f"template <typename R, typename AR, int LOGLB>\n__device__ __forceinline__ void "
            f"hmB_v{v}_lb{LB}_r{rho}_l{lam}(const R* __restrict__ T, R* __restrict__ F, int a, "
            f"const R* __restrict__ tab, int nmax, R base, int N, int D, int r, int dsto)")
@@ -553,6 +569,78 @@ def gen_small_full(v, HP, lam, nlog):
     return sig + " {\n" + "\n".join(em.lines) + "\n}\n"
 
 
+# --------------------------------------------- chain recombination (phase F)
+def gen_recomb(W, HW, lam, special):
+    """SplitTimeParity recombination Dct/Dst(n), n = 2W .. 2 W HW (= N), for
+    the thread owning k in [1, W/2): cells j*W + k (j < HW) and j*W - k
+    (1 <= j <= HW), closed under every level (pairs (y, n/2 - y), y < n/4).
+    special: the multiples of W/2 (k = 0 class).  Buffer padded by 1 per 32:
+    phys(y) = y + y/32; for W = 64, j*W + k -> j*66 + k, j*W - k -> j*66 - 1 - k."""
+    em = Emitter()
+    N = 2 * W * HW
+    if not special:
+        cells = [("a", j) for j in range(HW)] + [("b", j) for j in range(1, HW + 1)]
+        def val(c):  # symbolic (jW, sign)
+            return (c[1] * W, 1 if c[0] == "a" else -1)
+        name = {c: f"{c[0]}{c[1]}" for c in cells}
+        assert W == 64
+        em.emit("R* __restrict__ pa = F + k;")
+        em.emit("R* __restrict__ pb = F - 1 - k;")
+        for c in cells:
+            off = c[1] * 66
+            em.emit(f"R {name[c]} = {'pa' if c[0] == 'a' else 'pb'}[{off}];")
+        n = 2 * W
+        while n <= N:
+            m = n // (2 * W)          # n/4 = m W/2
+            for c in cells:
+                jW, sg = val(c)
+                j = c[1]
+                lower = (2 * j < m) if sg > 0 else (2 * j <= m)
+                if not lower:
+                    continue
+                # partner n/2 - y
+                pj = n // (2 * W) - j
+                pc = ("b", pj) if sg > 0 else ("a", pj)
+                e, o = name[c], name[pc]
+                em.tmp += 1
+                t = em.tmp
+                if lam == 0:
+                    em.emit(f"{{ const R e{t} = {e}; {e} = {add('e' + str(t), o)}; {o} = {sub('e' + str(t), o)}; }}")
+                else:
+                    em.emit(f"{{ const R e{t} = {e}; {e} = {add(o, 'e' + str(t))}; {o} = {sub(o, 'e' + str(t))}; }}")
+            n *= 2
+        for c in cells:
+            off = c[1] * 66
+            em.emit(f"{'pa' if c[0] == 'a' else 'pb'}[{off}] = {name[c]};")
+        sig = (f"template <typename R, typename AR>\n__device__ __forceinline__ void "
+               f"recomb_w{W}_hw{HW}_l{lam}(R* __restrict__ F, int k)")
+    else:
+        hw2 = W // 2
+        ys = [i * hw2 for i in range(0, 2 * HW + 1)]
+        if lam == 1:
+            ys = [y for y in ys if 1 <= y <= N // 2 - 1]
+        name = {y: f"s{y}" for y in ys}
+        for y in ys:
+            em.emit(f"R s{y} = F[{y + (y >> 5)}];")
+        n = 2 * W
+        while n <= N:
+            for y in ys:
+                if y < n // 4 and (lam == 0 or y >= 1):
+                    e, o = name[y], name[n // 2 - y]
+                    em.tmp += 1
+                    t = em.tmp
+                    if lam == 0:
+                        em.emit(f"{{ const R e{t} = {e}; {e} = {add('e' + str(t), o)}; {o} = {sub('e' + str(t), o)}; }}")
+                    else:
+                        em.emit(f"{{ const R e{t} = {e}; {e} = {add(o, 'e' + str(t))}; {o} = {sub(o, 'e' + str(t))}; }}")
+            n *= 2
+        for y in ys:
+            em.emit(f"F[{y + (y >> 5)}] = s{y};")
+        sig = (f"template <typename R, typename AR>\n__device__ __forceinline__ void "
+               f"recombsp_w{W}_hw{HW}_l{lam}(R* __restrict__ F)")
+    return sig + " {\n" + "\n".join(em.lines) + "\n}\n"
+
+
 # (LB, nlog) pairs of the fused kernels: LT = nlog - 1 - log2(LB), HP = 2^LT
 FULL_SIZES = [(64, 10), (64, 11), (64, 12), (64, 13)]
 
@@ -570,7 +658,7 @@ def main():
         "// Straight-line bottom-of-recursion code for the fused AM-QFT kernels.",
         "#pragma once",
         "#define PH(i) ((i) + ((i) >> LOGLB))",
-        "#define SW(i) ((i) ^ (((i) >> 5) & 31))",
+        "#define SW(i) ((i) + ((i) >> 5))",
         "namespace amqft_b200 {",
         "namespace gen {",
     ]
@@ -597,7 +685,28 @@ def main():
         for v in range(1, 9):
             for lam in (0, 1):
                 out.append(gen_small_full(v, HP, lam, nlog))
+    for LB, nlog in FULL_SIZES:
+        N = 1 << nlog
+        W = N // LB
+        HW = (N // 2) // W
+        if W == 64:
+            for lam in (0, 1):
+                out.append(gen_recomb(W, HW, lam, False))
+                out.append(gen_recomb(W, HW, lam, True))
     out.append("}  // namespace gen")
+    out.append("template <int W, int HW> struct Recomb;")
+    for LB, nlog in FULL_SIZES:
+        N = 1 << nlog
+        W = N // LB
+        HW = (N // 2) // W
+        if W == 64:
+            out.append(f"template <> struct Recomb<{W}, {HW}> {{")
+            out.append("  template <typename R, typename AR>")
+            out.append("  static __device__ __forceinline__ void run(int lam, R* F, int k) {")
+            out.append(f"    if (k == 0) {{ if (lam == 0) gen::recombsp_w{W}_hw{HW}_l0<R, AR>(F); else gen::recombsp_w{W}_hw{HW}_l1<R, AR>(F); }}")
+            out.append(f"    else {{ if (lam == 0) gen::recomb_w{W}_hw{HW}_l0<R, AR>(F, k); else gen::recomb_w{W}_hw{HW}_l1<R, AR>(F, k); }}")
+            out.append("  }")
+            out.append("};")
     out.append("template <int LB, int LT, int NLOG, int SINE> struct Top;")
     for LB, nlog in FULL_SIZES:
         LT = nlog - 1 - (LB.bit_length() - 1)

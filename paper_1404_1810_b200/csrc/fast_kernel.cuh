@@ -57,16 +57,19 @@ struct Cfg {
   static constexpr int NT = NT0 < 128 ? 128 : NT0;
   // chain stride: holds the skewed (H + H/LB + 1) and the swizzled
   // (32-aligned blocks up to H) layouts; +16 staggers the chains' banks.
-  static constexpr int CS = ((H + HP + 1 > H + 32 ? H + HP + 1 : H + 32) + 31) / 32 * 32 + 16;
+  static constexpr int CS = ((H + HP + 1 > H + H / 32 + 1 ? H + HP + 1 : H + H / 32 + 1) + 31) / 32 * 32 + 16;
   static constexpr bool TM = (V == 1 || V == 4 || V == 5 || V == 8);
   static constexpr int SINE = V >= 5 ? 1 : 0;
   static constexpr bool CHAIN = (V == 1 || V == 5 || V == 3 || V == 7);
-  static constexpr size_t SMEM = 8 * CS * sizeof(R);
+  // T, F (4 chains each) + the TMA staging buffer for the next row + mbarrier
+  static constexpr size_t STAGE_OFF = 8 * CS * sizeof(R);
+  static constexpr size_t SMEM = STAGE_OFF + 2 * N * sizeof(R) + 16;
   // Bank-conflict layouts: skew (i + i/LB) on the buffer holding the
   // index-space mirror network (T for time-major, F for harmonic-major);
-  // XOR swizzle (i ^ (i/32 mod 32)) on the other one (strided class runs).
+  // one pad word per 32 (i + i/32) on the other one (per-lane class runs,
+  // recombination sets j*64 +- k at immediate offsets).
   static __device__ __forceinline__ int skew(int i) { return i + (i >> LOGLB); }
-  static __device__ __forceinline__ int swz(int i) { return i ^ ((i >> 5) & 31); }
+  static __device__ __forceinline__ int swz(int i) { return i + (i >> 5); }
   static __device__ __forceinline__ int pt(int i) { return TM ? skew(i) : swz(i); }
   static __device__ __forceinline__ int pf(int i) { return TM ? swz(i) : skew(i); }
 };
@@ -203,50 +206,55 @@ __device__ __forceinline__ void am_levels_asc(R* B) {  // 0 .. D-1
 // cell(p) = hi - p).  Halo values cross lanes with warp shuffles; the last
 // lane of a block takes the class-end copy, so segment boundaries inside a
 // warp never consume foreign data.
+template <class C, bool BWD, int LAM, int D>
+struct AmPos {
+  static constexpr int V = C::V_;
+  static constexpr int RR = C::N / 128;
+  static constexpr int S = 2 << D;
+  // low bits of the block position p = i*RR + l are those of l (S <= RR)
+  static constexpr int lens(int l) { return (C::SINE && D > 0) ? ((l >> (D - 1)) & 1) : LAM; }
+  static constexpr bool is_o(int l) { return ((l >> D) & 1) == 1 - lens(l); }
+  static constexpr bool right(int l) {
+    return BWD ? ((V == 4) ? (lens(l) == 0) : (lens(l) == 1))    // AM_B M4 / M8
+               : ((V == 2) ? (lens(l) == 1) : (lens(l) == 0));   // AM_F M2 / M6
+  }
+};
+
 template <class C, typename R, bool BWD, int LAM, int D>
 __device__ __forceinline__ void am_depth(R (&x)[C::N / 128], bool last_lane, bool first_lane,
                                          bool blk_ok) {
   using A = Arith<R>;
-  constexpr int V = C::V_;
-  constexpr int RR = C::N / 128;
-  constexpr int S = 2 << D;
+  using P = AmPos<C, BWD, LAM, D>;
+  constexpr int RR = P::RR, S = P::S;
+  constexpr bool ADD = BWD ? (C::V_ == 4) : (C::V_ == 2);
   static_assert(S <= RR, "class stride must fit a lane's run");
+  // 1) halos (pre-update values of the neighbour lane), only the ones used
   R hr[S], hl[S];
 #pragma unroll
-  for (int h = 0; h < S; ++h) {
-    hr[h] = __shfl_down_sync(0xffffffffu, x[h], 1);
-    hl[h] = __shfl_up_sync(0xffffffffu, x[RR - 1 - h], 1);
-  }
-  R y[RR];
+  for (int l = RR - S; l < RR; ++l)
+    if (P::is_o(l) && P::right(l)) hr[l + S - RR] = __shfl_down_sync(0xffffffffu, x[l + S - RR], 1);
+#pragma unroll
+  for (int l = 0; l < S; ++l)
+    if (P::is_o(l) && !P::right(l)) hl[l] = __shfl_up_sync(0xffffffffu, x[l - S + RR], 1);
+  if (!blk_ok) return;
+  // 2) right-halo ops ascending, left-halo ops descending: in place, every
+  //    neighbour read happens before that neighbour is updated.
 #pragma unroll
   for (int l = 0; l < RR; ++l) {
-    // low bits of the block position p = i*RR + l are those of l (S <= RR)
-    const int obit = (l >> D) & 1;
-    const int lens = (C::SINE && D > 0) ? ((l >> (D - 1)) & 1) : LAM;
-    const bool is_o = obit == 1 - lens;
-    y[l] = x[l];
-    if (!is_o) continue;
-    bool right;
-    if (BWD) right = (V == 4) ? (lens == 0) : (lens == 1);   // AM_B M4 / M8
-    else right = (V == 2) ? (lens == 1) : (lens == 0);       // AM_F M2 / M6
+    if (!(P::is_o(l) && P::right(l))) continue;
     const R cj = x[l];
-    R cn;
-    bool edge;
-    if (right) {
-      cn = (l + S < RR) ? x[l + S] : hr[l + S - RR];
-      edge = (l + S >= RR) && last_lane;     // class end: copy
-    } else {
-      cn = (l - S >= 0) ? x[l - S] : hl[S - 1 - l];
-      edge = (l - S < 0) && first_lane;      // class start: copy
-    }
-    R o;
-    const bool addop = BWD ? (V == 4) : (V == 2);
-    if (addop) o = A::add(cj, cn);
-    else o = right ? (BWD ? A::sub(cj, cn) : A::sub(cj, cn)) : A::sub(cj, cn);
-    y[l] = (edge || !blk_ok) ? cj : o;
+    const R cn = (l + S < RR) ? x[(l + S) % RR] : hr[(l + S) % RR];
+    const R o = ADD ? A::add(cj, cn) : A::sub(cj, cn);
+    x[l] = (l + S >= RR && last_lane) ? cj : o;     // class end: copy
   }
 #pragma unroll
-  for (int l = 0; l < RR; ++l) x[l] = y[l];
+  for (int l = RR - 1; l >= 0; --l) {
+    if (!(P::is_o(l) && !P::right(l))) continue;
+    const R cj = x[l];
+    const R cn = (l - S >= 0) ? x[(l - S + RR) % RR] : hl[l % S];
+    const R o = ADD ? A::add(cj, cn) : A::sub(cj, cn);
+    x[l] = (l - S < 0 && first_lane) ? cj : o;      // class start: copy
+  }
 }
 
 template <class C, typename R, bool BWD, int LAM>
@@ -307,6 +315,34 @@ __device__ __forceinline__ void am_phase_regs(R* B) {
   }
 }
 
+// ---- TMA bulk staging of the next row (cp.async.bulk + mbarrier).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+               ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}"
+      ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
 #ifdef AMQFT_PHASE_TIMING
 // Instrumented build only (tools/phase_timing): CTA 0 accumulates the
 // cycles spent between phase boundaries.
@@ -324,7 +360,10 @@ __device__ unsigned long long g_phase_cycles[16];
 #endif
 
 template <int V, typename R, int LOGN, int LOGLB>
-__global__ void __launch_bounds__(Cfg<V, R, LOGN, LOGLB>::NT, (sizeof(R) == 4 ? 2 : 1))
+#ifndef AMQFT_FAST_MINB
+#define AMQFT_FAST_MINB 2
+#endif
+__global__ void __launch_bounds__(Cfg<V, R, LOGN, LOGLB>::NT, (sizeof(R) == 4 ? AMQFT_FAST_MINB : 1))
 k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
        const R* __restrict__ tab, int nmax, int inverse, R scale) {
 #ifdef AMQFT_PHASE_TIMING
@@ -336,14 +375,27 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
   extern __shared__ __align__(16) unsigned char smraw[];
   R* Tb = reinterpret_cast<R*>(smraw);
   R* Fb = Tb + 4 * C::CS;
+  R* Sb = reinterpret_cast<R*>(smraw + C::STAGE_OFF);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + C::STAGE_OFF + 2 * C::N * sizeof(R));
   const int tid = threadIdx.x;
   const R base = __ldg(tab + (nmax / 4 - 1));
   constexpr int N = C::N, H = C::H;
+  constexpr uint32_t ROW_BYTES = 2 * N * sizeof(R);
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0 && blockIdx.x < rows) tma_load_1d(Sb, in + blockIdx.x * 2 * N, ROW_BYTES, bar);
+  uint32_t parity = 0;
 
   for (size_t row = blockIdx.x; row < rows; row += gridDim.x) {
     PHASE_MARK(0);
     // ---- load: SplitComplex (elab.cpp:152-155) + SplitReal (185-197)
-    const V2* x = reinterpret_cast<const V2*>(in + row * 2 * N);
+    // from the TMA-staged row; then prefetch the CTA's next row.
+    mbar_wait(bar, parity);
+    parity ^= 1;
+    const V2* x = reinterpret_cast<const V2*>(Sb);
     for (int m = tid; m <= H; m += C::NT) {
       V2 a = x[m];
       if (inverse) { const R tmp = a.x; a.x = a.y; a.y = tmp; }
@@ -360,6 +412,10 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       }
     }
     __syncthreads();
+    if (tid == 0 && row + gridDim.x < rows) {
+      fence_proxy_async();
+      tma_load_1d(Sb, in + (row + gridDim.x) * 2 * N, ROW_BYTES, bar);
+    }
     PHASE_MARK(1);
 
     if constexpr (C::TM) {
@@ -416,10 +472,16 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
         __syncthreads();
       }
       PHASE_MARK(4);
-#pragma unroll 1
-      for (int n = 2 * (N / C::LB); n <= N; n <<= 1) {
-        chain_level<C, R, false>(Fb, n);
+      if constexpr (N / C::LB == 64) {
+        // generated: each thread owns the 64 cells j*64 +- k of its chain
+        if (tid < 128) Recomb<64, H / 64>::template run<R, A>((tid >> 5) & 1, Fb + (tid >> 5) * C::CS, tid & 31);
         __syncthreads();
+      } else {
+#pragma unroll 1
+        for (int n = 2 * (N / C::LB); n <= N; n <<= 1) {
+          chain_level<C, R, false>(Fb, n);
+          __syncthreads();
+        }
       }
     } else {
       if (tid < 4 * C::LB) {

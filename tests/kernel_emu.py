@@ -35,12 +35,13 @@ def lib():
         L.host_top.argtypes = [i, i, i, i, i, i, dp, i, dp, d]
         L.host_bottom.argtypes = [i, i, i, i, dp, dp, i, dp, i, d, i, i, i, i]
         L.host_small.argtypes = [i, i, i, i, i, dp, dp, dp, d]
+        L.host_recomb.argtypes = [i, i, i, dp, i]
         _lib = L
     return _lib
 
 
 def _swz(i):
-    return i ^ ((i >> 5) & 31)
+    return i + (i >> 5)
 
 
 def _par(x):
@@ -161,11 +162,11 @@ def emulate(v, N, LB, x, tab, base):
     HP = H // LB
     NSEG = 4 * HP
     NT = max(4 * LB, NSEG, 128)
-    CS = (max(H + HP + 1, H + 32) + 31) // 32 * 32 + 16
+    CS = (max(H + HP + 1, H + H // 32 + 1) + 31) // 32 * 32 + 16
     TM = v in (1, 4, 5, 8)
     SINE = 1 if v >= 5 else 0
     skew = lambda i: i + (i >> LOGLB)  # noqa: E731
-    swz = lambda i: i ^ ((i >> 5) & 31)  # noqa: E731
+    swz = lambda i: i + (i >> 5)  # noqa: E731
     pt = skew if TM else swz
     pf = swz if TM else skew
     T = np.zeros(4 * CS + 8)
@@ -218,10 +219,15 @@ def emulate(v, N, LB, x, tab, base):
                 _am_level(F, CS, N, LOGLB, depth, v, SINE, True)
         else:
             am_phase_regs(F, CS, N, LOGLB, LT, v, SINE, True)
-        n = 2 * (N // LB)
-        while n <= N:
-            _chain_level(F, CS, n, False)
-            n <<= 1
+        if N // LB == 64:
+            for c in range(4):
+                for k in range(32):
+                    assert L.host_recomb(64, H // 64, c & 1, Fp + 8 * c * CS, k) == 0
+        else:
+            n = 2 * (N // LB)
+            while n <= N:
+                _chain_level(F, CS, n, False)
+                n <<= 1
     else:
         for c in range(4):
             for vv in range(1, LB):

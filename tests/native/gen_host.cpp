@@ -90,4 +90,9 @@ int host_small(int V, int HP, int nlog, int LB, int lam, const double* T, double
   return -1;
 }
 
+int host_recomb(int W, int HW, int lam, double* F, int k) {
+  if (W == 64 && HW == 32) { Recomb<64, 32>::run<double, HA>(lam, F, k); return 0; }
+  return -1;
+}
+
 }  // extern "C"

@@ -3,6 +3,9 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -shared -Xcompiler -fPIC \
 //        -o tools/libphase_timing.so tools/phase_timing.cu
 #define AMQFT_PHASE_TIMING
+#ifndef AMQFT_FAST_MINB
+#define AMQFT_FAST_MINB 2
+#endif
 #include "../paper_1404_1810_b200/csrc/fast_kernel.cuh"
 
 using namespace amqft_b200::fastk;

@@ -7,7 +7,7 @@ import numpy as np
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-lib = C.CDLL(os.path.join(HERE, "libphase_timing.so"))
+lib = C.CDLL(os.path.join(HERE, os.environ.get("PT_LIB", "libphase_timing.so")))
 lib.pt_run.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_int,
                        C.c_void_p, C.c_int]
 N = 4096
@@ -24,7 +24,7 @@ for v in [int(a) for a in sys.argv[1:]] or [4]:
     x = torch.randn(rows, 2 * N, device="cuda")
     y = torch.empty_like(x)
     cyc = (C.c_ulonglong * 16)()
-    grid = 148 * 2
+    grid = 148 * int(os.environ.get("PT_CTAS", "2"))
     for _ in range(2):
         rc = lib.pt_run(v, x.data_ptr(), y.data_ptr(), rows, dtab.data_ptr(), N, cyc, grid)
     per = rows / grid
