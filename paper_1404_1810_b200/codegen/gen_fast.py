@@ -155,29 +155,40 @@ def spectrum_tm(em, v, x, a, L, rho, lens, sine, tcls):
     return interleave(lens, E, O)
 
 
+def store_off(p):
+    """Offset of F[SW(hi - p*2^D)] from F[SW(hi)] for compile-time D >= 5:
+    SW(hi - 32m) = SW(hi) - 33m  (SW(i) = i + i/32)."""
+    return f"-({p} * ((1 << D) + (1 << (D >= 5 ? D - 5 : 0))))"
+
+
 def gen_tmB(v, LB, rho, lam):
     """Class by class: mirror folds never mix trailing-zero classes
     (tz(v) == tz(L - v)), so each class is loaded, transformed and stored
-    on its own -- small live register set."""
+    on its own -- small live register set.  Addresses are immediate offsets
+    from two per-thread bases (segment start in T, class top in F)."""
     sine = 1 if v >= 5 else 0
     lg = LB.bit_length() - 1
     em = Emitter()
+    em.emit("const R* __restrict__ Tp = T + a + (a >> LOGLB);")
+    em.emit("const int swsh = dsto ? 0 : 31;")
     for t in range(lg):
         x = {}
         for u in range(1, LB):
             if tz(u) == t:
-                em.emit(f"const R x{u} = T[PH(a + {u})];")
+                em.emit(f"const R x{u} = Tp[{u}];")
                 x[u] = f"x{u}"
         mnet_fwd(em, x, 0, LB, rho, lam, sine, cls=t)
         sp = spectrum_tm(em, v, x, 0, LB, rho, lam, sine, t)
         em.emit(f"{{ const int hi = (N >> {t + 1}) - dsto - r;")
+        em.emit("  R* __restrict__ Fq = F + SW(hi);")
         for p, name in enumerate(sp):
-            em.emit(f"  F[SW(hi - ({p} << D))] = {name};")
+            em.emit(f"  if constexpr (D >= 5) Fq[{store_off(p)}] = {name}; "
+                    f"else F[SW(hi - ({p} << D))] = {name};")
         em.emit("}")
         em.emit('asm volatile("" ::: "memory");  // keep classes apart (register pressure)')
-    sig = (f"template <typename R, typename AR, int LOGLB>\n__device__ __forceinline__ void "
+    sig = (f"template <typename R, typename AR, int LOGLB, int D>\n__device__ __forceinline__ void "
            f"tmB_v{v}_lb{LB}_r{rho}_l{lam}(const R* __restrict__ T, R* __restrict__ F, int a, "
-           f"const R* __restrict__ tab, int nmax, R base, int N, int D, int r, int dsto)")
+           f"const R* __restrict__ tab, int nmax, R base, int N, int r, int dsto)")
     return sig + " {\n" + "\n".join(em.lines) + "\n}\n"
 
 
@@ -311,24 +322,27 @@ def gen_hmB(v, LB, rho, lam):
     sine = 1 if v >= 5 else 0
     lg = LB.bit_length() - 1
     em = Emitter()
+    em.emit("R* __restrict__ Fp = F + a + (a >> LOGLB);")
+    em.emit("const int swsh = dsto ? 0 : 31;")
     for t in range(lg):
         x = {}
         cnt = LB >> (t + 1)
         em.emit(f"{{ const int hi{t} = (N >> {t + 1}) - dsto - r;")
+        em.emit(f"  const R* __restrict__ Tq = T + SW(hi{t});")
         vals = []
         for p in range(cnt):
             nm = f"v{t}_{p}"
-            em.emit(f"const R {nm} = T[SW(hi{t} - ({p} << D))];")
+            em.emit(f"const R {nm} = (D >= 5) ? Tq[{store_off(p)}] : T[SW(hi{t} - ({p} << D))];")
             vals.append(nm)
         place_hm(em, v, vals, lam, sine, x, 0, LB, rho)
         mnet_bwd(em, x, 0, LB, rho, lam, sine, cls=t)
         for u in sorted(x):
-            em.emit(f"F[PH(a + {u})] = {x[u]};")
+            em.emit(f"Fp[{u}] = {x[u]};")
         em.emit("}")
         em.emit('asm volatile("" ::: "memory");  // keep classes apart (register pressure)')
-    sig = (f"template <typename R, typename AR, int LOGLB>\n__device__ __forceinline__ void "
+    sig = (f"template <typename R, typename AR, int LOGLB, int D>\n__device__ __forceinline__ void "
            f"hmB_v{v}_lb{LB}_r{rho}_l{lam}(const R* __restrict__ T, R* __restrict__ F, int a, "
-           f"const R* __restrict__ tab, int nmax, R base, int N, int D, int r, int dsto)")
+           f"const R* __restrict__ tab, int nmax, R base, int N, int r, int dsto)")
     return sig + " {\n" + "\n".join(em.lines) + "\n}\n"
 
 
@@ -504,6 +518,7 @@ def gen_small_full(v, HP, lam, nlog):
     network) + backward (tmS); harmonic-major = hmS + scaled backward."""
     sine = 1 if v >= 5 else 0
     em = Emitter()
+    em.emit(f"constexpr int swsh = {0 if lam else 31};")
     ks = range(0, HP + 1) if lam == 0 else range(1, HP)
     if v in TM:
         y = {}
@@ -584,8 +599,13 @@ def gen_recomb(W, HW, lam, special):
             return (c[1] * W, 1 if c[0] == "a" else -1)
         name = {c: f"{c[0]}{c[1]}" for c in cells}
         assert W == 64
-        em.emit("R* __restrict__ pa = F + k;")
-        em.emit("R* __restrict__ pb = F - 1 - k;")
+        # phys(y) = y + (y + sh)/32, sh = 31 (Dct chain) / 0 (Dst chain)
+        if lam == 0:
+            em.emit("R* __restrict__ pa = F + 1 + k;")
+            em.emit("R* __restrict__ pb = F - k;")
+        else:
+            em.emit("R* __restrict__ pa = F + k;")
+            em.emit("R* __restrict__ pb = F - 1 - k;")
         for c in cells:
             off = c[1] * 66
             em.emit(f"R {name[c]} = {'pa' if c[0] == 'a' else 'pb'}[{off}];")
@@ -620,8 +640,9 @@ def gen_recomb(W, HW, lam, special):
         if lam == 1:
             ys = [y for y in ys if 1 <= y <= N // 2 - 1]
         name = {y: f"s{y}" for y in ys}
+        sh = 31 if lam == 0 else 0
         for y in ys:
-            em.emit(f"R s{y} = F[{y + (y >> 5)}];")
+            em.emit(f"R s{y} = F[{y + ((y + sh) >> 5)}];")
         n = 2 * W
         while n <= N:
             for y in ys:
@@ -635,7 +656,7 @@ def gen_recomb(W, HW, lam, special):
                         em.emit(f"{{ const R e{t} = {e}; {e} = {add(o, 'e' + str(t))}; {o} = {sub(o, 'e' + str(t))}; }}")
             n *= 2
         for y in ys:
-            em.emit(f"F[{y + (y >> 5)}] = s{y};")
+            em.emit(f"F[{y + ((y + sh) >> 5)}] = s{y};")
         sig = (f"template <typename R, typename AR>\n__device__ __forceinline__ void "
                f"recombsp_w{W}_hw{HW}_l{lam}(R* __restrict__ F)")
     return sig + " {\n" + "\n".join(em.lines) + "\n}\n"
@@ -658,7 +679,7 @@ def main():
         "// Straight-line bottom-of-recursion code for the fused AM-QFT kernels.",
         "#pragma once",
         "#define PH(i) ((i) + ((i) >> LOGLB))",
-        "#define SW(i) ((i) + ((i) >> 5))",
+        "#define SW(i) ((i) + (((i) + swsh) >> 5))",
         "namespace amqft_b200 {",
         "namespace gen {",
     ]
@@ -737,13 +758,13 @@ def main():
         for v in range(1, 9):
             fam = "tmB" if v in TM else "hmB"
             out.append(f"template <> struct Bottom<{v}, {LB}> {{")
-            out.append("  template <typename R, typename AR, int LOGLB>")
+            out.append("  template <typename R, typename AR, int LOGLB, int D>")
             out.append("  static __device__ __forceinline__ void run(int rho, int lens, const R* T, R* F, int a, "
-                       "const R* tab, int nmax, R base, int N, int D, int r, int dsto) {")
+                       "const R* tab, int nmax, R base, int N, int r, int dsto) {")
             for rho in (0, 1):
                 for lam in (0, 1):
                     out.append(f"    if (rho == {rho} && lens == {lam}) {{ gen::{fam}_v{v}_lb{LB}_r{rho}_l{lam}"
-                               f"<R, AR, LOGLB>(T, F, a, tab, nmax, base, N, D, r, dsto); return; }}")
+                               f"<R, AR, LOGLB, D>(T, F, a, tab, nmax, base, N, r, dsto); return; }}")
             out.append("  }")
             out.append("};")
     out.append("template <int V, int HP> struct Small;")

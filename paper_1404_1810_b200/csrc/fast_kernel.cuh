@@ -68,10 +68,12 @@ struct Cfg {
   // index-space mirror network (T for time-major, F for harmonic-major);
   // one pad word per 32 (i + i/32) on the other one (per-lane class runs,
   // recombination sets j*64 +- k at immediate offsets).
+  // The pad is shifted per chain (31 for Dct chains, 0 for Dst chains) so
+  // every lane's 32-cell class run lies inside one padded block.
   static __device__ __forceinline__ int skew(int i) { return i + (i >> LOGLB); }
-  static __device__ __forceinline__ int swz(int i) { return i + (i >> 5); }
-  static __device__ __forceinline__ int pt(int i) { return TM ? skew(i) : swz(i); }
-  static __device__ __forceinline__ int pf(int i) { return TM ? swz(i) : skew(i); }
+  static __device__ __forceinline__ int swz(int i, int lam) { return i + ((i + (lam ? 0 : 31)) >> 5); }
+  static __device__ __forceinline__ int pt(int i, int lam) { return TM ? skew(i) : swz(i, lam); }
+  static __device__ __forceinline__ int pf(int i, int lam) { return TM ? swz(i, lam) : skew(i); }
 };
 
 // Segment parameters at depth d: orientation, lens, residue (fast_model.segment_params).
@@ -103,7 +105,7 @@ __device__ __forceinline__ void chain_level(R* B, int n) {
     const int lam = c & 1;
     if (lam && k == 0) continue;
     R* ch = B + c * C::CS;
-    const int i0 = C::swz(k), i1 = C::swz((n >> 1) - k);
+    const int i0 = C::swz(k, lam), i1 = C::swz((n >> 1) - k, lam);
     const R e = ch[i0], o = ch[i1];
     if (!FWD) {  // elaborations.cpp:310-329
       ch[i0] = lam ? A::add(o, e) : A::add(e, o);
@@ -128,7 +130,7 @@ __device__ __forceinline__ void chain_class(R* ch, int lam_c, int t, int r) {
   const int rO = r + ((1 - lens) << DEPTH);
   const int hi = (C::N >> (t + 1)) - lam_c;
   const int c0 = hi - rO;
-  auto at = [&](int jj) -> R& { return ch[C::swz(c0 - jj * stride)]; };
+  auto at = [&](int jj) -> R& { return ch[C::swz(c0 - jj * stride, lam_c)]; };
   if (C::TM) {
     // M1: cos asc/sub, sin desc/sub; M5: cos desc/add, sin asc/add
     const bool addop = V == 5;
@@ -301,17 +303,18 @@ __device__ __forceinline__ void am_phase_regs(R* B) {
   const int lam_c = c & 1;
   const int Mt = C::N >> (tt + 2);
   const int nl = 32 >> tt;                       // lanes of this block
-  R* chb = B + (c & 3) * C::CS;
   const int cell0 = (C::N >> (tt + 1)) - lam_c - (i << LOGR);
+  // runs end on a padded-block boundary: phys(cell0 - l) = phys(cell0) - l - l/32
+  R* chb = B + (c & 3) * C::CS + C::swz(cell0, lam_c);
   R x[RR];
 #pragma unroll
-  for (int l = 0; l < RR; ++l) x[l] = active ? chb[C::swz(cell0 - l)] : R(0);
+  for (int l = 0; l < RR; ++l) x[l] = active ? chb[-(l + (l >> 5))] : R(0);
   const bool last_lane = i == nl - 1, first_lane = i == 0;
   if (lam_c) am_depths<C, R, BWD, 1>(x, last_lane, first_lane, Mt);
   else am_depths<C, R, BWD, 0>(x, last_lane, first_lane, Mt);
   if (active) {
 #pragma unroll
-    for (int l = 0; l < RR; ++l) chb[C::swz(cell0 - l)] = x[l];
+    for (int l = 0; l < RR; ++l) chb[-(l + (l >> 5))] = x[l];
   }
 }
 
@@ -400,15 +403,15 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       V2 a = x[m];
       if (inverse) { const R tmp = a.x; a.x = a.y; a.y = tmp; }
       if (m == 0 || m == H) {
-        Tb[0 * C::CS + C::pt(m)] = a.x;
-        Tb[2 * C::CS + C::pt(m)] = a.y;
+        Tb[0 * C::CS + C::pt(m, 0)] = a.x;
+        Tb[2 * C::CS + C::pt(m, 0)] = a.y;
       } else {
         V2 b = x[N - m];
         if (inverse) { const R tmp = b.x; b.x = b.y; b.y = tmp; }
-        Tb[0 * C::CS + C::pt(m)] = A::add(a.x, b.x);
-        Tb[1 * C::CS + C::pt(m)] = A::sub(a.x, b.x);
-        Tb[2 * C::CS + C::pt(m)] = A::add(a.y, b.y);
-        Tb[3 * C::CS + C::pt(m)] = A::sub(a.y, b.y);
+        Tb[0 * C::CS + C::pt(m, 0)] = A::add(a.x, b.x);
+        Tb[1 * C::CS + C::pt(m, 1)] = A::sub(a.x, b.x);
+        Tb[2 * C::CS + C::pt(m, 0)] = A::add(a.y, b.y);
+        Tb[3 * C::CS + C::pt(m, 1)] = A::sub(a.y, b.y);
       }
     }
     __syncthreads();
@@ -451,9 +454,8 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       const int s = 2 * h + rho_bit;
       int rho, lens, r;
       seg_params<C::SINE>(lam_bit, s, C::LT, &rho, &lens, &r);
-      Bottom<V, C::LB>::template run<R, A, LOGLB>(rho, lens, Tb + c * C::CS, Fb + c * C::CS,
-                                                  s * C::LB, tab, nmax, base, N, C::LT, r,
-                                                  lam_bit);
+      Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT>(rho, lens, Tb + c * C::CS, Fb + c * C::CS,
+                                                         s * C::LB, tab, nmax, base, N, r, lam_bit);
     }
     if constexpr (!C::TM) {
       if (tid >= C::NT - 4) {
@@ -495,16 +497,16 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
     // ---- store: SplitReal bwd (elab.cpp:199-208) + SplitComplex bwd (162-183)
     V2* y = reinterpret_cast<V2*>(out + row * 2 * N);
     for (int k = tid; k <= H; k += C::NT) {
-      const R rd = Fb[0 * C::CS + C::pf(k)];
-      const R id = Fb[2 * C::CS + C::pf(k)];
+      const R rd = Fb[0 * C::CS + C::pf(k, 0)];
+      const R id = Fb[2 * C::CS + C::pf(k, 0)];
       V2 lo, hi;
       if (k == 0 || k == H) {
         lo.x = rd;
         lo.y = id;
         hi = lo;
       } else {
-        const R rs = Fb[1 * C::CS + C::pf(k)];
-        const R is = Fb[3 * C::CS + C::pf(k)];
+        const R rs = Fb[1 * C::CS + C::pf(k, 1)];
+        const R is = Fb[3 * C::CS + C::pf(k, 1)];
         lo.x = A::add(rd, is);
         lo.y = A::sub(id, rs);
         hi.x = A::sub(rd, is);

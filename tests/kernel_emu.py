@@ -40,8 +40,8 @@ def lib():
     return _lib
 
 
-def _swz(i):
-    return i + (i >> 5)
+def _swz(i, lam):
+    return i + ((i + (0 if lam else 31)) >> 5)
 
 
 def _par(x):
@@ -76,7 +76,7 @@ def _am_level(B, CS, N, LOGLB, depth, v, sine, tm):
             for r in range(1 << depth):
                 lens = ((r >> (depth - 1)) & 1) if (sine and depth > 0) else lam_c
                 rO = r + ((1 - lens) << depth)
-                cells = [c * CS + _swz(hi - rO - j * stride) for j in range(q)]
+                cells = [c * CS + _swz(hi - rO - j * stride, lam_c) for j in range(q)]
                 Cv = [B[p] for p in cells]
                 if chain:
                     out = _chain(v, tm, lens, Cv)
@@ -145,7 +145,7 @@ def _chain_level(B, CS, n, fwd):
         for k in range(q):
             if lam and k == 0:
                 continue
-            i0, i1 = c * CS + _swz(k), c * CS + _swz((n >> 1) - k)
+            i0, i1 = c * CS + _swz(k, lam), c * CS + _swz((n >> 1) - k, lam)
             e, o = B[i0], B[i1]
             if not fwd:
                 B[i0], B[i1] = (o + e, o - e) if lam else (e + o, e - o)
@@ -166,9 +166,8 @@ def emulate(v, N, LB, x, tab, base):
     TM = v in (1, 4, 5, 8)
     SINE = 1 if v >= 5 else 0
     skew = lambda i: i + (i >> LOGLB)  # noqa: E731
-    swz = lambda i: i + (i >> 5)  # noqa: E731
-    pt = skew if TM else swz
-    pf = swz if TM else skew
+    pt = (lambda i, lam: skew(i)) if TM else _swz
+    pf = _swz if TM else (lambda i, lam: skew(i))
     T = np.zeros(4 * CS + 8)
     F = np.zeros(4 * CS + 8)
     tab = np.ascontiguousarray(tab, dtype=np.float64)
@@ -178,13 +177,13 @@ def emulate(v, N, LB, x, tab, base):
     re, im = x[0::2], x[1::2]
     for m in range(H + 1):
         if m in (0, H):
-            T[0 * CS + pt(m)] = re[m]
-            T[2 * CS + pt(m)] = im[m]
+            T[0 * CS + pt(m, 0)] = re[m]
+            T[2 * CS + pt(m, 0)] = im[m]
         else:
-            T[0 * CS + pt(m)] = re[m] + re[N - m]
-            T[1 * CS + pt(m)] = re[m] - re[N - m]
-            T[2 * CS + pt(m)] = im[m] + im[N - m]
-            T[3 * CS + pt(m)] = im[m] - im[N - m]
+            T[0 * CS + pt(m, 0)] = re[m] + re[N - m]
+            T[1 * CS + pt(m, 1)] = re[m] - re[N - m]
+            T[2 * CS + pt(m, 0)] = im[m] + im[N - m]
+            T[3 * CS + pt(m, 1)] = im[m] - im[N - m]
     if TM:
         for c in range(4):
             for vv in range(1, LB):
@@ -234,11 +233,11 @@ def emulate(v, N, LB, x, tab, base):
                 assert L.host_top(LB, LT, LOGN, SINE, 1, c & 1, Fp + 8 * c * CS, vv, tp, base) == 0
     out = np.zeros(2 * N)
     for k in range(H + 1):
-        rd, idd = F[0 * CS + pf(k)], F[2 * CS + pf(k)]
+        rd, idd = F[0 * CS + pf(k, 0)], F[2 * CS + pf(k, 0)]
         if k in (0, H):
             out[2 * k], out[2 * k + 1] = rd, idd
         else:
-            rs, is_ = F[1 * CS + pf(k)], F[3 * CS + pf(k)]
+            rs, is_ = F[1 * CS + pf(k, 1)], F[3 * CS + pf(k, 1)]
             out[2 * k], out[2 * k + 1] = rd + is_, idd - rs
             out[2 * (N - k)], out[2 * (N - k) + 1] = rd - is_, idd + rs
     return out
@@ -264,7 +263,7 @@ def am_phase_regs(B, CS, N, LOGLB, LT, v, sine, bwd):
     for (warp, lane, c, t, i, active) in lanes:
         lam_c = c & 1
         basep = (N >> (t + 1)) - lam_c - (i << LOGR)
-        X[(warp, lane)] = [B[c * CS + _swz(basep - l)] if active else 0.0 for l in range(RR)]
+        X[(warp, lane)] = [B[c * CS + _swz(basep - l, lam_c)] if active else 0.0 for l in range(RR)]
     depths = list(range(LT - 1, -1, -1)) if bwd else list(range(LT))
     for D in depths:
         S = 2 << D
@@ -310,4 +309,4 @@ def am_phase_regs(B, CS, N, LOGLB, LT, v, sine, bwd):
         lam_c = c & 1
         basep = (N >> (t + 1)) - lam_c - (i << LOGR)
         for l in range(RR):
-            B[c * CS + _swz(basep - l)] = X[(warp, lane)][l]
+            B[c * CS + _swz(basep - l, lam_c)] = X[(warp, lane)][l]

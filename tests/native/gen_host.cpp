@@ -19,7 +19,13 @@ using namespace amqft_b200;
 template <int V>
 int bottom_v(int LB, int rho, int lens, const double* T, double* F, int a, const double* tab,
              int nmax, double base, int N, int D, int r, int dsto) {
-  if (LB == 64) { Bottom<V, 64>::template run<double, HA, 6>(rho, lens, T, F, a, tab, nmax, base, N, D, r, dsto); return 0; }
+  if (LB != 64) return -1;
+  switch (D) {
+    case 3: Bottom<V, 64>::template run<double, HA, 6, 3>(rho, lens, T, F, a, tab, nmax, base, N, r, dsto); return 0;
+    case 4: Bottom<V, 64>::template run<double, HA, 6, 4>(rho, lens, T, F, a, tab, nmax, base, N, r, dsto); return 0;
+    case 5: Bottom<V, 64>::template run<double, HA, 6, 5>(rho, lens, T, F, a, tab, nmax, base, N, r, dsto); return 0;
+    case 6: Bottom<V, 64>::template run<double, HA, 6, 6>(rho, lens, T, F, a, tab, nmax, base, N, r, dsto); return 0;
+  }
   return -1;
 }
 
