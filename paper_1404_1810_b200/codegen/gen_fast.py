@@ -161,7 +161,7 @@ def store_off(p):
     return f"-({p} * ((1 << D) + (1 << (D >= 5 ? D - 5 : 0))))"
 
 
-def gen_tmB(v, LB, rho, lam):
+def gen_tmB(v, LB, rho, lam, part=None):
     """Class by class: mirror folds never mix trailing-zero classes
     (tz(v) == tz(L - v)), so each class is loaded, transformed and stored
     on its own -- small live register set.  Addresses are immediate offsets
@@ -172,6 +172,8 @@ def gen_tmB(v, LB, rho, lam):
     em.emit("const R* __restrict__ Tp = T + a + (a >> LOGLB);")
     em.emit("const int swsh = dsto ? 0 : 31;")
     for t in range(lg):
+        if part is not None and (t == 0) != (part == 0):
+            continue
         x = {}
         for u in range(1, LB):
             if tz(u) == t:
@@ -186,8 +188,9 @@ def gen_tmB(v, LB, rho, lam):
                     f"else F[SW(hi - ({p} << D))] = {name};")
         em.emit("}")
         em.emit('asm volatile("" ::: "memory");  // keep classes apart (register pressure)')
+    sfx = "" if part is None else f"_p{part}"
     sig = (f"template <typename R, typename AR, int LOGLB, int D>\n__device__ __forceinline__ void "
-           f"tmB_v{v}_lb{LB}_r{rho}_l{lam}(const R* __restrict__ T, R* __restrict__ F, int a, "
+           f"tmB_v{v}_lb{LB}_r{rho}_l{lam}{sfx}(const R* __restrict__ T, R* __restrict__ F, int a, "
            f"const R* __restrict__ tab, int nmax, R base, int N, int r, int dsto)")
     return sig + " {\n" + "\n".join(em.lines) + "\n}\n"
 
@@ -317,7 +320,7 @@ def mnet_bwd(em, x, a, L, rho, lens, sine, cls=None):
             x[j], x[m] = em.new(add(O, E)), em.new(sub(O, E))
 
 
-def gen_hmB(v, LB, rho, lam):
+def gen_hmB(v, LB, rho, lam, part=None):
     """Class by class (see gen_tmB)."""
     sine = 1 if v >= 5 else 0
     lg = LB.bit_length() - 1
@@ -325,6 +328,8 @@ def gen_hmB(v, LB, rho, lam):
     em.emit("R* __restrict__ Fp = F + a + (a >> LOGLB);")
     em.emit("const int swsh = dsto ? 0 : 31;")
     for t in range(lg):
+        if part is not None and (t == 0) != (part == 0):
+            continue
         x = {}
         cnt = LB >> (t + 1)
         em.emit(f"{{ const int hi{t} = (N >> {t + 1}) - dsto - r;")
@@ -340,8 +345,9 @@ def gen_hmB(v, LB, rho, lam):
             em.emit(f"Fp[{u}] = {x[u]};")
         em.emit("}")
         em.emit('asm volatile("" ::: "memory");  // keep classes apart (register pressure)')
+    sfx = "" if part is None else f"_p{part}"
     sig = (f"template <typename R, typename AR, int LOGLB, int D>\n__device__ __forceinline__ void "
-           f"hmB_v{v}_lb{LB}_r{rho}_l{lam}(const R* __restrict__ T, R* __restrict__ F, int a, "
+           f"hmB_v{v}_lb{LB}_r{rho}_l{lam}{sfx}(const R* __restrict__ T, R* __restrict__ F, int a, "
            f"const R* __restrict__ tab, int nmax, R base, int N, int r, int dsto)")
     return sig + " {\n" + "\n".join(em.lines) + "\n}\n"
 
@@ -662,6 +668,167 @@ def gen_recomb(W, HW, lam, special):
     return sig + " {\n" + "\n".join(em.lines) + "\n}\n"
 
 
+# ------------------------------------ small chain, split for parallel lanes
+def scaled_mnet_cls(em, y, HP, lam, sine, direction, nlog, cls):
+    """scaled_mnet restricted to one trailing-zero class (classes never mix)."""
+    nmax = 1 << nlog
+    def rec(a, L, rho, lens):
+        if L < 4:
+            return
+        lo_l = lens if rho == 0 else lens ^ sine
+        hi_l = lens ^ sine if rho == 0 else lens
+        if direction == "bwd":
+            rec(a, L // 2, 0, lo_l)
+            rec(a + L // 2, L // 2, 1, hi_l)
+        lg2L = (2 * L).bit_length() - 1
+        for vv in range(1, L // 2):
+            if tz(vv) != cls:
+                continue
+            lo, hi = a + vv, a + L - vv
+            j, m = (lo, hi) if rho == 0 else (hi, lo)
+            k = "base" if vv == L // 4 else f"__ldg(tab + {vv * (nmax >> lg2L) - 1})"
+            if direction == "fwd":
+                p_, q_ = y[j], y[m]
+                s_, d_ = add(p_, q_), sub(p_, q_)
+                e_, o_ = (s_, d_) if lens == 0 else (d_, s_)
+                y[j] = em.new(e_)
+                y[m] = em.new(mul(o_, k))
+            else:
+                E, C = y[j], y[m]
+                O = em.new(mul(C, k))
+                if lens == 0:
+                    y[j], y[m] = em.new(add(E, O)), em.new(sub(E, O))
+                else:
+                    y[j], y[m] = em.new(add(O, E)), em.new(sub(O, E))
+        if direction == "fwd":
+            rec(a, L // 2, 0, lo_l)
+            rec(a + L // 2, L // 2, 1, hi_l)
+    rec(0, HP, 0, lam)
+
+
+def gen_small_tm_class(v, HP, lam, nlog, cls):
+    """Time-major: one class of the cells at multiples of LB -- forward
+    mirror levels and the spectrum of its small top block, written to F;
+    cls == log2(HP) is the Dct(2)/Dst(4) base."""
+    sine = 1 if v >= 5 else 0
+    em = Emitter()
+    em.emit(f"constexpr int swsh = {0 if lam else 31};")
+    lg = HP.bit_length() - 1
+    Np = 2 * HP
+    if cls == lg:
+        if lam == 0:
+            em.emit("const R y0 = T[PH(0)], yh = T[PH(" + str(HP) + " * LBV)];")
+            em.emit(f"F[SW(0)] = {add('y0', 'yh')};")
+            em.emit(f"F[SW(1)] = {sub('y0', 'yh')};")
+        else:
+            em.emit(f"F[SW(1)] = T[PH({HP // 2} * LBV)];")
+    elif lam == 1 and cls == lg - 1:
+        pass  # Dst chain: the centre is Dst(4), handled by the base lane
+    else:
+        y = {}
+        for k in range(1, HP):
+            if tz(k) == cls:
+                em.emit(f"const R y{k} = T[PH({k} * LBV)];")
+                y[k] = f"y{k}"
+        scaled_mnet_cls(em, y, HP, lam, sine, "fwd", nlog, cls)
+        sp = spectrum_tm(em, v, y, 0, HP, 0, lam, sine, cls)
+        hi = (Np >> (cls + 1)) - lam
+        for p, name in enumerate(sp):
+            em.emit(f"F[SW({hi - p})] = {name};")
+    sig = (f"template <typename R, typename AR, int LOGLB, int LBV>\n__device__ __forceinline__ void "
+           f"smtm_v{v}_hp{HP}_n{nlog}_l{lam}_c{cls}(const R* __restrict__ T, R* __restrict__ F, "
+           f"const R* __restrict__ tab, R base)")
+    return sig + " {\n" + "\n".join(em.lines) + "\n}\n"
+
+
+def gen_small_tm_recomb(HP, lam):
+    """Time-major: SplitTimeParity recombination Dct/Dst(n), n = 4|8 .. 2HP,
+    on F cells [0, HP] in registers."""
+    em = Emitter()
+    em.emit(f"constexpr int swsh = {0 if lam else 31};")
+    ks = range(0, HP + 1) if lam == 0 else range(1, HP)
+    G = {}
+    for k in ks:
+        em.emit(f"const R g{k} = F[SW({k})];")
+        G[k] = f"g{k}"
+    n = 4 if lam == 0 else 8
+    while n <= 2 * HP:
+        for k in (range(n // 4) if lam == 0 else range(1, n // 4)):
+            e, o = G[k], G[n // 2 - k]
+            if lam == 0:
+                G[k], G[n // 2 - k] = em.new(add(e, o)), em.new(sub(e, o))
+            else:
+                G[k], G[n // 2 - k] = em.new(add(o, e)), em.new(sub(o, e))
+        n *= 2
+    for k in ks:
+        em.emit(f"F[SW({k})] = {G[k]};")
+    sig = (f"template <typename R, typename AR>\n__device__ __forceinline__ void "
+           f"smtm_recomb_hp{HP}_l{lam}(R* __restrict__ F)")
+    return sig + " {\n" + "\n".join(em.lines) + "\n}\n"
+
+
+def gen_small_hm_fold(HP, lam):
+    """Harmonic-major: SplitHarmonicParity folds n = 2HP .. 4|8 on T cells
+    [0, HP] in registers (in place)."""
+    em = Emitter()
+    em.emit(f"constexpr int swsh = {0 if lam else 31};")
+    ks = range(0, HP + 1) if lam == 0 else range(1, HP)
+    S_ = {}
+    for k in ks:
+        em.emit(f"const R s{k} = T[SW({k})];")
+        S_[k] = f"s{k}"
+    n = 2 * HP
+    while n >= (4 if lam == 0 else 8):
+        for m in (range(n // 4) if lam == 0 else range(1, n // 4)):
+            a_, b_ = S_[m], S_[n // 2 - m]
+            if lam == 0:
+                S_[m], S_[n // 2 - m] = em.new(add(a_, b_)), em.new(sub(a_, b_))
+            else:
+                S_[m], S_[n // 2 - m] = em.new(sub(a_, b_)), em.new(add(a_, b_))
+        n //= 2
+    for k in ks:
+        em.emit(f"T[SW({k})] = {S_[k]};")
+    sig = (f"template <typename R, typename AR>\n__device__ __forceinline__ void "
+           f"smhm_fold_hp{HP}_l{lam}(R* __restrict__ T)")
+    return sig + " {\n" + "\n".join(em.lines) + "\n}\n"
+
+
+def gen_small_hm_class(v, HP, lam, nlog, cls):
+    """Harmonic-major: one small top block (after the folds, its temporal
+    cells are reversed in T (n/4, n/2]): gathers + AM_F placing its leaves
+    on the scaled segment, then its mirror levels, written to F at
+    multiples of LB; cls == log2(HP) is the Dct(2)/Dst(4) base."""
+    sine = 1 if v >= 5 else 0
+    em = Emitter()
+    em.emit(f"constexpr int swsh = {0 if lam else 31};")
+    lg = HP.bit_length() - 1
+    Np = 2 * HP
+    if cls == lg:
+        if lam == 0:
+            em.emit("const R t0 = T[SW(0)], t1 = T[SW(1)];")
+            em.emit(f"F[PH(0)] = {add('t0', 't1')};")
+            em.emit(f"F[PH({HP} * LBV)] = {sub('t0', 't1')};")
+        else:
+            em.emit(f"F[PH({HP // 2} * LBV)] = T[SW(1)];")
+    elif lam == 1 and cls == lg - 1:
+        pass
+    else:
+        n = Np >> cls
+        vals = []
+        for p in range(n // 4):
+            em.emit(f"const R u{p} = T[SW({n // 2 - p - lam})];")
+            vals.append(f"u{p}")
+        x = {}
+        place_hm(em, v, vals, lam, sine, x, 0, HP, 0)
+        scaled_mnet_cls(em, x, HP, lam, sine, "bwd", nlog, cls)
+        for k in sorted(x):
+            em.emit(f"F[PH({k} * LBV)] = {x[k]};")
+    sig = (f"template <typename R, typename AR, int LOGLB, int LBV>\n__device__ __forceinline__ void "
+           f"smhm_v{v}_hp{HP}_n{nlog}_l{lam}_c{cls}(const R* __restrict__ T, R* __restrict__ F, "
+           f"const R* __restrict__ tab, R base)")
+    return sig + " {\n" + "\n".join(em.lines) + "\n}\n"
+
+
 # (LB, nlog) pairs of the fused kernels: LT = nlog - 1 - log2(LB), HP = 2^LT
 FULL_SIZES = [(64, 10), (64, 11), (64, 12), (64, 13)]
 
@@ -688,7 +855,8 @@ def main():
         for v in range(1, 9):
             for rho in (0, 1):
                 for lam in (0, 1):
-                    out.append(gen_tmB(v, LB, rho, lam) if v in TM else gen_hmB(v, LB, rho, lam))
+                    for part in (0, 1):
+                        out.append(gen_tmB(v, LB, rho, lam, part) if v in TM else gen_hmB(v, LB, rho, lam, part))
     for v in range(1, 9):
         for hp in hp_all:
             for lam in (0, 1):
@@ -706,6 +874,20 @@ def main():
         for v in range(1, 9):
             for lam in (0, 1):
                 out.append(gen_small_full(v, HP, lam, nlog))
+    small_hps = set()
+    for LB, nlog in FULL_SIZES:
+        LT = nlog - 1 - (LB.bit_length() - 1)
+        HP = 1 << LT
+        small_hps.add(HP)
+        for v in range(1, 9):
+            for lam in (0, 1):
+                for cls in range(LT + 1):
+                    out.append(gen_small_tm_class(v, HP, lam, nlog, cls) if v in TM
+                               else gen_small_hm_class(v, HP, lam, nlog, cls))
+    for HP in sorted(small_hps):
+        for lam in (0, 1):
+            out.append(gen_small_tm_recomb(HP, lam))
+            out.append(gen_small_hm_fold(HP, lam))
     for LB, nlog in FULL_SIZES:
         N = 1 << nlog
         W = N // LB
@@ -740,6 +922,27 @@ def main():
                 out.append(f"    else gen::top_{direction}_lb{LB}_lt{LT}_n{nlog}_l1_s{sine}<R, AR>(B, v, tab, base);")
                 out.append("  }")
             out.append("};")
+    out.append("template <int V, int HP, int NLOG> struct SmallPar;")
+    for LB, nlog in FULL_SIZES:
+        LT = nlog - 1 - (LB.bit_length() - 1)
+        HP = 1 << LT
+        for v in range(1, 9):
+            fam = "smtm" if v in TM else "smhm"
+            out.append(f"template <> struct SmallPar<{v}, {HP}, {nlog}> {{")
+            out.append(f"  static constexpr int NCLS = {LT + 1};")
+            out.append("  template <typename R, typename AR, int LOGLB, int LBV>")
+            out.append("  static __device__ __forceinline__ void cls(int lam, int c, const R* T, R* F, const R* tab, R base) {")
+            for lam in (0, 1):
+                for cls in range(LT + 1):
+                    out.append(f"    if (lam == {lam} && c == {cls}) {{ gen::{fam}_v{v}_hp{HP}_n{nlog}_l{lam}_c{cls}"
+                               f"<R, AR, LOGLB, LBV>(T, F, tab, base); return; }}")
+            out.append("  }")
+            out.append("  template <typename R, typename AR>")
+            out.append("  static __device__ __forceinline__ void serial(int lam, R* B) {")
+            ser = "smtm_recomb" if v in TM else "smhm_fold"
+            out.append(f"    if (lam == 0) gen::{ser}_hp{HP}_l0<R, AR>(B); else gen::{ser}_hp{HP}_l1<R, AR>(B);")
+            out.append("  }")
+            out.append("};")
     out.append("template <int V, int HP, int NLOG> struct SmallFull;")
     for LB, nlog in FULL_SIZES:
         LT = nlog - 1 - (LB.bit_length() - 1)
@@ -758,12 +961,13 @@ def main():
         for v in range(1, 9):
             fam = "tmB" if v in TM else "hmB"
             out.append(f"template <> struct Bottom<{v}, {LB}> {{")
-            out.append("  template <typename R, typename AR, int LOGLB, int D>")
+            out.append("  template <typename R, typename AR, int LOGLB, int D, int PART>")
             out.append("  static __device__ __forceinline__ void run(int rho, int lens, const R* T, R* F, int a, "
                        "const R* tab, int nmax, R base, int N, int r, int dsto) {")
             for rho in (0, 1):
                 for lam in (0, 1):
-                    out.append(f"    if (rho == {rho} && lens == {lam}) {{ gen::{fam}_v{v}_lb{LB}_r{rho}_l{lam}"
+                    out.append(f"    if (rho == {rho} && lens == {lam}) {{ if constexpr (PART == 0) gen::{fam}_v{v}_lb{LB}_r{rho}_l{lam}_p0"
+                               f"<R, AR, LOGLB, D>(T, F, a, tab, nmax, base, N, r, dsto); else gen::{fam}_v{v}_lb{LB}_r{rho}_l{lam}_p1"
                                f"<R, AR, LOGLB, D>(T, F, a, tab, nmax, base, N, r, dsto); return; }}")
             out.append("  }")
             out.append("};")

@@ -53,8 +53,10 @@ struct Cfg {
   static constexpr int LT = LOGH - LOGLB;        // depth of the bottom segments
   static constexpr int HP = H / LB;               // cells at multiples of LB
   static constexpr int NSEG = 4 * HP;             // bottom segments (4 chains)
-  static constexpr int NT0 = (4 * LB > NSEG ? 4 * LB : NSEG);
-  static constexpr int NT = NT0 < 128 ? 128 : NT0;
+  // threads: top levels use 4*LB, the bottom NSEG + one warp for the
+  // small top blocks, the AM phase 8 warps
+  static constexpr int NT0 = (4 * LB > NSEG + 32 ? 4 * LB : NSEG + 32);
+  static constexpr int NT = NT0 < 256 ? 256 : NT0;
   // chain stride: holds the skewed (H + H/LB + 1) and the swizzled
   // (32-aligned blocks up to H) layouts; +16 staggers the chains' banks.
   static constexpr int CS = ((H + HP + 1 > H + H / 32 + 1 ? H + HP + 1 : H + H / 32 + 1) + 31) / 32 * 32 + 16;
@@ -363,6 +365,12 @@ __device__ unsigned long long g_phase_cycles[16];
 #endif
 
 template <int V, typename R, int LOGN, int LOGLB>
+#ifndef AMQFT_SMALL_MODE
+#define AMQFT_SMALL_MODE 0   // 0: serial small chain on spare lanes (measured best); 1: split into classes
+#endif
+#ifndef AMQFT_UNROLL_IO
+#define AMQFT_UNROLL_IO 1
+#endif
 #ifndef AMQFT_FAST_MINB
 #define AMQFT_FAST_MINB 2
 #endif
@@ -399,7 +407,14 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
     mbar_wait(bar, parity);
     parity ^= 1;
     const V2* x = reinterpret_cast<const V2*>(Sb);
-    for (int m = tid; m <= H; m += C::NT) {
+#if AMQFT_UNROLL_IO
+#pragma unroll
+#else
+#pragma unroll 1
+#endif
+    for (int it = 0; it < (H + C::NT) / C::NT; ++it) {
+      const int m = tid + it * C::NT;
+      if (m > H) break;
       V2 a = x[m];
       if (inverse) { const R tmp = a.x; a.x = a.y; a.y = tmp; }
       if (m == 0 || m == H) {
@@ -425,12 +440,11 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       // top mirror levels (generated, 2^LT cells per thread) || small chains
       if (tid < 4 * C::LB) {
         const int c = tid >> LOGLB, v = tid & (C::LB - 1);
-        if (v > 0) {
-          Top<C::LB, C::LT, LOGN, C::SINE>::template fwd<R, A>(c & 1, Tb + c * C::CS, v, tab, base);
-        } else {
-          SmallFull<V, C::HP, LOGN>::template run<R, A, LOGLB, C::LB>(c & 1, Tb + c * C::CS,
-                                                                      Fb + c * C::CS, tab, base);
-        }
+        if (v > 0) Top<C::LB, C::LT, LOGN, C::SINE>::template fwd<R, A>(c & 1, Tb + c * C::CS, v, tab, base);
+#if AMQFT_SMALL_MODE == 0
+        else SmallFull<V, C::HP, LOGN>::template run<R, A, LOGLB, C::LB>(c & 1, Tb + c * C::CS,
+                                                                         Fb + c * C::CS, tab, base);
+#endif
       }
     } else {
 #pragma unroll 1
@@ -440,12 +454,23 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       }
       if constexpr (C::CHAIN) am_levels_asc<C, R, C::LT>(Tb);
       else am_phase_regs<C, R, false>(Tb);
+      // small-chain folds (cells [0, N/LB] of T, untouched by the AM
+      // levels): lane 31 of chain c's second warp is idle in the AM phase
+#if AMQFT_SMALL_MODE == 1
+      if ((tid & 63) == 63 && tid < 256) {
+        const int c = tid >> 6;
+        SmallPar<V, C::HP, LOGN>::template serial<R, A>(c & 1, Tb + c * C::CS);
+      }
+#endif
     }
     __syncthreads();
     PHASE_MARK(2);
 
-    // ---- bottom: T -> F (generated, one LB-segment per thread)
+    // ---- bottom: T -> F (generated).  Two threads per LB-segment: the
+    // trailing-zero classes never mix, class 0 goes to warps 0-3 and
+    // classes 1.. to warps 4-7.
     if (tid < C::NSEG) {
+      // one thread per LB-segment (both class groups)
       const int half = C::HP / 2;
       const int h = tid % half;
       const int rest = tid / half;
@@ -454,25 +479,43 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       const int s = 2 * h + rho_bit;
       int rho, lens, r;
       seg_params<C::SINE>(lam_bit, s, C::LT, &rho, &lens, &r);
-      Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT>(rho, lens, Tb + c * C::CS, Fb + c * C::CS,
-                                                         s * C::LB, tab, nmax, base, N, r, lam_bit);
-    }
-    if constexpr (!C::TM) {
-      if (tid >= C::NT - 4) {
-        const int c = tid - (C::NT - 4);
-        SmallFull<V, C::HP, LOGN>::template run<R, A, LOGLB, C::LB>(c & 1, Tb + c * C::CS,
-                                                                    Fb + c * C::CS, tab, base);
+      Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, 0>(rho, lens, Tb + c * C::CS, Fb + c * C::CS,
+                                                            s * C::LB, tab, nmax, base, N, r, lam_bit);
+      Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, 1>(rho, lens, Tb + c * C::CS, Fb + c * C::CS,
+                                                            s * C::LB, tab, nmax, base, N, r, lam_bit);
+    } else {
+#if AMQFT_SMALL_MODE == 1
+      // the cells at multiples of LB (small top blocks): one lane per
+      // (chain, trailing-zero class), disjoint from the segments' cells
+      using SP = SmallPar<V, C::HP, LOGN>;
+      const int l = tid - C::NSEG;
+      if (l < 4 * SP::NCLS) {
+        const int c = l / SP::NCLS, cls = l - c * SP::NCLS;
+        SP::template cls<R, A, LOGLB, C::LB>(c & 1, cls, Tb + c * C::CS, Fb + c * C::CS, tab, base);
       }
+#else
+      if constexpr (!C::TM) {
+        const int l = tid - C::NSEG;
+        if (l < 4) SmallFull<V, C::HP, LOGN>::template run<R, A, LOGLB, C::LB>(l & 1, Tb + l * C::CS,
+                                                                             Fb + l * C::CS, tab, base);
+      }
+#endif
     }
     __syncthreads();
     PHASE_MARK(3);
 
     if constexpr (C::TM) {
       if constexpr (C::CHAIN) am_levels_desc<C, R, C::LT>(Fb);
-      else {
-        am_phase_regs<C, R, true>(Fb);
-        __syncthreads();
+      else am_phase_regs<C, R, true>(Fb);
+      // small-chain recombination Dct/Dst(4..N/LB) on F cells [0, N/LB]
+      // (disjoint from the AM levels): lane 31 of chain c's second warp
+#if AMQFT_SMALL_MODE == 1
+      if ((tid & 63) == 63 && tid < 256) {
+        const int c = tid >> 6;
+        SmallPar<V, C::HP, LOGN>::template serial<R, A>(c & 1, Fb + c * C::CS);
       }
+#endif
+      __syncthreads();
       PHASE_MARK(4);
       if constexpr (N / C::LB == 64) {
         // generated: each thread owns the 64 cells j*64 +- k of its chain
@@ -496,7 +539,14 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
 
     // ---- store: SplitReal bwd (elab.cpp:199-208) + SplitComplex bwd (162-183)
     V2* y = reinterpret_cast<V2*>(out + row * 2 * N);
-    for (int k = tid; k <= H; k += C::NT) {
+#if AMQFT_UNROLL_IO
+#pragma unroll
+#else
+#pragma unroll 1
+#endif
+    for (int it = 0; it < (H + C::NT) / C::NT; ++it) {
+      const int k = tid + it * C::NT;
+      if (k > H) break;
       const R rd = Fb[0 * C::CS + C::pf(k, 0)];
       const R id = Fb[2 * C::CS + C::pf(k, 0)];
       V2 lo, hi;

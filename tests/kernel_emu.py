@@ -36,6 +36,7 @@ def lib():
         L.host_bottom.argtypes = [i, i, i, i, dp, dp, i, dp, i, d, i, i, i, i]
         L.host_small.argtypes = [i, i, i, i, i, dp, dp, dp, d]
         L.host_recomb.argtypes = [i, i, i, dp, i]
+        L.host_smallpar.argtypes = [i, i, i, i, i, i, dp, dp, dp, d, i, dp]
         _lib = L
     return _lib
 
@@ -188,7 +189,9 @@ def emulate(v, N, LB, x, tab, base):
         for c in range(4):
             for vv in range(1, LB):
                 assert L.host_top(LB, LT, LOGN, SINE, 0, c & 1, Tp + 8 * c * CS, vv, tp, base) == 0
-            assert L.host_small(v, HP, LOGN, LB, c & 1, Tp + 8 * c * CS, Fp + 8 * c * CS, tp, base) == 0
+            for cls in range(LT + 1):
+                assert L.host_smallpar(v, HP, LOGN, LB, c & 1, cls, Tp + 8 * c * CS, Fp + 8 * c * CS,
+                                       tp, base, 0, None) == 0
     else:
         n = N
         while n >= 2 * (N // LB):
@@ -199,6 +202,8 @@ def emulate(v, N, LB, x, tab, base):
                 _am_level(T, CS, N, LOGLB, depth, v, SINE, False)
         else:
             am_phase_regs(T, CS, N, LOGLB, LT, v, SINE, False)
+        for c in range(4):
+            assert L.host_smallpar(v, HP, LOGN, LB, c & 1, 0, None, None, tp, base, 1, Tp + 8 * c * CS) == 0
     half = HP // 2
     for tid in range(NSEG):
         h = tid % half
@@ -209,9 +214,13 @@ def emulate(v, N, LB, x, tab, base):
         rho, lens, r = seg_params(SINE, lam_bit, s, LT)
         assert L.host_bottom(v, LB, rho, lens, Tp + 8 * c * CS, Fp + 8 * c * CS, s * LB, tp, N,
                              base, N, LT, r, lam_bit) == 0
-    if not TM:
-        for c in range(4):
-            assert L.host_small(v, HP, LOGN, LB, c & 1, Tp + 8 * c * CS, Fp + 8 * c * CS, tp, base) == 0
+    for c in range(4):
+        if TM:
+            assert L.host_smallpar(v, HP, LOGN, LB, c & 1, 0, None, None, tp, base, 1, Fp + 8 * c * CS) == 0
+        else:
+            for cls in range(LT + 1):
+                assert L.host_smallpar(v, HP, LOGN, LB, c & 1, cls, Tp + 8 * c * CS, Fp + 8 * c * CS,
+                                       tp, base, 0, None) == 0
     if TM:
         if v in (1, 5):
             for depth in range(LT - 1, -1, -1):

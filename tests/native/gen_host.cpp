@@ -21,10 +21,14 @@ int bottom_v(int LB, int rho, int lens, const double* T, double* F, int a, const
              int nmax, double base, int N, int D, int r, int dsto) {
   if (LB != 64) return -1;
   switch (D) {
-    case 3: Bottom<V, 64>::template run<double, HA, 6, 3>(rho, lens, T, F, a, tab, nmax, base, N, r, dsto); return 0;
-    case 4: Bottom<V, 64>::template run<double, HA, 6, 4>(rho, lens, T, F, a, tab, nmax, base, N, r, dsto); return 0;
-    case 5: Bottom<V, 64>::template run<double, HA, 6, 5>(rho, lens, T, F, a, tab, nmax, base, N, r, dsto); return 0;
-    case 6: Bottom<V, 64>::template run<double, HA, 6, 6>(rho, lens, T, F, a, tab, nmax, base, N, r, dsto); return 0;
+    case 3: Bottom<V, 64>::template run<double, HA, 6, 3, 0>(rho, lens, T, F, a, tab, nmax, base, N, r, dsto);
+             Bottom<V, 64>::template run<double, HA, 6, 3, 1>(rho, lens, T, F, a, tab, nmax, base, N, r, dsto); return 0;
+    case 4: Bottom<V, 64>::template run<double, HA, 6, 4, 0>(rho, lens, T, F, a, tab, nmax, base, N, r, dsto);
+             Bottom<V, 64>::template run<double, HA, 6, 4, 1>(rho, lens, T, F, a, tab, nmax, base, N, r, dsto); return 0;
+    case 5: Bottom<V, 64>::template run<double, HA, 6, 5, 0>(rho, lens, T, F, a, tab, nmax, base, N, r, dsto);
+             Bottom<V, 64>::template run<double, HA, 6, 5, 1>(rho, lens, T, F, a, tab, nmax, base, N, r, dsto); return 0;
+    case 6: Bottom<V, 64>::template run<double, HA, 6, 6, 0>(rho, lens, T, F, a, tab, nmax, base, N, r, dsto);
+             Bottom<V, 64>::template run<double, HA, 6, 6, 1>(rho, lens, T, F, a, tab, nmax, base, N, r, dsto); return 0;
   }
   return -1;
 }
@@ -42,6 +46,22 @@ int small_v(int HP, int nlog, int LB, int lam, const double* T, double* F, const
   if (HP == 16 && nlog == 11) return small_vh<V, 16, 11>(LB, lam, T, F, tab, base);
   if (HP == 32 && nlog == 12) return small_vh<V, 32, 12>(LB, lam, T, F, tab, base);
   if (HP == 64 && nlog == 13) return small_vh<V, 64, 13>(LB, lam, T, F, tab, base);
+  return -1;
+}
+
+
+template <int V>
+int smallpar_v(int HP, int nlog, int LB, int lam, int cls, const double* T, double* F,
+               const double* tab, double base, int serial, double* B) {
+  if (LB != 64) return -1;
+#define SPCASE(hp, nl)                                                                      \
+  if (HP == hp && nlog == nl) {                                                             \
+    if (serial) SmallPar<V, hp, nl>::template serial<double, HA>(lam, B);                   \
+    else SmallPar<V, hp, nl>::template cls<double, HA, 6, 64>(lam, cls, T, F, tab, base);   \
+    return 0;                                                                               \
+  }
+  SPCASE(8, 10) SPCASE(16, 11) SPCASE(32, 12) SPCASE(64, 13)
+#undef SPCASE
   return -1;
 }
 
@@ -92,6 +112,21 @@ int host_small(int V, int HP, int nlog, int LB, int lam, const double* T, double
     case 6: return small_v<6>(HP, nlog, LB, lam, T, F, tab, base);
     case 7: return small_v<7>(HP, nlog, LB, lam, T, F, tab, base);
     case 8: return small_v<8>(HP, nlog, LB, lam, T, F, tab, base);
+  }
+  return -1;
+}
+
+int host_smallpar(int V, int HP, int nlog, int LB, int lam, int cls, const double* T, double* F,
+                  const double* tab, double base, int serial, double* B) {
+  switch (V) {
+    case 1: return smallpar_v<1>(HP, nlog, LB, lam, cls, T, F, tab, base, serial, B);
+    case 2: return smallpar_v<2>(HP, nlog, LB, lam, cls, T, F, tab, base, serial, B);
+    case 3: return smallpar_v<3>(HP, nlog, LB, lam, cls, T, F, tab, base, serial, B);
+    case 4: return smallpar_v<4>(HP, nlog, LB, lam, cls, T, F, tab, base, serial, B);
+    case 5: return smallpar_v<5>(HP, nlog, LB, lam, cls, T, F, tab, base, serial, B);
+    case 6: return smallpar_v<6>(HP, nlog, LB, lam, cls, T, F, tab, base, serial, B);
+    case 7: return smallpar_v<7>(HP, nlog, LB, lam, cls, T, F, tab, base, serial, B);
+    case 8: return smallpar_v<8>(HP, nlog, LB, lam, cls, T, F, tab, base, serial, B);
   }
   return -1;
 }
