@@ -421,8 +421,10 @@ def gen_top(LB, LT, direction, lam, sine, nlog):
         L = H >> (i - 1)
         lg2L = (2 * L).bit_length() - 1
         sc = nmax >> lg2L
-        em.emit(f"{{ const R* __restrict__ tp = tab + v * {sc};")
-        em.emit(f"  const R* __restrict__ tm = tab - v * {sc};")
+        # per-level compacted table: ltab[off_i + u] = f(pi u / L), u < L/2
+        off_i = sum((H >> (j - 1)) // 2 for j in range(1, i))
+        em.emit(f"{{ const R* __restrict__ tp = ltab + {off_i} + v;")
+        em.emit(f"  const R* __restrict__ tm = ltab + {off_i} - v;")
         done = set()
         for z in range(2 * K):
             if z in done:
@@ -449,8 +451,7 @@ def gen_top(LB, LT, direction, lam, sine, nlog):
             par = bin(seg ^ (seg >> 1)).count("1") & 1
             lens = lam ^ (sine & par)
             jc, mcz = (lower, upper) if rho == 0 else (upper, lower)
-            idx0 = u0 * sc - 1
-            kexpr = f"__ldg({'tp' if lsg > 0 else 'tm'} + {idx0})"
+            kexpr = f"__ldg({'tp' if lsg > 0 else 'tm'} + {u0})"
             if u0 == 0 and lsg > 0 and i == LT:
                 kexpr = f"(v == {LB // 2} ? base : {kexpr})"
             p_, q_ = x[jc], x[mcz]
@@ -477,7 +478,7 @@ def gen_top(LB, LT, direction, lam, sine, nlog):
         em.emit(f"po[{(k + 1) * (W + 2)}] = x{2 * k + 1};")
     sig = (f"template <typename R, typename AR>\n__device__ __forceinline__ void "
            f"top_{direction}_lb{LB}_lt{LT}_n{nlog}_l{lam}_s{sine}(R* __restrict__ B, int v, "
-           f"const R* __restrict__ tab, R base)")
+           f"const R* __restrict__ ltab, R base)")
     return sig + " {\n" + "\n".join(em.lines) + "\n}\n"
 
 
@@ -591,7 +592,23 @@ def gen_small_full(v, HP, lam, nlog):
 
 
 # --------------------------------------------- chain recombination (phase F)
-def gen_recomb(W, HW, lam, special):
+def emit_pair(em, e, o, t, lam, fold):
+    """Recombination (SplitTimeParity bwd, elab.cpp:310-329):
+    Dct (E+O, E-O), Dst (O+E, O-E).  Fold (SplitHarmonicParity fwd,
+    elab.cpp:238-255): Dct (a+b, a-b), Dst (a-b, a+b)."""
+    if not fold:
+        if lam == 0:
+            em.emit(f"{{ const R e{t} = {e}; {e} = {add('e' + str(t), o)}; {o} = {sub('e' + str(t), o)}; }}")
+        else:
+            em.emit(f"{{ const R e{t} = {e}; {e} = {add(o, 'e' + str(t))}; {o} = {sub(o, 'e' + str(t))}; }}")
+    else:
+        if lam == 0:
+            em.emit(f"{{ const R e{t} = {e}; {e} = {add('e' + str(t), o)}; {o} = {sub('e' + str(t), o)}; }}")
+        else:
+            em.emit(f"{{ const R e{t} = {e}; {e} = {sub('e' + str(t), o)}; {o} = {add('e' + str(t), o)}; }}")
+
+
+def gen_recomb(W, HW, lam, special, fold=False):
     """SplitTimeParity recombination Dct/Dst(n), n = 2W .. 2 W HW (= N), for
     the thread owning k in [1, W/2): cells j*W + k (j < HW) and j*W - k
     (1 <= j <= HW), closed under every level (pairs (y, n/2 - y), y < n/4).
@@ -615,8 +632,14 @@ def gen_recomb(W, HW, lam, special):
         for c in cells:
             off = c[1] * 66
             em.emit(f"R {name[c]} = {'pa' if c[0] == 'a' else 'pb'}[{off}];")
+        levels = []
         n = 2 * W
         while n <= N:
+            levels.append(n)
+            n *= 2
+        if fold:
+            levels = levels[::-1]
+        for n in levels:
             m = n // (2 * W)          # n/4 = m W/2
             for c in cells:
                 jW, sg = val(c)
@@ -630,16 +653,13 @@ def gen_recomb(W, HW, lam, special):
                 e, o = name[c], name[pc]
                 em.tmp += 1
                 t = em.tmp
-                if lam == 0:
-                    em.emit(f"{{ const R e{t} = {e}; {e} = {add('e' + str(t), o)}; {o} = {sub('e' + str(t), o)}; }}")
-                else:
-                    em.emit(f"{{ const R e{t} = {e}; {e} = {add(o, 'e' + str(t))}; {o} = {sub(o, 'e' + str(t))}; }}")
-            n *= 2
+                emit_pair(em, e, o, t, lam, fold)
         for c in cells:
             off = c[1] * 66
             em.emit(f"{'pa' if c[0] == 'a' else 'pb'}[{off}] = {name[c]};")
+        nm = "fold" if fold else "recomb"
         sig = (f"template <typename R, typename AR>\n__device__ __forceinline__ void "
-               f"recomb_w{W}_hw{HW}_l{lam}(R* __restrict__ F, int k)")
+               f"{nm}_w{W}_hw{HW}_l{lam}(R* __restrict__ F, int k)")
     else:
         hw2 = W // 2
         ys = [i * hw2 for i in range(0, 2 * HW + 1)]
@@ -649,22 +669,25 @@ def gen_recomb(W, HW, lam, special):
         sh = 31 if lam == 0 else 0
         for y in ys:
             em.emit(f"R s{y} = F[{y + ((y + sh) >> 5)}];")
+        levels = []
         n = 2 * W
         while n <= N:
+            levels.append(n)
+            n *= 2
+        if fold:
+            levels = levels[::-1]
+        for n in levels:
             for y in ys:
                 if y < n // 4 and (lam == 0 or y >= 1):
                     e, o = name[y], name[n // 2 - y]
                     em.tmp += 1
                     t = em.tmp
-                    if lam == 0:
-                        em.emit(f"{{ const R e{t} = {e}; {e} = {add('e' + str(t), o)}; {o} = {sub('e' + str(t), o)}; }}")
-                    else:
-                        em.emit(f"{{ const R e{t} = {e}; {e} = {add(o, 'e' + str(t))}; {o} = {sub(o, 'e' + str(t))}; }}")
-            n *= 2
+                    emit_pair(em, e, o, t, lam, fold)
         for y in ys:
             em.emit(f"F[{y + ((y + sh) >> 5)}] = s{y};")
+        nm = "foldsp" if fold else "recombsp"
         sig = (f"template <typename R, typename AR>\n__device__ __forceinline__ void "
-               f"recombsp_w{W}_hw{HW}_l{lam}(R* __restrict__ F)")
+               f"{nm}_w{W}_hw{HW}_l{lam}(R* __restrict__ F)")
     return sig + " {\n" + "\n".join(em.lines) + "\n}\n"
 
 
@@ -894,8 +917,9 @@ def main():
         HW = (N // 2) // W
         if W == 64:
             for lam in (0, 1):
-                out.append(gen_recomb(W, HW, lam, False))
-                out.append(gen_recomb(W, HW, lam, True))
+                for fold in (False, True):
+                    out.append(gen_recomb(W, HW, lam, False, fold))
+                    out.append(gen_recomb(W, HW, lam, True, fold))
     out.append("}  // namespace gen")
     out.append("template <int W, int HW> struct Recomb;")
     for LB, nlog in FULL_SIZES:
@@ -909,6 +933,11 @@ def main():
             out.append(f"    if (k == 0) {{ if (lam == 0) gen::recombsp_w{W}_hw{HW}_l0<R, AR>(F); else gen::recombsp_w{W}_hw{HW}_l1<R, AR>(F); }}")
             out.append(f"    else {{ if (lam == 0) gen::recomb_w{W}_hw{HW}_l0<R, AR>(F, k); else gen::recomb_w{W}_hw{HW}_l1<R, AR>(F, k); }}")
             out.append("  }")
+            out.append("  template <typename R, typename AR>")
+            out.append("  static __device__ __forceinline__ void fold(int lam, R* F, int k) {")
+            out.append(f"    if (k == 0) {{ if (lam == 0) gen::foldsp_w{W}_hw{HW}_l0<R, AR>(F); else gen::foldsp_w{W}_hw{HW}_l1<R, AR>(F); }}")
+            out.append(f"    else {{ if (lam == 0) gen::fold_w{W}_hw{HW}_l0<R, AR>(F, k); else gen::fold_w{W}_hw{HW}_l1<R, AR>(F, k); }}")
+            out.append("  }")
             out.append("};")
     out.append("template <int LB, int LT, int NLOG, int SINE> struct Top;")
     for LB, nlog in FULL_SIZES:
@@ -917,9 +946,9 @@ def main():
             out.append(f"template <> struct Top<{LB}, {LT}, {nlog}, {sine}> {{")
             for direction in ("fwd", "bwd"):
                 out.append("  template <typename R, typename AR>")
-                out.append(f"  static __device__ __forceinline__ void {direction}(int lam, R* B, int v, const R* tab, R base) {{")
-                out.append(f"    if (lam == 0) gen::top_{direction}_lb{LB}_lt{LT}_n{nlog}_l0_s{sine}<R, AR>(B, v, tab, base);")
-                out.append(f"    else gen::top_{direction}_lb{LB}_lt{LT}_n{nlog}_l1_s{sine}<R, AR>(B, v, tab, base);")
+                out.append(f"  static __device__ __forceinline__ void {direction}(int lam, R* B, int v, const R* ltab, R base) {{")
+                out.append(f"    if (lam == 0) gen::top_{direction}_lb{LB}_lt{LT}_n{nlog}_l0_s{sine}<R, AR>(B, v, ltab, base);")
+                out.append(f"    else gen::top_{direction}_lb{LB}_lt{LT}_n{nlog}_l1_s{sine}<R, AR>(B, v, ltab, base);")
                 out.append("  }")
             out.append("};")
     out.append("template <int V, int HP, int NLOG> struct SmallPar;")

@@ -36,6 +36,13 @@
 #include "fast_gen.cuh"
 #include "generic.cuh"
 
+#ifndef AMQFT_BOTTOM_SPLIT
+#define AMQFT_BOTTOM_SPLIT 0   // 1: two threads per bottom segment (class 0 | classes 1..)
+#endif
+#ifndef AMQFT_TMA_STAGE
+#define AMQFT_TMA_STAGE 1   // stage the next row with cp.async.bulk (else direct loads)
+#endif
+
 namespace amqft_b200 {
 namespace fastk {
 
@@ -65,7 +72,7 @@ struct Cfg {
   static constexpr bool CHAIN = (V == 1 || V == 5 || V == 3 || V == 7);
   // T, F (4 chains each) + the TMA staging buffer for the next row + mbarrier
   static constexpr size_t STAGE_OFF = 8 * CS * sizeof(R);
-  static constexpr size_t SMEM = STAGE_OFF + 2 * N * sizeof(R) + 16;
+  static constexpr size_t SMEM = AMQFT_TMA_STAGE ? STAGE_OFF + 2 * N * sizeof(R) + 16 : STAGE_OFF;
   // Bank-conflict layouts: skew (i + i/LB) on the buffer holding the
   // index-space mirror network (T for time-major, F for harmonic-major);
   // one pad word per 32 (i + i/32) on the other one (per-lane class runs,
@@ -349,9 +356,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 #ifdef AMQFT_PHASE_TIMING
-// Instrumented build only (tools/phase_timing): CTA 0 accumulates the
-// cycles spent between phase boundaries.
+// Instrumented build only (tools/phase_timing): CTA 0 accumulates, per
+// phase, the cycles thread 0 spends between phase boundaries
+// (g_phase_cycles) and, per warp, the cycles until the warp reaches the
+// phase's barrier (g_warp_work[phase][warp]).
 __device__ unsigned long long g_phase_cycles[16];
+__device__ unsigned long long g_warp_work[16][16];
 #define PHASE_MARK(k)                                                          \
   do {                                                                         \
     if (blockIdx.x == 0 && threadIdx.x == 0) {                                 \
@@ -359,9 +369,16 @@ __device__ unsigned long long g_phase_cycles[16];
       if ((k) > 0) atomicAdd(&g_phase_cycles[(k) - 1], (unsigned long long)(now - t_prev)); \
       t_prev = now;                                                            \
     }                                                                          \
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0) w_start = clock64();       \
+  } while (0)
+#define WORK_MARK(k)                                                           \
+  do {                                                                         \
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0)                            \
+      atomicAdd(&g_warp_work[k][threadIdx.x >> 5], (unsigned long long)(clock64() - w_start)); \
   } while (0)
 #else
 #define PHASE_MARK(k) do {} while (0)
+#define WORK_MARK(k) do {} while (0)
 #endif
 
 template <int V, typename R, int LOGN, int LOGLB>
@@ -376,9 +393,9 @@ template <int V, typename R, int LOGN, int LOGLB>
 #endif
 __global__ void __launch_bounds__(Cfg<V, R, LOGN, LOGLB>::NT, (sizeof(R) == 4 ? AMQFT_FAST_MINB : 1))
 k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
-       const R* __restrict__ tab, int nmax, int inverse, R scale) {
+       const R* __restrict__ tab, const R* __restrict__ ltab, int nmax, int inverse, R scale) {
 #ifdef AMQFT_PHASE_TIMING
-  long long t_prev = 0;
+  long long t_prev = 0, w_start = 0;
 #endif
   using C = Cfg<V, R, LOGN, LOGLB>;
   using A = Arith<R>;
@@ -392,6 +409,7 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
   const R base = __ldg(tab + (nmax / 4 - 1));
   constexpr int N = C::N, H = C::H;
   constexpr uint32_t ROW_BYTES = 2 * N * sizeof(R);
+#if AMQFT_TMA_STAGE
   if (tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
@@ -399,14 +417,23 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
   __syncthreads();
   if (tid == 0 && blockIdx.x < rows) tma_load_1d(Sb, in + blockIdx.x * 2 * N, ROW_BYTES, bar);
   uint32_t parity = 0;
+#else
+  (void)Sb;
+  (void)bar;
+  (void)ROW_BYTES;
+#endif
 
   for (size_t row = blockIdx.x; row < rows; row += gridDim.x) {
     PHASE_MARK(0);
     // ---- load: SplitComplex (elab.cpp:152-155) + SplitReal (185-197)
     // from the TMA-staged row; then prefetch the CTA's next row.
+#if AMQFT_TMA_STAGE
     mbar_wait(bar, parity);
     parity ^= 1;
     const V2* x = reinterpret_cast<const V2*>(Sb);
+#else
+    const V2* x = reinterpret_cast<const V2*>(in + row * 2 * N);
+#endif
 #if AMQFT_UNROLL_IO
 #pragma unroll
 #else
@@ -429,28 +456,37 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
         Tb[3 * C::CS + C::pt(m, 1)] = A::sub(a.y, b.y);
       }
     }
+    WORK_MARK(0);
     __syncthreads();
+#if AMQFT_TMA_STAGE
     if (tid == 0 && row + gridDim.x < rows) {
       fence_proxy_async();
       tma_load_1d(Sb, in + (row + gridDim.x) * 2 * N, ROW_BYTES, bar);
     }
+#endif
     PHASE_MARK(1);
 
     if constexpr (C::TM) {
       // top mirror levels (generated, 2^LT cells per thread) || small chains
       if (tid < 4 * C::LB) {
         const int c = tid >> LOGLB, v = tid & (C::LB - 1);
-        if (v > 0) Top<C::LB, C::LT, LOGN, C::SINE>::template fwd<R, A>(c & 1, Tb + c * C::CS, v, tab, base);
+        if (v > 0) Top<C::LB, C::LT, LOGN, C::SINE>::template fwd<R, A>(c & 1, Tb + c * C::CS, v, ltab, base);
 #if AMQFT_SMALL_MODE == 0
         else SmallFull<V, C::HP, LOGN>::template run<R, A, LOGLB, C::LB>(c & 1, Tb + c * C::CS,
                                                                          Fb + c * C::CS, tab, base);
 #endif
       }
     } else {
-#pragma unroll 1
-      for (int n = N; n >= 2 * (N / C::LB); n >>= 1) {
-        chain_level<C, R, true>(Tb, n);
+      if constexpr (N / C::LB == 64) {
+        // generated: each thread owns the 64 cells j*64 +- k of its chain
+        if (tid < 128) Recomb<64, H / 64>::template fold<R, A>((tid >> 5) & 1, Tb + (tid >> 5) * C::CS, tid & 31);
         __syncthreads();
+      } else {
+#pragma unroll 1
+        for (int n = N; n >= 2 * (N / C::LB); n >>= 1) {
+          chain_level<C, R, true>(Tb, n);
+          __syncthreads();
+        }
       }
       if constexpr (C::CHAIN) am_levels_asc<C, R, C::LT>(Tb);
       else am_phase_regs<C, R, false>(Tb);
@@ -463,12 +499,32 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       }
 #endif
     }
+    WORK_MARK(1);
     __syncthreads();
     PHASE_MARK(2);
 
     // ---- bottom: T -> F (generated).  Two threads per LB-segment: the
     // trailing-zero classes never mix, class 0 goes to warps 0-3 and
     // classes 1.. to warps 4-7.
+#if AMQFT_BOTTOM_SPLIT
+    if (tid < 2 * C::NSEG) {
+      // two threads per LB-segment: class 0 on warps 0.., classes 1.. on the rest
+      const int w = tid % C::NSEG;
+      const int half = C::HP / 2;
+      const int h = w % half;
+      const int rest = w / half;
+      const int part = rest & 1, rho_bit = (rest >> 1) & 1, lam_bit = (rest >> 2) & 1;
+      const int c = part * 2 + lam_bit;
+      const int s = 2 * h + rho_bit;
+      int rho, lens, r;
+      seg_params<C::SINE>(lam_bit, s, C::LT, &rho, &lens, &r);
+      if (tid < C::NSEG)
+        Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, 0>(rho, lens, Tb + c * C::CS, Fb + c * C::CS,
+                                                              s * C::LB, tab, nmax, base, N, r, lam_bit);
+      else
+        Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, 1>(rho, lens, Tb + c * C::CS, Fb + c * C::CS,
+                                                              s * C::LB, tab, nmax, base, N, r, lam_bit);
+#else
     if (tid < C::NSEG) {
       // one thread per LB-segment (both class groups)
       const int half = C::HP / 2;
@@ -483,6 +539,7 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
                                                             s * C::LB, tab, nmax, base, N, r, lam_bit);
       Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, 1>(rho, lens, Tb + c * C::CS, Fb + c * C::CS,
                                                             s * C::LB, tab, nmax, base, N, r, lam_bit);
+#endif
     } else {
 #if AMQFT_SMALL_MODE == 1
       // the cells at multiples of LB (small top blocks): one lane per
@@ -501,6 +558,7 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       }
 #endif
     }
+    WORK_MARK(2);
     __syncthreads();
     PHASE_MARK(3);
 
@@ -515,11 +573,13 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
         SmallPar<V, C::HP, LOGN>::template serial<R, A>(c & 1, Fb + c * C::CS);
       }
 #endif
+      WORK_MARK(3);
       __syncthreads();
       PHASE_MARK(4);
       if constexpr (N / C::LB == 64) {
         // generated: each thread owns the 64 cells j*64 +- k of its chain
         if (tid < 128) Recomb<64, H / 64>::template run<R, A>((tid >> 5) & 1, Fb + (tid >> 5) * C::CS, tid & 31);
+        WORK_MARK(4);
         __syncthreads();
       } else {
 #pragma unroll 1
@@ -531,8 +591,9 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
     } else {
       if (tid < 4 * C::LB) {
         const int c = tid >> LOGLB, v = tid & (C::LB - 1);
-        if (v > 0) Top<C::LB, C::LT, LOGN, C::SINE>::template bwd<R, A>(c & 1, Fb + c * C::CS, v, tab, base);
+        if (v > 0) Top<C::LB, C::LT, LOGN, C::SINE>::template bwd<R, A>(c & 1, Fb + c * C::CS, v, ltab, base);
       }
+      WORK_MARK(4);
       __syncthreads();
     }
     PHASE_MARK(5);
@@ -569,8 +630,27 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       y[k] = lo;
       if (k != 0 && k != H) y[N - k] = hi;
     }
-    __syncthreads();
+    WORK_MARK(5);
+    // No barrier here: the next row's load writes only T (and the staging
+    // buffer through TMA), whose last readers are behind earlier barriers;
+    // F is next written after two more barriers.
     PHASE_MARK(6);
+  }
+}
+
+// Per-level compacted constants for the top mirror levels:
+// ltab[off_i + u] = tab[u * nmax / (2 L_i) - 1] (bitwise the TrigTable
+// values), L_i = H >> (i-1), u in [1, L_i/2), so a warp's lanes (consecutive
+// v) read consecutive words at every level.
+template <typename R>
+__global__ void k_level_table(const R* __restrict__ tab, R* __restrict__ ltab, int H, int LT,
+                              int nmax) {
+  int off = 0;
+  for (int i = 1; i <= LT; ++i) {
+    const int L = H >> (i - 1);
+    for (int u = threadIdx.x + blockIdx.x * blockDim.x; u < L / 2; u += blockDim.x * gridDim.x)
+      ltab[off + u] = u == 0 ? R(0) : tab[u * (nmax / (2 * L)) - 1];
+    off += L / 2;
   }
 }
 
@@ -591,12 +671,18 @@ class FastPlanImpl final : public FastPlan {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     grid_cap_ = std::max(1, per_sm) * sms;
     launches = 1;
+    e = cudaMalloc(&ltab_, sizeof(R) * C::H);
+    if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+    k_level_table<R><<<8, 256>>>(tab_, ltab_, C::H, C::LT, static_cast<int>(nmax_));
+    e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
   }
+  ~FastPlanImpl() override { if (ltab_) cudaFree(ltab_); }
   void exec(const void* in, void* out, size_t rows, int inverse, cudaStream_t st) override {
     using C = Cfg<V, R, LOGN, LOGLB>;
     const unsigned grid = static_cast<unsigned>(std::min<size_t>(rows, static_cast<size_t>(grid_cap_)));
     k_fast<V, R, LOGN, LOGLB><<<grid, C::NT, C::SMEM, st>>>(
-        static_cast<const R*>(in), static_cast<R*>(out), rows, tab_, static_cast<int>(nmax_),
+        static_cast<const R*>(in), static_cast<R*>(out), rows, tab_, ltab_, static_cast<int>(nmax_),
         inverse, R(1) / R(C::N));
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
@@ -604,6 +690,7 @@ class FastPlanImpl final : public FastPlan {
 
  private:
   const R* tab_;
+  R* ltab_ = nullptr;
   uint32_t nmax_;
   int grid_cap_ = 148;
 };

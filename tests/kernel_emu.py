@@ -36,6 +36,7 @@ def lib():
         L.host_bottom.argtypes = [i, i, i, i, dp, dp, i, dp, i, d, i, i, i, i]
         L.host_small.argtypes = [i, i, i, i, i, dp, dp, dp, d]
         L.host_recomb.argtypes = [i, i, i, dp, i]
+        L.host_fold.argtypes = [i, i, i, dp, i]
         L.host_smallpar.argtypes = [i, i, i, i, i, i, dp, dp, dp, d, i, dp]
         _lib = L
     return _lib
@@ -173,6 +174,13 @@ def emulate(v, N, LB, x, tab, base):
     F = np.zeros(4 * CS + 8)
     tab = np.ascontiguousarray(tab, dtype=np.float64)
     tp = tab.ctypes.data
+    # per-level compacted table for the top levels (fast_kernel.cuh k_level_table)
+    lt = []
+    for lvl in range(1, LT + 1):
+        Lv = H >> (lvl - 1)
+        lt += [0.0 if u == 0 else tab[u * (N // (2 * Lv)) - 1] for u in range(Lv // 2)]
+    ltab = np.ascontiguousarray(lt + [0.0], dtype=np.float64)
+    ltp = ltab.ctypes.data
     Tp, Fp = T.ctypes.data, F.ctypes.data
     x = np.asarray(x, dtype=np.float64)
     re, im = x[0::2], x[1::2]
@@ -188,15 +196,20 @@ def emulate(v, N, LB, x, tab, base):
     if TM:
         for c in range(4):
             for vv in range(1, LB):
-                assert L.host_top(LB, LT, LOGN, SINE, 0, c & 1, Tp + 8 * c * CS, vv, tp, base) == 0
+                assert L.host_top(LB, LT, LOGN, SINE, 0, c & 1, Tp + 8 * c * CS, vv, ltp, base) == 0
             for cls in range(LT + 1):
                 assert L.host_smallpar(v, HP, LOGN, LB, c & 1, cls, Tp + 8 * c * CS, Fp + 8 * c * CS,
                                        tp, base, 0, None) == 0
     else:
-        n = N
-        while n >= 2 * (N // LB):
-            _chain_level(T, CS, n, True)
-            n >>= 1
+        if N // LB == 64:
+            for c in range(4):
+                for k in range(32):
+                    assert L.host_fold(64, H // 64, c & 1, Tp + 8 * c * CS, k) == 0
+        else:
+            n = N
+            while n >= 2 * (N // LB):
+                _chain_level(T, CS, n, True)
+                n >>= 1
         if v in (3, 7):
             for depth in range(LT):
                 _am_level(T, CS, N, LOGLB, depth, v, SINE, False)
@@ -239,7 +252,7 @@ def emulate(v, N, LB, x, tab, base):
     else:
         for c in range(4):
             for vv in range(1, LB):
-                assert L.host_top(LB, LT, LOGN, SINE, 1, c & 1, Fp + 8 * c * CS, vv, tp, base) == 0
+                assert L.host_top(LB, LT, LOGN, SINE, 1, c & 1, Fp + 8 * c * CS, vv, ltp, base) == 0
     out = np.zeros(2 * N)
     for k in range(H + 1):
         rd, idd = F[0 * CS + pf(k, 0)], F[2 * CS + pf(k, 0)]

@@ -136,4 +136,9 @@ int host_recomb(int W, int HW, int lam, double* F, int k) {
   return -1;
 }
 
+int host_fold(int W, int HW, int lam, double* F, int k) {
+  if (W == 64 && HW == 32) { Recomb<64, 32>::fold<double, HA>(lam, F, k); return 0; }
+  return -1;
+}
+
 }  // extern "C"

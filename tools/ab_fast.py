@@ -25,7 +25,7 @@ for path in sorted(glob.glob(os.path.join(HERE, "ab_*.so"))):
         for rep in range(4):
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record()
-            lib.pt_run(v, x.data_ptr(), y.data_ptr(), rows, dtab.data_ptr(), N, cyc, 148 * 2)
+            lib.pt_run(v, x.data_ptr(), y.data_ptr(), rows, dtab.data_ptr(), N, cyc, 148 * int(os.path.basename(path).split('_m')[-1].split('.')[0]) if '_m' in path else 296)
             e.record()
             torch.cuda.synchronize()
             ts.append(s.elapsed_time(e))

@@ -3,6 +3,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -shared -Xcompiler -fPIC \
 //        -o tools/libphase_timing.so tools/phase_timing.cu
 #define AMQFT_PHASE_TIMING
+#include <cstdio>
 #ifndef AMQFT_FAST_MINB
 #define AMQFT_FAST_MINB 2
 #endif
@@ -18,9 +19,22 @@ static int run_v(const float* in, float* out, size_t rows, const float* tab, int
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
   unsigned long long z[16] = {0};
   cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
-  fn<<<grid, C::NT, C::SMEM>>>(in, out, rows, tab, nmax, 0, 1.0f / 4096);
+  unsigned long long zz[16][16] = {{0}};
+  cudaMemcpyToSymbol(g_warp_work, zz, sizeof(zz));
+  float* ltab = nullptr;
+  cudaMalloc(&ltab, sizeof(float) * C::H);
+  k_level_table<float><<<8, 256>>>(tab, ltab, C::H, C::LT, nmax);
+  fn<<<grid, C::NT, C::SMEM>>>(in, out, rows, tab, ltab, nmax, 0, 1.0f / 4096);
   cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(cyc, g_phase_cycles, sizeof(z));
+  cudaFree(ltab);
+  unsigned long long ww[16][16];
+  cudaMemcpyFromSymbol(ww, g_warp_work, sizeof(ww));
+  for (int p = 0; p < 6; ++p) {
+    printf("  phase %d warp work:", p);
+    for (int w = 0; w < C::NT / 32; ++w) printf(" %6llu", ww[p][w] / (rows / grid));
+    printf("\n");
+  }
   return (int)cudaGetLastError();
 }
 
