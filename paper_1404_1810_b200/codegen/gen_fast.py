@@ -401,14 +401,25 @@ def gen_top(LB, LT, direction, lam, sine, nlog):
     K = 1 << (LT - 1)          # cells per parity
     H = W * K
     em = Emitter()
+    # 'fwd' (time-major T): odd LB-segments are stored reversed (cell
+    # a + u at a + LB - u, see Cfg::pt), so (k+1)W - v sits at
+    # (2k+1) LB + v: every cell of the thread is B + v + s (LB + 1).
+    rev = direction == "fwd"
+    def addr(z):
+        k = z // 2
+        if rev:
+            return "pe", z * (LB + 1)
+        return ("pe", k * (W + 2)) if z % 2 == 0 else ("po", (k + 1) * (W + 2))
     em.emit("R* __restrict__ pe = B + v;")
-    em.emit("R* __restrict__ po = B - v - 1;")
+    if not rev:
+        em.emit("R* __restrict__ po = B - v - 1;")
     x = {}
     for k in range(K):
         x[2 * k] = f"x{2 * k}"
         x[2 * k + 1] = f"x{2 * k + 1}"
-        em.emit(f"R x{2 * k} = pe[{k * (W + 2)}];")
-        em.emit(f"R x{2 * k + 1} = po[{(k + 1) * (W + 2)}];")
+        for z in (2 * k, 2 * k + 1):
+            b_, o_ = addr(z)
+            em.emit(f"R x{z} = {b_}[{o_}];")
     # offsets of cells from 0: z_2k = kW + v (+v), z_2k+1 = (k+1)W - v (-v)
     def off(z):
         k = z // 2
@@ -473,9 +484,9 @@ def gen_top(LB, LT, direction, lam, sine, nlog):
                     em.emit(f"  const R e{t} = {p_}; {p_} = {add('o' + str(t), 'e' + str(t))}; "
                             f"{q_} = {sub('o' + str(t), 'e' + str(t))};")
         em.emit("}")
-    for k in range(K):
-        em.emit(f"pe[{k * (W + 2)}] = x{2 * k};")
-        em.emit(f"po[{(k + 1) * (W + 2)}] = x{2 * k + 1};")
+    for z in range(2 * K):
+        b_, o_ = addr(z)
+        em.emit(f"{b_}[{o_}] = x{z};")
     sig = (f"template <typename R, typename AR>\n__device__ __forceinline__ void "
            f"top_{direction}_lb{LB}_lt{LT}_n{nlog}_l{lam}_s{sine}(R* __restrict__ B, int v, "
            f"const R* __restrict__ ltab, R base)")

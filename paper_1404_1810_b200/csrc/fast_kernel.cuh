@@ -79,9 +79,30 @@ struct Cfg {
   // recombination sets j*64 +- k at immediate offsets).
   // The pad is shifted per chain (31 for Dct chains, 0 for Dst chains) so
   // every lane's 32-cell class run lies inside one padded block.
+  // Chain bases.  The bottom's warps pair chain c with chain c+2 (same
+  // orientation and lens, so no divergence); the Im chains are shifted so
+  // the two halves of the warp hit disjoint banks: by 1 word on the skewed
+  // buffer (lanes cover even banks) and by 16 on the padded one (lanes
+  // cover a 16-bank half).  Modelled in tools/bank_model.cpp.
+  static constexpr int SH_SKEW = 1, SH_SWZ = 16;
+  static __host__ __device__ __forceinline__ constexpr int co_sk(int c) { return c * CS + (c >> 1) * SH_SKEW; }
+  static __host__ __device__ __forceinline__ constexpr int co_sw(int c) { return c * CS + (c >> 1) * SH_SWZ; }
+  static __host__ __device__ __forceinline__ constexpr int coT(int c) { return TM ? co_sk(c) : co_sw(c); }
+  static __host__ __device__ __forceinline__ constexpr int coF(int c) { return TM ? co_sw(c) : co_sk(c); }
   static __device__ __forceinline__ int skew(int i) { return i + (i >> LOGLB); }
   static __device__ __forceinline__ int swz(int i, int lam) { return i + ((i + (lam ? 0 : 31)) >> 5); }
-  static __device__ __forceinline__ int pt(int i, int lam) { return TM ? skew(i) : swz(i, lam); }
+  // Time-major T: odd LB-segments are stored reversed (cell a + u at
+  // a + LB - u, 0 < u < LB).  A reversed segment is exactly the
+  // orientation-1 segment of the mirror network (fast_model: rho = 1 swaps
+  // the roles of a + v and a + L - v at every level), so the bottom runs one
+  // code path (rho = 0) for every segment and the top's cells are all
+  // B + v + s (LB + 1).
+  static __device__ __forceinline__ int tpos(int i) {
+    const int s = i >> LOGLB, u = i & (LB - 1);
+    const int j = ((s & 1) && u) ? i + LB - 2 * u : i;
+    return j + s;
+  }
+  static __device__ __forceinline__ int pt(int i, int lam) { return TM ? tpos(i) : swz(i, lam); }
   static __device__ __forceinline__ int pf(int i, int lam) { return TM ? swz(i, lam) : skew(i); }
 };
 
@@ -113,7 +134,7 @@ __device__ __forceinline__ void chain_level(R* B, int n) {
     const int k = g & (q - 1);
     const int lam = c & 1;
     if (lam && k == 0) continue;
-    R* ch = B + c * C::CS;
+    R* ch = B + C::co_sw(c);
     const int i0 = C::swz(k, lam), i1 = C::swz((n >> 1) - k, lam);
     const R e = ch[i0], o = ch[i1];
     if (!FWD) {  // elaborations.cpp:310-329
@@ -183,7 +204,7 @@ __device__ __forceinline__ void am_chains(R* B) {
     const int r = rem - t * classes;
     const int q = C::N >> (t + DEPTH + 3);
     if (q < 2) continue;
-    chain_class<C, DEPTH, R>(B + c * C::CS, c & 1, t, r);
+    chain_class<C, DEPTH, R>(B + C::co_sw(c), c & 1, t, r);
   }
   __syncthreads();
 }
@@ -314,7 +335,7 @@ __device__ __forceinline__ void am_phase_regs(R* B) {
   const int nl = 32 >> tt;                       // lanes of this block
   const int cell0 = (C::N >> (tt + 1)) - lam_c - (i << LOGR);
   // runs end on a padded-block boundary: phys(cell0 - l) = phys(cell0) - l - l/32
-  R* chb = B + (c & 3) * C::CS + C::swz(cell0, lam_c);
+  R* chb = B + C::co_sw(c & 3) + C::swz(cell0, lam_c);
   R x[RR];
 #pragma unroll
   for (int l = 0; l < RR; ++l) x[l] = active ? chb[-(l + (l >> 5))] : R(0);
@@ -325,6 +346,72 @@ __device__ __forceinline__ void am_phase_regs(R* B) {
 #pragma unroll
     for (int l = 0; l < RR; ++l) chb[-(l + (l >> 5))] = x[l];
   }
+}
+
+// ---- Multiples of 32 (the k = 0 class of the generated recombination,
+// N = 4096: cells y = 32 i, i in [0, 64], physical 33 i in both pads), one
+// warp per chain instead of one serial lane: lane l holds i = l and
+// i = 64 - l, lane 0 also i = 32.  Level t (n = 128 << t) pairs
+// (i, 2^(t+1) - i), i < 2^t: in-lane at t = 5 and for lane 0 at t = 4,
+// one shuffle otherwise.  Same operations and operand order as
+// codegen/gen_fast.py emit_pair (Dct chains use every cell; Dst chains skip
+// i = 0 and i = 64), so the fp64 instance stays bitwise.
+template <typename R, bool FOLD>
+__device__ __forceinline__ void pair_op(int lam, R e, R o, R& e2, R& o2) {
+  using A = Arith<R>;
+  if (!FOLD) {  // SplitTimeParity bwd (elaborations.cpp:310-329)
+    e2 = lam ? A::add(o, e) : A::add(e, o);
+    o2 = lam ? A::sub(o, e) : A::sub(e, o);
+  } else {      // SplitHarmonicParity fwd (elaborations.cpp:238-255)
+    e2 = lam ? A::sub(e, o) : A::add(e, o);
+    o2 = lam ? A::add(e, o) : A::sub(e, o);
+  }
+}
+
+template <typename R, bool FOLD>
+__device__ __forceinline__ void special_class64(R* ch, int lam, int lane) {
+  R a = ch[33 * lane], b = ch[33 * (64 - lane)];
+  R m = lane == 0 ? ch[33 * 32] : R(0);
+  auto level = [&](int t) {
+    if (t == 5) {
+      if (!(lam && lane == 0)) {
+        R e2, o2;
+        pair_op<R, FOLD>(lam, a, b, e2, o2);
+        a = e2;
+        b = o2;
+      }
+      return;
+    }
+    const int P = 2 << t, Hh = 1 << t;
+    const int src = lane <= P ? (P - lane) & 31 : lane;
+    const R pv = __shfl_sync(0xffffffffu, a, src);
+    R e2, o2;
+    if (lane == 0) {
+      if (!lam) {
+        pair_op<R, FOLD>(lam, a, t == 4 ? m : pv, e2, o2);
+        a = e2;
+        if (t == 4) m = o2;
+      }
+    } else if (lane < Hh) {
+      pair_op<R, FOLD>(lam, a, pv, e2, o2);
+      a = e2;
+    } else if (lane > Hh && lane <= P && !(lam && lane == P)) {
+      pair_op<R, FOLD>(lam, pv, a, e2, o2);
+      a = o2;
+    }
+  };
+  if (FOLD) {
+#pragma unroll
+    for (int t = 5; t >= 0; --t) level(t);
+  } else {
+#pragma unroll
+    for (int t = 0; t <= 5; ++t) level(t);
+  }
+  if (!(lam && lane == 0)) {
+    ch[33 * lane] = a;
+    ch[33 * (64 - lane)] = b;
+  }
+  if (lane == 0 && !lam) ch[33 * 32] = m;
 }
 
 // ---- TMA bulk staging of the next row (cp.async.bulk + mbarrier).
@@ -445,15 +532,15 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       V2 a = x[m];
       if (inverse) { const R tmp = a.x; a.x = a.y; a.y = tmp; }
       if (m == 0 || m == H) {
-        Tb[0 * C::CS + C::pt(m, 0)] = a.x;
-        Tb[2 * C::CS + C::pt(m, 0)] = a.y;
+        Tb[C::coT(0) + C::pt(m, 0)] = a.x;
+        Tb[C::coT(2) + C::pt(m, 0)] = a.y;
       } else {
         V2 b = x[N - m];
         if (inverse) { const R tmp = b.x; b.x = b.y; b.y = tmp; }
-        Tb[0 * C::CS + C::pt(m, 0)] = A::add(a.x, b.x);
-        Tb[1 * C::CS + C::pt(m, 1)] = A::sub(a.x, b.x);
-        Tb[2 * C::CS + C::pt(m, 0)] = A::add(a.y, b.y);
-        Tb[3 * C::CS + C::pt(m, 1)] = A::sub(a.y, b.y);
+        Tb[C::coT(0) + C::pt(m, 0)] = A::add(a.x, b.x);
+        Tb[C::coT(1) + C::pt(m, 1)] = A::sub(a.x, b.x);
+        Tb[C::coT(2) + C::pt(m, 0)] = A::add(a.y, b.y);
+        Tb[C::coT(3) + C::pt(m, 1)] = A::sub(a.y, b.y);
       }
     }
     WORK_MARK(0);
@@ -470,16 +557,18 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       // top mirror levels (generated, 2^LT cells per thread) || small chains
       if (tid < 4 * C::LB) {
         const int c = tid >> LOGLB, v = tid & (C::LB - 1);
-        if (v > 0) Top<C::LB, C::LT, LOGN, C::SINE>::template fwd<R, A>(c & 1, Tb + c * C::CS, v, ltab, base);
-#if AMQFT_SMALL_MODE == 0
-        else SmallFull<V, C::HP, LOGN>::template run<R, A, LOGLB, C::LB>(c & 1, Tb + c * C::CS,
-                                                                         Fb + c * C::CS, tab, base);
-#endif
+        if (v > 0) Top<C::LB, C::LT, LOGN, C::SINE>::template fwd<R, A>(c & 1, Tb + C::coT(c), v, ltab, base);
       }
     } else {
       if constexpr (N / C::LB == 64) {
         // generated: each thread owns the 64 cells j*64 +- k of its chain
-        if (tid < 128) Recomb<64, H / 64>::template fold<R, A>((tid >> 5) & 1, Tb + (tid >> 5) * C::CS, tid & 31);
+        // warps 0-3: the 64 cells j*64 +- k of k = lane (lane 0 idle);
+        // warps 4-7: the multiples of 32 of chain warp-4, cooperatively
+        if (tid < 128) {
+          if (tid & 31) Recomb<64, H / 64>::template fold<R, A>((tid >> 5) & 1, Tb + C::coT(tid >> 5), tid & 31);
+        } else if (tid < 256) {
+          special_class64<R, true>(Tb + C::coT((tid >> 5) - 4), (tid >> 5) & 1, tid & 31);
+        }
         __syncthreads();
       } else {
 #pragma unroll 1
@@ -495,7 +584,7 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
 #if AMQFT_SMALL_MODE == 1
       if ((tid & 63) == 63 && tid < 256) {
         const int c = tid >> 6;
-        SmallPar<V, C::HP, LOGN>::template serial<R, A>(c & 1, Tb + c * C::CS);
+        SmallPar<V, C::HP, LOGN>::template serial<R, A>(c & 1, Tb + C::coT(c));
       }
 #endif
     }
@@ -518,11 +607,12 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       const int s = 2 * h + rho_bit;
       int rho, lens, r;
       seg_params<C::SINE>(lam_bit, s, C::LT, &rho, &lens, &r);
+      if constexpr (C::TM) rho = 0;   // odd segments are stored reversed (Cfg::tpos)
       if (tid < C::NSEG)
-        Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, 0>(rho, lens, Tb + c * C::CS, Fb + c * C::CS,
+        Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, 0>(rho, lens, Tb + C::coT(c), Fb + C::coF(c),
                                                               s * C::LB, tab, nmax, base, N, r, lam_bit);
       else
-        Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, 1>(rho, lens, Tb + c * C::CS, Fb + c * C::CS,
+        Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, 1>(rho, lens, Tb + C::coT(c), Fb + C::coF(c),
                                                               s * C::LB, tab, nmax, base, N, r, lam_bit);
 #else
     if (tid < C::NSEG) {
@@ -535,9 +625,10 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       const int s = 2 * h + rho_bit;
       int rho, lens, r;
       seg_params<C::SINE>(lam_bit, s, C::LT, &rho, &lens, &r);
-      Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, 0>(rho, lens, Tb + c * C::CS, Fb + c * C::CS,
+      if constexpr (C::TM) rho = 0;   // odd segments are stored reversed (Cfg::tpos)
+      Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, 0>(rho, lens, Tb + C::coT(c), Fb + C::coF(c),
                                                             s * C::LB, tab, nmax, base, N, r, lam_bit);
-      Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, 1>(rho, lens, Tb + c * C::CS, Fb + c * C::CS,
+      Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, 1>(rho, lens, Tb + C::coT(c), Fb + C::coF(c),
                                                             s * C::LB, tab, nmax, base, N, r, lam_bit);
 #endif
     } else {
@@ -548,13 +639,19 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       const int l = tid - C::NSEG;
       if (l < 4 * SP::NCLS) {
         const int c = l / SP::NCLS, cls = l - c * SP::NCLS;
-        SP::template cls<R, A, LOGLB, C::LB>(c & 1, cls, Tb + c * C::CS, Fb + c * C::CS, tab, base);
+        SP::template cls<R, A, LOGLB, C::LB>(c & 1, cls, Tb + C::coT(c), Fb + C::coF(c), tab, base);
       }
 #else
-      if constexpr (!C::TM) {
-        const int l = tid - C::NSEG;
-        if (l < 4) SmallFull<V, C::HP, LOGN>::template run<R, A, LOGLB, C::LB>(l & 1, Tb + l * C::CS,
-                                                                             Fb + l * C::CS, tab, base);
+      // the small chains (cells at multiples of LB; disjoint from the
+      // segments' cells in T and F), one lane per chain, one warp each
+      // where the block has spare warps
+      constexpr int SPARE = C::NT - C::NSEG;
+      constexpr int STR = SPARE / 4 >= 32 ? 32 : SPARE / 4;
+      const int l = tid - C::NSEG;
+      if (l % STR == 0 && l / STR < 4) {
+        const int cc = l / STR;
+        SmallFull<V, C::HP, LOGN>::template run<R, A, LOGLB, C::LB>(cc & 1, Tb + C::coT(cc), Fb + C::coF(cc),
+                                                                     tab, base);
       }
 #endif
     }
@@ -570,7 +667,7 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
 #if AMQFT_SMALL_MODE == 1
       if ((tid & 63) == 63 && tid < 256) {
         const int c = tid >> 6;
-        SmallPar<V, C::HP, LOGN>::template serial<R, A>(c & 1, Fb + c * C::CS);
+        SmallPar<V, C::HP, LOGN>::template serial<R, A>(c & 1, Fb + C::coF(c));
       }
 #endif
       WORK_MARK(3);
@@ -578,7 +675,12 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       PHASE_MARK(4);
       if constexpr (N / C::LB == 64) {
         // generated: each thread owns the 64 cells j*64 +- k of its chain
-        if (tid < 128) Recomb<64, H / 64>::template run<R, A>((tid >> 5) & 1, Fb + (tid >> 5) * C::CS, tid & 31);
+        // as the fold: warps 0-3 the k = lane sets, warps 4-7 the multiples of 32
+        if (tid < 128) {
+          if (tid & 31) Recomb<64, H / 64>::template run<R, A>((tid >> 5) & 1, Fb + C::coF(tid >> 5), tid & 31);
+        } else if (tid < 256) {
+          special_class64<R, false>(Fb + C::coF((tid >> 5) - 4), (tid >> 5) & 1, tid & 31);
+        }
         WORK_MARK(4);
         __syncthreads();
       } else {
@@ -591,7 +693,7 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
     } else {
       if (tid < 4 * C::LB) {
         const int c = tid >> LOGLB, v = tid & (C::LB - 1);
-        if (v > 0) Top<C::LB, C::LT, LOGN, C::SINE>::template bwd<R, A>(c & 1, Fb + c * C::CS, v, ltab, base);
+        if (v > 0) Top<C::LB, C::LT, LOGN, C::SINE>::template bwd<R, A>(c & 1, Fb + C::coF(c), v, ltab, base);
       }
       WORK_MARK(4);
       __syncthreads();
@@ -608,16 +710,16 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
     for (int it = 0; it < (H + C::NT) / C::NT; ++it) {
       const int k = tid + it * C::NT;
       if (k > H) break;
-      const R rd = Fb[0 * C::CS + C::pf(k, 0)];
-      const R id = Fb[2 * C::CS + C::pf(k, 0)];
+      const R rd = Fb[C::coF(0) + C::pf(k, 0)];
+      const R id = Fb[C::coF(2) + C::pf(k, 0)];
       V2 lo, hi;
       if (k == 0 || k == H) {
         lo.x = rd;
         lo.y = id;
         hi = lo;
       } else {
-        const R rs = Fb[1 * C::CS + C::pf(k, 1)];
-        const R is = Fb[3 * C::CS + C::pf(k, 1)];
+        const R rs = Fb[C::coF(1) + C::pf(k, 1)];
+        const R is = Fb[C::coF(3) + C::pf(k, 1)];
         lo.x = A::add(rd, is);
         lo.y = A::sub(id, rs);
         hi.x = A::sub(rd, is);

@@ -168,7 +168,11 @@ def emulate(v, N, LB, x, tab, base):
     TM = v in (1, 4, 5, 8)
     SINE = 1 if v >= 5 else 0
     skew = lambda i: i + (i >> LOGLB)  # noqa: E731
-    pt = (lambda i, lam: skew(i)) if TM else _swz
+    def tpos(i):  # Cfg::tpos: odd LB-segments stored reversed
+        s_, u_ = i >> LOGLB, i & (LB - 1)
+        j = i + LB - 2 * u_ if (s_ & 1) and u_ else i
+        return j + s_
+    pt = (lambda i, lam: tpos(i)) if TM else _swz
     pf = _swz if TM else (lambda i, lam: skew(i))
     T = np.zeros(4 * CS + 8)
     F = np.zeros(4 * CS + 8)
@@ -197,9 +201,6 @@ def emulate(v, N, LB, x, tab, base):
         for c in range(4):
             for vv in range(1, LB):
                 assert L.host_top(LB, LT, LOGN, SINE, 0, c & 1, Tp + 8 * c * CS, vv, ltp, base) == 0
-            for cls in range(LT + 1):
-                assert L.host_smallpar(v, HP, LOGN, LB, c & 1, cls, Tp + 8 * c * CS, Fp + 8 * c * CS,
-                                       tp, base, 0, None) == 0
     else:
         if N // LB == 64:
             for c in range(4):
@@ -225,8 +226,15 @@ def emulate(v, N, LB, x, tab, base):
         c = part * 2 + lam_bit
         s = 2 * h + rho_bit
         rho, lens, r = seg_params(SINE, lam_bit, s, LT)
+        if TM:
+            rho = 0  # reversed odd segments (Cfg::tpos)
         assert L.host_bottom(v, LB, rho, lens, Tp + 8 * c * CS, Fp + 8 * c * CS, s * LB, tp, N,
                              base, N, LT, r, lam_bit) == 0
+    if TM:  # the small chain runs beside the bottom (disjoint cells)
+        for c in range(4):
+            for cls in range(LT + 1):
+                assert L.host_smallpar(v, HP, LOGN, LB, c & 1, cls, Tp + 8 * c * CS, Fp + 8 * c * CS,
+                                       tp, base, 0, None) == 0
     for c in range(4):
         if TM:
             assert L.host_smallpar(v, HP, LOGN, LB, c & 1, 0, None, None, tp, base, 1, Fp + 8 * c * CS) == 0

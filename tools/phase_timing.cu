@@ -1,6 +1,6 @@
 // phase_timing.cu -- DIAGNOSTIC build of the fused kernel with per-phase
 // clock64() accounting (CTA 0).  Not part of the product library.
-//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -shared -Xcompiler -fPIC \
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 --expt-relaxed-constexpr -shared -Xcompiler -fPIC \
 //        -o tools/libphase_timing.so tools/phase_timing.cu
 #define AMQFT_PHASE_TIMING
 #include <cstdio>
