@@ -401,10 +401,11 @@ def gen_top(LB, LT, direction, lam, sine, nlog):
     K = 1 << (LT - 1)          # cells per parity
     H = W * K
     em = Emitter()
-    # 'fwd' (time-major T): odd LB-segments are stored reversed (cell
-    # a + u at a + LB - u, see Cfg::pt), so (k+1)W - v sits at
-    # (2k+1) LB + v: every cell of the thread is B + v + s (LB + 1).
-    rev = direction == "fwd"
+    # The index-space buffer (T time-major, F harmonic-major) stores odd
+    # LB-segments reversed (cell a + u at a + LB - u, see Cfg::ipos), so
+    # (k+1)W - v sits at (2k+1) LB + v: every cell of the thread is
+    # B + v + s (LB + 1).
+    rev = True
     def addr(z):
         k = z // 2
         if rev:

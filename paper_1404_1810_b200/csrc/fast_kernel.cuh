@@ -91,19 +91,19 @@ struct Cfg {
   static __host__ __device__ __forceinline__ constexpr int coF(int c) { return TM ? co_sw(c) : co_sk(c); }
   static __device__ __forceinline__ int skew(int i) { return i + (i >> LOGLB); }
   static __device__ __forceinline__ int swz(int i, int lam) { return i + ((i + (lam ? 0 : 31)) >> 5); }
-  // Time-major T: odd LB-segments are stored reversed (cell a + u at
-  // a + LB - u, 0 < u < LB).  A reversed segment is exactly the
-  // orientation-1 segment of the mirror network (fast_model: rho = 1 swaps
-  // the roles of a + v and a + L - v at every level), so the bottom runs one
-  // code path (rho = 0) for every segment and the top's cells are all
-  // B + v + s (LB + 1).
-  static __device__ __forceinline__ int tpos(int i) {
+  // The index-space buffer (T time-major, F harmonic-major) stores odd
+  // LB-segments reversed (cell a + u at a + LB - u, 0 < u < LB), skewed.
+  // A reversed segment is exactly the orientation-1 segment of the mirror
+  // network (fast_model: rho = 1 swaps the roles of a + v and a + L - v at
+  // every level), so the bottom runs one code path (rho = 0) for every
+  // segment and the top's cells are all B + v + s (LB + 1).
+  static __device__ __forceinline__ int ipos(int i) {
     const int s = i >> LOGLB, u = i & (LB - 1);
     const int j = ((s & 1) && u) ? i + LB - 2 * u : i;
     return j + s;
   }
-  static __device__ __forceinline__ int pt(int i, int lam) { return TM ? tpos(i) : swz(i, lam); }
-  static __device__ __forceinline__ int pf(int i, int lam) { return TM ? swz(i, lam) : skew(i); }
+  static __device__ __forceinline__ int pt(int i, int lam) { return TM ? ipos(i) : swz(i, lam); }
+  static __device__ __forceinline__ int pf(int i, int lam) { return TM ? swz(i, lam) : ipos(i); }
 };
 
 // Segment parameters at depth d: orientation, lens, residue (fast_model.segment_params).
@@ -607,7 +607,7 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       const int s = 2 * h + rho_bit;
       int rho, lens, r;
       seg_params<C::SINE>(lam_bit, s, C::LT, &rho, &lens, &r);
-      if constexpr (C::TM) rho = 0;   // odd segments are stored reversed (Cfg::tpos)
+      rho = 0;   // odd segments are stored reversed (Cfg::ipos)
       if (tid < C::NSEG)
         Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, 0>(rho, lens, Tb + C::coT(c), Fb + C::coF(c),
                                                               s * C::LB, tab, nmax, base, N, r, lam_bit);
@@ -625,7 +625,7 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       const int s = 2 * h + rho_bit;
       int rho, lens, r;
       seg_params<C::SINE>(lam_bit, s, C::LT, &rho, &lens, &r);
-      if constexpr (C::TM) rho = 0;   // odd segments are stored reversed (Cfg::tpos)
+      rho = 0;   // odd segments are stored reversed (Cfg::ipos)
       Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, 0>(rho, lens, Tb + C::coT(c), Fb + C::coF(c),
                                                             s * C::LB, tab, nmax, base, N, r, lam_bit);
       Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, 1>(rho, lens, Tb + C::coT(c), Fb + C::coF(c),

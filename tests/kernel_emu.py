@@ -168,12 +168,12 @@ def emulate(v, N, LB, x, tab, base):
     TM = v in (1, 4, 5, 8)
     SINE = 1 if v >= 5 else 0
     skew = lambda i: i + (i >> LOGLB)  # noqa: E731
-    def tpos(i):  # Cfg::tpos: odd LB-segments stored reversed
+    def tpos(i):  # Cfg::ipos: odd LB-segments stored reversed
         s_, u_ = i >> LOGLB, i & (LB - 1)
         j = i + LB - 2 * u_ if (s_ & 1) and u_ else i
         return j + s_
     pt = (lambda i, lam: tpos(i)) if TM else _swz
-    pf = _swz if TM else (lambda i, lam: skew(i))
+    pf = _swz if TM else (lambda i, lam: tpos(i))
     T = np.zeros(4 * CS + 8)
     F = np.zeros(4 * CS + 8)
     tab = np.ascontiguousarray(tab, dtype=np.float64)
@@ -226,8 +226,7 @@ def emulate(v, N, LB, x, tab, base):
         c = part * 2 + lam_bit
         s = 2 * h + rho_bit
         rho, lens, r = seg_params(SINE, lam_bit, s, LT)
-        if TM:
-            rho = 0  # reversed odd segments (Cfg::tpos)
+        rho = 0  # reversed odd segments (Cfg::ipos)
         assert L.host_bottom(v, LB, rho, lens, Tp + 8 * c * CS, Fp + 8 * c * CS, s * LB, tp, N,
                              base, N, LT, r, lam_bit) == 0
     if TM:  # the small chain runs beside the bottom (disjoint cells)
