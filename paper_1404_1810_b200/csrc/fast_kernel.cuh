@@ -468,19 +468,16 @@ __device__ unsigned long long g_warp_work[16][16];
 #define WORK_MARK(k) do {} while (0)
 #endif
 
-template <int V, typename R, int LOGN, int LOGLB>
+template <int V, typename R, int LOGN, int LOGLB, bool INV>
 #ifndef AMQFT_SMALL_MODE
 #define AMQFT_SMALL_MODE 0   // 0: serial small chain on spare lanes (measured best); 1: split into classes
-#endif
-#ifndef AMQFT_UNROLL_IO
-#define AMQFT_UNROLL_IO 1
 #endif
 #ifndef AMQFT_FAST_MINB
 #define AMQFT_FAST_MINB 2
 #endif
 __global__ void __launch_bounds__(Cfg<V, R, LOGN, LOGLB>::NT, (sizeof(R) == 4 ? AMQFT_FAST_MINB : 1))
 k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
-       const R* __restrict__ tab, const R* __restrict__ ltab, int nmax, int inverse, R scale) {
+       const R* __restrict__ tab, const R* __restrict__ ltab, int nmax, R scale) {
 #ifdef AMQFT_PHASE_TIMING
   long long t_prev = 0, w_start = 0;
 #endif
@@ -496,6 +493,13 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
   const R base = __ldg(tab + (nmax / 4 - 1));
   constexpr int N = C::N, H = C::H;
   constexpr uint32_t ROW_BYTES = 2 * N * sizeof(R);
+  // load/store: 256 threads, cells tid + 256 it; address steps per it
+  constexpr int IO_T = 256, IO_IT = H / IO_T;
+  static_assert(H % IO_T == 0 && C::NT >= IO_T, "IO tiling");
+  constexpr int IDX_STEP = IO_T + IO_T / C::LB;          // ipos: skew by segment
+  constexpr int SWZ_STEP = IO_T + IO_T / 32;             // swz: one pad per 32
+  constexpr int PT_STEP = C::TM ? IDX_STEP : SWZ_STEP;
+  constexpr int PF_STEP = C::TM ? SWZ_STEP : IDX_STEP;
 #if AMQFT_TMA_STAGE
   if (tid == 0) {
     mbar_init(bar, 1);
@@ -521,26 +525,38 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
 #else
     const V2* x = reinterpret_cast<const V2*>(in + row * 2 * N);
 #endif
-#if AMQFT_UNROLL_IO
+    // Cells m = tid + 256 it (it < H/256) and m = H (thread 0): the
+    // physical offsets are linear in it (256 is a multiple of both layout
+    // periods), so every store is an immediate offset from a per-thread
+    // base.  INV (swap-trick inverse): re/im exchanged on the way in.
+    if (tid < IO_T) {
+      const int q0 = C::pt(tid, 0), q1 = C::pt(tid, 1);
+      R* t0 = Tb + C::coT(0) + q0;
+      R* t1 = Tb + C::coT(1) + q1;
+      R* t2 = Tb + C::coT(2) + q0;
+      R* t3 = Tb + C::coT(3) + q1;
 #pragma unroll
-#else
-#pragma unroll 1
-#endif
-    for (int it = 0; it < (H + C::NT) / C::NT; ++it) {
-      const int m = tid + it * C::NT;
-      if (m > H) break;
-      V2 a = x[m];
-      if (inverse) { const R tmp = a.x; a.x = a.y; a.y = tmp; }
-      if (m == 0 || m == H) {
-        Tb[C::coT(0) + C::pt(m, 0)] = a.x;
-        Tb[C::coT(2) + C::pt(m, 0)] = a.y;
-      } else {
+      for (int it = 0; it < IO_IT; ++it) {
+        const int m = tid + it * IO_T;
+        V2 a = x[m];
+        if (INV) a = V2{a.y, a.x};
+        if (it == 0 && tid == 0) {   // m = 0: Dct chains only
+          t0[0] = a.x;
+          t2[0] = a.y;
+          continue;
+        }
         V2 b = x[N - m];
-        if (inverse) { const R tmp = b.x; b.x = b.y; b.y = tmp; }
-        Tb[C::coT(0) + C::pt(m, 0)] = A::add(a.x, b.x);
-        Tb[C::coT(1) + C::pt(m, 1)] = A::sub(a.x, b.x);
-        Tb[C::coT(2) + C::pt(m, 0)] = A::add(a.y, b.y);
-        Tb[C::coT(3) + C::pt(m, 1)] = A::sub(a.y, b.y);
+        if (INV) b = V2{b.y, b.x};
+        t0[it * PT_STEP] = A::add(a.x, b.x);
+        t1[it * PT_STEP] = A::sub(a.x, b.x);
+        t2[it * PT_STEP] = A::add(a.y, b.y);
+        t3[it * PT_STEP] = A::sub(a.y, b.y);
+      }
+      if (tid == 0) {                // m = H
+        V2 a = x[H];
+        if (INV) a = V2{a.y, a.x};
+        Tb[C::coT(0) + C::pt(H, 0)] = a.x;
+        Tb[C::coT(2) + C::pt(H, 0)] = a.y;
       }
     }
     WORK_MARK(0);
@@ -626,10 +642,18 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       int rho, lens, r;
       seg_params<C::SINE>(lam_bit, s, C::LT, &rho, &lens, &r);
       rho = 0;   // odd segments are stored reversed (Cfg::ipos)
+#ifdef AMQFT_BOTTOM_EXPT
+      // timing experiment only (wrong results): every warp runs one block twice
+      Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, AMQFT_BOTTOM_EXPT>(0, 0, Tb + C::coT(c), Fb + C::coF(c),
+                                                            s * C::LB, tab, nmax, base, N, r, 0);
+      Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, AMQFT_BOTTOM_EXPT>(0, 0, Tb + C::coT(c), Fb + C::coF(c),
+                                                            s * C::LB, tab, nmax, base, N, r, 0);
+#else
       Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, 0>(rho, lens, Tb + C::coT(c), Fb + C::coF(c),
                                                             s * C::LB, tab, nmax, base, N, r, lam_bit);
       Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, 1>(rho, lens, Tb + C::coT(c), Fb + C::coF(c),
                                                             s * C::LB, tab, nmax, base, N, r, lam_bit);
+#endif
 #endif
     } else {
 #if AMQFT_SMALL_MODE == 1
@@ -702,35 +726,36 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
 
     // ---- store: SplitReal bwd (elab.cpp:199-208) + SplitComplex bwd (162-183)
     V2* y = reinterpret_cast<V2*>(out + row * 2 * N);
-#if AMQFT_UNROLL_IO
+    // Cells k = tid + 256 it and k = H (thread 0), immediate offsets as in
+    // the load.  INV: re/im exchanged and scaled by 1/N on the way out.
+    if (tid < IO_T) {
+      const int q0 = C::pf(tid, 0), q1 = C::pf(tid, 1);
+      const R* f0 = Fb + C::coF(0) + q0;
+      const R* f1 = Fb + C::coF(1) + q1;
+      const R* f2 = Fb + C::coF(2) + q0;
+      const R* f3 = Fb + C::coF(3) + q1;
 #pragma unroll
-#else
-#pragma unroll 1
-#endif
-    for (int it = 0; it < (H + C::NT) / C::NT; ++it) {
-      const int k = tid + it * C::NT;
-      if (k > H) break;
-      const R rd = Fb[C::coF(0) + C::pf(k, 0)];
-      const R id = Fb[C::coF(2) + C::pf(k, 0)];
-      V2 lo, hi;
-      if (k == 0 || k == H) {
-        lo.x = rd;
-        lo.y = id;
-        hi = lo;
-      } else {
-        const R rs = Fb[C::coF(1) + C::pf(k, 1)];
-        const R is = Fb[C::coF(3) + C::pf(k, 1)];
-        lo.x = A::add(rd, is);
-        lo.y = A::sub(id, rs);
-        hi.x = A::sub(rd, is);
-        hi.y = A::add(id, rs);
+      for (int it = 0; it < IO_IT; ++it) {
+        const int k = tid + it * IO_T;
+        const R rd = f0[it * PF_STEP], id = f2[it * PF_STEP];
+        if (it == 0 && tid == 0) {   // k = 0: Dct chains only
+          y[0] = INV ? V2{A::mul(id, scale), A::mul(rd, scale)} : V2{rd, id};
+          continue;
+        }
+        const R rs = f1[it * PF_STEP], is = f3[it * PF_STEP];
+        V2 lo{A::add(rd, is), A::sub(id, rs)};
+        V2 hi{A::sub(rd, is), A::add(id, rs)};
+        if (INV) {
+          lo = V2{A::mul(lo.y, scale), A::mul(lo.x, scale)};
+          hi = V2{A::mul(hi.y, scale), A::mul(hi.x, scale)};
+        }
+        y[k] = lo;
+        y[N - k] = hi;
       }
-      if (inverse) {
-        lo = V2{A::mul(lo.y, scale), A::mul(lo.x, scale)};
-        hi = V2{A::mul(hi.y, scale), A::mul(hi.x, scale)};
+      if (tid == 0) {                // k = H
+        const R rd = Fb[C::coF(0) + C::pf(H, 0)], id = Fb[C::coF(2) + C::pf(H, 0)];
+        y[H] = INV ? V2{A::mul(id, scale), A::mul(rd, scale)} : V2{rd, id};
       }
-      y[k] = lo;
-      if (k != 0 && k != H) y[N - k] = hi;
     }
     WORK_MARK(5);
     // No barrier here: the next row's load writes only T (and the staging
@@ -762,9 +787,12 @@ class FastPlanImpl final : public FastPlan {
   FastPlanImpl(const void* tab, uint32_t nmax, int device) : tab_(static_cast<const R*>(tab)),
                                                               nmax_(nmax) {
     using C = Cfg<V, R, LOGN, LOGLB>;
-    auto fn = k_fast<V, R, LOGN, LOGLB>;
+    auto fn = k_fast<V, R, LOGN, LOGLB, false>;
+    auto fi = k_fast<V, R, LOGN, LOGLB, true>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(C::SMEM));
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(fi, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM));
     if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, C::NT, C::SMEM);
@@ -783,9 +811,14 @@ class FastPlanImpl final : public FastPlan {
   void exec(const void* in, void* out, size_t rows, int inverse, cudaStream_t st) override {
     using C = Cfg<V, R, LOGN, LOGLB>;
     const unsigned grid = static_cast<unsigned>(std::min<size_t>(rows, static_cast<size_t>(grid_cap_)));
-    k_fast<V, R, LOGN, LOGLB><<<grid, C::NT, C::SMEM, st>>>(
-        static_cast<const R*>(in), static_cast<R*>(out), rows, tab_, ltab_, static_cast<int>(nmax_),
-        inverse, R(1) / R(C::N));
+    if (inverse)
+      k_fast<V, R, LOGN, LOGLB, true><<<grid, C::NT, C::SMEM, st>>>(
+          static_cast<const R*>(in), static_cast<R*>(out), rows, tab_, ltab_, static_cast<int>(nmax_),
+          R(1) / R(C::N));
+    else
+      k_fast<V, R, LOGN, LOGLB, false><<<grid, C::NT, C::SMEM, st>>>(
+          static_cast<const R*>(in), static_cast<R*>(out), rows, tab_, ltab_, static_cast<int>(nmax_),
+          R(1) / R(C::N));
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
   }

@@ -15,7 +15,7 @@ template <int V>
 static int run_v(const float* in, float* out, size_t rows, const float* tab, int nmax,
                  unsigned long long* cyc, int grid) {
   using C = Cfg<V, float, 12, 6>;
-  auto fn = k_fast<V, float, 12, 6>;
+  auto fn = k_fast<V, float, 12, 6, false>;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
   unsigned long long z[16] = {0};
   cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
@@ -24,7 +24,7 @@ static int run_v(const float* in, float* out, size_t rows, const float* tab, int
   float* ltab = nullptr;
   cudaMalloc(&ltab, sizeof(float) * C::H);
   k_level_table<float><<<8, 256>>>(tab, ltab, C::H, C::LT, nmax);
-  fn<<<grid, C::NT, C::SMEM>>>(in, out, rows, tab, ltab, nmax, 0, 1.0f / 4096);
+  fn<<<grid, C::NT, C::SMEM>>>(in, out, rows, tab, ltab, nmax, 1.0f / 4096);
   cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(cyc, g_phase_cycles, sizeof(z));
   cudaFree(ltab);
