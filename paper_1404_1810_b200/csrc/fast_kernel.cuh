@@ -289,12 +289,69 @@ __device__ __forceinline__ void am_depth(R (&x)[C::N / 128], bool last_lane, boo
   }
 }
 
+// ---- Serial recurrences (variants 1,3,5,7) as warp scans, fp32 only.
+// AM_B M1/M5 (elaborations.cpp:472-513): y_0 = C_0/2, y_k = C_k -/+ y_(k-1);
+// AM_F M3/M7 (elaborations.cpp:402-448): y_0 = C_0, y_k = C_k -/+ y_(k-1),
+// last y halved.  Along one odd class in its direction, y is a chain of
+// affine maps y -> C + s y (s = -1 sub, +1 add): each lane scans its own
+// RR/S elements, the lanes of a block combine their (A, s^m) aggregates
+// with a segmented shuffle scan, and every element is fixed up with the
+// prefix from the lanes before it.  Re-associated, so only the fp32 fast
+// path uses it; fp64 keeps the reference's serial order (bitwise).
+template <class C, typename R, bool BWD, int LAM, int D>
+__device__ __forceinline__ void am_scan_depth(R (&x)[C::N / 128], int i, int nl, bool blk_ok) {
+  using A = Arith<R>;
+  using P = AmPos<C, BWD, LAM, D>;
+  constexpr int V = C::V_;
+  constexpr int RR = P::RR, S = P::S, M = RR / S;
+  constexpr bool ADD = BWD ? (V == 5) : (V == 7);
+  static_assert(S <= RR, "class stride must fit a lane's run");
+#pragma unroll
+  for (int rho = 0; rho < S; ++rho) {
+    if (!P::is_o(rho)) continue;
+    const int lens = P::lens(rho);
+    const bool desc = BWD ? ((V == 1) ? (lens == 1) : (lens == 0))    // M1 / M5
+                          : ((V == 3) ? (lens == 0) : (lens == 1));   // M3 / M7
+    const int pos = desc ? (nl - 1 - i) : i;       // lane rank in the class direction
+    // local inclusive scan of this lane's elements (in direction), y_in = 0
+    R loc[M];
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      const int l = rho + (desc ? (M - 1 - j) : j) * S;
+      R e = x[l];
+      if (BWD && j == 0 && pos == 0) e = A::mul(R(0.5), e);   // AM_B seed C_0 / 2
+      loc[j] = j == 0 ? e : (ADD ? A::add(e, loc[j - 1]) : A::sub(e, loc[j - 1]));
+    }
+    // segmented inclusive scan of the lane aggregates (A, s^M) over the block
+    R acc = loc[M - 1];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const R o = desc ? __shfl_down_sync(0xffffffffu, acc, d) : __shfl_up_sync(0xffffffffu, acc, d);
+      const bool neg = !ADD && (M & 1) && (d & 1);            // factor s^(M d)
+      if (pos >= d) acc = neg ? A::sub(acc, o) : A::add(acc, o);
+    }
+    R yin = desc ? __shfl_down_sync(0xffffffffu, acc, 1) : __shfl_up_sync(0xffffffffu, acc, 1);
+    if (pos == 0) yin = R(0);
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      const int l = rho + (desc ? (M - 1 - j) : j) * S;
+      const bool negj = !ADD && ((j & 1) == 0);               // s^(j+1)
+      R y = negj ? A::sub(loc[j], yin) : A::add(loc[j], yin);
+      if (!BWD && j == M - 1 && pos == nl - 1) y = A::mul(R(0.5), y);   // AM_F final halving
+      if (blk_ok) x[l] = y;
+    }
+  }
+}
+
 template <class C, typename R, bool BWD, int LAM>
 __device__ __forceinline__ void am_depths(R (&x)[C::N / 128], bool last_lane, bool first_lane,
-                                          int Mt) {
+                                          int Mt, int i, int nl) {
   auto step = [&](auto dtag) {
     constexpr int D = decltype(dtag)::value;
-    am_depth<C, R, BWD, LAM, D>(x, last_lane, first_lane, (Mt >> (D + 1)) >= 2);
+    if constexpr (C::CHAIN)
+      am_scan_depth<C, R, BWD, LAM, D>(x, i, nl, (Mt >> (D + 1)) >= 2);
+    else
+      am_depth<C, R, BWD, LAM, D>(x, last_lane, first_lane, (Mt >> (D + 1)) >= 2);
   };
   static_assert(C::LT <= 6, "depth range");
   if constexpr (BWD) {
@@ -340,8 +397,8 @@ __device__ __forceinline__ void am_phase_regs(R* B) {
 #pragma unroll
   for (int l = 0; l < RR; ++l) x[l] = active ? chb[-(l + (l >> 5))] : R(0);
   const bool last_lane = i == nl - 1, first_lane = i == 0;
-  if (lam_c) am_depths<C, R, BWD, 1>(x, last_lane, first_lane, Mt);
-  else am_depths<C, R, BWD, 0>(x, last_lane, first_lane, Mt);
+  if (lam_c) am_depths<C, R, BWD, 1>(x, last_lane, first_lane, Mt, i, nl);
+  else am_depths<C, R, BWD, 0>(x, last_lane, first_lane, Mt, i, nl);
   if (active) {
 #pragma unroll
     for (int l = 0; l < RR; ++l) chb[-(l + (l >> 5))] = x[l];
@@ -593,7 +650,8 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
           __syncthreads();
         }
       }
-      if constexpr (C::CHAIN) am_levels_asc<C, R, C::LT>(Tb);
+      // serial recurrences: fp64 in the reference order (bitwise), fp32 as warp scans
+      if constexpr (C::CHAIN && sizeof(R) == 8) am_levels_asc<C, R, C::LT>(Tb);
       else am_phase_regs<C, R, false>(Tb);
       // small-chain folds (cells [0, N/LB] of T, untouched by the AM
       // levels): lane 31 of chain c's second warp is idle in the AM phase
@@ -684,7 +742,7 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
     PHASE_MARK(3);
 
     if constexpr (C::TM) {
-      if constexpr (C::CHAIN) am_levels_desc<C, R, C::LT>(Fb);
+      if constexpr (C::CHAIN && sizeof(R) == 8) am_levels_desc<C, R, C::LT>(Fb);
       else am_phase_regs<C, R, true>(Fb);
       // small-chain recombination Dct/Dst(4..N/LB) on F cells [0, N/LB]
       // (disjoint from the AM levels): lane 31 of chain c's second warp
