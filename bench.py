@@ -278,13 +278,14 @@ def main():
         torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()
+        plan.forward_host(hx, hy, stream=stream)   # creates the pipeline slots (untimed)
+        torch.cuda.synchronize(dev)
         s0 = torch.cuda.Event(enable_timing=True)
         s1 = torch.cuda.Event(enable_timing=True)
         s0.record(stream)
         for _ in range(args.e2e_steps):
-            x.copy_(hx, non_blocking=True)
-            plan.forward(x, y, stream=stream)
-            hy.copy_(y, non_blocking=True)
+            # public host-buffer entry point: H2D | transform | D2H pipelined
+            plan.forward_host(hx, hy, stream=stream)
         s1.record(stream)
         torch.cuda.synchronize(dev)
         ems = torch.tensor([s0.elapsed_time(s1)], device=dev, dtype=torch.float64)

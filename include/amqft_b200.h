@@ -111,6 +111,15 @@ amqft_status amqft_exec_inverse(amqft_plan plan, const void* d_in, void* d_out,
 amqft_status amqft_exec_rows(amqft_plan plan, const void* d_in, void* d_out,
                              size_t rows, int inverse, void* stream);
 
+/* Forward / inverse of `rows` rows between HOST buffers (any row count; the
+ * batch streams through three device slots as an H2D | transform | D2H
+ * pipeline on the plan's own streams).  Stream-ordered: `stream` waits for
+ * the last download.  Pass pinned host memory for asynchronous copies.
+ * Replaces the reference's per-signal loop over execute (accuracy.cpp:67-74,
+ * cli.cpp:155-174) for host-resident batches. */
+amqft_status amqft_exec_host_rows(amqft_plan plan, const void* h_in, void* h_out,
+                                  size_t rows, int inverse, void* stream);
+
 /* Convenience mirror of amqft::execute: one signal, HOST buffers (upload,
  * run on the device, download, synchronise).  meter3 (nullable) receives
  * {adds, muls, binary translations} of the executed schedule. */

@@ -191,6 +191,28 @@ class Plan:
         check(lib().amqft_exec_rows(self._h, self._ptr(d_in), self._ptr(d_out), rows, 1,
                                     self._stream(stream)))
 
+    def _check_host(self, t, rows):
+        if hasattr(t, "is_cuda"):
+            if t.is_cuda:
+                raise InvalidArgument(_native.EINVAL, "host tensors required")
+            if not t.is_contiguous():
+                raise InvalidArgument(_native.EINVAL, "contiguous tensors required")
+            want = 8 if self.dtype == "f64" else 4
+            if t.element_size() != want:
+                raise InvalidArgument(_native.EINVAL, f"tensor dtype does not match plan dtype {self.dtype}")
+            if t.numel() < rows * self.cells:
+                raise InvalidArgument(_native.EINVAL, "tensor smaller than rows * cells")
+
+    def forward_host(self, h_in, h_out, rows: int | None = None, stream=None, inverse: bool = False):
+        """Host (ideally pinned) tensors in and out; the batch streams through
+        the device as an H2D | transform | D2H pipeline (amqft_exec_host_rows).
+        Stream-ordered on `stream`; synchronise before reading h_out."""
+        rows = self.batch if rows is None else int(rows)
+        self._check_host(h_in, rows)
+        self._check_host(h_out, rows)
+        check(lib().amqft_exec_host_rows(self._h, self._ptr(h_in), self._ptr(h_out), rows,
+                                         1 if inverse else 0, self._stream(stream)))
+
     def op_counts(self):
         out = (C.c_uint64 * 3)()
         check(lib().amqft_plan_op_counts(self._h, out))

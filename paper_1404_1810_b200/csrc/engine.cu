@@ -84,6 +84,12 @@ struct amqft_plan_s {
   std::unique_ptr<FastPlan> fast;
   int launches = 0;
   int sms = 148;
+  // host-buffer pipeline (amqft_exec_host_rows), created on first use
+  static constexpr int NSLOT = 3;
+  void* slot[NSLOT] = {nullptr, nullptr, nullptr};
+  size_t slot_rows = 0;
+  cudaStream_t s_h2d = nullptr, s_run = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev_h2d[NSLOT] = {}, ev_run[NSLOT] = {}, ev_d2h[NSLOT] = {}, ev_in = nullptr;
 
   ~amqft_plan_s() {
     int cur = 0;
@@ -93,8 +99,14 @@ struct amqft_plan_s {
                     static_cast<void*>(d_prefix), static_cast<void*>(d_stages),
                     static_cast<void*>(d_progs), static_cast<void*>(d_jobs),
                     static_cast<void*>(d_geis), static_cast<void*>(d_gprefix),
-                    bufA, bufB})
+                    bufA, bufB, slot[0], slot[1], slot[2]})
       if (p) cudaFree(p);
+    for (cudaStream_t q : {s_h2d, s_run, s_d2h})
+      if (q) cudaStreamDestroy(q);
+    for (int k = 0; k < NSLOT; ++k)
+      for (cudaEvent_t e : {ev_h2d[k], ev_run[k], ev_d2h[k]})
+        if (e) cudaEventDestroy(e);
+    if (ev_in) cudaEventDestroy(ev_in);
     fast.reset();
     cudaSetDevice(cur);
   }
@@ -335,6 +347,70 @@ amqft_status amqft_exec_rows(amqft_plan P, const void* in, void* out, size_t row
     }
   } catch (const std::invalid_argument& e) {
     return set_err(AMQFT_EINVAL, e.what());
+  } catch (const CudaError& e) {
+    return set_err(AMQFT_ECUDA, e.what());
+  }
+  return AMQFT_OK;
+}
+
+// Host buffers in, host buffers out: the batch moves through NSLOT device
+// slots in chunks, as a three-stage pipeline (H2D copy engine | transform
+// | D2H copy engine) on three streams ordered by events, so the two PCIe
+// directions and the kernel overlap.  Stream-ordered with respect to
+// `stream` (the caller's stream waits for the last D2H).  Host memory
+// should be pinned for the copies to be asynchronous.
+amqft_status amqft_exec_host_rows(amqft_plan P, const void* h_in, void* h_out, size_t rows,
+                                  int inverse, void* stream) {
+  if (!P) return set_err(AMQFT_EINVAL, "null plan");
+  if (inverse && P->d.function != AMQFT_FN_CDFT)
+    return set_err(AMQFT_EINVAL, "the inverse is defined for CDFT plans only");
+  if (rows == 0) return AMQFT_OK;
+  if (!h_in || !h_out) return set_err(AMQFT_EINVAL, "null data pointer");
+  try {
+    ck(cudaSetDevice(P->d.device), "cudaSetDevice");
+    const size_t row_bytes = P->c.cells * P->esize;
+    if (!P->s_run) {
+      // ~64 MiB per slot, at least one full wave of CTAs, at most the plan batch
+      size_t r = std::max<size_t>(1, (size_t(64) << 20) / row_bytes);
+      r = std::max<size_t>(r, std::min<size_t>(P->d.batch, 2 * static_cast<size_t>(P->sms)));
+      P->slot_rows = std::min<size_t>(r, P->d.batch);
+      for (int k = 0; k < amqft_plan_s::NSLOT; ++k) {
+        ck(cudaMalloc(&P->slot[k], P->slot_rows * row_bytes), "cudaMalloc(host pipeline slot)");
+        ck(cudaEventCreateWithFlags(&P->ev_h2d[k], cudaEventDisableTiming), "cudaEventCreate");
+        ck(cudaEventCreateWithFlags(&P->ev_run[k], cudaEventDisableTiming), "cudaEventCreate");
+        ck(cudaEventCreateWithFlags(&P->ev_d2h[k], cudaEventDisableTiming), "cudaEventCreate");
+      }
+      ck(cudaEventCreateWithFlags(&P->ev_in, cudaEventDisableTiming), "cudaEventCreate");
+      ck(cudaStreamCreateWithFlags(&P->s_h2d, cudaStreamNonBlocking), "cudaStreamCreate");
+      ck(cudaStreamCreateWithFlags(&P->s_run, cudaStreamNonBlocking), "cudaStreamCreate");
+      ck(cudaStreamCreateWithFlags(&P->s_d2h, cudaStreamNonBlocking), "cudaStreamCreate");
+      for (int k = 0; k < amqft_plan_s::NSLOT; ++k) ck(cudaEventRecord(P->ev_d2h[k], P->s_d2h), "record");
+    }
+    cudaStream_t caller = static_cast<cudaStream_t>(stream);
+    ck(cudaEventRecord(P->ev_in, caller), "cudaEventRecord");
+    ck(cudaStreamWaitEvent(P->s_h2d, P->ev_in, 0), "wait");
+    const char* hi = static_cast<const char*>(h_in);
+    char* ho = static_cast<char*>(h_out);
+    size_t chunk = 0;
+    for (size_t r0 = 0; r0 < rows; r0 += P->slot_rows, ++chunk) {
+      const size_t nr = std::min(P->slot_rows, rows - r0);
+      const int k = static_cast<int>(chunk % amqft_plan_s::NSLOT);
+      const size_t bytes = nr * row_bytes;
+      ck(cudaStreamWaitEvent(P->s_h2d, P->ev_d2h[k], 0), "wait");           // slot free
+      ck(cudaMemcpyAsync(P->slot[k], hi + r0 * row_bytes, bytes, cudaMemcpyHostToDevice, P->s_h2d),
+         "cudaMemcpyAsync H2D");
+      ck(cudaEventRecord(P->ev_h2d[k], P->s_h2d), "record");
+      ck(cudaStreamWaitEvent(P->s_run, P->ev_h2d[k], 0), "wait");
+      const amqft_status st = amqft_exec_rows(P, P->slot[k], P->slot[k], nr, inverse, P->s_run);
+      if (st != AMQFT_OK) return st;
+      ck(cudaEventRecord(P->ev_run[k], P->s_run), "record");
+      ck(cudaStreamWaitEvent(P->s_d2h, P->ev_run[k], 0), "wait");
+      ck(cudaMemcpyAsync(ho + r0 * row_bytes, P->slot[k], bytes, cudaMemcpyDeviceToHost, P->s_d2h),
+         "cudaMemcpyAsync D2H");
+      ck(cudaEventRecord(P->ev_d2h[k], P->s_d2h), "record");
+    }
+    const int last = static_cast<int>((chunk - 1) % amqft_plan_s::NSLOT);
+    ck(cudaStreamWaitEvent(caller, P->ev_d2h[last], 0), "wait");
   } catch (const CudaError& e) {
     return set_err(AMQFT_ECUDA, e.what());
   }

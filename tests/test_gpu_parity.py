@@ -193,3 +193,51 @@ def test_fast_kernel_fp32_tolerance(oracle, restatement, n):
             err = r.rel_l2(got[k], r.execute(v, O.F_CDFT, n, xs[k].astype(np.float64)))
             if v <= 4:
                 assert err <= tol, (v, n, err)
+
+
+@pytest.mark.parametrize("v", range(1, 9))
+def test_fast_kernel_persistent_rows_bitwise(oracle, restatement, v):
+    """More rows than CTAs: every CTA loops over several rows with the next
+    row staged by TMA while the current one computes.  fp64 bitwise."""
+    r, O = restatement, oracle
+    n, batch = 4096, 700
+    plan = amqft.Plan(v, amqft.FunctionId.Cdft, n, batch, dtype="f64", order=amqft.Order.Fast)
+    assert plan.path()[0] == 2
+    rng = np.random.default_rng(100 + v)
+    x = torch.tensor(rng.uniform(-1, 1, (batch, 2 * n)), dtype=torch.float64, device=DEV)
+    y = torch.empty_like(x)
+    plan.forward(x, y)
+    torch.cuda.synchronize()
+    xs, ys = x.cpu().numpy(), y.cpu().numpy()
+    for row in (0, 1, 295, 296, 297, 591, 592, batch - 1):
+        assert ys[row].tobytes() == r.execute(v, O.F_CDFT, n, xs[row]).tobytes(), (v, row)
+
+
+def test_host_pipeline_matches_device_path():
+    """amqft_exec_host_rows (H2D | transform | D2H over three slots) gives the
+    device path's bytes, for a row count that is not a multiple of the slot."""
+    n, batch = 4096, 5000
+    plan = amqft.Plan(4, amqft.FunctionId.Cdft, n, batch, dtype="f32", order=amqft.Order.Fast)
+    g = torch.Generator().manual_seed(7)
+    hx = torch.randn(batch, 2 * n, generator=g).pin_memory()
+    hy = torch.empty_like(hx).pin_memory()
+    plan.forward_host(hx, hy)
+    torch.cuda.synchronize()
+    dx = hx.to(DEV)
+    dy = torch.empty_like(dx)
+    plan.forward(dx, dy)
+    torch.cuda.synchronize()
+    assert torch.equal(hy, dy.cpu())
+    hz = torch.empty_like(hx).pin_memory()
+    plan.forward_host(hy, hz, inverse=True)
+    torch.cuda.synchronize()
+    dz = torch.empty_like(dx)
+    plan.inverse(dy, dz)
+    torch.cuda.synchronize()
+    assert torch.equal(hz, dz.cpu())
+    assert float((hz - hx).norm() / hx.norm()) < 1e-5 * 12
+    # partial batch through the pipeline
+    hw = torch.zeros_like(hx).pin_memory()
+    plan.forward_host(hx, hw, rows=123)
+    torch.cuda.synchronize()
+    assert torch.equal(hw[:123], dy[:123].cpu()) and float(hw[123:].abs().max()) == 0.0
