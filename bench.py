@@ -180,6 +180,29 @@ def bench_reference(args, rank):
     return line
 
 
+def ncu_traffic(args, n):
+    """DRAM bytes per launch of the fused kernel from the committed ncu
+    --set full capture (profiles/, made by tools/profile_round.sh), when it
+    is a capture of this exact kernel (variant, N, fp32, fast order)."""
+    import glob
+    logn = n.bit_length() - 1
+    want = f"k_fast<{args.variant},float,{logn},6,0>"
+    if args.dtype != "f32" or args.order != "fast":
+        return None, None
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_k_fast_*.json")), reverse=True):
+        try:
+            d = json.load(open(f))
+        except (OSError, ValueError):
+            continue
+        if want not in d.get("Kernel Name", "") or int(float(d.get("launch__grid_size", 0))) <= 0:
+            continue
+        scale = {"Gbyte": 1e9, "Mbyte": 1e6, "byte": 1.0}
+        rd = float(d["dram__bytes_read.sum"]) * scale.get(d.get("dram__bytes_read.sum [unit]", "Gbyte"), 1e9)
+        wr = float(d["dram__bytes_write.sum"]) * scale.get(d.get("dram__bytes_write.sum [unit]", "Gbyte"), 1e9)
+        return rd + wr, os.path.relpath(f, ROOT)
+    return None, None
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -248,8 +271,10 @@ def main():
     alg_bytes = 2 * (2 * n * esize) * batch  # one read + one write per transform
     kernel_ms = ms_per_step / max(1, launches) if path != 1 else ms_per_step
     achieved = alg_bytes / (kernel_ms / 1000.0) / 1e9
+    traffic, traffic_src = ncu_traffic(args, n)
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm, "traffic": None,
+            "frac": achieved / hbm, "traffic": traffic, "traffic_unit": "bytes per launch (DRAM read + write)",
+            "traffic_source": traffic_src,
             "peak_source": hbm_src, "algorithmic_bytes_per_launch": alg_bytes,
             "kernel_ms": kernel_ms}
 
