@@ -36,11 +36,14 @@
 #include "fast_gen.cuh"
 #include "generic.cuh"
 
-#ifndef AMQFT_BOTTOM_SPLIT
-#define AMQFT_BOTTOM_SPLIT 0   // 1: two threads per bottom segment (class 0 | classes 1..)
+#ifndef AMQFT_RPC
+#define AMQFT_RPC 2   // rows per CTA (fp32, N <= 4096): both rows' warps run each phase in lockstep
 #endif
 #ifndef AMQFT_TMA_STAGE
 #define AMQFT_TMA_STAGE 1   // stage the next row with cp.async.bulk (else direct loads)
+#endif
+#ifndef AMQFT_TMA_STORE
+#define AMQFT_TMA_STORE 1   // fp32 N <= 4096: assemble the output row in smem, one bulk store
 #endif
 
 namespace amqft_b200 {
@@ -73,6 +76,21 @@ struct Cfg {
   // T, F (4 chains each) + the TMA staging buffer for the next row + mbarrier
   static constexpr size_t STAGE_OFF = 8 * CS * sizeof(R);
   static constexpr size_t SMEM = AMQFT_TMA_STAGE ? STAGE_OFF + 2 * N * sizeof(R) + 16 : STAGE_OFF;
+  // Rows per CTA: two fp32 rows (N <= 4096) share one 512-thread CTA, each
+  // with its own T/F/staging slot; every phase runs on both rows' warps at
+  // once, so the phase's straight-line code is fetched once per SM for two
+  // rows (instruction fetch was the top stall with one row per CTA).
+  // Measured (B200, config 2, tools/ab_kernel.py, with the bulk store):
+  // v4 1.646 -> 1.600 ms, v2 1.741 -> 1.568, v3 2.327 -> 1.936 against one
+  // row per CTA (two CTAs per SM).
+#ifdef AMQFT_RPC_FORCE   // A/B builds (tools/ab_kernel.cu)
+  static constexpr int RPC = (sizeof(R) == 4 && LOGN <= 12) ? AMQFT_RPC_FORCE : 1;
+#else
+  static constexpr int RPC = (sizeof(R) == 4 && LOGN <= 12) ? AMQFT_RPC : 1;
+#endif
+  static constexpr int NTB = NT * RPC;
+  static constexpr size_t SLOT = (SMEM + 127) / 128 * 128;
+  static constexpr size_t SMEM_BLOCK = SLOT * RPC;
   // Bank-conflict layouts: skew (i + i/LB) on the buffer holding the
   // index-space mirror network (T for time-major, F for harmonic-major);
   // one pad word per 32 (i + i/32) on the other one (per-lane class runs,
@@ -125,11 +143,11 @@ __device__ __forceinline__ void seg_params(int lam_c, int s, int d, int* rho, in
 // Dct/Dst chain recombination (time-major backward, FWD=false) or fold
 // (harmonic-major forward, FWD=true) at size n on an unskewed buffer.
 template <class C, typename R, bool FWD>
-__device__ __forceinline__ void chain_level(R* B, int n) {
+__device__ __forceinline__ void chain_level(R* B, int n, int tid) {
   using A = Arith<R>;
   const int q = n >> 2;
   const int lgq = 31 - __clz(q);
-  for (int g = threadIdx.x; g < n; g += C::NT) {
+  for (int g = tid; g < n; g += C::NT) {
     const int c = g >> lgq;
     const int k = g & (q - 1);
     const int lam = c & 1;
@@ -193,9 +211,9 @@ __device__ __forceinline__ void chain_class(R* ch, int lam_c, int t, int r) {
 }
 
 template <class C, int DEPTH, typename R>
-__device__ __forceinline__ void am_chains(R* B) {
+__device__ __forceinline__ void am_chains(R* B, int tid) {
   // one thread per odd class (serial recurrence); classes with m <= 2 skip
-  int idx = threadIdx.x;
+  int idx = tid;
   constexpr int classes = 1 << DEPTH;
   for (int g = idx; g < 4 * C::LOGLB_ * classes; g += C::NT) {
     const int c = g / (C::LOGLB_ * classes);
@@ -210,23 +228,23 @@ __device__ __forceinline__ void am_chains(R* B) {
 }
 
 template <class C, int DEPTH, typename R>
-__device__ __forceinline__ void am_level(R* B) {
-  am_chains<C, DEPTH, R>(B);
+__device__ __forceinline__ void am_level(R* B, int tid) {
+  am_chains<C, DEPTH, R>(B, tid);
 }
 
 // Depth loops unrolled at compile time.
 template <class C, typename R, int D>
-__device__ __forceinline__ void am_levels_desc(R* B) {  // D-1 .. 0
+__device__ __forceinline__ void am_levels_desc(R* B, int tid) {  // D-1 .. 0
   if constexpr (D > 0) {
-    am_level<C, D - 1, R>(B);
-    am_levels_desc<C, R, D - 1>(B);
+    am_level<C, D - 1, R>(B, tid);
+    am_levels_desc<C, R, D - 1>(B, tid);
   }
 }
 template <class C, typename R, int D, int I = 0>
-__device__ __forceinline__ void am_levels_asc(R* B) {  // 0 .. D-1
+__device__ __forceinline__ void am_levels_asc(R* B, int tid) {  // 0 .. D-1
   if constexpr (I < D) {
-    am_level<C, I, R>(B);
-    am_levels_asc<C, R, D, I + 1>(B);
+    am_level<C, I, R>(B, tid);
+    am_levels_asc<C, R, D, I + 1>(B, tid);
   }
 }
 
@@ -372,10 +390,10 @@ __device__ __forceinline__ void am_depths(R (&x)[C::N / 128], bool last_lane, bo
 }
 
 template <class C, typename R, bool BWD>
-__device__ __forceinline__ void am_phase_regs(R* B) {
+__device__ __forceinline__ void am_phase_regs(R* B, int tid) {
   constexpr int RR = C::N / 128;
   constexpr int LOGR = C::LOGN_ - 7;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = tid >> 5, lane = tid & 31;
   const int c = warp >> 1;
   int t, i;
   if ((warp & 1) == 0) {
@@ -490,6 +508,18 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
+// Bulk store smem -> global (cp.async.bulk, bulk-group completion).
+__device__ __forceinline__ void bulk_store(void* gdst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+               ::"l"(gdst), "r"(smem_u32(src)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_all() {   // smem source reusable
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {        // global writes complete
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
@@ -526,13 +556,11 @@ __device__ unsigned long long g_warp_work[16][16];
 #endif
 
 template <int V, typename R, int LOGN, int LOGLB, bool INV>
-#ifndef AMQFT_SMALL_MODE
-#define AMQFT_SMALL_MODE 0   // 0: serial small chain on spare lanes (measured best); 1: split into classes
-#endif
 #ifndef AMQFT_FAST_MINB
 #define AMQFT_FAST_MINB 2
 #endif
-__global__ void __launch_bounds__(Cfg<V, R, LOGN, LOGLB>::NT, (sizeof(R) == 4 ? AMQFT_FAST_MINB : 1))
+__global__ void __launch_bounds__(Cfg<V, R, LOGN, LOGLB>::NTB,
+                                  (Cfg<V, R, LOGN, LOGLB>::RPC > 1 ? 1 : (sizeof(R) == 4 ? AMQFT_FAST_MINB : 1)))
 k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
        const R* __restrict__ tab, const R* __restrict__ ltab, int nmax, R scale) {
 #ifdef AMQFT_PHASE_TIMING
@@ -541,12 +569,16 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
   using C = Cfg<V, R, LOGN, LOGLB>;
   using A = Arith<R>;
   using V2 = typename std::conditional<sizeof(R) == 4, float2, double2>::type;
-  extern __shared__ __align__(16) unsigned char smraw[];
-  R* Tb = reinterpret_cast<R*>(smraw);
+  extern __shared__ __align__(128) unsigned char smraw[];
+  // row slot: threads [slot*NT, (slot+1)*NT) own row slot of each pair
+  const int tid = threadIdx.x % C::NT;
+  const int slot = threadIdx.x / C::NT;
+  unsigned char* sm = smraw + slot * C::SLOT;
+  R* Tb = reinterpret_cast<R*>(sm);
   R* Fb = Tb + 4 * C::CS;
-  R* Sb = reinterpret_cast<R*>(smraw + C::STAGE_OFF);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + C::STAGE_OFF + 2 * C::N * sizeof(R));
-  const int tid = threadIdx.x;
+  R* Sb = reinterpret_cast<R*>(sm + C::STAGE_OFF);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::STAGE_OFF + 2 * C::N * sizeof(R));
+  constexpr size_t RSTEP = C::RPC;   // rows per CTA iteration
   const R base = __ldg(tab + (nmax / 4 - 1));
   constexpr int N = C::N, H = C::H;
   constexpr uint32_t ROW_BYTES = 2 * N * sizeof(R);
@@ -557,13 +589,19 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
   constexpr int SWZ_STEP = IO_T + IO_T / 32;             // swz: one pad per 32
   constexpr int PT_STEP = C::TM ? IDX_STEP : SWZ_STEP;
   constexpr int PF_STEP = C::TM ? SWZ_STEP : IDX_STEP;
+  // Output through a bulk store: the row is assembled in the F buffer (free
+  // once read; next written by the following row's bottom phase, after
+  // thread 0 has waited for the bulk read) and leaves with one cp.async.bulk.
+  constexpr bool BULK_ST = AMQFT_TMA_STORE && sizeof(R) == 4 && IO_IT <= 8 &&
+                           4 * C::CS * sizeof(R) >= 2 * N * sizeof(R);
 #if AMQFT_TMA_STAGE
   if (tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
   }
   __syncthreads();
-  if (tid == 0 && blockIdx.x < rows) tma_load_1d(Sb, in + blockIdx.x * 2 * N, ROW_BYTES, bar);
+  if (tid == 0 && blockIdx.x * RSTEP + slot < rows)
+    tma_load_1d(Sb, in + (blockIdx.x * RSTEP + slot) * 2 * N, ROW_BYTES, bar);
   uint32_t parity = 0;
 #else
   (void)Sb;
@@ -571,13 +609,18 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
   (void)ROW_BYTES;
 #endif
 
-  for (size_t row = blockIdx.x; row < rows; row += gridDim.x) {
+  for (size_t r0 = blockIdx.x * RSTEP; r0 < rows; r0 += gridDim.x * RSTEP) {
+    // every thread reaches every barrier; a slot past the last row idles
+    const size_t row = r0 + slot;
+    const bool act = row < rows;
     PHASE_MARK(0);
     // ---- load: SplitComplex (elab.cpp:152-155) + SplitReal (185-197)
     // from the TMA-staged row; then prefetch the CTA's next row.
 #if AMQFT_TMA_STAGE
-    mbar_wait(bar, parity);
-    parity ^= 1;
+    if (act) {
+      mbar_wait(bar, parity);
+      parity ^= 1;
+    }
     const V2* x = reinterpret_cast<const V2*>(Sb);
 #else
     const V2* x = reinterpret_cast<const V2*>(in + row * 2 * N);
@@ -586,7 +629,7 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
     // physical offsets are linear in it (256 is a multiple of both layout
     // periods), so every store is an immediate offset from a per-thread
     // base.  INV (swap-trick inverse): re/im exchanged on the way in.
-    if (tid < IO_T) {
+    if (act && tid < IO_T) {
       const int q0 = C::pt(tid, 0), q1 = C::pt(tid, 1);
       R* t0 = Tb + C::coT(0) + q0;
       R* t1 = Tb + C::coT(1) + q1;
@@ -619,16 +662,16 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
     WORK_MARK(0);
     __syncthreads();
 #if AMQFT_TMA_STAGE
-    if (tid == 0 && row + gridDim.x < rows) {
+    if (tid == 0 && row + gridDim.x * RSTEP < rows) {
       fence_proxy_async();
-      tma_load_1d(Sb, in + (row + gridDim.x) * 2 * N, ROW_BYTES, bar);
+      tma_load_1d(Sb, in + (row + gridDim.x * RSTEP) * 2 * N, ROW_BYTES, bar);
     }
 #endif
     PHASE_MARK(1);
 
     if constexpr (C::TM) {
       // top mirror levels (generated, 2^LT cells per thread) || small chains
-      if (tid < 4 * C::LB) {
+      if (act && tid < 4 * C::LB) {
         const int c = tid >> LOGLB, v = tid & (C::LB - 1);
         if (v > 0) Top<C::LB, C::LT, LOGN, C::SINE>::template fwd<R, A>(c & 1, Tb + C::coT(c), v, ltab, base);
       }
@@ -637,7 +680,8 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
         // generated: each thread owns the 64 cells j*64 +- k of its chain
         // warps 0-3: the 64 cells j*64 +- k of k = lane (lane 0 idle);
         // warps 4-7: the multiples of 32 of chain warp-4, cooperatively
-        if (tid < 128) {
+        if (!act) {
+        } else if (tid < 128) {
           if (tid & 31) Recomb<64, H / 64>::template fold<R, A>((tid >> 5) & 1, Tb + C::coT(tid >> 5), tid & 31);
         } else if (tid < 256) {
           special_class64<R, true>(Tb + C::coT((tid >> 5) - 4), (tid >> 5) & 1, tid & 31);
@@ -646,51 +690,28 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       } else {
 #pragma unroll 1
         for (int n = N; n >= 2 * (N / C::LB); n >>= 1) {
-          chain_level<C, R, true>(Tb, n);
+          if (act) chain_level<C, R, true>(Tb, n, tid);
           __syncthreads();
         }
       }
       // serial recurrences: fp64 in the reference order (bitwise), fp32 as warp scans
-      if constexpr (C::CHAIN && sizeof(R) == 8) am_levels_asc<C, R, C::LT>(Tb);
-      else am_phase_regs<C, R, false>(Tb);
+      if constexpr (C::CHAIN && sizeof(R) == 8) am_levels_asc<C, R, C::LT>(Tb, tid);   // RPC = 1
+      else if (act) am_phase_regs<C, R, false>(Tb, tid);
       // small-chain folds (cells [0, N/LB] of T, untouched by the AM
       // levels): lane 31 of chain c's second warp is idle in the AM phase
-#if AMQFT_SMALL_MODE == 1
-      if ((tid & 63) == 63 && tid < 256) {
-        const int c = tid >> 6;
-        SmallPar<V, C::HP, LOGN>::template serial<R, A>(c & 1, Tb + C::coT(c));
-      }
-#endif
     }
+    // the previous row's bulk store has long finished reading F (a load and
+    // a top phase ago); make it formal before the bottom writes F
+    if (BULK_ST && tid == 0) bulk_wait_read_all();
     WORK_MARK(1);
     __syncthreads();
     PHASE_MARK(2);
 
-    // ---- bottom: T -> F (generated).  Two threads per LB-segment: the
-    // trailing-zero classes never mix, class 0 goes to warps 0-3 and
-    // classes 1.. to warps 4-7.
-#if AMQFT_BOTTOM_SPLIT
-    if (tid < 2 * C::NSEG) {
-      // two threads per LB-segment: class 0 on warps 0.., classes 1.. on the rest
-      const int w = tid % C::NSEG;
-      const int half = C::HP / 2;
-      const int h = w % half;
-      const int rest = w / half;
-      const int part = rest & 1, rho_bit = (rest >> 1) & 1, lam_bit = (rest >> 2) & 1;
-      const int c = part * 2 + lam_bit;
-      const int s = 2 * h + rho_bit;
-      int rho, lens, r;
-      seg_params<C::SINE>(lam_bit, s, C::LT, &rho, &lens, &r);
-      rho = 0;   // odd segments are stored reversed (Cfg::ipos)
-      if (tid < C::NSEG)
-        Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, 0>(rho, lens, Tb + C::coT(c), Fb + C::coF(c),
-                                                              s * C::LB, tab, nmax, base, N, r, lam_bit);
-      else
-        Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, 1>(rho, lens, Tb + C::coT(c), Fb + C::coF(c),
-                                                              s * C::LB, tab, nmax, base, N, r, lam_bit);
-#else
-    if (tid < C::NSEG) {
-      // one thread per LB-segment (both class groups)
+    // ---- bottom: T -> F (generated).  One thread per LB-segment runs both
+    // class groups (class 0, then classes 1..; trailing-zero classes never
+    // mix) with one code path per lam (odd segments stored reversed).
+    if (!act) {
+    } else if (tid < C::NSEG) {
       const int half = C::HP / 2;
       const int h = tid % half;
       const int rest = tid / half;
@@ -700,30 +721,11 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       int rho, lens, r;
       seg_params<C::SINE>(lam_bit, s, C::LT, &rho, &lens, &r);
       rho = 0;   // odd segments are stored reversed (Cfg::ipos)
-#ifdef AMQFT_BOTTOM_EXPT
-      // timing experiment only (wrong results): every warp runs one block twice
-      Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, AMQFT_BOTTOM_EXPT>(0, 0, Tb + C::coT(c), Fb + C::coF(c),
-                                                            s * C::LB, tab, nmax, base, N, r, 0);
-      Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, AMQFT_BOTTOM_EXPT>(0, 0, Tb + C::coT(c), Fb + C::coF(c),
-                                                            s * C::LB, tab, nmax, base, N, r, 0);
-#else
       Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, 0>(rho, lens, Tb + C::coT(c), Fb + C::coF(c),
                                                             s * C::LB, tab, nmax, base, N, r, lam_bit);
       Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, 1>(rho, lens, Tb + C::coT(c), Fb + C::coF(c),
                                                             s * C::LB, tab, nmax, base, N, r, lam_bit);
-#endif
-#endif
     } else {
-#if AMQFT_SMALL_MODE == 1
-      // the cells at multiples of LB (small top blocks): one lane per
-      // (chain, trailing-zero class), disjoint from the segments' cells
-      using SP = SmallPar<V, C::HP, LOGN>;
-      const int l = tid - C::NSEG;
-      if (l < 4 * SP::NCLS) {
-        const int c = l / SP::NCLS, cls = l - c * SP::NCLS;
-        SP::template cls<R, A, LOGLB, C::LB>(c & 1, cls, Tb + C::coT(c), Fb + C::coF(c), tab, base);
-      }
-#else
       // the small chains (cells at multiples of LB; disjoint from the
       // segments' cells in T and F), one lane per chain, one warp each
       // where the block has spare warps
@@ -735,30 +737,24 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
         SmallFull<V, C::HP, LOGN>::template run<R, A, LOGLB, C::LB>(cc & 1, Tb + C::coT(cc), Fb + C::coF(cc),
                                                                      tab, base);
       }
-#endif
     }
     WORK_MARK(2);
     __syncthreads();
     PHASE_MARK(3);
 
     if constexpr (C::TM) {
-      if constexpr (C::CHAIN && sizeof(R) == 8) am_levels_desc<C, R, C::LT>(Fb);
-      else am_phase_regs<C, R, true>(Fb);
+      if constexpr (C::CHAIN && sizeof(R) == 8) am_levels_desc<C, R, C::LT>(Fb, tid);  // RPC = 1
+      else if (act) am_phase_regs<C, R, true>(Fb, tid);
       // small-chain recombination Dct/Dst(4..N/LB) on F cells [0, N/LB]
       // (disjoint from the AM levels): lane 31 of chain c's second warp
-#if AMQFT_SMALL_MODE == 1
-      if ((tid & 63) == 63 && tid < 256) {
-        const int c = tid >> 6;
-        SmallPar<V, C::HP, LOGN>::template serial<R, A>(c & 1, Fb + C::coF(c));
-      }
-#endif
       WORK_MARK(3);
       __syncthreads();
       PHASE_MARK(4);
       if constexpr (N / C::LB == 64) {
         // generated: each thread owns the 64 cells j*64 +- k of its chain
         // as the fold: warps 0-3 the k = lane sets, warps 4-7 the multiples of 32
-        if (tid < 128) {
+        if (!act) {
+        } else if (tid < 128) {
           if (tid & 31) Recomb<64, H / 64>::template run<R, A>((tid >> 5) & 1, Fb + C::coF(tid >> 5), tid & 31);
         } else if (tid < 256) {
           special_class64<R, false>(Fb + C::coF((tid >> 5) - 4), (tid >> 5) & 1, tid & 31);
@@ -768,12 +764,12 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       } else {
 #pragma unroll 1
         for (int n = 2 * (N / C::LB); n <= N; n <<= 1) {
-          chain_level<C, R, false>(Fb, n);
+          if (act) chain_level<C, R, false>(Fb, n, tid);
           __syncthreads();
         }
       }
     } else {
-      if (tid < 4 * C::LB) {
+      if (act && tid < 4 * C::LB) {
         const int c = tid >> LOGLB, v = tid & (C::LB - 1);
         if (v > 0) Top<C::LB, C::LT, LOGN, C::SINE>::template bwd<R, A>(c & 1, Fb + C::coF(c), v, ltab, base);
       }
@@ -784,35 +780,78 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
 
     // ---- store: SplitReal bwd (elab.cpp:199-208) + SplitComplex bwd (162-183)
     V2* y = reinterpret_cast<V2*>(out + row * 2 * N);
-    // Cells k = tid + 256 it and k = H (thread 0), immediate offsets as in
-    // the load.  INV: re/im exchanged and scaled by 1/N on the way out.
-    if (tid < IO_T) {
-      const int q0 = C::pf(tid, 0), q1 = C::pf(tid, 1);
-      const R* f0 = Fb + C::coF(0) + q0;
-      const R* f1 = Fb + C::coF(1) + q1;
-      const R* f2 = Fb + C::coF(2) + q0;
-      const R* f3 = Fb + C::coF(3) + q1;
+    if constexpr (BULK_ST) {
+      // read all cells (registers), barrier, write the natural-order row
+      // over F, barrier, one bulk store per row
+      V2 lo[IO_IT], hi[IO_IT], yH;
+      if (act && tid < IO_T) {
+        const int q0 = C::pf(tid, 0), q1 = C::pf(tid, 1);
+        const R* f0 = Fb + C::coF(0) + q0;
+        const R* f1 = Fb + C::coF(1) + q1;
+        const R* f2 = Fb + C::coF(2) + q0;
+        const R* f3 = Fb + C::coF(3) + q1;
 #pragma unroll
-      for (int it = 0; it < IO_IT; ++it) {
-        const int k = tid + it * IO_T;
-        const R rd = f0[it * PF_STEP], id = f2[it * PF_STEP];
-        if (it == 0 && tid == 0) {   // k = 0: Dct chains only
-          y[0] = INV ? V2{A::mul(id, scale), A::mul(rd, scale)} : V2{rd, id};
-          continue;
+        for (int it = 0; it < IO_IT; ++it) {
+          const R rd = f0[it * PF_STEP], id = f2[it * PF_STEP];
+          const R rs = f1[it * PF_STEP], is = f3[it * PF_STEP];   // k = 0: unused
+          lo[it] = V2{A::add(rd, is), A::sub(id, rs)};
+          hi[it] = V2{A::sub(rd, is), A::add(id, rs)};
+          if (it == 0 && tid == 0) lo[0] = V2{rd, id};            // k = 0: Dct chains only
+          if (INV) {
+            lo[it] = V2{A::mul(lo[it].y, scale), A::mul(lo[it].x, scale)};
+            hi[it] = V2{A::mul(hi[it].y, scale), A::mul(hi[it].x, scale)};
+          }
         }
-        const R rs = f1[it * PF_STEP], is = f3[it * PF_STEP];
-        V2 lo{A::add(rd, is), A::sub(id, rs)};
-        V2 hi{A::sub(rd, is), A::add(id, rs)};
-        if (INV) {
-          lo = V2{A::mul(lo.y, scale), A::mul(lo.x, scale)};
-          hi = V2{A::mul(hi.y, scale), A::mul(hi.x, scale)};
+        if (tid == 0) {              // k = H
+          const R rd = Fb[C::coF(0) + C::pf(H, 0)], id = Fb[C::coF(2) + C::pf(H, 0)];
+          yH = INV ? V2{A::mul(id, scale), A::mul(rd, scale)} : V2{rd, id};
         }
-        y[k] = lo;
-        y[N - k] = hi;
       }
-      if (tid == 0) {                // k = H
-        const R rd = Fb[C::coF(0) + C::pf(H, 0)], id = Fb[C::coF(2) + C::pf(H, 0)];
-        y[H] = INV ? V2{A::mul(id, scale), A::mul(rd, scale)} : V2{rd, id};
+      __syncthreads();
+      if (act && tid < IO_T) {
+        V2* ob = reinterpret_cast<V2*>(Fb);
+#pragma unroll
+        for (int it = 0; it < IO_IT; ++it) {
+          const int k = tid + it * IO_T;
+          ob[k] = lo[it];
+          if (!(it == 0 && tid == 0)) ob[N - k] = hi[it];
+        }
+        if (tid == 0) ob[H] = yH;
+        fence_proxy_async();         // generic-proxy writes -> async proxy
+      }
+      __syncthreads();
+      if (act && tid == 0) bulk_store(y, Fb, ROW_BYTES);
+    } else {
+      // Cells k = tid + 256 it and k = H (thread 0), immediate offsets as in
+      // the load.  INV: re/im exchanged and scaled by 1/N on the way out.
+      if (act && tid < IO_T) {
+        const int q0 = C::pf(tid, 0), q1 = C::pf(tid, 1);
+        const R* f0 = Fb + C::coF(0) + q0;
+        const R* f1 = Fb + C::coF(1) + q1;
+        const R* f2 = Fb + C::coF(2) + q0;
+        const R* f3 = Fb + C::coF(3) + q1;
+#pragma unroll
+        for (int it = 0; it < IO_IT; ++it) {
+          const int k = tid + it * IO_T;
+          const R rd = f0[it * PF_STEP], id = f2[it * PF_STEP];
+          if (it == 0 && tid == 0) {   // k = 0: Dct chains only
+            y[0] = INV ? V2{A::mul(id, scale), A::mul(rd, scale)} : V2{rd, id};
+            continue;
+          }
+          const R rs = f1[it * PF_STEP], is = f3[it * PF_STEP];
+          V2 lo{A::add(rd, is), A::sub(id, rs)};
+          V2 hi{A::sub(rd, is), A::add(id, rs)};
+          if (INV) {
+            lo = V2{A::mul(lo.y, scale), A::mul(lo.x, scale)};
+            hi = V2{A::mul(hi.y, scale), A::mul(hi.x, scale)};
+          }
+          y[k] = lo;
+          y[N - k] = hi;
+        }
+        if (tid == 0) {                // k = H
+          const R rd = Fb[C::coF(0) + C::pf(H, 0)], id = Fb[C::coF(2) + C::pf(H, 0)];
+          y[H] = INV ? V2{A::mul(id, scale), A::mul(rd, scale)} : V2{rd, id};
+        }
       }
     }
     WORK_MARK(5);
@@ -821,6 +860,7 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
     // F is next written after two more barriers.
     PHASE_MARK(6);
   }
+  if (BULK_ST && tid == 0) bulk_wait_all();   // smem must outlive the last bulk store
 }
 
 // Per-level compacted constants for the top mirror levels:
@@ -848,12 +888,12 @@ class FastPlanImpl final : public FastPlan {
     auto fn = k_fast<V, R, LOGN, LOGLB, false>;
     auto fi = k_fast<V, R, LOGN, LOGLB, true>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(C::SMEM));
+                                         static_cast<int>(C::SMEM_BLOCK));
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(fi, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM));
+      e = cudaFuncSetAttribute(fi, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM_BLOCK));
     if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, C::NT, C::SMEM);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, C::NTB, C::SMEM_BLOCK);
     if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -868,13 +908,14 @@ class FastPlanImpl final : public FastPlan {
   ~FastPlanImpl() override { if (ltab_) cudaFree(ltab_); }
   void exec(const void* in, void* out, size_t rows, int inverse, cudaStream_t st) override {
     using C = Cfg<V, R, LOGN, LOGLB>;
-    const unsigned grid = static_cast<unsigned>(std::min<size_t>(rows, static_cast<size_t>(grid_cap_)));
+    const size_t units = (rows + C::RPC - 1) / C::RPC;
+    const unsigned grid = static_cast<unsigned>(std::min<size_t>(units, static_cast<size_t>(grid_cap_)));
     if (inverse)
-      k_fast<V, R, LOGN, LOGLB, true><<<grid, C::NT, C::SMEM, st>>>(
+      k_fast<V, R, LOGN, LOGLB, true><<<grid, C::NTB, C::SMEM_BLOCK, st>>>(
           static_cast<const R*>(in), static_cast<R*>(out), rows, tab_, ltab_, static_cast<int>(nmax_),
           R(1) / R(C::N));
     else
-      k_fast<V, R, LOGN, LOGLB, false><<<grid, C::NT, C::SMEM, st>>>(
+      k_fast<V, R, LOGN, LOGLB, false><<<grid, C::NTB, C::SMEM_BLOCK, st>>>(
           static_cast<const R*>(in), static_cast<R*>(out), rows, tab_, ltab_, static_cast<int>(nmax_),
           R(1) / R(C::N));
     const cudaError_t e = cudaGetLastError();

@@ -16,7 +16,10 @@ static int run_v(const float* in, float* out, size_t rows, const float* tab, int
                  unsigned long long* cyc, int grid) {
   using C = Cfg<V, float, 12, 6>;
   auto fn = k_fast<V, float, 12, 6, false>;
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BLOCK);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, C::NTB, C::SMEM_BLOCK);
+  if (grid <= 0) grid = 148 * (per_sm > 0 ? per_sm : 1);
   unsigned long long z[16] = {0};
   cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
   unsigned long long zz[16][16] = {{0}};
@@ -24,7 +27,7 @@ static int run_v(const float* in, float* out, size_t rows, const float* tab, int
   float* ltab = nullptr;
   cudaMalloc(&ltab, sizeof(float) * C::H);
   k_level_table<float><<<8, 256>>>(tab, ltab, C::H, C::LT, nmax);
-  fn<<<grid, C::NT, C::SMEM>>>(in, out, rows, tab, ltab, nmax, 1.0f / 4096);
+  fn<<<grid, C::NTB, C::SMEM_BLOCK>>>(in, out, rows, tab, ltab, nmax, 1.0f / 4096);
   cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(cyc, g_phase_cycles, sizeof(z));
   cudaFree(ltab);
@@ -32,9 +35,11 @@ static int run_v(const float* in, float* out, size_t rows, const float* tab, int
   cudaMemcpyFromSymbol(ww, g_warp_work, sizeof(ww));
   for (int p = 0; p < 6; ++p) {
     printf("  phase %d warp work:", p);
-    for (int w = 0; w < C::NT / 32; ++w) printf(" %6llu", ww[p][w] / (rows / grid));
+    for (int w = 0; w < C::NTB / 32; ++w) printf(" %6llu", ww[p][w] / (rows / (grid * C::RPC)));
     printf("\n");
   }
+  printf("  (grid %d, %d rows per CTA iteration)\n", grid, C::RPC);
+  cyc[15] = (unsigned long long)grid * C::RPC;
   return (int)cudaGetLastError();
 }
 

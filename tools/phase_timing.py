@@ -24,10 +24,10 @@ for v in [int(a) for a in sys.argv[1:]] or [4]:
     x = torch.randn(rows, 2 * N, device="cuda")
     y = torch.empty_like(x)
     cyc = (C.c_ulonglong * 16)()
-    grid = 148 * int(os.environ.get("PT_CTAS", "2"))
+    grid = 148 * int(os.environ.get("PT_CTAS", "0"))   # 0: occupancy-derived
     for _ in range(2):
         rc = lib.pt_run(v, x.data_ptr(), y.data_ptr(), rows, dtab.data_ptr(), N, cyc, grid)
-    per = rows / grid
+    per = rows / cyc[15]   # CTA iterations = rows / (grid * rows per CTA)
     tot = sum(cyc[i] for i in range(6))
     print(f"variant {v}: {tot / per:.0f} cycles/transform on CTA 0 (rc={rc})")
     for i, nm in enumerate(names):
