@@ -20,6 +20,7 @@
 
 #include "../../include/amqft_b200.h"
 #include "fast.cuh"
+#include "fourstep.cuh"
 #include "generic_exec.hpp"
 #include "plan.hpp"
 #include "trig.hpp"
@@ -293,13 +294,18 @@ amqft_status amqft_plan_create(amqft_plan* out, const amqft_plan_desc* desc) {
     // Fast fused path where one exists for this request.
     if (desc->order == AMQFT_ORDER_FAST) {
       P->fast = make_fast_plan(*desc, P->d_trig, P->nmax);
+      int fpath = 2;
+      if (!P->fast && fourstep_covers(*desc)) {
+        P->fast = make_fourstep_plan(*desc, P->d_trig, P->nmax);
+        fpath = 3;
+      }
       if (P->fast) {
-        P->path = 2;
+        P->path = fpath;
         P->c.variant = desc->variant;
         P->c.fn = desc->function;
         P->c.n = n;
         P->c.cells = fn_cells(desc->function, n);
-        P->c.ops = fast_op_counts(*desc);
+        P->c.ops = fpath == 2 ? fast_op_counts(*desc) : fourstep_op_counts(*desc);
         P->launches = P->fast->launches;
         *out = P.release();
         return AMQFT_OK;
@@ -338,7 +344,7 @@ amqft_status amqft_exec_rows(amqft_plan P, const void* in, void* out, size_t row
   try {
     ck(cudaSetDevice(P->d.device), "cudaSetDevice");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (P->path == 2) {
+    if (P->path >= 2) {
       P->fast->exec(in, out, rows, inverse, st);
     } else if (P->d.dtype == AMQFT_F64) {
       exec_generic<double>(P, in, out, rows, inverse, st);
@@ -444,7 +450,7 @@ amqft_status amqft_plan_dump(amqft_plan P, int prog, void* records, size_t cap,
                              size_t* count, uint32_t* stages, size_t cap2,
                              size_t* nstages) {
   if (!P) return set_err(AMQFT_EINVAL, "null plan");
-  if (P->path == 2) return set_err(AMQFT_EINVAL, "fused plans carry no stage program");
+  if (P->path >= 2) return set_err(AMQFT_EINVAL, "fused plans carry no stage program");
   if (prog < 0 || static_cast<size_t>(prog) >= P->c.progs.size())
     return set_err(AMQFT_EINVAL, "no such program");
   const SubProgram& sp = P->c.progs[prog];

@@ -1,6 +1,7 @@
 // fast.cu -- dispatcher of the fused CDFT kernels (kernel: fast_kernel.cuh;
 // per-variant instances: fast_v1.cu .. fast_v8.cu).
 #include "fast.cuh"
+#include "fourstep.cuh"
 
 namespace amqft_b200 {
 namespace fastk {
@@ -22,6 +23,10 @@ std::unique_ptr<FastPlan> make_fast_typed(int v, size_t n, const void* tab, uint
     case 8: return make_for_variant<8, R>(n, tab, nmax, dev);
   }
   return nullptr;
+}
+
+std::unique_ptr<FastPlan> make_fast_typed_f32(int variant, size_t n, const void* tab, uint32_t nmax, int dev) {
+  return make_fast_typed<float>(variant, n, tab, nmax, dev);
 }
 
 std::unique_ptr<FastPlan> make_fast_plan(const amqft_plan_desc& d, const void* d_trig,

@@ -879,12 +879,32 @@ __global__ void k_level_table(const R* __restrict__ tab, R* __restrict__ ltab, i
   }
 }
 
+// The generated small-chain code indexes the constant table with
+// compile-time slots for Nmax = N.  A plan whose table was built for a
+// larger Nmax (table_max_n, or a four-step sub-transform) uses this
+// compacted copy: slot s of the Nmax = N table is slot (s+1) Nmax/N - 1 of
+// the big one, bitwise the same value (TrigTable level sharing,
+// variants.cpp:281).
+template <typename R>
+__global__ void k_compact_table(const R* __restrict__ tab, R* __restrict__ out, int n, int nmax) {
+  const int ratio = nmax / n;
+  for (int s = threadIdx.x + blockIdx.x * blockDim.x; s < n / 4; s += blockDim.x * gridDim.x)
+    out[s] = tab[(s + 1) * ratio - 1];
+}
+
 template <int V, typename R, int LOGN, int LOGLB>
 class FastPlanImpl final : public FastPlan {
  public:
   FastPlanImpl(const void* tab, uint32_t nmax, int device) : tab_(static_cast<const R*>(tab)),
                                                               nmax_(nmax) {
     using C = Cfg<V, R, LOGN, LOGLB>;
+    if (nmax_ != static_cast<uint32_t>(C::N)) {
+      cudaError_t e0 = cudaMalloc(&own_tab_, sizeof(R) * (C::N / 4));
+      if (e0 != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e0));
+      k_compact_table<R><<<8, 256>>>(tab_, own_tab_, C::N, static_cast<int>(nmax_));
+      tab_ = own_tab_;
+      nmax_ = C::N;
+    }
     auto fn = k_fast<V, R, LOGN, LOGLB, false>;
     auto fi = k_fast<V, R, LOGN, LOGLB, true>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -905,7 +925,10 @@ class FastPlanImpl final : public FastPlan {
     e = cudaDeviceSynchronize();
     if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
   }
-  ~FastPlanImpl() override { if (ltab_) cudaFree(ltab_); }
+  ~FastPlanImpl() override {
+    if (ltab_) cudaFree(ltab_);
+    if (own_tab_) cudaFree(own_tab_);
+  }
   void exec(const void* in, void* out, size_t rows, int inverse, cudaStream_t st) override {
     using C = Cfg<V, R, LOGN, LOGLB>;
     const size_t units = (rows + C::RPC - 1) / C::RPC;
@@ -924,6 +947,7 @@ class FastPlanImpl final : public FastPlan {
 
  private:
   const R* tab_;
+  R* own_tab_ = nullptr;
   R* ltab_ = nullptr;
   uint32_t nmax_;
   int grid_cap_ = 148;

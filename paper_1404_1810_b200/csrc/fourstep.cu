@@ -1,0 +1,215 @@
+// fourstep.cu -- large-N CDFT (N = N1 * N2 >= 2^20) as a four-step
+// decomposition whose two DFT passes are the fused AM-QFT kernel
+// (fast_kernel.cuh) on rows of length N1 and N2 (BASELINE config 4:
+// N = 2^24 = 4096 x 4096; SURVEY §8(d) C4, §8(e) C5 local passes).
+//
+//   n = N2 n1 + n2,  k = k1 + N1 k2:
+//   X[k1 + N1 k2] = sum_n2 w_N2^(n2 k2) [ w_N^(n2 k1) sum_n1 x[N2 n1 + n2] w_N1^(n1 k1) ]
+//
+//   1. transpose   x as [n1][n2] -> A[n2][n1]            (re/im swap for the inverse)
+//   2. AM-QFT      N2 rows of length N1, in place         (fused kernel, variant v)
+//   3. twiddle + transpose  A[n2][k1] w_N^(n2 k1) -> B[k1][n2]
+//   4. AM-QFT      N1 rows of length N2                   (fused kernel, variant v)
+//   5. transpose   Z[k1][k2] -> X[k2][k1] = natural order (swap + 1/N for the inverse)
+//
+// The AM-QFT recursion itself is not preserved across the split (the
+// sub-transforms are), so this path is fp32 "fast order" only; its
+// accuracy is checked against the fp64 oracle of the same variant.
+// Twiddles w_N^j = exp(-2 pi i j / N): TRIG_TABLE = two half-size tables
+// w^(jh B) and w^(jl) (B = 2^ceil(lg N / 2)) multiplied in fp64;
+// TRIG_ONTHEFLY = sincospi in fp64 per element.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "fast.cuh"
+#include "fourstep.cuh"
+
+namespace amqft_b200 {
+
+namespace {
+
+constexpr int TD = 32;   // transpose tile
+constexpr int TR = 8;    // rows of threads per tile
+
+// out[r][c] (C1 x R1 per matrix) = in[c][r] (R1 x C1), one matrix per
+// blockIdx.z.  MODE 0: plain; 1: twiddle by w_N^(r c) (r = row of out, c =
+// column of out); SWAP: exchange re/im of the input; scale multiplies the
+// result.  (A swap on both sides of a transform is the swap-trick inverse.)
+template <int MODE, bool SWAP>
+__global__ void __launch_bounds__(TD * TR) k_transpose(const float2* __restrict__ in, float2* __restrict__ out,
+                                                      int R1, int C1, float scale,
+                                                      const double2* __restrict__ twh,
+                                                      const double2* __restrict__ twl, int logb,
+                                                      int logn, int onthefly) {
+  __shared__ float2 tile[TD][TD + 1];
+  const size_t mat = static_cast<size_t>(blockIdx.z) * R1 * C1;
+  const int c0 = blockIdx.x * TD, r0 = blockIdx.y * TD;
+#pragma unroll
+  for (int j = 0; j < TD; j += TR) {
+    const int r = r0 + threadIdx.y + j, c = c0 + threadIdx.x;
+    float2 v = in[mat + static_cast<size_t>(r) * C1 + c];
+    if (SWAP) v = make_float2(v.y, v.x);
+    tile[threadIdx.y + j][threadIdx.x] = v;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < TD; j += TR) {
+    const int orow = c0 + threadIdx.y + j;   // row of out = column of in
+    const int ocol = r0 + threadIdx.x;
+    float2 v = tile[threadIdx.x][threadIdx.y + j];
+    if (MODE == 1) {
+      // w_N^(orow * ocol): j = (orow * ocol) mod N
+      const unsigned long long jj =
+          (static_cast<unsigned long long>(orow) * static_cast<unsigned long long>(ocol)) &
+          ((1ull << logn) - 1ull);
+      double wr, wi;
+      if (onthefly) {
+        double s, c;
+        sincospi(static_cast<double>(jj) * 2.0 / static_cast<double>(1ull << logn), &s, &c);
+        wr = c;
+        wi = -s;
+      } else {
+        const double2 a = twh[jj >> logb], b = twl[jj & ((1ull << logb) - 1ull)];
+        wr = a.x * b.x - a.y * b.y;
+        wi = a.x * b.y + a.y * b.x;
+      }
+      const float fr = static_cast<float>(wr), fi = static_cast<float>(wi);
+      v = make_float2(v.x * fr - v.y * fi, v.x * fi + v.y * fr);
+    }
+    v.x *= scale;
+    v.y *= scale;
+    out[mat + static_cast<size_t>(orow) * R1 + ocol] = v;
+  }
+}
+
+template <int MODE, bool SWAP>
+void launch_t(const float2* in, float2* out, size_t mats, int R1, int C1, float scale, const double2* twh,
+              const double2* twl, int logb, int logn, int onthefly, cudaStream_t st) {
+  // grid.z is limited to 65535: loop over chunks of matrices
+  for (size_t m0 = 0; m0 < mats; m0 += 65535) {
+    const unsigned nz = static_cast<unsigned>(std::min<size_t>(65535, mats - m0));
+    const dim3 grid(C1 / TD, R1 / TD, nz), block(TD, TR);
+    const size_t off = m0 * static_cast<size_t>(R1) * C1;
+    k_transpose<MODE, SWAP><<<grid, block, 0, st>>>(in + off, out + off, R1, C1, scale, twh, twl, logb, logn,
+                                                     onthefly);
+  }
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string("k_transpose: ") + cudaGetErrorString(e));
+}
+
+int lg2(size_t v) {
+  int l = 0;
+  while ((size_t(1) << l) < v) ++l;
+  return l;
+}
+
+class FourStepPlan final : public FastPlan {
+ public:
+  FourStepPlan(int variant, size_t n, size_t batch, int trig_mode, const void* tab, uint32_t nmax, int dev)
+      : n_(n), batch_(batch), onthefly_(trig_mode == AMQFT_TRIG_ONTHEFLY) {
+    logn_ = lg2(n);
+    const int l1 = (logn_ + 1) / 2, l2 = logn_ - l1;
+    n1_ = size_t(1) << l1;
+    n2_ = size_t(1) << l2;
+    p1_ = make_fast_typed_f32(variant, n1_, tab, nmax, dev);
+    p2_ = make_fast_typed_f32(variant, n2_, tab, nmax, dev);
+    if (!p1_ || !p2_) throw std::invalid_argument("four-step: no fused kernel for the sub-transform sizes");
+    // half-size twiddle tables: w^(jh B), w^(jl), long double -> double
+    logb_ = (logn_ + 1) / 2;
+    const size_t B = size_t(1) << logb_, NH = n >> logb_;
+    std::vector<double2> th(NH), tl(B);
+    const long double two_pi = 6.283185307179586476925286766559005768L;
+    for (size_t j = 0; j < NH; ++j) {
+      const long double a = two_pi * static_cast<long double>(j << logb_) / static_cast<long double>(n);
+      th[j] = make_double2(static_cast<double>(cosl(a)), static_cast<double>(-sinl(a)));
+    }
+    for (size_t j = 0; j < B; ++j) {
+      const long double a = two_pi * static_cast<long double>(j) / static_cast<long double>(n);
+      tl[j] = make_double2(static_cast<double>(cosl(a)), static_cast<double>(-sinl(a)));
+    }
+    check(cudaMalloc(&twh_, NH * sizeof(double2)), "cudaMalloc twiddles");
+    check(cudaMalloc(&twl_, B * sizeof(double2)), "cudaMalloc twiddles");
+    check(cudaMemcpy(twh_, th.data(), NH * sizeof(double2), cudaMemcpyHostToDevice), "cudaMemcpy");
+    check(cudaMemcpy(twl_, tl.data(), B * sizeof(double2), cudaMemcpyHostToDevice), "cudaMemcpy");
+    check(cudaMalloc(&scratch_, batch_ * n_ * sizeof(float2)), "cudaMalloc four-step scratch");
+    launches = 3 + p1_->launches + p2_->launches;
+  }
+  ~FourStepPlan() override {
+    if (twh_) cudaFree(twh_);
+    if (twl_) cudaFree(twl_);
+    if (scratch_) cudaFree(scratch_);
+  }
+  void exec(const void* in, void* out, size_t rows, int inverse, cudaStream_t st) override {
+    if (rows > batch_) throw std::invalid_argument("rows exceed the plan batch");
+    const float2* x = static_cast<const float2*>(in);
+    float2* y = static_cast<float2*>(out);
+    float2* s = scratch_;
+    const int R1 = static_cast<int>(n1_), C1 = static_cast<int>(n2_);
+    // 1. x [n1][n2] -> s [n2][n1]
+    if (inverse)
+      launch_t<0, true>(x, s, rows, R1, C1, 1.0f, nullptr, nullptr, 0, logn_, 0, st);
+    else
+      launch_t<0, false>(x, s, rows, R1, C1, 1.0f, nullptr, nullptr, 0, logn_, 0, st);
+    // 2. rows of length N1
+    p1_->exec(s, s, rows * n2_, 0, st);
+    // 3. s [n2][k1] * w^(n2 k1) -> y [k1][n2]
+    launch_t<1, false>(s, y, rows, C1, R1, 1.0f, twh_, twl_, logb_, logn_, onthefly_ ? 1 : 0, st);
+    // 4. rows of length N2: y -> s [k1][k2]
+    p2_->exec(y, s, rows * n1_, 0, st);
+    // 5. s [k1][k2] -> y [k2][k1]
+    if (inverse)
+      launch_t<0, true>(s, y, rows, R1, C1, 1.0f / static_cast<float>(n_), nullptr, nullptr, 0, logn_, 0, st);
+    else
+      launch_t<0, false>(s, y, rows, R1, C1, 1.0f, nullptr, nullptr, 0, logn_, 0, st);
+  }
+
+ private:
+  static void check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+  }
+  size_t n_, batch_, n1_ = 0, n2_ = 0;
+  int logn_ = 0, logb_ = 0;
+  bool onthefly_;
+  std::unique_ptr<FastPlan> p1_, p2_;
+  double2* twh_ = nullptr;
+  double2* twl_ = nullptr;
+  float2* scratch_ = nullptr;
+};
+
+}  // namespace
+
+bool fourstep_covers(const amqft_plan_desc& d) {
+  if (d.function != AMQFT_FN_CDFT || d.dtype != AMQFT_F32 || d.order != AMQFT_ORDER_FAST) return false;
+  if (d.n < (size_t(1) << 20) || d.n > (size_t(1) << 26) || (d.n & (d.n - 1)) != 0) return false;
+  return true;
+}
+
+OpCount fourstep_op_counts(const amqft_plan_desc& d) {
+  // N2 sub-transforms of length N1, N1 of length N2 (the reference DAG of
+  // each, fast_op_counts), plus one complex twiddle multiply per element
+  // (4 muls + 2 adds).
+  int lg = lg2(d.n);
+  const size_t n1 = size_t(1) << ((lg + 1) / 2), n2 = d.n / n1;
+  amqft_plan_desc a = d, b = d;
+  a.n = n1;
+  b.n = n2;
+  const OpCount c1 = fast_op_counts(a), c2 = fast_op_counts(b);
+  OpCount c;
+  c.adds = n2 * c1.adds + n1 * c2.adds + 2 * d.n;
+  c.muls = n2 * c1.muls + n1 * c2.muls + 4 * d.n;
+  c.bt = n2 * c1.bt + n1 * c2.bt;
+  return c;
+}
+
+std::unique_ptr<FastPlan> make_fourstep_plan(const amqft_plan_desc& d, const void* d_trig, uint32_t nmax) {
+  if (!fourstep_covers(d)) return nullptr;
+  return std::make_unique<FourStepPlan>(d.variant, d.n, d.batch, d.trig_mode, d_trig, nmax, d.device);
+}
+
+}  // namespace amqft_b200
