@@ -128,6 +128,28 @@ amqft_status amqft_execute_host(int variant, int function, size_t n,
                                 size_t table_max_n, int corrupt_constants,
                                 uint64_t* meter3);
 
+/* ---- Distributed four-step (BASELINE config 5), fp32
+ * complex.  One transform of length n = n1 * n2 over nparts ranks: rank p
+ * holds rows n2 in [p n2/P, (p+1) n2/P) of length n1 (x[n2_total * n1_idx +
+ * n2] gathered by column), transforms them (a length-n1 plan), then
+ * amqft_dist_twiddle_scatter multiplies by w_n^(n2 k1) and scatters the
+ * k1-slab of destination q to d_dst[q] at offset src_rank * rows * n1/P
+ * ([row][k1 - q n1/P]).  d_dst (a HOST array of nparts device pointers) is
+ * either the local send buffer's slots (followed by an all-to-all, e.g.
+ * NCCL) or the peers' receive buffers mapped over NVLink (no collective:
+ * the kernel's stores are the exchange).  After the exchange each rank
+ * transposes [n2][n1/P] -> [n1/P][n2] (amqft_transpose_c64) and runs a
+ * length-n2 plan; its output is X[k1 + n1 k2] for its k1-slab.  Replaces
+ * nothing in the reference (single-process only, variants.cpp:404). */
+amqft_status amqft_dist_twiddle_scatter(const void* d_rows, void* const* d_dst, size_t rows,
+                                        size_t n1, size_t n, size_t row0, int src_rank,
+                                        int nparts, int trig_mode, void* stream);
+
+/* Batched transpose of complex fp32 matrices: mats x [r][c] -> [c][r];
+ * r and c multiples of 32. */
+amqft_status amqft_transpose_c64(const void* d_in, void* d_out, size_t mats, size_t r,
+                                 size_t c, void* stream);
+
 /* Arithmetic performed per row by the compiled schedule (OpMeter,
  * include/amqft/opmeter.hpp:13-29): {adds, muls, binary translations}. */
 amqft_status amqft_plan_op_counts(amqft_plan plan, uint64_t* out3);

@@ -431,6 +431,37 @@ amqft_status amqft_exec_inverse(amqft_plan P, const void* in, void* out, void* s
   return amqft_exec_rows(P, in, out, P ? P->d.batch : 0, 1, stream);
 }
 
+amqft_status amqft_dist_twiddle_scatter(const void* d_rows, void* const* d_dst, size_t rows, size_t n1,
+                                        size_t n, size_t row0, int src_rank, int nparts, int trig_mode,
+                                        void* stream) {
+  if (!d_rows || !d_dst) return set_err(AMQFT_EINVAL, "null pointer");
+  if (n == 0 || (n & (n - 1)) || n1 == 0 || (n1 & (n1 - 1)) || n % n1 || n > (size_t(1) << 40))
+    return set_err(AMQFT_EINVAL, "n and n1 must be powers of two with n1 | n");
+  if (src_rank < 0 || src_rank >= nparts) return set_err(AMQFT_EINVAL, "src_rank out of range");
+  try {
+    dist_twiddle_scatter(d_rows, d_dst, rows, n1, n, row0, src_rank, nparts, trig_mode,
+                         static_cast<cudaStream_t>(stream));
+  } catch (const std::invalid_argument& e) {
+    return set_err(AMQFT_EINVAL, e.what());
+  } catch (const std::runtime_error& e) {
+    return set_err(AMQFT_ECUDA, e.what());
+  }
+  return AMQFT_OK;
+}
+
+amqft_status amqft_transpose_c64(const void* d_in, void* d_out, size_t mats, size_t r, size_t c,
+                                 void* stream) {
+  if (!d_in || !d_out) return set_err(AMQFT_EINVAL, "null pointer");
+  try {
+    transpose_c64(d_in, d_out, mats, r, c, static_cast<cudaStream_t>(stream));
+  } catch (const std::invalid_argument& e) {
+    return set_err(AMQFT_EINVAL, e.what());
+  } catch (const std::runtime_error& e) {
+    return set_err(AMQFT_ECUDA, e.what());
+  }
+  return AMQFT_OK;
+}
+
 amqft_status amqft_plan_op_counts(amqft_plan P, uint64_t* out3) {
   if (!P || !out3) return set_err(AMQFT_EINVAL, "null argument");
   out3[0] = P->c.ops.adds;

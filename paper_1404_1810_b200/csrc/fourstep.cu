@@ -103,6 +103,48 @@ void launch_t(const float2* in, float2* out, size_t mats, int R1, int C1, float 
   if (e != cudaSuccess) throw std::runtime_error(std::string("k_transpose: ") + cudaGetErrorString(e));
 }
 
+// Distributed four-step, one rank's half-way step: rows n2 = row0 + r
+// (r < rows) of length N1 (already transformed over n1) are multiplied by
+// w_N^(n2 k1) and scattered by k1-slab: destination q receives the
+// columns k1 in [q N1/P, (q+1) N1/P) at dst[q] + src * rows * (N1/P),
+// laid out [r][k1 - q N1/P].  dst[] are device pointers: the local send
+// buffer slots (then an all-to-all) or the peers' receive buffers mapped
+// over NVLink (the transfer is the kernel's own stores).
+constexpr int kMaxParts = 64;
+struct DstPtrs {
+  float2* p[kMaxParts];
+};
+
+__global__ void __launch_bounds__(256) k_twiddle_scatter(const float2* __restrict__ in, const DstPtrs dst,
+                                                         int rows, int n1, int logn, long long row0, int src,
+                                                         int nparts, const double2* __restrict__ twh,
+                                                         const double2* __restrict__ twl, int logb, int onthefly) {
+  const int w = n1 / nparts;
+  const long long total = static_cast<long long>(rows) * n1;
+  for (long long i = threadIdx.x + static_cast<long long>(blockIdx.x) * blockDim.x; i < total;
+       i += static_cast<long long>(blockDim.x) * gridDim.x) {
+    const int r = static_cast<int>(i / n1), k1 = static_cast<int>(i % n1);
+    const unsigned long long n2 = static_cast<unsigned long long>(row0 + r);
+    const unsigned long long jj = (n2 * static_cast<unsigned long long>(k1)) & ((1ull << logn) - 1ull);
+    double wr, wi;
+    if (onthefly) {
+      double sn, cs;
+      sincospi(static_cast<double>(jj) * 2.0 / static_cast<double>(1ull << logn), &sn, &cs);
+      wr = cs;
+      wi = -sn;
+    } else {
+      const double2 a = twh[jj >> logb], b = twl[jj & ((1ull << logb) - 1ull)];
+      wr = a.x * b.x - a.y * b.y;
+      wi = a.x * b.y + a.y * b.x;
+    }
+    const float2 v = in[i];
+    const float fr = static_cast<float>(wr), fi = static_cast<float>(wi);
+    const int q = k1 / w, kl = k1 - q * w;
+    dst.p[q][(static_cast<long long>(src) * rows + r) * w + kl] =
+        make_float2(v.x * fr - v.y * fi, v.x * fi + v.y * fr);
+  }
+}
+
 int lg2(size_t v) {
   int l = 0;
   while ((size_t(1) << l) < v) ++l;
@@ -183,6 +225,65 @@ class FourStepPlan final : public FastPlan {
 };
 
 }  // namespace
+
+// Half-size twiddle tables for w_N (fp64, from long double).
+struct Twiddles {
+  double2* hi = nullptr;
+  double2* lo = nullptr;
+  int logb = 0, logn = 0;
+  explicit Twiddles(size_t n) {
+    logn = lg2(n);
+    logb = (logn + 1) / 2;
+    const size_t B = size_t(1) << logb, NH = n >> logb;
+    std::vector<double2> th(NH), tl(B);
+    const long double two_pi = 6.283185307179586476925286766559005768L;
+    for (size_t j = 0; j < NH; ++j) {
+      const long double a = two_pi * static_cast<long double>(j << logb) / static_cast<long double>(n);
+      th[j] = make_double2(static_cast<double>(cosl(a)), static_cast<double>(-sinl(a)));
+    }
+    for (size_t j = 0; j < B; ++j) {
+      const long double a = two_pi * static_cast<long double>(j) / static_cast<long double>(n);
+      tl[j] = make_double2(static_cast<double>(cosl(a)), static_cast<double>(-sinl(a)));
+    }
+    if (cudaMalloc(&hi, NH * sizeof(double2)) != cudaSuccess || cudaMalloc(&lo, B * sizeof(double2)) != cudaSuccess)
+      throw std::runtime_error("cudaMalloc twiddles");
+    cudaMemcpy(hi, th.data(), NH * sizeof(double2), cudaMemcpyHostToDevice);
+    cudaMemcpy(lo, tl.data(), B * sizeof(double2), cudaMemcpyHostToDevice);
+  }
+  ~Twiddles() {
+    if (hi) cudaFree(hi);
+    if (lo) cudaFree(lo);
+  }
+};
+
+void dist_twiddle_scatter(const void* in, void* const* d_dst, size_t rows, size_t n1, size_t n, size_t row0,
+                          int src, int nparts, int trig_mode, cudaStream_t st) {
+  static thread_local std::unique_ptr<Twiddles> tw;
+  static thread_local int tw_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!tw || (size_t(1) << tw->logn) != n || tw_dev != dev) {
+    tw.reset(new Twiddles(n));
+    tw_dev = dev;
+  }
+  if (nparts < 1 || nparts > kMaxParts || n1 % nparts) throw std::invalid_argument("twiddle_scatter: bad part count");
+  DstPtrs dp{};
+  for (int q = 0; q < nparts; ++q) dp.p[q] = static_cast<float2*>(d_dst[q]);
+  const long long total = static_cast<long long>(rows) * static_cast<long long>(n1);
+  const unsigned grid = static_cast<unsigned>(std::min<long long>((total + 255) / 256, 148LL * 16));
+  k_twiddle_scatter<<<grid, 256, 0, st>>>(static_cast<const float2*>(in), dp,
+                                          static_cast<int>(rows), static_cast<int>(n1), tw->logn,
+                                          static_cast<long long>(row0), src, nparts, tw->hi, tw->lo, tw->logb,
+                                          trig_mode == AMQFT_TRIG_ONTHEFLY ? 1 : 0);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string("k_twiddle_scatter: ") + cudaGetErrorString(e));
+}
+
+void transpose_c64(const void* in, void* out, size_t mats, size_t r, size_t c, cudaStream_t st) {
+  if (r % TD || c % TD) throw std::invalid_argument("transpose: dimensions must be multiples of 32");
+  launch_t<0, false>(static_cast<const float2*>(in), static_cast<float2*>(out), mats, static_cast<int>(r),
+                     static_cast<int>(c), 1.0f, nullptr, nullptr, 0, 0, 0, st);
+}
 
 bool fourstep_covers(const amqft_plan_desc& d) {
   if (d.function != AMQFT_FN_CDFT || d.dtype != AMQFT_F32 || d.order != AMQFT_ORDER_FAST) return false;

@@ -2,6 +2,8 @@
 // (fourstep.cu).
 #pragma once
 
+#include <cuda_runtime.h>
+
 #include <memory>
 
 #include "fast.cuh"
@@ -15,5 +17,11 @@ std::unique_ptr<FastPlan> make_fast_typed_f32(int variant, size_t n, const void*
 bool fourstep_covers(const amqft_plan_desc& d);
 std::unique_ptr<FastPlan> make_fourstep_plan(const amqft_plan_desc& d, const void* d_trig, uint32_t nmax);
 OpCount fourstep_op_counts(const amqft_plan_desc& d);
+
+// Distributed four-step building blocks (amqft_dist_twiddle_scatter,
+// amqft_transpose_c64).  d_dst: host array of nparts device pointers.
+void dist_twiddle_scatter(const void* in, void* const* d_dst, size_t rows, size_t n1, size_t n, size_t row0,
+                          int src, int nparts, int trig_mode, cudaStream_t st);
+void transpose_c64(const void* in, void* out, size_t mats, size_t r, size_t c, cudaStream_t st);
 
 }  // namespace amqft_b200

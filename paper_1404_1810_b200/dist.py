@@ -3,15 +3,21 @@
 Batched AM-QFT workloads shard by rows with no data-path collective: rank r
 owns rows [start, start + count) of the global batch, runs its own plan on
 its own device, and only the timing (max over ranks) and optional result
-gathering use the process group.  The fused single-transform four-step
-over NCCL is not part of round 1.
+gathering use the process group.
+
+A single huge transform (BASELINE config 5, N = 2^30 over P GPUs; SURVEY
+8(e)) runs as a distributed four-step with exactly one exchange step:
+`DistFourStep` below.
 """
 from __future__ import annotations
 
 import torch
 import torch.distributed as dist
 
-from . import FunctionId, Order, Plan
+import ctypes as C
+
+from . import FunctionId, Order, Plan, TrigMode
+from ._native import check, lib
 
 
 def shard_rows(total_rows: int, world: int, rank: int):
@@ -62,3 +68,161 @@ class ShardedPlan:
     def forward(self, local_in, local_out, stream=None):
         if self.rows:
             self.plan.forward(local_in, local_out, rows=self.rows, stream=stream)
+
+
+def fourstep_split(n: int):
+    """N = n1 * n2 with n1 = 2^ceil(lg N / 2) (the single-GPU four-step's
+    split, csrc/fourstep.cu)."""
+    lg = int(n).bit_length() - 1
+    if n <= 0 or (1 << lg) != n:
+        raise ValueError("n must be a power of two")
+    n1 = 1 << ((lg + 1) // 2)
+    return n1, n // n1
+
+
+def _plan_covers_f32_fast(n: int) -> bool:
+    """Sizes with a fused fp32 path: the kernel (1024..8192) or the
+    single-GPU four-step over it (2^20..2^26)."""
+    return 1024 <= n <= 8192 or (1 << 20) <= n <= (1 << 26)
+
+
+def dist_split(n: int, world: int):
+    """n = n1 * n2 for the distributed four-step: n2 is a fused-kernel size
+    (rows after the exchange), n1 any size with a fused path (the local rows
+    before it; the single-GPU four-step for n1 >= 2^20), both divisible by
+    the world size.  Config 5, N = 2^30: n1 = 2^20, n2 = 2^10."""
+    fourstep_split(n)   # power-of-two check
+    for n2 in (8192, 4096, 2048, 1024):
+        n1 = n // n2
+        if n1 * n2 == n and _plan_covers_f32_fast(n1) and n1 % world == 0 and n2 % world == 0:
+            return n1, n2
+    raise ValueError(f"no distributed four-step split for n={n}, world={world}")
+
+
+class CudaLocalOps:
+    """One rank's device work for DistFourStep: the fused AM-QFT kernel on
+    rows of length n1 and n2, the twiddle+scatter kernel and the transpose
+    (C ABI amqft_dist_twiddle_scatter / amqft_transpose_c64)."""
+
+    def __init__(self, variant, n, n1, n2, world, device, trig_mode=TrigMode.Precomputed):
+        self.n, self.n1, self.n2 = n, n1, n2
+        self.trig_mode = int(trig_mode)
+        self.p1 = Plan(variant, FunctionId.Cdft, n1, n2 // world, dtype="f32", order=Order.Fast,
+                       device=device)
+        self.p2 = Plan(variant, FunctionId.Cdft, n2, n1 // world, dtype="f32", order=Order.Fast,
+                       device=device)
+
+    def dft_rows1(self, a, stream=None):
+        self.p1.forward(a, a, stream=stream)
+
+    def twiddle_scatter(self, a, dst_ptrs, rows, row0, src, nparts, stream=None):
+        arr = (C.c_void_p * nparts)(*[int(p) for p in dst_ptrs])
+        check(lib().amqft_dist_twiddle_scatter(int(a.data_ptr()), arr, rows, self.n1, self.n, row0, src,
+                                               nparts, self.trig_mode, Plan._stream(stream)))
+
+    def transpose(self, inp, out, r, c, stream=None):
+        check(lib().amqft_transpose_c64(int(inp.data_ptr()), int(out.data_ptr()), 1, r, c,
+                                        Plan._stream(stream)))
+
+    def dft_rows2(self, b, z, stream=None):
+        self.p2.forward(b, z, stream=stream)
+
+
+class DistFourStep:
+    """Distributed four-step CDFT of one length-N signal over the process
+    group (BASELINE config 5).
+
+    n = n1 n2, x viewed as M[n1][n2] = x[n2_total * i1 + i2].  Rank p owns the
+    column slab i2 in [p n2/P, (p+1) n2/P) stored as rows of length n1
+    (`local_input`).  forward():
+      1. length-n1 AM-QFT on the n2/P local rows (fused kernel);
+      2. twiddle w_N^(i2 k1) + scatter by k1-slab (one kernel), into the
+         send slots -- or, with `peer_recv`, straight into the peers'
+         receive buffers over NVLink (the stores are the exchange);
+      3. one all-to-all (NCCL) unless step 2 already delivered;
+      4. transpose [n2][n1/P] -> [n1/P][n2];
+      5. length-n2 AM-QFT on the n1/P rows.
+    The output of rank p is X[k1 + n1 k2] for k1 in [p n1/P, (p+1) n1/P),
+    as rows k1 of length n2 (`global_output` reassembles it).  One exchange:
+    a second all-to-all for natural-order output slabs is not done."""
+
+    def __init__(self, variant: int, n: int, *, group=None, device=None, trig_mode=TrigMode.Precomputed,
+                 ops=None, world: int | None = None, rank: int | None = None):
+        self.group = group
+        self.world = world if world is not None else (dist.get_world_size(group) if dist.is_initialized() else 1)
+        self.rank = rank if rank is not None else (dist.get_rank(group) if dist.is_initialized() else 0)
+        self.n = int(n)
+        self.n1, self.n2 = dist_split(self.n, self.world)
+        P = self.world
+        if self.n1 % P or self.n2 % P:
+            raise ValueError("n1 and n2 must be divisible by the world size")
+        self.rows1 = self.n2 // P          # local rows of length n1
+        self.w = self.n1 // P              # k1 slab width
+        self.device = device
+        self.ops = ops if ops is not None else CudaLocalOps(variant, self.n, self.n1, self.n2, P,
+                                                            device if device is not None else 0, trig_mode)
+
+    # ---- layout helpers (host side)
+    def local_input(self, x_full):
+        """Rank's slab from a full interleaved (re, im) signal: [n2/P][2 n1]."""
+        P, p = self.world, self.rank
+        xc = x_full.reshape(self.n1, self.n2, 2)
+        cols = xc[:, p * self.rows1:(p + 1) * self.rows1, :]
+        if hasattr(cols, "permute"):
+            return cols.permute(1, 0, 2).reshape(self.rows1, 2 * self.n1).contiguous()
+        return cols.transpose(1, 0, 2).reshape(self.rows1, 2 * self.n1).copy()
+
+    def global_output(self, parts):
+        """Natural-order X (interleaved) from every rank's [n1/P][2 n2] output."""
+        import numpy as np
+        X = np.empty((self.n2, self.n1, 2), dtype=np.asarray(parts[0]).dtype)
+        for q, z in enumerate(parts):
+            zc = np.asarray(z).reshape(self.w, self.n2, 2)
+            X[:, q * self.w:(q + 1) * self.w, :] = zc.transpose(1, 0, 2)
+        return X.reshape(-1)
+
+    def buffers(self, like):
+        """send, recv, b, z buffers for forward()."""
+        P = self.world
+        send = like.new_empty((P, self.rows1 * self.w * 2))
+        recv = like.new_empty((P, self.rows1 * self.w * 2))
+        b = like.new_empty((self.w, 2 * self.n2))
+        z = like.new_empty((self.w, 2 * self.n2))
+        return send, recv, b, z
+
+    def stage1(self, a, send, peer_recv=None, stream=None):
+        """Length-n1 transforms of the local rows, then twiddle + scatter by
+        k1-slab into the send slots, or into the peers' receive buffers."""
+        P, p = self.world, self.rank
+        self.ops.dft_rows1(a, stream)
+        row0 = p * self.rows1
+        if peer_recv is not None:
+            self.ops.twiddle_scatter(a, peer_recv, self.rows1, row0, p, P, stream)
+        else:
+            base = int(send.data_ptr())
+            slot = self.rows1 * self.w * 2 * a.element_size()
+            self.ops.twiddle_scatter(a, [base + q * slot for q in range(P)], self.rows1, row0, 0, P, stream)
+
+    def stage2(self, recv, b, z, stream=None):
+        """recv = [n2][n1/P] (complex) -> transpose -> length-n2 transforms."""
+        self.ops.transpose(recv, b, self.n2, self.w, stream)
+        self.ops.dft_rows2(b, z, stream)
+        return z
+
+    def forward(self, a, bufs=None, peer_recv=None, stream=None):
+        """a: this rank's [n2/P][2 n1] slab (overwritten).  Returns z, this
+        rank's [n1/P][2 n2] output slab."""
+        send, recv, b, z = bufs if bufs is not None else self.buffers(a)
+        self.stage1(a, send, peer_recv, stream)
+        if peer_recv is not None:
+            # the scatter's stores were the exchange; order them before the
+            # peers read their receive buffers
+            if self.world > 1 and dist.is_initialized():
+                if a.is_cuda:
+                    torch.cuda.synchronize()
+                dist.barrier(group=self.group)
+        elif self.world > 1:
+            dist.all_to_all_single(recv, send, group=self.group)
+        else:
+            recv = send   # one part: the scatter already produced the layout
+        return self.stage2(recv, b, z, stream)

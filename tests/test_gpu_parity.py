@@ -315,3 +315,67 @@ def test_fast_kernel_larger_table_bitwise(oracle, restatement, n):
         assert plan.path()[0] == 2
         got = run_plan(plan, xs)[0]
         assert got.tobytes() == r.execute(v, O.F_CDFT, n, xs[0]).tobytes(), (v, n)
+
+
+def _dist_run_sim(n, world, mode, x):
+    """Distributed four-step with `world` ranks simulated in this process on
+    one GPU: 'peer' = the fused twiddle-scatter writes straight into every
+    rank's receive buffer (as over NVLink); 'a2a' = send slots, then the
+    all-to-all done by copies."""
+    from paper_1404_1810_b200.dist import DistFourStep
+    ranks = [DistFourStep(4, n, world=world, rank=p, device=0) for p in range(world)]
+    xt = torch.tensor(x)
+    slabs = [r.local_input(xt).to(DEV) for r in ranks]
+    bufs = [r.buffers(slabs[0]) for r in ranks]
+    if mode == "peer":
+        peer = [int(b[1].data_ptr()) for b in bufs]
+        for r, a, b in zip(ranks, slabs, bufs):
+            r.stage1(a, b[0], peer_recv=peer)
+    else:
+        for r, a, b in zip(ranks, slabs, bufs):
+            r.stage1(a, b[0])
+        for q in range(world):
+            for p in range(world):
+                bufs[q][1][p].copy_(bufs[p][0][q])
+    torch.cuda.synchronize()
+    outs = [r.stage2(b[1], b[2], b[3]) for r, b in zip(ranks, bufs)]
+    torch.cuda.synchronize()
+    return ranks[0].global_output([o.cpu().numpy() for o in outs])
+
+
+def test_distributed_fourstep_single_gpu_simulation(oracle, restatement):
+    """Config 5 data path at N = 2^20 on one GPU: world 1, and world 2/4
+    simulated in-process through both exchange modes; every layout gives
+    the same bits, and the result matches the fp64 oracle (variant 4)."""
+    r, O = restatement, oracle
+    n = 1 << 20
+    x = np.random.default_rng(55).standard_normal(2 * n).astype(np.float32)
+    base = _dist_run_sim(n, 1, "a2a", x)
+    want = r.execute(4, O.F_CDFT, n, x.astype(np.float64))
+    assert r.rel_l2(base.astype(np.float64), want) <= 1e-5 * 20
+    for world in (2, 4):
+        for mode in ("a2a", "peer"):
+            got = _dist_run_sim(n, world, mode, x)
+            assert got.tobytes() == base.tobytes(), (world, mode)
+
+
+def test_distributed_fourstep_world1_process_group():
+    """The same path through torch.distributed (NCCL, world size 1)."""
+    import torch.distributed as dist
+    from paper_1404_1810_b200.dist import DistFourStep
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29571")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device(DEV))
+    try:
+        n = 1 << 21
+        x = np.random.default_rng(56).standard_normal(2 * n).astype(np.float32)
+        d = DistFourStep(2, n, device=0)
+        z = d.forward(d.local_input(torch.tensor(x)).to(DEV))
+        torch.cuda.synchronize()
+        X = d.global_output([z.cpu().numpy()]).astype(np.float64)
+        f = np.fft.fft(x[0::2].astype(np.float64) + 1j * x[1::2].astype(np.float64))
+        ref = np.empty(2 * n)
+        ref[0::2], ref[1::2] = f.real, f.imag
+        assert np.linalg.norm(X - ref) / np.linalg.norm(ref) <= 1e-5 * 21
+    finally:
+        dist.destroy_process_group()

@@ -66,3 +66,113 @@ def test_gloo_world2_shard_and_gather():
         p.join(timeout=60)
     assert ok
     assert ms == 2.0
+
+
+# ---- distributed four-step (config 5) host logic -----------------------
+class NumpyLocalOps:
+    """TEST STAND-IN for one rank's device kernels (CudaLocalOps): the same
+    index semantics (rows of interleaved fp32 complex, twiddle + scatter by
+    k1-slab into raw slot pointers, transpose) with numpy's FFT for the
+    local transforms.  Lets the gloo test check the distributed orchestration
+    (layouts, all-to-all, output mapping) without a GPU."""
+
+    def __init__(self, n, n1, n2):
+        self.n, self.n1, self.n2 = n, n1, n2
+
+    @staticmethod
+    def _c(t, rows, cols):
+        a = t.numpy().reshape(rows, cols, 2)
+        return a[..., 0] + 1j * a[..., 1]
+
+    @staticmethod
+    def _put(t, z):
+        a = t.numpy().reshape(z.shape + (2,))
+        a[..., 0], a[..., 1] = z.real, z.imag
+
+    def dft_rows1(self, a, stream=None):
+        rows = a.numel() // (2 * self.n1)
+        self._put(a, np.fft.fft(self._c(a, rows, self.n1), axis=1))
+
+    def twiddle_scatter(self, a, dst_ptrs, rows, row0, src, nparts, stream=None):
+        import ctypes as C
+        w = self.n1 // nparts
+        z = self._c(a, rows, self.n1)
+        i2 = (row0 + np.arange(rows))[:, None]
+        k1 = np.arange(self.n1)[None, :]
+        z = z * np.exp(-2j * np.pi * ((i2 * k1) % self.n) / self.n)
+        for q in range(nparts):
+            blk = z[:, q * w:(q + 1) * w]
+            buf = np.ctypeslib.as_array((C.c_float * (2 * rows * w * (src + 1))).from_address(int(dst_ptrs[q])))
+            out = buf[2 * src * rows * w:].reshape(rows, w, 2)
+            out[..., 0], out[..., 1] = blk.real, blk.imag
+
+    def transpose(self, inp, out, r, c, stream=None):
+        self._put(out, self._c(inp, r, c).T.copy())
+
+    def dft_rows2(self, b, z, stream=None):
+        rows = b.numel() // (2 * self.n2)
+        self._put(z, np.fft.fft(self._c(b, rows, self.n2), axis=1))
+
+
+def _dist_worker(rank, world, port, n, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1404_1810_b200.dist import DistFourStep, dist_split
+    n1, n2 = dist_split(n, world)
+    d = DistFourStep(4, n, ops=NumpyLocalOps(n, n1, n2))
+    rng = np.random.default_rng(30)
+    x = rng.standard_normal(2 * n).astype(np.float32)
+    a = d.local_input(torch.tensor(x))
+    z = d.forward(a)
+    parts = [torch.empty_like(z) for _ in range(world)]
+    dist.all_gather(parts, z)
+    if rank == 0:
+        X = d.global_output([p.numpy() for p in parts]).astype(np.float64)
+        f = np.fft.fft(x[0::2].astype(np.float64) + 1j * x[1::2].astype(np.float64))
+        ref = np.empty(2 * n)
+        ref[0::2], ref[1::2] = f.real, f.imag
+        q.put(float(np.linalg.norm(X - ref) / np.linalg.norm(ref)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(180)
+def test_gloo_world2_distributed_fourstep():
+    """Config 5 orchestration at world size 2 over gloo: column slabs in,
+    one all-to-all, k1-slabs out; reassembled output equals the DFT."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    n = 1 << 20
+    ps = [ctx.Process(target=_dist_worker, args=(r, 2, port, n, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    err = q.get(timeout=170)
+    for p in ps:
+        p.join(timeout=60)
+    assert err < 1e-5, err
+
+
+def test_dist_split_and_layout_helpers():
+    from paper_1404_1810_b200.dist import DistFourStep, dist_split
+    assert dist_split(1 << 30, 8) == (1 << 20, 1 << 10)
+    assert dist_split(1 << 24, 2) == (2048, 8192)
+    n = 1 << 20
+    for world in (1, 2, 4):
+        parts = []
+        for rank in range(world):
+            d = DistFourStep(4, n, ops=object(), world=world, rank=rank)
+            x = np.arange(2 * n, dtype=np.float32)
+            loc = d.local_input(x)
+            assert loc.shape == (d.rows1, 2 * d.n1)
+            # local row r, element i1 is x[n2 * i1 + rank * rows1 + r]
+            r, i1 = 3, 5
+            m = d.n2 * i1 + rank * d.rows1 + r
+            assert loc[r, 2 * i1] == x[2 * m]
+            parts.append(np.arange(d.w * 2 * d.n2, dtype=np.float64) + rank * 1e7)
+        X = DistFourStep(4, n, ops=object(), world=world, rank=0).global_output(parts)
+        d = DistFourStep(4, n, ops=object(), world=world, rank=0)
+        # X[k1 + n1 k2] comes from rank k1 // w, row k1 % w, column k2
+        k1, k2 = d.n1 - 1, 7
+        src = parts[k1 // d.w].reshape(d.w, d.n2, 2)[k1 % d.w, k2]
+        assert X[2 * (k1 + d.n1 * k2)] == src[0]
