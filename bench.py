@@ -48,6 +48,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--all-variants", action="store_true",
                    help="also time variants 1..8 (extra 'variants' key)")
+    p.add_argument("--config", type=int, choices=[2, 4, 5], default=2,
+                   help="BASELINE config: 2 batched N=4096 (default), 4 single N=2^24 four-step, "
+                        "5 single N=2^30 distributed four-step over the ranks")
     return p.parse_args()
 
 
@@ -203,11 +206,142 @@ def ncu_traffic(args, n):
     return None, None
 
 
+def _timed(fn, steps, warmup, stream, world, dev):
+    import torch
+    import torch.distributed as dist
+    for _ in range(max(warmup, 3)):
+        fn()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms / steps
+
+
+def cpu_baseline_large(variant, n_full, sample_n, seconds_cap=30.0):
+    """Bounded CPU sample for the single-transform configs: one transform at
+    a smaller N with the reference library, extrapolated by N log N."""
+    import numpy as np
+    from oracle import oracle as O
+    ref = O.reference()
+    kind = "reference"
+    if ref is None:
+        ref, kind = O.restatement(), "port"
+    x = np.random.default_rng(7).standard_normal(2 * sample_n)
+    t0 = time.perf_counter()
+    if kind == "reference":
+        ref.execute_rows(variant, O.CDFT, sample_n, x.reshape(1, -1), 1)
+    else:
+        ref.execute(variant, O.F_CDFT, sample_n, x)
+    dt = time.perf_counter() - t0
+    lg_s, lg_f = sample_n.bit_length() - 1, n_full.bit_length() - 1
+    est = dt * (n_full * lg_f) / (sample_n * lg_s)
+    return {"value": 1.0 / est, "unit": UNIT, "cores": 1, "kind": kind,
+            "sample": f"one CDFT N=2^{lg_s} (variant {variant}) in {dt:.1f} s on 1 thread (one transform does not "
+                      f"parallelise in the reference), extrapolated to N=2^{lg_f} by N log N: {est:.0f} s"}
+
+
+def bench_single(args, world, rank, local):
+    """Configs 4 (N=2^24, one GPU, four-step) and 5 (N=2^30, distributed
+    four-step over the ranks, one all-to-all)."""
+    import torch
+    import torch.distributed as dist
+    import paper_1404_1810_b200 as amqft
+    from paper_1404_1810_b200.dist import DistFourStep
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.current_stream(dev)
+    hbm, hbm_src = peaks()
+    g = torch.Generator(device=dev)
+    g.manual_seed(4242 + rank)
+    extra = {}
+    if args.config == 4:
+        n = 1 << 24
+        plan = amqft.Plan(args.variant, amqft.FunctionId.Cdft, n, 1, dtype="f32", order=amqft.Order.Fast,
+                          device=local)
+        x = torch.randn(1, 2 * n, generator=g, device=dev)
+        y = torch.empty_like(x)
+        ms = _timed(lambda: plan.forward(x, y, stream=stream), args.steps, args.warmup, stream, world, dev)
+        path, launches = plan.path()
+        workload = f"config 4: one complex forward DFT N=2^24 fp32, four-step 4096 x 4096 over the fused kernel, variant {args.variant}"
+        per_gpu_bytes = 16 * n
+        value = world / (ms / 1000.0)
+        hx = torch.empty(1, 2 * n, pin_memory=True)
+        hx.copy_(x)
+        hy = torch.empty_like(hx, pin_memory=True)
+        plan.forward_host(hx, hy, stream=stream)
+        e2e_ms = _timed(lambda: plan.forward_host(hx, hy, stream=stream), 3, 1, stream, world, dev)
+        e2e = {"value": world / (e2e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": 8 * n,
+               "d2h_bytes_per_step": 8 * n}
+        extra = {"hbm_passes": 5, "traffic_model_bytes": 5 * 16 * n}
+        cpu = cpu_baseline_large(args.variant, n, 1 << 20) if (rank == 0 and not args.no_cpu_baseline) else None
+    else:
+        n = 1 << 30
+        d = DistFourStep(args.variant, n, device=local)
+        # each rank generates its own column slab on the device (config 5)
+        a0 = torch.randn(d.rows1, 2 * d.n1, generator=g, device=dev)
+        a = torch.empty_like(a0)
+        bufs = d.buffers(a0)
+
+        def step():
+            a.copy_(a0)
+            d.forward(a, bufs=bufs, stream=stream)
+        ms = _timed(step, args.steps, args.warmup, stream, world, dev)
+        copy_ms = _timed(lambda: a.copy_(a0), args.steps, 1, stream, world, dev)
+        a2a_ms = None
+        if world > 1:
+            a2a_ms = _timed(lambda: dist.all_to_all_single(bufs[1], bufs[0]), args.steps, 1, stream, world, dev)
+        sent = (world - 1) * d.rows1 * d.w * 8
+        ms = ms - copy_ms        # the slab refresh is not part of the transform
+        path, launches = 3, None
+        workload = (f"config 5: one complex forward DFT N=2^30 fp32 over {world} GPU(s), distributed four-step "
+                    f"n1=2^{d.n1.bit_length() - 1} x n2=2^{d.n2.bit_length() - 1}, one all-to-all, variant {args.variant}")
+        per_gpu_bytes = 16 * n // world
+        value = 1.0 / (ms / 1000.0)
+        e2e = None
+        extra = {"a2a_ms": a2a_ms, "a2a_bytes_sent_per_gpu": sent,
+                 "nvlink_frac": (sent / (a2a_ms / 1000.0) / 900e9) if a2a_ms else None,
+                 "output_layout": "k1-slabs (rows k1 of length n2 per rank); no second all-to-all"}
+        cpu = None
+    achieved = per_gpu_bytes / (ms / 1000.0) / 1e9
+    if rank == 0:
+        line = {
+            "metric": f"AM-QFT transforms/s ({'N=2^24' if args.config == 4 else 'N=2^30'} fp32 single transform)",
+            "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic: iid N(0,1) from a seed, generated on the device",
+            "config": {"workload": workload, "n": n, "variant": args.variant, "path": path,
+                       "l2": "inputs >= 128 MiB > 126 MB L2; no flush"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": None, "peak_source": hbm_src,
+                         "algorithmic_bytes_per_gpu": per_gpu_bytes},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, **extra,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.config in (4, 5) and args.impl == "ours":
+        bench_single(args, world, rank, local)
+        return
 
     if args.impl == "reference":
         line = bench_reference(args, rank)

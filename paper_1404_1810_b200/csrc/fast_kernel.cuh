@@ -559,8 +559,12 @@ template <int V, typename R, int LOGN, int LOGLB, bool INV>
 #ifndef AMQFT_FAST_MINB
 #define AMQFT_FAST_MINB 2
 #endif
+// min blocks per SM: 2 only where two CTAs fit in shared memory (one-row
+// fp32 CTAs up to N = 4096); otherwise let ptxas use up to 255 registers
 __global__ void __launch_bounds__(Cfg<V, R, LOGN, LOGLB>::NTB,
-                                  (Cfg<V, R, LOGN, LOGLB>::RPC > 1 ? 1 : (sizeof(R) == 4 ? AMQFT_FAST_MINB : 1)))
+                                  ((Cfg<V, R, LOGN, LOGLB>::RPC == 1 && sizeof(R) == 4 &&
+                                    2 * Cfg<V, R, LOGN, LOGLB>::SMEM_BLOCK <= 227 * 1024)
+                                       ? AMQFT_FAST_MINB : 1))
 k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
        const R* __restrict__ tab, const R* __restrict__ ltab, int nmax, R scale) {
 #ifdef AMQFT_PHASE_TIMING
