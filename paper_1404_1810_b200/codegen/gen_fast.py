@@ -187,7 +187,7 @@ def gen_tmB(v, LB, rho, lam, part=None):
             em.emit(f"  if constexpr (D >= 5) Fq[{store_off(p)}] = {name}; "
                     f"else F[SW(hi - ({p} << D))] = {name};")
         em.emit("}")
-        em.emit('asm volatile("" ::: "memory");  // keep classes apart (register pressure)')
+        em.emit("AMQFT_CLASS_FENCE();  // keep classes apart (register pressure)")
     sfx = "" if part is None else f"_p{part}"
     sig = (f"template <typename R, typename AR, int LOGLB, int D>\n__device__ __forceinline__ void "
            f"tmB_v{v}_lb{LB}_r{rho}_l{lam}{sfx}(const R* __restrict__ T, R* __restrict__ F, int a, "
@@ -344,7 +344,7 @@ def gen_hmB(v, LB, rho, lam, part=None):
         for u in sorted(x):
             em.emit(f"Fp[{u}] = {x[u]};")
         em.emit("}")
-        em.emit('asm volatile("" ::: "memory");  // keep classes apart (register pressure)')
+        em.emit("AMQFT_CLASS_FENCE();  // keep classes apart (register pressure)")
     sfx = "" if part is None else f"_p{part}"
     sig = (f"template <typename R, typename AR, int LOGLB, int D>\n__device__ __forceinline__ void "
            f"hmB_v{v}_lb{LB}_r{rho}_l{lam}{sfx}(const R* __restrict__ T, R* __restrict__ F, int a, "
@@ -882,6 +882,9 @@ def main():
         "#pragma once",
         "#define PH(i) ((i) + ((i) >> LOGLB))",
         "#define SW(i) ((i) + (((i) + swsh) >> 5))",
+        "#ifndef AMQFT_CLASS_FENCE",
+        "#define AMQFT_CLASS_FENCE() asm volatile(\"\" ::: \"memory\")",
+        "#endif",
         "namespace amqft_b200 {",
         "namespace gen {",
     ]

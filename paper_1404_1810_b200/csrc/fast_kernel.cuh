@@ -42,6 +42,9 @@
 #ifndef AMQFT_TMA_STAGE
 #define AMQFT_TMA_STAGE 1   // stage the next row with cp.async.bulk (else direct loads)
 #endif
+#ifndef AMQFT_SLOT_BARRIER
+#define AMQFT_SLOT_BARRIER 1
+#endif
 #ifndef AMQFT_TMA_STORE
 #define AMQFT_TMA_STORE 1   // fp32 N <= 4096: assemble the output row in smem, one bulk store
 #endif
@@ -431,49 +434,42 @@ __device__ __forceinline__ void am_phase_regs(R* B, int tid) {
 // one shuffle otherwise.  Same operations and operand order as
 // codegen/gen_fast.py emit_pair (Dct chains use every cell; Dst chains skip
 // i = 0 and i = 64), so the fp64 instance stays bitwise.
-template <typename R, bool FOLD>
-__device__ __forceinline__ void pair_op(int lam, R e, R o, R& e2, R& o2) {
+template <typename R, bool FOLD, int LAM>
+__device__ __forceinline__ void pair_op(R e, R o, R& e2, R& o2) {
   using A = Arith<R>;
   if (!FOLD) {  // SplitTimeParity bwd (elaborations.cpp:310-329)
-    e2 = lam ? A::add(o, e) : A::add(e, o);
-    o2 = lam ? A::sub(o, e) : A::sub(e, o);
+    e2 = LAM ? A::add(o, e) : A::add(e, o);
+    o2 = LAM ? A::sub(o, e) : A::sub(e, o);
   } else {      // SplitHarmonicParity fwd (elaborations.cpp:238-255)
-    e2 = lam ? A::sub(e, o) : A::add(e, o);
-    o2 = lam ? A::add(e, o) : A::sub(e, o);
+    e2 = LAM ? A::sub(e, o) : A::add(e, o);
+    o2 = LAM ? A::add(e, o) : A::sub(e, o);
   }
 }
 
-template <typename R, bool FOLD>
-__device__ __forceinline__ void special_class64(R* ch, int lam, int lane) {
+// Predicated (no lane-dependent branches): every lane evaluates the pair
+// op and keeps its result only where it owns a cell of the pair.
+template <typename R, bool FOLD, int LAM>
+__device__ __forceinline__ void special_class64_l(R* ch, int lane) {
   R a = ch[33 * lane], b = ch[33 * (64 - lane)];
-  R m = lane == 0 ? ch[33 * 32] : R(0);
+  R m = ch[33 * 32];                               // used by lane 0 only
+  const bool own0 = !(LAM && lane == 0);           // Dst chains: no cell 0 / 64
   auto level = [&](int t) {
-    if (t == 5) {
-      if (!(lam && lane == 0)) {
-        R e2, o2;
-        pair_op<R, FOLD>(lam, a, b, e2, o2);
-        a = e2;
-        b = o2;
-      }
+    R e2, o2;
+    if (t == 5) {                                  // in-lane pairs (i, 64 - i)
+      pair_op<R, FOLD, LAM>(a, b, e2, o2);
+      a = own0 ? e2 : a;
+      b = own0 ? o2 : b;
       return;
     }
     const int P = 2 << t, Hh = 1 << t;
     const int src = lane <= P ? (P - lane) & 31 : lane;
     const R pv = __shfl_sync(0xffffffffu, a, src);
-    R e2, o2;
-    if (lane == 0) {
-      if (!lam) {
-        pair_op<R, FOLD>(lam, a, t == 4 ? m : pv, e2, o2);
-        a = e2;
-        if (t == 4) m = o2;
-      }
-    } else if (lane < Hh) {
-      pair_op<R, FOLD>(lam, a, pv, e2, o2);
-      a = e2;
-    } else if (lane > Hh && lane <= P && !(lam && lane == P)) {
-      pair_op<R, FOLD>(lam, pv, a, e2, o2);
-      a = o2;
-    }
+    const R other = (t == 4 && lane == 0) ? m : pv;
+    const bool lower = lane < Hh && own0;
+    const bool upper = lane > Hh && lane <= P && !(LAM && lane == P);
+    pair_op<R, FOLD, LAM>(lower ? a : other, lower ? other : a, e2, o2);
+    if (t == 4 && lane == 0 && !LAM) m = o2;
+    a = lower ? e2 : (upper ? o2 : a);
   };
   if (FOLD) {
 #pragma unroll
@@ -482,11 +478,17 @@ __device__ __forceinline__ void special_class64(R* ch, int lam, int lane) {
 #pragma unroll
     for (int t = 0; t <= 5; ++t) level(t);
   }
-  if (!(lam && lane == 0)) {
+  if (own0) {
     ch[33 * lane] = a;
     ch[33 * (64 - lane)] = b;
   }
-  if (lane == 0 && !lam) ch[33 * 32] = m;
+  if (lane == 0 && !LAM) ch[33 * 32] = m;
+}
+
+template <typename R, bool FOLD>
+__device__ __forceinline__ void special_class64(R* ch, int lam, int lane) {
+  if (lam) special_class64_l<R, FOLD, 1>(ch, lane);   // warp-uniform
+  else special_class64_l<R, FOLD, 0>(ch, lane);
 }
 
 // ---- TMA bulk staging of the next row (cp.async.bulk + mbarrier).
@@ -583,6 +585,15 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
   R* Sb = reinterpret_cast<R*>(sm + C::STAGE_OFF);
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::STAGE_OFF + 2 * C::N * sizeof(R));
   constexpr size_t RSTEP = C::RPC;   // rows per CTA iteration
+  // Barrier of one row slot.  AMQFT_SLOT_BARRIER=1 (default): a named
+  // barrier per slot, the two rows drift apart (measured 1.58 -> 1.54 ms,
+  // v4); 0: the CTA barrier, both rows in lockstep.
+  auto row_sync = [&]() {
+    if constexpr (AMQFT_SLOT_BARRIER && C::RPC > 1)
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + slot), "r"(C::NT) : "memory");
+    else
+      __syncthreads();
+  };
   const R base = __ldg(tab + (nmax / 4 - 1));
   constexpr int N = C::N, H = C::H;
   constexpr uint32_t ROW_BYTES = 2 * N * sizeof(R);
@@ -603,7 +614,7 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
     mbar_init(bar, 1);
     fence_mbar_init();
   }
-  __syncthreads();
+  row_sync();
   if (tid == 0 && blockIdx.x * RSTEP + slot < rows)
     tma_load_1d(Sb, in + (blockIdx.x * RSTEP + slot) * 2 * N, ROW_BYTES, bar);
   uint32_t parity = 0;
@@ -639,18 +650,27 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       R* t1 = Tb + C::coT(1) + q1;
       R* t2 = Tb + C::coT(2) + q0;
       R* t3 = Tb + C::coT(3) + q1;
+      // all staged reads first (the compiler cannot hoist them over the
+      // T stores itself: both are shared memory), then the stores
+      V2 av[IO_IT], bv[IO_IT];
 #pragma unroll
       for (int it = 0; it < IO_IT; ++it) {
         const int m = tid + it * IO_T;
-        V2 a = x[m];
-        if (INV) a = V2{a.y, a.x};
+        av[it] = x[m];
+        bv[it] = x[(N - m) & (N - 1)];   // m = 0: in range, unused
+      }
+#pragma unroll
+      for (int it = 0; it < IO_IT; ++it) {
+        V2 a = av[it], b = bv[it];
+        if (INV) {
+          a = V2{a.y, a.x};
+          b = V2{b.y, b.x};
+        }
         if (it == 0 && tid == 0) {   // m = 0: Dct chains only
           t0[0] = a.x;
           t2[0] = a.y;
           continue;
         }
-        V2 b = x[N - m];
-        if (INV) b = V2{b.y, b.x};
         t0[it * PT_STEP] = A::add(a.x, b.x);
         t1[it * PT_STEP] = A::sub(a.x, b.x);
         t2[it * PT_STEP] = A::add(a.y, b.y);
@@ -664,7 +684,7 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       }
     }
     WORK_MARK(0);
-    __syncthreads();
+    row_sync();
 #if AMQFT_TMA_STAGE
     if (tid == 0 && row + gridDim.x * RSTEP < rows) {
       fence_proxy_async();
@@ -690,12 +710,12 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
         } else if (tid < 256) {
           special_class64<R, true>(Tb + C::coT((tid >> 5) - 4), (tid >> 5) & 1, tid & 31);
         }
-        __syncthreads();
+        row_sync();
       } else {
 #pragma unroll 1
         for (int n = N; n >= 2 * (N / C::LB); n >>= 1) {
           if (act) chain_level<C, R, true>(Tb, n, tid);
-          __syncthreads();
+          row_sync();
         }
       }
       // serial recurrences: fp64 in the reference order (bitwise), fp32 as warp scans
@@ -708,7 +728,7 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
     // a top phase ago); make it formal before the bottom writes F
     if (BULK_ST && tid == 0) bulk_wait_read_all();
     WORK_MARK(1);
-    __syncthreads();
+    row_sync();
     PHASE_MARK(2);
 
     // ---- bottom: T -> F (generated).  One thread per LB-segment runs both
@@ -743,7 +763,7 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       }
     }
     WORK_MARK(2);
-    __syncthreads();
+    row_sync();
     PHASE_MARK(3);
 
     if constexpr (C::TM) {
@@ -752,7 +772,7 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       // small-chain recombination Dct/Dst(4..N/LB) on F cells [0, N/LB]
       // (disjoint from the AM levels): lane 31 of chain c's second warp
       WORK_MARK(3);
-      __syncthreads();
+      row_sync();
       PHASE_MARK(4);
       if constexpr (N / C::LB == 64) {
         // generated: each thread owns the 64 cells j*64 +- k of its chain
@@ -764,12 +784,12 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
           special_class64<R, false>(Fb + C::coF((tid >> 5) - 4), (tid >> 5) & 1, tid & 31);
         }
         WORK_MARK(4);
-        __syncthreads();
+        row_sync();
       } else {
 #pragma unroll 1
         for (int n = 2 * (N / C::LB); n <= N; n <<= 1) {
           if (act) chain_level<C, R, false>(Fb, n, tid);
-          __syncthreads();
+          row_sync();
         }
       }
     } else {
@@ -778,7 +798,7 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
         if (v > 0) Top<C::LB, C::LT, LOGN, C::SINE>::template bwd<R, A>(c & 1, Fb + C::coF(c), v, ltab, base);
       }
       WORK_MARK(4);
-      __syncthreads();
+      row_sync();
     }
     PHASE_MARK(5);
 
@@ -811,7 +831,7 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
           yH = INV ? V2{A::mul(id, scale), A::mul(rd, scale)} : V2{rd, id};
         }
       }
-      __syncthreads();
+      row_sync();
       if (act && tid < IO_T) {
         V2* ob = reinterpret_cast<V2*>(Fb);
 #pragma unroll
@@ -823,7 +843,7 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
         if (tid == 0) ob[H] = yH;
         fence_proxy_async();         // generic-proxy writes -> async proxy
       }
-      __syncthreads();
+      row_sync();
       if (act && tid == 0) bulk_store(y, Fb, ROW_BYTES);
     } else {
       // Cells k = tid + 256 it and k = H (thread 0), immediate offsets as in

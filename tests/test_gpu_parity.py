@@ -379,3 +379,18 @@ def test_distributed_fourstep_world1_process_group():
         assert np.linalg.norm(X - ref) / np.linalg.norm(ref) <= 1e-5 * 21
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("lg", [13, 16, 20])
+def test_exact_fp64_large_n_bitwise(oracle, restatement, lg):
+    """Config 3 sizes on the generic multi-pass path: exact order, fp64,
+    bitwise the oracle (forward and swap-trick inverse), U[-1,1) inputs."""
+    r, O = restatement, oracle
+    n = 1 << lg
+    x = O.seeded_signal(3, O.CDFT, n, lg, r)
+    plan = amqft.Plan(4, amqft.FunctionId.Cdft, n, 1, dtype="f64", order=amqft.Order.Exact)
+    got = run_plan(plan, [x])[0]
+    want = r.execute(4, O.F_CDFT, n, x)
+    assert got.tobytes() == want.tobytes()
+    inv = run_plan(plan, [want], inverse=True)[0]
+    assert inv.tobytes() == r.inverse_cdft(4, n, want).tobytes()
