@@ -163,21 +163,26 @@ def store_off(p):
 
 def gen_tmB(v, LB, rho, lam, part=None):
     """Class by class: mirror folds never mix trailing-zero classes
-    (tz(v) == tz(L - v)), so each class is loaded, transformed and stored
-    on its own -- small live register set.  Addresses are immediate offsets
-    from two per-thread bases (segment start in T, class top in F)."""
+    (tz(v) == tz(L - v)), so each class is transformed and stored on its own
+    -- small live register set.  Addresses are immediate offsets from two
+    per-thread bases (segment start in T, class top in F).  part 0 = class
+    0, part 1 = classes 1.., part 2 = all classes with every T load hoisted
+    to the top (the stores of one class would otherwise keep the next
+    class's loads waiting: both are shared memory)."""
     sine = 1 if v >= 5 else 0
     lg = LB.bit_length() - 1
     em = Emitter()
-    em.emit("const R* __restrict__ Tp = T + a + (a >> LOGLB);")
-    em.emit("const int swsh = dsto ? 0 : 31;")
+    ld = Emitter()
+    hoist = part == 2
+    ld.emit("const R* __restrict__ Tp = T + a + (a >> LOGLB);")
+    ld.emit("const int swsh = dsto ? 0 : 31;")
     for t in range(lg):
-        if part is not None and (t == 0) != (part == 0):
+        if part in (0, 1) and (t == 0) != (part == 0):
             continue
         x = {}
         for u in range(1, LB):
             if tz(u) == t:
-                em.emit(f"const R x{u} = Tp[{u}];")
+                (ld if hoist else em).emit(f"const R x{u} = Tp[{u}];")
                 x[u] = f"x{u}"
         mnet_fwd(em, x, 0, LB, rho, lam, sine, cls=t)
         sp = spectrum_tm(em, v, x, 0, LB, rho, lam, sine, t)
@@ -187,12 +192,13 @@ def gen_tmB(v, LB, rho, lam, part=None):
             em.emit(f"  if constexpr (D >= 5) Fq[{store_off(p)}] = {name}; "
                     f"else F[SW(hi - ({p} << D))] = {name};")
         em.emit("}")
-        em.emit("AMQFT_CLASS_FENCE();  // keep classes apart (register pressure)")
+        if not hoist:
+            em.emit("AMQFT_CLASS_FENCE();  // keep classes apart (register pressure)")
     sfx = "" if part is None else f"_p{part}"
     sig = (f"template <typename R, typename AR, int LOGLB, int D>\n__device__ __forceinline__ void "
            f"tmB_v{v}_lb{LB}_r{rho}_l{lam}{sfx}(const R* __restrict__ T, R* __restrict__ F, int a, "
            f"const R* __restrict__ tab, int nmax, R base, int N, int r, int dsto)")
-    return sig + " {\n" + "\n".join(em.lines) + "\n}\n"
+    return sig + " {\n" + "\n".join(ld.lines + em.lines) + "\n}\n"
 
 
 def gen_tmS(v, HP, LB, lam):
@@ -321,35 +327,43 @@ def mnet_bwd(em, x, a, L, rho, lens, sine, cls=None):
 
 
 def gen_hmB(v, LB, rho, lam, part=None):
-    """Class by class (see gen_tmB)."""
+    """Class by class (see gen_tmB; part 2 hoists every T load)."""
     sine = 1 if v >= 5 else 0
     lg = LB.bit_length() - 1
     em = Emitter()
-    em.emit("R* __restrict__ Fp = F + a + (a >> LOGLB);")
-    em.emit("const int swsh = dsto ? 0 : 31;")
+    ld = Emitter()
+    hoist = part == 2
+    ld.emit("R* __restrict__ Fp = F + a + (a >> LOGLB);")
+    ld.emit("const int swsh = dsto ? 0 : 31;")
     for t in range(lg):
-        if part is not None and (t == 0) != (part == 0):
+        if part in (0, 1) and (t == 0) != (part == 0):
             continue
         x = {}
         cnt = LB >> (t + 1)
-        em.emit(f"{{ const int hi{t} = (N >> {t + 1}) - dsto - r;")
-        em.emit(f"  const R* __restrict__ Tq = T + SW(hi{t});")
+        tgt = ld if hoist else em
+        if not hoist:
+            em.emit("{")
+        tgt.emit(f"const int hi{t} = (N >> {t + 1}) - dsto - r;")
+        tgt.emit(f"const R* __restrict__ Tq{t} = T + SW(hi{t});")
         vals = []
         for p in range(cnt):
             nm = f"v{t}_{p}"
-            em.emit(f"const R {nm} = (D >= 5) ? Tq[{store_off(p)}] : T[SW(hi{t} - ({p} << D))];")
+            tgt.emit(f"const R {nm} = (D >= 5) ? Tq{t}[{store_off(p)}] : T[SW(hi{t} - ({p} << D))];")
             vals.append(nm)
+        if hoist:
+            em.emit("{")
         place_hm(em, v, vals, lam, sine, x, 0, LB, rho)
         mnet_bwd(em, x, 0, LB, rho, lam, sine, cls=t)
         for u in sorted(x):
             em.emit(f"Fp[{u}] = {x[u]};")
         em.emit("}")
-        em.emit("AMQFT_CLASS_FENCE();  // keep classes apart (register pressure)")
+        if not hoist:
+            em.emit("AMQFT_CLASS_FENCE();  // keep classes apart (register pressure)")
     sfx = "" if part is None else f"_p{part}"
     sig = (f"template <typename R, typename AR, int LOGLB, int D>\n__device__ __forceinline__ void "
            f"hmB_v{v}_lb{LB}_r{rho}_l{lam}{sfx}(const R* __restrict__ T, R* __restrict__ F, int a, "
            f"const R* __restrict__ tab, int nmax, R base, int N, int r, int dsto)")
-    return sig + " {\n" + "\n".join(em.lines) + "\n}\n"
+    return sig + " {\n" + "\n".join(ld.lines + em.lines) + "\n}\n"
 
 
 def gen_hmS(v, HP, LB, lam):
@@ -893,7 +907,7 @@ def main():
         for v in range(1, 9):
             for rho in (0, 1):
                 for lam in (0, 1):
-                    for part in (0, 1):
+                    for part in ((0, 1, 2) if rho == 0 else (0, 1)):
                         out.append(gen_tmB(v, LB, rho, lam, part) if v in TM else gen_hmB(v, LB, rho, lam, part))
     for v in range(1, 9):
         for hp in hp_all:
@@ -1010,8 +1024,10 @@ def main():
                        "const R* tab, int nmax, R base, int N, int r, int dsto) {")
             for rho in (0, 1):
                 for lam in (0, 1):
+                    p2 = (f"else if constexpr (PART == 2) gen::{fam}_v{v}_lb{LB}_r{rho}_l{lam}_p2"
+                          f"<R, AR, LOGLB, D>(T, F, a, tab, nmax, base, N, r, dsto); ") if rho == 0 else ""
                     out.append(f"    if (rho == {rho} && lens == {lam}) {{ if constexpr (PART == 0) gen::{fam}_v{v}_lb{LB}_r{rho}_l{lam}_p0"
-                               f"<R, AR, LOGLB, D>(T, F, a, tab, nmax, base, N, r, dsto); else gen::{fam}_v{v}_lb{LB}_r{rho}_l{lam}_p1"
+                               f"<R, AR, LOGLB, D>(T, F, a, tab, nmax, base, N, r, dsto); {p2}else gen::{fam}_v{v}_lb{LB}_r{rho}_l{lam}_p1"
                                f"<R, AR, LOGLB, D>(T, F, a, tab, nmax, base, N, r, dsto); return; }}")
             out.append("  }")
             out.append("};")

@@ -42,6 +42,9 @@
 #ifndef AMQFT_TMA_STAGE
 #define AMQFT_TMA_STAGE 1   // stage the next row with cp.async.bulk (else direct loads)
 #endif
+#ifndef AMQFT_BOTTOM_HOIST
+#define AMQFT_BOTTOM_HOIST 1   // bottom: one function per segment, T loads hoisted (else class groups 0 | 1..)
+#endif
 #ifndef AMQFT_SLOT_BARRIER
 #define AMQFT_SLOT_BARRIER 1
 #endif
@@ -563,7 +566,12 @@ template <int V, typename R, int LOGN, int LOGLB, bool INV>
 #endif
 // min blocks per SM: 2 only where two CTAs fit in shared memory (one-row
 // fp32 CTAs up to N = 4096); otherwise let ptxas use up to 255 registers
-__global__ void __launch_bounds__(Cfg<V, R, LOGN, LOGLB>::NTB,
+__global__ void __launch_bounds__(
+#ifdef AMQFT_LB_THREADS   // register-budget experiments (tools/ab_kernel.cu)
+                                  AMQFT_LB_THREADS,
+#else
+                                  Cfg<V, R, LOGN, LOGLB>::NTB,
+#endif
                                   ((Cfg<V, R, LOGN, LOGLB>::RPC == 1 && sizeof(R) == 4 &&
                                     2 * Cfg<V, R, LOGN, LOGLB>::SMEM_BLOCK <= 227 * 1024)
                                        ? AMQFT_FAST_MINB : 1))
@@ -745,10 +753,16 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       int rho, lens, r;
       seg_params<C::SINE>(lam_bit, s, C::LT, &rho, &lens, &r);
       rho = 0;   // odd segments are stored reversed (Cfg::ipos)
+#if AMQFT_BOTTOM_HOIST
+      // all classes in one function, every T load hoisted above the F stores
+      Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, 2>(rho, lens, Tb + C::coT(c), Fb + C::coF(c),
+                                                            s * C::LB, tab, nmax, base, N, r, lam_bit);
+#else
       Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, 0>(rho, lens, Tb + C::coT(c), Fb + C::coF(c),
                                                             s * C::LB, tab, nmax, base, N, r, lam_bit);
       Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, 1>(rho, lens, Tb + C::coT(c), Fb + C::coF(c),
                                                             s * C::LB, tab, nmax, base, N, r, lam_bit);
+#endif
     } else {
       // the small chains (cells at multiples of LB; disjoint from the
       // segments' cells in T and F), one lane per chain, one warp each
