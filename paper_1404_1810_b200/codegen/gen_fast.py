@@ -647,16 +647,16 @@ def gen_recomb(W, HW, lam, special, fold=False):
         def val(c):  # symbolic (jW, sign)
             return (c[1] * W, 1 if c[0] == "a" else -1)
         name = {c: f"{c[0]}{c[1]}" for c in cells}
-        assert W == 64
-        # phys(y) = y + (y + sh)/32, sh = 31 (Dct chain) / 0 (Dst chain)
-        if lam == 0:
-            em.emit("R* __restrict__ pa = F + 1 + k;")
-            em.emit("R* __restrict__ pb = F - k;")
-        else:
-            em.emit("R* __restrict__ pa = F + k;")
-            em.emit("R* __restrict__ pb = F - 1 - k;")
+        assert W >= 64 and W % 32 == 0
+        # phys(y) = y + (y + sh)/32, sh = 31 (Dct chain) / 0 (Dst chain):
+        # phys(jW +- k) = j (W + W/32) +- k + ((sh +- k) >> 5), the last term a
+        # per-thread constant (arithmetic shift = floor)
+        JS = W + W // 32
+        em.emit(f"constexpr int swsh = {31 if lam == 0 else 0};")
+        em.emit("R* __restrict__ pa = F + k + ((k + swsh) >> 5);")
+        em.emit("R* __restrict__ pb = F - k + ((swsh - k) >> 5);")
         for c in cells:
-            off = c[1] * 66
+            off = c[1] * JS
             em.emit(f"R {name[c]} = {'pa' if c[0] == 'a' else 'pb'}[{off}];")
         levels = []
         n = 2 * W
@@ -681,7 +681,7 @@ def gen_recomb(W, HW, lam, special, fold=False):
                 t = em.tmp
                 emit_pair(em, e, o, t, lam, fold)
         for c in cells:
-            off = c[1] * 66
+            off = c[1] * JS
             em.emit(f"{'pa' if c[0] == 'a' else 'pb'}[{off}] = {name[c]};")
         nm = "fold" if fold else "recomb"
         sig = (f"template <typename R, typename AR>\n__device__ __forceinline__ void "
@@ -942,20 +942,19 @@ def main():
             out.append(gen_small_hm_fold(HP, lam))
     for LB, nlog in FULL_SIZES:
         N = 1 << nlog
-        W = N // LB
+        W = max(64, N // LB)      # recombination thread sets {j W +- k}
         HW = (N // 2) // W
-        if W == 64:
-            for lam in (0, 1):
-                for fold in (False, True):
-                    out.append(gen_recomb(W, HW, lam, False, fold))
-                    out.append(gen_recomb(W, HW, lam, True, fold))
+        for lam in (0, 1):
+            for fold in (False, True):
+                out.append(gen_recomb(W, HW, lam, False, fold))
+                out.append(gen_recomb(W, HW, lam, True, fold))
     out.append("}  // namespace gen")
     out.append("template <int W, int HW> struct Recomb;")
     for LB, nlog in FULL_SIZES:
         N = 1 << nlog
-        W = N // LB
+        W = max(64, N // LB)
         HW = (N // 2) // W
-        if W == 64:
+        if True:
             out.append(f"template <> struct Recomb<{W}, {HW}> {{")
             out.append("  template <typename R, typename AR>")
             out.append("  static __device__ __forceinline__ void run(int lam, R* F, int k) {")

@@ -42,9 +42,6 @@
 #ifndef AMQFT_TMA_STAGE
 #define AMQFT_TMA_STAGE 1   // stage the next row with cp.async.bulk (else direct loads)
 #endif
-#ifndef AMQFT_BOTTOM_HOIST
-#define AMQFT_BOTTOM_HOIST 1   // bottom: one function per segment, T loads hoisted (else class groups 0 | 1..)
-#endif
 #ifndef AMQFT_SLOT_BARRIER
 #define AMQFT_SLOT_BARRIER 1
 #endif
@@ -69,10 +66,11 @@ struct Cfg {
   static constexpr int LT = LOGH - LOGLB;        // depth of the bottom segments
   static constexpr int HP = H / LB;               // cells at multiples of LB
   static constexpr int NSEG = 4 * HP;             // bottom segments (4 chains)
-  // threads: top levels use 4*LB, the bottom NSEG + one warp for the
-  // small top blocks, the AM phase 8 warps
-  static constexpr int NT0 = (4 * LB > NSEG + 32 ? 4 * LB : NSEG + 32);
-  static constexpr int NT = NT0 < 256 ? 256 : NT0;
+  // threads: top levels use 4*LB, the AM phase 8 warps, the bottom 4 warps
+  // (N <= 4096: + 4 small-chain lanes on the others) or NSEG = 256 threads
+  // (N = 8192: + two warps for the small chains, one per lam)
+  static constexpr int NT0 = (4 * LB > NSEG + 64 ? 4 * LB : NSEG + 64);
+  static constexpr int NT = NSEG >= 256 ? NT0 : 256;
   // chain stride: holds the skewed (H + H/LB + 1) and the swizzled
   // (32-aligned blocks up to H) layouts; +16 staggers the chains' banks.
   static constexpr int CS = ((H + HP + 1 > H + H / 32 + 1 ? H + HP + 1 : H + H / 32 + 1) + 31) / 32 * 32 + 16;
@@ -451,11 +449,19 @@ __device__ __forceinline__ void pair_op(R e, R o, R& e2, R& o2) {
 
 // Predicated (no lane-dependent branches): every lane evaluates the pair
 // op and keeps its result only where it owns a cell of the pair.
-template <typename R, bool FOLD, int LAM>
-__device__ __forceinline__ void special_class64_l(R* ch, int lane) {
-  R a = ch[33 * lane], b = ch[33 * (64 - lane)];
-  R m = ch[33 * 32];                               // used by lane 0 only
-  const bool own0 = !(LAM && lane == 0);           // Dst chains: no cell 0 / 64
+// General form for HW in {8, 16, 32}: cells i in [0, 2 HW] (y = i W/2,
+// physical ST i), lane l holds i = l (l <= 2 HW), for HW = 32 also
+// i = 64 - l, for HW >= 16 lane 0 also i = 32; levels t = 0 .. log2 HW.
+template <typename R, bool FOLD, int LAM, int HW, int ST>
+__device__ __forceinline__ void special_class_l(R* ch, int lane) {
+  static_assert(HW == 8 || HW == 16 || HW == 32, "special class size");
+  constexpr int NC = 2 * HW;
+  constexpr int TMAX = HW == 32 ? 5 : (HW == 16 ? 4 : 3);
+  const bool has = lane <= NC;
+  R a = has ? ch[ST * lane] : R(0);
+  R b = HW == 32 ? ch[ST * (64 - lane)] : R(0);
+  R m = HW >= 16 ? ch[ST * 32] : R(0);             // used by lane 0 only
+  const bool own0 = !(LAM && lane == 0);           // Dst chains: no cell 0 / 2 HW
   auto level = [&](int t) {
     R e2, o2;
     if (t == 5) {                                  // in-lane pairs (i, 64 - i)
@@ -476,22 +482,74 @@ __device__ __forceinline__ void special_class64_l(R* ch, int lane) {
   };
   if (FOLD) {
 #pragma unroll
-    for (int t = 5; t >= 0; --t) level(t);
+    for (int t = TMAX; t >= 0; --t) level(t);
   } else {
 #pragma unroll
-    for (int t = 0; t <= 5; ++t) level(t);
+    for (int t = 0; t <= TMAX; ++t) level(t);
   }
-  if (own0) {
-    ch[33 * lane] = a;
-    ch[33 * (64 - lane)] = b;
-  }
-  if (lane == 0 && !LAM) ch[33 * 32] = m;
+  if (own0 && has) ch[ST * lane] = a;
+  if (HW == 32 && own0) ch[ST * (64 - lane)] = b;
+  if (HW >= 16 && lane == 0 && !LAM) ch[ST * 32] = m;
 }
 
-template <typename R, bool FOLD>
-__device__ __forceinline__ void special_class64(R* ch, int lam, int lane) {
-  if (lam) special_class64_l<R, FOLD, 1>(ch, lane);   // warp-uniform
-  else special_class64_l<R, FOLD, 0>(ch, lane);
+template <typename R, bool FOLD, int HW, int ST>
+__device__ __forceinline__ void special_class(R* ch, int lam, int lane) {
+  if (lam) special_class_l<R, FOLD, 1, HW, ST>(ch, lane);   // warp-uniform
+  else special_class_l<R, FOLD, 0, HW, ST>(ch, lane);
+}
+
+// Recombination (TM, FOLD = false) / fold (HM, FOLD = true) of all four
+// chains on buffer B for n = 2N/LB .. N: generated thread sets {j WR +- k}
+// (WR = max(64, N/LB)) for n >= 2 WR, the levels below 2 WR level by level;
+// the k = 0 class (multiples of WR/2) cooperatively, one warp per chain.
+// Every thread of the row calls it (it contains the row barriers).
+template <class C, typename R, bool FOLD, class Sync>
+__device__ __forceinline__ void recombine(R* B, int tid, bool act, Sync row_sync) {
+  using A = Arith<R>;
+  constexpr int N = C::N, H = C::H;
+  constexpr int WR = (N / C::LB > 64) ? N / C::LB : 64;
+  constexpr int HWR = H / WR;
+  constexpr int ST = WR / 2 + WR / 64;
+  constexpr int n0 = 2 * (N / C::LB);
+  constexpr int GT = 2 * WR;                       // generated-set threads (4 chains x WR/2)
+  auto pre = [&]() {
+    if constexpr (!FOLD) {
+#pragma unroll 1
+      for (int n = n0; n < 2 * WR; n <<= 1) {
+        if (act) chain_level<C, R, false>(B, n, tid);
+        row_sync();
+      }
+    }
+  };
+  auto post = [&]() {
+    if constexpr (FOLD) {
+#pragma unroll 1
+      for (int n = WR; n >= n0; n >>= 1) {
+        row_sync();
+        if (act) chain_level<C, R, true>(B, n, tid);
+      }
+    }
+  };
+  pre();
+  if (act) {
+    if (tid < GT) {
+      const int c = tid / (WR / 2), k = tid % (WR / 2);
+      if (k) {
+        if constexpr (FOLD) Recomb<WR, HWR>::template fold<R, A>(c & 1, B + C::co_sw(c), k);
+        else Recomb<WR, HWR>::template run<R, A>(c & 1, B + C::co_sw(c), k);
+      }
+    } else if (GT == 128 && tid < 256) {
+      const int c = (tid >> 5) - 4;
+      special_class<R, FOLD, HWR, ST>(B + C::co_sw(c), c & 1, tid & 31);
+    } else if (GT == 256 && tid >= 256 && tid < C::NT) {
+      // spare warps 8.. take the four chains' k = 0 classes in turn
+      constexpr int NW = (C::NT - 256) / 32;
+#pragma unroll 1
+      for (int c = (tid - 256) >> 5; c < 4; c += NW)
+        special_class<R, FOLD, HWR, ST>(B + C::co_sw(c), c & 1, tid & 31);
+    }
+  }
+  post();
 }
 
 // ---- TMA bulk staging of the next row (cp.async.bulk + mbarrier).
@@ -708,24 +766,9 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
         if (v > 0) Top<C::LB, C::LT, LOGN, C::SINE>::template fwd<R, A>(c & 1, Tb + C::coT(c), v, ltab, base);
       }
     } else {
-      if constexpr (N / C::LB == 64) {
-        // generated: each thread owns the 64 cells j*64 +- k of its chain
-        // warps 0-3: the 64 cells j*64 +- k of k = lane (lane 0 idle);
-        // warps 4-7: the multiples of 32 of chain warp-4, cooperatively
-        if (!act) {
-        } else if (tid < 128) {
-          if (tid & 31) Recomb<64, H / 64>::template fold<R, A>((tid >> 5) & 1, Tb + C::coT(tid >> 5), tid & 31);
-        } else if (tid < 256) {
-          special_class64<R, true>(Tb + C::coT((tid >> 5) - 4), (tid >> 5) & 1, tid & 31);
-        }
-        row_sync();
-      } else {
-#pragma unroll 1
-        for (int n = N; n >= 2 * (N / C::LB); n >>= 1) {
-          if (act) chain_level<C, R, true>(Tb, n, tid);
-          row_sync();
-        }
-      }
+      // chain folds n = N .. 2N/LB (generated sets, cooperative k = 0 class)
+      recombine<C, R, true>(Tb, tid, act, row_sync);
+      row_sync();
       // serial recurrences: fp64 in the reference order (bitwise), fp32 as warp scans
       if constexpr (C::CHAIN && sizeof(R) == 8) am_levels_asc<C, R, C::LT>(Tb, tid);   // RPC = 1
       else if (act) am_phase_regs<C, R, false>(Tb, tid);
@@ -739,39 +782,53 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
     row_sync();
     PHASE_MARK(2);
 
-    // ---- bottom: T -> F (generated).  One thread per LB-segment runs both
-    // class groups (class 0, then classes 1..; trailing-zero classes never
-    // mix) with one code path per lam (odd segments stored reversed).
+    // ---- bottom: T -> F (generated).  Segment code depends only on lam
+    // (odd segments stored reversed, Cfg::ipos).  N >= 4096: one thread per
+    // LB-segment runs all classes (loads hoisted).  N <= 2048 (few
+    // segments): warp w of warps 0-3 runs class group (w/2: class 0 |
+    // classes 1..) of the lam = w%2 segments, one per lane.
+    constexpr bool SPLIT = C::NSEG <= 64;
+    constexpr int BT = SPLIT ? 128 : C::NSEG;        // bottom threads
     if (!act) {
-    } else if (tid < C::NSEG) {
-      const int half = C::HP / 2;
-      const int h = tid % half;
-      const int rest = tid / half;
-      const int part = rest & 1, rho_bit = (rest >> 1) & 1, lam_bit = (rest >> 2) & 1;
-      const int c = part * 2 + lam_bit;
-      const int s = 2 * h + rho_bit;
-      int rho, lens, r;
-      seg_params<C::SINE>(lam_bit, s, C::LT, &rho, &lens, &r);
-      rho = 0;   // odd segments are stored reversed (Cfg::ipos)
-#if AMQFT_BOTTOM_HOIST
-      // all classes in one function, every T load hoisted above the F stores
-      Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, 2>(rho, lens, Tb + C::coT(c), Fb + C::coF(c),
-                                                            s * C::LB, tab, nmax, base, N, r, lam_bit);
-#else
-      Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, 0>(rho, lens, Tb + C::coT(c), Fb + C::coF(c),
-                                                            s * C::LB, tab, nmax, base, N, r, lam_bit);
-      Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, 1>(rho, lens, Tb + C::coT(c), Fb + C::coF(c),
-                                                            s * C::LB, tab, nmax, base, N, r, lam_bit);
-#endif
+    } else if (tid < BT) {
+      if constexpr (SPLIT) {
+        const int w = tid >> 5, g = tid & 31;
+        const int lam_bit = w & 1;
+        if (g < 2 * C::HP) {
+          const int c = lam_bit + 2 * (g / C::HP), sg = g % C::HP;
+          int rho, lens, r;
+          seg_params<C::SINE>(lam_bit, sg, C::LT, &rho, &lens, &r);
+          if (w >> 1)
+            Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, 1>(0, lens, Tb + C::coT(c), Fb + C::coF(c),
+                                                                  sg * C::LB, tab, nmax, base, N, r, lam_bit);
+          else
+            Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, 0>(0, lens, Tb + C::coT(c), Fb + C::coF(c),
+                                                                  sg * C::LB, tab, nmax, base, N, r, lam_bit);
+        }
+      } else {
+        const int half = C::HP / 2;
+        const int h = tid % half;
+        const int rest = tid / half;
+        const int part = rest & 1, rho_bit = (rest >> 1) & 1, lam_bit = (rest >> 2) & 1;
+        const int c = part * 2 + lam_bit;
+        const int sg = 2 * h + rho_bit;
+        int rho, lens, r;
+        seg_params<C::SINE>(lam_bit, sg, C::LT, &rho, &lens, &r);
+        // all classes in one function, every T load hoisted above the F stores
+        Bottom<V, C::LB>::template run<R, A, LOGLB, C::LT, 2>(0, lens, Tb + C::coT(c), Fb + C::coF(c),
+                                                              sg * C::LB, tab, nmax, base, N, r, lam_bit);
+      }
     } else {
       // the small chains (cells at multiples of LB; disjoint from the
-      // segments' cells in T and F), one lane per chain, one warp each
-      // where the block has spare warps
-      constexpr int SPARE = C::NT - C::NSEG;
+      // segments' cells in T and F), one lane per chain, on the first lane
+      // of four warps past the bottom threads where the block has them
+      constexpr int SPARE = C::NT - BT;
       constexpr int STR = SPARE / 4 >= 32 ? 32 : SPARE / 4;
-      const int l = tid - C::NSEG;
-      if (l % STR == 0 && l / STR < 4) {
-        const int cc = l / STR;
+      const int l = tid - BT;
+      // SPARE = 64: two warps, chains (0, 2) on the first and (1, 3) on the
+      // second (one code path per warp); otherwise one lane per warp
+      const int cc = SPARE == 64 ? ((l >> 5) | (((l & 31) >> 4) << 1)) : l / STR;
+      if ((SPARE == 64 ? (l & 15) == 0 : l % STR == 0) && cc < 4) {
         SmallFull<V, C::HP, LOGN>::template run<R, A, LOGLB, C::LB>(cc & 1, Tb + C::coT(cc), Fb + C::coF(cc),
                                                                      tab, base);
       }
@@ -788,24 +845,10 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       WORK_MARK(3);
       row_sync();
       PHASE_MARK(4);
-      if constexpr (N / C::LB == 64) {
-        // generated: each thread owns the 64 cells j*64 +- k of its chain
-        // as the fold: warps 0-3 the k = lane sets, warps 4-7 the multiples of 32
-        if (!act) {
-        } else if (tid < 128) {
-          if (tid & 31) Recomb<64, H / 64>::template run<R, A>((tid >> 5) & 1, Fb + C::coF(tid >> 5), tid & 31);
-        } else if (tid < 256) {
-          special_class64<R, false>(Fb + C::coF((tid >> 5) - 4), (tid >> 5) & 1, tid & 31);
-        }
-        WORK_MARK(4);
-        row_sync();
-      } else {
-#pragma unroll 1
-        for (int n = 2 * (N / C::LB); n <= N; n <<= 1) {
-          if (act) chain_level<C, R, false>(Fb, n, tid);
-          row_sync();
-        }
-      }
+      // chain recombination n = 2N/LB .. N (generated sets, cooperative k = 0 class)
+      recombine<C, R, false>(Fb, tid, act, row_sync);
+      WORK_MARK(4);
+      row_sync();
     } else {
       if (act && tid < 4 * C::LB) {
         const int c = tid >> LOGLB, v = tid & (C::LB - 1);

@@ -202,15 +202,16 @@ def emulate(v, N, LB, x, tab, base):
             for vv in range(1, LB):
                 assert L.host_top(LB, LT, LOGN, SINE, 0, c & 1, Tp + 8 * c * CS, vv, ltp, base) == 0
     else:
-        if N // LB == 64:
-            for c in range(4):
-                for k in range(32):
-                    assert L.host_fold(64, H // 64, c & 1, Tp + 8 * c * CS, k) == 0
-        else:
-            n = N
-            while n >= 2 * (N // LB):
-                _chain_level(T, CS, n, True)
-                n >>= 1
+        # generated folds on the sets {j W +- k} for n = N .. 2W, then the
+        # levels below 2W (down to 2N/LB) level by level (fast_kernel.cuh)
+        W = max(64, N // LB)
+        for c in range(4):
+            for k in range(W // 2):
+                assert L.host_fold(W, H // W, c & 1, Tp + 8 * c * CS, k) == 0
+        n = W
+        while n >= 2 * (N // LB):
+            _chain_level(T, CS, n, True)
+            n >>= 1
         if v in (3, 7):
             for depth in range(LT):
                 _am_level(T, CS, N, LOGLB, depth, v, SINE, False)
@@ -247,15 +248,14 @@ def emulate(v, N, LB, x, tab, base):
                 _am_level(F, CS, N, LOGLB, depth, v, SINE, True)
         else:
             am_phase_regs(F, CS, N, LOGLB, LT, v, SINE, True)
-        if N // LB == 64:
-            for c in range(4):
-                for k in range(32):
-                    assert L.host_recomb(64, H // 64, c & 1, Fp + 8 * c * CS, k) == 0
-        else:
-            n = 2 * (N // LB)
-            while n <= N:
-                _chain_level(F, CS, n, False)
-                n <<= 1
+        W = max(64, N // LB)
+        n = 2 * (N // LB)
+        while n < 2 * W:
+            _chain_level(F, CS, n, False)
+            n <<= 1
+        for c in range(4):
+            for k in range(W // 2):
+                assert L.host_recomb(W, H // W, c & 1, Fp + 8 * c * CS, k) == 0
     else:
         for c in range(4):
             for vv in range(1, LB):

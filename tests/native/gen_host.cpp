@@ -151,13 +151,18 @@ int host_smallpar(int V, int HP, int nlog, int LB, int lam, int cls, const doubl
   return -1;
 }
 
+#define RECOMB_SIZES(X) X(64, 8) X(64, 16) X(64, 32) X(128, 32)
 int host_recomb(int W, int HW, int lam, double* F, int k) {
-  if (W == 64 && HW == 32) { Recomb<64, 32>::run<double, HA>(lam, F, k); return 0; }
+#define X(w, hw) if (W == w && HW == hw) { Recomb<w, hw>::run<double, HA>(lam, F, k); return 0; }
+  RECOMB_SIZES(X)
+#undef X
   return -1;
 }
 
 int host_fold(int W, int HW, int lam, double* F, int k) {
-  if (W == 64 && HW == 32) { Recomb<64, 32>::fold<double, HA>(lam, F, k); return 0; }
+#define X(w, hw) if (W == w && HW == hw) { Recomb<w, hw>::fold<double, HA>(lam, F, k); return 0; }
+  RECOMB_SIZES(X)
+#undef X
   return -1;
 }
 

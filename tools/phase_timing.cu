@@ -11,11 +11,11 @@
 
 using namespace amqft_b200::fastk;
 
-template <int V>
+template <int V, int LOGN>
 static int run_v(const float* in, float* out, size_t rows, const float* tab, int nmax,
                  unsigned long long* cyc, int grid) {
-  using C = Cfg<V, float, 12, 6>;
-  auto fn = k_fast<V, float, 12, 6, false>;
+  using C = Cfg<V, float, LOGN, 6>;
+  auto fn = k_fast<V, float, LOGN, 6, false>;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BLOCK);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, C::NTB, C::SMEM_BLOCK);
@@ -27,7 +27,7 @@ static int run_v(const float* in, float* out, size_t rows, const float* tab, int
   float* ltab = nullptr;
   cudaMalloc(&ltab, sizeof(float) * C::H);
   k_level_table<float><<<8, 256>>>(tab, ltab, C::H, C::LT, nmax);
-  fn<<<grid, C::NTB, C::SMEM_BLOCK>>>(in, out, rows, tab, ltab, nmax, 1.0f / 4096);
+  fn<<<grid, C::NTB, C::SMEM_BLOCK>>>(in, out, rows, tab, ltab, nmax, 1.0f / C::N);
   cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(cyc, g_phase_cycles, sizeof(z));
   cudaFree(ltab);
@@ -45,10 +45,17 @@ static int run_v(const float* in, float* out, size_t rows, const float* tab, int
 
 extern "C" int pt_run(int v, const float* in, float* out, size_t rows, const float* tab,
                       int nmax, unsigned long long* cyc, int grid) {
-  switch (v) {
-    case 1: return run_v<1>(in, out, rows, tab, nmax, cyc, grid);
-    case 2: return run_v<2>(in, out, rows, tab, nmax, cyc, grid);
-    case 4: return run_v<4>(in, out, rows, tab, nmax, cyc, grid);
+  // nmax is the transform size (table built for Nmax = N)
+  switch (v * 100 + nmax / 1024) {
+    case 101: return run_v<1, 10>(in, out, rows, tab, nmax, cyc, grid);
+    case 104: return run_v<1, 12>(in, out, rows, tab, nmax, cyc, grid);
+    case 201: return run_v<2, 10>(in, out, rows, tab, nmax, cyc, grid);
+    case 202: return run_v<2, 11>(in, out, rows, tab, nmax, cyc, grid);
+    case 204: return run_v<2, 12>(in, out, rows, tab, nmax, cyc, grid);
+    case 401: return run_v<4, 10>(in, out, rows, tab, nmax, cyc, grid);
+    case 402: return run_v<4, 11>(in, out, rows, tab, nmax, cyc, grid);
+    case 404: return run_v<4, 12>(in, out, rows, tab, nmax, cyc, grid);
+    case 408: return run_v<4, 13>(in, out, rows, tab, nmax, cyc, grid);
   }
   return -1;
 }

@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 lib = C.CDLL(os.path.join(HERE, os.environ.get("PT_LIB", "libphase_timing.so")))
 lib.pt_run.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_int,
                        C.c_void_p, C.c_int]
-N = 4096
+N = int(os.environ.get("PT_N", "4096"))
 names = ["load", "top||small / chainfold+AM_F", "bottom", "AM_B levels", "chain recomb / top bwd",
          "store"]
 for v in [int(a) for a in sys.argv[1:]] or [4]:
@@ -20,7 +20,7 @@ for v in [int(a) for a in sys.argv[1:]] or [4]:
     f = {0: 2 * np.cos(ang), 2: 1 / (2 * np.cos(ang))}[kind]
     tab = np.concatenate([f.astype(np.float64), [np.cos(np.longdouble(np.pi) / 4)]]).astype(np.float32)
     dtab = torch.tensor(tab, device="cuda")
-    rows = 65536
+    rows = 65536 * 4096 // N
     x = torch.randn(rows, 2 * N, device="cuda")
     y = torch.empty_like(x)
     cyc = (C.c_ulonglong * 16)()
