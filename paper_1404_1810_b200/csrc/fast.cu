@@ -5,36 +5,44 @@
 
 namespace amqft_b200 {
 namespace fastk {
+// instances: fast_v<V>.cu (CDFT rows), fast_rv<V>.cu (RDFT rows)
+template <int V, typename R, bool RD>
+std::unique_ptr<FastPlan> make_sized(size_t n, const void* tab, uint32_t nmax, int dev);
+
 template <int V, typename R>
-std::unique_ptr<FastPlan> make_for_variant(size_t n, const void* tab, uint32_t nmax, int dev);
+std::unique_ptr<FastPlan> make_for_variant(int kind, size_t n, const void* tab, uint32_t nmax, int dev) {
+  return kind == 1 ? make_sized<V, R, true>(n, tab, nmax, dev) : make_sized<V, R, false>(n, tab, nmax, dev);
+}
 }  // namespace fastk
 
+// kind 0: CDFT rows; 1: RDFT rows
 template <typename R>
-std::unique_ptr<FastPlan> make_fast_typed(int v, size_t n, const void* tab, uint32_t nmax, int dev) {
+std::unique_ptr<FastPlan> make_fast_typed(int v, int kind, size_t n, const void* tab, uint32_t nmax, int dev) {
   using namespace fastk;
   switch (v) {
-    case 1: return make_for_variant<1, R>(n, tab, nmax, dev);
-    case 2: return make_for_variant<2, R>(n, tab, nmax, dev);
-    case 3: return make_for_variant<3, R>(n, tab, nmax, dev);
-    case 4: return make_for_variant<4, R>(n, tab, nmax, dev);
-    case 5: return make_for_variant<5, R>(n, tab, nmax, dev);
-    case 6: return make_for_variant<6, R>(n, tab, nmax, dev);
-    case 7: return make_for_variant<7, R>(n, tab, nmax, dev);
-    case 8: return make_for_variant<8, R>(n, tab, nmax, dev);
+    case 1: return make_for_variant<1, R>(kind, n, tab, nmax, dev);
+    case 2: return make_for_variant<2, R>(kind, n, tab, nmax, dev);
+    case 3: return make_for_variant<3, R>(kind, n, tab, nmax, dev);
+    case 4: return make_for_variant<4, R>(kind, n, tab, nmax, dev);
+    case 5: return make_for_variant<5, R>(kind, n, tab, nmax, dev);
+    case 6: return make_for_variant<6, R>(kind, n, tab, nmax, dev);
+    case 7: return make_for_variant<7, R>(kind, n, tab, nmax, dev);
+    case 8: return make_for_variant<8, R>(kind, n, tab, nmax, dev);
   }
   return nullptr;
 }
 
 std::unique_ptr<FastPlan> make_fast_typed_f32(int variant, size_t n, const void* tab, uint32_t nmax, int dev) {
-  return make_fast_typed<float>(variant, n, tab, nmax, dev);
+  return make_fast_typed<float>(variant, 0, n, tab, nmax, dev);
 }
 
 std::unique_ptr<FastPlan> make_fast_plan(const amqft_plan_desc& d, const void* d_trig,
                                          uint32_t nmax) {
-  if (d.function != AMQFT_FN_CDFT) return nullptr;
+  if (d.function != AMQFT_FN_CDFT && d.function != AMQFT_FN_RDFT) return nullptr;
   if (d.trig_mode != AMQFT_TRIG_TABLE) return nullptr;
-  if (d.dtype == AMQFT_F32) return make_fast_typed<float>(d.variant, d.n, d_trig, nmax, d.device);
-  return make_fast_typed<double>(d.variant, d.n, d_trig, nmax, d.device);
+  const int kind = d.function == AMQFT_FN_RDFT ? 1 : 0;
+  if (d.dtype == AMQFT_F32) return make_fast_typed<float>(d.variant, kind, d.n, d_trig, nmax, d.device);
+  return make_fast_typed<double>(d.variant, kind, d.n, d_trig, nmax, d.device);
 }
 
 OpCount fast_op_counts(const amqft_plan_desc& d) {
@@ -47,6 +55,12 @@ OpCount fast_op_counts(const amqft_plan_desc& d) {
   c.adds = 3 * n * lg - 3 * n + 4;
   c.muls = n * lg - 3 * n + 4;
   c.bt = (d.variant % 2 == 1) ? n - 4 * lg + 4 : 0;
+  if (d.function == AMQFT_FN_RDFT) {
+    // CDFT = SplitComplex bwd (2N - 4 adds, elaborations_test.cpp:91-92) + 2 RDFT
+    c.adds = (c.adds - (2 * n - 4)) / 2;
+    c.muls /= 2;
+    c.bt /= 2;
+  }
   return c;
 }
 

@@ -618,7 +618,10 @@ __device__ unsigned long long g_warp_work[16][16];
 #define WORK_MARK(k) do {} while (0)
 #endif
 
-template <int V, typename R, int LOGN, int LOGLB, bool INV>
+// MODE 0: CDFT forward; 1: CDFT inverse (swap trick); 2: RDFT forward, two
+// real rows per kernel row (row A -> chains 0/1, row B -> chains 2/3: the
+// same Dct/Dst chains as the Re/Im halves of a CDFT, variants.cpp:190-209).
+template <int V, typename R, int LOGN, int LOGLB, int MODE>
 #ifndef AMQFT_FAST_MINB
 #define AMQFT_FAST_MINB 2
 #endif
@@ -633,8 +636,12 @@ __global__ void __launch_bounds__(
                                   ((Cfg<V, R, LOGN, LOGLB>::RPC == 1 && sizeof(R) == 4 &&
                                     2 * Cfg<V, R, LOGN, LOGLB>::SMEM_BLOCK <= 227 * 1024)
                                        ? AMQFT_FAST_MINB : 1))
-k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
+k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows_in,
        const R* __restrict__ tab, const R* __restrict__ ltab, int nmax, R scale) {
+  constexpr bool INV = MODE == 1;
+  constexpr bool RDFT = MODE == 2;
+  // kernel rows: CDFT rows, or pairs of RDFT rows (the last one maybe single)
+  const size_t rows = RDFT ? (rows_in + 1) / 2 : rows_in;
 #ifdef AMQFT_PHASE_TIMING
   long long t_prev = 0, w_start = 0;
 #endif
@@ -681,8 +688,12 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
     fence_mbar_init();
   }
   row_sync();
+  // bytes of kernel row kr (an odd RDFT batch ends with a single real row)
+  auto row_bytes = [&](size_t kr) -> uint32_t {
+    return (RDFT && 2 * kr + 1 >= rows_in) ? ROW_BYTES / 2 : ROW_BYTES;
+  };
   if (tid == 0 && blockIdx.x * RSTEP + slot < rows)
-    tma_load_1d(Sb, in + (blockIdx.x * RSTEP + slot) * 2 * N, ROW_BYTES, bar);
+    tma_load_1d(Sb, in + (blockIdx.x * RSTEP + slot) * 2 * N, row_bytes(blockIdx.x * RSTEP + slot), bar);
   uint32_t parity = 0;
 #else
   (void)Sb;
@@ -718,12 +729,21 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       R* t3 = Tb + C::coT(3) + q1;
       // all staged reads first (the compiler cannot hoist them over the
       // T stores itself: both are shared memory), then the stores
+      // RDFT: rows A and B (N reals each) take the places of re and im
+      const R* xa = reinterpret_cast<const R*>(x);
+      const R* xb = xa + N;
       V2 av[IO_IT], bv[IO_IT];
 #pragma unroll
       for (int it = 0; it < IO_IT; ++it) {
         const int m = tid + it * IO_T;
-        av[it] = x[m];
-        bv[it] = x[(N - m) & (N - 1)];   // m = 0: in range, unused
+        const int mm = (N - m) & (N - 1);   // m = 0: in range, unused
+        if constexpr (RDFT) {
+          av[it] = V2{xa[m], xb[m]};
+          bv[it] = V2{xa[mm], xb[mm]};
+        } else {
+          av[it] = x[m];
+          bv[it] = x[mm];
+        }
       }
 #pragma unroll
       for (int it = 0; it < IO_IT; ++it) {
@@ -743,7 +763,7 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
         t3[it * PT_STEP] = A::sub(a.y, b.y);
       }
       if (tid == 0) {                // m = H
-        V2 a = x[H];
+        V2 a = RDFT ? V2{xa[H], xb[H]} : x[H];
         if (INV) a = V2{a.y, a.x};
         Tb[C::coT(0) + C::pt(H, 0)] = a.x;
         Tb[C::coT(2) + C::pt(H, 0)] = a.y;
@@ -754,7 +774,7 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
 #if AMQFT_TMA_STAGE
     if (tid == 0 && row + gridDim.x * RSTEP < rows) {
       fence_proxy_async();
-      tma_load_1d(Sb, in + (row + gridDim.x * RSTEP) * 2 * N, ROW_BYTES, bar);
+      tma_load_1d(Sb, in + (row + gridDim.x * RSTEP) * 2 * N, row_bytes(row + gridDim.x * RSTEP), bar);
     }
 #endif
     PHASE_MARK(1);
@@ -875,8 +895,13 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
         for (int it = 0; it < IO_IT; ++it) {
           const R rd = f0[it * PF_STEP], id = f2[it * PF_STEP];
           const R rs = f1[it * PF_STEP], is = f3[it * PF_STEP];   // k = 0: unused
-          lo[it] = V2{A::add(rd, is), A::sub(id, rs)};
-          hi[it] = V2{A::sub(rd, is), A::add(id, rs)};
+          if constexpr (RDFT) {      // SplitReal bwd: copies (Dct k, Dst N-k)
+            lo[it] = V2{rd, id};
+            hi[it] = V2{rs, is};
+          } else {
+            lo[it] = V2{A::add(rd, is), A::sub(id, rs)};
+            hi[it] = V2{A::sub(rd, is), A::add(id, rs)};
+          }
           if (it == 0 && tid == 0) lo[0] = V2{rd, id};            // k = 0: Dct chains only
           if (INV) {
             lo[it] = V2{A::mul(lo[it].y, scale), A::mul(lo[it].x, scale)};
@@ -890,51 +915,96 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       }
       row_sync();
       if (act && tid < IO_T) {
-        V2* ob = reinterpret_cast<V2*>(Fb);
+        if constexpr (RDFT) {        // rows A | B, N reals each
+          R* oa = Fb;
+          R* ob = Fb + N;
 #pragma unroll
-        for (int it = 0; it < IO_IT; ++it) {
-          const int k = tid + it * IO_T;
-          ob[k] = lo[it];
-          if (!(it == 0 && tid == 0)) ob[N - k] = hi[it];
+          for (int it = 0; it < IO_IT; ++it) {
+            const int k = tid + it * IO_T;
+            oa[k] = lo[it].x;
+            ob[k] = lo[it].y;
+            if (!(it == 0 && tid == 0)) {
+              oa[N - k] = hi[it].x;
+              ob[N - k] = hi[it].y;
+            }
+          }
+          if (tid == 0) {
+            oa[H] = yH.x;
+            ob[H] = yH.y;
+          }
+        } else {
+          V2* ob = reinterpret_cast<V2*>(Fb);
+#pragma unroll
+          for (int it = 0; it < IO_IT; ++it) {
+            const int k = tid + it * IO_T;
+            ob[k] = lo[it];
+            if (!(it == 0 && tid == 0)) ob[N - k] = hi[it];
+          }
+          if (tid == 0) ob[H] = yH;
         }
-        if (tid == 0) ob[H] = yH;
         fence_proxy_async();         // generic-proxy writes -> async proxy
       }
       row_sync();
-      if (act && tid == 0) bulk_store(y, Fb, ROW_BYTES);
+      if (act && tid == 0) bulk_store(y, Fb, row_bytes(row));
     } else {
       // Cells k = tid + 256 it and k = H (thread 0), immediate offsets as in
       // the load.  INV: re/im exchanged and scaled by 1/N on the way out.
-      if (act && tid < IO_T) {
-        const int q0 = C::pf(tid, 0), q1 = C::pf(tid, 1);
-        const R* f0 = Fb + C::coF(0) + q0;
-        const R* f1 = Fb + C::coF(1) + q1;
-        const R* f2 = Fb + C::coF(2) + q0;
-        const R* f3 = Fb + C::coF(3) + q1;
+      if constexpr (RDFT) {
+        if (act && tid < IO_T) {
+          const bool two = 2 * row + 1 < rows_in;
+          R* ya = out + row * 2 * N;
+          R* yb = ya + N;
+          const int q0 = C::pf(tid, 0), q1 = C::pf(tid, 1);
+          const R* f0 = Fb + C::coF(0) + q0;
+          const R* f1 = Fb + C::coF(1) + q1;
+          const R* f2 = Fb + C::coF(2) + q0;
+          const R* f3 = Fb + C::coF(3) + q1;
 #pragma unroll
-        for (int it = 0; it < IO_IT; ++it) {
-          const int k = tid + it * IO_T;
-          const R rd = f0[it * PF_STEP], id = f2[it * PF_STEP];
-          if (it == 0 && tid == 0) {   // k = 0: Dct chains only
-            y[0] = INV ? V2{A::mul(id, scale), A::mul(rd, scale)} : V2{rd, id};
-            continue;
+          for (int it = 0; it < IO_IT; ++it) {
+            const int k = tid + it * IO_T;
+            ya[k] = f0[it * PF_STEP];
+            if (two) yb[k] = f2[it * PF_STEP];
+            if (it == 0 && tid == 0) continue;
+            ya[N - k] = f1[it * PF_STEP];
+            if (two) yb[N - k] = f3[it * PF_STEP];
           }
-          const R rs = f1[it * PF_STEP], is = f3[it * PF_STEP];
-          V2 lo{A::add(rd, is), A::sub(id, rs)};
-          V2 hi{A::sub(rd, is), A::add(id, rs)};
-          if (INV) {
-            lo = V2{A::mul(lo.y, scale), A::mul(lo.x, scale)};
-            hi = V2{A::mul(hi.y, scale), A::mul(hi.x, scale)};
+          if (tid == 0) {
+            ya[H] = Fb[C::coF(0) + C::pf(H, 0)];
+            if (two) yb[H] = Fb[C::coF(2) + C::pf(H, 0)];
           }
-          y[k] = lo;
-          y[N - k] = hi;
         }
-        if (tid == 0) {                // k = H
-          const R rd = Fb[C::coF(0) + C::pf(H, 0)], id = Fb[C::coF(2) + C::pf(H, 0)];
-          y[H] = INV ? V2{A::mul(id, scale), A::mul(rd, scale)} : V2{rd, id};
+      } else {
+      if (act && tid < IO_T) {
+          const int q0 = C::pf(tid, 0), q1 = C::pf(tid, 1);
+          const R* f0 = Fb + C::coF(0) + q0;
+          const R* f1 = Fb + C::coF(1) + q1;
+          const R* f2 = Fb + C::coF(2) + q0;
+          const R* f3 = Fb + C::coF(3) + q1;
+  #pragma unroll
+          for (int it = 0; it < IO_IT; ++it) {
+            const int k = tid + it * IO_T;
+            const R rd = f0[it * PF_STEP], id = f2[it * PF_STEP];
+            if (it == 0 && tid == 0) {   // k = 0: Dct chains only
+              y[0] = INV ? V2{A::mul(id, scale), A::mul(rd, scale)} : V2{rd, id};
+              continue;
+            }
+            const R rs = f1[it * PF_STEP], is = f3[it * PF_STEP];
+            V2 lo{A::add(rd, is), A::sub(id, rs)};
+            V2 hi{A::sub(rd, is), A::add(id, rs)};
+            if (INV) {
+              lo = V2{A::mul(lo.y, scale), A::mul(lo.x, scale)};
+              hi = V2{A::mul(hi.y, scale), A::mul(hi.x, scale)};
+            }
+            y[k] = lo;
+            y[N - k] = hi;
+          }
+          if (tid == 0) {                // k = H
+            const R rd = Fb[C::coF(0) + C::pf(H, 0)], id = Fb[C::coF(2) + C::pf(H, 0)];
+            y[H] = INV ? V2{A::mul(id, scale), A::mul(rd, scale)} : V2{rd, id};
+          }
         }
       }
-    }
+      }
     WORK_MARK(5);
     // No barrier here: the next row's load writes only T (and the staging
     // buffer through TMA), whose last readers are behind earlier barriers;
@@ -973,7 +1043,7 @@ __global__ void k_compact_table(const R* __restrict__ tab, R* __restrict__ out, 
     out[s] = tab[(s + 1) * ratio - 1];
 }
 
-template <int V, typename R, int LOGN, int LOGLB>
+template <int V, typename R, int LOGN, int LOGLB, bool RDFT_ROWS>
 class FastPlanImpl final : public FastPlan {
  public:
   FastPlanImpl(const void* tab, uint32_t nmax, int device) : tab_(static_cast<const R*>(tab)),
@@ -986,8 +1056,9 @@ class FastPlanImpl final : public FastPlan {
       tab_ = own_tab_;
       nmax_ = C::N;
     }
-    auto fn = k_fast<V, R, LOGN, LOGLB, false>;
-    auto fi = k_fast<V, R, LOGN, LOGLB, true>;
+    // CDFT plans: forward (MODE 0) and inverse (1); RDFT plans: MODE 2
+    auto fn = k_fast<V, R, LOGN, LOGLB, RDFT_ROWS ? 2 : 0>;
+    auto fi = k_fast<V, R, LOGN, LOGLB, RDFT_ROWS ? 2 : 1>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(C::SMEM_BLOCK));
     if (e == cudaSuccess)
@@ -1012,14 +1083,18 @@ class FastPlanImpl final : public FastPlan {
   }
   void exec(const void* in, void* out, size_t rows, int inverse, cudaStream_t st) override {
     using C = Cfg<V, R, LOGN, LOGLB>;
-    const size_t units = (rows + C::RPC - 1) / C::RPC;
+    const size_t krows = RDFT_ROWS ? (rows + 1) / 2 : rows;   // kernel rows
+    const size_t units = (krows + C::RPC - 1) / C::RPC;
     const unsigned grid = static_cast<unsigned>(std::min<size_t>(units, static_cast<size_t>(grid_cap_)));
-    if (inverse)
-      k_fast<V, R, LOGN, LOGLB, true><<<grid, C::NTB, C::SMEM_BLOCK, st>>>(
+    if (RDFT_ROWS)
+      k_fast<V, R, LOGN, LOGLB, 2><<<grid, C::NTB, C::SMEM_BLOCK, st>>>(
+          static_cast<const R*>(in), static_cast<R*>(out), rows, tab_, ltab_, static_cast<int>(nmax_), R(1));
+    else if (inverse)
+      k_fast<V, R, LOGN, LOGLB, 1><<<grid, C::NTB, C::SMEM_BLOCK, st>>>(
           static_cast<const R*>(in), static_cast<R*>(out), rows, tab_, ltab_, static_cast<int>(nmax_),
           R(1) / R(C::N));
     else
-      k_fast<V, R, LOGN, LOGLB, false><<<grid, C::NTB, C::SMEM_BLOCK, st>>>(
+      k_fast<V, R, LOGN, LOGLB, 0><<<grid, C::NTB, C::SMEM_BLOCK, st>>>(
           static_cast<const R*>(in), static_cast<R*>(out), rows, tab_, ltab_, static_cast<int>(nmax_),
           R(1) / R(C::N));
     const cudaError_t e = cudaGetLastError();
@@ -1034,14 +1109,14 @@ class FastPlanImpl final : public FastPlan {
   int grid_cap_ = 148;
 };
 
-template <int V, typename R>
-std::unique_ptr<FastPlan> make_for_variant(size_t n, const void* tab, uint32_t nmax, int dev) {
+template <int V, typename R, bool RD>
+std::unique_ptr<FastPlan> make_sized(size_t n, const void* tab, uint32_t nmax, int dev) {
   switch (n) {
-    case 1024: return std::make_unique<FastPlanImpl<V, R, 10, 6>>(tab, nmax, dev);
-    case 2048: return std::make_unique<FastPlanImpl<V, R, 11, 6>>(tab, nmax, dev);
-    case 4096: return std::make_unique<FastPlanImpl<V, R, 12, 6>>(tab, nmax, dev);
+    case 1024: return std::make_unique<FastPlanImpl<V, R, 10, 6, RD>>(tab, nmax, dev);
+    case 2048: return std::make_unique<FastPlanImpl<V, R, 11, 6, RD>>(tab, nmax, dev);
+    case 4096: return std::make_unique<FastPlanImpl<V, R, 12, 6, RD>>(tab, nmax, dev);
     case 8192:
-      if constexpr (sizeof(R) == 4) return std::make_unique<FastPlanImpl<V, R, 13, 6>>(tab, nmax, dev);
+      if constexpr (sizeof(R) == 4) return std::make_unique<FastPlanImpl<V, R, 13, 6, RD>>(tab, nmax, dev);
       break;
   }
   return nullptr;

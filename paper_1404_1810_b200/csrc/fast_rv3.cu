@@ -1,0 +1,10 @@
+// fast_rv3.cu -- fused-kernel instances for AM-QFT variant 3, RDFT rows
+// (two real rows per kernel row).
+#include "fast_kernel.cuh"
+
+namespace amqft_b200 {
+namespace fastk {
+template std::unique_ptr<FastPlan> make_sized<3, float, true>(size_t, const void*, uint32_t, int);
+template std::unique_ptr<FastPlan> make_sized<3, double, true>(size_t, const void*, uint32_t, int);
+}  // namespace fastk
+}  // namespace amqft_b200

@@ -1,9 +1,9 @@
-// fast_v1.cu -- fused-kernel instances for AM-QFT variant 1.
+// fast_v1.cu -- fused-kernel instances for AM-QFT variant 1, CDFT rows.
 #include "fast_kernel.cuh"
 
 namespace amqft_b200 {
 namespace fastk {
-template std::unique_ptr<FastPlan> make_for_variant<1, float>(size_t, const void*, uint32_t, int);
-template std::unique_ptr<FastPlan> make_for_variant<1, double>(size_t, const void*, uint32_t, int);
+template std::unique_ptr<FastPlan> make_sized<1, float, false>(size_t, const void*, uint32_t, int);
+template std::unique_ptr<FastPlan> make_sized<1, double, false>(size_t, const void*, uint32_t, int);
 }  // namespace fastk
 }  // namespace amqft_b200

@@ -1,9 +1,9 @@
-// fast_v4.cu -- fused-kernel instances for AM-QFT variant 4.
+// fast_v4.cu -- fused-kernel instances for AM-QFT variant 4, CDFT rows.
 #include "fast_kernel.cuh"
 
 namespace amqft_b200 {
 namespace fastk {
-template std::unique_ptr<FastPlan> make_for_variant<4, float>(size_t, const void*, uint32_t, int);
-template std::unique_ptr<FastPlan> make_for_variant<4, double>(size_t, const void*, uint32_t, int);
+template std::unique_ptr<FastPlan> make_sized<4, float, false>(size_t, const void*, uint32_t, int);
+template std::unique_ptr<FastPlan> make_sized<4, double, false>(size_t, const void*, uint32_t, int);
 }  // namespace fastk
 }  // namespace amqft_b200

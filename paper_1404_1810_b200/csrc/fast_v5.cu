@@ -1,9 +1,9 @@
-// fast_v5.cu -- fused-kernel instances for AM-QFT variant 5.
+// fast_v5.cu -- fused-kernel instances for AM-QFT variant 5, CDFT rows.
 #include "fast_kernel.cuh"
 
 namespace amqft_b200 {
 namespace fastk {
-template std::unique_ptr<FastPlan> make_for_variant<5, float>(size_t, const void*, uint32_t, int);
-template std::unique_ptr<FastPlan> make_for_variant<5, double>(size_t, const void*, uint32_t, int);
+template std::unique_ptr<FastPlan> make_sized<5, float, false>(size_t, const void*, uint32_t, int);
+template std::unique_ptr<FastPlan> make_sized<5, double, false>(size_t, const void*, uint32_t, int);
 }  // namespace fastk
 }  // namespace amqft_b200

@@ -1,9 +1,9 @@
-// fast_v6.cu -- fused-kernel instances for AM-QFT variant 6.
+// fast_v6.cu -- fused-kernel instances for AM-QFT variant 6, CDFT rows.
 #include "fast_kernel.cuh"
 
 namespace amqft_b200 {
 namespace fastk {
-template std::unique_ptr<FastPlan> make_for_variant<6, float>(size_t, const void*, uint32_t, int);
-template std::unique_ptr<FastPlan> make_for_variant<6, double>(size_t, const void*, uint32_t, int);
+template std::unique_ptr<FastPlan> make_sized<6, float, false>(size_t, const void*, uint32_t, int);
+template std::unique_ptr<FastPlan> make_sized<6, double, false>(size_t, const void*, uint32_t, int);
 }  // namespace fastk
 }  // namespace amqft_b200

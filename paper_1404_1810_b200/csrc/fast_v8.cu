@@ -1,9 +1,9 @@
-// fast_v8.cu -- fused-kernel instances for AM-QFT variant 8.
+// fast_v8.cu -- fused-kernel instances for AM-QFT variant 8, CDFT rows.
 #include "fast_kernel.cuh"
 
 namespace amqft_b200 {
 namespace fastk {
-template std::unique_ptr<FastPlan> make_for_variant<8, float>(size_t, const void*, uint32_t, int);
-template std::unique_ptr<FastPlan> make_for_variant<8, double>(size_t, const void*, uint32_t, int);
+template std::unique_ptr<FastPlan> make_sized<8, float, false>(size_t, const void*, uint32_t, int);
+template std::unique_ptr<FastPlan> make_sized<8, double, false>(size_t, const void*, uint32_t, int);
 }  // namespace fastk
 }  // namespace amqft_b200

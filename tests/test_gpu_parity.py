@@ -394,3 +394,32 @@ def test_exact_fp64_large_n_bitwise(oracle, restatement, lg):
     assert got.tobytes() == want.tobytes()
     inv = run_plan(plan, [want], inverse=True)[0]
     assert inv.tobytes() == r.inverse_cdft(4, n, want).tobytes()
+
+
+@pytest.mark.parametrize("n", [1024, 4096])
+def test_fast_kernel_rdft_fp64_bitwise(oracle, restatement, n):
+    """RDFT rows through the fused kernel (two real rows per kernel row,
+    odd batch: the last kernel row holds one): bitwise the oracle's Rdft."""
+    r, O = restatement, oracle
+    for v in range(1, 9):
+        xs = [r.uniform(r.mix_seed(40, v, n, k), n) * 2 - 1 for k in range(5)]
+        plan = amqft.Plan(v, amqft.FunctionId.Rdft, n, 5, dtype="f64", order=amqft.Order.Fast)
+        assert plan.path()[0] == 2, "fused kernel expected for RDFT"
+        got = run_plan(plan, xs)
+        for k in range(5):
+            assert got[k].tobytes() == r.execute(v, 1, n, xs[k]).tobytes(), (v, n, k)
+        assert plan.op_counts() == r.execute(v, 1, n, xs[0], meter=True)[1]
+
+
+@pytest.mark.parametrize("n", [2048, 8192])
+def test_fast_kernel_rdft_fp32_tolerance(oracle, restatement, n):
+    r, O = restatement, oracle
+    rng = np.random.default_rng(n + 1)
+    xs = rng.standard_normal((7, n)).astype(np.float32)
+    tol = 1e-5 * math.log2(n)
+    for v in (1, 2, 3, 4):
+        plan = amqft.Plan(v, amqft.FunctionId.Rdft, n, 7, dtype="f32", order=amqft.Order.Fast)
+        got = run_plan(plan, xs)
+        for k in (0, 5, 6):
+            err = r.rel_l2(got[k], r.execute(v, 1, n, xs[k].astype(np.float64)))
+            assert err <= tol, (v, n, k, err)
