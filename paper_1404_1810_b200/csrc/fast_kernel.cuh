@@ -352,7 +352,9 @@ __device__ __forceinline__ void am_scan_depth(R (&x)[C::N / 128], int i, int nl,
       const bool neg = !ADD && (M & 1) && (d & 1);            // factor s^(M d)
       if (pos >= d) acc = neg ? A::sub(acc, o) : A::add(acc, o);
     }
-    R yin = desc ? __shfl_down_sync(0xffffffffu, acc, 1) : __shfl_up_sync(0xffffffffu, acc, 1);
+    // exclusive prefix without another shuffle: acc = A_own + s^M y_in
+    constexpr bool SIGN_NEG = !ADD && (M & 1);
+    R yin = SIGN_NEG ? A::sub(loc[M - 1], acc) : A::sub(acc, loc[M - 1]);
     if (pos == 0) yin = R(0);
 #pragma unroll
     for (int j = 0; j < M; ++j) {
