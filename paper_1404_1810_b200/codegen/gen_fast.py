@@ -66,7 +66,7 @@ def const_expr(v, L):
     if v == L // 4:
         return "base"
     lg = (2 * L).bit_length() - 1
-    return f"__ldg(tab + ({v} * (nmax >> {lg}) - 1))"
+    return f"AMQFT_TABLD(tab, ({v} * (nmax >> {lg}) - 1))"
 
 
 # --------------------------------------------------------------- time-major
@@ -524,7 +524,7 @@ def scaled_mnet(em, y, HP, lam, sine, direction, nlog, LB):
         for vv in range(1, L // 2):
             lo, hi = a + vv, a + L - vv
             j, m = (lo, hi) if rho == 0 else (hi, lo)
-            k = "base" if vv == L // 4 else f"__ldg(tab + {vv * (nmax >> lg2L) - 1})"
+            k = "base" if vv == L // 4 else f"AMQFT_TABLD(tab, {vv * (nmax >> lg2L) - 1})"
             if direction == "fwd":
                 p_, q_ = y[j], y[m]
                 s_, d_ = add(p_, q_), sub(p_, q_)
@@ -735,7 +735,7 @@ def scaled_mnet_cls(em, y, HP, lam, sine, direction, nlog, cls):
                 continue
             lo, hi = a + vv, a + L - vv
             j, m = (lo, hi) if rho == 0 else (hi, lo)
-            k = "base" if vv == L // 4 else f"__ldg(tab + {vv * (nmax >> lg2L) - 1})"
+            k = "base" if vv == L // 4 else f"AMQFT_TABLD(tab, {vv * (nmax >> lg2L) - 1})"
             if direction == "fwd":
                 p_, q_ = y[j], y[m]
                 s_, d_ = add(p_, q_), sub(p_, q_)
@@ -896,6 +896,11 @@ def main():
         "#pragma once",
         "#define PH(i) ((i) + ((i) >> LOGLB))",
         "#define SW(i) ((i) + (((i) + swsh) >> 5))",
+        "// constant-table read: __ldg from global memory by default; the fused",
+        "// kernel reads it from its parameter space (constant bank operands)",
+        "#ifndef AMQFT_TABLD",
+        "#define AMQFT_TABLD(t, i) __ldg((t) + (i))",
+        "#endif",
         "#ifndef AMQFT_CLASS_FENCE",
         "#define AMQFT_CLASS_FENCE() asm volatile(\"\" ::: \"memory\")",
         "#endif",

@@ -33,6 +33,9 @@
 #include <type_traits>
 
 #include "fast.cuh"
+// The fused kernel reads the AM constant table from its parameter space:
+// the generated code's compile-time slots become constant-bank operands.
+#define AMQFT_TABLD(t, i) ((t)[i])
 #include "fast_gen.cuh"
 #include "generic.cuh"
 
@@ -53,6 +56,12 @@ namespace amqft_b200 {
 namespace fastk {
 
 __device__ __forceinline__ int parity(unsigned x) { return __popc(x) & 1; }
+
+// Kernel-parameter copy of the constant table (N/4 values: 4-8 KB).
+template <typename R, int K>
+struct TabParam {
+  R v[K];
+};
 
 template <int V, typename R, int LOGN, int LOGLB>
 struct Cfg {
@@ -639,7 +648,13 @@ __global__ void __launch_bounds__(
                                     2 * Cfg<V, R, LOGN, LOGLB>::SMEM_BLOCK <= 227 * 1024)
                                        ? AMQFT_FAST_MINB : 1))
 k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows_in,
-       const R* __restrict__ tab, const R* __restrict__ ltab, int nmax, R scale) {
+       const __grid_constant__ TabParam<R, (1 << LOGN) / 4> tparam, const R* __restrict__ ltab, int nmax_unused,
+       R scale) {
+  (void)nmax_unused;
+  // the plan compacts its table to Nmax = N (k_compact_table), so every
+  // generated slot index is a compile-time constant into the parameter space
+  const R* tab = tparam.v;
+  constexpr int nmax = 1 << LOGN;
   constexpr bool INV = MODE == 1;
   constexpr bool RDFT = MODE == 2;
   // kernel rows: CDFT rows, or pairs of RDFT rows (the last one maybe single)
@@ -669,7 +684,7 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows_in,
     else
       __syncthreads();
   };
-  const R base = __ldg(tab + (nmax / 4 - 1));
+  const R base = tab[nmax / 4 - 1];
   constexpr int N = C::N, H = C::H;
   constexpr uint32_t ROW_BYTES = 2 * N * sizeof(R);
   // load/store: 256 threads, cells tid + 256 it; address steps per it
@@ -1078,6 +1093,8 @@ class FastPlanImpl final : public FastPlan {
     k_level_table<R><<<8, 256>>>(tab_, ltab_, C::H, C::LT, static_cast<int>(nmax_));
     e = cudaDeviceSynchronize();
     if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+    e = cudaMemcpy(tparam_.v, tab_, sizeof(tparam_.v), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
   }
   ~FastPlanImpl() override {
     if (ltab_) cudaFree(ltab_);
@@ -1090,14 +1107,14 @@ class FastPlanImpl final : public FastPlan {
     const unsigned grid = static_cast<unsigned>(std::min<size_t>(units, static_cast<size_t>(grid_cap_)));
     if (RDFT_ROWS)
       k_fast<V, R, LOGN, LOGLB, 2><<<grid, C::NTB, C::SMEM_BLOCK, st>>>(
-          static_cast<const R*>(in), static_cast<R*>(out), rows, tab_, ltab_, static_cast<int>(nmax_), R(1));
+          static_cast<const R*>(in), static_cast<R*>(out), rows, tparam_, ltab_, static_cast<int>(nmax_), R(1));
     else if (inverse)
       k_fast<V, R, LOGN, LOGLB, 1><<<grid, C::NTB, C::SMEM_BLOCK, st>>>(
-          static_cast<const R*>(in), static_cast<R*>(out), rows, tab_, ltab_, static_cast<int>(nmax_),
+          static_cast<const R*>(in), static_cast<R*>(out), rows, tparam_, ltab_, static_cast<int>(nmax_),
           R(1) / R(C::N));
     else
       k_fast<V, R, LOGN, LOGLB, 0><<<grid, C::NTB, C::SMEM_BLOCK, st>>>(
-          static_cast<const R*>(in), static_cast<R*>(out), rows, tab_, ltab_, static_cast<int>(nmax_),
+          static_cast<const R*>(in), static_cast<R*>(out), rows, tparam_, ltab_, static_cast<int>(nmax_),
           R(1) / R(C::N));
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
@@ -1105,6 +1122,7 @@ class FastPlanImpl final : public FastPlan {
 
  private:
   const R* tab_;
+  TabParam<R, (1 << LOGN) / 4> tparam_{};
   R* own_tab_ = nullptr;
   R* ltab_ = nullptr;
   uint32_t nmax_;

@@ -20,13 +20,15 @@ static float run_v(const float* in, float* out, size_t rows, const float* tab, i
   float* ltab = nullptr;
   cudaMalloc(&ltab, sizeof(float) * C::H);
   k_level_table<float><<<8, 256>>>(tab, ltab, C::H, C::LT, nmax);
+  TabParam<float, C::N / 4> tp;
+  cudaMemcpy(tp.v, tab, sizeof(tp.v), cudaMemcpyDeviceToHost);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   float best = 1e30f;
   for (int r = 0; r < reps; ++r) {
     cudaEventRecord(a);
-    fn<<<grid, C::NTB, C::SMEM_BLOCK>>>(in, out, rows, tab, ltab, nmax, 1.0f / 4096);
+    fn<<<grid, C::NTB, C::SMEM_BLOCK>>>(in, out, rows, tp, ltab, nmax, 1.0f / 4096);
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     float ms = 0;

@@ -27,7 +27,9 @@ static int run_v(const float* in, float* out, size_t rows, const float* tab, int
   float* ltab = nullptr;
   cudaMalloc(&ltab, sizeof(float) * C::H);
   k_level_table<float><<<8, 256>>>(tab, ltab, C::H, C::LT, nmax);
-  fn<<<grid, C::NTB, C::SMEM_BLOCK>>>(in, out, rows, tab, ltab, nmax, 1.0f / C::N);
+  TabParam<float, C::N / 4> tp;
+  cudaMemcpy(tp.v, tab, sizeof(tp.v), cudaMemcpyDeviceToHost);
+  fn<<<grid, C::NTB, C::SMEM_BLOCK>>>(in, out, rows, tp, ltab, nmax, 1.0f / C::N);
   cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(cyc, g_phase_cycles, sizeof(z));
   cudaFree(ltab);
