@@ -470,171 +470,8 @@ def main():
                "h2d_bytes_per_step": batch * 2 * n * esize, "d2h_bytes_per_step": batch * 2 * n * esize,
                "steps": args.e2e_steps}
 
-    cpu = None
-    accuracy = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            cpu = cpu_baseline(args)
-        except Exception as e:  # noqa: BLE001
-            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
-                   "sample": f"failed: {e}"}
-        # CPU leg, checker use of the oracle: parity of the timed rows, and
-        # every variant's config-1 accuracy (N = 1024 fp64 exact path on the
-        # device) against the reference CPU result, the naive O(N^2) fp64
-        # DFT and the extended-precision spectrum (north_star reporting)
-        try:
-            parity, accuracy = oracle_checks(args, kept, amqft, kept_v)
-        except Exception as e:  # noqa: BLE001
-            parity = f"unavailable: {e}"
-
-    if rank == 0:
-        line = {
-            "metric": f"AM-QFT transforms/s ({'N=2^24' if args.config == 4 else 'N=2^30'} fp32 single transform)",
-            "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f32", "data": "synthetic: iid N(0,1) from a seed, generated on the device",
-            "config": {"workload": workload, "n": n, "variant": args.variant, "path": path,
-                       "l2": "inputs >= 128 MiB > 126 MB L2; no flush"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": None, "peak_source": hbm_src,
-                         "algorithmic_bytes_per_gpu": per_gpu_bytes},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, **extra,
-        }
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
-
-
-def main():
-    args = parse()
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.config in (4, 5) and args.impl == "ours":
-        bench_single(args, world, rank, local)
-        return
-
-    if args.impl == "reference":
-        line = bench_reference(args, rank)
-        if line is not None:
-            print(json.dumps(line), flush=True)
-        return
-
-    import torch
-    import torch.distributed as dist
-    import paper_1404_1810_b200 as amqft
-
-    torch.cuda.set_device(local)
-    dev = torch.device(f"cuda:{local}")
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-
-    n, batch = args.n, args.batch
-    dtype = torch.float32 if args.dtype == "f32" else torch.float64
-    esize = 4 if args.dtype == "f32" else 8
-    order = amqft.Order.Fast if args.order == "fast" else amqft.Order.Exact
-    plan = amqft.Plan(args.variant, amqft.FunctionId.Cdft, n, batch, dtype=args.dtype,
-                      order=order, device=local)
-    path, launches = plan.path()
-    g = torch.Generator(device=dev)
-    g.manual_seed(20260 + rank)
-    x = torch.randn(batch, 2 * n, generator=g, device=dev, dtype=dtype)
-    y = torch.empty_like(x)
-    stream = torch.cuda.current_stream(dev)
-
-    for _ in range(max(args.warmup, 3)):
-        plan.forward(x, y, stream=stream)
-    torch.cuda.synchronize(dev)
-
-    sampler = ClockSampler(local)
-    sampler.start()
-    time.sleep(0.3)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        plan.forward(x, y, stream=stream)
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
-    clocks = sampler.stop()
-    ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], device=dev, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
-    ms_per_step = ms / args.steps
-    value = world * batch * args.steps / (ms / 1000.0)
-
-    # Dominant-kernel roofline: the exec call is one kernel on path 0/2;
-    # per-launch duration from CUDA events on the launching stream.
-    hbm, hbm_src = peaks()
-    alg_bytes = 2 * (2 * n * esize) * batch  # one read + one write per transform
-    kernel_ms = ms_per_step / max(1, launches) if path != 1 else ms_per_step
-    achieved = alg_bytes / (kernel_ms / 1000.0) / 1e9
-    traffic, traffic_src = ncu_traffic(args, n)
-    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm, "traffic": traffic, "traffic_unit": "bytes per launch (DRAM read + write)",
-            "traffic_source": traffic_src,
-            "peak_source": hbm_src, "algorithmic_bytes_per_launch": alg_bytes,
-            "kernel_ms": kernel_ms}
-
-    # Parity of what was timed (checked in the CPU-baseline leg below, the
-    # one place the oracle runs): keep a few output rows on the host.
-    check_rows = (0, batch // 2, batch - 1)
-    kept = [(x[row].double().cpu().numpy(), y[row].double().cpu().numpy()) for row in check_rows]
-    parity = None
-
-    # End to end through the public API with HOST buffers (pinned): H2D of the
-    # step's input, the transform, D2H of the result, every step.
-    e2e = None
-    if args.e2e_steps > 0:
-        hx = torch.empty(batch, 2 * n, dtype=dtype, pin_memory=True)
-        hx.copy_(x)
-        hy = torch.empty_like(hx, pin_memory=True)
-        plan.forward(x, y, stream=stream)
-        torch.cuda.synchronize(dev)
-        if world > 1:
-            dist.barrier()
-        plan.forward_host(hx, hy, stream=stream)   # creates the pipeline slots (untimed)
-        torch.cuda.synchronize(dev)
-        s0 = torch.cuda.Event(enable_timing=True)
-        s1 = torch.cuda.Event(enable_timing=True)
-        s0.record(stream)
-        for _ in range(args.e2e_steps):
-            # public host-buffer entry point: H2D | transform | D2H pipelined
-            plan.forward_host(hx, hy, stream=stream)
-        s1.record(stream)
-        torch.cuda.synchronize(dev)
-        ems = torch.tensor([s0.elapsed_time(s1)], device=dev, dtype=torch.float64)
-        if world > 1:
-            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * batch * args.e2e_steps / (float(ems.item()) / 1000.0), "unit": UNIT,
-               "h2d_bytes_per_step": batch * 2 * n * esize, "d2h_bytes_per_step": batch * 2 * n * esize,
-               "steps": args.e2e_steps}
-
-    cpu = None
-    accuracy = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            cpu = cpu_baseline(args)
-        except Exception as e:  # noqa: BLE001
-            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
-                   "sample": f"failed: {e}"}
-        # CPU leg, checker use of the oracle: parity of the timed rows, and
-        # every variant's config-1 accuracy (N = 1024 fp64 exact path on the
-        # device) against the reference CPU result, the naive O(N^2) fp64
-        # DFT and the extended-precision spectrum (north_star reporting)
-        try:
-            parity, accuracy = oracle_checks(args, kept, amqft)
-        except Exception as e:  # noqa: BLE001
-            parity = f"unavailable: {e}"
-
     variants = None
+    kept_v = {}
     if args.all_variants:
         variants = {}
         for v in range(1, 9):
@@ -652,7 +489,25 @@ def main():
             vms = a.elapsed_time(b) / args.steps
             variants[str(v)] = {"transforms_per_s": batch / (vms / 1000.0), "ms": vms,
                                 "gbs": alg_bytes / (vms / 1000.0) / 1e9}
+            kept_v[v] = (x[0].double().cpu().numpy(), y[0].double().cpu().numpy())
             pv.close()
+
+    cpu = None
+    accuracy = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(args)
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                   "sample": f"failed: {e}"}
+        # CPU leg, checker use of the oracle: parity of the timed rows, and
+        # every variant's config-1 accuracy (N = 1024 fp64 exact path on the
+        # device) against the reference CPU result, the naive O(N^2) fp64
+        # DFT and the extended-precision spectrum (north_star reporting)
+        try:
+            parity, accuracy = oracle_checks(args, kept, amqft, kept_v)
+        except Exception as e:  # noqa: BLE001
+            parity = f"unavailable: {e}"
 
     if rank == 0:
         line = {
