@@ -910,9 +910,9 @@ def main():
     hp_all = sorted({hp for _, hps in CONFIGS for hp in hps})
     for LB, hps in CONFIGS:
         for v in range(1, 9):
-            for rho in (0, 1):
+            for rho in (0,):   # odd segments are stored reversed (Cfg::ipos)
                 for lam in (0, 1):
-                    for part in ((0, 1, 2) if rho == 0 else (0, 1)):
+                    for part in (0, 1, 2):
                         out.append(gen_tmB(v, LB, rho, lam, part) if v in TM else gen_hmB(v, LB, rho, lam, part))
     for v in range(1, 9):
         for hp in hp_all:
@@ -1026,13 +1026,14 @@ def main():
             out.append("  template <typename R, typename AR, int LOGLB, int D, int PART>")
             out.append("  static __device__ __forceinline__ void run(int rho, int lens, const R* T, R* F, int a, "
                        "const R* tab, int nmax, R base, int N, int r, int dsto) {")
-            for rho in (0, 1):
-                for lam in (0, 1):
-                    p2 = (f"else if constexpr (PART == 2) gen::{fam}_v{v}_lb{LB}_r{rho}_l{lam}_p2"
-                          f"<R, AR, LOGLB, D>(T, F, a, tab, nmax, base, N, r, dsto); ") if rho == 0 else ""
-                    out.append(f"    if (rho == {rho} && lens == {lam}) {{ if constexpr (PART == 0) gen::{fam}_v{v}_lb{LB}_r{rho}_l{lam}_p0"
-                               f"<R, AR, LOGLB, D>(T, F, a, tab, nmax, base, N, r, dsto); {p2}else gen::{fam}_v{v}_lb{LB}_r{rho}_l{lam}_p1"
-                               f"<R, AR, LOGLB, D>(T, F, a, tab, nmax, base, N, r, dsto); return; }}")
+            # orientation 0 only (rho is ignored): odd segments are stored
+            # reversed, which is exactly the orientation-1 segment
+            out.append("    (void)rho;")
+            for lam in (0, 1):
+                pre = f"gen::{fam}_v{v}_lb{LB}_r0_l{lam}"
+                args = "<R, AR, LOGLB, D>(T, F, a, tab, nmax, base, N, r, dsto)"
+                out.append(f"    if (lens == {lam}) {{ if constexpr (PART == 0) {pre}_p0{args}; "
+                           f"else if constexpr (PART == 2) {pre}_p2{args}; else {pre}_p1{args}; return; }}")
             out.append("  }")
             out.append("};")
     out.append("template <int V, int HP> struct Small;")

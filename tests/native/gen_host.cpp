@@ -22,33 +22,21 @@ int bottom_v(int LB, int rho, int lens, const double* T, double* F, int a, const
   if (LB != 64) return -1;
   switch (D) {
     case 3:
-      if (rho == 0) {   // the kernel's path: all classes, loads hoisted
-        Bottom<V, 64>::template run<double, HA, 6, 3, 2>(rho, lens, T, F, a, tab, nmax, base, N, r, dsto);
-        return 0;
-      }
-      Bottom<V, 64>::template run<double, HA, 6, 3, 0>(rho, lens, T, F, a, tab, nmax, base, N, r, dsto);
-      Bottom<V, 64>::template run<double, HA, 6, 3, 1>(rho, lens, T, F, a, tab, nmax, base, N, r, dsto); return 0;
+      if (rho != 0) return -1;   // odd segments are stored reversed: orientation 0 only
+      Bottom<V, 64>::template run<double, HA, 6, 3, 2>(rho, lens, T, F, a, tab, nmax, base, N, r, dsto);
+      return 0;
     case 4:
-      if (rho == 0) {   // the kernel's path: all classes, loads hoisted
-        Bottom<V, 64>::template run<double, HA, 6, 4, 2>(rho, lens, T, F, a, tab, nmax, base, N, r, dsto);
-        return 0;
-      }
-      Bottom<V, 64>::template run<double, HA, 6, 4, 0>(rho, lens, T, F, a, tab, nmax, base, N, r, dsto);
-      Bottom<V, 64>::template run<double, HA, 6, 4, 1>(rho, lens, T, F, a, tab, nmax, base, N, r, dsto); return 0;
+      if (rho != 0) return -1;   // odd segments are stored reversed: orientation 0 only
+      Bottom<V, 64>::template run<double, HA, 6, 4, 2>(rho, lens, T, F, a, tab, nmax, base, N, r, dsto);
+      return 0;
     case 5:
-      if (rho == 0) {   // the kernel's path: all classes, loads hoisted
-        Bottom<V, 64>::template run<double, HA, 6, 5, 2>(rho, lens, T, F, a, tab, nmax, base, N, r, dsto);
-        return 0;
-      }
-      Bottom<V, 64>::template run<double, HA, 6, 5, 0>(rho, lens, T, F, a, tab, nmax, base, N, r, dsto);
-      Bottom<V, 64>::template run<double, HA, 6, 5, 1>(rho, lens, T, F, a, tab, nmax, base, N, r, dsto); return 0;
+      if (rho != 0) return -1;   // odd segments are stored reversed: orientation 0 only
+      Bottom<V, 64>::template run<double, HA, 6, 5, 2>(rho, lens, T, F, a, tab, nmax, base, N, r, dsto);
+      return 0;
     case 6:
-      if (rho == 0) {   // the kernel's path: all classes, loads hoisted
-        Bottom<V, 64>::template run<double, HA, 6, 6, 2>(rho, lens, T, F, a, tab, nmax, base, N, r, dsto);
-        return 0;
-      }
-      Bottom<V, 64>::template run<double, HA, 6, 6, 0>(rho, lens, T, F, a, tab, nmax, base, N, r, dsto);
-      Bottom<V, 64>::template run<double, HA, 6, 6, 1>(rho, lens, T, F, a, tab, nmax, base, N, r, dsto); return 0;
+      if (rho != 0) return -1;   // odd segments are stored reversed: orientation 0 only
+      Bottom<V, 64>::template run<double, HA, 6, 6, 2>(rho, lens, T, F, a, tab, nmax, base, N, r, dsto);
+      return 0;
   }
   return -1;
 }
