@@ -465,3 +465,32 @@ def test_fast_kernel_fp32_deterministic_across_launch_shapes(v):
         one_r.forward(xr[row:row + 1].contiguous(), z)
         torch.cuda.synchronize()
         assert torch.equal(z[0], r1[row]), (v, row)
+
+
+@pytest.mark.parametrize("v", [1, 2, 3, 4])
+def test_config2_full_size_properties(v):
+    """Config 2 at full size (65536 x N=4096 fp32) through size-independent
+    properties: Parseval (||X||^2 = N ||x||^2), linearity
+    (F(ax + by) = aF(x) + bF(y)) and the swap-trick round trip, per row, with
+    the fp32 tolerance 1e-5 log2 N."""
+    n, rows = 4096, 65536
+    tol = 1e-5 * math.log2(n)
+    g = torch.Generator(device=DEV).manual_seed(7000 + v)
+    x = torch.randn(rows, 2 * n, generator=g, device=DEV)
+    y = torch.randn(rows, 2 * n, generator=g, device=DEV)
+    plan = amqft.Plan(v, amqft.FunctionId.Cdft, n, rows, dtype="f32", order=amqft.Order.Fast)
+    fx, fy, fz = torch.empty_like(x), torch.empty_like(x), torch.empty_like(x)
+    plan.forward(x, fx)
+    plan.forward(y, fy)
+    a, b = 0.75, -1.25
+    plan.forward(a * x + b * y, fz)
+    back = torch.empty_like(x)
+    plan.inverse(fx, back)
+    torch.cuda.synchronize()
+    ex = x.double().pow(2).sum(1)
+    parseval = (fx.double().pow(2).sum(1) / (n * ex) - 1).abs().max().item()
+    assert parseval < 2 * tol, parseval
+    lin = ((fz - (a * fx + b * fy)).double().norm(dim=1) / fz.double().norm(dim=1)).max().item()
+    assert lin < 2 * tol, lin
+    rt = ((back - x).double().norm(dim=1) / x.double().norm(dim=1)).max().item()
+    assert rt < 2 * tol, rt
