@@ -8,6 +8,8 @@
 //           the subtrees below as per-CTA jobs (k_prog).  This keeps the
 //           reference recursion (and fp64 bitwise parity) at any N.
 //   path 2  fused fast kernels (fast.cuh) for the CDFT hot path.
+//   path 3  four-step over the fused kernel (fourstep.cuh), large N, fp32.
+//   path 4  one thread per row (small_kernel.cuh), small CDFTs.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -295,6 +297,11 @@ amqft_status amqft_plan_create(amqft_plan* out, const amqft_plan_desc* desc) {
     if (desc->order == AMQFT_ORDER_FAST) {
       P->fast = make_fast_plan(*desc, P->d_trig, P->nmax);
       int fpath = 2;
+      OpCount small_ops{};
+      if (!P->fast) {
+        P->fast = make_small_plan(*desc, P->d_trig, P->nmax, &small_ops);
+        if (P->fast) fpath = 4;
+      }
       if (!P->fast && fourstep_covers(*desc)) {
         P->fast = make_fourstep_plan(*desc, P->d_trig, P->nmax);
         fpath = 3;
@@ -305,7 +312,7 @@ amqft_status amqft_plan_create(amqft_plan* out, const amqft_plan_desc* desc) {
         P->c.fn = desc->function;
         P->c.n = n;
         P->c.cells = fn_cells(desc->function, n);
-        P->c.ops = fpath == 2 ? fast_op_counts(*desc) : fourstep_op_counts(*desc);
+        P->c.ops = fpath == 2 ? fast_op_counts(*desc) : fpath == 4 ? small_ops : fourstep_op_counts(*desc);
         P->launches = P->fast->launches;
         *out = P.release();
         return AMQFT_OK;

@@ -2,6 +2,7 @@
 // per-variant instances: fast_v1.cu .. fast_v8.cu).
 #include "fast.cuh"
 #include "fourstep.cuh"
+#include "small_gen.cuh"
 
 namespace amqft_b200 {
 namespace fastk {
@@ -43,6 +44,52 @@ std::unique_ptr<FastPlan> make_fast_plan(const amqft_plan_desc& d, const void* d
   const int kind = d.function == AMQFT_FN_RDFT ? 1 : 0;
   if (d.dtype == AMQFT_F32) return make_fast_typed<float>(d.variant, kind, d.n, d_trig, nmax, d.device);
   return make_fast_typed<double>(d.variant, kind, d.n, d_trig, nmax, d.device);
+}
+
+namespace smallk {
+template <int V, typename R>
+std::unique_ptr<FastPlan> make_small_sized(size_t n, const void* tab, uint32_t nmax, int dev);
+
+template <int V, typename R, int LOGN>
+bool small_ops(OpCount* o) {
+  using G = SmallGen<V, 0, LOGN, R>;
+  o->adds = G::OPS[0];
+  o->muls = G::OPS[1];
+  o->bt = G::OPS[2];
+  return true;
+}
+template <int V, typename R>
+bool small_ops_n(size_t n, OpCount* o) {
+  switch (n) {
+    case 2: return small_ops<V, R, 1>(o);
+    case 4: return small_ops<V, R, 2>(o);
+    case 8: return small_ops<V, R, 3>(o);
+    case 16: return small_ops<V, R, 4>(o);
+    case 32: return small_ops<V, R, 5>(o);
+    case 64:
+      if constexpr (sizeof(R) == 4) return small_ops<V, R, 6>(o);
+      break;
+  }
+  return false;
+}
+template <typename R>
+std::unique_ptr<FastPlan> make_small_typed(int v, size_t n, const void* tab, uint32_t nmax, int dev, OpCount* o) {
+  switch (v) {
+#define AMQFT_SMALL_CASE(V) \
+  case V: if (!small_ops_n<V, R>(n, o)) return nullptr; return make_small_sized<V, R>(n, tab, nmax, dev);
+    AMQFT_SMALL_CASE(1) AMQFT_SMALL_CASE(2) AMQFT_SMALL_CASE(3) AMQFT_SMALL_CASE(4)
+    AMQFT_SMALL_CASE(5) AMQFT_SMALL_CASE(6) AMQFT_SMALL_CASE(7) AMQFT_SMALL_CASE(8)
+#undef AMQFT_SMALL_CASE
+  }
+  return nullptr;
+}
+}  // namespace smallk
+
+std::unique_ptr<FastPlan> make_small_plan(const amqft_plan_desc& d, const void* d_trig, uint32_t nmax,
+                                          OpCount* ops) {
+  if (d.function != AMQFT_FN_CDFT || d.trig_mode != AMQFT_TRIG_TABLE) return nullptr;
+  if (d.dtype == AMQFT_F32) return smallk::make_small_typed<float>(d.variant, d.n, d_trig, nmax, d.device, ops);
+  return smallk::make_small_typed<double>(d.variant, d.n, d_trig, nmax, d.device, ops);
 }
 
 OpCount fast_op_counts(const amqft_plan_desc& d) {

@@ -23,4 +23,10 @@ std::unique_ptr<FastPlan> make_fast_plan(const amqft_plan_desc& d,
                                          const void* d_trig, uint32_t nmax);
 OpCount fast_op_counts(const amqft_plan_desc& d);
 
+// One-thread-per-row kernel for small CDFTs (small_kernel.cuh): fp32 N <= 64,
+// fp64 N <= 32.  nullptr when not covered; *ops receives the traced
+// schedule's op counts (= the reference meter).
+std::unique_ptr<FastPlan> make_small_plan(const amqft_plan_desc& d, const void* d_trig, uint32_t nmax,
+                                          OpCount* ops);
+
 }  // namespace amqft_b200

@@ -1,0 +1,255 @@
+// small_kernel.cuh -- one whole small CDFT per thread (path 4).
+//
+// For N <= 64 (fp32) / N <= 32 (fp64) a thread owns one row: the traced
+// stage program of the plan compiler, emitted as straight-line code by
+// codegen/gen_small.py (small_gen.cuh), keeps the row in registers.  Every
+// line is one reference add/sub/mul on the reference operands (no FMA
+// contraction, Arith<R>), so the fp64 instance is bitwise amqft::execute for
+// all 8 variants, in both execution orders.
+//
+// Data movement (HBM-bound; ~0.3-1.2 flop/B):
+//  * rows of <= 64 B: straight from global memory, 16-byte vector loads and
+//    stores per thread (a warp touches 32 consecutive rows, every fetched
+//    sector is used);
+//  * larger rows: a CTA tile of T rows is staged in shared memory by one
+//    cp.async.bulk per row into slots padded by 16 bytes (so the 8 lanes of
+//    a quarter-warp reading the same 16-byte chunk of 8 rows hit 8 distinct
+//    bank groups), transformed in place, and written back by one bulk store
+//    per row.
+// The inverse is the swap trick (x = swap(DFT(swap(X))) / N), fused into the
+// chunk loads and stores.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <memory>
+#include <stdexcept>
+
+#include "fast.cuh"
+#include "generic.cuh"
+#include "small_gen.cuh"
+
+namespace amqft_b200 {
+namespace smallk {
+
+template <typename R, int K>
+struct TabP {
+  R v[K];
+};
+
+template <typename R> struct Vec;
+template <> struct Vec<float> { using T = float4; static constexpr int W = 4; };
+template <> struct Vec<double> { using T = double2; static constexpr int W = 2; };
+
+// Chunk I/O of one row (p: the row in global or shared memory).
+template <typename R, bool INV> struct RowIO;
+template <bool INV> struct RowIO<float, INV> {
+  float4* p;
+  float scale;
+  __device__ __forceinline__ void ld(int c, float& a, float& b, float& d, float& e) const {
+    const float4 v = p[c];
+    if (INV) { a = v.y; b = v.x; d = v.w; e = v.z; }
+    else { a = v.x; b = v.y; d = v.z; e = v.w; }
+  }
+  __device__ __forceinline__ void st(int c, float a, float b, float d, float e) const {
+    using A = Arith<float>;
+    if (INV) p[c] = make_float4(A::mul(b, scale), A::mul(a, scale), A::mul(e, scale), A::mul(d, scale));
+    else p[c] = make_float4(a, b, d, e);
+  }
+};
+template <bool INV> struct RowIO<double, INV> {
+  double2* p;
+  double scale;
+  __device__ __forceinline__ void ld(int c, double& a, double& b) const {
+    const double2 v = p[c];
+    if (INV) { a = v.y; b = v.x; }
+    else { a = v.x; b = v.y; }
+  }
+  __device__ __forceinline__ void st(int c, double a, double b) const {
+    using A = Arith<double>;
+    if (INV) p[c] = make_double2(A::mul(b, scale), A::mul(a, scale));
+    else p[c] = make_double2(a, b);
+  }
+};
+
+// Global-memory variant: the input comes from `in`, the output goes to `out`.
+template <typename R, bool INV> struct GRowIO;
+template <bool INV> struct GRowIO<float, INV> {
+  const float4* __restrict__ pi;
+  float4* __restrict__ po;
+  float scale;
+  __device__ __forceinline__ void ld(int c, float& a, float& b, float& d, float& e) const {
+    const float4 v = __ldg(pi + c);
+    if (INV) { a = v.y; b = v.x; d = v.w; e = v.z; }
+    else { a = v.x; b = v.y; d = v.z; e = v.w; }
+  }
+  __device__ __forceinline__ void st(int c, float a, float b, float d, float e) const {
+    using A = Arith<float>;
+    if (INV) __stcs(po + c, make_float4(A::mul(b, scale), A::mul(a, scale), A::mul(e, scale), A::mul(d, scale)));
+    else __stcs(po + c, make_float4(a, b, d, e));
+  }
+};
+template <bool INV> struct GRowIO<double, INV> {
+  const double2* __restrict__ pi;
+  double2* __restrict__ po;
+  double scale;
+  __device__ __forceinline__ void ld(int c, double& a, double& b) const {
+    const double2 v = __ldg(pi + c);
+    if (INV) { a = v.y; b = v.x; }
+    else { a = v.x; b = v.y; }
+  }
+  __device__ __forceinline__ void st(int c, double a, double b) const {
+    using A = Arith<double>;
+    if (INV) __stcs(po + c, make_double2(A::mul(b, scale), A::mul(a, scale)));
+    else __stcs(po + c, make_double2(a, b));
+  }
+};
+
+__device__ __forceinline__ uint32_t s_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+template <typename R, int LOGN>
+struct SCfg {
+  static constexpr int N = 1 << LOGN;
+  static constexpr int NT = (N < 8 ? 8 : N) / 4;      // constant table (Nmax = max(N, 8))
+  static constexpr int ROWB = 2 * N * static_cast<int>(sizeof(R));
+  static constexpr bool DIRECT = ROWB <= 64;   // measured: 128-B rows are faster staged
+  static constexpr int STRIDE = ROWB + 16;             // padded slot (bytes)
+  static constexpr int T = 128;                        // rows (threads) per CTA
+  static constexpr size_t SMEM = DIRECT ? 0 : static_cast<size_t>(T) * STRIDE + 16;
+};
+
+template <int V, typename R, int LOGN, bool INV>
+__global__ void __launch_bounds__(128)
+k_small(const R* __restrict__ in, R* __restrict__ out, size_t rows,
+        const __grid_constant__ TabP<R, SCfg<R, LOGN>::NT> tp, R scale) {
+  using C = SCfg<R, LOGN>;
+  using G = SmallGen<V, 0, LOGN, R>;
+  using VT = typename Vec<R>::T;
+  constexpr int N = C::N;
+  const int tid = threadIdx.x;
+  if constexpr (C::DIRECT) {
+    for (size_t row = blockIdx.x * size_t(C::T) + tid; row < rows; row += size_t(gridDim.x) * C::T) {
+      GRowIO<R, INV> io{reinterpret_cast<const VT*>(in + row * 2 * N), reinterpret_cast<VT*>(out + row * 2 * N),
+                        scale};
+      G::template run<Arith<R>>(io, tp.v);
+    }
+  } else {
+    extern __shared__ __align__(128) unsigned char sm[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + size_t(C::T) * C::STRIDE);
+    const int warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(bar)), "r"(1) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t parity = 0;
+    const size_t tiles = (rows + C::T - 1) / C::T;
+    for (size_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      const size_t row0 = tile * C::T;
+      const int nr = static_cast<int>(rows - row0 < size_t(C::T) ? rows - row0 : size_t(C::T));
+      if (warp == 0) {
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                       ::"r"(s_u32(bar)), "r"(static_cast<uint32_t>(nr * C::ROWB)) : "memory");
+        __syncwarp();
+        for (int r = lane; r < nr; r += 32)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+              ::"r"(s_u32(sm + size_t(r) * C::STRIDE)), "l"(in + (row0 + r) * 2 * N), "r"(C::ROWB),
+                "r"(s_u32(bar)) : "memory");
+      }
+      asm volatile(
+          "{\n\t.reg .pred p;\n"
+          "WAIT_%=:\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+          "@!p bra WAIT_%=;\n}" ::"r"(s_u32(bar)), "r"(parity) : "memory");
+      parity ^= 1;
+      if (tid < nr) {
+        RowIO<R, INV> io{reinterpret_cast<VT*>(sm + size_t(tid) * C::STRIDE), scale};
+        G::template run<Arith<R>>(io, tp.v);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      if (warp == 0) {
+        for (int r = lane; r < nr; r += 32)
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                       ::"l"(out + (row0 + r) * 2 * N), "r"(s_u32(sm + size_t(r) * C::STRIDE)), "r"(C::ROWB)
+                       : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      }
+      __syncthreads();
+    }
+    if (warp == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+}
+
+template <int V, typename R, int LOGN>
+class SmallPlanImpl final : public FastPlan {
+  using C = SCfg<R, LOGN>;
+
+ public:
+  SmallPlanImpl(const void* tab, uint32_t nmax, int device) {
+    // the generated slots index the Nmax = max(N, 8) table; a larger table
+    // holds the same values at slot (s + 1) nmax / Nsmall - 1 (TrigTable
+    // level sharing, variants.cpp:281)
+    const int nsm = C::NT * 4;
+    std::vector<R> big(nmax / 4);
+    cudaError_t e = cudaMemcpy(big.data(), tab, sizeof(R) * big.size(), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+    const uint32_t ratio = nmax / static_cast<uint32_t>(nsm);
+    for (int s = 0; s < C::NT; ++s) tp_.v[s] = big[(s + 1) * ratio - 1];
+    auto f0 = k_small<V, R, LOGN, false>;
+    auto f1 = k_small<V, R, LOGN, true>;
+    if (C::SMEM > 48 * 1024) {
+      e = cudaFuncSetAttribute(f0, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM));
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM));
+      if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+    }
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f0, C::T, C::SMEM);
+    if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    grid_cap_ = std::max(1, per_sm) * sms;
+    launches = 1;
+  }
+  void exec(const void* in, void* out, size_t rows, int inverse, cudaStream_t st) override {
+    const size_t tiles = (rows + C::T - 1) / C::T;
+    const unsigned grid = static_cast<unsigned>(std::min<size_t>(tiles, static_cast<size_t>(grid_cap_)));
+    const R scale = R(1) / R(C::N);
+    if (inverse)
+      k_small<V, R, LOGN, true><<<grid, C::T, C::SMEM, st>>>(static_cast<const R*>(in), static_cast<R*>(out), rows,
+                                                             tp_, scale);
+    else
+      k_small<V, R, LOGN, false><<<grid, C::T, C::SMEM, st>>>(static_cast<const R*>(in), static_cast<R*>(out), rows,
+                                                              tp_, scale);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+  }
+
+ private:
+  TabP<R, C::NT> tp_{};
+  int grid_cap_ = 148;
+};
+
+template <int V, typename R>
+std::unique_ptr<FastPlan> make_small_sized(size_t n, const void* tab, uint32_t nmax, int dev) {
+  switch (n) {
+    case 2: return std::make_unique<SmallPlanImpl<V, R, 1>>(tab, nmax, dev);
+    case 4: return std::make_unique<SmallPlanImpl<V, R, 2>>(tab, nmax, dev);
+    case 8: return std::make_unique<SmallPlanImpl<V, R, 3>>(tab, nmax, dev);
+    case 16: return std::make_unique<SmallPlanImpl<V, R, 4>>(tab, nmax, dev);
+    case 32: return std::make_unique<SmallPlanImpl<V, R, 5>>(tab, nmax, dev);
+    case 64:
+      if constexpr (sizeof(R) == 4) return std::make_unique<SmallPlanImpl<V, R, 6>>(tab, nmax, dev);
+      break;
+  }
+  return nullptr;
+}
+
+}  // namespace smallk
+}  // namespace amqft_b200

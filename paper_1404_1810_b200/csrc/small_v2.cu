@@ -1,0 +1,9 @@
+// small_v2.cu -- one-thread-per-row kernel instances for AM-QFT variant 2.
+#include "small_kernel.cuh"
+
+namespace amqft_b200 {
+namespace smallk {
+template std::unique_ptr<FastPlan> make_small_sized<2, float>(size_t, const void*, uint32_t, int);
+template std::unique_ptr<FastPlan> make_small_sized<2, double>(size_t, const void*, uint32_t, int);
+}  // namespace smallk
+}  // namespace amqft_b200

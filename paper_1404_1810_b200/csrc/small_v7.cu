@@ -1,0 +1,9 @@
+// small_v7.cu -- one-thread-per-row kernel instances for AM-QFT variant 7.
+#include "small_kernel.cuh"
+
+namespace amqft_b200 {
+namespace smallk {
+template std::unique_ptr<FastPlan> make_small_sized<7, float>(size_t, const void*, uint32_t, int);
+template std::unique_ptr<FastPlan> make_small_sized<7, double>(size_t, const void*, uint32_t, int);
+}  // namespace smallk
+}  // namespace amqft_b200

@@ -494,3 +494,63 @@ def test_config2_full_size_properties(v):
     assert lin < 2 * tol, lin
     rt = ((back - x).double().norm(dim=1) / x.double().norm(dim=1)).max().item()
     assert rt < 2 * tol, rt
+
+
+# ---- one-thread-per-row kernel (path 4, small_kernel.cuh): small CDFTs
+SMALL_SIZES = {"f64": (2, 4, 8, 16, 32), "f32": (2, 4, 8, 16, 32, 64)}
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_small_kernel_parity(oracle, restatement, dtype):
+    """fp64: bitwise the oracle, forward and swap-trick inverse, all 8
+    variants; fp32: bitwise the fp32 exact-order generic path (same ops, same
+    order) and within 1e-5 log2 N of the fp64 oracle for variants 1-4.  300
+    rows = two full 128-row tiles + a partial one (TMA path) / grid-stride
+    rows (direct path)."""
+    r, O = restatement, oracle
+    rows = 300
+    for n in SMALL_SIZES[dtype]:
+        rng = np.random.default_rng(n)
+        xs = rng.uniform(-1, 1, (rows, 2 * n))
+        if dtype == "f32":
+            xs = xs.astype(np.float32).astype(np.float64)
+        for v in range(1, 9):
+            plan = amqft.Plan(v, amqft.FunctionId.Cdft, n, rows, dtype=dtype, order=amqft.Order.Fast)
+            assert plan.path()[0] == 4, (v, n)
+            got = run_plan(plan, xs)
+            inv = run_plan(plan, xs, inverse=True)
+            assert plan.op_counts() == r.execute(v, O.F_CDFT, n, xs[0], meter=True)[1]
+            if dtype == "f64":
+                for row in (0, 127, 128, 299):
+                    assert got[row].tobytes() == r.execute(v, O.F_CDFT, n, xs[row]).tobytes(), (v, n, row)
+                    assert inv[row].tobytes() == r.inverse_cdft(v, n, xs[row]).tobytes(), (v, n, row)
+            else:
+                ex = amqft.Plan(v, amqft.FunctionId.Cdft, n, rows, dtype="f32", order=amqft.Order.Exact)
+                assert ex.path()[0] == 0
+                assert got.tobytes() == run_plan(ex, xs).tobytes(), (v, n)
+                assert inv.tobytes() == run_plan(ex, xs, inverse=True).tobytes(), (v, n)
+                if v <= 4:
+                    for row in (0, 299):
+                        want = r.execute(v, O.F_CDFT, n, xs[row])
+                        assert r.rel_l2(got[row], want) <= 1e-5 * max(1, math.log2(n)), (v, n)
+
+
+def test_small_kernel_large_batch_round_trip():
+    """Config-3 shape at N = 16 (2^22 rows, 1 GiB fp64): forward then inverse
+    returns the input (size-independent property), and rows are independent
+    (a row transformed alone equals the same row in the batch)."""
+    n, rows = 16, 1 << 22
+    g = torch.Generator(device=DEV).manual_seed(3)
+    x = torch.rand(rows, 2 * n, dtype=torch.float64, device=DEV, generator=g) * 2 - 1
+    y = torch.empty_like(x)
+    z = torch.empty_like(x)
+    plan = amqft.Plan(4, amqft.FunctionId.Cdft, n, rows, dtype="f64", order=amqft.Order.Fast)
+    plan.forward(x, y)
+    plan.inverse(y, z)
+    torch.cuda.synchronize()
+    assert float((z - x).norm() / x.norm()) < 1e-15
+    one = amqft.Plan(4, amqft.FunctionId.Cdft, n, 1, dtype="f64", order=amqft.Order.Fast)
+    y1 = torch.empty(1, 2 * n, dtype=torch.float64, device=DEV)
+    one.forward(x[rows - 1:].contiguous(), y1)
+    torch.cuda.synchronize()
+    assert torch.equal(y1[0], y[rows - 1])
