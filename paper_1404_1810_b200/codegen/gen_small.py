@@ -19,7 +19,8 @@ same chunk of 8 different rows hit 8 different 16-byte bank groups.  The
 row is transformed in place: a chunk is stored only once all its cells are
 final, and never before its input cells were loaded.
 
-  python3 paper_1404_1810_b200/codegen/gen_small.py > paper_1404_1810_b200/csrc/small_gen.cuh
+Run by csrc/Makefile at build time (the output is not committed):
+  python3 codegen/gen_small.py --lib csrc/build/libamqft_plan.so --out csrc/gen
 """
 from __future__ import annotations
 
@@ -37,6 +38,9 @@ FL_DESC, FL_ADD = 4, 8
 
 # Sizes covered per dtype (register budget: the live set of one thread).
 SIZES = {"float": (2, 4, 8, 16, 32, 64), "double": (2, 4, 8, 16, 32)}
+# Cooperative rows: N -> (head stages, tail stages, warp roles)
+COOP = {"float": {128: (2, 2, 4), 256: (3, 3, 8), 512: (4, 4, 16)},
+        "double": {64: (2, 2, 4), 128: (3, 3, 8), 256: (4, 4, 16)}}
 
 
 def _items(op, n):
@@ -205,15 +209,46 @@ def _chain(T, e, L):
     return out
 
 
+_PLANLIB = None
+
+
+def _schedule_dump(v, f, n):
+    """The plan compiler's single-CTA stage program.  At build time from the
+    host-only library build/libamqft_plan.so (plan.cpp, no CUDA), else
+    through the package."""
+    if _PLANLIB is None:
+        import paper_1404_1810_b200 as amqft
+        return amqft.schedule_dump(v, f, n)
+    import ctypes as C
+    import numpy as np
+    from paper_1404_1810_b200 import EI_DTYPE
+    L = _PLANLIB
+    cnt, nst = C.c_size_t(), C.c_size_t()
+    st0 = L.amqft_schedule_dump(v, f, n, 1 << 20, None, 0, C.byref(cnt), None, 0, C.byref(nst), None)
+    assert st0 == 0
+    recs = np.zeros(cnt.value, dtype=EI_DTYPE)
+    st = np.zeros(2 * nst.value, dtype=np.uint32)
+    ops = (C.c_uint64 * 3)()
+    st0 = L.amqft_schedule_dump(v, f, n, 1 << 20, C.c_void_p(recs.ctypes.data), recs.size, C.byref(cnt),
+                                C.c_void_p(st.ctypes.data), nst.value, C.byref(nst), ops)
+    assert st0 == 0
+    return recs, st.reshape(-1, 2), tuple(int(x) for x in ops)
+
+
 def trace(v, f, n):
     """(Trace, outputs): outputs[p] = node holding output cell p."""
-    import paper_1404_1810_b200 as amqft
-    recs, stages, ops = amqft.schedule_dump(v, f, n)
+    recs, stages, ops = _schedule_dump(v, f, n)
     nmax = max(n, 8)
-    cells = amqft.cell_count(f, n)
+    cells = 2 * n if f == 0 else None
+    if cells is None:
+        import paper_1404_1810_b200 as amqft
+        cells = amqft.cell_count(f, n)
     T = Trace(cells)
+    T.stage = [-1] * cells
+    T.snap = [list(range(cells))]        # arena after each stage
     x = list(range(cells))
-    for b, e in stages:
+    for si, (b, e) in enumerate(stages):
+        first = len(T.nodes)
         writes = []
         for k in range(int(b), int(e)):
             r = recs[k]
@@ -228,6 +263,8 @@ def trace(v, f, n):
                     writes.append((off + i, _item(T, ei[:5], i, L, nmax)))
         for p, node in writes:
             x[p] = node
+        T.stage += [si] * (len(T.nodes) - first)
+        T.snap.append(list(x))
     return T, x, ops
 
 
@@ -432,20 +469,297 @@ def emit_fn(v, f, n, R):
     return "\n".join(lines)
 
 
+# ---------------------------------------------------------------------------
+# Cooperative rows (N too large for one thread's registers): R warp roles per
+# 32-row tile, lane = row.  The stage program is cut into three bands:
+#   head   stages [0, hd)       SplitComplex/SplitReal (+ first splits)
+#   middle stages [hd, S - td)  independent subtrees (connected components)
+#   tail   stages [S - td, S)   the last recombinations
+# Band B (head + middle): each role loads the input chunks of its subtrees'
+# head cones, computes the head ops it needs (recomputed where two roles
+# share a head value), barrier, runs its subtrees and stores the values the
+# tail reads at their arena positions (the cut).  Band C (tail): each role
+# loads the cut chunks its output chunks need, barrier, computes and stores
+# whole output chunks.  Same nodes as the trace, so still bitwise.
+
+
+class UF:
+    def __init__(self):
+        self.p = {}
+
+    def find(self, a):
+        self.p.setdefault(a, a)
+        while self.p[a] != a:
+            self.p[a] = self.p[self.p[a]]
+            a = self.p[a]
+        return a
+
+    def union(self, a, b):
+        ra, rb = self.find(a), self.find(b)
+        if ra != rb:
+            self.p[max(ra, rb)] = min(ra, rb)
+
+
+def _operands(nd):
+    return [nd[1], nd[2]] if nd[0] in ("add", "sub") else ([nd[1]] if nd[0] in ("mul", "half") else [])
+
+
+def _cone(T, roots, stop):
+    """Nodes reachable from roots through operands, not descending below
+    nodes for which stop(u) is true (those are included)."""
+    seen, stack = set(), list(roots)
+    while stack:
+        u = stack.pop()
+        if u in seen:
+            continue
+        seen.add(u)
+        if not stop(u):
+            stack += _operands(T.nodes[u])
+    return seen
+
+
+def _pack(items, R):
+    """LPT: items = [(weight, payload)] -> R bins of payloads."""
+    bins = [[0, []] for _ in range(R)]
+    for w, pl in sorted(items, key=lambda t: -t[0]):
+        b = min(bins, key=lambda t: t[0])
+        b[0] += w
+        b[1].append(pl)
+    return [b[1] for b in bins]
+
+
+def plan_roles(T, outs, hd, td, W, R):
+    S = len(T.snap) - 1
+    band = lambda u: "H" if T.stage[u] < hd else ("T" if T.stage[u] >= S - td else "M")  # noqa: E731
+    need = _cone(T, outs, lambda u: False)
+    cut = T.snap[S - td]
+    where = {}
+    for q, u in enumerate(cut):
+        where.setdefault(u, q)
+    # middle components
+    uf = UF()
+    mids = [u for u in sorted(need) if band(u) == "M"]
+    for u in mids:
+        uf.find(u)
+        for o in _operands(T.nodes[u]):
+            if band(o) == "M":
+                uf.union(u, o)
+    comps = {}
+    for u in mids:
+        comps.setdefault(uf.find(u), []).append(u)
+    # tail: one unit per output chunk; tail intermediates shared by two
+    # chunks are recomputed by both (unioning them chains every chunk of a
+    # time-major chain recombination into one component)
+    nch = len(outs) // W
+    tail_units = []
+    for c in range(nch):
+        outs_c = [outs[p] for p in range(c * W, c * W + W)]
+        cone = _cone(T, outs_c, lambda z: band(z) != "T")
+        tnodes = sorted(w for w in cone if band(w) == "T")
+        reads = sorted({w for w in cone if band(w) != "T"})
+        tail_units.append((len(tnodes) + len(reads), ([c], tnodes, reads)))
+    troles = _pack(tail_units, R)
+    # cut values the tail reads -> stored by band B at position where[v]
+    cut_reads = sorted({v for _, (ch, tn, rd) in tail_units for v in rd})
+    for v in cut_reads:
+        assert v in where, "tail operand not in the arena at the cut"
+    # band-B roles: middle components (+ head/input values to be stored)
+    units = [(len(m), ("m", m)) for m in comps.values()]
+    broles = _pack(units, R)
+    owner = {}
+    for r, lst in enumerate(broles):
+        for _, m in lst:
+            for u in m:
+                owner[u] = r
+    stores = [[] for _ in range(R)]
+    load = [sum(len(m) for _, m in lst) for lst in broles]
+    for v in cut_reads:
+        if band(v) == "M":
+            r = owner[v]
+        else:   # a head value / an input passing through: least-loaded role
+            r = min(range(R), key=lambda k: load[k])
+            load[r] += 1
+        stores[r].append(v)
+    return dict(band=band, cut=cut, where=where, broles=broles, stores=stores, troles=troles, S=S)
+
+
+def emit_roles(v, n, R_t, hd, td, R):
+    W = 4 if R_t == "float" else 2
+    T, outs, ops = trace(v, 0, n)
+    P = plan_roles(T, outs, hd, td, W, R)
+    band, where = P["band"], P["where"]
+    name = lambda u: (f"x{u}" if T.nodes[u][0] == "in" else f"t{u}")  # noqa: E731
+
+    def op_line(u):
+        nd = T.nodes[u]
+        if nd[0] == "add":
+            ex = f"AR::add({name(nd[1])}, {name(nd[2])})"
+        elif nd[0] == "sub":
+            ex = f"AR::sub({name(nd[1])}, {name(nd[2])})"
+        elif nd[0] == "mul":
+            ex = f"AR::mul({name(nd[1])}, tab[{nd[2]}])"
+        else:
+            ex = f"AR::mul({R_t}(0.5), {name(nd[1])})"
+        return f"    const {R_t} t{u} = {ex};"
+
+    fns, peaks = [], []
+    # position -> role that stores it (for chunk ownership)
+    pos_owner = {}
+    for r in range(R):
+        for val in P["stores"][r]:
+            pos_owner[where[val]] = r
+    for r in range(R):
+        mids = sorted(u for _, m in P["broles"][r] for u in m)
+        st_vals = P["stores"][r]
+        head_roots = [o for u in mids for o in _operands(T.nodes[u]) if band(o) == "H"]
+        head_roots += [val for val in st_vals if band(val) == "H"]
+        head = sorted(_cone(T, head_roots, lambda z: band(z) != "H"))
+        lines = [f"  template <class AR, class IO>",
+                 f"  static __device__ __forceinline__ void b{r}(IO& io, const {R_t}* __restrict__ tab) {{"]
+        loaded = set()
+        live = 0
+        for u in head:
+            nd = T.nodes[u]
+            if nd[0] == "in":
+                c = nd[1] // W
+                if c not in loaded:
+                    loaded.add(c)
+                    nm = ", ".join(f"x{p}" for p in range(c * W, c * W + W))
+                    lines.append(f"    {R_t} {nm}; io.ld({c}, {nm});")
+            else:
+                lines.append(op_line(u))
+        lines.append("    io.sync();")
+        # stores: chunks owned entirely (among needed positions) -> vector
+        my_pos = {where[val]: val for val in st_vals}
+        chunk_vec = set()
+        for q in my_pos:
+            c = q // W
+            if all(pos_owner.get(p, r) == r for p in range(c * W, c * W + W)):
+                chunk_vec.add(c)
+        pending = {c: set(p for p in range(c * W, c * W + W) if p in my_pos) for c in chunk_vec}
+        ready = set(u for u in head) | set()
+        emitted_st = set()
+
+        def try_store(val):
+            q = where[val]
+            c = q // W
+            if c in chunk_vec:
+                pending[c].discard(q)
+                if not pending[c] and c not in emitted_st:
+                    emitted_st.add(c)
+                    vals = []
+                    for p in range(c * W, c * W + W):
+                        vals.append(name(my_pos[p]) if p in my_pos else f"{R_t}(0)")
+                    lines.append(f"    io.str({c}, {', '.join(vals)});")
+            else:
+                lines.append(f"    io.st1({q}, {name(val)});")
+
+        for val in st_vals:            # head values / inputs stored as they are
+            if band(val) == "H":
+                try_store(val)
+        sv = set(st_vals)
+        for u in mids:
+            lines.append(op_line(u))
+            if u in sv:
+                try_store(u)
+        lines.append("    io.sync();")
+        lines.append("  }")
+        fns.append("\n".join(lines))
+        peaks.append(len(mids))
+    for r in range(R):
+        units = P["troles"][r]
+        lines = [f"  template <class AR, class IO>",
+                 f"  static __device__ __forceinline__ void c{r}(IO& io, const {R_t}* __restrict__ tab) {{"]
+        reads = sorted({val for chunks, tn, rd in units for val in rd})
+        chunks_needed = sorted({where[val] // W for val in reads})
+        for c in chunks_needed:
+            nm = ", ".join(f"y{p}" for p in range(c * W, c * W + W))
+            lines.append(f"    {R_t} {nm}; io.ldr({c}, {nm});")
+        lines.append("    io.sync();")
+        # alias: value name -> the cut register
+        alias = {val: f"y{where[val]}" for val in reads}
+        nm2 = lambda u: alias.get(u, name(u))  # noqa: E731
+        tnodes = sorted({u for chunks, tn, rd in units for u in tn})
+        for u in tnodes:
+            nd = T.nodes[u]
+            if nd[0] == "add":
+                ex = f"AR::add({nm2(nd[1])}, {nm2(nd[2])})"
+            elif nd[0] == "sub":
+                ex = f"AR::sub({nm2(nd[1])}, {nm2(nd[2])})"
+            elif nd[0] == "mul":
+                ex = f"AR::mul({nm2(nd[1])}, tab[{nd[2]}])"
+            else:
+                ex = f"AR::mul({R_t}(0.5), {nm2(nd[1])})"
+            lines.append(f"    const {R_t} t{u} = {ex};")
+        for chunks, tn, rd in units:
+            for c in chunks:
+                lines.append(f"    io.st({c}, " + ", ".join(nm2(outs[p]) for p in range(c * W, c * W + W)) + ");")
+        lines.append("  }")
+        fns.append("\n".join(lines))
+    body = [f"template <> struct SmallRoles<{v}, {n.bit_length() - 1}, {R_t}> {{",
+            f"  static constexpr int R = {R};",
+            f"  static constexpr unsigned long long OPS[3] = {{{ops[0]}ull, {ops[1]}ull, {ops[2]}ull}};"]
+    body += fns
+    body.append("  template <class AR, class IO>")
+    body.append(f"  static __device__ __forceinline__ void run(int role, IO& io, const {R_t}* __restrict__ tab) {{")
+    body.append("    switch (role) {")
+    for r in range(R):
+        body.append(f"      case {r}: b{r}<AR>(io, tab); c{r}<AR>(io, tab); break;")
+    body += ["    }", "  }", "};"]
+    return "\n".join(body), P, peaks
+
+
+HEAD = ["#pragma once",
+        "namespace amqft_b200 {",
+        "namespace smallk {",
+        "template <int V, int F, int LOGN, typename R> struct SmallGen;",
+        "template <int V, int LOGN, typename R> struct SmallRoles;"]
+TAIL = ["}  // namespace smallk", "}  // namespace amqft_b200", ""]
+
+
 def main():
-    out = ["// small_gen.cuh -- GENERATED by codegen/gen_small.py; do not edit.",
-           "// One whole CDFT per thread: the traced AM-QFT stage program of plan.cpp as",
-           "// straight-line code (one reference add/sub/mul per line).",
-           "#pragma once",
-           "namespace amqft_b200 {",
-           "namespace smallk {",
-           "template <int V, int F, int LOGN, typename R> struct SmallGen;"]
-    for R, sizes in SIZES.items():
-        for n in sizes:
-            for v in range(1, 9):
+    """Writes <out>/small_gen_v<V>.cuh (code) and <out>/small_ops.cuh (op
+    counts per instance, for the plan's meter)."""
+    import argparse
+    import ctypes
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--lib", help="host-only plan library (libamqft_plan.so)")
+    ap.add_argument("--out", required=True)
+    a = ap.parse_args()
+    global _PLANLIB
+    if a.lib:
+        _PLANLIB = ctypes.CDLL(a.lib)
+        _PLANLIB.amqft_schedule_dump.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_size_t, ctypes.c_size_t,
+                                                 ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
+                                                 ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
+                                                 ctypes.c_void_p]
+    os.makedirs(a.out, exist_ok=True)
+    ops_lines = ["// GENERATED by codegen/gen_small.py: op counts of the generated small kernels.",
+                 "#pragma once", "namespace amqft_b200 {", "namespace smallk {",
+                 "// {adds, muls, halvings} for CDFT variant V, log2 N, dtype (0 fp32, 1 fp64); 0 = not covered",
+                 "struct SmallOps { int v, logn, f64; unsigned long long a, m, b; };",
+                 "static constexpr SmallOps kSmallOps[] = {"]
+    for v in range(1, 9):
+        out = [f"// small_gen_v{v}.cuh -- GENERATED by codegen/gen_small.py; do not edit.",
+               "// Small CDFTs of AM-QFT variant %d: the traced stage program of plan.cpp as" % v,
+               "// straight-line code (one reference add/sub/mul per line)."] + HEAD
+        for R, sizes in SIZES.items():
+            for n in sizes:
                 out.append(emit_fn(v, 0, n, R))
-    out += ["}  // namespace smallk", "}  // namespace amqft_b200", ""]
-    sys.stdout.write("\n".join(out))
+                _, _, ops = trace(v, 0, n)
+                ops_lines.append(f"  {{{v}, {n.bit_length() - 1}, {int(R == 'double')}, {ops[0]}ull, {ops[1]}ull, {ops[2]}ull}},")
+        for R, cfg in COOP.items():
+            for n, (hd, td, nr) in cfg.items():
+                code, _, _ = emit_roles(v, n, R, hd, td, nr)
+                out.append(code)
+                _, _, ops = trace(v, 0, n)
+                ops_lines.append(f"  {{{v}, {n.bit_length() - 1}, {int(R == 'double')}, {ops[0]}ull, {ops[1]}ull, {ops[2]}ull}},")
+        out += TAIL
+        with open(os.path.join(a.out, f"small_gen_v{v}.cuh"), "w") as f:
+            f.write("\n".join(out))
+    ops_lines += ["};", "}  // namespace smallk", "}  // namespace amqft_b200", ""]
+    with open(os.path.join(a.out, "small_ops.cuh"), "w") as f:
+        f.write("\n".join(ops_lines))
 
 
 if __name__ == "__main__":

@@ -2,7 +2,7 @@
 // per-variant instances: fast_v1.cu .. fast_v8.cu).
 #include "fast.cuh"
 #include "fourstep.cuh"
-#include "small_gen.cuh"
+#include "gen/small_ops.cuh"
 
 namespace amqft_b200 {
 namespace fastk {
@@ -50,33 +50,21 @@ namespace smallk {
 template <int V, typename R>
 std::unique_ptr<FastPlan> make_small_sized(size_t n, const void* tab, uint32_t nmax, int dev);
 
-template <int V, typename R, int LOGN>
-bool small_ops(OpCount* o) {
-  using G = SmallGen<V, 0, LOGN, R>;
-  o->adds = G::OPS[0];
-  o->muls = G::OPS[1];
-  o->bt = G::OPS[2];
-  return true;
-}
-template <int V, typename R>
-bool small_ops_n(size_t n, OpCount* o) {
-  switch (n) {
-    case 2: return small_ops<V, R, 1>(o);
-    case 4: return small_ops<V, R, 2>(o);
-    case 8: return small_ops<V, R, 3>(o);
-    case 16: return small_ops<V, R, 4>(o);
-    case 32: return small_ops<V, R, 5>(o);
-    case 64:
-      if constexpr (sizeof(R) == 4) return small_ops<V, R, 6>(o);
-      break;
-  }
+bool small_ops_n(int v, size_t n, bool f64, OpCount* o) {
+  for (const SmallOps& e : kSmallOps)
+    if (e.v == v && (size_t(1) << e.logn) == n && e.f64 == static_cast<int>(f64)) {
+      o->adds = e.a;
+      o->muls = e.m;
+      o->bt = e.b;
+      return true;
+    }
   return false;
 }
 template <typename R>
 std::unique_ptr<FastPlan> make_small_typed(int v, size_t n, const void* tab, uint32_t nmax, int dev, OpCount* o) {
   switch (v) {
 #define AMQFT_SMALL_CASE(V) \
-  case V: if (!small_ops_n<V, R>(n, o)) return nullptr; return make_small_sized<V, R>(n, tab, nmax, dev);
+  case V: if (!small_ops_n(V, n, sizeof(R) == 8, o)) return nullptr; return make_small_sized<V, R>(n, tab, nmax, dev);
     AMQFT_SMALL_CASE(1) AMQFT_SMALL_CASE(2) AMQFT_SMALL_CASE(3) AMQFT_SMALL_CASE(4)
     AMQFT_SMALL_CASE(5) AMQFT_SMALL_CASE(6) AMQFT_SMALL_CASE(7) AMQFT_SMALL_CASE(8)
 #undef AMQFT_SMALL_CASE

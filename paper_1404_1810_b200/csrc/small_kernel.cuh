@@ -1,6 +1,6 @@
-// small_kernel.cuh -- one whole small CDFT per thread (path 4).
+// small_kernel.cuh -- small CDFTs, one row per thread (path 4).
 //
-// For N <= 64 (fp32) / N <= 32 (fp64) a thread owns one row: the traced
+// k_small: for N <= 64 (fp32) / N <= 32 (fp64) a thread owns one row: the traced
 // stage program of the plan compiler, emitted as straight-line code by
 // codegen/gen_small.py (small_gen.cuh), keeps the row in registers.  Every
 // line is one reference add/sub/mul on the reference operands (no FMA
@@ -16,6 +16,8 @@
 //    a quarter-warp reading the same 16-byte chunk of 8 rows hit 8 distinct
 //    bank groups), transformed in place, and written back by one bulk store
 //    per row.
+// k_coop (below): N = 128..512 (fp32) / 64..256 (fp64), a row per lane and
+// one warp per subtree role.
 // The inverse is the swap trick (x = swap(DFT(swap(X))) / N), fused into the
 // chunk loads and stores.
 #pragma once
@@ -24,13 +26,18 @@
 #include <algorithm>
 #include <memory>
 #include <stdexcept>
+#include <vector>
 
 #include "fast.cuh"
 #include "generic.cuh"
-#include "small_gen.cuh"
 
 namespace amqft_b200 {
 namespace smallk {
+
+// generated per variant (codegen/gen_small.py -> gen/small_gen_v<V>.cuh,
+// included by small_v<V>.cu before this header)
+template <int V, int F, int LOGN, typename R> struct SmallGen;
+template <int V, int LOGN, typename R> struct SmallRoles;
 
 template <typename R, int K>
 struct TabP {
@@ -186,6 +193,150 @@ k_small(const R* __restrict__ in, R* __restrict__ out, size_t rows,
   }
 }
 
+// ---- Cooperative rows (fp32 N = 128..512, fp64 N = 64..256): a 32-row
+// tile per CTA, lane = row, one warp per generated role
+// (SmallRoles<V, LOGN, R>::run).  Band B: a role loads the input chunks of
+// its subtrees, barrier, runs them, stores the values the tail reads at
+// their arena positions; band C: loads those chunks, barrier, computes and
+// stores whole output chunks.  The barriers are named (bar.sync 1) and
+// reached from every role's own code path.
+template <typename R, bool INV, int NTH> struct CoopIO;
+template <bool INV, int NTH> struct CoopIO<float, INV, NTH> : RowIO<float, INV> {
+  __device__ __forceinline__ void ldr(int c, float& a, float& b, float& d, float& e) const {
+    const float4 v = this->p[c];
+    a = v.x; b = v.y; d = v.z; e = v.w;
+  }
+  __device__ __forceinline__ void str(int c, float a, float b, float d, float e) const {
+    this->p[c] = make_float4(a, b, d, e);
+  }
+  __device__ __forceinline__ void st1(int q, float a) const { reinterpret_cast<float*>(this->p)[q] = a; }
+  __device__ __forceinline__ void sync() const { asm volatile("bar.sync 1, %0;" ::"n"(NTH) : "memory"); }
+};
+template <bool INV, int NTH> struct CoopIO<double, INV, NTH> : RowIO<double, INV> {
+  __device__ __forceinline__ void ldr(int c, double& a, double& b) const {
+    const double2 v = this->p[c];
+    a = v.x; b = v.y;
+  }
+  __device__ __forceinline__ void str(int c, double a, double b) const { this->p[c] = make_double2(a, b); }
+  __device__ __forceinline__ void st1(int q, double a) const { reinterpret_cast<double*>(this->p)[q] = a; }
+  __device__ __forceinline__ void sync() const { asm volatile("bar.sync 1, %0;" ::"n"(NTH) : "memory"); }
+};
+
+template <int V, typename R, int LOGN>
+struct CCfg {
+  using G = SmallRoles<V, LOGN, R>;
+  static constexpr int N = 1 << LOGN;
+  static constexpr int NT = N / 4;
+  static constexpr int ROWS = 32;
+  static constexpr int NTH = 32 * G::R;
+  static constexpr int ROWB = 2 * N * static_cast<int>(sizeof(R));
+  static constexpr int STRIDE = ROWB + 16;
+  static constexpr size_t SMEM = static_cast<size_t>(ROWS) * STRIDE + 16;
+};
+
+template <int V, typename R, int LOGN, bool INV>
+__global__ void __launch_bounds__(CCfg<V, R, LOGN>::NTH)
+k_coop(const R* __restrict__ in, R* __restrict__ out, size_t rows,
+       const __grid_constant__ TabP<R, CCfg<V, R, LOGN>::NT> tp, R scale) {
+  using C = CCfg<V, R, LOGN>;
+  using VT = typename Vec<R>::T;
+  constexpr int N = C::N;
+  extern __shared__ __align__(128) unsigned char sm[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + size_t(C::ROWS) * C::STRIDE);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(bar)), "r"(1) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t parity = 0;
+  const size_t tiles = (rows + C::ROWS - 1) / C::ROWS;
+  for (size_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const size_t row0 = tile * C::ROWS;
+    const int nr = static_cast<int>(rows - row0 < size_t(C::ROWS) ? rows - row0 : size_t(C::ROWS));
+    if (warp == 0) {
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                     ::"r"(s_u32(bar)), "r"(static_cast<uint32_t>(nr * C::ROWB)) : "memory");
+      __syncwarp();
+      if (lane < nr)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            ::"r"(s_u32(sm + size_t(lane) * C::STRIDE)), "l"(in + (row0 + lane) * 2 * N), "r"(C::ROWB),
+              "r"(s_u32(bar)) : "memory");
+    }
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(s_u32(bar)), "r"(parity) : "memory");
+    parity ^= 1;
+    // every lane runs (lanes past the tile's rows on stale data, not
+    // stored): the roles' named barriers count all NTH threads
+    CoopIO<R, INV, C::NTH> io;
+    io.p = reinterpret_cast<VT*>(sm + size_t(lane) * C::STRIDE);
+    io.scale = scale;
+    C::G::template run<Arith<R>>(warp, io, tp.v);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) {
+      if (lane < nr)
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                     ::"l"(out + (row0 + lane) * 2 * N), "r"(s_u32(sm + size_t(lane) * C::STRIDE)), "r"(C::ROWB)
+                     : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+    __syncthreads();
+  }
+  if (warp == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+template <int V, typename R, int LOGN>
+class CoopPlanImpl final : public FastPlan {
+  using C = CCfg<V, R, LOGN>;
+
+ public:
+  CoopPlanImpl(const void* tab, uint32_t nmax, int device) {
+    std::vector<R> big(nmax / 4);
+    cudaError_t e = cudaMemcpy(big.data(), tab, sizeof(R) * big.size(), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+    const uint32_t ratio = nmax / static_cast<uint32_t>(C::N);
+    for (int s = 0; s < C::NT; ++s) tp_.v[s] = big[(s + 1) * ratio - 1];
+    auto f0 = k_coop<V, R, LOGN, false>;
+    auto f1 = k_coop<V, R, LOGN, true>;
+    e = cudaFuncSetAttribute(f0, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM));
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM));
+    if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f0, C::NTH, C::SMEM);
+    if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+    if (per_sm < 1) throw std::runtime_error("cooperative small kernel does not fit an SM");
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    grid_cap_ = per_sm * sms;
+    launches = 1;
+  }
+  void exec(const void* in, void* out, size_t rows, int inverse, cudaStream_t st) override {
+    const size_t tiles = (rows + C::ROWS - 1) / C::ROWS;
+    const unsigned grid = static_cast<unsigned>(std::min<size_t>(tiles, static_cast<size_t>(grid_cap_)));
+    const R scale = R(1) / R(C::N);
+    if (inverse)
+      k_coop<V, R, LOGN, true><<<grid, C::NTH, C::SMEM, st>>>(static_cast<const R*>(in), static_cast<R*>(out),
+                                                              rows, tp_, scale);
+    else
+      k_coop<V, R, LOGN, false><<<grid, C::NTH, C::SMEM, st>>>(static_cast<const R*>(in), static_cast<R*>(out),
+                                                               rows, tp_, scale);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+  }
+
+ private:
+  TabP<R, C::NT> tp_{};
+  int grid_cap_ = 148;
+};
+
 template <int V, typename R, int LOGN>
 class SmallPlanImpl final : public FastPlan {
   using C = SCfg<R, LOGN>;
@@ -246,6 +397,11 @@ std::unique_ptr<FastPlan> make_small_sized(size_t n, const void* tab, uint32_t n
     case 32: return std::make_unique<SmallPlanImpl<V, R, 5>>(tab, nmax, dev);
     case 64:
       if constexpr (sizeof(R) == 4) return std::make_unique<SmallPlanImpl<V, R, 6>>(tab, nmax, dev);
+      else return std::make_unique<CoopPlanImpl<V, R, 6>>(tab, nmax, dev);
+    case 128: return std::make_unique<CoopPlanImpl<V, R, 7>>(tab, nmax, dev);
+    case 256: return std::make_unique<CoopPlanImpl<V, R, 8>>(tab, nmax, dev);
+    case 512:
+      if constexpr (sizeof(R) == 4) return std::make_unique<CoopPlanImpl<V, R, 9>>(tab, nmax, dev);
       break;
   }
   return nullptr;

@@ -1,4 +1,5 @@
 // small_v1.cu -- one-thread-per-row kernel instances for AM-QFT variant 1.
+#include "gen/small_gen_v1.cuh"
 #include "small_kernel.cuh"
 
 namespace amqft_b200 {

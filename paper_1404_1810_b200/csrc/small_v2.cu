@@ -1,4 +1,5 @@
 // small_v2.cu -- one-thread-per-row kernel instances for AM-QFT variant 2.
+#include "gen/small_gen_v2.cuh"
 #include "small_kernel.cuh"
 
 namespace amqft_b200 {

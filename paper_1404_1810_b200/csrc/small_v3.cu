@@ -1,4 +1,5 @@
 // small_v3.cu -- one-thread-per-row kernel instances for AM-QFT variant 3.
+#include "gen/small_gen_v3.cuh"
 #include "small_kernel.cuh"
 
 namespace amqft_b200 {

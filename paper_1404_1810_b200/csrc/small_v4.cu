@@ -1,4 +1,5 @@
 // small_v4.cu -- one-thread-per-row kernel instances for AM-QFT variant 4.
+#include "gen/small_gen_v4.cuh"
 #include "small_kernel.cuh"
 
 namespace amqft_b200 {

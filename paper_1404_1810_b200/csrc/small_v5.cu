@@ -1,4 +1,5 @@
 // small_v5.cu -- one-thread-per-row kernel instances for AM-QFT variant 5.
+#include "gen/small_gen_v5.cuh"
 #include "small_kernel.cuh"
 
 namespace amqft_b200 {

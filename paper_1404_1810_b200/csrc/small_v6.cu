@@ -1,4 +1,5 @@
 // small_v6.cu -- one-thread-per-row kernel instances for AM-QFT variant 6.
+#include "gen/small_gen_v6.cuh"
 #include "small_kernel.cuh"
 
 namespace amqft_b200 {

@@ -1,4 +1,5 @@
 // small_v7.cu -- one-thread-per-row kernel instances for AM-QFT variant 7.
+#include "gen/small_gen_v7.cuh"
 #include "small_kernel.cuh"
 
 namespace amqft_b200 {

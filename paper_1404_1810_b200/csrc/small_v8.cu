@@ -1,4 +1,5 @@
 // small_v8.cu -- one-thread-per-row kernel instances for AM-QFT variant 8.
+#include "gen/small_gen_v8.cuh"
 #include "small_kernel.cuh"
 
 namespace amqft_b200 {

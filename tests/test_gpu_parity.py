@@ -497,7 +497,7 @@ def test_config2_full_size_properties(v):
 
 
 # ---- one-thread-per-row kernel (path 4, small_kernel.cuh): small CDFTs
-SMALL_SIZES = {"f64": (2, 4, 8, 16, 32), "f32": (2, 4, 8, 16, 32, 64)}
+SMALL_SIZES = {"f64": (2, 4, 8, 16, 32, 64, 128, 256), "f32": (2, 4, 8, 16, 32, 64, 128, 256, 512)}
 
 
 @pytest.mark.parametrize("dtype", ["f64", "f32"])

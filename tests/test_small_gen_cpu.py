@@ -45,11 +45,64 @@ def test_small_schedule_in_place_safe():
                 assert stored == set(range(2 * n // W))
 
 
-def test_small_gen_header_up_to_date():
-    import io
-    import contextlib
-    buf = io.StringIO()
-    with contextlib.redirect_stdout(buf):
-        G.main()
-    with open(os.path.join(ROOT, "paper_1404_1810_b200", "csrc", "small_gen.cuh")) as f:
-        assert f.read() == buf.getvalue()
+@pytest.mark.parametrize("dtype", ["float", "double"])
+def test_coop_roles_partition(dtype):
+    """Cooperative plans: every middle node belongs to exactly one role,
+    every output chunk to exactly one tail role, and the tail only reads
+    values the band-B roles store at the cut (so the two-band in-place
+    execution computes the traced program)."""
+    W = 4 if dtype == "float" else 2
+    for n, (hd, td, R) in G.COOP[dtype].items():
+        for v in (1, 2, 4, 7):
+            T, outs, _ = G.trace(v, 0, n)
+            P = G.plan_roles(T, outs, hd, td, W, R)
+            mids = [u for lst in P["broles"] for _, m in lst for u in m]
+            assert len(mids) == len(set(mids))
+            chunks = sorted(c for lst in P["troles"] for ch, _, _ in lst for c in ch)
+            assert chunks == list(range(2 * n // W))
+            stored = {x for lst in P["stores"] for x in lst}
+            for lst in P["troles"]:
+                for _, _, rd in lst:
+                    assert set(rd) <= stored
+            assert len(stored) == sum(len(x) for x in P["stores"])
+
+
+def test_coop_two_band_emulation(oracle, restatement):
+    """Execute the cooperative plan band by band on a numpy arena (band B:
+    head cones from the inputs, subtrees, stores at the cut; band C: reads
+    of the cut, tail nodes, whole output chunks): bitwise the oracle."""
+    r, O = restatement, oracle
+    for dtype, W in (("float", 4), ("double", 2)):
+        for n, (hd, td, R) in G.COOP[dtype].items():
+            if n > 256:
+                continue
+            for v in (3, 4, 6):
+                T, outs, _ = G.trace(v, 0, n)
+                P = G.plan_roles(T, outs, hd, td, W, R)
+                x = r.uniform(r.mix_seed(99, v, n), 2 * n)
+                tab = r.trig_constants(v, n)
+                full = G.evaluate(T, list(range(len(T.nodes))), x, tab)
+                arena = np.array(x)
+                for lst in P["stores"]:
+                    for val in lst:
+                        arena[P["where"][val]] = full[val]
+                out = np.full(2 * n, np.nan)
+                for lst in P["troles"]:
+                    for ch, tn, rd in lst:
+                        val = {u: arena[P["where"][u]] for u in rd}
+                        for u in tn:
+                            nd = T.nodes[u]
+                            a = val[nd[1]]
+                            if nd[0] == "add":
+                                val[u] = a + val[nd[2]]
+                            elif nd[0] == "sub":
+                                val[u] = a - val[nd[2]]
+                            elif nd[0] == "mul":
+                                val[u] = a * tab[nd[2]]
+                            else:
+                                val[u] = 0.5 * a
+                        for c in ch:
+                            for p in range(c * W, c * W + W):
+                                out[p] = val[outs[p]]
+                want = r.execute(v, O.F_CDFT, n, x)
+                assert out.tobytes() == want.tobytes(), (dtype, n, v)
