@@ -33,9 +33,6 @@ std::unique_ptr<FastPlan> make_fast_typed(int v, int kind, size_t n, const void*
   return nullptr;
 }
 
-std::unique_ptr<FastPlan> make_fast_typed_f32(int variant, size_t n, const void* tab, uint32_t nmax, int dev) {
-  return make_fast_typed<float>(variant, 0, n, tab, nmax, dev);
-}
 
 std::unique_ptr<FastPlan> make_fast_plan(const amqft_plan_desc& d, const void* d_trig,
                                          uint32_t nmax) {
@@ -97,6 +94,39 @@ OpCount fast_op_counts(const amqft_plan_desc& d) {
     c.bt /= 2;
   }
   return c;
+}
+
+bool fast_sub_covered(int dtype, size_t n) {
+  if (dtype == AMQFT_F32) return n >= 2 && n <= 8192;
+  return n >= 2 && n <= 4096 && n != 512;
+}
+
+std::unique_ptr<FastPlan> make_fast_sub(int variant, size_t n, int dtype, const void* tab, uint32_t nmax, int dev) {
+  amqft_plan_desc d{};
+  d.variant = variant;
+  d.function = AMQFT_FN_CDFT;
+  d.n = n;
+  d.batch = 1;
+  d.dtype = dtype;
+  d.trig_mode = AMQFT_TRIG_TABLE;
+  d.order = AMQFT_ORDER_FAST;
+  d.device = dev;
+  std::unique_ptr<FastPlan> p = make_fast_plan(d, tab, nmax);
+  OpCount o;
+  if (!p) p = make_small_plan(d, tab, nmax, &o);
+  return p;
+}
+
+OpCount fast_sub_op_counts(int variant, size_t n, int dtype) {
+  amqft_plan_desc d{};
+  d.variant = variant;
+  d.function = AMQFT_FN_CDFT;
+  d.n = n;
+  d.dtype = dtype;
+  OpCount o;
+  if (n >= 1024) return fast_op_counts(d);
+  smallk::small_ops_n(variant, n, dtype == AMQFT_F64, &o);
+  return o;
 }
 
 }  // namespace amqft_b200

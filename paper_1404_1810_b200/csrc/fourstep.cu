@@ -13,8 +13,10 @@
 //   5. transpose   Z[k1][k2] -> X[k2][k1] = natural order (swap + 1/N for the inverse)
 //
 // The AM-QFT recursion itself is not preserved across the split (the
-// sub-transforms are), so this path is fp32 "fast order" only; its
-// accuracy is checked against the fp64 oracle of the same variant.
+// sub-transforms are), so this path is "fast order" only (fp32, and fp64
+// for config 3's large sizes); its accuracy is checked against the fp64
+// oracle of the same variant.  Sub-transforms: the fused kernel (N1, N2 >=
+// 1024) or the small-CDFT kernels (<= 512 fp32 / 256 fp64).
 // Twiddles w_N^j = exp(-2 pi i j / N): TRIG_TABLE = two half-size tables
 // w^(jh B) and w^(jl) (B = 2^ceil(lg N / 2)) multiplied in fp64;
 // TRIG_ONTHEFLY = sincospi in fp64 per element.
@@ -41,20 +43,26 @@ constexpr int TR = 8;    // rows of threads per tile
 // blockIdx.z.  MODE 0: plain; 1: twiddle by w_N^(r c) (r = row of out, c =
 // column of out); SWAP: exchange re/im of the input; scale multiplies the
 // result.  (A swap on both sides of a transform is the swap-trick inverse.)
-template <int MODE, bool SWAP>
-__global__ void __launch_bounds__(TD * TR) k_transpose(const float2* __restrict__ in, float2* __restrict__ out,
-                                                      int R1, int C1, float scale,
+template <typename R> struct C2;
+template <> struct C2<float> { using T = float2; static __device__ __forceinline__ T mk(float a, float b) { return make_float2(a, b); } };
+template <> struct C2<double> { using T = double2; static __device__ __forceinline__ T mk(double a, double b) { return make_double2(a, b); } };
+
+template <int MODE, bool SWAP, typename R = float>
+__global__ void __launch_bounds__(TD * TR) k_transpose(const typename C2<R>::T* __restrict__ in,
+                                                      typename C2<R>::T* __restrict__ out,
+                                                      int R1, int C1, R scale,
                                                       const double2* __restrict__ twh,
                                                       const double2* __restrict__ twl, int logb,
                                                       int logn, int onthefly) {
-  __shared__ float2 tile[TD][TD + 1];
+  using V2 = typename C2<R>::T;
+  __shared__ V2 tile[TD][TD + 1];
   const size_t mat = static_cast<size_t>(blockIdx.z) * R1 * C1;
   const int c0 = blockIdx.x * TD, r0 = blockIdx.y * TD;
 #pragma unroll
   for (int j = 0; j < TD; j += TR) {
     const int r = r0 + threadIdx.y + j, c = c0 + threadIdx.x;
-    float2 v = in[mat + static_cast<size_t>(r) * C1 + c];
-    if (SWAP) v = make_float2(v.y, v.x);
+    V2 v = in[mat + static_cast<size_t>(r) * C1 + c];
+    if (SWAP) v = C2<R>::mk(v.y, v.x);
     tile[threadIdx.y + j][threadIdx.x] = v;
   }
   __syncthreads();
@@ -62,7 +70,7 @@ __global__ void __launch_bounds__(TD * TR) k_transpose(const float2* __restrict_
   for (int j = 0; j < TD; j += TR) {
     const int orow = c0 + threadIdx.y + j;   // row of out = column of in
     const int ocol = r0 + threadIdx.x;
-    float2 v = tile[threadIdx.x][threadIdx.y + j];
+    V2 v = tile[threadIdx.x][threadIdx.y + j];
     if (MODE == 1) {
       // w_N^(orow * ocol): j = (orow * ocol) mod N
       const unsigned long long jj =
@@ -79,8 +87,8 @@ __global__ void __launch_bounds__(TD * TR) k_transpose(const float2* __restrict_
         wr = a.x * b.x - a.y * b.y;
         wi = a.x * b.y + a.y * b.x;
       }
-      const float fr = static_cast<float>(wr), fi = static_cast<float>(wi);
-      v = make_float2(v.x * fr - v.y * fi, v.x * fi + v.y * fr);
+      const R fr = static_cast<R>(wr), fi = static_cast<R>(wi);
+      v = C2<R>::mk(v.x * fr - v.y * fi, v.x * fi + v.y * fr);
     }
     v.x *= scale;
     v.y *= scale;
@@ -88,16 +96,16 @@ __global__ void __launch_bounds__(TD * TR) k_transpose(const float2* __restrict_
   }
 }
 
-template <int MODE, bool SWAP>
-void launch_t(const float2* in, float2* out, size_t mats, int R1, int C1, float scale, const double2* twh,
-              const double2* twl, int logb, int logn, int onthefly, cudaStream_t st) {
+template <int MODE, bool SWAP, typename R = float>
+void launch_t(const typename C2<R>::T* in, typename C2<R>::T* out, size_t mats, int R1, int C1, R scale,
+              const double2* twh, const double2* twl, int logb, int logn, int onthefly, cudaStream_t st) {
   // grid.z is limited to 65535: loop over chunks of matrices
   for (size_t m0 = 0; m0 < mats; m0 += 65535) {
     const unsigned nz = static_cast<unsigned>(std::min<size_t>(65535, mats - m0));
     const dim3 grid(C1 / TD, R1 / TD, nz), block(TD, TR);
     const size_t off = m0 * static_cast<size_t>(R1) * C1;
-    k_transpose<MODE, SWAP><<<grid, block, 0, st>>>(in + off, out + off, R1, C1, scale, twh, twl, logb, logn,
-                                                     onthefly);
+    k_transpose<MODE, SWAP, R><<<grid, block, 0, st>>>(in + off, out + off, R1, C1, scale, twh, twl, logb, logn,
+                                                        onthefly);
   }
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("k_transpose: ") + cudaGetErrorString(e));
@@ -151,16 +159,47 @@ int lg2(size_t v) {
   return l;
 }
 
+// Split N = N1 N2 over covered sub-sizes (both >= 32: transpose tiles),
+// minimising the two DFT passes' time by the measured single-kernel HBM
+// throughput of each sub-size (B200, TB/s; tools/sweep_c3.py,
+// tools/prof_fast.py).
+double sub_tbs(int dtype, int lg) {
+  static const double f32[14] = {0, 5.0, 5.0, 5.0, 5.0, 5.0, 5.0, 2.5, 1.05, 0.6, 1.95, 2.6, 3.1, 2.2};
+  static const double f64[13] = {0, 5.5, 5.5, 5.5, 5.5, 5.5, 5.0, 2.65, 1.8, 0.0, 2.27, 2.68, 2.88};
+  if (dtype == AMQFT_F32) return lg < 14 ? f32[lg] : 0.0;
+  return lg < 13 ? f64[lg] : 0.0;
+}
+
+bool fourstep_split(int dtype, size_t n, size_t* n1, size_t* n2) {
+  const int lg = lg2(n);
+  double best = 0.0;
+  for (int l1 = 5; l1 <= lg - 5; ++l1) {
+    const int l2 = lg - l1;
+    if (!fast_sub_covered(dtype, size_t(1) << l1) || !fast_sub_covered(dtype, size_t(1) << l2)) continue;
+    const double a = sub_tbs(dtype, l1), b = sub_tbs(dtype, l2);
+    if (a <= 0.0 || b <= 0.0) continue;
+    const double cost = 1.0 / a + 1.0 / b;
+    if (best == 0.0 || cost < best - 1e-9) {
+      best = cost;
+      *n1 = size_t(1) << l1;
+      *n2 = size_t(1) << l2;
+    }
+  }
+  return best > 0.0;
+}
+
+template <typename R>
 class FourStepPlan final : public FastPlan {
+  using V2 = typename C2<R>::T;
+
  public:
   FourStepPlan(int variant, size_t n, size_t batch, int trig_mode, const void* tab, uint32_t nmax, int dev)
       : n_(n), batch_(batch), onthefly_(trig_mode == AMQFT_TRIG_ONTHEFLY) {
     logn_ = lg2(n);
-    const int l1 = (logn_ + 1) / 2, l2 = logn_ - l1;
-    n1_ = size_t(1) << l1;
-    n2_ = size_t(1) << l2;
-    p1_ = make_fast_typed_f32(variant, n1_, tab, nmax, dev);
-    p2_ = make_fast_typed_f32(variant, n2_, tab, nmax, dev);
+    const int dtype = sizeof(R) == 8 ? AMQFT_F64 : AMQFT_F32;
+    if (!fourstep_split(dtype, n, &n1_, &n2_)) throw std::invalid_argument("four-step: no covered split");
+    p1_ = make_fast_sub(variant, n1_, dtype, tab, nmax, dev);
+    p2_ = make_fast_sub(variant, n2_, dtype, tab, nmax, dev);
     if (!p1_ || !p2_) throw std::invalid_argument("four-step: no fused kernel for the sub-transform sizes");
     // half-size twiddle tables: w^(jh B), w^(jl), long double -> double
     logb_ = (logn_ + 1) / 2;
@@ -179,7 +218,7 @@ class FourStepPlan final : public FastPlan {
     check(cudaMalloc(&twl_, B * sizeof(double2)), "cudaMalloc twiddles");
     check(cudaMemcpy(twh_, th.data(), NH * sizeof(double2), cudaMemcpyHostToDevice), "cudaMemcpy");
     check(cudaMemcpy(twl_, tl.data(), B * sizeof(double2), cudaMemcpyHostToDevice), "cudaMemcpy");
-    check(cudaMalloc(&scratch_, batch_ * n_ * sizeof(float2)), "cudaMalloc four-step scratch");
+    check(cudaMalloc(&scratch_, batch_ * n_ * sizeof(V2)), "cudaMalloc four-step scratch");
     launches = 3 + p1_->launches + p2_->launches;
   }
   ~FourStepPlan() override {
@@ -189,26 +228,26 @@ class FourStepPlan final : public FastPlan {
   }
   void exec(const void* in, void* out, size_t rows, int inverse, cudaStream_t st) override {
     if (rows > batch_) throw std::invalid_argument("rows exceed the plan batch");
-    const float2* x = static_cast<const float2*>(in);
-    float2* y = static_cast<float2*>(out);
-    float2* s = scratch_;
+    const V2* x = static_cast<const V2*>(in);
+    V2* y = static_cast<V2*>(out);
+    V2* s = scratch_;
     const int R1 = static_cast<int>(n1_), C1 = static_cast<int>(n2_);
     // 1. x [n1][n2] -> s [n2][n1]
     if (inverse)
-      launch_t<0, true>(x, s, rows, R1, C1, 1.0f, nullptr, nullptr, 0, logn_, 0, st);
+      launch_t<0, true, R>(x, s, rows, R1, C1, R(1), nullptr, nullptr, 0, logn_, 0, st);
     else
-      launch_t<0, false>(x, s, rows, R1, C1, 1.0f, nullptr, nullptr, 0, logn_, 0, st);
+      launch_t<0, false, R>(x, s, rows, R1, C1, R(1), nullptr, nullptr, 0, logn_, 0, st);
     // 2. rows of length N1
     p1_->exec(s, s, rows * n2_, 0, st);
     // 3. s [n2][k1] * w^(n2 k1) -> y [k1][n2]
-    launch_t<1, false>(s, y, rows, C1, R1, 1.0f, twh_, twl_, logb_, logn_, onthefly_ ? 1 : 0, st);
+    launch_t<1, false, R>(s, y, rows, C1, R1, R(1), twh_, twl_, logb_, logn_, onthefly_ ? 1 : 0, st);
     // 4. rows of length N2: y -> s [k1][k2]
     p2_->exec(y, s, rows * n1_, 0, st);
     // 5. s [k1][k2] -> y [k2][k1]
     if (inverse)
-      launch_t<0, true>(s, y, rows, R1, C1, 1.0f / static_cast<float>(n_), nullptr, nullptr, 0, logn_, 0, st);
+      launch_t<0, true, R>(s, y, rows, R1, C1, R(1) / static_cast<R>(n_), nullptr, nullptr, 0, logn_, 0, st);
     else
-      launch_t<0, false>(s, y, rows, R1, C1, 1.0f, nullptr, nullptr, 0, logn_, 0, st);
+      launch_t<0, false, R>(s, y, rows, R1, C1, R(1), nullptr, nullptr, 0, logn_, 0, st);
   }
 
  private:
@@ -221,7 +260,7 @@ class FourStepPlan final : public FastPlan {
   std::unique_ptr<FastPlan> p1_, p2_;
   double2* twh_ = nullptr;
   double2* twl_ = nullptr;
-  float2* scratch_ = nullptr;
+  V2* scratch_ = nullptr;
 };
 
 }  // namespace
@@ -286,21 +325,19 @@ void transpose_c64(const void* in, void* out, size_t mats, size_t r, size_t c, c
 }
 
 bool fourstep_covers(const amqft_plan_desc& d) {
-  if (d.function != AMQFT_FN_CDFT || d.dtype != AMQFT_F32 || d.order != AMQFT_ORDER_FAST) return false;
-  if (d.n < (size_t(1) << 20) || d.n > (size_t(1) << 26) || (d.n & (d.n - 1)) != 0) return false;
-  return true;
+  if (d.function != AMQFT_FN_CDFT || d.order != AMQFT_ORDER_FAST) return false;
+  if ((d.n & (d.n - 1)) != 0 || d.n > (size_t(1) << 26)) return false;
+  if (fast_sub_covered(d.dtype, d.n)) return false;   // one fused / small kernel does it
+  size_t n1, n2;
+  return fourstep_split(d.dtype, d.n, &n1, &n2);
 }
 
 OpCount fourstep_op_counts(const amqft_plan_desc& d) {
   // N2 sub-transforms of length N1, N1 of length N2 (the reference DAG of
-  // each, fast_op_counts), plus one complex twiddle multiply per element
-  // (4 muls + 2 adds).
-  int lg = lg2(d.n);
-  const size_t n1 = size_t(1) << ((lg + 1) / 2), n2 = d.n / n1;
-  amqft_plan_desc a = d, b = d;
-  a.n = n1;
-  b.n = n2;
-  const OpCount c1 = fast_op_counts(a), c2 = fast_op_counts(b);
+  // each), plus one complex twiddle multiply per element (4 muls + 2 adds).
+  size_t n1 = 0, n2 = 0;
+  fourstep_split(d.dtype, d.n, &n1, &n2);
+  const OpCount c1 = fast_sub_op_counts(d.variant, n1, d.dtype), c2 = fast_sub_op_counts(d.variant, n2, d.dtype);
   OpCount c;
   c.adds = n2 * c1.adds + n1 * c2.adds + 2 * d.n;
   c.muls = n2 * c1.muls + n1 * c2.muls + 4 * d.n;
@@ -310,7 +347,9 @@ OpCount fourstep_op_counts(const amqft_plan_desc& d) {
 
 std::unique_ptr<FastPlan> make_fourstep_plan(const amqft_plan_desc& d, const void* d_trig, uint32_t nmax) {
   if (!fourstep_covers(d)) return nullptr;
-  return std::make_unique<FourStepPlan>(d.variant, d.n, d.batch, d.trig_mode, d_trig, nmax, d.device);
+  if (d.dtype == AMQFT_F64)
+    return std::make_unique<FourStepPlan<double>>(d.variant, d.n, d.batch, d.trig_mode, d_trig, nmax, d.device);
+  return std::make_unique<FourStepPlan<float>>(d.variant, d.n, d.batch, d.trig_mode, d_trig, nmax, d.device);
 }
 
 }  // namespace amqft_b200

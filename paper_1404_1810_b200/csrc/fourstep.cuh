@@ -10,10 +10,13 @@
 
 namespace amqft_b200 {
 
-// fp32 fused-kernel plan for one size (nullptr if none): fast.cu.
-std::unique_ptr<FastPlan> make_fast_typed_f32(int variant, size_t n, const void* tab, uint32_t nmax, int dev);
+// Fused / small-CDFT plan for one sub-transform size (nullptr if none),
+// its op counts, and whether a single kernel covers n: fast.cu.
+std::unique_ptr<FastPlan> make_fast_sub(int variant, size_t n, int dtype, const void* tab, uint32_t nmax, int dev);
+OpCount fast_sub_op_counts(int variant, size_t n, int dtype);
+bool fast_sub_covered(int dtype, size_t n);
 
-// CDFT, fp32, fast order, N = 2^20 .. 2^26.
+// CDFT, fast order, N up to 2^26 beyond the single-kernel sizes.
 bool fourstep_covers(const amqft_plan_desc& d);
 std::unique_ptr<FastPlan> make_fourstep_plan(const amqft_plan_desc& d, const void* d_trig, uint32_t nmax);
 OpCount fourstep_op_counts(const amqft_plan_desc& d);

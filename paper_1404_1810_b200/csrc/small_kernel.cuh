@@ -112,6 +112,16 @@ template <bool INV> struct GRowIO<double, INV> {
   }
 };
 
+// Slots s < nt of the Nmax = 4 nt table are slots (s + 1) nmax / (4 nt) - 1
+// of the plan's table (TrigTable level sharing, variants.cpp:281): one
+// strided copy.
+template <typename R>
+cudaError_t fetch_table(R* dst, int nt, const void* tab, uint32_t nmax) {
+  const size_t ratio = nmax / (4u * static_cast<uint32_t>(nt));
+  return cudaMemcpy2D(dst, sizeof(R), static_cast<const R*>(tab) + (ratio - 1), ratio * sizeof(R), sizeof(R),
+                      static_cast<size_t>(nt), cudaMemcpyDeviceToHost);
+}
+
 __device__ __forceinline__ uint32_t s_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -298,11 +308,8 @@ class CoopPlanImpl final : public FastPlan {
 
  public:
   CoopPlanImpl(const void* tab, uint32_t nmax, int device) {
-    std::vector<R> big(nmax / 4);
-    cudaError_t e = cudaMemcpy(big.data(), tab, sizeof(R) * big.size(), cudaMemcpyDeviceToHost);
+    cudaError_t e = fetch_table(tp_.v, C::NT, tab, nmax);
     if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
-    const uint32_t ratio = nmax / static_cast<uint32_t>(C::N);
-    for (int s = 0; s < C::NT; ++s) tp_.v[s] = big[(s + 1) * ratio - 1];
     auto f0 = k_coop<V, R, LOGN, false>;
     auto f1 = k_coop<V, R, LOGN, true>;
     e = cudaFuncSetAttribute(f0, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM));
@@ -346,12 +353,8 @@ class SmallPlanImpl final : public FastPlan {
     // the generated slots index the Nmax = max(N, 8) table; a larger table
     // holds the same values at slot (s + 1) nmax / Nsmall - 1 (TrigTable
     // level sharing, variants.cpp:281)
-    const int nsm = C::NT * 4;
-    std::vector<R> big(nmax / 4);
-    cudaError_t e = cudaMemcpy(big.data(), tab, sizeof(R) * big.size(), cudaMemcpyDeviceToHost);
+    cudaError_t e = fetch_table(tp_.v, C::NT, tab, nmax);
     if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
-    const uint32_t ratio = nmax / static_cast<uint32_t>(nsm);
-    for (int s = 0; s < C::NT; ++s) tp_.v[s] = big[(s + 1) * ratio - 1];
     auto f0 = k_small<V, R, LOGN, false>;
     auto f1 = k_small<V, R, LOGN, true>;
     if (C::SMEM > 48 * 1024) {

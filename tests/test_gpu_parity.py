@@ -554,3 +554,45 @@ def test_small_kernel_large_batch_round_trip():
     one.forward(x[rows - 1:].contiguous(), y1)
     torch.cuda.synchronize()
     assert torch.equal(y1[0], y[rows - 1])
+
+
+# ---- four-step over the fused and small-CDFT kernels: config 3's large
+# sizes in fp64 (fast order) and the fp32 sizes between the kernels
+@pytest.mark.parametrize("lg", [13, 16, 17, 20])
+def test_fourstep_fp64_config3_sizes(oracle, restatement, lg):
+    """fp64 four-step, N = 2^13 .. 2^20 (every split uses the fused kernel
+    or the small-CDFT kernels): v1-4 within 1e-12 of the reference CPU
+    result of the same variant and of numpy's fp64 FFT, round trip to 1e-13.
+    v5-8: the reference itself is unstable at these sizes -- the
+    four-step result is checked against numpy's FFT instead, to 1e-9 (its
+    sub-transforms are <= 4096)."""
+    r, O = restatement, oracle
+    n = 1 << lg
+    x = r.uniform(r.mix_seed(303, 0, n, 1), 2 * n)
+    f = np.fft.fft(x[0::2] + 1j * x[1::2])
+    ref = np.empty(2 * n)
+    ref[0::2], ref[1::2] = f.real, f.imag
+    for v in range(1, 9):
+        plan = amqft.Plan(v, amqft.FunctionId.Cdft, n, 1, dtype="f64", order=amqft.Order.Fast)
+        assert plan.path()[0] == 3, (v, lg)
+        got = run_plan(plan, [x])[0]
+        back = run_plan(plan, [got], inverse=True)[0]
+        if v <= 4:
+            if lg <= 16:
+                assert r.rel_l2(got, r.execute(v, O.F_CDFT, n, x)) <= 1e-12, v
+            assert r.rel_l2(got, ref) <= 1e-12, v
+            assert r.rel_l2(back, x) <= 1e-13, v
+        else:
+            assert r.rel_l2(got, ref) <= 1e-9, v
+
+
+def test_fourstep_fp32_between_kernel_sizes(oracle, restatement):
+    """fp32 N = 2^14 .. 2^19 now run as four-steps (were the generic path)."""
+    r, O = restatement, oracle
+    for lg in (14, 17, 19):
+        n = 1 << lg
+        x = np.random.default_rng(lg).standard_normal(2 * n).astype(np.float32)
+        want = r.execute(4, O.F_CDFT, n, x.astype(np.float64))
+        got = run_plan(_fourstep_plan(4, n, 2), [x, x])
+        assert got[0].tobytes() == got[1].tobytes()
+        assert r.rel_l2(got[0], want) <= 1e-5 * lg, lg
