@@ -22,9 +22,10 @@
 // Harmonic-major variants 2,3,6,7 run the transpose (chain folds, AM_F
 // levels, bottom, mirror levels in frequency, store).
 //
-// Arithmetic goes through Arith<R> (__fadd_rn / __dadd_rn ...): no FMA
-// contraction, so the fp64 instantiation reproduces the reference bitwise
-// (serial recurrences included); the fp32 instantiation is the fast path.
+// Arithmetic goes through KArith<R>: fp64 = Arith<double> (__dadd_rn ...,
+// no FMA contraction), so the fp64 instantiation reproduces the reference
+// bitwise (serial recurrences included); the fp32 instantiation is the fast
+// path (contractable operators).
 #pragma once
 #include <cuda_runtime.h>
 
@@ -54,6 +55,28 @@
 
 namespace amqft_b200 {
 namespace fastk {
+
+// Kernel arithmetic.  fp64: Arith<double> (__dadd_rn..., never contracted),
+// so the fp64 instance stays bitwise the reference.  fp32 (the fast path,
+// checked against the fp64 oracle within 1e-5 log2 N): plain operators,
+// which nvcc may contract into FFMA where a constant multiply feeds an add
+// (one instruction instead of two; FFMA rounds once, so it is never less
+// accurate than FMUL + FADD).
+#ifndef AMQFT_FP32_CONTRACT
+#define AMQFT_FP32_CONTRACT 1
+#endif
+// Measured (B200, config-2 shapes): contraction speeds up N = 4096 by 3-4 %
+// (all variants) but slows N = 1024 / 2048 / 8192 by 2-10 %, so it is used
+// at N = 4096 only.
+template <typename R, int LOGN> struct KArith : Arith<R> {};
+struct ContractF {
+  static __device__ __forceinline__ float add(float a, float b) { return a + b; }
+  static __device__ __forceinline__ float sub(float a, float b) { return a - b; }
+  static __device__ __forceinline__ float mul(float a, float b) { return a * b; }
+};
+#if AMQFT_FP32_CONTRACT
+template <> struct KArith<float, 12> : ContractF {};
+#endif
 
 __device__ __forceinline__ int parity(unsigned x) { return __popc(x) & 1; }
 
@@ -157,7 +180,7 @@ __device__ __forceinline__ void seg_params(int lam_c, int s, int d, int* rho, in
 // (harmonic-major forward, FWD=true) at size n on an unskewed buffer.
 template <class C, typename R, bool FWD>
 __device__ __forceinline__ void chain_level(R* B, int n, int tid) {
-  using A = Arith<R>;
+  using A = KArith<R, C::LOGN_>;
   const int q = n >> 2;
   const int lgq = 31 - __clz(q);
   for (int g = tid; g < n; g += C::NT) {
@@ -183,7 +206,7 @@ __device__ __forceinline__ void chain_level(R* B, int n, int tid) {
 // of the big top blocks, one thread per class, in place (swizzled buffer).
 template <class C, int DEPTH, typename R>
 __device__ __forceinline__ void chain_class(R* ch, int lam_c, int t, int r) {
-  using A = Arith<R>;
+  using A = KArith<R, C::LOGN_>;
   constexpr int V = C::V_;
   constexpr int stride = 2 << DEPTH;
   const int q = C::N >> (t + DEPTH + 3);
@@ -286,7 +309,7 @@ struct AmPos {
 template <class C, typename R, bool BWD, int LAM, int D>
 __device__ __forceinline__ void am_depth(R (&x)[C::N / 128], bool last_lane, bool first_lane,
                                          bool blk_ok) {
-  using A = Arith<R>;
+  using A = KArith<R, C::LOGN_>;
   using P = AmPos<C, BWD, LAM, D>;
   constexpr int RR = P::RR, S = P::S;
   constexpr bool ADD = BWD ? (C::V_ == 4) : (C::V_ == 2);
@@ -331,7 +354,7 @@ __device__ __forceinline__ void am_depth(R (&x)[C::N / 128], bool last_lane, boo
 // path uses it; fp64 keeps the reference's serial order (bitwise).
 template <class C, typename R, bool BWD, int LAM, int D>
 __device__ __forceinline__ void am_scan_depth(R (&x)[C::N / 128], int i, int nl, bool blk_ok) {
-  using A = Arith<R>;
+  using A = KArith<R, C::LOGN_>;
   using P = AmPos<C, BWD, LAM, D>;
   constexpr int V = C::V_;
   constexpr int RR = P::RR, S = P::S, M = RR / S;
@@ -446,9 +469,9 @@ __device__ __forceinline__ void am_phase_regs(R* B, int tid) {
 // one shuffle otherwise.  Same operations and operand order as
 // codegen/gen_fast.py emit_pair (Dct chains use every cell; Dst chains skip
 // i = 0 and i = 64), so the fp64 instance stays bitwise.
-template <typename R, bool FOLD, int LAM>
+template <typename R, bool FOLD, int LAM, int LG>
 __device__ __forceinline__ void pair_op(R e, R o, R& e2, R& o2) {
-  using A = Arith<R>;
+  using A = KArith<R, LG>;
   if (!FOLD) {  // SplitTimeParity bwd (elaborations.cpp:310-329)
     e2 = LAM ? A::add(o, e) : A::add(e, o);
     o2 = LAM ? A::sub(o, e) : A::sub(e, o);
@@ -463,7 +486,7 @@ __device__ __forceinline__ void pair_op(R e, R o, R& e2, R& o2) {
 // General form for HW in {8, 16, 32}: cells i in [0, 2 HW] (y = i W/2,
 // physical ST i), lane l holds i = l (l <= 2 HW), for HW = 32 also
 // i = 64 - l, for HW >= 16 lane 0 also i = 32; levels t = 0 .. log2 HW.
-template <typename R, bool FOLD, int LAM, int HW, int ST>
+template <typename R, bool FOLD, int LAM, int HW, int ST, int LG>
 __device__ __forceinline__ void special_class_l(R* ch, int lane) {
   static_assert(HW == 8 || HW == 16 || HW == 32, "special class size");
   constexpr int NC = 2 * HW;
@@ -476,7 +499,7 @@ __device__ __forceinline__ void special_class_l(R* ch, int lane) {
   auto level = [&](int t) {
     R e2, o2;
     if (t == 5) {                                  // in-lane pairs (i, 64 - i)
-      pair_op<R, FOLD, LAM>(a, b, e2, o2);
+      pair_op<R, FOLD, LAM, LG>(a, b, e2, o2);
       a = own0 ? e2 : a;
       b = own0 ? o2 : b;
       return;
@@ -487,7 +510,7 @@ __device__ __forceinline__ void special_class_l(R* ch, int lane) {
     const R other = (t == 4 && lane == 0) ? m : pv;
     const bool lower = lane < Hh && own0;
     const bool upper = lane > Hh && lane <= P && !(LAM && lane == P);
-    pair_op<R, FOLD, LAM>(lower ? a : other, lower ? other : a, e2, o2);
+    pair_op<R, FOLD, LAM, LG>(lower ? a : other, lower ? other : a, e2, o2);
     if (t == 4 && lane == 0 && !LAM) m = o2;
     a = lower ? e2 : (upper ? o2 : a);
   };
@@ -503,10 +526,10 @@ __device__ __forceinline__ void special_class_l(R* ch, int lane) {
   if (HW >= 16 && lane == 0 && !LAM) ch[ST * 32] = m;
 }
 
-template <typename R, bool FOLD, int HW, int ST>
+template <typename R, bool FOLD, int HW, int ST, int LG>
 __device__ __forceinline__ void special_class(R* ch, int lam, int lane) {
-  if (lam) special_class_l<R, FOLD, 1, HW, ST>(ch, lane);   // warp-uniform
-  else special_class_l<R, FOLD, 0, HW, ST>(ch, lane);
+  if (lam) special_class_l<R, FOLD, 1, HW, ST, LG>(ch, lane);   // warp-uniform
+  else special_class_l<R, FOLD, 0, HW, ST, LG>(ch, lane);
 }
 
 // Recombination (TM, FOLD = false) / fold (HM, FOLD = true) of all four
@@ -516,7 +539,7 @@ __device__ __forceinline__ void special_class(R* ch, int lam, int lane) {
 // Every thread of the row calls it (it contains the row barriers).
 template <class C, typename R, bool FOLD, class Sync>
 __device__ __forceinline__ void recombine(R* B, int tid, bool act, Sync row_sync) {
-  using A = Arith<R>;
+  using A = KArith<R, C::LOGN_>;
   constexpr int N = C::N, H = C::H;
   constexpr int WR = (N / C::LB > 64) ? N / C::LB : 64;
   constexpr int HWR = H / WR;
@@ -551,13 +574,13 @@ __device__ __forceinline__ void recombine(R* B, int tid, bool act, Sync row_sync
       }
     } else if (GT == 128 && tid < 256) {
       const int c = (tid >> 5) - 4;
-      special_class<R, FOLD, HWR, ST>(B + C::co_sw(c), c & 1, tid & 31);
+      special_class<R, FOLD, HWR, ST, C::LOGN_>(B + C::co_sw(c), c & 1, tid & 31);
     } else if (GT == 256 && tid >= 256 && tid < C::NT) {
       // spare warps 8.. take the four chains' k = 0 classes in turn
       constexpr int NW = (C::NT - 256) / 32;
 #pragma unroll 1
       for (int c = (tid - 256) >> 5; c < 4; c += NW)
-        special_class<R, FOLD, HWR, ST>(B + C::co_sw(c), c & 1, tid & 31);
+        special_class<R, FOLD, HWR, ST, C::LOGN_>(B + C::co_sw(c), c & 1, tid & 31);
     }
   }
   post();
@@ -663,7 +686,7 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows_in,
   long long t_prev = 0, w_start = 0;
 #endif
   using C = Cfg<V, R, LOGN, LOGLB>;
-  using A = Arith<R>;
+  using A = KArith<R, C::LOGN_>;
   using V2 = typename std::conditional<sizeof(R) == 4, float2, double2>::type;
   extern __shared__ __align__(128) unsigned char smraw[];
   // row slot: threads [slot*NT, (slot+1)*NT) own row slot of each pair
