@@ -41,6 +41,10 @@ SIZES = {"float": (2, 4, 8, 16, 32, 64), "double": (2, 4, 8, 16, 32)}
 # Cooperative rows: N -> (head stages, tail stages, warp roles)
 COOP = {"float": {128: (2, 2, 4), 256: (3, 3, 8), 512: (4, 4, 16)},
         "double": {64: (2, 2, 4), 128: (3, 3, 8), 256: (4, 4, 16)}}
+# rows per CTA tile (lanes past it duplicate rows lane % ROWS); 32 for all
+# generated instances (fp64 N = 512 would need 16-row tiles for shared memory
+# and spills at 16 roles: it runs as a 16 x 32 four-step instead)
+COOP_ROWS = {}
 
 
 def _items(op, n):
@@ -698,6 +702,7 @@ def emit_roles(v, n, R_t, hd, td, R):
         fns.append("\n".join(lines))
     body = [f"template <> struct SmallRoles<{v}, {n.bit_length() - 1}, {R_t}> {{",
             f"  static constexpr int R = {R};",
+            f"  static constexpr int ROWS = {COOP_ROWS.get((R_t, n), 32)};",
             f"  static constexpr unsigned long long OPS[3] = {{{ops[0]}ull, {ops[1]}ull, {ops[2]}ull}};"]
     body += fns
     body.append("  template <class AR, class IO>")

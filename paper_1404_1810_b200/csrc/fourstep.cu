@@ -96,9 +96,57 @@ __global__ void __launch_bounds__(TD * TR) k_transpose(const typename C2<R>::T* 
   }
 }
 
+// Element-wise variant for matrices with a side below the 32-wide tile
+// (four-step splits with a sub-size of 2..16): one thread per output
+// element, same twiddle/swap/scale semantics.
+template <int MODE, bool SWAP, typename R>
+__global__ void __launch_bounds__(256) k_transpose_small(const typename C2<R>::T* __restrict__ in,
+                                                        typename C2<R>::T* __restrict__ out, size_t mats,
+                                                        int R1, int C1, R scale, const double2* __restrict__ twh,
+                                                        const double2* __restrict__ twl, int logb, int logn,
+                                                        int onthefly) {
+  using V2 = typename C2<R>::T;
+  const size_t per = static_cast<size_t>(R1) * C1, total = mats * per;
+  for (size_t i = threadIdx.x + static_cast<size_t>(blockIdx.x) * blockDim.x; i < total;
+       i += static_cast<size_t>(blockDim.x) * gridDim.x) {
+    const size_t mat = i / per;
+    const int e = static_cast<int>(i - mat * per);
+    const int orow = e / R1, ocol = e - orow * R1;        // out is C1 x R1
+    V2 v = in[mat * per + static_cast<size_t>(ocol) * C1 + orow];
+    if (SWAP) v = C2<R>::mk(v.y, v.x);
+    if (MODE == 1) {
+      const unsigned long long jj =
+          (static_cast<unsigned long long>(orow) * static_cast<unsigned long long>(ocol)) & ((1ull << logn) - 1ull);
+      double wr, wi;
+      if (onthefly) {
+        double sn, cs;
+        sincospi(static_cast<double>(jj) * 2.0 / static_cast<double>(1ull << logn), &sn, &cs);
+        wr = cs;
+        wi = -sn;
+      } else {
+        const double2 a = twh[jj >> logb], b = twl[jj & ((1ull << logb) - 1ull)];
+        wr = a.x * b.x - a.y * b.y;
+        wi = a.x * b.y + a.y * b.x;
+      }
+      const R fr = static_cast<R>(wr), fi = static_cast<R>(wi);
+      v = C2<R>::mk(v.x * fr - v.y * fi, v.x * fi + v.y * fr);
+    }
+    out[i] = C2<R>::mk(v.x * scale, v.y * scale);
+  }
+}
+
 template <int MODE, bool SWAP, typename R = float>
 void launch_t(const typename C2<R>::T* in, typename C2<R>::T* out, size_t mats, int R1, int C1, R scale,
               const double2* twh, const double2* twl, int logb, int logn, int onthefly, cudaStream_t st) {
+  if (R1 % TD || C1 % TD) {
+    const size_t total = mats * static_cast<size_t>(R1) * C1;
+    const unsigned grid = static_cast<unsigned>(std::min<size_t>((total + 255) / 256, 148 * 32));
+    k_transpose_small<MODE, SWAP, R><<<grid, 256, 0, st>>>(in, out, mats, R1, C1, scale, twh, twl, logb, logn,
+                                                           onthefly);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw std::runtime_error(std::string("k_transpose_small: ") + cudaGetErrorString(e));
+    return;
+  }
   // grid.z is limited to 65535: loop over chunks of matrices
   for (size_t m0 = 0; m0 < mats; m0 += 65535) {
     const unsigned nz = static_cast<unsigned>(std::min<size_t>(65535, mats - m0));
@@ -159,7 +207,8 @@ int lg2(size_t v) {
   return l;
 }
 
-// Split N = N1 N2 over covered sub-sizes (both >= 32: transpose tiles),
+// Split N = N1 N2 over covered sub-sizes (both >= 32 from N = 2^10 on, for
+// the tiled transposes; below that the element-wise transpose),
 // minimising the two DFT passes' time by the measured single-kernel HBM
 // throughput of each sub-size (B200, TB/s; tools/sweep_c3.py,
 // tools/prof_fast.py).
@@ -173,8 +222,9 @@ double sub_tbs(int dtype, int lg) {
 bool fourstep_split(int dtype, size_t n, size_t* n1, size_t* n2) {
   const int lg = lg2(n);
   double best = 0.0;
-  for (int l1 = 5; l1 <= lg - 5; ++l1) {
+  for (int l1 = 1; l1 < lg; ++l1) {
     const int l2 = lg - l1;
+    if ((l1 < 5 || l2 < 5) && lg >= 10) continue;   // 32 x 32 tiled transposes where the sizes allow
     if (!fast_sub_covered(dtype, size_t(1) << l1) || !fast_sub_covered(dtype, size_t(1) << l2)) continue;
     const double a = sub_tbs(dtype, l1), b = sub_tbs(dtype, l2);
     if (a <= 0.0 || b <= 0.0) continue;

@@ -237,7 +237,7 @@ struct CCfg {
   using G = SmallRoles<V, LOGN, R>;
   static constexpr int N = 1 << LOGN;
   static constexpr int NT = N / 4;
-  static constexpr int ROWS = 32;
+  static constexpr int ROWS = G::ROWS;          // 32, or 16 (lanes 16-31 duplicate rows 0-15)
   static constexpr int NTH = 32 * G::R;
   static constexpr int ROWB = 2 * N * static_cast<int>(sizeof(R));
   static constexpr int STRIDE = ROWB + 16;
@@ -284,7 +284,7 @@ k_coop(const R* __restrict__ in, R* __restrict__ out, size_t rows,
     // every lane runs (lanes past the tile's rows on stale data, not
     // stored): the roles' named barriers count all NTH threads
     CoopIO<R, INV, C::NTH> io;
-    io.p = reinterpret_cast<VT*>(sm + size_t(lane) * C::STRIDE);
+    io.p = reinterpret_cast<VT*>(sm + size_t(lane % C::ROWS) * C::STRIDE);
     io.scale = scale;
     C::G::template run<Arith<R>>(warp, io, tp.v);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

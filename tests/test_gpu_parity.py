@@ -558,7 +558,7 @@ def test_small_kernel_large_batch_round_trip():
 
 # ---- four-step over the fused and small-CDFT kernels: config 3's large
 # sizes in fp64 (fast order) and the fp32 sizes between the kernels
-@pytest.mark.parametrize("lg", [13, 16, 17, 20])
+@pytest.mark.parametrize("lg", [9, 13, 16, 17, 20])
 def test_fourstep_fp64_config3_sizes(oracle, restatement, lg):
     """fp64 four-step, N = 2^13 .. 2^20 (every split uses the fused kernel
     or the small-CDFT kernels): v1-4 within 1e-12 of the reference CPU
