@@ -532,7 +532,7 @@ def _pack(items, R):
     return [b[1] for b in bins]
 
 
-def plan_roles(T, outs, hd, td, W, R):
+def plan_roles(T, outs, hd, td, W, R, pair=False):
     S = len(T.snap) - 1
     band = lambda u: "H" if T.stage[u] < hd else ("T" if T.stage[u] >= S - td else "M")  # noqa: E731
     need = _cone(T, outs, lambda u: False)
@@ -568,14 +568,44 @@ def plan_roles(T, outs, hd, td, W, R):
     for v in cut_reads:
         assert v in where, "tail operand not in the arena at the cut"
     # band-B roles: middle components (+ head/input values to be stored)
+    owner = {}
+    stores = [[] for _ in range(R)]
+    tw = _twins(T) if pair else None
+    if tw is not None:
+        # Re/Im pairing: roles r < R/2 run Re components, role r + R/2 the
+        # Im twins (same code, part = 1): the instruction working set halves
+        par = tw["par"]
+        re = [m for m in comps.values() if par[m[0]] == 1]
+        im = [m for m in comps.values() if par[m[0]] == 2]
+        assert len(re) == len(im) and all(len({par[u] for u in m}) == 1 for m in comps.values())
+        half = _pack([(len(m), ("m", m)) for m in re], R // 2)
+        broles = half + [[("m", sorted(tw["twin"][u] for u in m)) for _, m in lst] for lst in half]
+        for r, lst in enumerate(broles):
+            for _, m in lst:
+                for u in m:
+                    owner[u] = r
+        load = [sum(len(m) for _, m in lst) for lst in half]
+        cut_set = set(cut_reads)
+        for v in cut_reads:
+            if par[v] == 2:
+                continue           # stored by the twin role of its Re value
+            assert par[v] == 1, "a cut value mixing Re and Im"
+            t = tw["twin"][v]
+            assert t in cut_set and where[t] == where[v] + len(cut) // 2, "Im twin not at the shifted position"
+            if band(v) == "M":
+                r = owner[v]
+            else:
+                r = min(range(R // 2), key=lambda k: load[k])
+                load[r] += 1
+            stores[r].append(v)
+            stores[r + R // 2].append(t)
+        return dict(band=band, cut=cut, where=where, broles=broles, stores=stores, troles=troles, S=S, pair=True)
     units = [(len(m), ("m", m)) for m in comps.values()]
     broles = _pack(units, R)
-    owner = {}
     for r, lst in enumerate(broles):
         for _, m in lst:
             for u in m:
                 owner[u] = r
-    stores = [[] for _ in range(R)]
     load = [sum(len(m) for _, m in lst) for lst in broles]
     for v in cut_reads:
         if band(v) == "M":
@@ -584,13 +614,51 @@ def plan_roles(T, outs, hd, td, W, R):
             r = min(range(R), key=lambda k: load[k])
             load[r] += 1
         stores[r].append(v)
-    return dict(band=band, cut=cut, where=where, broles=broles, stores=stores, troles=troles, S=S)
+    return dict(band=band, cut=cut, where=where, broles=broles, stores=stores, troles=troles, S=S, pair=False)
 
 
-def emit_roles(v, n, R_t, hd, td, R):
+def _twins(T):
+    """Re/Im twins of a CDFT trace: nodes with the same structure over the
+    even (Re) and odd (Im) input cells.  par[u]: 1 Re only, 2 Im only, 3 both.
+    None when the structure does not pair up."""
+    key, par, intern = {}, [], {}
+
+    def cons(t):       # hash-consing: structurally equal nodes get one id
+        return intern.setdefault(t, len(intern))
+
+    for u, nd in enumerate(T.nodes):
+        if nd[0] == "in":
+            key[u] = cons(("in", nd[1] >> 1))
+            par.append(1 + (nd[1] & 1))
+            continue
+        ops = _operands(nd)
+        key[u] = cons((nd[0],) + tuple(key[o] for o in ops) + ((nd[2],) if nd[0] == "mul" else ()))
+        pr = 0
+        for o in ops:
+            pr |= par[o]
+        par.append(pr)
+    groups = {}
+    for u in range(len(T.nodes)):
+        if par[u] in (1, 2):
+            groups.setdefault((key[u], par[u]), []).append(u)
+    twin = {}
+    for (k, pr), lst in groups.items():
+        if pr != 1:
+            continue
+        other = groups.get((k, 2), [])
+        if len(other) != len(lst):
+            return None
+        for a, b in zip(lst, other):
+            twin[a] = b
+    return {"twin": twin, "par": par}
+
+
+def emit_roles(v, n, R_t, hd, td, R, pair=True):
     W = 4 if R_t == "float" else 2
     T, outs, ops = trace(v, 0, n)
-    P = plan_roles(T, outs, hd, td, W, R)
+    P = plan_roles(T, outs, hd, td, W, R, pair=pair)
+    pair = P["pair"]
+    NB = R // 2 if pair else R        # band-B code functions
     band, where = P["band"], P["where"]
     name = lambda u: (f"x{u}" if T.nodes[u][0] == "in" else f"t{u}")  # noqa: E731
 
@@ -612,14 +680,14 @@ def emit_roles(v, n, R_t, hd, td, R):
     for r in range(R):
         for val in P["stores"][r]:
             pos_owner[where[val]] = r
-    for r in range(R):
+    for r in range(NB):
         mids = sorted(u for _, m in P["broles"][r] for u in m)
         st_vals = P["stores"][r]
         head_roots = [o for u in mids for o in _operands(T.nodes[u]) if band(o) == "H"]
         head_roots += [val for val in st_vals if band(val) == "H"]
         head = sorted(_cone(T, head_roots, lambda z: band(z) != "H"))
         lines = [f"  template <class AR, class IO>",
-                 f"  static __device__ __forceinline__ void b{r}(IO& io, const {R_t}* __restrict__ tab) {{"]
+                 f"  static __device__ __forceinline__ void b{r}(IO& io, int part, const {R_t}* __restrict__ tab) {{"]
         loaded = set()
         live = 0
         for u in head:
@@ -628,8 +696,12 @@ def emit_roles(v, n, R_t, hd, td, R):
                 c = nd[1] // W
                 if c not in loaded:
                     loaded.add(c)
-                    nm = ", ".join(f"x{p}" for p in range(c * W, c * W + W))
-                    lines.append(f"    {R_t} {nm}; io.ld({c}, {nm});")
+                    if pair:      # the Re cells of chunk c (part 1: its Im cells)
+                        nm = ", ".join(f"x{p}" for p in range(c * W, c * W + W, 2))
+                        lines.append(f"    {R_t} {nm}; io.ldp({c}, part, {nm});")
+                    else:
+                        nm = ", ".join(f"x{p}" for p in range(c * W, c * W + W))
+                        lines.append(f"    {R_t} {nm}; io.ld({c}, {nm});")
             else:
                 lines.append(op_line(u))
         lines.append("    io.sync();")
@@ -654,9 +726,9 @@ def emit_roles(v, n, R_t, hd, td, R):
                     vals = []
                     for p in range(c * W, c * W + W):
                         vals.append(name(my_pos[p]) if p in my_pos else f"{R_t}(0)")
-                    lines.append(f"    io.str({c}, {', '.join(vals)});")
+                    lines.append(f"    io.str({c}, part, {', '.join(vals)});")
             else:
-                lines.append(f"    io.st1({q}, {name(val)});")
+                lines.append(f"    io.st1({q}, part, {name(val)});")
 
         for val in st_vals:            # head values / inputs stored as they are
             if band(val) == "H":
@@ -703,13 +775,17 @@ def emit_roles(v, n, R_t, hd, td, R):
     body = [f"template <> struct SmallRoles<{v}, {n.bit_length() - 1}, {R_t}> {{",
             f"  static constexpr int R = {R};",
             f"  static constexpr int ROWS = {COOP_ROWS.get((R_t, n), 32)};",
+            f"  static constexpr int HALF = {n};   // cells between a Re role's cut positions and its Im twin's",
             f"  static constexpr unsigned long long OPS[3] = {{{ops[0]}ull, {ops[1]}ull, {ops[2]}ull}};"]
     body += fns
     body.append("  template <class AR, class IO>")
     body.append(f"  static __device__ __forceinline__ void run(int role, IO& io, const {R_t}* __restrict__ tab) {{")
-    body.append("    switch (role) {")
+    body.append(f"    switch (role % {NB}) {{")
+    for r in range(NB):
+        body.append(f"      case {r}: b{r}<AR>(io, role / {NB}, tab); break;")
+    body += ["    }", "    switch (role) {"]
     for r in range(R):
-        body.append(f"      case {r}: b{r}<AR>(io, tab); c{r}<AR>(io, tab); break;")
+        body.append(f"      case {r}: c{r}<AR>(io, tab); break;")
     body += ["    }", "  }", "};"]
     return "\n".join(body), P, peaks
 

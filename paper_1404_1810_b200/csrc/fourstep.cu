@@ -213,8 +213,8 @@ int lg2(size_t v) {
 // throughput of each sub-size (B200, TB/s; tools/sweep_c3.py,
 // tools/prof_fast.py).
 double sub_tbs(int dtype, int lg) {
-  static const double f32[14] = {0, 5.0, 5.0, 5.0, 5.0, 5.0, 5.0, 2.5, 1.05, 0.6, 1.95, 2.6, 3.1, 2.2};
-  static const double f64[13] = {0, 5.5, 5.5, 5.5, 5.5, 5.5, 5.0, 2.65, 1.8, 0.0, 2.27, 2.68, 2.88};
+  static const double f32[14] = {0, 5.0, 5.0, 5.0, 5.0, 5.0, 5.0, 3.9, 1.78, 1.26, 1.72, 2.43, 3.17, 2.09};
+  static const double f64[13] = {0, 5.5, 5.5, 5.5, 5.5, 5.5, 5.4, 2.94, 2.06, 0.0, 2.27, 2.68, 2.88};
   if (dtype == AMQFT_F32) return lg < 14 ? f32[lg] : 0.0;
   return lg < 13 ? f64[lg] : 0.0;
 }

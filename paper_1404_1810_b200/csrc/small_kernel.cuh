@@ -210,25 +210,45 @@ k_small(const R* __restrict__ in, R* __restrict__ out, size_t rows,
 // their arena positions; band C: loads those chunks, barrier, computes and
 // stores whole output chunks.  The barriers are named (bar.sync 1) and
 // reached from every role's own code path.
-template <typename R, bool INV, int NTH> struct CoopIO;
-template <bool INV, int NTH> struct CoopIO<float, INV, NTH> : RowIO<float, INV> {
+// Band-B roles come in Re/Im pairs (generated code shared, part = 0 / 1):
+// ldp returns the chunk's Re cells (part 1: its Im cells; the swap-trick
+// inverse exchanges them), str/st1 store at the cut position shifted by
+// part * HALF cells (the Im half of the arena).
+template <typename R, bool INV, int NTH, int HALF> struct CoopIO;
+template <bool INV, int NTH, int HALF> struct CoopIO<float, INV, NTH, HALF> : RowIO<float, INV> {
+  __device__ __forceinline__ void ldp(int c, int part, float& a, float& b) const {
+    const float4 v = this->p[c];
+    const bool im = (part != 0) != INV;
+    a = im ? v.y : v.x;
+    b = im ? v.w : v.z;
+  }
   __device__ __forceinline__ void ldr(int c, float& a, float& b, float& d, float& e) const {
     const float4 v = this->p[c];
     a = v.x; b = v.y; d = v.z; e = v.w;
   }
-  __device__ __forceinline__ void str(int c, float a, float b, float d, float e) const {
-    this->p[c] = make_float4(a, b, d, e);
+  __device__ __forceinline__ void str(int c, int part, float a, float b, float d, float e) const {
+    this->p[c + part * (HALF / 4)] = make_float4(a, b, d, e);
   }
-  __device__ __forceinline__ void st1(int q, float a) const { reinterpret_cast<float*>(this->p)[q] = a; }
+  __device__ __forceinline__ void st1(int q, int part, float a) const {
+    reinterpret_cast<float*>(this->p)[q + part * HALF] = a;
+  }
   __device__ __forceinline__ void sync() const { asm volatile("bar.sync 1, %0;" ::"n"(NTH) : "memory"); }
 };
-template <bool INV, int NTH> struct CoopIO<double, INV, NTH> : RowIO<double, INV> {
+template <bool INV, int NTH, int HALF> struct CoopIO<double, INV, NTH, HALF> : RowIO<double, INV> {
+  __device__ __forceinline__ void ldp(int c, int part, double& a) const {
+    const double2 v = this->p[c];
+    a = ((part != 0) != INV) ? v.y : v.x;
+  }
   __device__ __forceinline__ void ldr(int c, double& a, double& b) const {
     const double2 v = this->p[c];
     a = v.x; b = v.y;
   }
-  __device__ __forceinline__ void str(int c, double a, double b) const { this->p[c] = make_double2(a, b); }
-  __device__ __forceinline__ void st1(int q, double a) const { reinterpret_cast<double*>(this->p)[q] = a; }
+  __device__ __forceinline__ void str(int c, int part, double a, double b) const {
+    this->p[c + part * (HALF / 2)] = make_double2(a, b);
+  }
+  __device__ __forceinline__ void st1(int q, int part, double a) const {
+    reinterpret_cast<double*>(this->p)[q + part * HALF] = a;
+  }
   __device__ __forceinline__ void sync() const { asm volatile("bar.sync 1, %0;" ::"n"(NTH) : "memory"); }
 };
 
@@ -283,7 +303,7 @@ k_coop(const R* __restrict__ in, R* __restrict__ out, size_t rows,
     parity ^= 1;
     // every lane runs (lanes past the tile's rows on stale data, not
     // stored): the roles' named barriers count all NTH threads
-    CoopIO<R, INV, C::NTH> io;
+    CoopIO<R, INV, C::NTH, C::G::HALF> io;
     io.p = reinterpret_cast<VT*>(sm + size_t(lane % C::ROWS) * C::STRIDE);
     io.scale = scale;
     C::G::template run<Arith<R>>(warp, io, tp.v);

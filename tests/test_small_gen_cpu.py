@@ -45,8 +45,9 @@ def test_small_schedule_in_place_safe():
                 assert stored == set(range(2 * n // W))
 
 
+@pytest.mark.parametrize("pair", [False, True])
 @pytest.mark.parametrize("dtype", ["float", "double"])
-def test_coop_roles_partition(dtype):
+def test_coop_roles_partition(dtype, pair):
     """Cooperative plans: every middle node belongs to exactly one role,
     every output chunk to exactly one tail role, and the tail only reads
     values the band-B roles store at the cut (so the two-band in-place
@@ -55,7 +56,16 @@ def test_coop_roles_partition(dtype):
     for n, (hd, td, R) in G.COOP[dtype].items():
         for v in (1, 2, 4, 7):
             T, outs, _ = G.trace(v, 0, n)
-            P = G.plan_roles(T, outs, hd, td, W, R)
+            P = G.plan_roles(T, outs, hd, td, W, R, pair=pair)
+            assert P["pair"] == pair
+            if pair:   # role r + R/2 runs the Im twins of role r's nodes, stored N cells further
+                tw = G._twins(T)["twin"]
+                for r in range(R // 2):
+                    re = sorted(u for _, m in P["broles"][r] for u in m)
+                    assert sorted(tw[u] for u in re) == sorted(u for _, m in P["broles"][r + R // 2] for u in m)
+                    assert [P["where"][tw[x]] for x in P["stores"][r]] == \
+                        [P["where"][x] + n for x in P["stores"][r + R // 2]] or \
+                        [P["where"][x] for x in P["stores"][r + R // 2]] == [P["where"][x] + n for x in P["stores"][r]]
             mids = [u for lst in P["broles"] for _, m in lst for u in m]
             assert len(mids) == len(set(mids))
             chunks = sorted(c for lst in P["troles"] for ch, _, _ in lst for c in ch)
@@ -78,7 +88,7 @@ def test_coop_two_band_emulation(oracle, restatement):
                 continue
             for v in (3, 4, 6):
                 T, outs, _ = G.trace(v, 0, n)
-                P = G.plan_roles(T, outs, hd, td, W, R)
+                P = G.plan_roles(T, outs, hd, td, W, R, pair=True)
                 x = r.uniform(r.mix_seed(99, v, n), 2 * n)
                 tab = r.trig_constants(v, n)
                 full = G.evaluate(T, list(range(len(T.nodes))), x, tab)
