@@ -10,11 +10,28 @@
 
 namespace amqft_b200 {
 
+// Four-step twiddles w_N^j (fourstep.cu): two half-size fp64 tables
+// (w^(jh B), w^(jl)) or sincospi on the fly.
+struct ColTwiddle {
+  const double2* hi = nullptr;
+  const double2* lo = nullptr;
+  int logb = 0, logn = 0, onthefly = 0;
+};
+
 class FastPlan {
  public:
   virtual ~FastPlan() = default;
   virtual void exec(const void* in, void* out, size_t rows, int inverse,
                     cudaStream_t st) = 0;
+  // Column mode (four-step first pass): `mats` matrices [N][cols] of
+  // complex values; transform every column (length N, stride cols) into
+  // `out` in the same layout, output k1 of column n2 multiplied by
+  // w^(n2 k1).  Inverse: input re/im exchanged (the swap trick's first
+  // half).  Returns false when the plan has no column mode.
+  virtual bool exec_columns(const void*, void*, size_t /*mats*/, size_t /*cols*/, int /*inverse*/,
+                            const ColTwiddle&, cudaStream_t) {
+    return false;
+  }
   int launches = 1;
 };
 

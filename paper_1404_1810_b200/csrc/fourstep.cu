@@ -208,8 +208,9 @@ int lg2(size_t v) {
 }
 
 // Split N = N1 N2 over covered sub-sizes (both >= 32 from N = 2^10 on, for
-// the tiled transposes; below that the element-wise transpose),
-// minimising the two DFT passes' time by the measured single-kernel HBM
+// the tiled transposes; below that the element-wise transpose), and the
+// column mode where N1 is a one-thread-per-row size,
+// minimising the two DFT passes' and the transposes' time by the measured HBM
 // throughput of each sub-size (B200, TB/s; tools/sweep_c3.py,
 // tools/prof_fast.py).
 double sub_tbs(int dtype, int lg) {
@@ -219,20 +220,33 @@ double sub_tbs(int dtype, int lg) {
   return lg < 13 ? f64[lg] : 0.0;
 }
 
-bool fourstep_split(int dtype, size_t n, size_t* n1, size_t* n2) {
+// Column mode: the first pass runs the one-thread-per-row kernel straight
+// on the columns of x (coalesced: a warp's lanes take consecutive columns)
+// with the twiddle fused into its stores, so transposes 1 and 2 vanish.
+bool col_capable(int dtype, int lg) { return lg >= 1 && lg <= (dtype == AMQFT_F32 ? 6 : 5); }
+
+bool fourstep_split(int dtype, size_t n, size_t* n1, size_t* n2, bool* col = nullptr) {
+  constexpr double kTransposeTBs = 6.9;   // measured k_transpose (B200)
   const int lg = lg2(n);
   double best = 0.0;
   for (int l1 = 1; l1 < lg; ++l1) {
     const int l2 = lg - l1;
-    if ((l1 < 5 || l2 < 5) && lg >= 10) continue;   // 32 x 32 tiled transposes where the sizes allow
     if (!fast_sub_covered(dtype, size_t(1) << l1) || !fast_sub_covered(dtype, size_t(1) << l2)) continue;
     const double a = sub_tbs(dtype, l1), b = sub_tbs(dtype, l2);
     if (a <= 0.0 || b <= 0.0) continue;
-    const double cost = 1.0 / a + 1.0 / b;
-    if (best == 0.0 || cost < best - 1e-9) {
-      best = cost;
-      *n1 = size_t(1) << l1;
-      *n2 = size_t(1) << l2;
+    for (int c = 0; c < 2; ++c) {
+      if (c == 1 && !col_capable(dtype, l1)) continue;
+      // tiled transposes need both sides >= 32 from N = 2^10 on (column
+      // mode: only the last transpose, N1 x N2)
+      if (c == 0 && (l1 < 5 || l2 < 5) && lg >= 10) continue;
+      if (c == 1 && (l1 < 5 || l2 < 5) && lg >= 10) continue;
+      const double cost = 1.0 / a + 1.0 / b + (c ? 1.0 : 3.0) / kTransposeTBs;
+      if (best == 0.0 || cost < best - 1e-9) {
+        best = cost;
+        *n1 = size_t(1) << l1;
+        *n2 = size_t(1) << l2;
+        if (col) *col = c == 1;
+      }
     }
   }
   return best > 0.0;
@@ -247,7 +261,7 @@ class FourStepPlan final : public FastPlan {
       : n_(n), batch_(batch), onthefly_(trig_mode == AMQFT_TRIG_ONTHEFLY) {
     logn_ = lg2(n);
     const int dtype = sizeof(R) == 8 ? AMQFT_F64 : AMQFT_F32;
-    if (!fourstep_split(dtype, n, &n1_, &n2_)) throw std::invalid_argument("four-step: no covered split");
+    if (!fourstep_split(dtype, n, &n1_, &n2_, &col_)) throw std::invalid_argument("four-step: no covered split");
     p1_ = make_fast_sub(variant, n1_, dtype, tab, nmax, dev);
     p2_ = make_fast_sub(variant, n2_, dtype, tab, nmax, dev);
     if (!p1_ || !p2_) throw std::invalid_argument("four-step: no fused kernel for the sub-transform sizes");
@@ -269,7 +283,7 @@ class FourStepPlan final : public FastPlan {
     check(cudaMemcpy(twh_, th.data(), NH * sizeof(double2), cudaMemcpyHostToDevice), "cudaMemcpy");
     check(cudaMemcpy(twl_, tl.data(), B * sizeof(double2), cudaMemcpyHostToDevice), "cudaMemcpy");
     check(cudaMalloc(&scratch_, batch_ * n_ * sizeof(V2)), "cudaMalloc four-step scratch");
-    launches = 3 + p1_->launches + p2_->launches;
+    launches = col_ ? 1 + p1_->launches + p2_->launches : 3 + p1_->launches + p2_->launches;
   }
   ~FourStepPlan() override {
     if (twh_) cudaFree(twh_);
@@ -282,6 +296,25 @@ class FourStepPlan final : public FastPlan {
     V2* y = static_cast<V2*>(out);
     V2* s = scratch_;
     const int R1 = static_cast<int>(n1_), C1 = static_cast<int>(n2_);
+    if (col_) {
+      // 1+2+3. columns of x [n1][n2] -> s [k1][n2], times w^(n2 k1)
+      ColTwiddle tw;
+      tw.hi = twh_;
+      tw.lo = twl_;
+      tw.logb = logb_;
+      tw.logn = logn_;
+      tw.onthefly = onthefly_ ? 1 : 0;
+      if (!p1_->exec_columns(x, s, rows, n2_, inverse, tw, st))
+        throw std::runtime_error("four-step: sub-plan has no column mode");
+      // 4. rows of length N2, in place: s [k1][k2]
+      p2_->exec(s, s, rows * n1_, 0, st);
+      // 5. s [k1][k2] -> y [k2][k1]
+      if (inverse)
+        launch_t<0, true, R>(s, y, rows, R1, C1, R(1) / static_cast<R>(n_), nullptr, nullptr, 0, logn_, 0, st);
+      else
+        launch_t<0, false, R>(s, y, rows, R1, C1, R(1), nullptr, nullptr, 0, logn_, 0, st);
+      return;
+    }
     // 1. x [n1][n2] -> s [n2][n1]
     if (inverse)
       launch_t<0, true, R>(x, s, rows, R1, C1, R(1), nullptr, nullptr, 0, logn_, 0, st);
@@ -307,6 +340,7 @@ class FourStepPlan final : public FastPlan {
   size_t n_, batch_, n1_ = 0, n2_ = 0;
   int logn_ = 0, logb_ = 0;
   bool onthefly_;
+  bool col_ = false;
   std::unique_ptr<FastPlan> p1_, p2_;
   double2* twh_ = nullptr;
   double2* twl_ = nullptr;

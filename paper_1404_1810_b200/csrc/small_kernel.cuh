@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <memory>
 #include <stdexcept>
+#include <type_traits>
 #include <vector>
 
 #include "fast.cuh"
@@ -364,6 +365,83 @@ class CoopPlanImpl final : public FastPlan {
   int grid_cap_ = 148;
 };
 
+// ---- Column mode (four-step first pass): thread = (matrix, column n2);
+// element n1 of the column at in[(n1 cols + n2)], consecutive threads on
+// consecutive columns (every load and store instruction of a warp touches
+// 256 contiguous bytes).  Output k1 goes to out[(k1 cols + n2)] times
+// w_N^(n2 k1) (fp64 twiddle, as the four-step transposes).
+template <typename R>
+__device__ __forceinline__ void col_twiddle(R& x, R& y, unsigned long long j, const ColTwiddle& t) {
+  j &= (1ull << t.logn) - 1ull;
+  double wr, wi;
+  if (t.onthefly) {
+    double sn, cs;
+    sincospi(static_cast<double>(j) * 2.0 / static_cast<double>(1ull << t.logn), &sn, &cs);
+    wr = cs;
+    wi = -sn;
+  } else {
+    const double2 a = t.hi[j >> t.logb], b = t.lo[j & ((1ull << t.logb) - 1ull)];
+    wr = a.x * b.x - a.y * b.y;
+    wi = a.x * b.y + a.y * b.x;
+  }
+  const R fr = static_cast<R>(wr), fi = static_cast<R>(wi);
+  const R nx = x * fr - y * fi, ny = x * fi + y * fr;
+  x = nx;
+  y = ny;
+}
+
+template <typename R, bool INV> struct ColIO;
+template <bool INV> struct ColIO<float, INV> {   // chunk c = complex 2c, 2c+1
+  const float2* __restrict__ pi;
+  float2* __restrict__ po;
+  size_t stride;
+  unsigned long long col;
+  ColTwiddle tw;
+  __device__ __forceinline__ void ld(int c, float& a, float& b, float& d, float& e) const {
+    const float2 u = __ldg(pi + size_t(2 * c) * stride), v = __ldg(pi + size_t(2 * c + 1) * stride);
+    if (INV) { a = u.y; b = u.x; d = v.y; e = v.x; }
+    else { a = u.x; b = u.y; d = v.x; e = v.y; }
+  }
+  __device__ __forceinline__ void st(int c, float a, float b, float d, float e) const {
+    col_twiddle(a, b, col * static_cast<unsigned long long>(2 * c), tw);
+    col_twiddle(d, e, col * static_cast<unsigned long long>(2 * c + 1), tw);
+    po[size_t(2 * c) * stride] = make_float2(a, b);
+    po[size_t(2 * c + 1) * stride] = make_float2(d, e);
+  }
+};
+template <bool INV> struct ColIO<double, INV> {  // chunk c = complex c
+  const double2* __restrict__ pi;
+  double2* __restrict__ po;
+  size_t stride;
+  unsigned long long col;
+  ColTwiddle tw;
+  __device__ __forceinline__ void ld(int c, double& a, double& b) const {
+    const double2 u = __ldg(pi + size_t(c) * stride);
+    if (INV) { a = u.y; b = u.x; }
+    else { a = u.x; b = u.y; }
+  }
+  __device__ __forceinline__ void st(int c, double a, double b) const {
+    col_twiddle(a, b, col * static_cast<unsigned long long>(c), tw);
+    po[size_t(c) * stride] = make_double2(a, b);
+  }
+};
+
+template <int V, typename R, int LOGN, bool INV>
+__global__ void __launch_bounds__(128)
+k_small_col(const R* __restrict__ in, R* __restrict__ out, size_t mats, size_t cols,
+            const __grid_constant__ TabP<R, SCfg<R, LOGN>::NT> tp, const ColTwiddle tw) {
+  using C2T = typename std::conditional<sizeof(R) == 4, float2, double2>::type;
+  using G = SmallGen<V, 0, LOGN, R>;
+  constexpr size_t N = size_t(1) << LOGN;
+  const size_t total = mats * cols;
+  for (size_t t = blockIdx.x * size_t(blockDim.x) + threadIdx.x; t < total; t += size_t(gridDim.x) * blockDim.x) {
+    const size_t mat = t / cols, col = t - mat * cols;
+    const size_t base = mat * N * cols + col;
+    ColIO<R, INV> io{reinterpret_cast<const C2T*>(in) + base, reinterpret_cast<C2T*>(out) + base, cols, col, tw};
+    G::template run<Arith<R>>(io, tp.v);
+  }
+}
+
 template <int V, typename R, int LOGN>
 class SmallPlanImpl final : public FastPlan {
   using C = SCfg<R, LOGN>;
@@ -403,6 +481,20 @@ class SmallPlanImpl final : public FastPlan {
                                                               tp_, scale);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+  }
+  bool exec_columns(const void* in, void* out, size_t mats, size_t cols, int inverse, const ColTwiddle& tw,
+                    cudaStream_t st) override {
+    const size_t total = mats * cols;
+    const unsigned grid = static_cast<unsigned>(std::min<size_t>((total + 127) / 128, size_t(148) * 16));
+    if (inverse)
+      k_small_col<V, R, LOGN, true><<<grid, 128, 0, st>>>(static_cast<const R*>(in), static_cast<R*>(out), mats,
+                                                           cols, tp_, tw);
+    else
+      k_small_col<V, R, LOGN, false><<<grid, 128, 0, st>>>(static_cast<const R*>(in), static_cast<R*>(out), mats,
+                                                            cols, tp_, tw);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+    return true;
   }
 
  private:
