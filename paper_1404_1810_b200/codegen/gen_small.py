@@ -38,6 +38,8 @@ FL_DESC, FL_ADD = 4, 8
 
 # Sizes covered per dtype (register budget: the live set of one thread).
 SIZES = {"float": (2, 4, 8, 16, 32, 64), "double": (2, 4, 8, 16, 32)}
+# RDFT rows (FunctionId::Rdft, N reals, packed spectrum): half the live set
+RDFT_SIZES = {"float": (4, 8, 16, 32, 64, 128), "double": (2, 4, 8, 16, 32, 64)}
 # Cooperative rows: N -> (head stages, tail stages, warp roles)
 COOP = {"float": {128: (2, 2, 4), 256: (3, 3, 8), 512: (4, 4, 16)},
         "double": {64: (2, 2, 4), 128: (3, 3, 8), 256: (4, 4, 16)}}
@@ -243,7 +245,7 @@ def trace(v, f, n):
     """(Trace, outputs): outputs[p] = node holding output cell p."""
     recs, stages, ops = _schedule_dump(v, f, n)
     nmax = max(n, 8)
-    cells = 2 * n if f == 0 else None
+    cells = {0: 2 * n, 1: n}.get(f)     # CDFT, RDFT (signal.cpp:118-223)
     if cells is None:
         import paper_1404_1810_b200 as amqft
         cells = amqft.cell_count(f, n)
@@ -818,23 +820,26 @@ def main():
     ops_lines = ["// GENERATED by codegen/gen_small.py: op counts of the generated small kernels.",
                  "#pragma once", "namespace amqft_b200 {", "namespace smallk {",
                  "// {adds, muls, halvings} for CDFT variant V, log2 N, dtype (0 fp32, 1 fp64); 0 = not covered",
-                 "struct SmallOps { int v, logn, f64; unsigned long long a, m, b; };",
+                 "struct SmallOps { int v, fn, logn, f64; unsigned long long a, m, b; };",
                  "static constexpr SmallOps kSmallOps[] = {"]
     for v in range(1, 9):
         out = [f"// small_gen_v{v}.cuh -- GENERATED by codegen/gen_small.py; do not edit.",
                "// Small CDFTs of AM-QFT variant %d: the traced stage program of plan.cpp as" % v,
                "// straight-line code (one reference add/sub/mul per line)."] + HEAD
-        for R, sizes in SIZES.items():
-            for n in sizes:
-                out.append(emit_fn(v, 0, n, R))
-                _, _, ops = trace(v, 0, n)
-                ops_lines.append(f"  {{{v}, {n.bit_length() - 1}, {int(R == 'double')}, {ops[0]}ull, {ops[1]}ull, {ops[2]}ull}},")
+        for fn, table in ((0, SIZES), (1, RDFT_SIZES)):
+            for R, sizes in table.items():
+                for n in sizes:
+                    out.append(emit_fn(v, fn, n, R))
+                    _, _, ops = trace(v, fn, n)
+                    ops_lines.append(f"  {{{v}, {fn}, {n.bit_length() - 1}, {int(R == 'double')}, "
+                                     f"{ops[0]}ull, {ops[1]}ull, {ops[2]}ull}},")
         for R, cfg in COOP.items():
             for n, (hd, td, nr) in cfg.items():
                 code, _, _ = emit_roles(v, n, R, hd, td, nr)
                 out.append(code)
                 _, _, ops = trace(v, 0, n)
-                ops_lines.append(f"  {{{v}, {n.bit_length() - 1}, {int(R == 'double')}, {ops[0]}ull, {ops[1]}ull, {ops[2]}ull}},")
+                ops_lines.append(f"  {{{v}, 0, {n.bit_length() - 1}, {int(R == 'double')}, "
+                                 f"{ops[0]}ull, {ops[1]}ull, {ops[2]}ull}},")
         out += TAIL
         with open(os.path.join(a.out, f"small_gen_v{v}.cuh"), "w") as f:
             f.write("\n".join(out))

@@ -127,29 +127,32 @@ __device__ __forceinline__ uint32_t s_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-template <typename R, int LOGN>
+// F: 0 CDFT rows (2N interleaved reals), 1 RDFT rows (N reals, packed
+// spectrum, signal.hpp:122-124)
+template <typename R, int LOGN, int F = 0>
 struct SCfg {
   static constexpr int N = 1 << LOGN;
+  static constexpr int CELLS = F == 0 ? 2 * N : N;
   static constexpr int NT = (N < 8 ? 8 : N) / 4;      // constant table (Nmax = max(N, 8))
-  static constexpr int ROWB = 2 * N * static_cast<int>(sizeof(R));
+  static constexpr int ROWB = CELLS * static_cast<int>(sizeof(R));
   static constexpr bool DIRECT = ROWB <= 64;   // measured: 128-B rows are faster staged
   static constexpr int STRIDE = ROWB + 16;             // padded slot (bytes)
   static constexpr int T = 128;                        // rows (threads) per CTA
   static constexpr size_t SMEM = DIRECT ? 0 : static_cast<size_t>(T) * STRIDE + 16;
 };
 
-template <int V, typename R, int LOGN, bool INV>
+template <int V, typename R, int LOGN, bool INV, int F = 0>
 __global__ void __launch_bounds__(128)
 k_small(const R* __restrict__ in, R* __restrict__ out, size_t rows,
-        const __grid_constant__ TabP<R, SCfg<R, LOGN>::NT> tp, R scale) {
-  using C = SCfg<R, LOGN>;
-  using G = SmallGen<V, 0, LOGN, R>;
+        const __grid_constant__ TabP<R, SCfg<R, LOGN, F>::NT> tp, R scale) {
+  using C = SCfg<R, LOGN, F>;
+  using G = SmallGen<V, F, LOGN, R>;
   using VT = typename Vec<R>::T;
-  constexpr int N = C::N;
+  constexpr int CELLS = C::CELLS;
   const int tid = threadIdx.x;
   if constexpr (C::DIRECT) {
     for (size_t row = blockIdx.x * size_t(C::T) + tid; row < rows; row += size_t(gridDim.x) * C::T) {
-      GRowIO<R, INV> io{reinterpret_cast<const VT*>(in + row * 2 * N), reinterpret_cast<VT*>(out + row * 2 * N),
+      GRowIO<R, INV> io{reinterpret_cast<const VT*>(in + row * CELLS), reinterpret_cast<VT*>(out + row * CELLS),
                         scale};
       G::template run<Arith<R>>(io, tp.v);
     }
@@ -175,7 +178,7 @@ k_small(const R* __restrict__ in, R* __restrict__ out, size_t rows,
         for (int r = lane; r < nr; r += 32)
           asm volatile(
               "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-              ::"r"(s_u32(sm + size_t(r) * C::STRIDE)), "l"(in + (row0 + r) * 2 * N), "r"(C::ROWB),
+              ::"r"(s_u32(sm + size_t(r) * C::STRIDE)), "l"(in + (row0 + r) * CELLS), "r"(C::ROWB),
                 "r"(s_u32(bar)) : "memory");
       }
       asm volatile(
@@ -193,7 +196,7 @@ k_small(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       if (warp == 0) {
         for (int r = lane; r < nr; r += 32)
           asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
-                       ::"l"(out + (row0 + r) * 2 * N), "r"(s_u32(sm + size_t(r) * C::STRIDE)), "r"(C::ROWB)
+                       ::"l"(out + (row0 + r) * CELLS), "r"(s_u32(sm + size_t(r) * C::STRIDE)), "r"(C::ROWB)
                        : "memory");
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -429,7 +432,7 @@ template <bool INV> struct ColIO<double, INV> {  // chunk c = complex c
 template <int V, typename R, int LOGN, bool INV>
 __global__ void __launch_bounds__(128)
 k_small_col(const R* __restrict__ in, R* __restrict__ out, size_t mats, size_t cols,
-            const __grid_constant__ TabP<R, SCfg<R, LOGN>::NT> tp, const ColTwiddle tw) {
+            const __grid_constant__ TabP<R, SCfg<R, LOGN, 0>::NT> tp, const ColTwiddle tw) {
   using C2T = typename std::conditional<sizeof(R) == 4, float2, double2>::type;
   using G = SmallGen<V, 0, LOGN, R>;
   constexpr size_t N = size_t(1) << LOGN;
@@ -442,9 +445,9 @@ k_small_col(const R* __restrict__ in, R* __restrict__ out, size_t mats, size_t c
   }
 }
 
-template <int V, typename R, int LOGN>
+template <int V, typename R, int LOGN, int F = 0>
 class SmallPlanImpl final : public FastPlan {
-  using C = SCfg<R, LOGN>;
+  using C = SCfg<R, LOGN, F>;
 
  public:
   SmallPlanImpl(const void* tab, uint32_t nmax, int device) {
@@ -453,8 +456,8 @@ class SmallPlanImpl final : public FastPlan {
     // level sharing, variants.cpp:281)
     cudaError_t e = fetch_table(tp_.v, C::NT, tab, nmax);
     if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
-    auto f0 = k_small<V, R, LOGN, false>;
-    auto f1 = k_small<V, R, LOGN, true>;
+    auto f0 = k_small<V, R, LOGN, false, F>;
+    auto f1 = k_small<V, R, LOGN, true, F>;
     if (C::SMEM > 48 * 1024) {
       e = cudaFuncSetAttribute(f0, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM));
       if (e == cudaSuccess)
@@ -474,16 +477,20 @@ class SmallPlanImpl final : public FastPlan {
     const unsigned grid = static_cast<unsigned>(std::min<size_t>(tiles, static_cast<size_t>(grid_cap_)));
     const R scale = R(1) / R(C::N);
     if (inverse)
-      k_small<V, R, LOGN, true><<<grid, C::T, C::SMEM, st>>>(static_cast<const R*>(in), static_cast<R*>(out), rows,
+      k_small<V, R, LOGN, true, F><<<grid, C::T, C::SMEM, st>>>(static_cast<const R*>(in), static_cast<R*>(out), rows,
                                                              tp_, scale);
     else
-      k_small<V, R, LOGN, false><<<grid, C::T, C::SMEM, st>>>(static_cast<const R*>(in), static_cast<R*>(out), rows,
+      k_small<V, R, LOGN, false, F><<<grid, C::T, C::SMEM, st>>>(static_cast<const R*>(in), static_cast<R*>(out), rows,
                                                               tp_, scale);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
   }
   bool exec_columns(const void* in, void* out, size_t mats, size_t cols, int inverse, const ColTwiddle& tw,
                     cudaStream_t st) override {
+    if constexpr (F != 0) {   // CDFT rows only
+      (void)in, (void)out, (void)mats, (void)cols, (void)inverse, (void)tw, (void)st;
+      return false;
+    } else {
     const size_t total = mats * cols;
     const unsigned grid = static_cast<unsigned>(std::min<size_t>((total + 127) / 128, size_t(148) * 16));
     if (inverse)
@@ -495,6 +502,7 @@ class SmallPlanImpl final : public FastPlan {
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
     return true;
+    }
   }
 
  private:
@@ -517,6 +525,24 @@ std::unique_ptr<FastPlan> make_small_sized(size_t n, const void* tab, uint32_t n
     case 256: return std::make_unique<CoopPlanImpl<V, R, 8>>(tab, nmax, dev);
     case 512:
       if constexpr (sizeof(R) == 4) return std::make_unique<CoopPlanImpl<V, R, 9>>(tab, nmax, dev);
+      break;
+  }
+  return nullptr;
+}
+
+template <int V, typename R>
+std::unique_ptr<FastPlan> make_small_rdft(size_t n, const void* tab, uint32_t nmax, int dev) {
+  switch (n) {
+    case 2:
+      if constexpr (sizeof(R) == 8) return std::make_unique<SmallPlanImpl<V, R, 1, 1>>(tab, nmax, dev);
+      break;
+    case 4: return std::make_unique<SmallPlanImpl<V, R, 2, 1>>(tab, nmax, dev);
+    case 8: return std::make_unique<SmallPlanImpl<V, R, 3, 1>>(tab, nmax, dev);
+    case 16: return std::make_unique<SmallPlanImpl<V, R, 4, 1>>(tab, nmax, dev);
+    case 32: return std::make_unique<SmallPlanImpl<V, R, 5, 1>>(tab, nmax, dev);
+    case 64: return std::make_unique<SmallPlanImpl<V, R, 6, 1>>(tab, nmax, dev);
+    case 128:
+      if constexpr (sizeof(R) == 4) return std::make_unique<SmallPlanImpl<V, R, 7, 1>>(tab, nmax, dev);
       break;
   }
   return nullptr;

@@ -6,5 +6,7 @@ namespace amqft_b200 {
 namespace smallk {
 template std::unique_ptr<FastPlan> make_small_sized<6, float>(size_t, const void*, uint32_t, int);
 template std::unique_ptr<FastPlan> make_small_sized<6, double>(size_t, const void*, uint32_t, int);
+template std::unique_ptr<FastPlan> make_small_rdft<6, float>(size_t, const void*, uint32_t, int);
+template std::unique_ptr<FastPlan> make_small_rdft<6, double>(size_t, const void*, uint32_t, int);
 }  // namespace smallk
 }  // namespace amqft_b200

@@ -6,5 +6,7 @@ namespace amqft_b200 {
 namespace smallk {
 template std::unique_ptr<FastPlan> make_small_sized<7, float>(size_t, const void*, uint32_t, int);
 template std::unique_ptr<FastPlan> make_small_sized<7, double>(size_t, const void*, uint32_t, int);
+template std::unique_ptr<FastPlan> make_small_rdft<7, float>(size_t, const void*, uint32_t, int);
+template std::unique_ptr<FastPlan> make_small_rdft<7, double>(size_t, const void*, uint32_t, int);
 }  // namespace smallk
 }  // namespace amqft_b200

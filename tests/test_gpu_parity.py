@@ -597,3 +597,35 @@ def test_fourstep_fp32_between_kernel_sizes(oracle, restatement):
         got = run_plan(_fourstep_plan(4, n, 2), [x, x])
         assert got[0].tobytes() == got[1].tobytes()
         assert r.rel_l2(got[0], want) <= 1e-5 * lg, lg
+
+
+RDFT_SMALL = {"f64": (2, 4, 8, 16, 32, 64), "f32": (4, 8, 16, 32, 64, 128)}
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_small_kernel_rdft_rows(oracle, restatement, dtype):
+    """FunctionId::Rdft on the one-thread-per-row kernel (SURVEY 8(f) rank
+    1): N reals in, the packed spectrum out (signal.hpp:122-124).  fp64
+    bitwise the oracle for all 8 variants, fp32 bitwise the fp32 exact
+    path; 200 rows (partial tiles); op counts = the reference meter."""
+    r, O = restatement, oracle
+    rows = 200
+    for n in RDFT_SMALL[dtype]:
+        xs = np.random.default_rng(n + 7).uniform(-1, 1, (rows, n))
+        if dtype == "f32":
+            xs = xs.astype(np.float32).astype(np.float64)
+        for v in range(1, 9):
+            plan = amqft.Plan(v, amqft.FunctionId.Rdft, n, rows, dtype=dtype, order=amqft.Order.Fast)
+            assert plan.path()[0] == 4, (v, n)
+            got = run_plan(plan, xs)
+            assert plan.op_counts() == r.execute(v, O.F_RDFT, n, xs[0], meter=True)[1]
+            if dtype == "f64":
+                for row in (0, 127, 128, 199):
+                    assert got[row].tobytes() == r.execute(v, O.F_RDFT, n, xs[row]).tobytes(), (v, n, row)
+            else:
+                ex = amqft.Plan(v, amqft.FunctionId.Rdft, n, rows, dtype="f32", order=amqft.Order.Exact)
+                assert got.tobytes() == run_plan(ex, xs).tobytes(), (v, n)
+            with pytest.raises(amqft.InvalidArgument):
+                plan.inverse(torch.zeros(rows, n, dtype=torch.float64 if dtype == "f64" else torch.float32,
+                                         device=DEV), torch.empty(rows, n, device=DEV,
+                                                                  dtype=torch.float64 if dtype == "f64" else torch.float32))
