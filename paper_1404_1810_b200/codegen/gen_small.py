@@ -40,6 +40,9 @@ FL_DESC, FL_ADD = 4, 8
 SIZES = {"float": (2, 4, 8, 16, 32, 64), "double": (2, 4, 8, 16, 32)}
 # RDFT rows (FunctionId::Rdft, N reals, packed spectrum): half the live set
 RDFT_SIZES = {"float": (4, 8, 16, 32, 64, 128), "double": (2, 4, 8, 16, 32, 64)}
+# DCT-0 / DST-0 rows (FunctionId::Dct/Dst; N/2 + 1 / N/2 - 1 cells)
+DCT_SIZES = {"float": (4, 8, 16, 32, 64, 128, 256), "double": (4, 8, 16, 32, 64, 128)}
+DST_SIZES = {"float": (8, 16, 32, 64, 128, 256), "double": (8, 16, 32, 64, 128)}
 # Cooperative rows: N -> (head stages, tail stages, warp roles)
 COOP = {"float": {128: (2, 2, 4), 256: (3, 3, 8), 512: (4, 4, 16)},
         "double": {64: (2, 2, 4), 128: (3, 3, 8), 256: (4, 4, 16)}}
@@ -245,7 +248,7 @@ def trace(v, f, n):
     """(Trace, outputs): outputs[p] = node holding output cell p."""
     recs, stages, ops = _schedule_dump(v, f, n)
     nmax = max(n, 8)
-    cells = {0: 2 * n, 1: n}.get(f)     # CDFT, RDFT (signal.cpp:118-223)
+    cells = {0: 2 * n, 1: n, 2: n // 2 + 1, 3: n // 2 - 1}.get(f)   # CDFT, RDFT, DCT, DST (signal.cpp:118-223)
     if cells is None:
         import paper_1404_1810_b200 as amqft
         cells = amqft.cell_count(f, n)
@@ -442,7 +445,9 @@ def max_live(T, outs, prog, W):
 
 
 def emit_fn(v, f, n, R):
-    W = 4 if R == "float" else 2
+    # chunk width: 16-byte vectors for CDFT/RDFT rows; DCT/DST rows (N/2 +- 1
+    # cells, odd) are scalar (their odd smem row stride is conflict-free)
+    W = 1 if f in (2, 3) else (4 if R == "float" else 2)
     T, outs, ops = trace(v, f, n)
     prog = schedule_trace(T, outs, W)
     name = lambda u: (f"x{u}" if T.nodes[u][0] == "in" else f"t{u}")  # noqa: E731
@@ -826,7 +831,7 @@ def main():
         out = [f"// small_gen_v{v}.cuh -- GENERATED by codegen/gen_small.py; do not edit.",
                "// Small CDFTs of AM-QFT variant %d: the traced stage program of plan.cpp as" % v,
                "// straight-line code (one reference add/sub/mul per line)."] + HEAD
-        for fn, table in ((0, SIZES), (1, RDFT_SIZES)):
+        for fn, table in ((0, SIZES), (1, RDFT_SIZES), (2, DCT_SIZES), (3, DST_SIZES)):
             for R, sizes in table.items():
                 for n in sizes:
                     out.append(emit_fn(v, fn, n, R))

@@ -48,6 +48,8 @@ template <int V, typename R>
 std::unique_ptr<FastPlan> make_small_sized(size_t n, const void* tab, uint32_t nmax, int dev);
 template <int V, typename R>
 std::unique_ptr<FastPlan> make_small_rdft(size_t n, const void* tab, uint32_t nmax, int dev);
+template <int V, typename R>
+std::unique_ptr<FastPlan> make_small_dctdst(int fn, size_t n, const void* tab, uint32_t nmax, int dev);
 
 bool small_ops_n(int v, size_t n, bool f64, OpCount* o, int fn = AMQFT_FN_CDFT) {
   for (const SmallOps& e : kSmallOps)
@@ -65,7 +67,9 @@ std::unique_ptr<FastPlan> make_small_typed(int v, size_t n, const void* tab, uin
   switch (v) {
 #define AMQFT_SMALL_CASE(V) \
   case V: if (!small_ops_n(V, n, sizeof(R) == 8, o, fn)) return nullptr; \
-    return fn == AMQFT_FN_RDFT ? make_small_rdft<V, R>(n, tab, nmax, dev) : make_small_sized<V, R>(n, tab, nmax, dev);
+    return fn == AMQFT_FN_RDFT ? make_small_rdft<V, R>(n, tab, nmax, dev)                                  \
+         : fn == AMQFT_FN_CDFT ? make_small_sized<V, R>(n, tab, nmax, dev)                                 \
+                               : make_small_dctdst<V, R>(fn, n, tab, nmax, dev);
     AMQFT_SMALL_CASE(1) AMQFT_SMALL_CASE(2) AMQFT_SMALL_CASE(3) AMQFT_SMALL_CASE(4)
     AMQFT_SMALL_CASE(5) AMQFT_SMALL_CASE(6) AMQFT_SMALL_CASE(7) AMQFT_SMALL_CASE(8)
 #undef AMQFT_SMALL_CASE
@@ -76,7 +80,7 @@ std::unique_ptr<FastPlan> make_small_typed(int v, size_t n, const void* tab, uin
 
 std::unique_ptr<FastPlan> make_small_plan(const amqft_plan_desc& d, const void* d_trig, uint32_t nmax,
                                           OpCount* ops) {
-  if ((d.function != AMQFT_FN_CDFT && d.function != AMQFT_FN_RDFT) || d.trig_mode != AMQFT_TRIG_TABLE) return nullptr;
+  if (d.function > AMQFT_FN_DST || d.trig_mode != AMQFT_TRIG_TABLE) return nullptr;
   if (d.dtype == AMQFT_F32)
     return smallk::make_small_typed<float>(d.variant, d.n, d_trig, nmax, d.device, ops, d.function);
   return smallk::make_small_typed<double>(d.variant, d.n, d_trig, nmax, d.device, ops, d.function);

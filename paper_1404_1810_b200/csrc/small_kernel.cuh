@@ -548,5 +548,147 @@ std::unique_ptr<FastPlan> make_small_rdft(size_t n, const void* tab, uint32_t nm
   return nullptr;
 }
 
+// ---- DCT-0 / DST-0 rows (FunctionId::Dct / Dst, N/2 + 1 / N/2 - 1 cells,
+// oracle.hpp:38-41): scalar cells.  A 128-row tile is contiguous in global
+// memory (a multiple of 16 bytes), so one bulk copy brings it in; the odd
+// row stride makes lane-per-row scalar accesses conflict-free.  The rows
+// past the last full tile are read and written straight from global memory.
+template <typename R> struct ScalarIO {
+  R* p;
+  __device__ __forceinline__ void ld(int c, R& a) const { a = p[c]; }
+  __device__ __forceinline__ void st(int c, R a) const { p[c] = a; }
+};
+template <typename R> struct GScalarIO {
+  const R* __restrict__ pi;
+  R* __restrict__ po;
+  __device__ __forceinline__ void ld(int c, R& a) const { a = __ldg(pi + c); }
+  __device__ __forceinline__ void st(int c, R a) const { po[c] = a; }
+};
+
+template <typename R, int LOGN, int F>
+struct KCfg {
+  static constexpr int N = 1 << LOGN;
+  static constexpr int CELLS = F == 2 ? N / 2 + 1 : N / 2 - 1;
+  static constexpr int NT = (N < 8 ? 8 : N) / 4;
+  static constexpr int T = 128;
+  static constexpr uint32_t TILEB = static_cast<uint32_t>(T) * CELLS * sizeof(R);
+  static constexpr size_t SMEM = TILEB + 16;
+  static_assert(TILEB % 16 == 0, "bulk copies move multiples of 16 bytes");
+};
+
+template <int V, typename R, int LOGN, int F>
+__global__ void __launch_bounds__(128)
+k_scalar(const R* __restrict__ in, R* __restrict__ out, size_t rows,
+         const __grid_constant__ TabP<R, KCfg<R, LOGN, F>::NT> tp) {
+  using C = KCfg<R, LOGN, F>;
+  using G = SmallGen<V, F, LOGN, R>;
+  extern __shared__ __align__(128) unsigned char sm[];
+  R* tile_s = reinterpret_cast<R*>(sm);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::TILEB);
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(bar)), "r"(1) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t parity = 0;
+  const size_t full = rows / C::T;
+  for (size_t tile = blockIdx.x; tile < full; tile += gridDim.x) {
+    const R* src = in + tile * C::T * C::CELLS;
+    if (tid == 0) {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                   ::"r"(s_u32(bar)), "r"(C::TILEB) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(s_u32(tile_s)), "l"(src), "r"(C::TILEB), "r"(s_u32(bar)) : "memory");
+    }
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(s_u32(bar)), "r"(parity) : "memory");
+    parity ^= 1;
+    ScalarIO<R> io{tile_s + tid * C::CELLS};
+    G::template run<Arith<R>>(io, tp.v);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                   ::"l"(out + tile * C::T * C::CELLS), "r"(s_u32(tile_s)), "r"(C::TILEB) : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+    __syncthreads();
+  }
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (blockIdx.x == gridDim.x - 1) {   // rows past the last full tile
+    const size_t row = full * C::T + tid;
+    if (row < rows) {
+      GScalarIO<R> io{in + row * C::CELLS, out + row * C::CELLS};
+      G::template run<Arith<R>>(io, tp.v);
+    }
+  }
+}
+
+template <int V, typename R, int LOGN, int F>
+class ScalarPlanImpl final : public FastPlan {
+  using C = KCfg<R, LOGN, F>;
+
+ public:
+  ScalarPlanImpl(const void* tab, uint32_t nmax, int device) {
+    cudaError_t e = fetch_table(tp_.v, C::NT, tab, nmax);
+    if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+    auto f0 = k_scalar<V, R, LOGN, F>;
+    if (C::SMEM > 48 * 1024) {
+      e = cudaFuncSetAttribute(f0, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM));
+      if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+    }
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f0, C::T, C::SMEM);
+    if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    grid_cap_ = std::max(1, per_sm) * sms;
+    launches = 1;
+  }
+  void exec(const void* in, void* out, size_t rows, int inverse, cudaStream_t st) override {
+    if (inverse) throw std::invalid_argument("the inverse is defined for CDFT plans only");
+    const size_t full = rows / C::T;
+    const unsigned grid = static_cast<unsigned>(std::max<size_t>(1, std::min<size_t>(full, grid_cap_)));
+    k_scalar<V, R, LOGN, F><<<grid, C::T, C::SMEM, st>>>(static_cast<const R*>(in), static_cast<R*>(out), rows,
+                                                         tp_);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+  }
+
+ private:
+  TabP<R, C::NT> tp_{};
+  int grid_cap_ = 148;
+};
+
+template <int V, typename R>
+std::unique_ptr<FastPlan> make_small_dctdst(int fn, size_t n, const void* tab, uint32_t nmax, int dev) {
+#define AMQFT_SCALAR_CASE(LG)                                                                         \
+  case (1 << LG):                                                                                     \
+    if (fn == AMQFT_FN_DCT) return std::make_unique<ScalarPlanImpl<V, R, LG, 2>>(tab, nmax, dev);     \
+    if (LG >= 3) return std::make_unique<ScalarPlanImpl<V, R, (LG >= 3 ? LG : 3), 3>>(tab, nmax, dev); \
+    break;
+  switch (n) {
+    AMQFT_SCALAR_CASE(2)
+    AMQFT_SCALAR_CASE(3)
+    AMQFT_SCALAR_CASE(4)
+    AMQFT_SCALAR_CASE(5)
+    AMQFT_SCALAR_CASE(6)
+    AMQFT_SCALAR_CASE(7)
+    case 256:
+      if constexpr (sizeof(R) == 4) {
+        if (fn == AMQFT_FN_DCT) return std::make_unique<ScalarPlanImpl<V, R, 8, 2>>(tab, nmax, dev);
+        return std::make_unique<ScalarPlanImpl<V, R, 8, 3>>(tab, nmax, dev);
+      }
+      break;
+  }
+#undef AMQFT_SCALAR_CASE
+  return nullptr;
+}
+
 }  // namespace smallk
 }  // namespace amqft_b200

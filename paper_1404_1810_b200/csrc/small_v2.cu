@@ -8,5 +8,7 @@ template std::unique_ptr<FastPlan> make_small_sized<2, float>(size_t, const void
 template std::unique_ptr<FastPlan> make_small_sized<2, double>(size_t, const void*, uint32_t, int);
 template std::unique_ptr<FastPlan> make_small_rdft<2, float>(size_t, const void*, uint32_t, int);
 template std::unique_ptr<FastPlan> make_small_rdft<2, double>(size_t, const void*, uint32_t, int);
+template std::unique_ptr<FastPlan> make_small_dctdst<2, float>(int, size_t, const void*, uint32_t, int);
+template std::unique_ptr<FastPlan> make_small_dctdst<2, double>(int, size_t, const void*, uint32_t, int);
 }  // namespace smallk
 }  // namespace amqft_b200

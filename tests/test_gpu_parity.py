@@ -629,3 +629,34 @@ def test_small_kernel_rdft_rows(oracle, restatement, dtype):
                 plan.inverse(torch.zeros(rows, n, dtype=torch.float64 if dtype == "f64" else torch.float32,
                                          device=DEV), torch.empty(rows, n, device=DEV,
                                                                   dtype=torch.float64 if dtype == "f64" else torch.float32))
+
+
+DCTDST_SMALL = {"f64": {2: (4, 8, 16, 32, 64, 128), 3: (8, 16, 32, 64, 128)},
+                "f32": {2: (4, 8, 16, 32, 64, 128, 256), 3: (8, 16, 32, 64, 128, 256)}}
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_small_kernel_dct_dst_rows(oracle, restatement, dtype):
+    """FunctionId::Dct / Dst (DCT-0 / DST-0, N/2 + 1 / N/2 - 1 cells) on the
+    one-thread-per-row scalar kernel: fp64 bitwise the oracle for every
+    variant, fp32 bitwise the fp32 exact path; 300 rows = two bulk-copied
+    128-row tiles + 44 rows straight from global memory."""
+    r, O = restatement, oracle
+    rows = 300
+    for f, sizes in DCTDST_SMALL[dtype].items():
+        for n in sizes:
+            cells = amqft.cell_count(f, n)
+            xs = np.random.default_rng(10 * n + f).uniform(-1, 1, (rows, cells))
+            if dtype == "f32":
+                xs = xs.astype(np.float32).astype(np.float64)
+            for v in range(1, 9):
+                plan = amqft.Plan(v, f, n, rows, dtype=dtype, order=amqft.Order.Fast)
+                assert plan.path()[0] == 4, (f, v, n)
+                got = run_plan(plan, xs)
+                assert plan.op_counts() == r.execute(v, f, n, xs[0], meter=True)[1]
+                if dtype == "f64":
+                    for row in (0, 127, 128, 255, 256, 299):
+                        assert got[row].tobytes() == r.execute(v, f, n, xs[row]).tobytes(), (f, v, n, row)
+                else:
+                    ex = amqft.Plan(v, f, n, rows, dtype="f32", order=amqft.Order.Exact)
+                    assert got.tobytes() == run_plan(ex, xs).tobytes(), (f, v, n)
