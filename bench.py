@@ -18,6 +18,7 @@ its sources) on the host cores over a bounded sample of the same workload.
 from __future__ import annotations
 
 import argparse
+import math
 import json
 import os
 import statistics
@@ -275,6 +276,46 @@ def oracle_checks(args, kept, amqft, kept_v=None):
     return parity, out
 
 
+def config4_accuracy(amqft, x, n, local, stream, args):
+    """BASELINE config 4: every variant's fp32 result against an fp64 result
+    of the same input, with the tabulated and the on-the-fly half-size
+    twiddle sets.  The fp64 result is the GPU fp64 four-step of variant 4
+    (sub-transforms bitwise the reference recursion), itself checked
+    against numpy's fp64 FFT (C4 is beyond a timely CPU
+    oracle)."""
+    import numpy as np
+    import torch
+    ref = amqft.Plan(4, amqft.FunctionId.Cdft, n, 1, dtype="f64", order=amqft.Order.Fast, device=local)
+    xd = x.double()
+    y64 = torch.empty_like(xd)
+    ref.forward(xd, y64, stream=stream)
+    torch.cuda.synchronize()
+    xh = xd[0].cpu().numpy()
+    f = np.fft.fft(xh[0::2] + 1j * xh[1::2])
+    fh = np.empty(2 * n)
+    fh[0::2], fh[1::2] = f.real, f.imag
+    yh = y64[0].cpu().numpy()
+    out = {"reference": "GPU fp64 four-step, variant 4",
+           "reference_vs_numpy_fft_rel_l2": float(np.linalg.norm(yh - fh) / np.linalg.norm(fh))}
+    del ref
+    y = torch.empty_like(x)
+    for trig, key in ((amqft.TrigMode.Precomputed, "table"), (amqft.TrigMode.OnTheFly, "onthefly")):
+        errs = {}
+        for v in range(1, 9):
+            p = amqft.Plan(v, amqft.FunctionId.Cdft, n, 1, dtype="f32", order=amqft.Order.Fast, trig_mode=trig,
+                           device=local)
+            p.forward(x, y, stream=stream)
+            torch.cuda.synchronize()
+            e = float((y.double() - y64).norm() / y64.norm())
+            errs[str(v)] = e if math.isfinite(e) else str(e)
+            if v == args.variant:
+                out[f"ms_{key}"] = _timed(lambda: p.forward(x, y, stream=stream), 5, 2, stream, 1, torch.device(f"cuda:{local}"))
+            del p
+        out[f"rel_l2_fp32_vs_fp64_{key}"] = errs
+    out["tolerance_fp32"] = 1e-5 * 24
+    return out
+
+
 def bench_single(args, world, rank, local):
     """Configs 4 (N=2^24, one GPU, four-step) and 5 (N=2^30, distributed
     four-step over the ranks, one all-to-all)."""
@@ -310,6 +351,8 @@ def bench_single(args, world, rank, local):
         e2e = {"value": world / (e2e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": 8 * n,
                "d2h_bytes_per_step": 8 * n}
         extra = {"hbm_passes": 5, "traffic_model_bytes": 5 * 16 * n}
+        if rank == 0:
+            extra["accuracy"] = config4_accuracy(amqft, x, n, local, stream, args)
         cpu = cpu_baseline_large(args.variant, n, 1 << 20) if (rank == 0 and not args.no_cpu_baseline) else None
     else:
         n = 1 << 30
