@@ -99,7 +99,10 @@ amqft_status amqft_plan_destroy(amqft_plan plan);
 /* Cells per row of the plan's operand (cell_count, signal.cpp:254-258). */
 size_t amqft_plan_cells(amqft_plan plan);
 
-/* Forward transform of `plan->batch` rows: d_in -> d_out (may alias). */
+/* Forward transform of `plan->batch` rows: d_in -> d_out (may alias).
+ * Fast-order plans (fused, four-step and small-CDFT kernels) need 16-byte
+ * aligned device buffers (TMA bulk copies, 16-byte vectors): AMQFT_EINVAL
+ * otherwise.  Exact-order plans take any alignment of the dtype. */
 amqft_status amqft_exec_forward(amqft_plan plan, const void* d_in, void* d_out,
                                 void* stream);
 

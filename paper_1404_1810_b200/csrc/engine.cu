@@ -348,6 +348,10 @@ amqft_status amqft_exec_rows(amqft_plan P, const void* in, void* out, size_t row
     return set_err(AMQFT_EINVAL, "the inverse is defined for CDFT plans only");
   if (rows == 0) return AMQFT_OK;
   if (!in || !out) return set_err(AMQFT_EINVAL, "null data pointer");
+  // the fused, four-step and small-CDFT kernels move rows with TMA bulk
+  // copies and 16-byte vectors: their device buffers must be 16-byte aligned
+  if (P->path >= 2 && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15u))
+    return set_err(AMQFT_EINVAL, "device buffers of fast-order plans must be 16-byte aligned");
   try {
     ck(cudaSetDevice(P->d.device), "cudaSetDevice");
     cudaStream_t st = static_cast<cudaStream_t>(stream);

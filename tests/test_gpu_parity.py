@@ -660,3 +660,25 @@ def test_small_kernel_dct_dst_rows(oracle, restatement, dtype):
                 else:
                     ex = amqft.Plan(v, f, n, rows, dtype="f32", order=amqft.Order.Exact)
                     assert got.tobytes() == run_plan(ex, xs).tobytes(), (f, v, n)
+
+
+def test_fast_plans_reject_misaligned_buffers():
+    """Fast-order plans move rows with TMA bulk copies: a device pointer that
+    is not 16-byte aligned (e.g. a view starting at row 1 of DCT rows, 4*9
+    bytes in) is rejected with AMQFT_EINVAL instead of faulting; the exact
+    path accepts it."""
+    n, rows = 16, 8
+    cells = amqft.cell_count(amqft.FunctionId.Dct, n)
+    x = torch.randn(rows + 1, cells, dtype=torch.float32, device=DEV)
+    y = torch.empty_like(x)
+    fast = amqft.Plan(4, amqft.FunctionId.Dct, n, rows, dtype="f32", order=amqft.Order.Fast)
+    with pytest.raises(amqft.InvalidArgument):
+        fast.forward(x[1:], y[1:], rows=rows)
+    exact = amqft.Plan(4, amqft.FunctionId.Dct, n, rows, dtype="f32", order=amqft.Order.Exact)
+    exact.forward(x[1:], y[1:], rows=rows)
+    fast.forward(x[:rows], y[:rows], rows=rows)
+    torch.cuda.synchronize()
+    z = torch.empty(rows, cells, dtype=torch.float32, device=DEV)
+    exact.forward(x[:rows].contiguous(), z, rows=rows)
+    torch.cuda.synchronize()
+    assert torch.equal(z, y[:rows])
