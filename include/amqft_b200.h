@@ -21,9 +21,12 @@
  *    DCT = N/2+1, DST = N/2-1, restricted types per their stored ranges.
  *    Batches are row-major: row r starts at r * cells.
  *  - Transforms are unnormalised forward sums with kernel e^{-2 pi i nk/N}
- *    (src/oracle.cpp:69-84).  amqft_exec_inverse (CDFT only) is the
- *    builder-defined inverse x = swap(DFT(swap(X))) / N, exact in its swap
- *    and power-of-two scale.
+ *    (src/oracle.cpp:69-84).  amqft_exec_inverse is builder-defined (the
+ *    reference has none): CDFT x = swap(DFT(swap(X))) / N; DCT-0
+ *    x = (4/N) W DCT(W C), W = diag(1/2, 1, .., 1, 1/2); DST-0
+ *    x = (4/N) DST(S); RDFT through those two on the split packed spectrum
+ *    (csrc/inverse.cu).  Only exact power-of-two scalings and one butterfly
+ *    are added to the forward transforms.
  *  - Errors mirror the reference's std::invalid_argument cases
  *    (variants.cpp:404-421, signal.cpp:138-147) as AMQFT_EINVAL;
  *    amqft_last_error() returns the message (thread-local).
@@ -106,7 +109,8 @@ size_t amqft_plan_cells(amqft_plan plan);
 amqft_status amqft_exec_forward(amqft_plan plan, const void* d_in, void* d_out,
                                 void* stream);
 
-/* Inverse CDFT of `batch` rows (swap trick; CDFT plans only). */
+/* Inverse of `batch` rows: CDFT (swap trick), RDFT / DCT / DST (n >= 4);
+ * AMQFT_EINVAL for the odd-function plans. */
 amqft_status amqft_exec_inverse(amqft_plan plan, const void* d_in, void* d_out,
                                 void* stream);
 

@@ -175,6 +175,31 @@ class Restatement(_Backend):
         self._check(self.lib.oracle_inverse_cdft(v, n, x, out))
         return out
 
+    def inverse_real(self, v: int, f: int, n: int, spectrum) -> np.ndarray:
+        """Builder-defined inverses of the real transforms on top of the
+        reference forward (csrc/inverse.cu): DCT-0 (4/N) W DCT(W C), DST-0
+        (4/N) DST(S), RDFT through both on the split packed spectrum; the
+        same operations in the same order as the device."""
+        y = np.ascontiguousarray(spectrum, dtype=np.float64)
+        h = n // 2
+        if f == F_DST:
+            return self.execute(v, F_DST, n, y) * (4.0 / n)
+        w = np.ones(h + 1)
+        w[0] = w[-1] = 0.5
+        if f == F_DCT:
+            sc = np.full(h + 1, 4.0 / n)
+            sc[0] = sc[-1] = 2.0 / n
+            return self.execute(v, F_DCT, n, y * w) * sc
+        assert f == F_RDFT
+        c = self.execute(v, F_DCT, n, y[:h + 1] * w) * (4.0 / n)
+        s = self.execute(v, F_DST, n, y[h + 1:][::-1].copy()) * (4.0 / n)
+        x = np.empty(n)
+        x[0], x[h] = c[0] * 0.5, c[h] * 0.5
+        m = np.arange(1, h)
+        x[m] = (c[m] + s[m - 1]) * 0.5
+        x[n - m] = (c[m] - s[m - 1]) * 0.5
+        return x
+
     def reference_spectrum(self, signal_type: int, n: int, x) -> np.ndarray:
         x = np.ascontiguousarray(x, dtype=np.float64)
         out = np.empty(self.cell_count(signal_type, n), dtype=np.float64)

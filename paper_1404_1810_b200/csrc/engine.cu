@@ -24,6 +24,7 @@
 #include "fast.cuh"
 #include "fourstep.cuh"
 #include "generic_exec.hpp"
+#include "inverse.cuh"
 #include "plan.hpp"
 #include "trig.hpp"
 
@@ -93,8 +94,17 @@ struct amqft_plan_s {
   size_t slot_rows = 0;
   cudaStream_t s_h2d = nullptr, s_run = nullptr, s_d2h = nullptr;
   cudaEvent_t ev_h2d[NSLOT] = {}, ev_run[NSLOT] = {}, ev_d2h[NSLOT] = {}, ev_in = nullptr;
+  // inverses of the real transforms (inverse.cu), created on first use
+  void* inv_a = nullptr;
+  void* inv_b = nullptr;
+  amqft_plan_s* inv_dct = nullptr;
+  amqft_plan_s* inv_dst = nullptr;
 
   ~amqft_plan_s() {
+    delete inv_dct;
+    delete inv_dst;
+    if (inv_a) cudaFree(inv_a);
+    if (inv_b) cudaFree(inv_b);
     int cur = 0;
     cudaGetDevice(&cur);
     cudaSetDevice(d.device);
@@ -340,12 +350,75 @@ amqft_status amqft_plan_destroy(amqft_plan plan) {
 
 size_t amqft_plan_cells(amqft_plan plan) { return plan ? plan->c.cells : 0; }
 
+namespace {
+
+bool inverse_defined(const amqft_plan_s* P) {
+  return P->d.function == AMQFT_FN_CDFT ||
+         ((P->d.function == AMQFT_FN_RDFT || P->d.function == AMQFT_FN_DCT || P->d.function == AMQFT_FN_DST) &&
+          P->d.n >= 4);
+}
+
+// Inverse RDFT / DCT-0 / DST-0 (inverse.cu): the plan's own forward DCT-0 /
+// DST-0 between exact power-of-two weightings.
+amqft_status exec_real_inverse(amqft_plan_s* P, const void* in, void* out, size_t rows, cudaStream_t st) {
+  const int f64 = P->d.dtype == AMQFT_F64;
+  const double n = static_cast<double>(P->d.n);
+  const size_t h = P->d.n / 2;
+  auto sub = [&](int fn) -> amqft_plan_s* {
+    amqft_plan_desc d = P->d;
+    d.function = fn;
+    amqft_plan q = nullptr;
+    const amqft_status s = amqft_plan_create(&q, &d);
+    if (s != AMQFT_OK) throw std::runtime_error(std::string("inverse sub-plan: ") + g_err);
+    return q;
+  };
+  if (P->d.function == AMQFT_FN_DST) {          // (4/N) DST-0(S)
+    amqft_status s = amqft_exec_rows(P, in, out, rows, 0, st);
+    if (s != AMQFT_OK) return s;
+    inv_weight(f64, out, out, rows, P->c.cells, 4.0 / n, 4.0 / n, st);
+    return AMQFT_OK;
+  }
+  if (P->d.function == AMQFT_FN_DCT) {          // (4/N) W DCT-0(W C)
+    if (!P->inv_a) ck(cudaMalloc(&P->inv_a, P->d.batch * P->c.cells * P->esize), "cudaMalloc inverse scratch");
+    inv_weight(f64, in, P->inv_a, rows, P->c.cells, 1.0, 0.5, st);
+    amqft_status s = amqft_exec_rows(P, P->inv_a, out, rows, 0, st);
+    if (s != AMQFT_OK) return s;
+    inv_weight(f64, out, out, rows, P->c.cells, 4.0 / n, 2.0 / n, st);
+    return AMQFT_OK;
+  }
+  // RDFT: split the packed spectrum, DCT-0 and DST-0 inverses, butterfly
+  if (!P->inv_dct) P->inv_dct = sub(AMQFT_FN_DCT);
+  if (!P->inv_dst) P->inv_dst = sub(AMQFT_FN_DST);
+  if (!P->inv_a) ck(cudaMalloc(&P->inv_a, P->d.batch * (h + 1) * P->esize), "cudaMalloc inverse scratch");
+  if (!P->inv_b) ck(cudaMalloc(&P->inv_b, P->d.batch * (h - 1) * P->esize), "cudaMalloc inverse scratch");
+  inv_rdft_split(f64, in, P->inv_a, P->inv_b, rows, P->d.n, st);
+  amqft_status s = amqft_exec_rows(P->inv_dct, P->inv_a, P->inv_a, rows, 0, st);
+  if (s == AMQFT_OK) s = amqft_exec_rows(P->inv_dst, P->inv_b, P->inv_b, rows, 0, st);
+  if (s != AMQFT_OK) return s;
+  inv_rdft_combine(f64, P->inv_a, P->inv_b, out, rows, P->d.n, 4.0 / n, st);
+  return AMQFT_OK;
+}
+
+}  // namespace
+
 amqft_status amqft_exec_rows(amqft_plan P, const void* in, void* out, size_t rows,
                              int inverse, void* stream) {
   if (!P) return set_err(AMQFT_EINVAL, "null plan");
   if (rows > P->d.batch) return set_err(AMQFT_EINVAL, "rows exceed the plan batch");
-  if (inverse && P->d.function != AMQFT_FN_CDFT)
-    return set_err(AMQFT_EINVAL, "the inverse is defined for CDFT plans only");
+  if (inverse && !inverse_defined(P))
+    return set_err(AMQFT_EINVAL, "the inverse is defined for CDFT, and for RDFT / DCT / DST plans with n >= 4");
+  if (inverse && P->d.function != AMQFT_FN_CDFT) {
+    if (rows == 0) return AMQFT_OK;
+    if (!in || !out) return set_err(AMQFT_EINVAL, "null data pointer");
+    try {
+      ck(cudaSetDevice(P->d.device), "cudaSetDevice");
+      return exec_real_inverse(P, in, out, rows, static_cast<cudaStream_t>(stream));
+    } catch (const CudaError& e) {
+      return set_err(AMQFT_ECUDA, e.what());
+    } catch (const std::runtime_error& e) {
+      return set_err(AMQFT_ECUDA, e.what());
+    }
+  }
   if (rows == 0) return AMQFT_OK;
   if (!in || !out) return set_err(AMQFT_EINVAL, "null data pointer");
   // the fused, four-step and small-CDFT kernels move rows with TMA bulk
@@ -379,8 +452,8 @@ amqft_status amqft_exec_rows(amqft_plan P, const void* in, void* out, size_t row
 amqft_status amqft_exec_host_rows(amqft_plan P, const void* h_in, void* h_out, size_t rows,
                                   int inverse, void* stream) {
   if (!P) return set_err(AMQFT_EINVAL, "null plan");
-  if (inverse && P->d.function != AMQFT_FN_CDFT)
-    return set_err(AMQFT_EINVAL, "the inverse is defined for CDFT plans only");
+  if (inverse && !inverse_defined(P))
+    return set_err(AMQFT_EINVAL, "the inverse is defined for CDFT, and for RDFT / DCT / DST plans with n >= 4");
   if (rows == 0) return AMQFT_OK;
   if (!h_in || !h_out) return set_err(AMQFT_EINVAL, "null data pointer");
   try {

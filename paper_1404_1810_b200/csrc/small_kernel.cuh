@@ -83,11 +83,11 @@ template <bool INV> struct RowIO<double, INV> {
 // Global-memory variant: the input comes from `in`, the output goes to `out`.
 template <typename R, bool INV> struct GRowIO;
 template <bool INV> struct GRowIO<float, INV> {
-  const float4* __restrict__ pi;
-  float4* __restrict__ po;
+  const float4* pi;   // may alias po (in-place rows): no __restrict__
+  float4* po;
   float scale;
   __device__ __forceinline__ void ld(int c, float& a, float& b, float& d, float& e) const {
-    const float4 v = __ldg(pi + c);
+    const float4 v = pi[c];
     if (INV) { a = v.y; b = v.x; d = v.w; e = v.z; }
     else { a = v.x; b = v.y; d = v.z; e = v.w; }
   }
@@ -98,11 +98,11 @@ template <bool INV> struct GRowIO<float, INV> {
   }
 };
 template <bool INV> struct GRowIO<double, INV> {
-  const double2* __restrict__ pi;
-  double2* __restrict__ po;
+  const double2* pi;
+  double2* po;
   double scale;
   __device__ __forceinline__ void ld(int c, double& a, double& b) const {
-    const double2 v = __ldg(pi + c);
+    const double2 v = pi[c];
     if (INV) { a = v.y; b = v.x; }
     else { a = v.x; b = v.y; }
   }
@@ -413,8 +413,8 @@ template <bool INV> struct ColIO<float, INV> {   // chunk c = complex 2c, 2c+1
   }
 };
 template <bool INV> struct ColIO<double, INV> {  // chunk c = complex c
-  const double2* __restrict__ pi;
-  double2* __restrict__ po;
+  const double2* pi;
+  double2* po;
   size_t stride;
   unsigned long long col;
   ColTwiddle tw;
@@ -559,9 +559,9 @@ template <typename R> struct ScalarIO {
   __device__ __forceinline__ void st(int c, R a) const { p[c] = a; }
 };
 template <typename R> struct GScalarIO {
-  const R* __restrict__ pi;
-  R* __restrict__ po;
-  __device__ __forceinline__ void ld(int c, R& a) const { a = __ldg(pi + c); }
+  const R* pi;   // may alias po (in-place rows)
+  R* po;
+  __device__ __forceinline__ void ld(int c, R& a) const { a = pi[c]; }
   __device__ __forceinline__ void st(int c, R a) const { po[c] = a; }
 };
 

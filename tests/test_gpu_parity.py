@@ -138,8 +138,8 @@ def test_device_rejections():
         amqft.Plan(2, amqft.FunctionId.DctOddTime, 64, 1)
     with pytest.raises(amqft.InvalidArgument):
         amqft.Plan(1, amqft.FunctionId.Cdft, 96, 1)
-    p = amqft.Plan(1, amqft.FunctionId.Dct, 64, 1, dtype="f64")
-    x = torch.zeros(33, dtype=torch.float64, device=DEV)
+    p = amqft.Plan(1, amqft.FunctionId.DctOddTime, 64, 1, dtype="f64")
+    x = torch.zeros(p.cells, dtype=torch.float64, device=DEV)
     with pytest.raises(amqft.InvalidArgument):
         p.inverse(x, x)
     with pytest.raises(amqft.InvalidArgument):
@@ -625,10 +625,10 @@ def test_small_kernel_rdft_rows(oracle, restatement, dtype):
             else:
                 ex = amqft.Plan(v, amqft.FunctionId.Rdft, n, rows, dtype="f32", order=amqft.Order.Exact)
                 assert got.tobytes() == run_plan(ex, xs).tobytes(), (v, n)
-            with pytest.raises(amqft.InvalidArgument):
-                plan.inverse(torch.zeros(rows, n, dtype=torch.float64 if dtype == "f64" else torch.float32,
-                                         device=DEV), torch.empty(rows, n, device=DEV,
-                                                                  dtype=torch.float64 if dtype == "f64" else torch.float32))
+            if n == 2:   # the RDFT inverse needs the DST-0 of n >= 4
+                z = torch.zeros(rows, n, dtype=torch.float64, device=DEV)
+                with pytest.raises(amqft.InvalidArgument):
+                    plan.inverse(z, torch.empty_like(z))
 
 
 DCTDST_SMALL = {"f64": {2: (4, 8, 16, 32, 64, 128), 3: (8, 16, 32, 64, 128)},
@@ -682,3 +682,67 @@ def test_fast_plans_reject_misaligned_buffers():
     exact.forward(x[:rows].contiguous(), z, rows=rows)
     torch.cuda.synchronize()
     assert torch.equal(z, y[:rows])
+
+
+@pytest.mark.parametrize("order", [amqft.Order.Exact, amqft.Order.Fast])
+def test_real_transform_inverses(oracle, restatement, order):
+    """Inverses of RDFT / DCT-0 / DST-0 (csrc/inverse.cu):
+    fp64 bitwise the oracle composition (the reference forward between the
+    same exact power-of-two weightings and butterfly) on the exact generic
+    path and on the fast kernels; round trip <= 1e-13 for v1-4; odd-function
+    plans still reject the inverse."""
+    r, O = restatement, oracle
+    for f in (O.F_RDFT, O.F_DCT, O.F_DST):
+        for n in (4, 16, 128, 1024):
+            cells = amqft.cell_count(f, n)
+            rows = 3
+            xs = np.stack([r.uniform(r.mix_seed(41, f, n, row), cells) for row in range(rows)])
+            for v in (1, 4, 6):
+                plan = amqft.Plan(v, f, n, rows, dtype="f64", order=order)
+                spec = run_plan(plan, xs)
+                back = run_plan(plan, spec, inverse=True)
+                for row in range(rows):
+                    want = r.inverse_real(v, f, n, spec[row])
+                    assert back[row].tobytes() == want.tobytes(), (f, n, v, row)
+                if v <= 4:
+                    assert r.rel_l2(back.ravel(), xs.ravel()) < 1e-13, (f, n, v)
+    odd = amqft.Plan(2, amqft.FunctionId.DctOddHarm, 64, 1, dtype="f64")
+    z = torch.zeros(1, odd.cells, dtype=torch.float64, device=DEV)
+    with pytest.raises(amqft.InvalidArgument):
+        odd.inverse(z, torch.empty_like(z))
+
+
+def test_real_inverse_fp32_round_trip():
+    """fp32 fast path: RDFT N = 64 (small kernel) and 4096 (fused kernel) and
+    DCT/DST N = 256 round trips within 1e-5 log2 N."""
+    for f, n in ((1, 64), (1, 4096), (2, 256), (3, 256)):
+        cells = amqft.cell_count(f, n)
+        plan = amqft.Plan(4, f, n, 64, dtype="f32", order=amqft.Order.Fast)
+        x = torch.randn(64, cells, device=DEV)
+        y = torch.empty_like(x)
+        z = torch.empty_like(x)
+        plan.forward(x, y)
+        plan.inverse(y, z)
+        torch.cuda.synchronize()
+        assert float((z - x).norm() / x.norm()) < 1e-5 * math.log2(n), (f, n)
+
+
+def test_small_kernels_in_place():
+    """d_in == d_out on the small kernels' global-memory paths (CDFT rows of
+    <= 64 B, DCT/DST rows past the last full tile) and the staged paths:
+    bitwise the out-of-place result (regression: the row I/O must not be
+    declared non-aliasing)."""
+    cases = [(0, 4, "f32"), (0, 8, "f32"), (0, 4, "f64"), (0, 32, "f32"), (2, 64, "f64"), (3, 128, "f32"),
+             (1, 16, "f32")]
+    for f, n, dtype in cases:
+        dt = torch.float64 if dtype == "f64" else torch.float32
+        for rows in (100, 300):
+            plan = amqft.Plan(3, f, n, rows, dtype=dtype, order=amqft.Order.Fast)
+            assert plan.path()[0] == 4
+            x = torch.randn(rows, plan.cells, dtype=dt, device=DEV)
+            y = torch.empty_like(x)
+            plan.forward(x, y)
+            z = x.clone()
+            plan.forward(z, z)
+            torch.cuda.synchronize()
+            assert torch.equal(y, z), (f, n, dtype, rows)
