@@ -65,3 +65,33 @@ def test_invalid_requests_map_to_einval():
         amqft.Plan(0, amqft.FunctionId.Cdft, 1024, 1)
     with pytest.raises(amqft.InvalidArgument):
         amqft.Plan(1, amqft.FunctionId.Cdft, 1024, 0)
+
+
+def build_shim_caller(tmpdir):
+    """g++ a reference-style caller against include/amqft_b200.hpp, linked to
+    the product library (no other source change: the drop-in boundary)."""
+    import subprocess
+    exe = os.path.join(str(tmpdir), "shim_caller")
+    lib_dir = os.path.dirname(_native.LIB_PATH)
+    subprocess.run(["g++", "-std=c++17", "-O2", "-Wall", "-Wextra", "-I", os.path.join(ROOT, "include"),
+                    "-I", "/usr/local/cuda/include", os.path.join(ROOT, "tests", "native", "shim_caller.cpp"),
+                    "-o", exe, "-L", lib_dir, "-lamqft_b200", f"-Wl,-rpath,{lib_dir}"], check=True)
+    return exe
+
+
+def test_reference_style_caller_builds_and_has_no_cpu_path(tmp_path):
+    """The C++ shim compiles a reference caller unchanged; without a CUDA
+    device the call fails loudly (no CPU fallback)."""
+    import subprocess
+    import numpy as np
+    exe = build_shim_caller(tmp_path)
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("GPU present: the GPU test runs the caller")
+    except ImportError:
+        pass
+    inp = tmp_path / "x.f64"
+    np.arange(32, dtype=np.float64).tofile(inp)
+    r = subprocess.run([exe, "4", "16", str(inp), str(tmp_path / "y.f64")], capture_output=True, text=True)
+    assert r.returncode == 3 and "CUDA" in r.stderr, (r.returncode, r.stderr)

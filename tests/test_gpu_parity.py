@@ -746,3 +746,24 @@ def test_small_kernels_in_place():
             plan.forward(z, z)
             torch.cuda.synchronize()
             assert torch.equal(y, z), (f, n, dtype, rows)
+
+
+def test_reference_style_caller_through_the_shim(tmp_path, oracle, restatement):
+    """A caller written against the reference API (amqft::execute, TrigTable,
+    OpMeter; tests/native/shim_caller.cpp), compiled against
+    include/amqft_b200.hpp: bitwise the oracle and the reference meter."""
+    import subprocess
+    from test_capi import build_shim_caller
+    r, O = restatement, oracle
+    exe = build_shim_caller(tmp_path)
+    n = 1024
+    for v in (1, 4, 7):
+        x = O.seeded_signal(1, O.CDFT, n, v, r)
+        x.tofile(tmp_path / "x.f64")
+        res = subprocess.run([exe, str(v), str(n), str(tmp_path / "x.f64"), str(tmp_path / "y.f64")],
+                             capture_output=True, text=True)
+        assert res.returncode == 0, res.stderr
+        got = np.fromfile(tmp_path / "y.f64", dtype=np.float64)
+        want, meter = r.execute(v, O.F_CDFT, n, x, meter=True)
+        assert got.tobytes() == want.tobytes(), v
+        assert tuple(int(t) for t in res.stdout.split()) == tuple(meter), v
