@@ -47,8 +47,9 @@ def parse():
     p.add_argument("--order", choices=["fast", "exact"], default="fast")
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--all-variants", action="store_true",
-                   help="also time variants 1..8 (extra 'variants' key)")
+    p.add_argument("--all-variants", action=argparse.BooleanOptionalAction, default=True,
+                   help="after the timed region, also time variants 1..8 and report their fp32 error "
+                        "(extra 'variants' and accuracy keys; --no-all-variants to skip)")
     p.add_argument("--config", type=int, choices=[2, 4, 5], default=2,
                    help="BASELINE config: 2 batched N=4096 (default), 4 single N=2^24 four-step, "
                         "5 single N=2^30 distributed four-step over the ranks")
@@ -254,6 +255,7 @@ def cpu_baseline_large(variant, n_full, sample_n, seconds_cap=30.0):
 
 def oracle_checks(args, kept, amqft, kept_v=None):
     """Checker only (runs in the CPU-baseline leg)."""
+    import numpy as np
     from oracle import oracle as O
     r = O.restatement()
     n = args.n
@@ -273,6 +275,12 @@ def oracle_checks(args, kept, amqft, kept_v=None):
     if kept_v:
         out["config2_fp32_row0_rel_l2_vs_cpu_same_variant"] = {
             str(v): r.rel_l2(got, r.execute(v, O.F_CDFT, n, xin)) for v, (xin, got) in sorted(kept_v.items())}
+        xin0 = next(iter(kept_v.values()))[0]
+        naive_n = r.naive(O.CDFT, n, xin0)      # O(N^2) fp64 DFT of the same row (BASELINE)
+        out["config2_fp32_row0_rel_l2_vs_naive_fp64"] = {
+            str(v): r.rel_l2(got, naive_n) for v, (xin, got) in sorted(kept_v.items()) if xin is xin0 or
+            np.array_equal(xin, xin0)}
+        out["config2_tolerance_fp32"] = 1e-5 * math.log2(n)
     return parity, out
 
 
