@@ -81,18 +81,20 @@ def fourstep_split(n: int):
 
 
 def _plan_covers_f32_fast(n: int) -> bool:
-    """Sizes with a fused fp32 path: the kernel (1024..8192) or the
-    single-GPU four-step over it (2^20..2^26)."""
-    return 1024 <= n <= 8192 or (1 << 20) <= n <= (1 << 26)
+    """Sizes with an fp32 fast-order path: the small-CDFT kernels (2..512),
+    the fused kernel (1024..8192) and the single-GPU four-step over them
+    (column mode where the first factor is small) up to 2^26."""
+    return 2 <= n <= (1 << 26)
 
 
 def dist_split(n: int, world: int):
     """n = n1 * n2 for the distributed four-step: n2 is a fused-kernel size
-    (rows after the exchange), n1 any size with a fused path (the local rows
-    before it; the single-GPU four-step for n1 >= 2^20), both divisible by
-    the world size.  Config 5, N = 2^30: n1 = 2^20, n2 = 2^10."""
+    (rows after the exchange; 4096 first, the fastest fused size), n1 any
+    size with a fast path (the local rows before it; a column-mode
+    single-GPU four-step for 2^13..2^19), both divisible by the world size.
+    Config 5, N = 2^30: n1 = 2^18 (64 x 4096, column mode), n2 = 2^12."""
     fourstep_split(n)   # power-of-two check
-    for n2 in (8192, 4096, 2048, 1024):
+    for n2 in (4096, 8192, 2048, 1024):
         n1 = n // n2
         if n1 * n2 == n and _plan_covers_f32_fast(n1) and n1 % world == 0 and n2 % world == 0:
             return n1, n2

@@ -155,8 +155,10 @@ def test_gloo_world2_distributed_fourstep():
 
 def test_dist_split_and_layout_helpers():
     from paper_1404_1810_b200.dist import DistFourStep, dist_split
-    assert dist_split(1 << 30, 8) == (1 << 20, 1 << 10)
-    assert dist_split(1 << 24, 2) == (2048, 8192)
+    assert dist_split(1 << 30, 8) == (1 << 18, 1 << 12)
+    assert dist_split(1 << 24, 2) == (4096, 4096)
+    with pytest.raises(ValueError):
+        dist_split(3 << 20, 2)
     n = 1 << 20
     for world in (1, 2, 4):
         parts = []
