@@ -16,6 +16,7 @@ struct ColTwiddle {
   const double2* hi = nullptr;
   const double2* lo = nullptr;
   int logb = 0, logn = 0, onthefly = 0;
+  unsigned long long mul = 1;   // exponent scale: w_N^(mul n2 k1) = w_(N/mul)^(n2 k1)
 };
 
 class FastPlan {

@@ -159,6 +159,51 @@ void launch_t(const typename C2<R>::T* in, typename C2<R>::T* out, size_t mats, 
   if (e != cudaSuccess) throw std::runtime_error(std::string("k_transpose: ") + cudaGetErrorString(e));
 }
 
+// Three-factor four-step, last pass: U[mat][k1][jb][jc] (dims A, B, C) ->
+// Y[mat][jc][jb][k1], i.e. for every (mat, jb) the A x C matrix of rows k1
+// (stride B C) transposed into rows jc (stride B A); 32 x 32 tiles.
+// SWAP / scale: the swap-trick inverse's second half.
+template <bool SWAP, typename R>
+__global__ void __launch_bounds__(TD * TR) k_transpose3(const typename C2<R>::T* __restrict__ in,
+                                                       typename C2<R>::T* __restrict__ out, int A, int B, int Cc,
+                                                       R scale) {
+  using V2 = typename C2<R>::T;
+  __shared__ V2 tile[TD][TD + 1];
+  const size_t z = blockIdx.z;                    // mat * B + jb
+  const size_t mat = z / B, jb = z - mat * B;
+  const int c0 = blockIdx.x * TD, r0 = blockIdx.y * TD;   // jc block, k1 block
+  const size_t base_in = mat * size_t(A) * B * Cc + jb * Cc;
+  const size_t base_out = mat * size_t(A) * B * Cc + jb * A;
+#pragma unroll
+  for (int j = 0; j < TD; j += TR) {
+    const int k1 = r0 + threadIdx.y + j, jc = c0 + threadIdx.x;
+    V2 v = in[base_in + size_t(k1) * B * Cc + jc];
+    if (SWAP) v = C2<R>::mk(v.y, v.x);
+    tile[threadIdx.y + j][threadIdx.x] = v;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < TD; j += TR) {
+    const int jc = c0 + threadIdx.y + j, k1 = r0 + threadIdx.x;
+    const V2 v = tile[threadIdx.x][threadIdx.y + j];
+    out[base_out + size_t(jc) * B * A + k1] = C2<R>::mk(v.x * scale, v.y * scale);
+  }
+}
+
+template <bool SWAP, typename R>
+void launch_t3(const typename C2<R>::T* in, typename C2<R>::T* out, size_t mats, int A, int B, int Cc, R scale,
+               cudaStream_t st) {
+  const size_t zs = mats * B;
+  for (size_t z0 = 0; z0 < zs; z0 += 65535) {
+    const unsigned nz = static_cast<unsigned>(std::min<size_t>(65535, zs - z0));
+    if (z0 % B) throw std::invalid_argument("transpose3: matrix chunking");
+    const size_t off = (z0 / B) * size_t(A) * B * Cc;
+    k_transpose3<SWAP, R><<<dim3(Cc / TD, A / TD, nz), dim3(TD, TR), 0, st>>>(in + off, out + off, A, B, Cc, scale);
+  }
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string("k_transpose3: ") + cudaGetErrorString(e));
+}
+
 // Distributed four-step, one rank's half-way step: rows n2 = row0 + r
 // (r < rows) of length N1 (already transformed over n1) are multiplied by
 // w_N^(n2 k1) and scattered by k1-slab: destination q receives the
@@ -252,6 +297,40 @@ bool fourstep_split(int dtype, size_t n, size_t* n1, size_t* n2, bool* col = nul
   return best > 0.0;
 }
 
+// Three-factor mode: N = A B C, A and B one-thread-per-row sizes (column
+// passes, coalesced, twiddles fused into their stores), C a single-kernel
+// row size, and one 3D transpose: 4 passes.  Chosen when cheaper than the
+// best two-factor plan by the same throughput model.
+bool fourstep_split3(int dtype, size_t n, size_t* a, size_t* b, size_t* c, double* cost) {
+  constexpr double kTransposeTBs = 6.9;
+  const int lg = lg2(n);
+  double best = 0.0;
+  // column factors <= 32: the column kernel with its per-element twiddle
+  // lookups ran at ~2-2.5 TB/s for 64-point columns (N = 2^24 as 64 x 64 x
+  // 4096: 0.396 ms vs 0.353 ms for the two-factor 4096 x 4096)
+  for (int la = 5; la <= 5; ++la)
+    for (int lb = 1; lb <= 5; ++lb) {
+      const int lc = lg - la - lb;
+      if (lc < 5 || !col_capable(dtype, la) || !col_capable(dtype, lb)) continue;
+      if (!fast_sub_covered(dtype, size_t(1) << lc)) continue;
+      const double ta = sub_tbs(dtype, la), tb = sub_tbs(dtype, lb), tc = sub_tbs(dtype, lc);
+      if (ta <= 0.0 || tb <= 0.0 || tc <= 0.0) continue;
+      const double cst = 1.0 / ta + 1.0 / tb + 1.0 / tc + 1.0 / kTransposeTBs;
+      if (best == 0.0 || cst < best - 1e-9) {
+        best = cst;
+        *a = size_t(1) << la;
+        *b = size_t(1) << lb;
+        *c = size_t(1) << lc;
+      }
+    }
+  if (cost) *cost = best;
+  return best > 0.0;
+}
+
+double fourstep_cost2(int dtype, size_t n1, size_t n2, bool col) {
+  return 1.0 / sub_tbs(dtype, lg2(n1)) + 1.0 / sub_tbs(dtype, lg2(n2)) + (col ? 1.0 : 3.0) / 6.9;
+}
+
 template <typename R>
 class FourStepPlan final : public FastPlan {
   using V2 = typename C2<R>::T;
@@ -261,7 +340,19 @@ class FourStepPlan final : public FastPlan {
       : n_(n), batch_(batch), onthefly_(trig_mode == AMQFT_TRIG_ONTHEFLY) {
     logn_ = lg2(n);
     const int dtype = sizeof(R) == 8 ? AMQFT_F64 : AMQFT_F32;
-    if (!fourstep_split(dtype, n, &n1_, &n2_, &col_)) throw std::invalid_argument("four-step: no covered split");
+    const bool two = fourstep_split(dtype, n, &n1_, &n2_, &col_);
+    double c3 = 0.0;
+    size_t a3 = 0, b3 = 0, cc3 = 0;
+    three_ = fourstep_split3(dtype, n, &a3, &b3, &cc3, &c3) &&
+             (!two || c3 < fourstep_cost2(dtype, n1_, n2_, col_) - 1e-9);
+    if (!two && !three_) throw std::invalid_argument("four-step: no covered split");
+    if (three_) {   // p1_: A columns, pb_: B columns, p2_: C rows
+      n1_ = a3;
+      nb_ = b3;
+      n2_ = cc3;
+      pb_ = make_fast_sub(variant, nb_, dtype, tab, nmax, dev);
+      if (!pb_) throw std::invalid_argument("four-step: no kernel for the middle factor");
+    }
     p1_ = make_fast_sub(variant, n1_, dtype, tab, nmax, dev);
     p2_ = make_fast_sub(variant, n2_, dtype, tab, nmax, dev);
     if (!p1_ || !p2_) throw std::invalid_argument("four-step: no fused kernel for the sub-transform sizes");
@@ -283,9 +374,11 @@ class FourStepPlan final : public FastPlan {
     check(cudaMemcpy(twh_, th.data(), NH * sizeof(double2), cudaMemcpyHostToDevice), "cudaMemcpy");
     check(cudaMemcpy(twl_, tl.data(), B * sizeof(double2), cudaMemcpyHostToDevice), "cudaMemcpy");
     check(cudaMalloc(&scratch_, batch_ * n_ * sizeof(V2)), "cudaMalloc four-step scratch");
-    launches = col_ ? 1 + p1_->launches + p2_->launches : 3 + p1_->launches + p2_->launches;
+    if (three_) check(cudaMalloc(&scratch2_, batch_ * n_ * sizeof(V2)), "cudaMalloc four-step scratch");
+    launches = three_ ? 4 : (col_ ? 1 + p1_->launches + p2_->launches : 3 + p1_->launches + p2_->launches);
   }
   ~FourStepPlan() override {
+    if (scratch2_) cudaFree(scratch2_);
     if (twh_) cudaFree(twh_);
     if (twl_) cudaFree(twl_);
     if (scratch_) cudaFree(scratch_);
@@ -296,6 +389,31 @@ class FourStepPlan final : public FastPlan {
     V2* y = static_cast<V2*>(out);
     V2* s = scratch_;
     const int R1 = static_cast<int>(n1_), C1 = static_cast<int>(n2_);
+    if (three_) {
+      // x [a][b][c] (dims A, B, C): columns over a (length A, stride B C),
+      // times w_N^((b C + c) ka) -> s [ka][b][c]
+      ColTwiddle tw;
+      tw.hi = twh_;
+      tw.lo = twl_;
+      tw.logb = logb_;
+      tw.logn = logn_;
+      tw.onthefly = onthefly_ ? 1 : 0;
+      if (!p1_->exec_columns(x, s, rows, nb_ * n2_, inverse, tw, st))
+        throw std::runtime_error("four-step: sub-plan has no column mode");
+      // rows ka of length M = B C: columns over b (stride C), times
+      // w_M^(c kb) = w_N^(A c kb) -> s2 [ka][kb][c]
+      tw.mul = n1_;
+      if (!pb_->exec_columns(s, scratch2_, rows * n1_, n2_, 0, tw, st))
+        throw std::runtime_error("four-step: sub-plan has no column mode");
+      // rows of length C, in place: s2 [ka][kb][kc] = X[ka + A (kb + B kc)]
+      p2_->exec(scratch2_, scratch2_, rows * n1_ * nb_, 0, st);
+      // s2 [ka][kb][kc] -> y [kc][kb][ka]
+      if (inverse)
+        launch_t3<true, R>(scratch2_, y, rows, R1, static_cast<int>(nb_), C1, R(1) / static_cast<R>(n_), st);
+      else
+        launch_t3<false, R>(scratch2_, y, rows, R1, static_cast<int>(nb_), C1, R(1), st);
+      return;
+    }
     if (col_) {
       // 1+2+3. columns of x [n1][n2] -> s [k1][n2], times w^(n2 k1)
       ColTwiddle tw;
@@ -341,6 +459,10 @@ class FourStepPlan final : public FastPlan {
   int logn_ = 0, logb_ = 0;
   bool onthefly_;
   bool col_ = false;
+  bool three_ = false;   // N = A B C: two column passes, rows, one 3D transpose
+  size_t nb_ = 0;
+  std::unique_ptr<FastPlan> pb_;
+  V2* scratch2_ = nullptr;
   std::unique_ptr<FastPlan> p1_, p2_;
   double2* twh_ = nullptr;
   double2* twl_ = nullptr;

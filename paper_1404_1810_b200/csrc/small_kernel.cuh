@@ -406,8 +406,8 @@ template <bool INV> struct ColIO<float, INV> {   // chunk c = complex 2c, 2c+1
     else { a = u.x; b = u.y; d = v.x; e = v.y; }
   }
   __device__ __forceinline__ void st(int c, float a, float b, float d, float e) const {
-    col_twiddle(a, b, col * static_cast<unsigned long long>(2 * c), tw);
-    col_twiddle(d, e, col * static_cast<unsigned long long>(2 * c + 1), tw);
+    col_twiddle(a, b, col * tw.mul * static_cast<unsigned long long>(2 * c), tw);
+    col_twiddle(d, e, col * tw.mul * static_cast<unsigned long long>(2 * c + 1), tw);
     po[size_t(2 * c) * stride] = make_float2(a, b);
     po[size_t(2 * c + 1) * stride] = make_float2(d, e);
   }
@@ -424,7 +424,7 @@ template <bool INV> struct ColIO<double, INV> {  // chunk c = complex c
     else { a = u.x; b = u.y; }
   }
   __device__ __forceinline__ void st(int c, double a, double b) const {
-    col_twiddle(a, b, col * static_cast<unsigned long long>(c), tw);
+    col_twiddle(a, b, col * tw.mul * static_cast<unsigned long long>(c), tw);
     po[size_t(c) * stride] = make_double2(a, b);
   }
 };
