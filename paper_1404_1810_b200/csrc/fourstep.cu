@@ -193,10 +193,10 @@ __global__ void __launch_bounds__(TD * TR) k_transpose3(const typename C2<R>::T*
 template <bool SWAP, typename R>
 void launch_t3(const typename C2<R>::T* in, typename C2<R>::T* out, size_t mats, int A, int B, int Cc, R scale,
                cudaStream_t st) {
-  const size_t zs = mats * B;
-  for (size_t z0 = 0; z0 < zs; z0 += 65535) {
-    const unsigned nz = static_cast<unsigned>(std::min<size_t>(65535, zs - z0));
-    if (z0 % B) throw std::invalid_argument("transpose3: matrix chunking");
+  // grid.z <= 65535: chunks of whole matrices (a multiple of B slices)
+  const size_t zs = mats * B, step = (65535 / static_cast<size_t>(B)) * B;
+  for (size_t z0 = 0; z0 < zs; z0 += step) {
+    const unsigned nz = static_cast<unsigned>(std::min<size_t>(step, zs - z0));
     const size_t off = (z0 / B) * size_t(A) * B * Cc;
     k_transpose3<SWAP, R><<<dim3(Cc / TD, A / TD, nz), dim3(TD, TR), 0, st>>>(in + off, out + off, A, B, Cc, scale);
   }

@@ -767,3 +767,24 @@ def test_reference_style_caller_through_the_shim(tmp_path, oracle, restatement):
         want, meter = r.execute(v, O.F_CDFT, n, x, meter=True)
         assert got.tobytes() == want.tobytes(), v
         assert tuple(int(t) for t in res.stdout.split()) == tuple(meter), v
+
+
+def test_fourstep_large_batch_grid_chunking(oracle, restatement):
+    """Config-3 shape that overflows one launch's grid.z in the transposes
+    (fp64 N = 2^13, 2^13 rows = 1 GiB; the sweep found a chunking bug here):
+    sampled rows against the oracle, round trip."""
+    r, O = restatement, oracle
+    n, rows = 1 << 13, 1 << 13
+    g = torch.Generator(device=DEV).manual_seed(13)
+    x = torch.rand(rows, 2 * n, dtype=torch.float64, device=DEV, generator=g) * 2 - 1
+    y = torch.empty_like(x)
+    z = torch.empty_like(x)
+    plan = amqft.Plan(4, amqft.FunctionId.Cdft, n, rows, dtype="f64", order=amqft.Order.Fast)
+    assert plan.path()[0] == 3
+    plan.forward(x, y)
+    plan.inverse(y, z)
+    torch.cuda.synchronize()
+    for row in (0, rows // 2 + 3, rows - 1):
+        want = r.execute(4, O.F_CDFT, n, x[row].cpu().numpy())
+        assert r.rel_l2(y[row].cpu().numpy(), want) <= 1e-12, row
+    assert float((z - x).norm() / x.norm()) < 1e-14
