@@ -37,7 +37,9 @@ std::unique_ptr<FastPlan> make_fast_typed(int v, int kind, size_t n, const void*
 std::unique_ptr<FastPlan> make_fast_plan(const amqft_plan_desc& d, const void* d_trig,
                                          uint32_t nmax) {
   if (d.function != AMQFT_FN_CDFT && d.function != AMQFT_FN_RDFT) return nullptr;
-  if (d.trig_mode != AMQFT_TRIG_TABLE) return nullptr;
+  // AM constants: both trig modes read the plan's host-built table, whose
+  // values are bitwise the reference's on-the-fly long double values
+  // (variants_test.cpp:267-277); the mode matters only for four-step twiddles
   const int kind = d.function == AMQFT_FN_RDFT ? 1 : 0;
   if (d.dtype == AMQFT_F32) return make_fast_typed<float>(d.variant, kind, d.n, d_trig, nmax, d.device);
   return make_fast_typed<double>(d.variant, kind, d.n, d_trig, nmax, d.device);
@@ -80,7 +82,7 @@ std::unique_ptr<FastPlan> make_small_typed(int v, size_t n, const void* tab, uin
 
 std::unique_ptr<FastPlan> make_small_plan(const amqft_plan_desc& d, const void* d_trig, uint32_t nmax,
                                           OpCount* ops) {
-  if (d.function > AMQFT_FN_DST || d.trig_mode != AMQFT_TRIG_TABLE) return nullptr;
+  if (d.function > AMQFT_FN_DST) return nullptr;   // AM constants from the table in both trig modes
   if (d.dtype == AMQFT_F32)
     return smallk::make_small_typed<float>(d.variant, d.n, d_trig, nmax, d.device, ops, d.function);
   return smallk::make_small_typed<double>(d.variant, d.n, d_trig, nmax, d.device, ops, d.function);

@@ -19,7 +19,10 @@
 // 1024) or the small-CDFT kernels (<= 512 fp32 / 256 fp64).
 // Twiddles w_N^j = exp(-2 pi i j / N): TRIG_TABLE = two half-size tables
 // w^(jh B) and w^(jl) (B = 2^ceil(lg N / 2)) multiplied in fp64;
-// TRIG_ONTHEFLY = sincospi in fp64 per element.
+// TRIG_ONTHEFLY = sincospi of the exact integer phase 2 (j mod N) / N per
+// element: sincospif for fp32 plans (no table reads: the lane-scattered
+// table lookups were the slow part of the twiddle passes), fp64 sincospi
+// for fp64 plans.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -76,18 +79,34 @@ __global__ void __launch_bounds__(TD * TR) k_transpose(const typename C2<R>::T* 
       const unsigned long long jj =
           (static_cast<unsigned long long>(orow) * static_cast<unsigned long long>(ocol)) &
           ((1ull << logn) - 1ull);
-      double wr, wi;
-      if (onthefly) {
-        double s, c;
-        sincospi(static_cast<double>(jj) * 2.0 / static_cast<double>(1ull << logn), &s, &c);
-        wr = c;
-        wi = -s;
+      R fr, fi;
+      if constexpr (sizeof(R) == 4) {
+        if (onthefly) {   // fp32 plans: sincospif of the exact integer phase (no table reads)
+          float sn, cs;
+          sincospif(static_cast<float>(static_cast<double>(jj) * (2.0 / static_cast<double>(1ull << logn))), &sn,
+                    &cs);
+          fr = cs;
+          fi = -sn;
+        } else {
+          const double2 a = twh[jj >> logb], b = twl[jj & ((1ull << logb) - 1ull)];
+          fr = static_cast<R>(a.x * b.x - a.y * b.y);
+          fi = static_cast<R>(a.x * b.y + a.y * b.x);
+        }
       } else {
-        const double2 a = twh[jj >> logb], b = twl[jj & ((1ull << logb) - 1ull)];
-        wr = a.x * b.x - a.y * b.y;
-        wi = a.x * b.y + a.y * b.x;
+        double wr, wi;
+        if (onthefly) {
+          double s, c;
+          sincospi(static_cast<double>(jj) * 2.0 / static_cast<double>(1ull << logn), &s, &c);
+          wr = c;
+          wi = -s;
+        } else {
+          const double2 a = twh[jj >> logb], b = twl[jj & ((1ull << logb) - 1ull)];
+          wr = a.x * b.x - a.y * b.y;
+          wi = a.x * b.y + a.y * b.x;
+        }
+        fr = static_cast<R>(wr);
+        fi = static_cast<R>(wi);
       }
-      const R fr = static_cast<R>(wr), fi = static_cast<R>(wi);
       v = C2<R>::mk(v.x * fr - v.y * fi, v.x * fi + v.y * fr);
     }
     v.x *= scale;
@@ -227,19 +246,18 @@ __global__ void __launch_bounds__(256) k_twiddle_scatter(const float2* __restric
     const int r = static_cast<int>(i / n1), k1 = static_cast<int>(i % n1);
     const unsigned long long n2 = static_cast<unsigned long long>(row0 + r);
     const unsigned long long jj = (n2 * static_cast<unsigned long long>(k1)) & ((1ull << logn) - 1ull);
-    double wr, wi;
-    if (onthefly) {
-      double sn, cs;
-      sincospi(static_cast<double>(jj) * 2.0 / static_cast<double>(1ull << logn), &sn, &cs);
-      wr = cs;
-      wi = -sn;
+    float fr, fi;
+    if (onthefly) {   // sincospif of the exact integer phase (as the fp32 four-step)
+      float sn, cs;
+      sincospif(static_cast<float>(static_cast<double>(jj) * (2.0 / static_cast<double>(1ull << logn))), &sn, &cs);
+      fr = cs;
+      fi = -sn;
     } else {
       const double2 a = twh[jj >> logb], b = twl[jj & ((1ull << logb) - 1ull)];
-      wr = a.x * b.x - a.y * b.y;
-      wi = a.x * b.y + a.y * b.x;
+      fr = static_cast<float>(a.x * b.x - a.y * b.y);
+      fi = static_cast<float>(a.x * b.y + a.y * b.x);
     }
     const float2 v = in[i];
-    const float fr = static_cast<float>(wr), fi = static_cast<float>(wi);
     const int q = k1 / w, kl = k1 - q * w;
     dst.p[q][(static_cast<long long>(src) * rows + r) * w + kl] =
         make_float2(v.x * fr - v.y * fi, v.x * fi + v.y * fr);

@@ -32,6 +32,13 @@
 #include "fast.cuh"
 #include "generic.cuh"
 
+#ifndef AMQFT_COL_STAGED
+// TMA-staged column tiles (k_small_colt) where cols % 128 == 0.  Measured
+// (B200, table twiddles): no better than the direct column kernel (fp32
+// 2^15 / 2^16 / 2^17: 1.21 / 1.18 / 1.46 vs 1.10 / 1.35 / 1.54 TB/s), so off.
+#define AMQFT_COL_STAGED 0
+#endif
+
 namespace amqft_b200 {
 namespace smallk {
 
@@ -376,18 +383,33 @@ class CoopPlanImpl final : public FastPlan {
 template <typename R>
 __device__ __forceinline__ void col_twiddle(R& x, R& y, unsigned long long j, const ColTwiddle& t) {
   j &= (1ull << t.logn) - 1ull;
-  double wr, wi;
-  if (t.onthefly) {
-    double sn, cs;
-    sincospi(static_cast<double>(j) * 2.0 / static_cast<double>(1ull << t.logn), &sn, &cs);
-    wr = cs;
-    wi = -sn;
+  R fr, fi;
+  if constexpr (sizeof(R) == 4) {
+    if (t.onthefly) {   // fp32 plans: sincospif of the exact integer phase (no table reads)
+      float sn, cs;
+      sincospif(static_cast<float>(static_cast<double>(j) * (2.0 / static_cast<double>(1ull << t.logn))), &sn, &cs);
+      fr = cs;
+      fi = -sn;
+    } else {
+      const double2 a = t.hi[j >> t.logb], b = t.lo[j & ((1ull << t.logb) - 1ull)];
+      fr = static_cast<R>(a.x * b.x - a.y * b.y);
+      fi = static_cast<R>(a.x * b.y + a.y * b.x);
+    }
   } else {
-    const double2 a = t.hi[j >> t.logb], b = t.lo[j & ((1ull << t.logb) - 1ull)];
-    wr = a.x * b.x - a.y * b.y;
-    wi = a.x * b.y + a.y * b.x;
+    double wr, wi;
+    if (t.onthefly) {
+      double sn, cs;
+      sincospi(static_cast<double>(j) * 2.0 / static_cast<double>(1ull << t.logn), &sn, &cs);
+      wr = cs;
+      wi = -sn;
+    } else {
+      const double2 a = t.hi[j >> t.logb], b = t.lo[j & ((1ull << t.logb) - 1ull)];
+      wr = a.x * b.x - a.y * b.y;
+      wi = a.x * b.y + a.y * b.x;
+    }
+    fr = static_cast<R>(wr);
+    fi = static_cast<R>(wi);
   }
-  const R fr = static_cast<R>(wr), fi = static_cast<R>(wi);
   const R nx = x * fr - y * fi, ny = x * fi + y * fr;
   x = nx;
   y = ny;
@@ -445,6 +467,102 @@ k_small_col(const R* __restrict__ in, R* __restrict__ out, size_t mats, size_t c
   }
 }
 
+// Staged variant (cols a multiple of 128): a tile of 128 consecutive
+// columns arrives by N bulk copies of one contiguous 128-element run each
+// into smem [n1][128]; thread t transforms column t out of shared memory
+// (lanes on consecutive 8/16-byte elements: conflict-free) and the tile
+// leaves by N bulk stores.  The TMA keeps every row of the tile in flight
+// at once, which the direct loads above do not.
+template <typename R, bool INV> struct ColSIO;
+template <bool INV> struct ColSIO<float, INV> {
+  float2* s;
+  int t;
+  unsigned long long col;
+  ColTwiddle tw;
+  __device__ __forceinline__ void ld(int c, float& a, float& b, float& d, float& e) const {
+    const float2 u = s[(2 * c) * 128 + t], v = s[(2 * c + 1) * 128 + t];
+    if (INV) { a = u.y; b = u.x; d = v.y; e = v.x; }
+    else { a = u.x; b = u.y; d = v.x; e = v.y; }
+  }
+  __device__ __forceinline__ void st(int c, float a, float b, float d, float e) const {
+    col_twiddle(a, b, col * tw.mul * static_cast<unsigned long long>(2 * c), tw);
+    col_twiddle(d, e, col * tw.mul * static_cast<unsigned long long>(2 * c + 1), tw);
+    s[(2 * c) * 128 + t] = make_float2(a, b);
+    s[(2 * c + 1) * 128 + t] = make_float2(d, e);
+  }
+};
+template <bool INV> struct ColSIO<double, INV> {
+  double2* s;
+  int t;
+  unsigned long long col;
+  ColTwiddle tw;
+  __device__ __forceinline__ void ld(int c, double& a, double& b) const {
+    const double2 u = s[c * 128 + t];
+    if (INV) { a = u.y; b = u.x; }
+    else { a = u.x; b = u.y; }
+  }
+  __device__ __forceinline__ void st(int c, double a, double b) const {
+    col_twiddle(a, b, col * tw.mul * static_cast<unsigned long long>(c), tw);
+    s[c * 128 + t] = make_double2(a, b);
+  }
+};
+
+template <int V, typename R, int LOGN, bool INV>
+__global__ void __launch_bounds__(128)
+k_small_colt(const R* __restrict__ in, R* __restrict__ out, size_t mats, size_t cols,
+             const __grid_constant__ TabP<R, SCfg<R, LOGN, 0>::NT> tp, const ColTwiddle tw) {
+  using C2T = typename std::conditional<sizeof(R) == 4, float2, double2>::type;
+  using G = SmallGen<V, 0, LOGN, R>;
+  constexpr int N = 1 << LOGN;
+  constexpr uint32_t SEG = 128 * sizeof(C2T);
+  extern __shared__ __align__(128) unsigned char sm[];
+  C2T* tile_s = reinterpret_cast<C2T*>(sm);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + size_t(N) * SEG);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(bar)), "r"(1) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t parity = 0;
+  const size_t cb = cols / 128, tiles = mats * cb;
+  for (size_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const size_t mat = tile / cb, col0 = (tile - mat * cb) * 128;
+    const C2T* src = reinterpret_cast<const C2T*>(in) + mat * size_t(N) * cols + col0;
+    C2T* dst = reinterpret_cast<C2T*>(out) + mat * size_t(N) * cols + col0;
+    if (warp == 0) {
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                     ::"r"(s_u32(bar)), "r"(static_cast<uint32_t>(N) * SEG) : "memory");
+      __syncwarp();
+      for (int k = lane; k < N; k += 32)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            ::"r"(s_u32(tile_s + size_t(k) * 128)), "l"(src + size_t(k) * cols), "r"(SEG), "r"(s_u32(bar))
+            : "memory");
+    }
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(s_u32(bar)), "r"(parity) : "memory");
+    parity ^= 1;
+    ColSIO<R, INV> io{tile_s, tid, static_cast<unsigned long long>(col0 + tid), tw};
+    G::template run<Arith<R>>(io, tp.v);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) {
+      for (int k = lane; k < N; k += 32)
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                     ::"l"(dst + size_t(k) * cols), "r"(s_u32(tile_s + size_t(k) * 128)), "r"(SEG) : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+    __syncthreads();
+  }
+  if (warp == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 template <int V, typename R, int LOGN, int F = 0>
 class SmallPlanImpl final : public FastPlan {
   using C = SCfg<R, LOGN, F>;
@@ -491,6 +609,32 @@ class SmallPlanImpl final : public FastPlan {
       (void)in, (void)out, (void)mats, (void)cols, (void)inverse, (void)tw, (void)st;
       return false;
     } else {
+#if AMQFT_COL_STAGED
+    if (cols % 128 == 0 && C::N >= 4) {
+      constexpr size_t SMEM = size_t(C::N) * 128 * 2 * sizeof(R) + 16;
+      auto f0 = k_small_colt<V, R, LOGN, false>;
+      auto f1 = k_small_colt<V, R, LOGN, true>;
+      if (!colt_ready_) {
+        cudaError_t e0 = cudaFuncSetAttribute(f0, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(SMEM));
+        if (e0 == cudaSuccess)
+          e0 = cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(SMEM));
+        int per_sm = 0;
+        if (e0 == cudaSuccess) e0 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f0, 128, SMEM);
+        if (e0 != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e0));
+        colt_grid_ = std::max(1, per_sm) * 148;
+        colt_ready_ = true;
+      }
+      const size_t tiles = mats * (cols / 128);
+      const unsigned g = static_cast<unsigned>(std::min<size_t>(tiles, static_cast<size_t>(colt_grid_)));
+      if (inverse)
+        f1<<<g, 128, SMEM, st>>>(static_cast<const R*>(in), static_cast<R*>(out), mats, cols, tp_, tw);
+      else
+        f0<<<g, 128, SMEM, st>>>(static_cast<const R*>(in), static_cast<R*>(out), mats, cols, tp_, tw);
+      const cudaError_t e1 = cudaGetLastError();
+      if (e1 != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e1));
+      return true;
+    }
+#endif
     const size_t total = mats * cols;
     const unsigned grid = static_cast<unsigned>(std::min<size_t>((total + 127) / 128, size_t(148) * 16));
     if (inverse)
@@ -506,6 +650,8 @@ class SmallPlanImpl final : public FastPlan {
   }
 
  private:
+  bool colt_ready_ = false;
+  int colt_grid_ = 148;
   TabP<R, C::NT> tp_{};
   int grid_cap_ = 148;
 };

@@ -109,10 +109,11 @@ class CudaLocalOps:
     def __init__(self, variant, n, n1, n2, world, device, trig_mode=TrigMode.Precomputed):
         self.n, self.n1, self.n2 = n, n1, n2
         self.trig_mode = int(trig_mode)
+        # the local sub-plans use the same twiddle set (a four-step's own twiddles)
         self.p1 = Plan(variant, FunctionId.Cdft, n1, n2 // world, dtype="f32", order=Order.Fast,
-                       device=device)
+                       device=device, trig_mode=trig_mode)
         self.p2 = Plan(variant, FunctionId.Cdft, n2, n1 // world, dtype="f32", order=Order.Fast,
-                       device=device)
+                       device=device, trig_mode=trig_mode)
 
     def dft_rows1(self, a, stream=None):
         self.p1.forward(a, a, stream=stream)

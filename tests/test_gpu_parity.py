@@ -788,3 +788,20 @@ def test_fourstep_large_batch_grid_chunking(oracle, restatement):
         want = r.execute(4, O.F_CDFT, n, x[row].cpu().numpy())
         assert r.rel_l2(y[row].cpu().numpy(), want) <= 1e-12, row
     assert float((z - x).norm() / x.norm()) < 1e-14
+
+
+def test_fast_plans_onthefly_constants_are_the_table(oracle, restatement):
+    """Fast-order plans read the AM constants from the host-built table in
+    both trig modes (bitwise the reference's on-the-fly long double values,
+    variants_test.cpp:267-277): fused and small kernels give bitwise the
+    same fp64 result; only four-step twiddles depend on the mode."""
+    r, O = restatement, oracle
+    for n in (64, 4096):
+        x = O.seeded_signal(5, O.CDFT, n, 1, r)
+        for v in (2, 5):
+            a = amqft.Plan(v, amqft.FunctionId.Cdft, n, 1, dtype="f64", order=amqft.Order.Fast)
+            b = amqft.Plan(v, amqft.FunctionId.Cdft, n, 1, dtype="f64", order=amqft.Order.Fast,
+                           trig_mode=amqft.TrigMode.OnTheFly)
+            assert a.path()[0] == b.path()[0] >= 2
+            ga, gb = run_plan(a, [x])[0], run_plan(b, [x])[0]
+            assert ga.tobytes() == gb.tobytes() == r.execute(v, O.F_CDFT, n, x).tobytes(), (n, v)
