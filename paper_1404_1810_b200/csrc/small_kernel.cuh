@@ -415,21 +415,64 @@ __device__ __forceinline__ void col_twiddle(R& x, R& y, unsigned long long j, co
   y = ny;
 }
 
+// fp64 value of w_N^j from the plan's twiddle set (tables, or sincospi).
+__device__ __forceinline__ void twiddle_d(unsigned long long j, const ColTwiddle& t, double& wr, double& wi) {
+  j &= (1ull << t.logn) - 1ull;
+  if (t.onthefly) {
+    double sn, cs;
+    sincospi(static_cast<double>(j) * 2.0 / static_cast<double>(1ull << t.logn), &sn, &cs);
+    wr = cs;
+    wi = -sn;
+  } else {
+    const double2 a = t.hi[j >> t.logb], b = t.lo[j & ((1ull << t.logb) - 1ull)];
+    wr = a.x * b.x - a.y * b.y;
+    wi = a.x * b.y + a.y * b.x;
+  }
+}
+
+// Twiddles of one column, w^(col k) for the outputs k in store order: the
+// generated code stores output chunks in ascending k (the last stage,
+// SplitComplex bwd, produces them in order), so each is the previous one
+// times w^col in fp64 (~1e-14 after 64 steps); any other order falls back
+// to the direct value.  Replaces a table pair (or a sincospif) per element.
+struct TwRec {
+  double cr = 1.0, ci = 0.0, sr = 1.0, si = 0.0;
+  unsigned long long base = 0;
+  int next = 0;
+  ColTwiddle tw;
+  __device__ __forceinline__ void init(unsigned long long col_mul, const ColTwiddle& t) {
+    tw = t;
+    base = col_mul;
+    twiddle_d(col_mul, t, sr, si);
+  }
+  template <typename R>
+  __device__ __forceinline__ void apply(int k, R& x, R& y) {
+    if (k != next) twiddle_d(base * static_cast<unsigned long long>(k), tw, cr, ci);
+    const R fr = static_cast<R>(cr), fi = static_cast<R>(ci);
+    const R nx = x * fr - y * fi, ny = x * fi + y * fr;
+    x = nx;
+    y = ny;
+    const double tr = cr * sr - ci * si, ti = cr * si + ci * sr;
+    cr = tr;
+    ci = ti;
+    next = k + 1;
+  }
+};
+
 template <typename R, bool INV> struct ColIO;
 template <bool INV> struct ColIO<float, INV> {   // chunk c = complex 2c, 2c+1
   const float2* __restrict__ pi;
   float2* __restrict__ po;
   size_t stride;
-  unsigned long long col;
-  ColTwiddle tw;
+  TwRec tr;
   __device__ __forceinline__ void ld(int c, float& a, float& b, float& d, float& e) const {
     const float2 u = __ldg(pi + size_t(2 * c) * stride), v = __ldg(pi + size_t(2 * c + 1) * stride);
     if (INV) { a = u.y; b = u.x; d = v.y; e = v.x; }
     else { a = u.x; b = u.y; d = v.x; e = v.y; }
   }
-  __device__ __forceinline__ void st(int c, float a, float b, float d, float e) const {
-    col_twiddle(a, b, col * tw.mul * static_cast<unsigned long long>(2 * c), tw);
-    col_twiddle(d, e, col * tw.mul * static_cast<unsigned long long>(2 * c + 1), tw);
+  __device__ __forceinline__ void st(int c, float a, float b, float d, float e) {
+    tr.apply(2 * c, a, b);
+    tr.apply(2 * c + 1, d, e);
     po[size_t(2 * c) * stride] = make_float2(a, b);
     po[size_t(2 * c + 1) * stride] = make_float2(d, e);
   }
@@ -438,15 +481,14 @@ template <bool INV> struct ColIO<double, INV> {  // chunk c = complex c
   const double2* pi;
   double2* po;
   size_t stride;
-  unsigned long long col;
-  ColTwiddle tw;
+  TwRec tr;
   __device__ __forceinline__ void ld(int c, double& a, double& b) const {
     const double2 u = __ldg(pi + size_t(c) * stride);
     if (INV) { a = u.y; b = u.x; }
     else { a = u.x; b = u.y; }
   }
-  __device__ __forceinline__ void st(int c, double a, double b) const {
-    col_twiddle(a, b, col * tw.mul * static_cast<unsigned long long>(c), tw);
+  __device__ __forceinline__ void st(int c, double a, double b) {
+    tr.apply(c, a, b);
     po[size_t(c) * stride] = make_double2(a, b);
   }
 };
@@ -462,7 +504,8 @@ k_small_col(const R* __restrict__ in, R* __restrict__ out, size_t mats, size_t c
   for (size_t t = blockIdx.x * size_t(blockDim.x) + threadIdx.x; t < total; t += size_t(gridDim.x) * blockDim.x) {
     const size_t mat = t / cols, col = t - mat * cols;
     const size_t base = mat * N * cols + col;
-    ColIO<R, INV> io{reinterpret_cast<const C2T*>(in) + base, reinterpret_cast<C2T*>(out) + base, cols, col, tw};
+    ColIO<R, INV> io{reinterpret_cast<const C2T*>(in) + base, reinterpret_cast<C2T*>(out) + base, cols, TwRec{}};
+    io.tr.init(static_cast<unsigned long long>(col) * tw.mul, tw);
     G::template run<Arith<R>>(io, tp.v);
   }
 }
