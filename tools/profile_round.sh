@@ -6,9 +6,9 @@
 # Each ncu pass runs only after the same command exited 0 without ncu.
 set -u
 mkdir -p gpurun_out
-python bench.py --steps 20 --warmup 5 --all-variants > gpurun_out/bench_n1.log 2>&1 || { tail -5 gpurun_out/bench_n1.log; exit 1; }
+python bench.py --steps 20 --warmup 5 > gpurun_out/bench_n1.log 2>&1 || { tail -5 gpurun_out/bench_n1.log; exit 1; }
 tail -1 gpurun_out/bench_n1.log > gpurun_out/bench_n1.json
-SHORT="python bench.py --steps 2 --warmup 3 --e2e-steps 0 --no-cpu-baseline"
+SHORT="python bench.py --steps 2 --warmup 3 --e2e-steps 0 --no-cpu-baseline --no-all-variants"
 $SHORT > gpurun_out/short.log 2>&1 || { tail -5 gpurun_out/short.log; exit 1; }
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $SHORT \
   > gpurun_out/ncu_launches.log 2>&1
