@@ -235,32 +235,55 @@ struct DstPtrs {
   float2* p[kMaxParts];
 };
 
+// Each thread takes 4 consecutive k1 of one row (two 16-byte loads and
+// stores; w = n1 / nparts is a multiple of 4, so they share a slab) and
+// one twiddle evaluation: w^(n2 (k1 + e)) = w^(n2 k1) (w^n2)^e in fp64.
+__device__ __forceinline__ void scatter_tw(unsigned long long jj, int logn, const double2* __restrict__ twh,
+                                           const double2* __restrict__ twl, int logb, int onthefly, double& wr,
+                                           double& wi) {
+  jj &= (1ull << logn) - 1ull;
+  if (onthefly) {
+    double sn, cs;
+    sincospi(static_cast<double>(jj) * 2.0 / static_cast<double>(1ull << logn), &sn, &cs);
+    wr = cs;
+    wi = -sn;
+  } else {
+    const double2 a = twh[jj >> logb], b = twl[jj & ((1ull << logb) - 1ull)];
+    wr = a.x * b.x - a.y * b.y;
+    wi = a.x * b.y + a.y * b.x;
+  }
+}
+
 __global__ void __launch_bounds__(256) k_twiddle_scatter(const float2* __restrict__ in, const DstPtrs dst,
                                                          int rows, int n1, int logn, long long row0, int src,
                                                          int nparts, const double2* __restrict__ twh,
                                                          const double2* __restrict__ twl, int logb, int onthefly) {
   const int w = n1 / nparts;
-  const long long total = static_cast<long long>(rows) * n1;
+  const long long total = static_cast<long long>(rows) * (n1 / 4);
   for (long long i = threadIdx.x + static_cast<long long>(blockIdx.x) * blockDim.x; i < total;
        i += static_cast<long long>(blockDim.x) * gridDim.x) {
-    const int r = static_cast<int>(i / n1), k1 = static_cast<int>(i % n1);
+    const int r = static_cast<int>(i / (n1 / 4)), k1 = 4 * static_cast<int>(i % (n1 / 4));
     const unsigned long long n2 = static_cast<unsigned long long>(row0 + r);
-    const unsigned long long jj = (n2 * static_cast<unsigned long long>(k1)) & ((1ull << logn) - 1ull);
-    float fr, fi;
-    if (onthefly) {   // sincospif of the exact integer phase (as the fp32 four-step)
-      float sn, cs;
-      sincospif(static_cast<float>(static_cast<double>(jj) * (2.0 / static_cast<double>(1ull << logn))), &sn, &cs);
-      fr = cs;
-      fi = -sn;
-    } else {
-      const double2 a = twh[jj >> logb], b = twl[jj & ((1ull << logb) - 1ull)];
-      fr = static_cast<float>(a.x * b.x - a.y * b.y);
-      fi = static_cast<float>(a.x * b.y + a.y * b.x);
+    double cr, ci, sr, si;
+    scatter_tw(n2 * static_cast<unsigned long long>(k1), logn, twh, twl, logb, onthefly, cr, ci);
+    scatter_tw(n2, logn, twh, twl, logb, onthefly, sr, si);
+    const float4* src4 = reinterpret_cast<const float4*>(in + static_cast<long long>(r) * n1 + k1);
+    const float4 u0 = src4[0], u1 = src4[1];
+    const float v[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+    float o[8];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float fr = static_cast<float>(cr), fi = static_cast<float>(ci);
+      o[2 * e] = v[2 * e] * fr - v[2 * e + 1] * fi;
+      o[2 * e + 1] = v[2 * e] * fi + v[2 * e + 1] * fr;
+      const double tr = cr * sr - ci * si, ti = cr * si + ci * sr;
+      cr = tr;
+      ci = ti;
     }
-    const float2 v = in[i];
     const int q = k1 / w, kl = k1 - q * w;
-    dst.p[q][(static_cast<long long>(src) * rows + r) * w + kl] =
-        make_float2(v.x * fr - v.y * fi, v.x * fi + v.y * fr);
+    float4* d4 = reinterpret_cast<float4*>(dst.p[q] + (static_cast<long long>(src) * rows + r) * w + kl);
+    d4[0] = make_float4(o[0], o[1], o[2], o[3]);
+    d4[1] = make_float4(o[4], o[5], o[6], o[7]);
   }
 }
 
@@ -529,10 +552,11 @@ void dist_twiddle_scatter(const void* in, void* const* d_dst, size_t rows, size_
     tw.reset(new Twiddles(n));
     tw_dev = dev;
   }
-  if (nparts < 1 || nparts > kMaxParts || n1 % nparts) throw std::invalid_argument("twiddle_scatter: bad part count");
+  if (nparts < 1 || nparts > kMaxParts || n1 % nparts || (n1 / nparts) % 4)
+    throw std::invalid_argument("twiddle_scatter: bad part count (n1 / parts must be a multiple of 4)");
   DstPtrs dp{};
   for (int q = 0; q < nparts; ++q) dp.p[q] = static_cast<float2*>(d_dst[q]);
-  const long long total = static_cast<long long>(rows) * static_cast<long long>(n1);
+  const long long total = static_cast<long long>(rows) * static_cast<long long>(n1 / 4);
   const unsigned grid = static_cast<unsigned>(std::min<long long>((total + 255) / 256, 148LL * 16));
   k_twiddle_scatter<<<grid, 256, 0, st>>>(static_cast<const float2*>(in), dp,
                                           static_cast<int>(rows), static_cast<int>(n1), tw->logn,
