@@ -154,7 +154,7 @@ def cpu_baseline(args, seconds_target=10.0):
     return {"value": value, "unit": UNIT, "cores": used, "kind": kind,
             "sample": f"{rows} rows of CDFT N={n} (variant {args.variant}), fp32 data widened to fp64, "
                       f"{used} threads, {dt:.1f} s",
-            "gbs_fp32_bytes": value * 16 * n / 1e9}
+            "gbs_fp32_bytes": value * 16 * n / 1e9, "gbs_fp64_bytes": value * 32 * n / 1e9}
 
 
 def bench_reference(args, rank):
@@ -577,6 +577,8 @@ def main():
                        "l2": "inputs 2 GiB per GPU > 126 MB L2; no flush",
                        "parallelism": f"batch-sharded x{world}, no communication"},
             "gbs": alg_bytes * world / (ms_per_step / 1000.0) / 1e9,
+            "per_gpu": {"transforms_per_s": value / world, "gbs": alg_bytes / (ms_per_step / 1000.0) / 1e9,
+                        "frac_of_n_x_hbm": (alg_bytes * world / (ms_per_step / 1000.0) / 1e9) / (world * hbm)},
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
