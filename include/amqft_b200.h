@@ -152,6 +152,20 @@ amqft_status amqft_dist_twiddle_scatter(const void* d_rows, void* const* d_dst, 
                                         size_t n1, size_t n, size_t row0, int src_rank,
                                         int nparts, int trig_mode, void* stream);
 
+/* Distributed four-step with the local four-step's final transpose folded
+ * into the scatter (config 5): for a column-mode four-step plan (path 3),
+ * amqft_plan_transposed_factor gives its column factor A (0 otherwise) and
+ * amqft_exec_rows_transposed leaves each row as out[r][ka][kb] = X[ka + A kb];
+ * amqft_dist_twiddle_scatter_t is amqft_dist_twiddle_scatter for rows in
+ * that order (A and n1/A multiples of 32, n1/nparts a multiple of 32).
+ * Replaces nothing in the reference (it has no distributed path). */
+amqft_status amqft_plan_transposed_factor(amqft_plan plan, size_t* a);
+amqft_status amqft_exec_rows_transposed(amqft_plan plan, const void* d_in, void* d_out, size_t rows,
+                                        void* stream);
+amqft_status amqft_dist_twiddle_scatter_t(const void* d_rows, void* const* d_dst, size_t rows, size_t n1,
+                                          size_t n, size_t row0, int src_rank, int nparts, int trig_mode,
+                                          size_t a, void* stream);
+
 /* Batched transpose of complex fp32 matrices: mats x [r][c] -> [c][r];
  * r and c multiples of 32. */
 amqft_status amqft_transpose_c64(const void* d_in, void* d_out, size_t mats, size_t r,

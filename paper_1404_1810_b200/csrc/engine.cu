@@ -533,6 +533,50 @@ amqft_status amqft_dist_twiddle_scatter(const void* d_rows, void* const* d_dst, 
   return AMQFT_OK;
 }
 
+amqft_status amqft_plan_transposed_factor(amqft_plan P, size_t* a) {
+  if (!P || !a) return set_err(AMQFT_EINVAL, "null argument");
+  *a = (P->path == 3 && P->fast) ? P->fast->transposed_factor() : 0;
+  return AMQFT_OK;
+}
+
+amqft_status amqft_exec_rows_transposed(amqft_plan P, const void* in, void* out, size_t rows, void* stream) {
+  if (!P) return set_err(AMQFT_EINVAL, "null plan");
+  if (rows > P->d.batch) return set_err(AMQFT_EINVAL, "rows exceed the plan batch");
+  if (P->path != 3 || !P->fast || P->fast->transposed_factor() == 0)
+    return set_err(AMQFT_EINVAL, "transposed output needs a column-mode four-step plan");
+  if (!in || !out) return set_err(AMQFT_EINVAL, "null data pointer");
+  if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15u)
+    return set_err(AMQFT_EINVAL, "device buffers of fast-order plans must be 16-byte aligned");
+  if (rows == 0) return AMQFT_OK;
+  try {
+    ck(cudaSetDevice(P->d.device), "cudaSetDevice");
+    P->fast->exec_transposed(in, out, rows, static_cast<cudaStream_t>(stream));
+  } catch (const std::invalid_argument& e) {
+    return set_err(AMQFT_EINVAL, e.what());
+  } catch (const std::runtime_error& e) {
+    return set_err(AMQFT_ECUDA, e.what());
+  }
+  return AMQFT_OK;
+}
+
+amqft_status amqft_dist_twiddle_scatter_t(const void* d_rows, void* const* d_dst, size_t rows, size_t n1,
+                                          size_t n, size_t row0, int src_rank, int nparts, int trig_mode,
+                                          size_t a, void* stream) {
+  if (!d_rows || !d_dst) return set_err(AMQFT_EINVAL, "null pointer");
+  if (n == 0 || (n & (n - 1)) || n1 == 0 || (n1 & (n1 - 1)) || n % n1 || n > (size_t(1) << 40))
+    return set_err(AMQFT_EINVAL, "n and n1 must be powers of two with n1 | n");
+  if (src_rank < 0 || src_rank >= nparts) return set_err(AMQFT_EINVAL, "src_rank out of range");
+  try {
+    dist_twiddle_scatter_t(d_rows, d_dst, rows, n1, n, row0, src_rank, nparts, trig_mode, a,
+                           static_cast<cudaStream_t>(stream));
+  } catch (const std::invalid_argument& e) {
+    return set_err(AMQFT_EINVAL, e.what());
+  } catch (const std::runtime_error& e) {
+    return set_err(AMQFT_ECUDA, e.what());
+  }
+  return AMQFT_OK;
+}
+
 amqft_status amqft_transpose_c64(const void* d_in, void* d_out, size_t mats, size_t r, size_t c,
                                  void* stream) {
   if (!d_in || !d_out) return set_err(AMQFT_EINVAL, "null pointer");

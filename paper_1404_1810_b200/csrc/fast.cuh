@@ -33,6 +33,11 @@ class FastPlan {
                             const ColTwiddle&, cudaStream_t) {
     return false;
   }
+  // Column-mode four-steps only (distributed four-step, config 5): the
+  // transform without its final transpose, rows left as out[r][ka][kb] =
+  // X[ka + A kb]; returns A, or 0 when the plan has no such mode.
+  virtual size_t transposed_factor() const { return 0; }
+  virtual void exec_transposed(const void*, void*, size_t, cudaStream_t) {}
   int launches = 1;
 };
 

@@ -287,6 +287,45 @@ __global__ void __launch_bounds__(256) k_twiddle_scatter(const float2* __restric
   }
 }
 
+// The same scatter for rows left in a column-mode four-step's transposed
+// order in[r][ka][kb] = row value at k1 = ka + A kb (A x B, B = n1 / A):
+// the four-step's final transpose folded in.  32 x 32 tiles (ka, kb) per
+// row: reads coalesced along kb, writes along ka (consecutive k1, one
+// slab when w is a multiple of 32); per thread 4 elements kb + 8 j share
+// one twiddle evaluation and a recurrence (step w^(8 A n2)).
+__global__ void __launch_bounds__(256) k_twiddle_scatter_t(const float2* __restrict__ in, const DstPtrs dst,
+                                                           int rows, int n1, int A, int logn, long long row0,
+                                                           int src, int nparts, const double2* __restrict__ twh,
+                                                           const double2* __restrict__ twl, int logb, int onthefly) {
+  __shared__ float2 tile[32][33];
+  const int B = n1 / A, w = n1 / nparts;
+  const int r = blockIdx.z;
+  const int kb0 = blockIdx.x * 32, ka0 = blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
+  const float2* row = in + static_cast<long long>(r) * n1;
+#pragma unroll
+  for (int j = 0; j < 32; j += 8) tile[ty + j][tx] = row[static_cast<long long>(ka0 + ty + j) * B + kb0 + tx];
+  __syncthreads();
+  const unsigned long long n2 = static_cast<unsigned long long>(row0 + r);
+  const int ka = ka0 + tx;
+  double cr, ci, sr, si;
+  scatter_tw(n2 * static_cast<unsigned long long>(ka + A * (kb0 + ty)), logn, twh, twl, logb, onthefly, cr, ci);
+  scatter_tw(n2 * static_cast<unsigned long long>(8 * A), logn, twh, twl, logb, onthefly, sr, si);
+#pragma unroll
+  for (int j = 0; j < 32; j += 8) {
+    const int kb = kb0 + ty + j;
+    const float2 v = tile[tx][ty + j];
+    const float fr = static_cast<float>(cr), fi = static_cast<float>(ci);
+    const int k1 = ka + A * kb;
+    const int q = k1 / w, kl = k1 - q * w;
+    dst.p[q][(static_cast<long long>(src) * rows + r) * w + kl] =
+        make_float2(v.x * fr - v.y * fi, v.x * fi + v.y * fr);
+    const double t0 = cr * sr - ci * si, t1 = cr * si + ci * sr;
+    cr = t0;
+    ci = t1;
+  }
+}
+
 int lg2(size_t v) {
   int l = 0;
   while ((size_t(1) << l) < v) ++l;
@@ -417,6 +456,19 @@ class FourStepPlan final : public FastPlan {
     check(cudaMalloc(&scratch_, batch_ * n_ * sizeof(V2)), "cudaMalloc four-step scratch");
     if (three_) check(cudaMalloc(&scratch2_, batch_ * n_ * sizeof(V2)), "cudaMalloc four-step scratch");
     launches = three_ ? 4 : (col_ ? 1 + p1_->launches + p2_->launches : 3 + p1_->launches + p2_->launches);
+  }
+  size_t transposed_factor() const override { return (col_ && !three_) ? n1_ : 0; }
+  void exec_transposed(const void* in, void* out, size_t rows, cudaStream_t st) override {
+    if (!col_ || three_) throw std::invalid_argument("transposed output needs a column-mode four-step");
+    ColTwiddle tw;
+    tw.hi = twh_;
+    tw.lo = twl_;
+    tw.logb = logb_;
+    tw.logn = logn_;
+    tw.onthefly = onthefly_ ? 1 : 0;
+    if (!p1_->exec_columns(in, scratch_, rows, n2_, 0, tw, st))
+      throw std::runtime_error("four-step: sub-plan has no column mode");
+    p2_->exec(scratch_, out, rows * n1_, 0, st);
   }
   ~FourStepPlan() override {
     if (scratch2_) cudaFree(scratch2_);
@@ -564,6 +616,31 @@ void dist_twiddle_scatter(const void* in, void* const* d_dst, size_t rows, size_
                                           trig_mode == AMQFT_TRIG_ONTHEFLY ? 1 : 0);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("k_twiddle_scatter: ") + cudaGetErrorString(e));
+}
+
+void dist_twiddle_scatter_t(const void* in, void* const* d_dst, size_t rows, size_t n1, size_t n, size_t row0,
+                            int src, int nparts, int trig_mode, size_t a, cudaStream_t st) {
+  static thread_local std::unique_ptr<Twiddles> tw;
+  static thread_local int tw_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!tw || (size_t(1) << tw->logn) != n || tw_dev != dev) {
+    tw.reset(new Twiddles(n));
+    tw_dev = dev;
+  }
+  if (nparts < 1 || nparts > kMaxParts || n1 % nparts || (n1 / nparts) % 32)
+    throw std::invalid_argument("twiddle_scatter_t: n1 / parts must be a multiple of 32");
+  if (a == 0 || a % 32 || n1 % a || (n1 / a) % 32 || rows > 65535)
+    throw std::invalid_argument("twiddle_scatter_t: A and n1 / A must be multiples of 32, rows <= 65535");
+  DstPtrs dp{};
+  for (int q = 0; q < nparts; ++q) dp.p[q] = static_cast<float2*>(d_dst[q]);
+  const dim3 grid(static_cast<unsigned>(n1 / a / 32), static_cast<unsigned>(a / 32), static_cast<unsigned>(rows));
+  k_twiddle_scatter_t<<<grid, dim3(32, 8), 0, st>>>(static_cast<const float2*>(in), dp, static_cast<int>(rows),
+                                                     static_cast<int>(n1), static_cast<int>(a), tw->logn,
+                                                     static_cast<long long>(row0), src, nparts, tw->hi, tw->lo,
+                                                     tw->logb, trig_mode == AMQFT_TRIG_ONTHEFLY ? 1 : 0);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string("k_twiddle_scatter_t: ") + cudaGetErrorString(e));
 }
 
 void transpose_c64(const void* in, void* out, size_t mats, size_t r, size_t c, cudaStream_t st) {

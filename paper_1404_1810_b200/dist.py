@@ -115,13 +115,29 @@ class CudaLocalOps:
         self.p2 = Plan(variant, FunctionId.Cdft, n2, n1 // world, dtype="f32", order=Order.Fast,
                        device=device, trig_mode=trig_mode)
 
+        # a column-mode four-step for n1 leaves its rows transposed and the
+        # scatter reads them in that order (its final transpose folded in)
+        fa = C.c_size_t(0)
+        check(lib().amqft_plan_transposed_factor(self.p1._h, C.byref(fa)))
+        w = n1 // world
+        self.a_t = fa.value if (fa.value and fa.value % 32 == 0 and (n1 // fa.value) % 32 == 0 and w % 32 == 0
+                                and n2 // world <= 65535) else 0
+
     def dft_rows1(self, a, stream=None):
-        self.p1.forward(a, a, stream=stream)
+        if self.a_t:
+            check(lib().amqft_exec_rows_transposed(self.p1._h, int(a.data_ptr()), int(a.data_ptr()),
+                                                   a.shape[0], Plan._stream(stream)))
+        else:
+            self.p1.forward(a, a, stream=stream)
 
     def twiddle_scatter(self, a, dst_ptrs, rows, row0, src, nparts, stream=None):
         arr = (C.c_void_p * nparts)(*[int(p) for p in dst_ptrs])
-        check(lib().amqft_dist_twiddle_scatter(int(a.data_ptr()), arr, rows, self.n1, self.n, row0, src,
-                                               nparts, self.trig_mode, Plan._stream(stream)))
+        if self.a_t:
+            check(lib().amqft_dist_twiddle_scatter_t(int(a.data_ptr()), arr, rows, self.n1, self.n, row0, src,
+                                                     nparts, self.trig_mode, self.a_t, Plan._stream(stream)))
+        else:
+            check(lib().amqft_dist_twiddle_scatter(int(a.data_ptr()), arr, rows, self.n1, self.n, row0, src,
+                                                   nparts, self.trig_mode, Plan._stream(stream)))
 
     def transpose(self, inp, out, r, c, stream=None):
         check(lib().amqft_transpose_c64(int(inp.data_ptr()), int(out.data_ptr()), 1, r, c,

@@ -805,3 +805,49 @@ def test_fast_plans_onthefly_constants_are_the_table(oracle, restatement):
             assert a.path()[0] == b.path()[0] >= 2
             ga, gb = run_plan(a, [x])[0], run_plan(b, [x])[0]
             assert ga.tobytes() == gb.tobytes() == r.execute(v, O.F_CDFT, n, x).tobytes(), (n, v)
+
+
+def test_distributed_fourstep_transposed_scatter():
+    """Config-5 shape with a column-mode local four-step (N = 2^29: n1 = 2^17
+    = 32 x 4096, n2 = 2^12): the local four-step leaves its rows transposed
+    and the twiddle-scatter reads them in that order (final transpose
+    folded in).  Against the unfolded path on the same device data (1e-6),
+    and worlds 2 (both exchange modes) bitwise equal to world 1."""
+    from paper_1404_1810_b200.dist import DistFourStep
+    n = 1 << 29
+    g = torch.Generator(device=DEV).manual_seed(29)
+
+    def run(world, mode, force_plain=False):
+        ranks = [DistFourStep(4, n, world=world, rank=p, device=0) for p in range(world)]
+        d0 = ranks[0]
+        if force_plain:
+            for rk in ranks:
+                rk.ops.a_t = 0
+        assert force_plain or d0.ops.a_t == 32, d0.ops.a_t
+        xg = xdev.view(d0.n1, d0.n2, 2)
+        slabs = [xg[:, p * d0.rows1:(p + 1) * d0.rows1, :].permute(1, 0, 2).reshape(d0.rows1, 2 * d0.n1).contiguous()
+                 for p in range(world)]
+        bufs = [rk.buffers(slabs[0]) for rk in ranks]
+        if mode == "peer":
+            peer = [int(b[1].data_ptr()) for b in bufs]
+            for rk, a, b in zip(ranks, slabs, bufs):
+                rk.stage1(a, b[0], peer_recv=peer)
+        else:
+            for rk, a, b in zip(ranks, slabs, bufs):
+                rk.stage1(a, b[0])
+            for q in range(world):
+                for p in range(world):
+                    bufs[q][1][p].copy_(bufs[p][0][q])
+        torch.cuda.synchronize()
+        outs = [rk.stage2(b[1], b[2], b[3]).clone() for rk, b in zip(ranks, bufs)]
+        torch.cuda.synchronize()
+        return torch.cat([o.reshape(-1) for o in outs])
+
+    xdev = torch.randn(2 * n, device=DEV, generator=g)
+    base = run(1, "a2a")
+    plain = run(1, "a2a", force_plain=True)
+    rel = float((base - plain).norm() / plain.norm())
+    assert rel < 1e-6, rel
+    for mode in ("a2a", "peer"):
+        got = run(2, mode)
+        assert torch.equal(got, base), mode
