@@ -383,7 +383,11 @@ def bench_single(args, world, rank, local):
             a2a_ms = _timed(lambda: dist.all_to_all_single(bufs[1], bufs[0]), args.steps, 1, stream, world, dev)
         sent = (world - 1) * d.rows1 * d.w * 8
         ms = ms - copy_ms        # the slab refresh is not part of the transform
-        path, launches = 3, None
+        # our kernels per step: the local length-n1 plan (its final transpose
+        # folded into the scatter when it runs transposed), the twiddle-scatter,
+        # the transpose, the length-n2 plan
+        l1 = d.ops.p1.path()[1] - (1 if d.ops.a_t else 0)
+        path, launches = 3, l1 + 2 + d.ops.p2.path()[1]
         workload = (f"config 5: one complex forward DFT N=2^30 fp32 over {world} GPU(s), distributed four-step "
                     f"n1=2^{d.n1.bit_length() - 1} x n2=2^{d.n2.bit_length() - 1}, one all-to-all, on-the-fly twiddles, "
                     f"variant {args.variant}")
@@ -406,7 +410,9 @@ def bench_single(args, world, rank, local):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": None, "peak_source": hbm_src,
                          "algorithmic_bytes_per_gpu": per_gpu_bytes},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, **extra,
+            "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches * args.steps if launches is not None else None,   # inside the timed region
+            "launches_per_step": launches, **extra,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
