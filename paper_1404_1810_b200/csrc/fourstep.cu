@@ -242,9 +242,9 @@ __device__ __forceinline__ void scatter_tw(unsigned long long jj, int logn, cons
                                            const double2* __restrict__ twl, int logb, int onthefly, double& wr,
                                            double& wi) {
   jj &= (1ull << logn) - 1ull;
-  if (onthefly) {
-    double sn, cs;
-    sincospi(static_cast<double>(jj) * 2.0 / static_cast<double>(1ull << logn), &sn, &cs);
+  if (onthefly) {   // fp32 data: sincospif of the exact integer phase (as the fp32 four-step)
+    float sn, cs;
+    sincospif(static_cast<float>(static_cast<double>(jj) * (2.0 / static_cast<double>(1ull << logn))), &sn, &cs);
     wr = cs;
     wi = -sn;
   } else {
