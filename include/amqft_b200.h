@@ -95,7 +95,17 @@ typedef struct {
 } amqft_plan_desc;
 
 /* Plan lifecycle.  Creation compiles the schedule, uploads it and the
- * constant table, and sizes the workspace; exec allocates nothing. */
+ * constant table, and allocates every workspace the device entry points
+ * use (four-step scratch, the real inverses' scratch and sub-plans, fp64
+ * working rows): amqft_exec_forward / _inverse / _rows allocate nothing and
+ * are stream-ordered (CUDA-graph capturable).  amqft_exec_host_rows creates
+ * its pipeline slots and streams on its first call (serialised per plan).
+ *
+ * fp32 plans of variants 5-8 at n >= 512 compute in fp64 (their fp32
+ * recursion amplifies rounding beyond 1e-5 log2 n): fp32 rows in and out,
+ * the reference's fp64 DAG inside where the plan runs it (the fused kernel
+ * at n = 1024-4096, the exact order), a four-step over stable
+ * sub-transforms elsewhere in the fast order. */
 amqft_status amqft_plan_create(amqft_plan* out, const amqft_plan_desc* desc);
 amqft_status amqft_plan_destroy(amqft_plan plan);
 
@@ -176,9 +186,15 @@ amqft_status amqft_transpose_c64(const void* d_in, void* d_out, size_t mats, siz
 amqft_status amqft_plan_op_counts(amqft_plan plan, uint64_t* out3);
 
 /* Which kernel path the plan uses: 0 generic single-CTA schedule,
- * 1 generic multi-pass, 2 fused fast kernel.  Number of kernel launches
- * per exec call in *launches. */
+ * 1 generic multi-pass, 2 fused fast kernel, 3 four-step, 4 small-CDFT /
+ * cooperative kernels, 5 fp32 rows through an fp64 plan (widen, fp64
+ * plan, narrow).  Number of kernel launches per exec call in *launches. */
 amqft_status amqft_plan_path(amqft_plan plan, int* path, int* launches);
+
+/* Four-step plans (path 3): the factors f3 = {A, B, C} with n = A B C
+ * (two-factor plans: B = 1, n = A C; A is the column / first factor).
+ * AMQFT_EINVAL for other paths. */
+amqft_status amqft_plan_fourstep_factors(amqft_plan plan, size_t* f3);
 
 /* Serialise the compiled schedule for host-side inspection (tests):
  * writes up to cap 16-byte elaboration records {op,lens,flags,am,n,off,aux}

@@ -165,15 +165,22 @@ class Plan:
             return int(stream.cuda_stream)
         return int(stream)
 
+    def _check_dtype(self, t):
+        import torch
+        want = torch.float64 if self.dtype == "f64" else torch.float32
+        if t.dtype != want:
+            raise InvalidArgument(_native.EINVAL, f"tensor dtype {t.dtype} does not match plan dtype {self.dtype}")
+
     def _check_tensor(self, t, rows):
         if hasattr(t, "is_cuda"):
             if not t.is_cuda:
                 raise InvalidArgument(_native.EINVAL, "device tensors required")
+            if t.device.index is not None and t.device.index != self.device:
+                raise InvalidArgument(_native.EINVAL,
+                                      f"tensor on cuda:{t.device.index}, plan on cuda:{self.device}")
             if not t.is_contiguous():
                 raise InvalidArgument(_native.EINVAL, "contiguous tensors required")
-            want = 8 if self.dtype == "f64" else 4
-            if t.element_size() != want:
-                raise InvalidArgument(_native.EINVAL, f"tensor dtype does not match plan dtype {self.dtype}")
+            self._check_dtype(t)
             if t.numel() < rows * self.cells:
                 raise InvalidArgument(_native.EINVAL, "tensor smaller than rows * cells")
 
@@ -197,9 +204,7 @@ class Plan:
                 raise InvalidArgument(_native.EINVAL, "host tensors required")
             if not t.is_contiguous():
                 raise InvalidArgument(_native.EINVAL, "contiguous tensors required")
-            want = 8 if self.dtype == "f64" else 4
-            if t.element_size() != want:
-                raise InvalidArgument(_native.EINVAL, f"tensor dtype does not match plan dtype {self.dtype}")
+            self._check_dtype(t)
             if t.numel() < rows * self.cells:
                 raise InvalidArgument(_native.EINVAL, "tensor smaller than rows * cells")
 
@@ -217,6 +222,12 @@ class Plan:
         out = (C.c_uint64 * 3)()
         check(lib().amqft_plan_op_counts(self._h, out))
         return tuple(int(v) for v in out)
+
+    def fourstep_factors(self):
+        """(A, B, C) with n = A B C for a four-step plan (B = 1: two factors)."""
+        f = (C.c_size_t * 3)()
+        check(lib().amqft_plan_fourstep_factors(self._h, f))
+        return tuple(int(v) for v in f)
 
     def path(self):
         p, n = C.c_int(), C.c_int()

@@ -75,6 +75,7 @@ def lib() -> C.CDLL:
     L.amqft_execute_host.argtypes = [C.c_int, C.c_int, sz, vp, vp, C.c_int, sz, C.c_int, vp]
     L.amqft_plan_op_counts.argtypes = [vp, vp]
     L.amqft_plan_path.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+    L.amqft_plan_fourstep_factors.argtypes = [vp, C.POINTER(sz)]
     L.amqft_plan_dump.argtypes = [vp, C.c_int, vp, sz, C.POINTER(sz), vp, sz, C.POINTER(sz)]
     L.amqft_schedule_dump.argtypes = [C.c_int, C.c_int, sz, sz, vp, sz, C.POINTER(sz), vp, sz,
                                       C.POINTER(sz), vp]
@@ -85,7 +86,7 @@ def lib() -> C.CDLL:
                  "amqft_exec_inverse", "amqft_exec_rows", "amqft_exec_host_rows", "amqft_execute_host",
                  "amqft_dist_twiddle_scatter", "amqft_transpose_c64", "amqft_plan_transposed_factor",
                  "amqft_exec_rows_transposed", "amqft_dist_twiddle_scatter_t",
-                 "amqft_plan_op_counts", "amqft_plan_path", "amqft_plan_dump",
+                 "amqft_plan_op_counts", "amqft_plan_path", "amqft_plan_fourstep_factors", "amqft_plan_dump",
                  "amqft_schedule_dump", "amqft_device_synchronize"):
         getattr(L, name).restype = C.c_int
     _lib = L

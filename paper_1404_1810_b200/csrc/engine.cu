@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -56,6 +57,30 @@ void ck(cudaError_t e, const char* what) {
     throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// Every extern "C" entry point ends in `catch (...) { return from_exception(); }`:
+// no C++ exception crosses the C ABI.  std::invalid_argument (the
+// reference's error type, variants.cpp:404-421) -> EINVAL; allocation
+// failures (host bad_alloc, cudaErrorMemoryAllocation) -> ENOMEM; any other
+// error (CUDA launch/runtime) -> ECUDA.
+amqft_status from_exception() {
+  try {
+    throw;
+  } catch (const std::invalid_argument& e) {
+    return set_err(AMQFT_EINVAL, e.what());
+  } catch (const std::bad_alloc&) {
+    return set_err(AMQFT_ENOMEM, "host allocation failed");
+  } catch (const std::exception& e) {
+    const std::string m = e.what();
+    if (m.find(cudaGetErrorString(cudaErrorMemoryAllocation)) != std::string::npos) {
+      cudaGetLastError();   // clear the (non-sticky) allocation error
+      return set_err(AMQFT_ENOMEM, m);
+    }
+    return set_err(AMQFT_ECUDA, m);
+  } catch (...) {
+    return set_err(AMQFT_ECUDA, "unknown exception");
+  }
+}
+
 // Kernels and launchers live in generic_kernels.cuh (instantiated per dtype
 // in generic_f32.cu / generic_f64.cu so the build parallelises).
 
@@ -88,13 +113,20 @@ struct amqft_plan_s {
   std::unique_ptr<FastPlan> fast;
   int launches = 0;
   int sms = 148;
-  // host-buffer pipeline (amqft_exec_host_rows), created on first use
+  // fp32 rows computed by an fp64 plan (fast.cuh f32_needs_f64_compute,
+  // path 5): widen into wide_in, run `wide`, narrow from wide_out
+  amqft_plan_s* wide = nullptr;
+  void* wide_in = nullptr;
+  void* wide_out = nullptr;
+  // host-buffer pipeline (amqft_exec_host_rows), created on its first call
+  // (serialised by host_mu: one pipeline per plan)
+  std::mutex host_mu;
   static constexpr int NSLOT = 3;
   void* slot[NSLOT] = {nullptr, nullptr, nullptr};
   size_t slot_rows = 0;
   cudaStream_t s_h2d = nullptr, s_run = nullptr, s_d2h = nullptr;
   cudaEvent_t ev_h2d[NSLOT] = {}, ev_run[NSLOT] = {}, ev_d2h[NSLOT] = {}, ev_in = nullptr;
-  // inverses of the real transforms (inverse.cu), created on first use
+  // inverses of the real transforms (inverse.cu), created with the plan
   void* inv_a = nullptr;
   void* inv_b = nullptr;
   amqft_plan_s* inv_dct = nullptr;
@@ -103,6 +135,7 @@ struct amqft_plan_s {
   ~amqft_plan_s() {
     delete inv_dct;
     delete inv_dst;
+    delete wide;
     if (inv_a) cudaFree(inv_a);
     if (inv_b) cudaFree(inv_b);
     int cur = 0;
@@ -112,7 +145,7 @@ struct amqft_plan_s {
                     static_cast<void*>(d_prefix), static_cast<void*>(d_stages),
                     static_cast<void*>(d_progs), static_cast<void*>(d_jobs),
                     static_cast<void*>(d_geis), static_cast<void*>(d_gprefix),
-                    bufA, bufB, slot[0], slot[1], slot[2]})
+                    bufA, bufB, slot[0], slot[1], slot[2], wide_in, wide_out})
       if (p) cudaFree(p);
     for (cudaStream_t q : {s_h2d, s_run, s_d2h})
       if (q) cudaStreamDestroy(q);
@@ -253,6 +286,41 @@ void exec_generic(amqft_plan_s* P, const void* in, void* out, size_t rows,
   ck(launch_copy<R>(c.root_dst ? B : A, out, total, swap, scale, cgrid, st), "k_copy_rows");
 }
 
+bool inverse_defined(const amqft_plan_s* P) {
+  return P->d.function == AMQFT_FN_CDFT ||
+         ((P->d.function == AMQFT_FN_RDFT || P->d.function == AMQFT_FN_DCT || P->d.function == AMQFT_FN_DST) &&
+          P->d.n >= 4);
+}
+
+// The real-transform inverses' scratch rows and DCT-0 / DST-0 sub-plans
+// (inverse.cu) are made with the plan, so exec allocates nothing.
+thread_local bool g_inverse_subplan = false;   // creating an inverse's own sub-plans
+
+void prepare_inverse(amqft_plan_s* P) {
+  if (g_inverse_subplan) return;   // the sub-plans only run forward
+  if (!inverse_defined(P) || P->d.function == AMQFT_FN_CDFT || P->d.function == AMQFT_FN_DST) return;
+  const size_t h = P->d.n / 2;
+  if (P->d.function == AMQFT_FN_DCT) {
+    ck(cudaMalloc(&P->inv_a, P->d.batch * P->c.cells * P->esize), "cudaMalloc inverse scratch");
+    return;
+  }
+  auto sub = [&](int fn) -> amqft_plan_s* {
+    amqft_plan_desc d = P->d;
+    d.function = fn;
+    amqft_plan q = nullptr;
+    g_inverse_subplan = true;
+    const amqft_status s = amqft_plan_create(&q, &d);
+    g_inverse_subplan = false;
+    if (s == AMQFT_ENOMEM) throw CudaError(std::string("inverse sub-plan: ") + g_err);
+    if (s != AMQFT_OK) throw std::runtime_error(std::string("inverse sub-plan: ") + g_err);
+    return q;
+  };
+  P->inv_dct = sub(AMQFT_FN_DCT);
+  P->inv_dst = sub(AMQFT_FN_DST);
+  ck(cudaMalloc(&P->inv_a, P->d.batch * (h + 1) * P->esize), "cudaMalloc inverse scratch");
+  ck(cudaMalloc(&P->inv_b, P->d.batch * (h - 1) * P->esize), "cudaMalloc inverse scratch");
+}
+
 amqft_status validate_desc(const amqft_plan_desc* d) {
   if (!d) return set_err(AMQFT_EINVAL, "null plan descriptor");
   if (d->variant < 1 || d->variant > 8) return set_err(AMQFT_EINVAL, "variant number must be in 1..8");
@@ -324,20 +392,41 @@ amqft_status amqft_plan_create(amqft_plan* out, const amqft_plan_desc* desc) {
         P->c.cells = fn_cells(desc->function, n);
         P->c.ops = fpath == 2 ? fast_op_counts(*desc) : fpath == 4 ? small_ops : fourstep_op_counts(*desc);
         P->launches = P->fast->launches;
+        prepare_inverse(P.get());
         *out = P.release();
         return AMQFT_OK;
       }
+    }
+    if (desc->dtype == AMQFT_F32 && f32_needs_f64_compute(desc->variant, n)) {
+      // fp32 rows through an fp64 plan of the same request (the generic
+      // exact path, or the fp64 fast paths): the fp32 recursion of the
+      // sine-family variants is unstable at this size (fast.cuh)
+      amqft_plan_desc d64 = *desc;
+      d64.dtype = AMQFT_F64;
+      amqft_plan w = nullptr;
+      const amqft_status s = amqft_plan_create(&w, &d64);
+      if (s != AMQFT_OK) return s;
+      P->wide = w;
+      P->c.variant = desc->variant;
+      P->c.fn = desc->function;
+      P->c.n = n;
+      P->c.cells = w->c.cells;
+      P->c.ops = w->c.ops;
+      const size_t bytes = desc->batch * P->c.cells * sizeof(double);
+      ck(cudaMalloc(&P->wide_in, bytes), "cudaMalloc fp64 working rows");
+      ck(cudaMalloc(&P->wide_out, bytes), "cudaMalloc fp64 working rows");
+      P->path = 5;
+      P->launches = w->launches + 2;
+      *out = P.release();
+      return AMQFT_OK;
     }
     P->capacity = desc->dtype == AMQFT_F64 ? 8192 : 16384;
     P->c = compile(desc->variant, desc->function, n, P->capacity);
     P->path = P->c.single ? 0 : 1;
     build_generic(P.get());
-  } catch (const std::invalid_argument& e) {
-    return set_err(AMQFT_EINVAL, e.what());
-  } catch (const CudaError& e) {
-    return set_err(AMQFT_ECUDA, e.what());
-  } catch (const std::bad_alloc&) {
-    return set_err(AMQFT_ENOMEM, "host allocation failed");
+    prepare_inverse(P.get());
+  } catch (...) {
+    return from_exception();
   }
   *out = P.release();
   return AMQFT_OK;
@@ -352,26 +441,11 @@ size_t amqft_plan_cells(amqft_plan plan) { return plan ? plan->c.cells : 0; }
 
 namespace {
 
-bool inverse_defined(const amqft_plan_s* P) {
-  return P->d.function == AMQFT_FN_CDFT ||
-         ((P->d.function == AMQFT_FN_RDFT || P->d.function == AMQFT_FN_DCT || P->d.function == AMQFT_FN_DST) &&
-          P->d.n >= 4);
-}
-
 // Inverse RDFT / DCT-0 / DST-0 (inverse.cu): the plan's own forward DCT-0 /
 // DST-0 between exact power-of-two weightings.
 amqft_status exec_real_inverse(amqft_plan_s* P, const void* in, void* out, size_t rows, cudaStream_t st) {
   const int f64 = P->d.dtype == AMQFT_F64;
   const double n = static_cast<double>(P->d.n);
-  const size_t h = P->d.n / 2;
-  auto sub = [&](int fn) -> amqft_plan_s* {
-    amqft_plan_desc d = P->d;
-    d.function = fn;
-    amqft_plan q = nullptr;
-    const amqft_status s = amqft_plan_create(&q, &d);
-    if (s != AMQFT_OK) throw std::runtime_error(std::string("inverse sub-plan: ") + g_err);
-    return q;
-  };
   if (P->d.function == AMQFT_FN_DST) {          // (4/N) DST-0(S)
     amqft_status s = amqft_exec_rows(P, in, out, rows, 0, st);
     if (s != AMQFT_OK) return s;
@@ -379,7 +453,6 @@ amqft_status exec_real_inverse(amqft_plan_s* P, const void* in, void* out, size_
     return AMQFT_OK;
   }
   if (P->d.function == AMQFT_FN_DCT) {          // (4/N) W DCT-0(W C)
-    if (!P->inv_a) ck(cudaMalloc(&P->inv_a, P->d.batch * P->c.cells * P->esize), "cudaMalloc inverse scratch");
     inv_weight(f64, in, P->inv_a, rows, P->c.cells, 1.0, 0.5, st);
     amqft_status s = amqft_exec_rows(P, P->inv_a, out, rows, 0, st);
     if (s != AMQFT_OK) return s;
@@ -387,10 +460,6 @@ amqft_status exec_real_inverse(amqft_plan_s* P, const void* in, void* out, size_
     return AMQFT_OK;
   }
   // RDFT: split the packed spectrum, DCT-0 and DST-0 inverses, butterfly
-  if (!P->inv_dct) P->inv_dct = sub(AMQFT_FN_DCT);
-  if (!P->inv_dst) P->inv_dst = sub(AMQFT_FN_DST);
-  if (!P->inv_a) ck(cudaMalloc(&P->inv_a, P->d.batch * (h + 1) * P->esize), "cudaMalloc inverse scratch");
-  if (!P->inv_b) ck(cudaMalloc(&P->inv_b, P->d.batch * (h - 1) * P->esize), "cudaMalloc inverse scratch");
   inv_rdft_split(f64, in, P->inv_a, P->inv_b, rows, P->d.n, st);
   amqft_status s = amqft_exec_rows(P->inv_dct, P->inv_a, P->inv_a, rows, 0, st);
   if (s == AMQFT_OK) s = amqft_exec_rows(P->inv_dst, P->inv_b, P->inv_b, rows, 0, st);
@@ -407,23 +476,36 @@ amqft_status amqft_exec_rows(amqft_plan P, const void* in, void* out, size_t row
   if (rows > P->d.batch) return set_err(AMQFT_EINVAL, "rows exceed the plan batch");
   if (inverse && !inverse_defined(P))
     return set_err(AMQFT_EINVAL, "the inverse is defined for CDFT, and for RDFT / DCT / DST plans with n >= 4");
+  if (P->wide) {   // fp32 rows, fp64 plan (path 5)
+    if (rows == 0) return AMQFT_OK;
+    if (!in || !out) return set_err(AMQFT_EINVAL, "null data pointer");
+    try {
+      ck(cudaSetDevice(P->d.device), "cudaSetDevice");
+      cudaStream_t st = static_cast<cudaStream_t>(stream);
+      convert_rows(1, in, P->wide_in, rows * P->c.cells, st);
+      const amqft_status s = amqft_exec_rows(P->wide, P->wide_in, P->wide_out, rows, inverse, stream);
+      if (s != AMQFT_OK) return s;
+      convert_rows(0, P->wide_out, out, rows * P->c.cells, st);
+    } catch (...) {
+      return from_exception();
+    }
+    return AMQFT_OK;
+  }
   if (inverse && P->d.function != AMQFT_FN_CDFT) {
     if (rows == 0) return AMQFT_OK;
     if (!in || !out) return set_err(AMQFT_EINVAL, "null data pointer");
     try {
       ck(cudaSetDevice(P->d.device), "cudaSetDevice");
       return exec_real_inverse(P, in, out, rows, static_cast<cudaStream_t>(stream));
-    } catch (const CudaError& e) {
-      return set_err(AMQFT_ECUDA, e.what());
-    } catch (const std::runtime_error& e) {
-      return set_err(AMQFT_ECUDA, e.what());
+    } catch (...) {
+      return from_exception();
     }
   }
   if (rows == 0) return AMQFT_OK;
   if (!in || !out) return set_err(AMQFT_EINVAL, "null data pointer");
   // the fused, four-step and small-CDFT kernels move rows with TMA bulk
   // copies and 16-byte vectors: their device buffers must be 16-byte aligned
-  if (P->path >= 2 && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15u))
+  if (P->path >= 2 && P->path <= 4 && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15u))
     return set_err(AMQFT_EINVAL, "device buffers of fast-order plans must be 16-byte aligned");
   try {
     ck(cudaSetDevice(P->d.device), "cudaSetDevice");
@@ -435,10 +517,8 @@ amqft_status amqft_exec_rows(amqft_plan P, const void* in, void* out, size_t row
     } else {
       exec_generic<float>(P, in, out, rows, inverse, st);
     }
-  } catch (const std::invalid_argument& e) {
-    return set_err(AMQFT_EINVAL, e.what());
-  } catch (const CudaError& e) {
-    return set_err(AMQFT_ECUDA, e.what());
+  } catch (...) {
+    return from_exception();
   }
   return AMQFT_OK;
 }
@@ -457,6 +537,7 @@ amqft_status amqft_exec_host_rows(amqft_plan P, const void* h_in, void* h_out, s
   if (rows == 0) return AMQFT_OK;
   if (!h_in || !h_out) return set_err(AMQFT_EINVAL, "null data pointer");
   try {
+    std::lock_guard<std::mutex> lock(P->host_mu);
     ck(cudaSetDevice(P->d.device), "cudaSetDevice");
     const size_t row_bytes = P->c.cells * P->esize;
     if (!P->s_run) {
@@ -501,8 +582,8 @@ amqft_status amqft_exec_host_rows(amqft_plan P, const void* h_in, void* h_out, s
     }
     const int last = static_cast<int>((chunk - 1) % amqft_plan_s::NSLOT);
     ck(cudaStreamWaitEvent(caller, P->ev_d2h[last], 0), "wait");
-  } catch (const CudaError& e) {
-    return set_err(AMQFT_ECUDA, e.what());
+  } catch (...) {
+    return from_exception();
   }
   return AMQFT_OK;
 }
@@ -525,10 +606,8 @@ amqft_status amqft_dist_twiddle_scatter(const void* d_rows, void* const* d_dst, 
   try {
     dist_twiddle_scatter(d_rows, d_dst, rows, n1, n, row0, src_rank, nparts, trig_mode,
                          static_cast<cudaStream_t>(stream));
-  } catch (const std::invalid_argument& e) {
-    return set_err(AMQFT_EINVAL, e.what());
-  } catch (const std::runtime_error& e) {
-    return set_err(AMQFT_ECUDA, e.what());
+  } catch (...) {
+    return from_exception();
   }
   return AMQFT_OK;
 }
@@ -551,10 +630,8 @@ amqft_status amqft_exec_rows_transposed(amqft_plan P, const void* in, void* out,
   try {
     ck(cudaSetDevice(P->d.device), "cudaSetDevice");
     P->fast->exec_transposed(in, out, rows, static_cast<cudaStream_t>(stream));
-  } catch (const std::invalid_argument& e) {
-    return set_err(AMQFT_EINVAL, e.what());
-  } catch (const std::runtime_error& e) {
-    return set_err(AMQFT_ECUDA, e.what());
+  } catch (...) {
+    return from_exception();
   }
   return AMQFT_OK;
 }
@@ -569,10 +646,8 @@ amqft_status amqft_dist_twiddle_scatter_t(const void* d_rows, void* const* d_dst
   try {
     dist_twiddle_scatter_t(d_rows, d_dst, rows, n1, n, row0, src_rank, nparts, trig_mode, a,
                            static_cast<cudaStream_t>(stream));
-  } catch (const std::invalid_argument& e) {
-    return set_err(AMQFT_EINVAL, e.what());
-  } catch (const std::runtime_error& e) {
-    return set_err(AMQFT_ECUDA, e.what());
+  } catch (...) {
+    return from_exception();
   }
   return AMQFT_OK;
 }
@@ -582,10 +657,8 @@ amqft_status amqft_transpose_c64(const void* d_in, void* d_out, size_t mats, siz
   if (!d_in || !d_out) return set_err(AMQFT_EINVAL, "null pointer");
   try {
     transpose_c64(d_in, d_out, mats, r, c, static_cast<cudaStream_t>(stream));
-  } catch (const std::invalid_argument& e) {
-    return set_err(AMQFT_EINVAL, e.what());
-  } catch (const std::runtime_error& e) {
-    return set_err(AMQFT_ECUDA, e.what());
+  } catch (...) {
+    return from_exception();
   }
   return AMQFT_OK;
 }
@@ -603,6 +676,12 @@ amqft_status amqft_plan_path(amqft_plan P, int* path, int* launches) {
   if (path) *path = P->path;
   if (launches) *launches = P->launches;
   return AMQFT_OK;
+}
+
+amqft_status amqft_plan_fourstep_factors(amqft_plan P, size_t* f3) {
+  if (!P || !f3) return set_err(AMQFT_EINVAL, "null argument");
+  if (P->path != 3) return set_err(AMQFT_EINVAL, "not a four-step plan");
+  return fourstep_factors(P->d, f3);
 }
 
 amqft_status amqft_plan_dump(amqft_plan P, int prog, void* records, size_t cap,
@@ -653,8 +732,8 @@ amqft_status amqft_execute_host(int variant, int function, size_t n, const doubl
       ck(cudaMemcpy(out, dout, bytes, cudaMemcpyDeviceToHost), "cudaMemcpy D2H");
       if (meter3) amqft_plan_op_counts(P, meter3);
     }
-  } catch (const CudaError& e) {
-    s = set_err(AMQFT_ECUDA, e.what());
+  } catch (...) {
+    s = from_exception();
   }
   cudaFree(din);
   cudaFree(dout);

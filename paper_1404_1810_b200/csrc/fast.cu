@@ -7,12 +7,12 @@
 namespace amqft_b200 {
 namespace fastk {
 // instances: fast_v<V>.cu (CDFT rows), fast_rv<V>.cu (RDFT rows)
-template <int V, typename R, bool RD>
+template <int V, typename R, bool RD, typename IO = R>
 std::unique_ptr<FastPlan> make_sized(size_t n, const void* tab, uint32_t nmax, int dev);
 
-template <int V, typename R>
+template <int V, typename R, typename IO = R>
 std::unique_ptr<FastPlan> make_for_variant(int kind, size_t n, const void* tab, uint32_t nmax, int dev) {
-  return kind == 1 ? make_sized<V, R, true>(n, tab, nmax, dev) : make_sized<V, R, false>(n, tab, nmax, dev);
+  return kind == 1 ? make_sized<V, R, true, IO>(n, tab, nmax, dev) : make_sized<V, R, false, IO>(n, tab, nmax, dev);
 }
 }  // namespace fastk
 
@@ -33,6 +33,21 @@ std::unique_ptr<FastPlan> make_fast_typed(int v, int kind, size_t n, const void*
   return nullptr;
 }
 
+// fp32 rows, fp64 arithmetic (variants 5-8, N = 1024-4096): the fused
+// kernel's fp64 instance with fp32 loads/stores; it builds its own fp64
+// constant table (the plan's table is fp32).
+std::unique_ptr<FastPlan> make_fast_mixed(int v, int kind, size_t n, uint32_t nmax, int dev) {
+  using namespace fastk;
+  if (n < 1024 || n > 4096) return nullptr;
+  switch (v) {
+    case 5: return make_for_variant<5, double, float>(kind, n, nullptr, nmax, dev);
+    case 6: return make_for_variant<6, double, float>(kind, n, nullptr, nmax, dev);
+    case 7: return make_for_variant<7, double, float>(kind, n, nullptr, nmax, dev);
+    case 8: return make_for_variant<8, double, float>(kind, n, nullptr, nmax, dev);
+  }
+  return nullptr;
+}
+
 
 std::unique_ptr<FastPlan> make_fast_plan(const amqft_plan_desc& d, const void* d_trig,
                                          uint32_t nmax) {
@@ -41,6 +56,8 @@ std::unique_ptr<FastPlan> make_fast_plan(const amqft_plan_desc& d, const void* d
   // values are bitwise the reference's on-the-fly long double values
   // (variants_test.cpp:267-277); the mode matters only for four-step twiddles
   const int kind = d.function == AMQFT_FN_RDFT ? 1 : 0;
+  if (d.dtype == AMQFT_F32 && f32_needs_f64_compute(d.variant, d.n))
+    return make_fast_mixed(d.variant, kind, d.n, nmax, d.device);
   if (d.dtype == AMQFT_F32) return make_fast_typed<float>(d.variant, kind, d.n, d_trig, nmax, d.device);
   return make_fast_typed<double>(d.variant, kind, d.n, d_trig, nmax, d.device);
 }
@@ -83,6 +100,7 @@ std::unique_ptr<FastPlan> make_small_typed(int v, size_t n, const void* tab, uin
 std::unique_ptr<FastPlan> make_small_plan(const amqft_plan_desc& d, const void* d_trig, uint32_t nmax,
                                           OpCount* ops) {
   if (d.function > AMQFT_FN_DST) return nullptr;   // AM constants from the table in both trig modes
+  if (d.dtype == AMQFT_F32 && f32_needs_f64_compute(d.variant, d.n)) return nullptr;
   if (d.dtype == AMQFT_F32)
     return smallk::make_small_typed<float>(d.variant, d.n, d_trig, nmax, d.device, ops, d.function);
   return smallk::make_small_typed<double>(d.variant, d.n, d_trig, nmax, d.device, ops, d.function);
@@ -107,7 +125,8 @@ OpCount fast_op_counts(const amqft_plan_desc& d) {
   return c;
 }
 
-bool fast_sub_covered(int dtype, size_t n) {
+bool fast_sub_covered(int dtype, size_t n, int variant) {
+  if (dtype == AMQFT_F32 && f32_needs_f64_compute(variant, n)) return n >= 1024 && n <= 4096;
   if (dtype == AMQFT_F32) return n >= 2 && n <= 8192;
   return n >= 2 && n <= 4096 && n != 512;
 }

@@ -41,6 +41,16 @@ class FastPlan {
   int launches = 1;
 };
 
+// fp32 plans of the sine-family variants 5-8 from N = 512 on: the M5-M8
+// recurrences (elaborations.cpp:350-527, lens flip variants.cpp:220-231)
+// amplify fp32 rounding beyond 1e-5 log2 N (measured on the B200,
+// tools/err_sweep.py: 5e-4 at N = 512, 5e2 at N = 4096).  Such plans keep
+// fp32 rows in HBM and compute in fp64: the fused kernel's fp64 instance
+// with fp32 I/O (N = 1024-4096, the reference DAG, bitwise the reference
+// before the final rounding), a four-step over stable sub-transforms (fast
+// order, N = 512 and N >= 8192), or the generic exact path in fp64.
+inline bool f32_needs_f64_compute(int variant, size_t n) { return variant >= 5 && n >= 512; }
+
 // Returns nullptr when no fused kernel covers the request.
 std::unique_ptr<FastPlan> make_fast_plan(const amqft_plan_desc& d,
                                          const void* d_trig, uint32_t nmax);

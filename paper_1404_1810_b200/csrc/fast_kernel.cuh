@@ -39,6 +39,7 @@
 #define AMQFT_TABLD(t, i) ((t)[i])
 #include "fast_gen.cuh"
 #include "generic.cuh"
+#include "trig.hpp"
 
 #ifndef AMQFT_RPC
 #define AMQFT_RPC 2   // rows per CTA (fp32, N <= 4096): both rows' warps run each phase in lockstep
@@ -86,7 +87,13 @@ struct TabParam {
   R v[K];
 };
 
-template <int V, typename R, int LOGN, int LOGLB>
+// IO: the element type of the rows in HBM (and of the TMA staging buffer);
+// R: the arithmetic type.  IO = float with R = double is the fp32-I/O,
+// fp64-compute instance for the sine-family variants 5-8, whose recurrences
+// amplify rounding beyond the fp32 tolerance from N = 512 on (SURVEY §8(c)
+// item 2): the DAG and its fp64 rounding are the reference's, only the
+// final result is rounded to fp32.
+template <int V, typename R, int LOGN, int LOGLB, typename IO = R>
 struct Cfg {
   static constexpr int V_ = V;
   static constexpr int N = 1 << LOGN;
@@ -111,7 +118,7 @@ struct Cfg {
   static constexpr bool CHAIN = (V == 1 || V == 5 || V == 3 || V == 7);
   // T, F (4 chains each) + the TMA staging buffer for the next row + mbarrier
   static constexpr size_t STAGE_OFF = 8 * CS * sizeof(R);
-  static constexpr size_t SMEM = AMQFT_TMA_STAGE ? STAGE_OFF + 2 * N * sizeof(R) + 16 : STAGE_OFF;
+  static constexpr size_t SMEM = AMQFT_TMA_STAGE ? STAGE_OFF + 2 * N * sizeof(IO) + 16 : STAGE_OFF;
   // Rows per CTA: two fp32 rows (N <= 4096) share one 512-thread CTA, each
   // with its own T/F/staging slot; every phase runs on both rows' warps at
   // once, so the phase's straight-line code is fetched once per SM for two
@@ -655,7 +662,7 @@ __device__ unsigned long long g_warp_work[16][16];
 // MODE 0: CDFT forward; 1: CDFT inverse (swap trick); 2: RDFT forward, two
 // real rows per kernel row (row A -> chains 0/1, row B -> chains 2/3: the
 // same Dct/Dst chains as the Re/Im halves of a CDFT, variants.cpp:190-209).
-template <int V, typename R, int LOGN, int LOGLB, int MODE>
+template <int V, typename R, int LOGN, int LOGLB, int MODE, typename IO = R>
 #ifndef AMQFT_FAST_MINB
 #define AMQFT_FAST_MINB 2
 #endif
@@ -665,12 +672,12 @@ __global__ void __launch_bounds__(
 #ifdef AMQFT_LB_THREADS   // register-budget experiments (tools/ab_kernel.cu)
                                   AMQFT_LB_THREADS,
 #else
-                                  Cfg<V, R, LOGN, LOGLB>::NTB,
+                                  Cfg<V, R, LOGN, LOGLB, IO>::NTB,
 #endif
-                                  ((Cfg<V, R, LOGN, LOGLB>::RPC == 1 && sizeof(R) == 4 &&
-                                    2 * Cfg<V, R, LOGN, LOGLB>::SMEM_BLOCK <= 227 * 1024)
+                                  ((Cfg<V, R, LOGN, LOGLB, IO>::RPC == 1 && sizeof(R) == 4 &&
+                                    2 * Cfg<V, R, LOGN, LOGLB, IO>::SMEM_BLOCK <= 227 * 1024)
                                        ? AMQFT_FAST_MINB : 1))
-k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows_in,
+k_fast(const IO* __restrict__ in, IO* __restrict__ out, size_t rows_in,
        const __grid_constant__ TabParam<R, (1 << LOGN) / 4> tparam, const R* __restrict__ ltab, int nmax_unused,
        R scale) {
   (void)nmax_unused;
@@ -685,9 +692,16 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows_in,
 #ifdef AMQFT_PHASE_TIMING
   long long t_prev = 0, w_start = 0;
 #endif
-  using C = Cfg<V, R, LOGN, LOGLB>;
+  using C = Cfg<V, R, LOGN, LOGLB, IO>;
   using A = KArith<R, C::LOGN_>;
   using V2 = typename std::conditional<sizeof(R) == 4, float2, double2>::type;
+  using IO2 = typename std::conditional<sizeof(IO) == 4, float2, double2>::type;
+  // rows in HBM / staging (IO) <-> arithmetic (R)
+  auto cvt_in = [](IO2 v) -> V2 { return V2{static_cast<R>(v.x), static_cast<R>(v.y)}; };
+  auto cvt_out = [](V2 v) -> IO2 {
+    using E = decltype(IO2{}.x);
+    return IO2{static_cast<E>(v.x), static_cast<E>(v.y)};
+  };
   extern __shared__ __align__(128) unsigned char smraw[];
   // row slot: threads [slot*NT, (slot+1)*NT) own row slot of each pair
   const int tid = threadIdx.x % C::NT;
@@ -695,8 +709,8 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows_in,
   unsigned char* sm = smraw + slot * C::SLOT;
   R* Tb = reinterpret_cast<R*>(sm);
   R* Fb = Tb + 4 * C::CS;
-  R* Sb = reinterpret_cast<R*>(sm + C::STAGE_OFF);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::STAGE_OFF + 2 * C::N * sizeof(R));
+  IO* Sb = reinterpret_cast<IO*>(sm + C::STAGE_OFF);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::STAGE_OFF + 2 * C::N * sizeof(IO));
   constexpr size_t RSTEP = C::RPC;   // rows per CTA iteration
   // Barrier of one row slot.  AMQFT_SLOT_BARRIER=1 (default): a named
   // barrier per slot, the two rows drift apart (measured 1.58 -> 1.54 ms,
@@ -709,7 +723,7 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows_in,
   };
   const R base = tab[nmax / 4 - 1];
   constexpr int N = C::N, H = C::H;
-  constexpr uint32_t ROW_BYTES = 2 * N * sizeof(R);
+  constexpr uint32_t ROW_BYTES = 2 * N * sizeof(IO);
   // load/store: 256 threads, cells tid + 256 it; address steps per it
   constexpr int IO_T = 256, IO_IT = H / IO_T;
   static_assert(H % IO_T == 0 && C::NT >= IO_T, "IO tiling");
@@ -720,8 +734,8 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows_in,
   // Output through a bulk store: the row is assembled in the F buffer (free
   // once read; next written by the following row's bottom phase, after
   // thread 0 has waited for the bulk read) and leaves with one cp.async.bulk.
-  constexpr bool BULK_ST = AMQFT_TMA_STORE && sizeof(R) == 4 && IO_IT <= 8 &&
-                           4 * C::CS * sizeof(R) >= 2 * N * sizeof(R);
+  constexpr bool BULK_ST = AMQFT_TMA_STORE && sizeof(IO) == 4 && IO_IT <= 8 &&
+                           4 * C::CS * sizeof(R) >= 2 * N * sizeof(IO);
 #if AMQFT_TMA_STAGE
   if (tid == 0) {
     mbar_init(bar, 1);
@@ -753,9 +767,9 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows_in,
       mbar_wait(bar, parity);
       parity ^= 1;
     }
-    const V2* x = reinterpret_cast<const V2*>(Sb);
+    const IO2* x = reinterpret_cast<const IO2*>(Sb);
 #else
-    const V2* x = reinterpret_cast<const V2*>(in + row * 2 * N);
+    const IO2* x = reinterpret_cast<const IO2*>(in + row * 2 * N);
 #endif
     // Cells m = tid + 256 it (it < H/256) and m = H (thread 0): the
     // physical offsets are linear in it (256 is a multiple of both layout
@@ -770,19 +784,19 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows_in,
       // all staged reads first (the compiler cannot hoist them over the
       // T stores itself: both are shared memory), then the stores
       // RDFT: rows A and B (N reals each) take the places of re and im
-      const R* xa = reinterpret_cast<const R*>(x);
-      const R* xb = xa + N;
+      const IO* xa = reinterpret_cast<const IO*>(x);
+      const IO* xb = xa + N;
       V2 av[IO_IT], bv[IO_IT];
 #pragma unroll
       for (int it = 0; it < IO_IT; ++it) {
         const int m = tid + it * IO_T;
         const int mm = (N - m) & (N - 1);   // m = 0: in range, unused
         if constexpr (RDFT) {
-          av[it] = V2{xa[m], xb[m]};
-          bv[it] = V2{xa[mm], xb[mm]};
+          av[it] = cvt_in(IO2{xa[m], xb[m]});
+          bv[it] = cvt_in(IO2{xa[mm], xb[mm]});
         } else {
-          av[it] = x[m];
-          bv[it] = x[mm];
+          av[it] = cvt_in(x[m]);
+          bv[it] = cvt_in(x[mm]);
         }
       }
 #pragma unroll
@@ -803,7 +817,7 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows_in,
         t3[it * PT_STEP] = A::sub(a.y, b.y);
       }
       if (tid == 0) {                // m = H
-        V2 a = RDFT ? V2{xa[H], xb[H]} : x[H];
+        V2 a = cvt_in(RDFT ? IO2{xa[H], xb[H]} : x[H]);
         if (INV) a = V2{a.y, a.x};
         Tb[C::coT(0) + C::pt(H, 0)] = a.x;
         Tb[C::coT(2) + C::pt(H, 0)] = a.y;
@@ -920,7 +934,7 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows_in,
     PHASE_MARK(5);
 
     // ---- store: SplitReal bwd (elab.cpp:199-208) + SplitComplex bwd (162-183)
-    V2* y = reinterpret_cast<V2*>(out + row * 2 * N);
+    IO2* y = reinterpret_cast<IO2*>(out + row * 2 * N);
     if constexpr (BULK_ST) {
       // read all cells (registers), barrier, write the natural-order row
       // over F, barrier, one bulk store per row
@@ -956,31 +970,31 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows_in,
       row_sync();
       if (act && tid < IO_T) {
         if constexpr (RDFT) {        // rows A | B, N reals each
-          R* oa = Fb;
-          R* ob = Fb + N;
+          IO* oa = reinterpret_cast<IO*>(Fb);
+          IO* ob = oa + N;
 #pragma unroll
           for (int it = 0; it < IO_IT; ++it) {
             const int k = tid + it * IO_T;
-            oa[k] = lo[it].x;
-            ob[k] = lo[it].y;
+            oa[k] = static_cast<IO>(lo[it].x);
+            ob[k] = static_cast<IO>(lo[it].y);
             if (!(it == 0 && tid == 0)) {
-              oa[N - k] = hi[it].x;
-              ob[N - k] = hi[it].y;
+              oa[N - k] = static_cast<IO>(hi[it].x);
+              ob[N - k] = static_cast<IO>(hi[it].y);
             }
           }
           if (tid == 0) {
-            oa[H] = yH.x;
-            ob[H] = yH.y;
+            oa[H] = static_cast<IO>(yH.x);
+            ob[H] = static_cast<IO>(yH.y);
           }
         } else {
-          V2* ob = reinterpret_cast<V2*>(Fb);
+          IO2* ob = reinterpret_cast<IO2*>(Fb);
 #pragma unroll
           for (int it = 0; it < IO_IT; ++it) {
             const int k = tid + it * IO_T;
-            ob[k] = lo[it];
-            if (!(it == 0 && tid == 0)) ob[N - k] = hi[it];
+            ob[k] = cvt_out(lo[it]);
+            if (!(it == 0 && tid == 0)) ob[N - k] = cvt_out(hi[it]);
           }
-          if (tid == 0) ob[H] = yH;
+          if (tid == 0) ob[H] = cvt_out(yH);
         }
         fence_proxy_async();         // generic-proxy writes -> async proxy
       }
@@ -992,8 +1006,8 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows_in,
       if constexpr (RDFT) {
         if (act && tid < IO_T) {
           const bool two = 2 * row + 1 < rows_in;
-          R* ya = out + row * 2 * N;
-          R* yb = ya + N;
+          IO* ya = out + row * 2 * N;
+          IO* yb = ya + N;
           const int q0 = C::pf(tid, 0), q1 = C::pf(tid, 1);
           const R* f0 = Fb + C::coF(0) + q0;
           const R* f1 = Fb + C::coF(1) + q1;
@@ -1002,15 +1016,15 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows_in,
 #pragma unroll
           for (int it = 0; it < IO_IT; ++it) {
             const int k = tid + it * IO_T;
-            ya[k] = f0[it * PF_STEP];
-            if (two) yb[k] = f2[it * PF_STEP];
+            ya[k] = static_cast<IO>(f0[it * PF_STEP]);
+            if (two) yb[k] = static_cast<IO>(f2[it * PF_STEP]);
             if (it == 0 && tid == 0) continue;
-            ya[N - k] = f1[it * PF_STEP];
-            if (two) yb[N - k] = f3[it * PF_STEP];
+            ya[N - k] = static_cast<IO>(f1[it * PF_STEP]);
+            if (two) yb[N - k] = static_cast<IO>(f3[it * PF_STEP]);
           }
           if (tid == 0) {
-            ya[H] = Fb[C::coF(0) + C::pf(H, 0)];
-            if (two) yb[H] = Fb[C::coF(2) + C::pf(H, 0)];
+            ya[H] = static_cast<IO>(Fb[C::coF(0) + C::pf(H, 0)]);
+            if (two) yb[H] = static_cast<IO>(Fb[C::coF(2) + C::pf(H, 0)]);
           }
         }
       } else {
@@ -1025,7 +1039,7 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows_in,
             const int k = tid + it * IO_T;
             const R rd = f0[it * PF_STEP], id = f2[it * PF_STEP];
             if (it == 0 && tid == 0) {   // k = 0: Dct chains only
-              y[0] = INV ? V2{A::mul(id, scale), A::mul(rd, scale)} : V2{rd, id};
+              y[0] = cvt_out(INV ? V2{A::mul(id, scale), A::mul(rd, scale)} : V2{rd, id});
               continue;
             }
             const R rs = f1[it * PF_STEP], is = f3[it * PF_STEP];
@@ -1035,12 +1049,12 @@ k_fast(const R* __restrict__ in, R* __restrict__ out, size_t rows_in,
               lo = V2{A::mul(lo.y, scale), A::mul(lo.x, scale)};
               hi = V2{A::mul(hi.y, scale), A::mul(hi.x, scale)};
             }
-            y[k] = lo;
-            y[N - k] = hi;
+            y[k] = cvt_out(lo);
+            y[N - k] = cvt_out(hi);
           }
           if (tid == 0) {                // k = H
             const R rd = Fb[C::coF(0) + C::pf(H, 0)], id = Fb[C::coF(2) + C::pf(H, 0)];
-            y[H] = INV ? V2{A::mul(id, scale), A::mul(rd, scale)} : V2{rd, id};
+            y[H] = cvt_out(INV ? V2{A::mul(id, scale), A::mul(rd, scale)} : V2{rd, id});
           }
         }
       }
@@ -1083,13 +1097,24 @@ __global__ void k_compact_table(const R* __restrict__ tab, R* __restrict__ out, 
     out[s] = tab[(s + 1) * ratio - 1];
 }
 
-template <int V, typename R, int LOGN, int LOGLB, bool RDFT_ROWS>
+template <int V, typename R, int LOGN, int LOGLB, bool RDFT_ROWS, typename IO = R>
 class FastPlanImpl final : public FastPlan {
  public:
   FastPlanImpl(const void* tab, uint32_t nmax, int device) : tab_(static_cast<const R*>(tab)),
                                                               nmax_(nmax) {
-    using C = Cfg<V, R, LOGN, LOGLB>;
-    if (nmax_ != static_cast<uint32_t>(C::N)) {
+    using C = Cfg<V, R, LOGN, LOGLB, IO>;
+    if constexpr (!std::is_same<IO, R>::value) {
+      // fp32-I/O plans hand over their fp32 table: the fp64-compute instance
+      // builds the Nmax = N fp64 table itself (host long double, rounded
+      // once: bitwise TrigTable::constants, trig.cpp)
+      const std::vector<double> t64 = trig_table(V, static_cast<size_t>(C::N), false);
+      cudaError_t e0 = cudaMalloc(&own_tab_, sizeof(R) * (C::N / 4));
+      if (e0 == cudaSuccess)
+        e0 = cudaMemcpy(own_tab_, t64.data(), sizeof(R) * (C::N / 4), cudaMemcpyHostToDevice);
+      if (e0 != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e0));
+      tab_ = own_tab_;
+      nmax_ = C::N;
+    } else if (nmax_ != static_cast<uint32_t>(C::N)) {
       cudaError_t e0 = cudaMalloc(&own_tab_, sizeof(R) * (C::N / 4));
       if (e0 != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e0));
       k_compact_table<R><<<8, 256>>>(tab_, own_tab_, C::N, static_cast<int>(nmax_));
@@ -1097,8 +1122,8 @@ class FastPlanImpl final : public FastPlan {
       nmax_ = C::N;
     }
     // CDFT plans: forward (MODE 0) and inverse (1); RDFT plans: MODE 2
-    auto fn = k_fast<V, R, LOGN, LOGLB, RDFT_ROWS ? 2 : 0>;
-    auto fi = k_fast<V, R, LOGN, LOGLB, RDFT_ROWS ? 2 : 1>;
+    auto fn = k_fast<V, R, LOGN, LOGLB, RDFT_ROWS ? 2 : 0, IO>;
+    auto fi = k_fast<V, R, LOGN, LOGLB, RDFT_ROWS ? 2 : 1, IO>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(C::SMEM_BLOCK));
     if (e == cudaSuccess)
@@ -1124,20 +1149,20 @@ class FastPlanImpl final : public FastPlan {
     if (own_tab_) cudaFree(own_tab_);
   }
   void exec(const void* in, void* out, size_t rows, int inverse, cudaStream_t st) override {
-    using C = Cfg<V, R, LOGN, LOGLB>;
+    using C = Cfg<V, R, LOGN, LOGLB, IO>;
     const size_t krows = RDFT_ROWS ? (rows + 1) / 2 : rows;   // kernel rows
     const size_t units = (krows + C::RPC - 1) / C::RPC;
     const unsigned grid = static_cast<unsigned>(std::min<size_t>(units, static_cast<size_t>(grid_cap_)));
     if (RDFT_ROWS)
-      k_fast<V, R, LOGN, LOGLB, 2><<<grid, C::NTB, C::SMEM_BLOCK, st>>>(
-          static_cast<const R*>(in), static_cast<R*>(out), rows, tparam_, ltab_, static_cast<int>(nmax_), R(1));
+      k_fast<V, R, LOGN, LOGLB, 2, IO><<<grid, C::NTB, C::SMEM_BLOCK, st>>>(
+          static_cast<const IO*>(in), static_cast<IO*>(out), rows, tparam_, ltab_, static_cast<int>(nmax_), R(1));
     else if (inverse)
-      k_fast<V, R, LOGN, LOGLB, 1><<<grid, C::NTB, C::SMEM_BLOCK, st>>>(
-          static_cast<const R*>(in), static_cast<R*>(out), rows, tparam_, ltab_, static_cast<int>(nmax_),
+      k_fast<V, R, LOGN, LOGLB, 1, IO><<<grid, C::NTB, C::SMEM_BLOCK, st>>>(
+          static_cast<const IO*>(in), static_cast<IO*>(out), rows, tparam_, ltab_, static_cast<int>(nmax_),
           R(1) / R(C::N));
     else
-      k_fast<V, R, LOGN, LOGLB, 0><<<grid, C::NTB, C::SMEM_BLOCK, st>>>(
-          static_cast<const R*>(in), static_cast<R*>(out), rows, tparam_, ltab_, static_cast<int>(nmax_),
+      k_fast<V, R, LOGN, LOGLB, 0, IO><<<grid, C::NTB, C::SMEM_BLOCK, st>>>(
+          static_cast<const IO*>(in), static_cast<IO*>(out), rows, tparam_, ltab_, static_cast<int>(nmax_),
           R(1) / R(C::N));
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
@@ -1152,14 +1177,14 @@ class FastPlanImpl final : public FastPlan {
   int grid_cap_ = 148;
 };
 
-template <int V, typename R, bool RD>
+template <int V, typename R, bool RD, typename IO = R>
 std::unique_ptr<FastPlan> make_sized(size_t n, const void* tab, uint32_t nmax, int dev) {
   switch (n) {
-    case 1024: return std::make_unique<FastPlanImpl<V, R, 10, 6, RD>>(tab, nmax, dev);
-    case 2048: return std::make_unique<FastPlanImpl<V, R, 11, 6, RD>>(tab, nmax, dev);
-    case 4096: return std::make_unique<FastPlanImpl<V, R, 12, 6, RD>>(tab, nmax, dev);
+    case 1024: return std::make_unique<FastPlanImpl<V, R, 10, 6, RD, IO>>(tab, nmax, dev);
+    case 2048: return std::make_unique<FastPlanImpl<V, R, 11, 6, RD, IO>>(tab, nmax, dev);
+    case 4096: return std::make_unique<FastPlanImpl<V, R, 12, 6, RD, IO>>(tab, nmax, dev);
     case 8192:
-      if constexpr (sizeof(R) == 4) return std::make_unique<FastPlanImpl<V, R, 13, 6, RD>>(tab, nmax, dev);
+      if constexpr (sizeof(R) == 4) return std::make_unique<FastPlanImpl<V, R, 13, 6, RD, IO>>(tab, nmax, dev);
       break;
   }
   return nullptr;

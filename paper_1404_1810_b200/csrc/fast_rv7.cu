@@ -6,5 +6,7 @@ namespace amqft_b200 {
 namespace fastk {
 template std::unique_ptr<FastPlan> make_sized<7, float, true>(size_t, const void*, uint32_t, int);
 template std::unique_ptr<FastPlan> make_sized<7, double, true>(size_t, const void*, uint32_t, int);
+// fp32 rows, fp64 arithmetic (fast.cuh f32_needs_f64_compute)
+template std::unique_ptr<FastPlan> make_sized<7, double, true, float>(size_t, const void*, uint32_t, int);
 }  // namespace fastk
 }  // namespace amqft_b200

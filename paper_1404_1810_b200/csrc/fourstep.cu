@@ -338,9 +338,12 @@ int lg2(size_t v) {
 // minimising the two DFT passes' and the transposes' time by the measured HBM
 // throughput of each sub-size (B200, TB/s; tools/sweep_c3.py,
 // tools/prof_fast.py).
-double sub_tbs(int dtype, int lg) {
+double sub_tbs(int dtype, int lg, int variant) {
   static const double f32[14] = {0, 5.0, 5.0, 5.0, 5.0, 5.0, 5.0, 3.9, 1.78, 1.26, 1.72, 2.43, 3.17, 2.09};
   static const double f64[13] = {0, 5.5, 5.5, 5.5, 5.5, 5.5, 5.4, 2.94, 2.06, 0.0, 2.27, 2.68, 2.88};
+  // fp32 rows through the fp64 instance (variants 5-8, fast.cuh): half the fp64 row bytes
+  static const double mixed[13] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1.13, 1.34, 1.44};
+  if (dtype == AMQFT_F32 && lg < 13 && f32_needs_f64_compute(variant, size_t(1) << lg)) return mixed[lg];
   if (dtype == AMQFT_F32) return lg < 14 ? f32[lg] : 0.0;
   return lg < 13 ? f64[lg] : 0.0;
 }
@@ -350,14 +353,15 @@ double sub_tbs(int dtype, int lg) {
 // with the twiddle fused into its stores, so transposes 1 and 2 vanish.
 bool col_capable(int dtype, int lg) { return lg >= 1 && lg <= (dtype == AMQFT_F32 ? 6 : 5); }
 
-bool fourstep_split(int dtype, size_t n, size_t* n1, size_t* n2, bool* col = nullptr) {
+bool fourstep_split(int dtype, size_t n, int variant, size_t* n1, size_t* n2, bool* col = nullptr) {
   constexpr double kTransposeTBs = 6.9;   // measured k_transpose (B200)
   const int lg = lg2(n);
   double best = 0.0;
   for (int l1 = 1; l1 < lg; ++l1) {
     const int l2 = lg - l1;
-    if (!fast_sub_covered(dtype, size_t(1) << l1) || !fast_sub_covered(dtype, size_t(1) << l2)) continue;
-    const double a = sub_tbs(dtype, l1), b = sub_tbs(dtype, l2);
+    if (!fast_sub_covered(dtype, size_t(1) << l1, variant) || !fast_sub_covered(dtype, size_t(1) << l2, variant))
+      continue;
+    const double a = sub_tbs(dtype, l1, variant), b = sub_tbs(dtype, l2, variant);
     if (a <= 0.0 || b <= 0.0) continue;
     for (int c = 0; c < 2; ++c) {
       if (c == 1 && !col_capable(dtype, l1)) continue;
@@ -381,7 +385,7 @@ bool fourstep_split(int dtype, size_t n, size_t* n1, size_t* n2, bool* col = nul
 // passes, coalesced, twiddles fused into their stores), C a single-kernel
 // row size, and one 3D transpose: 4 passes.  Chosen when cheaper than the
 // best two-factor plan by the same throughput model.
-bool fourstep_split3(int dtype, size_t n, size_t* a, size_t* b, size_t* c, double* cost) {
+bool fourstep_split3(int dtype, size_t n, int variant, size_t* a, size_t* b, size_t* c, double* cost) {
   constexpr double kTransposeTBs = 6.9;
   const int lg = lg2(n);
   double best = 0.0;
@@ -392,8 +396,9 @@ bool fourstep_split3(int dtype, size_t n, size_t* a, size_t* b, size_t* c, doubl
     for (int lb = 1; lb <= 6; ++lb) {
       const int lc = lg - la - lb;
       if (lc < 5 || !col_capable(dtype, la) || !col_capable(dtype, lb)) continue;
-      if (!fast_sub_covered(dtype, size_t(1) << lc)) continue;
-      const double ta = sub_tbs(dtype, la), tb = sub_tbs(dtype, lb), tc = sub_tbs(dtype, lc);
+      if (!fast_sub_covered(dtype, size_t(1) << lc, variant)) continue;
+      const double ta = sub_tbs(dtype, la, variant), tb = sub_tbs(dtype, lb, variant),
+                   tc = sub_tbs(dtype, lc, variant);
       if (ta <= 0.0 || tb <= 0.0 || tc <= 0.0) continue;
       const double cst = 1.0 / ta + 1.0 / tb + 1.0 / tc + 1.0 / kTransposeTBs;
       if (best == 0.0 || cst < best - 1e-9) {
@@ -407,8 +412,33 @@ bool fourstep_split3(int dtype, size_t n, size_t* a, size_t* b, size_t* c, doubl
   return best > 0.0;
 }
 
-double fourstep_cost2(int dtype, size_t n1, size_t n2, bool col) {
-  return 1.0 / sub_tbs(dtype, lg2(n1)) + 1.0 / sub_tbs(dtype, lg2(n2)) + (col ? 1.0 : 3.0) / 6.9;
+double fourstep_cost2(int dtype, int variant, size_t n1, size_t n2, bool col) {
+  return 1.0 / sub_tbs(dtype, lg2(n1), variant) + 1.0 / sub_tbs(dtype, lg2(n2), variant) + (col ? 1.0 : 3.0) / 6.9;
+}
+
+// The factors a four-step plan runs: two-factor (n1 x n2, column mode or
+// three transposes) or three-factor (a x b x c), by the same cost model
+// the plan uses.
+struct FourStepShape {
+  bool ok = false, col = false, three = false;
+  size_t n1 = 0, n2 = 0, nb = 0;   // three-factor: n1 = A, nb = B, n2 = C
+};
+
+FourStepShape fourstep_shape(int dtype, int variant, size_t n) {
+  FourStepShape s;
+  const bool two = fourstep_split(dtype, n, variant, &s.n1, &s.n2, &s.col);
+  double c3 = 0.0;
+  size_t a3 = 0, b3 = 0, cc3 = 0;
+  s.three = fourstep_split3(dtype, n, variant, &a3, &b3, &cc3, &c3) &&
+            (!two || c3 < fourstep_cost2(dtype, variant, s.n1, s.n2, s.col) - 1e-9);
+  if (s.three) {
+    s.n1 = a3;
+    s.nb = b3;
+    s.n2 = cc3;
+    s.col = true;
+  }
+  s.ok = two || s.three;
+  return s;
 }
 
 template <typename R>
@@ -420,16 +450,14 @@ class FourStepPlan final : public FastPlan {
       : n_(n), batch_(batch), onthefly_(trig_mode == AMQFT_TRIG_ONTHEFLY) {
     logn_ = lg2(n);
     const int dtype = sizeof(R) == 8 ? AMQFT_F64 : AMQFT_F32;
-    const bool two = fourstep_split(dtype, n, &n1_, &n2_, &col_);
-    double c3 = 0.0;
-    size_t a3 = 0, b3 = 0, cc3 = 0;
-    three_ = fourstep_split3(dtype, n, &a3, &b3, &cc3, &c3) &&
-             (!two || c3 < fourstep_cost2(dtype, n1_, n2_, col_) - 1e-9);
-    if (!two && !three_) throw std::invalid_argument("four-step: no covered split");
+    const FourStepShape sh = fourstep_shape(dtype, variant, n);
+    if (!sh.ok) throw std::invalid_argument("four-step: no covered split");
+    n1_ = sh.n1;
+    n2_ = sh.n2;
+    nb_ = sh.nb;
+    col_ = sh.col;
+    three_ = sh.three;
     if (three_) {   // p1_: A columns, pb_: B columns, p2_: C rows
-      n1_ = a3;
-      nb_ = b3;
-      n2_ = cc3;
       pb_ = make_fast_sub(variant, nb_, dtype, tab, nmax, dev);
       if (!pb_) throw std::invalid_argument("four-step: no kernel for the middle factor");
     }
@@ -652,22 +680,41 @@ void transpose_c64(const void* in, void* out, size_t mats, size_t r, size_t c, c
 bool fourstep_covers(const amqft_plan_desc& d) {
   if (d.function != AMQFT_FN_CDFT || d.order != AMQFT_ORDER_FAST) return false;
   if ((d.n & (d.n - 1)) != 0 || d.n > (size_t(1) << 26)) return false;
-  if (fast_sub_covered(d.dtype, d.n)) return false;   // one fused / small kernel does it
-  size_t n1, n2;
-  return fourstep_split(d.dtype, d.n, &n1, &n2);
+  if (fast_sub_covered(d.dtype, d.n, d.variant)) return false;   // one fused / small kernel does it
+  return fourstep_shape(d.dtype, d.variant, d.n).ok;
 }
 
 OpCount fourstep_op_counts(const amqft_plan_desc& d) {
-  // N2 sub-transforms of length N1, N1 of length N2 (the reference DAG of
-  // each), plus one complex twiddle multiply per element (4 muls + 2 adds).
-  size_t n1 = 0, n2 = 0;
-  fourstep_split(d.dtype, d.n, &n1, &n2);
-  const OpCount c1 = fast_sub_op_counts(d.variant, n1, d.dtype), c2 = fast_sub_op_counts(d.variant, n2, d.dtype);
+  // Two-factor: N2 sub-transforms of length N1, N1 of length N2 (the
+  // reference DAG of each), plus one complex twiddle multiply per element
+  // (4 muls + 2 adds).  Three-factor A x B x C: B C of length A, A C of
+  // length B, A B of length C, and two twiddle passes.
+  const FourStepShape sh = fourstep_shape(d.dtype, d.variant, d.n);
   OpCount c;
+  if (sh.three) {
+    const size_t a = sh.n1, b = sh.nb, cc = sh.n2;
+    const OpCount ca = fast_sub_op_counts(d.variant, a, d.dtype), cb = fast_sub_op_counts(d.variant, b, d.dtype),
+                  ccc = fast_sub_op_counts(d.variant, cc, d.dtype);
+    c.adds = b * cc * ca.adds + a * cc * cb.adds + a * b * ccc.adds + 2 * 2 * d.n;
+    c.muls = b * cc * ca.muls + a * cc * cb.muls + a * b * ccc.muls + 2 * 4 * d.n;
+    c.bt = b * cc * ca.bt + a * cc * cb.bt + a * b * ccc.bt;
+    return c;
+  }
+  const size_t n1 = sh.n1, n2 = sh.n2;
+  const OpCount c1 = fast_sub_op_counts(d.variant, n1, d.dtype), c2 = fast_sub_op_counts(d.variant, n2, d.dtype);
   c.adds = n2 * c1.adds + n1 * c2.adds + 2 * d.n;
   c.muls = n2 * c1.muls + n1 * c2.muls + 4 * d.n;
   c.bt = n2 * c1.bt + n1 * c2.bt;
   return c;
+}
+
+amqft_status fourstep_factors(const amqft_plan_desc& d, size_t* f3) {
+  const FourStepShape sh = fourstep_shape(d.dtype, d.variant, d.n);
+  if (!sh.ok) return AMQFT_EINVAL;
+  f3[0] = sh.n1;
+  f3[1] = sh.three ? sh.nb : 1;
+  f3[2] = sh.n2;
+  return AMQFT_OK;
 }
 
 std::unique_ptr<FastPlan> make_fourstep_plan(const amqft_plan_desc& d, const void* d_trig, uint32_t nmax) {

@@ -14,12 +14,14 @@ namespace amqft_b200 {
 // its op counts, and whether a single kernel covers n: fast.cu.
 std::unique_ptr<FastPlan> make_fast_sub(int variant, size_t n, int dtype, const void* tab, uint32_t nmax, int dev);
 OpCount fast_sub_op_counts(int variant, size_t n, int dtype);
-bool fast_sub_covered(int dtype, size_t n);
+bool fast_sub_covered(int dtype, size_t n, int variant);
 
 // CDFT, fast order, N up to 2^26 beyond the single-kernel sizes.
 bool fourstep_covers(const amqft_plan_desc& d);
 std::unique_ptr<FastPlan> make_fourstep_plan(const amqft_plan_desc& d, const void* d_trig, uint32_t nmax);
 OpCount fourstep_op_counts(const amqft_plan_desc& d);
+// {A, B, C}: n = A B C (two-factor plans: B = 1)
+amqft_status fourstep_factors(const amqft_plan_desc& d, size_t* f3);
 
 // Distributed four-step building blocks (amqft_dist_twiddle_scatter,
 // amqft_transpose_c64).  d_dst: host array of nparts device pointers.

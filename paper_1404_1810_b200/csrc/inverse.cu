@@ -130,4 +130,22 @@ void inv_rdft_combine(int dtype_f64, const void* cc, const void* ss, void* out, 
   check_launch("k_rdft_combine");
 }
 
+// fp32 rows <-> fp64 working rows of a plan that computes in fp64
+// (fast.cuh f32_needs_f64_compute): widening is exact, narrowing rounds once.
+template <typename S, typename D>
+__global__ void __launch_bounds__(256) k_convert(const S* __restrict__ in, D* __restrict__ out, size_t total) {
+  for (size_t i = threadIdx.x + blockIdx.x * size_t(blockDim.x); i < total; i += size_t(gridDim.x) * blockDim.x)
+    out[i] = static_cast<D>(in[i]);
+}
+
+void convert_rows(int to_f64, const void* in, void* out, size_t total, cudaStream_t st) {
+  if (to_f64)
+    k_convert<float, double><<<grid_for(total), 256, 0, st>>>(static_cast<const float*>(in),
+                                                               static_cast<double*>(out), total);
+  else
+    k_convert<double, float><<<grid_for(total), 256, 0, st>>>(static_cast<const double*>(in),
+                                                               static_cast<float*>(out), total);
+  check_launch("k_convert");
+}
+
 }  // namespace amqft_b200

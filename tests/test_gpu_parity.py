@@ -2,9 +2,12 @@
 
 Bar: fp64 exact order is BITWISE the reference recursion (all 8 variants,
 every wired function); fp32 is within rel-L2 1e-5*log2(N) of the fp64
-reference result of the same variant for variants 1-4 (variants 5-8 are
-numerically unstable in the reference itself; their fp32 error is
-reported, and their fp64 exact path is bitwise).
+reference result of the same variant, all 8 variants.  The sine-family
+variants 5-8 amplify rounding, so their fp32 plans compute in
+fp64 from N = 512 on (fast.cuh f32_needs_f64_compute).  From N = 2^13 the
+reference's own fp64 v5-8 result drifts from the true DFT (1e-3 and up,
+SURVEY 0); there the fast order's four-step is checked against numpy's
+fp64 FFT and the exact order (the reference DAG in fp64) against the CPU.
 """
 import math
 import os
@@ -19,6 +22,16 @@ import paper_1404_1810_b200 as amqft  # noqa: E402
 
 GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 DEV = "cuda:0"
+
+
+def numpy_dft(x):
+    """numpy's fp64 FFT of one interleaved complex row (an independent
+    reference for sizes where the reference's v5-8 are themselves inexact)."""
+    x = np.asarray(x, dtype=np.float64)
+    f = np.fft.fft(x[0::2] + 1j * x[1::2])
+    out = np.empty(2 * f.size)
+    out[0::2], out[1::2] = f.real, f.imag
+    return out
 
 
 def run_plan(plan, rows, inverse=False):
@@ -106,10 +119,7 @@ def test_fp32_batched_tolerance(oracle, restatement, order):
         for row in (0, 7):
             want = r.execute(v, O.F_CDFT, n, xs[row].astype(np.float64))
             err = r.rel_l2(got[row], want)
-            if v <= 4:
-                assert err <= tol, (v, err)
-            else:
-                assert np.isfinite(err)  # reported; unstable family
+            assert err <= tol, (v, err)
 
 
 def test_onthefly_constants_close_to_table(oracle, restatement):
@@ -187,12 +197,15 @@ def test_fast_kernel_fp32_tolerance(oracle, restatement, n):
     tol = 1e-5 * math.log2(n)
     for v in range(1, 9):
         plan = amqft.Plan(v, amqft.FunctionId.Cdft, n, 4, dtype="f32", order=amqft.Order.Fast)
-        assert plan.path()[0] == 2
+        # v5-8 at N = 8192: a four-step over stable sub-transforms
+        assert plan.path()[0] == (3 if (v >= 5 and n == 8192) else 2), (v, n)
         got = run_plan(plan, xs)
         for k in (0, 3):
-            err = r.rel_l2(got[k], r.execute(v, O.F_CDFT, n, xs[k].astype(np.float64)))
-            if v <= 4:
-                assert err <= tol, (v, n, err)
+            if v >= 5 and n == 8192:
+                err = r.rel_l2(got[k], numpy_dft(xs[k]))
+            else:
+                err = r.rel_l2(got[k], r.execute(v, O.F_CDFT, n, xs[k].astype(np.float64)))
+            assert err <= tol, (v, n, err)
 
 
 @pytest.mark.parametrize("v", range(1, 9))
@@ -254,7 +267,8 @@ def _fourstep_plan(v, n, batch, trig=None):
 def test_fourstep_vs_oracle_2_20(oracle, restatement, v):
     """N = 2^20 = 1024 x 1024 four-step over the fused kernel, fp32, against
     the fp64 oracle of the same variant; tolerance 1e-5 log2 N (v1-4).
-    v5-8 are unstable in the reference itself: reported only."""
+    v5-8: the reference itself is unstable at this size; the
+    four-step over stable sub-transforms is checked against numpy's fp64 FFT."""
     r, O = restatement, oracle
     n = 1 << 20
     x = np.random.default_rng(2020 + v).standard_normal(2 * n).astype(np.float32)
@@ -266,6 +280,11 @@ def test_fourstep_vs_oracle_2_20(oracle, restatement, v):
         errs[trig] = r.rel_l2(got, want)
     if v <= 4:
         assert max(errs.values()) <= tol, (v, errs)
+    else:
+        ref = numpy_dft(x)
+        for trig in (amqft.TrigMode.Precomputed, amqft.TrigMode.OnTheFly):
+            got = run_plan(_fourstep_plan(v, n, 1, trig), [x])[0]
+            assert r.rel_l2(got, ref) <= tol, (v, trig)
 
 
 def test_fourstep_2_24_roundtrip_and_fft_crosscheck():
@@ -450,8 +469,7 @@ def test_fast_kernel_fp32_deterministic_across_launch_shapes(v):
     xi = torch.empty_like(x)
     plan.inverse(y1, xi)
     torch.cuda.synchronize()
-    if v <= 4:   # v5-8 are unstable in fp32 at this size: determinism only
-        assert float((xi - x).norm() / x.norm()) < 1e-5 * 12
+    assert float((xi - x).norm() / x.norm()) < 1e-5 * 12, v
     rp = amqft.Plan(v, amqft.FunctionId.Rdft, n, 2 * rows + 1, dtype="f32", order=amqft.Order.Fast)
     xr = torch.randn(2 * rows + 1, n, generator=g, device=DEV)
     r1, r2 = torch.empty_like(xr), torch.empty_like(xr)
@@ -516,6 +534,15 @@ def test_small_kernel_parity(oracle, restatement, dtype):
             xs = xs.astype(np.float32).astype(np.float64)
         for v in range(1, 9):
             plan = amqft.Plan(v, amqft.FunctionId.Cdft, n, rows, dtype=dtype, order=amqft.Order.Fast)
+            if dtype == "f32" and v >= 5 and n >= 512:
+                # unstable in fp32 from N = 512 (fast.cuh): a four-step over
+                # stable sub-transforms instead of the cooperative kernel
+                assert plan.path()[0] == 3, (v, n)
+                got = run_plan(plan, xs)
+                for row in (0, 299):
+                    want = r.execute(v, O.F_CDFT, n, xs[row])
+                    assert r.rel_l2(got[row], want) <= 1e-5 * math.log2(n), (v, n)
+                continue
             assert plan.path()[0] == 4, (v, n)
             got = run_plan(plan, xs)
             inv = run_plan(plan, xs, inverse=True)
@@ -529,10 +556,9 @@ def test_small_kernel_parity(oracle, restatement, dtype):
                 assert ex.path()[0] == 0
                 assert got.tobytes() == run_plan(ex, xs).tobytes(), (v, n)
                 assert inv.tobytes() == run_plan(ex, xs, inverse=True).tobytes(), (v, n)
-                if v <= 4:
-                    for row in (0, 299):
-                        want = r.execute(v, O.F_CDFT, n, xs[row])
-                        assert r.rel_l2(got[row], want) <= 1e-5 * max(1, math.log2(n)), (v, n)
+                for row in (0, 299):
+                    want = r.execute(v, O.F_CDFT, n, xs[row])
+                    assert r.rel_l2(got[row], want) <= 1e-5 * max(1, math.log2(n)), (v, n)
 
 
 def test_small_kernel_large_batch_round_trip():
@@ -851,3 +877,55 @@ def test_distributed_fourstep_transposed_scatter():
     for mode in ("a2a", "peer"):
         got = run(2, mode)
         assert torch.equal(got, base), mode
+
+
+# ---- fp32 plans of the sine-family variants (5-8): fp64 compute from N = 512
+@pytest.mark.parametrize("n", [512, 1024, 2048, 4096])
+def test_fp32_sine_variants_match_cpu(oracle, restatement, n):
+    """fp32 rows in and out, every function the plan covers at this size:
+    CDFT (fast: the fused kernel's fp64 instance with fp32 I/O at N =
+    1024-4096, a four-step at 512; exact: fp32 rows through the fp64 exact
+    plan), RDFT, DCT-0 and DST-0 -- all within 1e-5 log2 N of the CPU
+    reference of the same variant (which is itself accurate to <= 4e-6 here,
+    SURVEY 0).  Inverse round trips within the same tolerance."""
+    r, O = restatement, oracle
+    tol = 1e-5 * math.log2(n)
+    rows = 3
+    for f in (O.F_CDFT, O.F_RDFT, O.F_DCT, O.F_DST):
+        cells = amqft.cell_count(f, n)
+        xs = np.random.default_rng(n + f).standard_normal((rows, cells)).astype(np.float32).astype(np.float64)
+        for v in range(5, 9):
+            for order in (amqft.Order.Fast, amqft.Order.Exact):
+                plan = amqft.Plan(v, f, n, rows, dtype="f32", order=order)
+                if f == O.F_CDFT and order == amqft.Order.Fast:
+                    assert plan.path()[0] == (3 if n == 512 else 2), (v, n)
+                if order == amqft.Order.Exact:
+                    assert plan.path()[0] == 5, (v, f, n)
+                got = run_plan(plan, xs)
+                for row in range(rows):
+                    err = r.rel_l2(got[row], r.execute(v, f, n, xs[row]))
+                    assert err <= tol, (v, f, n, order, err)
+                back = run_plan(plan, got.astype(np.float32), inverse=True)
+                assert r.rel_l2(back.ravel(), xs.ravel()) <= tol, (v, f, n, order)
+
+
+@pytest.mark.parametrize("lg", [13, 14, 16])
+def test_fp32_sine_variants_large_n(oracle, restatement, lg):
+    """N >= 2^13: the reference's own fp64 v5-8 drift from the true DFT
+    (1e-3 at 2^13, O(1) at 2^14).  Fast order (four-step over
+    stable sub-transforms) against numpy's fp64 FFT; exact order (the
+    reference DAG in fp64, fp32 rows) against the CPU reference at 2^13."""
+    r, O = restatement, oracle
+    n = 1 << lg
+    tol = 1e-5 * lg
+    x = np.random.default_rng(lg).standard_normal(2 * n).astype(np.float32).astype(np.float64)
+    ref = numpy_dft(x)
+    for v in range(5, 9):
+        plan = amqft.Plan(v, amqft.FunctionId.Cdft, n, 1, dtype="f32", order=amqft.Order.Fast)
+        assert plan.path()[0] == 3
+        got = run_plan(plan, [x])[0]
+        assert r.rel_l2(got, ref) <= tol, (v, lg)
+        if lg == 13:
+            ex = amqft.Plan(v, amqft.FunctionId.Cdft, n, 1, dtype="f32", order=amqft.Order.Exact)
+            got = run_plan(ex, [x])[0]
+            assert r.rel_l2(got, r.execute(v, O.F_CDFT, n, x)) <= tol, v
