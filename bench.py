@@ -50,6 +50,9 @@ def parse():
     p.add_argument("--all-variants", action=argparse.BooleanOptionalAction, default=True,
                    help="after the timed region, also time variants 1..8 and report their fp32 error "
                         "(extra 'variants' and accuracy keys; --no-all-variants to skip)")
+    p.add_argument("--strong", action="store_true",
+                   help="config 2 strong scaling: the fixed batch is sharded by global row over the ranks "
+                        "(default: weak scaling, every rank runs its own full batch)")
     p.add_argument("--config", type=int, choices=[2, 4, 5], default=2,
                    help="BASELINE config: 2 batched N=4096 (default), 4 single N=2^24 four-step, "
                         "5 single N=2^30 distributed four-step over the ranks")
@@ -158,25 +161,54 @@ def cpu_baseline(args, seconds_target=10.0):
 
 
 def bench_reference(args, rank):
-    """--impl reference: the reference's own CPU implementation, rank 0 only."""
+    """--impl reference: the reference's own CPU implementation, rank 0 only.
+    One step = the reference library (oracle/_ref) over a fixed sample of
+    rows of the config-2 workload on every host thread; the sample is sized
+    once in the warm-up (~2 s per step), then every timed step runs exactly
+    that many rows and its wall time is measured."""
     if rank != 0:
         return None
-    cb = None
-    times = []
-    for _ in range(args.warmup):
-        cpu_baseline(args, seconds_target=1.0)
-    for _ in range(args.steps):
-        cb = cpu_baseline(args, seconds_target=3.0)
-        times.append(cb["value"])
-    value = statistics.median(times)
-    cb["value"] = value
+    import numpy as np
+    from oracle import oracle as O
+    ref = O.reference()
+    kind = "reference"
+    if ref is None:  # reference never compiled: the C restatement stands in
+        ref, kind = O.restatement(), "port"
+    threads = os.cpu_count() or 1
+    n = args.n
+    x = np.random.default_rng(1234).standard_normal((max(threads, 8), 2 * n)).astype(np.float32).astype(np.float64)
+
+    def step(rows):
+        xs = np.resize(x, (rows, 2 * n))
+        t0 = time.perf_counter()
+        if kind == "reference":
+            ref.execute_rows(args.variant, O.CDFT, n, xs, threads)
+        else:
+            for r in range(rows):
+                ref.execute(args.variant, O.F_CDFT, n, xs[r])
+        return time.perf_counter() - t0
+
+    probe = max(threads, 8)
+    rate = probe / step(probe)
+    rows = int(min(max(probe, rate * 2.0), args.batch))
+    for _ in range(max(0, args.warmup - 1)):
+        step(rows)
+    times = [step(rows) for _ in range(args.steps)]
+    step_s = statistics.mean(times)
+    value = rows / step_s
+    used = threads if kind == "reference" else 1
+    cb = {"value": value, "unit": UNIT, "cores": used, "kind": kind,
+          "sample": f"{rows} rows of CDFT N={n} (variant {args.variant}) per step, fp32 data widened to fp64, "
+                    f"{used} threads; {args.steps} steps, mean {step_s:.2f} s",
+          "gbs_fp32_bytes": value * 16 * n / 1e9, "gbs_fp64_bytes": value * 32 * n / 1e9}
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000.0 * args.batch / value, "higher_is_better": True,
+        "ms_per_step": 1000.0 * step_s, "rows_per_step": rows, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic N(0,1) (seeded), fp32 values widened to fp64",
-        "config": {"workload": f"config 2: batched CDFT N={args.n} x {args.batch}, variant {args.variant}",
+        "config": {"workload": f"config 2: batched CDFT N={args.n} x {args.batch}, variant {args.variant} "
+                               f"(each step a {rows}-row sample)",
                    "n": args.n, "batch": args.batch, "variant": args.variant,
                    "parallelism": "host threads"},
         "cpu_baseline": cb,
@@ -206,6 +238,26 @@ def ncu_traffic(args, n):
         wr = float(d["dram__bytes_write.sum"]) * scale.get(d.get("dram__bytes_write.sum [unit]", "Gbyte"), 1e9)
         return rd + wr, os.path.relpath(f, ROOT)
     return None, None
+
+
+CHUNK = 512   # rows per generator chunk
+
+
+def gen_rows(row0, rows, n, dtype, dev, seed=20260):
+    """Rows [row0, row0 + rows) of the synthetic config-2 batch, iid N(0,1):
+    counter-based by 512-row chunk (a Philox torch.Generator seeded with
+    seed + chunk index), so a row's values depend only on its global index,
+    never on how the batch is sharded over ranks."""
+    import torch
+    out = torch.empty(rows, 2 * n, dtype=dtype, device=dev)
+    g = torch.Generator(device=dev)
+    c0, c1 = row0 // CHUNK, (row0 + rows + CHUNK - 1) // CHUNK
+    for c in range(c0, c1):
+        g.manual_seed(seed + c)
+        blk = torch.randn(CHUNK, 2 * n, generator=g, device=dev, dtype=dtype)
+        lo, hi = max(row0, c * CHUNK), min(row0 + rows, (c + 1) * CHUNK)
+        out[lo - row0:hi - row0] = blk[lo - c * CHUNK:hi - c * CHUNK]
+    return out
 
 
 def _timed(fn, steps, warmup, stream, world, dev):
@@ -350,8 +402,11 @@ def bench_single(args, world, rank, local):
         y = torch.empty_like(x)
         ms = _timed(lambda: plan.forward(x, y, stream=stream), args.steps, args.warmup, stream, world, dev)
         path, launches = plan.path()
-        workload = (f"config 4: one complex forward DFT N=2^24 fp32, four-step 4096 x 4096 over the fused kernel, "
-                    f"on-the-fly twiddles, variant {args.variant}")
+        fa, fb, fc = plan.fourstep_factors()
+        shape = f"three-factor {fa} x {fb} x {fc}" if fb > 1 else f"two-factor {fa} x {fc}"
+        workload = (f"config 4: one complex forward DFT N=2^24 fp32, four-step {shape} "
+                    f"(column passes + fused-kernel rows + one transpose), on-the-fly twiddles, "
+                    f"variant {args.variant}")
         per_gpu_bytes = 16 * n
         value = world / (ms / 1000.0)
         hx = torch.empty(1, 2 * n, pin_memory=True)
@@ -361,7 +416,9 @@ def bench_single(args, world, rank, local):
         e2e_ms = _timed(lambda: plan.forward_host(hx, hy, stream=stream), 3, 1, stream, world, dev)
         e2e = {"value": world / (e2e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": 8 * n,
                "d2h_bytes_per_step": 8 * n}
-        extra = {"hbm_passes": 5, "traffic_model_bytes": 5 * 16 * n}
+        # every launch reads and writes the whole signal once
+        extra = {"hbm_passes": launches, "traffic_model_bytes": launches * 16 * n,
+                 "factors": [fa, fb, fc]}
         if rank == 0:
             extra["accuracy"] = config4_accuracy(amqft, x, n, local, stream, args)
         cpu = cpu_baseline_large(args.variant, n, 1 << 20) if (rank == 0 and not args.no_cpu_baseline) else None
@@ -443,16 +500,24 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    n, batch = args.n, args.batch
+    n = args.n
+    # weak (default): every rank runs a full batch of its own rows; strong
+    # (--strong): the fixed batch sharded by global row
+    if args.strong:
+        if args.batch % world:
+            raise SystemExit("--strong: the batch must divide over the ranks")
+        batch = args.batch // world
+        row0 = rank * batch
+    else:
+        batch = args.batch
+        row0 = rank * batch
     dtype = torch.float32 if args.dtype == "f32" else torch.float64
     esize = 4 if args.dtype == "f32" else 8
     order = amqft.Order.Fast if args.order == "fast" else amqft.Order.Exact
     plan = amqft.Plan(args.variant, amqft.FunctionId.Cdft, n, batch, dtype=args.dtype,
                       order=order, device=local)
     path, launches = plan.path()
-    g = torch.Generator(device=dev)
-    g.manual_seed(20260 + rank)
-    x = torch.randn(batch, 2 * n, generator=g, device=dev, dtype=dtype)
+    x = gen_rows(row0, batch, n, dtype, dev)
     y = torch.empty_like(x)
     stream = torch.cuda.current_stream(dev)
 
@@ -574,13 +639,16 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": args.dtype, "data": "synthetic: iid N(0,1) from a seed (torch.Generator)",
-            "config": {"workload": f"config 2: batched complex forward DFT N={n}, batch {batch} per GPU, "
-                                   f"interleaved re/im, AM-QFT variant {args.variant}",
-                       "n": n, "batch_per_gpu": batch, "variant": args.variant,
+            "higher_is_better": True, "scaling": "strong" if args.strong else "weak", "vs_baseline": None,
+            "dtype": args.dtype,
+            "data": "synthetic: iid N(0,1), counter-based per 512-row chunk of the global batch (Philox)",
+            "config": {"workload": f"config 2: batched complex forward DFT N={n}, "
+                                   + (f"batch {args.batch} sharded over {world} GPU(s) by global row"
+                                      if args.strong else f"batch {batch} per GPU")
+                                   + f", interleaved re/im, AM-QFT variant {args.variant}",
+                       "n": n, "batch_per_gpu": batch, "global_batch": batch * world, "variant": args.variant,
                        "order": args.order, "path": path, "launches_per_step": launches,
-                       "l2": "inputs 2 GiB per GPU > 126 MB L2; no flush",
+                       "l2": f"inputs {batch * 2 * n * esize / 2**30:.2f} GiB per GPU > 126 MB L2; no flush",
                        "parallelism": f"batch-sharded x{world}, no communication"},
             "gbs": alg_bytes * world / (ms_per_step / 1000.0) / 1e9,
             "per_gpu": {"transforms_per_s": value / world, "gbs": alg_bytes / (ms_per_step / 1000.0) / 1e9,

@@ -116,6 +116,12 @@ struct Cfg {
   static constexpr bool TM = (V == 1 || V == 4 || V == 5 || V == 8);
   static constexpr int SINE = V >= 5 ? 1 : 0;
   static constexpr bool CHAIN = (V == 1 || V == 5 || V == 3 || V == 7);
+  // Serial recurrences in the reference's order (one thread per class):
+  // only the fp64 instance that must stay bitwise the reference.  fp32 and
+  // the fp32-I/O fp64 instance evaluate them as segmented warp scans
+  // (re-associated; for the fp64-compute instance the difference to the
+  // serial order is fp64 rounding, far below the fp32 output rounding).
+  static constexpr bool SERIAL = CHAIN && sizeof(R) == 8 && std::is_same<IO, R>::value;
   // T, F (4 chains each) + the TMA staging buffer for the next row + mbarrier
   static constexpr size_t STAGE_OFF = 8 * CS * sizeof(R);
   static constexpr size_t SMEM = AMQFT_TMA_STAGE ? STAGE_OFF + 2 * N * sizeof(IO) + 16 : STAGE_OFF;
@@ -844,7 +850,7 @@ k_fast(const IO* __restrict__ in, IO* __restrict__ out, size_t rows_in,
       recombine<C, R, true>(Tb, tid, act, row_sync);
       row_sync();
       // serial recurrences: fp64 in the reference order (bitwise), fp32 as warp scans
-      if constexpr (C::CHAIN && sizeof(R) == 8) am_levels_asc<C, R, C::LT>(Tb, tid);   // RPC = 1
+      if constexpr (C::SERIAL) am_levels_asc<C, R, C::LT>(Tb, tid);   // RPC = 1
       else if (act) am_phase_regs<C, R, false>(Tb, tid);
       // small-chain folds (cells [0, N/LB] of T, untouched by the AM
       // levels): lane 31 of chain c's second warp is idle in the AM phase
@@ -912,7 +918,7 @@ k_fast(const IO* __restrict__ in, IO* __restrict__ out, size_t rows_in,
     PHASE_MARK(3);
 
     if constexpr (C::TM) {
-      if constexpr (C::CHAIN && sizeof(R) == 8) am_levels_desc<C, R, C::LT>(Fb, tid);  // RPC = 1
+      if constexpr (C::SERIAL) am_levels_desc<C, R, C::LT>(Fb, tid);  // RPC = 1
       else if (act) am_phase_regs<C, R, true>(Fb, tid);
       // small-chain recombination Dct/Dst(4..N/LB) on F cells [0, N/LB]
       // (disjoint from the AM levels): lane 31 of chain c's second warp
