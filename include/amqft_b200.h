@@ -109,6 +109,15 @@ typedef struct {
 amqft_status amqft_plan_create(amqft_plan* out, const amqft_plan_desc* desc);
 amqft_status amqft_plan_destroy(amqft_plan plan);
 
+/* Plan creation with caller-supplied constants (the TrigSource plugin,
+ * elaborations.hpp:90-98): `constants` in the TrigTable::constants layout
+ * (variants.cpp:289-299) for Nmax = desc->table_max_n (0: max(n, 8)): the
+ * slots f(2 pi p / Nmax), p = 1 .. Nmax/4 - 1, then the base constant;
+ * count must be Nmax / 4.  desc->corrupt_constants is ignored (the values
+ * are taken as given). */
+amqft_status amqft_plan_create_with_constants(amqft_plan* out, const amqft_plan_desc* desc,
+                                              const double* constants, size_t count);
+
 /* Cells per row of the plan's operand (cell_count, signal.cpp:254-258). */
 size_t amqft_plan_cells(amqft_plan plan);
 
@@ -144,6 +153,17 @@ amqft_status amqft_execute_host(int variant, int function, size_t n,
                                 const double* in, double* out, int trig_mode,
                                 size_t table_max_n, int corrupt_constants,
                                 uint64_t* meter3);
+
+/* amqft::execute(v, f, input, trig, meter) for an arbitrary TrigSource:
+ * as amqft_execute_host with the constants given in the TrigTable layout at
+ * Nmax = 4 * count (amqft_plan_create_with_constants).  The C++ execute
+ * (include/amqft_b200.hpp) collects them from the caller's TrigSource. */
+amqft_status amqft_execute_host_constants(int variant, int function, size_t n, const double* in,
+                                          double* out, const double* constants, size_t count,
+                                          uint64_t* meter3);
+
+/* Inverse CDFT of one host spectrum (swap trick, exact fp64 order). */
+amqft_status amqft_execute_host_inverse(int variant, size_t n, const double* in, double* out);
 
 /* ---- Distributed four-step (BASELINE config 5), fp32
  * complex.  One transform of length n = n1 * n2 over nparts ranks: rank p

@@ -9,6 +9,7 @@
 // copied here.
 #include <atomic>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -186,6 +187,96 @@ int ref_measure_accuracy(int v, int kind, std::size_t n, int trials,
         seed);
     mean_max[0] = c.mean_rel_err;
     mean_max[1] = c.max_rel_err;
+    return 0;
+  } catch (const std::exception& e) {
+    return guard(e);
+  }
+}
+
+// ordering_check (accuracy.cpp:80-133): out = mean_err[8], max_err[8],
+// reference_self_err; flags = {trustworthy, families_ordered,
+// families_margin, v2_best_of_cosine}.
+int ref_ordering_check(int kind, std::size_t n, int trials, std::uint64_t seed, double* out, int* flags) {
+  try {
+    const OrderingReport r = ordering_check(static_cast<TransformKind>(kind), n, trials, seed);
+    for (int i = 0; i < 8; ++i) {
+      out[i] = r.mean_err[i];
+      out[8 + i] = r.max_err[i];
+    }
+    out[16] = r.reference_self_err;
+    flags[0] = r.reference_trustworthy;
+    flags[1] = r.families_ordered;
+    flags[2] = r.families_margin;
+    flags[3] = r.v2_best_of_cosine;
+    return 0;
+  } catch (const std::exception& e) {
+    return guard(e);
+  }
+}
+
+// Layout metadata (signal.hpp): stored_range -> {first, step, count};
+// info -> {kind, time parity, harmonic parity, min periodization}.
+int ref_stored_range(int type, std::size_t n, int frequency, std::size_t* out3) {
+  try {
+    const IndexRange r =
+        stored_range(static_cast<SignalType>(type), n, frequency ? Domain::Frequency : Domain::Temporal);
+    out3[0] = r.first;
+    out3[1] = r.step;
+    out3[2] = r.count;
+    return 0;
+  } catch (const std::exception& e) {
+    return guard(e);
+  }
+}
+
+int ref_type_info(int type, int* out4, char* name, std::size_t cap) {
+  try {
+    const SignalType t = static_cast<SignalType>(type);
+    out4[0] = static_cast<int>(kind_of(t));
+    out4[1] = static_cast<int>(time_parity(t));
+    out4[2] = static_cast<int>(harmonic_parity(t));
+    out4[3] = static_cast<int>(min_periodization(t));
+    std::snprintf(name, cap, "%s", type_name(t));
+    return 0;
+  } catch (const std::exception& e) {
+    return guard(e);
+  }
+}
+
+// build_plan(v) flattened: per wired function {id, operand, base, #fwd,
+// fwd..., #calls, (target, divisor)...}; returns the length written.
+int ref_plan_encode(int v, long long* out, int cap) {
+  try {
+    const VariantPlan p = build_plan(variant_from_number(v));
+    std::vector<long long> e;
+    for (const FunctionPlan& f : p.functions) {
+      e.push_back(static_cast<long long>(f.id));
+      e.push_back(static_cast<long long>(f.operand));
+      e.push_back(static_cast<long long>(f.base_size));
+      e.push_back(static_cast<long long>(f.forward.size()));
+      for (ElaborationId id : f.forward) e.push_back(static_cast<long long>(id));
+      e.push_back(static_cast<long long>(f.calls.size()));
+      for (const RecursionCall& c : f.calls) {
+        e.push_back(static_cast<long long>(c.target));
+        e.push_back(static_cast<long long>(c.size_divisor));
+      }
+      if (!p.has_function(f.id)) return -1;
+    }
+    if (static_cast<int>(e.size()) > cap) return -1;
+    std::memcpy(out, e.data(), e.size() * sizeof(long long));
+    return static_cast<int>(e.size());
+  } catch (const std::exception& e) {
+    return guard(e);
+  }
+}
+
+// TrigTable::value(kind, index, m) of a (v, max_n, mode[, corrupted]) table.
+int ref_trig_value(int v, std::size_t max_n, int on_the_fly, int corrupt, int kind, std::size_t index,
+                   std::size_t m, double* out) {
+  try {
+    TrigTable t(variant_from_number(v), max_n, on_the_fly ? TrigMode::OnTheFly : TrigMode::Precomputed);
+    if (corrupt) t.corrupt_for_testing();
+    *out = t.value(static_cast<TrigKind>(kind), index, m);
     return 0;
   } catch (const std::exception& e) {
     return guard(e);

@@ -100,6 +100,7 @@ struct amqft_plan_s {
   uint32_t nmax = 8;
   // device arrays
   void* d_trig = nullptr;
+  void* d_trig64 = nullptr;   // fp32 plans computing in fp64: the fp64 copy of the table
   EI* d_eis = nullptr;
   uint32_t* d_prefix = nullptr;
   Stage* d_stages = nullptr;
@@ -141,7 +142,7 @@ struct amqft_plan_s {
     int cur = 0;
     cudaGetDevice(&cur);
     cudaSetDevice(d.device);
-    for (void* p : {static_cast<void*>(d_trig), static_cast<void*>(d_eis),
+    for (void* p : {static_cast<void*>(d_trig), d_trig64, static_cast<void*>(d_eis),
                     static_cast<void*>(d_prefix), static_cast<void*>(d_stages),
                     static_cast<void*>(d_progs), static_cast<void*>(d_jobs),
                     static_cast<void*>(d_geis), static_cast<void*>(d_gprefix),
@@ -296,7 +297,9 @@ bool inverse_defined(const amqft_plan_s* P) {
 // (inverse.cu) are made with the plan, so exec allocates nothing.
 thread_local bool g_inverse_subplan = false;   // creating an inverse's own sub-plans
 
-void prepare_inverse(amqft_plan_s* P) {
+amqft_status create_plan(amqft_plan* out, const amqft_plan_desc* desc, const std::vector<double>* host_tab);
+
+void prepare_inverse(amqft_plan_s* P, const std::vector<double>* host_tab) {
   if (g_inverse_subplan) return;   // the sub-plans only run forward
   if (!inverse_defined(P) || P->d.function == AMQFT_FN_CDFT || P->d.function == AMQFT_FN_DST) return;
   const size_t h = P->d.n / 2;
@@ -309,7 +312,7 @@ void prepare_inverse(amqft_plan_s* P) {
     d.function = fn;
     amqft_plan q = nullptr;
     g_inverse_subplan = true;
-    const amqft_status s = amqft_plan_create(&q, &d);
+    const amqft_status s = create_plan(&q, &d, host_tab);
     g_inverse_subplan = false;
     if (s == AMQFT_ENOMEM) throw CudaError(std::string("inverse sub-plan: ") + g_err);
     if (s != AMQFT_OK) throw std::runtime_error(std::string("inverse sub-plan: ") + g_err);
@@ -341,7 +344,15 @@ extern "C" {
 const char* amqft_last_error(void) { return g_err.c_str(); }
 const char* amqft_version(void) { return "amqft_b200 0.1 (sm_100a)"; }
 
-amqft_status amqft_plan_create(amqft_plan* out, const amqft_plan_desc* desc) {
+}  // extern "C"
+
+namespace {
+
+// Plan creation.  host_tab (nullable): the caller's constants in the
+// TrigTable::constants layout for Nmax = table_max_n (or max(n, 8)) --
+// amqft_plan_create_with_constants, the C++ execute over an arbitrary
+// TrigSource; otherwise the TrigTable values are built here.
+amqft_status create_plan(amqft_plan* out, const amqft_plan_desc* desc, const std::vector<double>* host_tab) {
   if (!out) return set_err(AMQFT_EINVAL, "null plan pointer");
   *out = nullptr;
   const amqft_status vs = validate_desc(desc);
@@ -363,17 +374,20 @@ amqft_status amqft_plan_create(amqft_plan* out, const amqft_plan_desc* desc) {
       return set_err(AMQFT_EINVAL, "constant table needs a power-of-two max periodization >= max(n, 8)");
     P->nmax = static_cast<uint32_t>(tmax);
     // Constant table (TrigTable::constants layout), host long double.
+    if (host_tab && host_tab->size() != tmax / 4)
+      return set_err(AMQFT_EINVAL, "constant table must hold table_max_n / 4 values (slots, then the base constant)");
     const std::vector<double> tab =
-        trig_table(desc->variant, tmax, desc->corrupt_constants != 0);
+        host_tab ? *host_tab : trig_table(desc->variant, tmax, desc->corrupt_constants != 0);
     if (desc->dtype == AMQFT_F64) {
       P->d_trig = upload(tab);
     } else {
       std::vector<float> tf(tab.begin(), tab.end());
       P->d_trig = upload(tf);
+      if (f32_needs_f64_compute(desc->variant, n)) P->d_trig64 = upload(tab);
     }
     // Fast fused path where one exists for this request.
     if (desc->order == AMQFT_ORDER_FAST) {
-      P->fast = make_fast_plan(*desc, P->d_trig, P->nmax);
+      P->fast = make_fast_plan(*desc, P->d_trig, P->nmax, P->d_trig64);
       int fpath = 2;
       OpCount small_ops{};
       if (!P->fast) {
@@ -381,7 +395,7 @@ amqft_status amqft_plan_create(amqft_plan* out, const amqft_plan_desc* desc) {
         if (P->fast) fpath = 4;
       }
       if (!P->fast && fourstep_covers(*desc)) {
-        P->fast = make_fourstep_plan(*desc, P->d_trig, P->nmax);
+        P->fast = make_fourstep_plan(*desc, P->d_trig, P->nmax, P->d_trig64);
         fpath = 3;
       }
       if (P->fast) {
@@ -392,7 +406,7 @@ amqft_status amqft_plan_create(amqft_plan* out, const amqft_plan_desc* desc) {
         P->c.cells = fn_cells(desc->function, n);
         P->c.ops = fpath == 2 ? fast_op_counts(*desc) : fpath == 4 ? small_ops : fourstep_op_counts(*desc);
         P->launches = P->fast->launches;
-        prepare_inverse(P.get());
+        prepare_inverse(P.get(), host_tab);
         *out = P.release();
         return AMQFT_OK;
       }
@@ -404,7 +418,7 @@ amqft_status amqft_plan_create(amqft_plan* out, const amqft_plan_desc* desc) {
       amqft_plan_desc d64 = *desc;
       d64.dtype = AMQFT_F64;
       amqft_plan w = nullptr;
-      const amqft_status s = amqft_plan_create(&w, &d64);
+      const amqft_status s = create_plan(&w, &d64, host_tab);
       if (s != AMQFT_OK) return s;
       P->wide = w;
       P->c.variant = desc->variant;
@@ -424,12 +438,31 @@ amqft_status amqft_plan_create(amqft_plan* out, const amqft_plan_desc* desc) {
     P->c = compile(desc->variant, desc->function, n, P->capacity);
     P->path = P->c.single ? 0 : 1;
     build_generic(P.get());
-    prepare_inverse(P.get());
+    prepare_inverse(P.get(), host_tab);
   } catch (...) {
     return from_exception();
   }
   *out = P.release();
   return AMQFT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+amqft_status amqft_plan_create(amqft_plan* out, const amqft_plan_desc* desc) {
+  return create_plan(out, desc, nullptr);
+}
+
+amqft_status amqft_plan_create_with_constants(amqft_plan* out, const amqft_plan_desc* desc,
+                                              const double* constants, size_t count) {
+  if (!constants) return set_err(AMQFT_EINVAL, "null constant table");
+  try {
+    const std::vector<double> tab(constants, constants + count);
+    return create_plan(out, desc, &tab);
+  } catch (...) {
+    return from_exception();
+  }
 }
 
 amqft_status amqft_plan_destroy(amqft_plan plan) {
@@ -703,23 +736,15 @@ amqft_status amqft_plan_dump(amqft_plan P, int prog, void* records, size_t cap,
   return AMQFT_OK;
 }
 
-amqft_status amqft_execute_host(int variant, int function, size_t n, const double* in,
-                                double* out, int trig_mode, size_t table_max_n,
-                                int corrupt_constants, uint64_t* meter3) {
-  amqft_plan_desc d{};
-  d.variant = variant;
-  d.function = function;
-  d.n = n;
-  d.batch = 1;
-  d.dtype = AMQFT_F64;
-  d.trig_mode = trig_mode;
-  d.order = AMQFT_ORDER_EXACT;
-  d.device = 0;
-  cudaGetDevice(&d.device);
-  d.table_max_n = table_max_n;
-  d.corrupt_constants = corrupt_constants;
+}  // extern "C"
+
+namespace {
+
+// One signal between host buffers on the current device, exact fp64 order.
+amqft_status execute_host_impl(const amqft_plan_desc& d, const std::vector<double>* host_tab, const double* in,
+                               double* out, int inverse, uint64_t* meter3) {
   amqft_plan P = nullptr;
-  amqft_status s = amqft_plan_create(&P, &d);
+  amqft_status s = create_plan(&P, &d, host_tab);
   if (s != AMQFT_OK) return s;
   const size_t bytes = P->c.cells * sizeof(double);
   void *din = nullptr, *dout = nullptr;
@@ -727,7 +752,7 @@ amqft_status amqft_execute_host(int variant, int function, size_t n, const doubl
     ck(cudaMalloc(&din, bytes), "cudaMalloc");
     ck(cudaMalloc(&dout, bytes), "cudaMalloc");
     ck(cudaMemcpy(din, in, bytes, cudaMemcpyHostToDevice), "cudaMemcpy H2D");
-    s = amqft_exec_rows(P, din, dout, 1, 0, nullptr);
+    s = amqft_exec_rows(P, din, dout, 1, inverse, nullptr);
     if (s == AMQFT_OK) {
       ck(cudaMemcpy(out, dout, bytes, cudaMemcpyDeviceToHost), "cudaMemcpy D2H");
       if (meter3) amqft_plan_op_counts(P, meter3);
@@ -739,6 +764,52 @@ amqft_status amqft_execute_host(int variant, int function, size_t n, const doubl
   cudaFree(dout);
   amqft_plan_destroy(P);
   return s;
+}
+
+amqft_plan_desc host_desc(int variant, int function, size_t n) {
+  amqft_plan_desc d{};
+  d.variant = variant;
+  d.function = function;
+  d.n = n;
+  d.batch = 1;
+  d.dtype = AMQFT_F64;
+  d.trig_mode = AMQFT_TRIG_TABLE;
+  d.order = AMQFT_ORDER_EXACT;
+  d.device = 0;
+  cudaGetDevice(&d.device);
+  return d;
+}
+
+}  // namespace
+
+extern "C" {
+
+amqft_status amqft_execute_host_constants(int variant, int function, size_t n, const double* in, double* out,
+                                          const double* constants, size_t count, uint64_t* meter3) {
+  if (!constants || !in || !out) return set_err(AMQFT_EINVAL, "null buffer");
+  try {
+    const std::vector<double> tab(constants, constants + count);
+    amqft_plan_desc d = host_desc(variant, function, n);
+    d.table_max_n = 4 * count;
+    return execute_host_impl(d, &tab, in, out, 0, meter3);
+  } catch (...) {
+    return from_exception();
+  }
+}
+
+amqft_status amqft_execute_host_inverse(int variant, size_t n, const double* in, double* out) {
+  if (!in || !out) return set_err(AMQFT_EINVAL, "null buffer");
+  return execute_host_impl(host_desc(variant, AMQFT_FN_CDFT, n), nullptr, in, out, 1, nullptr);
+}
+
+amqft_status amqft_execute_host(int variant, int function, size_t n, const double* in,
+                                double* out, int trig_mode, size_t table_max_n,
+                                int corrupt_constants, uint64_t* meter3) {
+  amqft_plan_desc d = host_desc(variant, function, n);
+  d.trig_mode = trig_mode;
+  d.table_max_n = table_max_n;
+  d.corrupt_constants = corrupt_constants;
+  return execute_host_impl(d, nullptr, in, out, 0, meter3);
 }
 
 amqft_status amqft_device_synchronize(int device) {

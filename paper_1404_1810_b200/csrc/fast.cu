@@ -34,30 +34,30 @@ std::unique_ptr<FastPlan> make_fast_typed(int v, int kind, size_t n, const void*
 }
 
 // fp32 rows, fp64 arithmetic (variants 5-8, N = 1024-4096): the fused
-// kernel's fp64 instance with fp32 loads/stores; it builds its own fp64
-// constant table (the plan's table is fp32).
-std::unique_ptr<FastPlan> make_fast_mixed(int v, int kind, size_t n, uint32_t nmax, int dev) {
+// kernel's fp64 instance with fp32 loads/stores, on the plan's fp64 copy of
+// its constant table.
+std::unique_ptr<FastPlan> make_fast_mixed(int v, int kind, size_t n, const void* tab64, uint32_t nmax, int dev) {
   using namespace fastk;
-  if (n < 1024 || n > 4096) return nullptr;
+  if (n < 1024 || n > 4096 || !tab64) return nullptr;
   switch (v) {
-    case 5: return make_for_variant<5, double, float>(kind, n, nullptr, nmax, dev);
-    case 6: return make_for_variant<6, double, float>(kind, n, nullptr, nmax, dev);
-    case 7: return make_for_variant<7, double, float>(kind, n, nullptr, nmax, dev);
-    case 8: return make_for_variant<8, double, float>(kind, n, nullptr, nmax, dev);
+    case 5: return make_for_variant<5, double, float>(kind, n, tab64, nmax, dev);
+    case 6: return make_for_variant<6, double, float>(kind, n, tab64, nmax, dev);
+    case 7: return make_for_variant<7, double, float>(kind, n, tab64, nmax, dev);
+    case 8: return make_for_variant<8, double, float>(kind, n, tab64, nmax, dev);
   }
   return nullptr;
 }
 
 
 std::unique_ptr<FastPlan> make_fast_plan(const amqft_plan_desc& d, const void* d_trig,
-                                         uint32_t nmax) {
+                                         uint32_t nmax, const void* d_trig64) {
   if (d.function != AMQFT_FN_CDFT && d.function != AMQFT_FN_RDFT) return nullptr;
   // AM constants: both trig modes read the plan's host-built table, whose
   // values are bitwise the reference's on-the-fly long double values
   // (variants_test.cpp:267-277); the mode matters only for four-step twiddles
   const int kind = d.function == AMQFT_FN_RDFT ? 1 : 0;
   if (d.dtype == AMQFT_F32 && f32_needs_f64_compute(d.variant, d.n))
-    return make_fast_mixed(d.variant, kind, d.n, nmax, d.device);
+    return make_fast_mixed(d.variant, kind, d.n, d_trig64, nmax, d.device);
   if (d.dtype == AMQFT_F32) return make_fast_typed<float>(d.variant, kind, d.n, d_trig, nmax, d.device);
   return make_fast_typed<double>(d.variant, kind, d.n, d_trig, nmax, d.device);
 }
@@ -131,7 +131,8 @@ bool fast_sub_covered(int dtype, size_t n, int variant) {
   return n >= 2 && n <= 4096 && n != 512;
 }
 
-std::unique_ptr<FastPlan> make_fast_sub(int variant, size_t n, int dtype, const void* tab, uint32_t nmax, int dev) {
+std::unique_ptr<FastPlan> make_fast_sub(int variant, size_t n, int dtype, const void* tab, uint32_t nmax, int dev,
+                                        const void* tab64) {
   amqft_plan_desc d{};
   d.variant = variant;
   d.function = AMQFT_FN_CDFT;
@@ -141,7 +142,7 @@ std::unique_ptr<FastPlan> make_fast_sub(int variant, size_t n, int dtype, const 
   d.trig_mode = AMQFT_TRIG_TABLE;
   d.order = AMQFT_ORDER_FAST;
   d.device = dev;
-  std::unique_ptr<FastPlan> p = make_fast_plan(d, tab, nmax);
+  std::unique_ptr<FastPlan> p = make_fast_plan(d, tab, nmax, tab64);
   OpCount o;
   if (!p) p = make_small_plan(d, tab, nmax, &o);
   return p;

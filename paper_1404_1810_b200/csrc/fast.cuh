@@ -52,8 +52,10 @@ class FastPlan {
 inline bool f32_needs_f64_compute(int variant, size_t n) { return variant >= 5 && n >= 512; }
 
 // Returns nullptr when no fused kernel covers the request.
+// d_trig64: fp64 copy of the table for fp32 plans that compute in fp64.
 std::unique_ptr<FastPlan> make_fast_plan(const amqft_plan_desc& d,
-                                         const void* d_trig, uint32_t nmax);
+                                         const void* d_trig, uint32_t nmax,
+                                         const void* d_trig64 = nullptr);
 OpCount fast_op_counts(const amqft_plan_desc& d);
 
 // One-thread-per-row kernel for small CDFTs (small_kernel.cuh): fp32 N <= 64,

@@ -1109,18 +1109,9 @@ class FastPlanImpl final : public FastPlan {
   FastPlanImpl(const void* tab, uint32_t nmax, int device) : tab_(static_cast<const R*>(tab)),
                                                               nmax_(nmax) {
     using C = Cfg<V, R, LOGN, LOGLB, IO>;
-    if constexpr (!std::is_same<IO, R>::value) {
-      // fp32-I/O plans hand over their fp32 table: the fp64-compute instance
-      // builds the Nmax = N fp64 table itself (host long double, rounded
-      // once: bitwise TrigTable::constants, trig.cpp)
-      const std::vector<double> t64 = trig_table(V, static_cast<size_t>(C::N), false);
-      cudaError_t e0 = cudaMalloc(&own_tab_, sizeof(R) * (C::N / 4));
-      if (e0 == cudaSuccess)
-        e0 = cudaMemcpy(own_tab_, t64.data(), sizeof(R) * (C::N / 4), cudaMemcpyHostToDevice);
-      if (e0 != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e0));
-      tab_ = own_tab_;
-      nmax_ = C::N;
-    } else if (nmax_ != static_cast<uint32_t>(C::N)) {
+    // (fp32-I/O fp64-compute instances receive the plan's fp64 copy of the
+    // table: tab is always of type R)
+    if (nmax_ != static_cast<uint32_t>(C::N)) {
       cudaError_t e0 = cudaMalloc(&own_tab_, sizeof(R) * (C::N / 4));
       if (e0 != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e0));
       k_compact_table<R><<<8, 256>>>(tab_, own_tab_, C::N, static_cast<int>(nmax_));

@@ -446,7 +446,8 @@ class FourStepPlan final : public FastPlan {
   using V2 = typename C2<R>::T;
 
  public:
-  FourStepPlan(int variant, size_t n, size_t batch, int trig_mode, const void* tab, uint32_t nmax, int dev)
+  FourStepPlan(int variant, size_t n, size_t batch, int trig_mode, const void* tab, uint32_t nmax, int dev,
+               const void* tab64)
       : n_(n), batch_(batch), onthefly_(trig_mode == AMQFT_TRIG_ONTHEFLY) {
     logn_ = lg2(n);
     const int dtype = sizeof(R) == 8 ? AMQFT_F64 : AMQFT_F32;
@@ -458,11 +459,11 @@ class FourStepPlan final : public FastPlan {
     col_ = sh.col;
     three_ = sh.three;
     if (three_) {   // p1_: A columns, pb_: B columns, p2_: C rows
-      pb_ = make_fast_sub(variant, nb_, dtype, tab, nmax, dev);
+      pb_ = make_fast_sub(variant, nb_, dtype, tab, nmax, dev, tab64);
       if (!pb_) throw std::invalid_argument("four-step: no kernel for the middle factor");
     }
-    p1_ = make_fast_sub(variant, n1_, dtype, tab, nmax, dev);
-    p2_ = make_fast_sub(variant, n2_, dtype, tab, nmax, dev);
+    p1_ = make_fast_sub(variant, n1_, dtype, tab, nmax, dev, tab64);
+    p2_ = make_fast_sub(variant, n2_, dtype, tab, nmax, dev, tab64);
     if (!p1_ || !p2_) throw std::invalid_argument("four-step: no fused kernel for the sub-transform sizes");
     // half-size twiddle tables: w^(jh B), w^(jl), long double -> double
     logb_ = (logn_ + 1) / 2;
@@ -717,11 +718,14 @@ amqft_status fourstep_factors(const amqft_plan_desc& d, size_t* f3) {
   return AMQFT_OK;
 }
 
-std::unique_ptr<FastPlan> make_fourstep_plan(const amqft_plan_desc& d, const void* d_trig, uint32_t nmax) {
+std::unique_ptr<FastPlan> make_fourstep_plan(const amqft_plan_desc& d, const void* d_trig, uint32_t nmax,
+                                             const void* d_trig64) {
   if (!fourstep_covers(d)) return nullptr;
   if (d.dtype == AMQFT_F64)
-    return std::make_unique<FourStepPlan<double>>(d.variant, d.n, d.batch, d.trig_mode, d_trig, nmax, d.device);
-  return std::make_unique<FourStepPlan<float>>(d.variant, d.n, d.batch, d.trig_mode, d_trig, nmax, d.device);
+    return std::make_unique<FourStepPlan<double>>(d.variant, d.n, d.batch, d.trig_mode, d_trig, nmax, d.device,
+                                                   d_trig64);
+  return std::make_unique<FourStepPlan<float>>(d.variant, d.n, d.batch, d.trig_mode, d_trig, nmax, d.device,
+                                                d_trig64);
 }
 
 }  // namespace amqft_b200

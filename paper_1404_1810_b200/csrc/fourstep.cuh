@@ -12,13 +12,16 @@ namespace amqft_b200 {
 
 // Fused / small-CDFT plan for one sub-transform size (nullptr if none),
 // its op counts, and whether a single kernel covers n: fast.cu.
-std::unique_ptr<FastPlan> make_fast_sub(int variant, size_t n, int dtype, const void* tab, uint32_t nmax, int dev);
+std::unique_ptr<FastPlan> make_fast_sub(int variant, size_t n, int dtype, const void* tab, uint32_t nmax, int dev,
+                                        const void* tab64 = nullptr);
 OpCount fast_sub_op_counts(int variant, size_t n, int dtype);
 bool fast_sub_covered(int dtype, size_t n, int variant);
 
 // CDFT, fast order, N up to 2^26 beyond the single-kernel sizes.
 bool fourstep_covers(const amqft_plan_desc& d);
-std::unique_ptr<FastPlan> make_fourstep_plan(const amqft_plan_desc& d, const void* d_trig, uint32_t nmax);
+// d_trig64: fp64 copy of the table (fp32 plans whose sub-transforms compute in fp64)
+std::unique_ptr<FastPlan> make_fourstep_plan(const amqft_plan_desc& d, const void* d_trig, uint32_t nmax,
+                                             const void* d_trig64 = nullptr);
 OpCount fourstep_op_counts(const amqft_plan_desc& d);
 // {A, B, C}: n = A B C (two-factor plans: B = 1)
 amqft_status fourstep_factors(const amqft_plan_desc& d, size_t* f3);

@@ -73,7 +73,7 @@ def build_shim_caller(tmpdir):
     import subprocess
     exe = os.path.join(str(tmpdir), "shim_caller")
     lib_dir = os.path.dirname(_native.LIB_PATH)
-    subprocess.run(["g++", "-std=c++17", "-O2", "-Wall", "-Wextra", "-I", os.path.join(ROOT, "include"),
+    subprocess.run(["g++", "-std=c++20", "-O2", "-Wall", "-Wextra", "-I", os.path.join(ROOT, "include"),
                     "-I", "/usr/local/cuda/include", os.path.join(ROOT, "tests", "native", "shim_caller.cpp"),
                     "-o", exe, "-L", lib_dir, "-lamqft_b200", f"-Wl,-rpath,{lib_dir}"], check=True)
     return exe
