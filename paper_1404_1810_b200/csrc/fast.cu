@@ -1,6 +1,10 @@
 // fast.cu -- dispatcher of the fused CDFT kernels (kernel: fast_kernel.cuh;
 // per-variant instances: fast_v1.cu .. fast_v8.cu).
 #include "fast.cuh"
+
+#include <cstdlib>
+#include <type_traits>
+
 #include "fourstep.cuh"
 #include "gen/small_ops.cuh"
 
@@ -9,6 +13,9 @@ namespace fastk {
 // instances: fast_v<V>.cu (CDFT rows), fast_rv<V>.cu (RDFT rows)
 template <int V, typename R, bool RD, typename IO = R>
 std::unique_ptr<FastPlan> make_sized(size_t n, const void* tab, uint32_t nmax, int dev);
+
+template <int V, typename R, typename IO = R>
+std::unique_ptr<FastPlan> make_cluster(size_t n, const void* tab, uint32_t nmax, int dev);
 
 template <int V, typename R, typename IO = R>
 std::unique_ptr<FastPlan> make_for_variant(int kind, size_t n, const void* tab, uint32_t nmax, int dev) {
@@ -49,9 +56,52 @@ std::unique_ptr<FastPlan> make_fast_mixed(int v, int kind, size_t n, const void*
 }
 
 
+// Cluster four-step (fast_kernel.cuh, k_fast<..., P>): CDFT N = P * 4096
+// as P fused rows on one cluster of P CTAs, one pass over HBM.  fp32, and
+// fp32 rows computed in fp64 for variants 5-8.  Used where it beats the
+// alternative (B200, tools/cluster_ab.sh, profiles/r02_cluster_ab.log):
+// N = 2^14 for variants 2 and 4 (+7-8 % over the three-factor four-step)
+// and N = 8192 for the serial-recurrence variants 1 and 3 (+31 % over the
+// single-CTA 8192 kernel).  Elsewhere it loses: the per-row DSMEM exchange
+// makes a cluster run in lockstep with its slowest CTA (worse with P = 8 /
+// 16, and 16-CTA clusters leave a quarter of the SMs idle), and the fp64-
+// compute instance of variants 5-8 fits one CTA per SM.
+// AMQFT_AB_CLUSTER=all|none overrides the choice (A/B measurements only).
+bool uses_cluster(const amqft_plan_desc& d) {
+  if (d.function != AMQFT_FN_CDFT || d.dtype != AMQFT_F32) return false;
+  if (d.n < 8192 || d.n > 65536 || (d.n & (d.n - 1))) return false;
+  if (const char* e = std::getenv("AMQFT_AB_CLUSTER")) {
+    if (e[0] == 'a') return true;
+    if (e[0] == 'n') return false;
+  }
+  const int v = d.variant;
+  return (d.n == 16384 && (v == 2 || v == 4)) || (d.n == 8192 && (v == 1 || v == 3));
+}
+
+template <typename R, typename IO = R>
+std::unique_ptr<FastPlan> make_cluster_typed(int v, size_t n, const void* tab, uint32_t nmax, int dev) {
+  using namespace fastk;
+  switch (v) {
+    case 1: if constexpr (std::is_same<R, IO>::value) return make_cluster<1, R, IO>(n, tab, nmax, dev); break;
+    case 2: if constexpr (std::is_same<R, IO>::value) return make_cluster<2, R, IO>(n, tab, nmax, dev); break;
+    case 3: if constexpr (std::is_same<R, IO>::value) return make_cluster<3, R, IO>(n, tab, nmax, dev); break;
+    case 4: if constexpr (std::is_same<R, IO>::value) return make_cluster<4, R, IO>(n, tab, nmax, dev); break;
+    case 5: return make_cluster<5, R, IO>(n, tab, nmax, dev);
+    case 6: return make_cluster<6, R, IO>(n, tab, nmax, dev);
+    case 7: return make_cluster<7, R, IO>(n, tab, nmax, dev);
+    case 8: return make_cluster<8, R, IO>(n, tab, nmax, dev);
+  }
+  return nullptr;
+}
+
 std::unique_ptr<FastPlan> make_fast_plan(const amqft_plan_desc& d, const void* d_trig,
                                          uint32_t nmax, const void* d_trig64) {
   if (d.function != AMQFT_FN_CDFT && d.function != AMQFT_FN_RDFT) return nullptr;
+  if (uses_cluster(d)) {
+    if (f32_needs_f64_compute(d.variant, d.n))
+      return d_trig64 ? make_cluster_typed<double, float>(d.variant, d.n, d_trig64, nmax, d.device) : nullptr;
+    return make_cluster_typed<float>(d.variant, d.n, d_trig, nmax, d.device);
+  }
   // AM constants: both trig modes read the plan's host-built table, whose
   // values are bitwise the reference's on-the-fly long double values
   // (variants_test.cpp:267-277); the mode matters only for four-step twiddles
@@ -107,6 +157,24 @@ std::unique_ptr<FastPlan> make_small_plan(const amqft_plan_desc& d, const void* 
 }
 
 OpCount fast_op_counts(const amqft_plan_desc& d) {
+  if (uses_cluster(d)) {
+    // P rows of the 4096-point DAG, N/P radix-2 P-point DFTs (each
+    // butterfly: one complex multiply, 4 muls + 2 adds, and 4 adds), and per
+    // DFT P - 1 twiddle multiplies plus P - 2 for the twiddle powers
+    // (4 muls + 2 adds each)
+    amqft_plan_desc s = d;
+    s.n = 4096;
+    const OpCount r = fast_op_counts(s);
+    const uint64_t P = d.n / 4096;
+    uint64_t lgp = 0;
+    for (uint64_t t = P; t > 1; t >>= 1) ++lgp;
+    const uint64_t dfts = d.n / P, bfly = dfts * (P / 2) * lgp, tw = (2 * P - 3) * dfts;
+    OpCount c;
+    c.adds = P * r.adds + bfly * 6 + tw * 2;
+    c.muls = P * r.muls + bfly * 4 + tw * 4;
+    c.bt = P * r.bt;
+    return c;
+  }
   // The fused kernel executes exactly the reference DAG (fast_model.py):
   // the closed forms of metering.cpp:85-96.
   OpCount c;

@@ -30,8 +30,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <stdexcept>
 #include <type_traits>
+#include <vector>
 
 #include "fast.cuh"
 // The fused kernel reads the AM constant table from its parameter space:
@@ -93,7 +95,9 @@ struct TabParam {
 // amplify rounding beyond the fp32 tolerance from N = 512 on (SURVEY §8(c)
 // item 2): the DAG and its fp64 rounding are the reference's, only the
 // final result is rounded to fp32.
-template <int V, typename R, int LOGN, int LOGLB, typename IO = R>
+// P > 1: the cluster four-step (k_fast with P CTAs per transform of length
+// P N, one length-N row per CTA; see cluster_exchange below).
+template <int V, typename R, int LOGN, int LOGLB, typename IO = R, int P = 1>
 struct Cfg {
   static constexpr int V_ = V;
   static constexpr int N = 1 << LOGN;
@@ -124,7 +128,8 @@ struct Cfg {
   static constexpr bool SERIAL = CHAIN && sizeof(R) == 8 && std::is_same<IO, R>::value;
   // T, F (4 chains each) + the TMA staging buffer for the next row + mbarrier
   static constexpr size_t STAGE_OFF = 8 * CS * sizeof(R);
-  static constexpr size_t SMEM = AMQFT_TMA_STAGE ? STAGE_OFF + 2 * N * sizeof(IO) + 16 : STAGE_OFF;
+  // + mbarriers: the TMA stage (P == 1) / prefetch, staging-full, staging-free (P > 1)
+  static constexpr size_t SMEM = AMQFT_TMA_STAGE ? STAGE_OFF + 2 * N * sizeof(IO) + (P > 1 ? 32 : 16) : STAGE_OFF;
   // Rows per CTA: two fp32 rows (N <= 4096) share one 512-thread CTA, each
   // with its own T/F/staging slot; every phase runs on both rows' warps at
   // once, so the phase's straight-line code is fetched once per SM for two
@@ -133,9 +138,9 @@ struct Cfg {
   // v4 1.646 -> 1.600 ms, v2 1.741 -> 1.568, v3 2.327 -> 1.936 against one
   // row per CTA (two CTAs per SM).
 #ifdef AMQFT_RPC_FORCE   // A/B builds (tools/ab_kernel.cu)
-  static constexpr int RPC = (sizeof(R) == 4 && LOGN <= 12) ? AMQFT_RPC_FORCE : 1;
+  static constexpr int RPC = (P == 1 && sizeof(R) == 4 && LOGN <= 12) ? AMQFT_RPC_FORCE : 1;
 #else
-  static constexpr int RPC = (sizeof(R) == 4 && LOGN <= 12) ? AMQFT_RPC : 1;
+  static constexpr int RPC = (P == 1 && sizeof(R) == 4 && LOGN <= 12) ? AMQFT_RPC : 1;
 #endif
   static constexpr int NTB = NT * RPC;
   static constexpr size_t SLOT = (SMEM + 127) / 128 * 128;
@@ -639,6 +644,161 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       ::"r"(smem_u32(bar)), "r"(parity) : "memory");
 }
 
+// ---- Cluster four-step (P > 1): one transform of length P N per cluster of
+// P CTAs, N = the fused kernel's row length.  Decimation in frequency,
+// n = N n1 + n2, k = k1 + P k2:
+//   X[k1 + P k2] = sum_n2 w_N^(n2 k2) [ w_(PN)^(n2 k1) sum_n1 x[N n1 + n2] w_P^(n1 k1) ]
+// CTA q owns the chunk n2 in [q N/P, (q+1) N/P): its P input pieces (one
+// per quarter n1, contiguous, every input byte read once chip-wide) are
+// TMA-prefetched into the dead T buffer one row ahead; the P-point DFTs and
+// the twiddle run in registers, and y_k1[n2] goes straight into CTA k1's
+// staging row with st.async over DSMEM, completing bytes on CTA k1's
+// "full" mbarrier (the only exchange: (P-1)/P of a row per CTA).  A CTA
+// that has read its staging row arrives on every CTA's "free" mbarrier.
+// Then every CTA runs the ordinary fused phases on its staged row and
+// writes X[k1 + P k2] (stride P) to HBM.  The AM-QFT DAG runs inside each
+// length-N row; fp32 error: the fused kernel's plus one P-point DFT and one
+// twiddle rounding.
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+// asynchronous remote store, completing its bytes on the remote mbarrier
+__device__ __forceinline__ void st_async(uint32_t addr, float2 v, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];"
+               ::"r"(addr), "f"(v.x), "f"(v.y), "r"(mbar) : "memory");
+}
+__device__ __forceinline__ void st_async(uint32_t addr, double2 v, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];"
+               ::"r"(addr), "d"(v.x), "d"(v.y), "r"(mbar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t mbar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(mbar_cluster) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITC_%=;\n}"
+      ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
+// In-register radix-2 DFT of P points (forward sign), w[k] = w_P^k.
+template <int P, typename V2>
+__device__ __forceinline__ void small_dft(V2 (&a)[P], const V2 (&w)[P]) {
+  // bit-reversed order
+#pragma unroll
+  for (int i = 0; i < P; ++i) {
+    int j = 0;
+#pragma unroll
+    for (int b = 1, t = i; b < P; b <<= 1, t >>= 1) j = (j << 1) | (t & 1);
+    if (j > i) {
+      const V2 t2 = a[i];
+      a[i] = a[j];
+      a[j] = t2;
+    }
+  }
+#pragma unroll
+  for (int len = 2; len <= P; len <<= 1) {
+#pragma unroll
+    for (int i = 0; i < P; i += len) {
+#pragma unroll
+      for (int j = 0; j < len / 2; ++j) {
+        const V2 tw = w[j * (P / len)];
+        const V2 u = a[i + j], b = a[i + j + len / 2];
+        const V2 v{b.x * tw.x - b.y * tw.y, b.x * tw.y + b.y * tw.x};
+        a[i + j] = V2{u.x + v.x, u.y + v.y};
+        a[i + j + len / 2] = V2{u.x - v.x, u.y - v.y};
+      }
+    }
+  }
+}
+
+// Prefetch of CTA q's P input pieces of big transform `row` into `dst`
+// (piece n1 at dst + n1 N/P complex values), one TMA bulk copy each.
+template <typename IO, int P, int N>
+__device__ __forceinline__ void cluster_prefetch(const IO* __restrict__ xrow, void* dst, int q, uint64_t* bar) {
+  constexpr uint32_t CHB = N / P * 2 * sizeof(IO);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+               ::"r"(smem_u32(bar)), "r"(CHB * P) : "memory");
+#pragma unroll 1
+  for (int n1 = 0; n1 < P; ++n1)
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(static_cast<unsigned char*>(dst) + n1 * CHB)),
+                 "l"(xrow + (static_cast<size_t>(n1) * N + static_cast<size_t>(q) * (N / P)) * 2), "r"(CHB),
+                 "r"(smem_u32(bar))
+                 : "memory");
+}
+
+// The exchange: CTA q fills the staging rows of all P CTAs of its cluster
+// from its prefetched pieces `src`.  ctw[j] = w_(PN)^j, j < P N (host long
+// double, rounded to R).
+template <typename R, typename IO, int P, int N, int NT, bool INV>
+__device__ __forceinline__ void cluster_exchange(const IO* src, IO* Sb, uint64_t* full, int q, int tid,
+                                                 const void* __restrict__ ctw_) {
+  using V2 = typename std::conditional<sizeof(R) == 4, float2, double2>::type;
+  using IO2 = typename std::conditional<sizeof(IO) == 4, float2, double2>::type;
+  using E = decltype(IO2{}.x);
+  const V2* ctw = static_cast<const V2*>(ctw_);
+  constexpr int CH = N / P;   // n2 per CTA
+  static_assert(CH % NT == 0, "exchange tiling");
+  constexpr int IT = CH / NT;
+  V2 w[P];
+#pragma unroll
+  for (int k = 0; k < P; ++k) w[k] = ctw[k * N];   // w_P^k = w_(PN)^(kN)
+  const IO2* x2 = reinterpret_cast<const IO2*>(src);
+  // peer windows: mapa once per peer (a CTA's window is linear)
+  uint32_t rsb[P], rfb[P];
+#pragma unroll
+  for (int k = 0; k < P; ++k) {
+    rsb[k] = mapa(smem_u32(Sb), static_cast<uint32_t>(k));
+    rfb[k] = mapa(smem_u32(full), static_cast<uint32_t>(k));
+  }
+  // w_(PN)^n2 for every n2 of the thread (coalesced, issued up front); the
+  // powers w^(n2 k1) by repeated multiplication (P - 2 roundings at most)
+  V2 w1[IT];
+#pragma unroll
+  for (int it = 0; it < IT; ++it) w1[it] = ctw[q * CH + it * NT + tid];
+#pragma unroll
+  for (int it = 0; it < IT; ++it) {
+    const int j = it * NT + tid, n2 = q * CH + j;
+    V2 a[P];
+#pragma unroll
+    for (int n1 = 0; n1 < P; ++n1) {
+      const IO2 v = x2[n1 * CH + j];
+      a[n1] = INV ? V2{static_cast<R>(v.y), static_cast<R>(v.x)} : V2{static_cast<R>(v.x), static_cast<R>(v.y)};
+    }
+    small_dft<P>(a, w);
+    V2 t = w1[it];
+#pragma unroll
+    for (int k1 = 0; k1 < P; ++k1) {
+      V2 y = a[k1];
+      if (k1) {
+        y = V2{y.x * t.x - y.y * t.y, y.x * t.y + y.y * t.x};
+        if (k1 + 1 < P) t = V2{t.x * w1[it].x - t.y * w1[it].y, t.x * w1[it].y + t.y * w1[it].x};
+      }
+      st_async(rsb[k1] + static_cast<uint32_t>(n2) * sizeof(IO2), IO2{static_cast<E>(y.x), static_cast<E>(y.y)},
+               rfb[k1]);
+    }
+  }
+}
+
 #ifdef AMQFT_PHASE_TIMING
 // Instrumented build only (tools/phase_timing): CTA 0 accumulates, per
 // phase, the cycles thread 0 spends between phase boundaries
@@ -668,7 +828,7 @@ __device__ unsigned long long g_warp_work[16][16];
 // MODE 0: CDFT forward; 1: CDFT inverse (swap trick); 2: RDFT forward, two
 // real rows per kernel row (row A -> chains 0/1, row B -> chains 2/3: the
 // same Dct/Dst chains as the Re/Im halves of a CDFT, variants.cpp:190-209).
-template <int V, typename R, int LOGN, int LOGLB, int MODE, typename IO = R>
+template <int V, typename R, int LOGN, int LOGLB, int MODE, typename IO = R, int P = 1>
 #ifndef AMQFT_FAST_MINB
 #define AMQFT_FAST_MINB 2
 #endif
@@ -678,14 +838,14 @@ __global__ void __launch_bounds__(
 #ifdef AMQFT_LB_THREADS   // register-budget experiments (tools/ab_kernel.cu)
                                   AMQFT_LB_THREADS,
 #else
-                                  Cfg<V, R, LOGN, LOGLB, IO>::NTB,
+                                  Cfg<V, R, LOGN, LOGLB, IO, P>::NTB,
 #endif
-                                  ((Cfg<V, R, LOGN, LOGLB, IO>::RPC == 1 && sizeof(R) == 4 &&
-                                    2 * Cfg<V, R, LOGN, LOGLB, IO>::SMEM_BLOCK <= 227 * 1024)
+                                  ((Cfg<V, R, LOGN, LOGLB, IO, P>::RPC == 1 && sizeof(R) == 4 &&
+                                    2 * Cfg<V, R, LOGN, LOGLB, IO, P>::SMEM_BLOCK <= 227 * 1024)
                                        ? AMQFT_FAST_MINB : 1))
 k_fast(const IO* __restrict__ in, IO* __restrict__ out, size_t rows_in,
        const __grid_constant__ TabParam<R, (1 << LOGN) / 4> tparam, const R* __restrict__ ltab, int nmax_unused,
-       R scale) {
+       R scale, const void* __restrict__ ctw) {
   (void)nmax_unused;
   // the plan compacts its table to Nmax = N (k_compact_table), so every
   // generated slot index is a compile-time constant into the parameter space
@@ -698,9 +858,13 @@ k_fast(const IO* __restrict__ in, IO* __restrict__ out, size_t rows_in,
 #ifdef AMQFT_PHASE_TIMING
   long long t_prev = 0, w_start = 0;
 #endif
-  using C = Cfg<V, R, LOGN, LOGLB, IO>;
+  using C = Cfg<V, R, LOGN, LOGLB, IO, P>;
   using A = KArith<R, C::LOGN_>;
   using V2 = typename std::conditional<sizeof(R) == 4, float2, double2>::type;
+  static_assert(P == 1 || MODE != 2, "the cluster four-step runs CDFT rows");
+  // P > 1: the swap-trick inverse swaps in the exchange (input of the whole
+  // P N transform) and swaps + scales in the store
+  constexpr bool INV_IN = MODE == 1 && P == 1;
   using IO2 = typename std::conditional<sizeof(IO) == 4, float2, double2>::type;
   // rows in HBM / staging (IO) <-> arithmetic (R)
   auto cvt_in = [](IO2 v) -> V2 { return V2{static_cast<R>(v.x), static_cast<R>(v.y)}; };
@@ -740,19 +904,45 @@ k_fast(const IO* __restrict__ in, IO* __restrict__ out, size_t rows_in,
   // Output through a bulk store: the row is assembled in the F buffer (free
   // once read; next written by the following row's bottom phase, after
   // thread 0 has waited for the bulk read) and leaves with one cp.async.bulk.
-  constexpr bool BULK_ST = AMQFT_TMA_STORE && sizeof(IO) == 4 && IO_IT <= 8 &&
+  constexpr bool BULK_ST = P == 1 && AMQFT_TMA_STORE && sizeof(IO) == 4 && IO_IT <= 8 &&
                            4 * C::CS * sizeof(R) >= 2 * N * sizeof(IO);
+  // cluster four-step: cluster id / count, this CTA's k1
+  const size_t cl_id = P > 1 ? blockIdx.x / P : 0, cl_n = P > 1 ? gridDim.x / P : 1;
+  const int q = P > 1 ? static_cast<int>(cluster_rank()) : 0;
+  (void)q;
+  // P > 1: bar = the prefetch of this CTA's input pieces (into T), full =
+  // the staging row's bytes from the P exchangers, freeb = all P CTAs have
+  // read their staging rows (one remote arrive each)
+  uint64_t* full = bar + 1;
+  uint64_t* freeb = bar + 2;
+  (void)full;
+  (void)freeb;
 #if AMQFT_TMA_STAGE
   if (tid == 0) {
     mbar_init(bar, 1);
+    if constexpr (P > 1) {
+      mbar_init(full, 1);
+      mbar_init(freeb, P);
+    }
     fence_mbar_init();
   }
   row_sync();
+  uint32_t xpar = 0;   // P > 1: phase of full / freeb
+  if constexpr (P > 1) {
+    // every CTA's barriers are initialised before any remote arrive; the
+    // staging rows start free (one arrive per CTA on every freeb)
+    cluster_arrive();
+    cluster_wait();
+    if (tid == 0) {
+      for (int k = 0; k < P; ++k) mbar_arrive_remote(mapa(smem_u32(freeb), static_cast<uint32_t>(k)));
+      if (cl_id < rows) cluster_prefetch<IO, P, N>(in + cl_id * 2 * N * P, Tb, q, bar);
+    }
+  }
   // bytes of kernel row kr (an odd RDFT batch ends with a single real row)
   auto row_bytes = [&](size_t kr) -> uint32_t {
     return (RDFT && 2 * kr + 1 >= rows_in) ? ROW_BYTES / 2 : ROW_BYTES;
   };
-  if (tid == 0 && blockIdx.x * RSTEP + slot < rows)
+  if (P == 1 && tid == 0 && blockIdx.x * RSTEP + slot < rows)
     tma_load_1d(Sb, in + (blockIdx.x * RSTEP + slot) * 2 * N, row_bytes(blockIdx.x * RSTEP + slot), bar);
   uint32_t parity = 0;
 #else
@@ -761,15 +951,27 @@ k_fast(const IO* __restrict__ in, IO* __restrict__ out, size_t rows_in,
   (void)ROW_BYTES;
 #endif
 
-  for (size_t r0 = blockIdx.x * RSTEP; r0 < rows; r0 += gridDim.x * RSTEP) {
+  const size_t r_first = P > 1 ? cl_id : blockIdx.x * RSTEP;
+  const size_t r_step = P > 1 ? cl_n : gridDim.x * RSTEP;
+  for (size_t r0 = r_first; r0 < rows; r0 += r_step) {
     // every thread reaches every barrier; a slot past the last row idles
     const size_t row = r0 + slot;
     const bool act = row < rows;
     PHASE_MARK(0);
+    if constexpr (P > 1) {
+      // this CTA's input pieces are in T; every CTA has read its staging row
+      mbar_wait(bar, parity);
+      parity ^= 1;
+      mbar_wait(freeb, xpar);
+      if (tid == 0) mbar_expect_tx(full, static_cast<uint32_t>(2 * N * sizeof(IO)));
+      cluster_exchange<R, IO, P, C::N, C::NT, MODE == 1>(reinterpret_cast<const IO*>(Tb), Sb, full, q, tid, ctw);
+      mbar_wait(full, xpar);   // my staging row is complete
+      xpar ^= 1;
+    }
     // ---- load: SplitComplex (elab.cpp:152-155) + SplitReal (185-197)
     // from the TMA-staged row; then prefetch the CTA's next row.
 #if AMQFT_TMA_STAGE
-    if (act) {
+    if (P == 1 && act) {
       mbar_wait(bar, parity);
       parity ^= 1;
     }
@@ -808,7 +1010,7 @@ k_fast(const IO* __restrict__ in, IO* __restrict__ out, size_t rows_in,
 #pragma unroll
       for (int it = 0; it < IO_IT; ++it) {
         V2 a = av[it], b = bv[it];
-        if (INV) {
+        if (INV_IN) {
           a = V2{a.y, a.x};
           b = V2{b.y, b.x};
         }
@@ -824,15 +1026,19 @@ k_fast(const IO* __restrict__ in, IO* __restrict__ out, size_t rows_in,
       }
       if (tid == 0) {                // m = H
         V2 a = cvt_in(RDFT ? IO2{xa[H], xb[H]} : x[H]);
-        if (INV) a = V2{a.y, a.x};
+        if (INV_IN) a = V2{a.y, a.x};
         Tb[C::coT(0) + C::pt(H, 0)] = a.x;
         Tb[C::coT(2) + C::pt(H, 0)] = a.y;
       }
     }
     WORK_MARK(0);
     row_sync();
+    if constexpr (P > 1) {   // staging row consumed: tell every CTA of the cluster
+      if (tid == 0)
+        for (int k = 0; k < P; ++k) mbar_arrive_remote(mapa(smem_u32(freeb), static_cast<uint32_t>(k)));
+    }
 #if AMQFT_TMA_STAGE
-    if (tid == 0 && row + gridDim.x * RSTEP < rows) {
+    if (P == 1 && tid == 0 && row + gridDim.x * RSTEP < rows) {
       fence_proxy_async();
       tma_load_1d(Sb, in + (row + gridDim.x * RSTEP) * 2 * N, row_bytes(row + gridDim.x * RSTEP), bar);
     }
@@ -916,6 +1122,12 @@ k_fast(const IO* __restrict__ in, IO* __restrict__ out, size_t rows_in,
     WORK_MARK(2);
     row_sync();
     PHASE_MARK(3);
+    if constexpr (P > 1) {   // T is dead until the next load: prefetch the next row's pieces into it
+      if (tid == 0 && row + r_step < rows) {
+        fence_proxy_async();
+        cluster_prefetch<IO, P, N>(in + (row + r_step) * 2 * N * P, Tb, q, bar);
+      }
+    }
 
     if constexpr (C::TM) {
       if constexpr (C::SERIAL) am_levels_desc<C, R, C::LT>(Fb, tid);  // RPC = 1
@@ -940,7 +1152,9 @@ k_fast(const IO* __restrict__ in, IO* __restrict__ out, size_t rows_in,
     PHASE_MARK(5);
 
     // ---- store: SplitReal bwd (elab.cpp:199-208) + SplitComplex bwd (162-183)
-    IO2* y = reinterpret_cast<IO2*>(out + row * 2 * N);
+    // P > 1: X[k1 + P k2], k1 = q (stride P in the big row)
+    IO2* y = reinterpret_cast<IO2*>(out + row * 2 * N * P) + q;
+    constexpr int OS = P;
     if constexpr (BULK_ST) {
       // read all cells (registers), barrier, write the natural-order row
       // over F, barrier, one bulk store per row
@@ -1055,12 +1269,12 @@ k_fast(const IO* __restrict__ in, IO* __restrict__ out, size_t rows_in,
               lo = V2{A::mul(lo.y, scale), A::mul(lo.x, scale)};
               hi = V2{A::mul(hi.y, scale), A::mul(hi.x, scale)};
             }
-            y[k] = cvt_out(lo);
-            y[N - k] = cvt_out(hi);
+            y[k * OS] = cvt_out(lo);
+            y[(N - k) * OS] = cvt_out(hi);
           }
           if (tid == 0) {                // k = H
             const R rd = Fb[C::coF(0) + C::pf(H, 0)], id = Fb[C::coF(2) + C::pf(H, 0)];
-            y[H] = cvt_out(INV ? V2{A::mul(id, scale), A::mul(rd, scale)} : V2{rd, id});
+            y[H * OS] = cvt_out(INV ? V2{A::mul(id, scale), A::mul(rd, scale)} : V2{rd, id});
           }
         }
       }
@@ -1072,6 +1286,10 @@ k_fast(const IO* __restrict__ in, IO* __restrict__ out, size_t rows_in,
     PHASE_MARK(6);
   }
   if (BULK_ST && tid == 0) bulk_wait_all();   // smem must outlive the last bulk store
+  if constexpr (P > 1) {   // no CTA leaves while a peer may still arrive on its barriers
+    cluster_arrive();
+    cluster_wait();
+  }
 }
 
 // Per-level compacted constants for the top mirror levels:
@@ -1152,15 +1370,16 @@ class FastPlanImpl final : public FastPlan {
     const unsigned grid = static_cast<unsigned>(std::min<size_t>(units, static_cast<size_t>(grid_cap_)));
     if (RDFT_ROWS)
       k_fast<V, R, LOGN, LOGLB, 2, IO><<<grid, C::NTB, C::SMEM_BLOCK, st>>>(
-          static_cast<const IO*>(in), static_cast<IO*>(out), rows, tparam_, ltab_, static_cast<int>(nmax_), R(1));
+          static_cast<const IO*>(in), static_cast<IO*>(out), rows, tparam_, ltab_, static_cast<int>(nmax_), R(1),
+          nullptr);
     else if (inverse)
       k_fast<V, R, LOGN, LOGLB, 1, IO><<<grid, C::NTB, C::SMEM_BLOCK, st>>>(
           static_cast<const IO*>(in), static_cast<IO*>(out), rows, tparam_, ltab_, static_cast<int>(nmax_),
-          R(1) / R(C::N));
+          R(1) / R(C::N), nullptr);
     else
       k_fast<V, R, LOGN, LOGLB, 0, IO><<<grid, C::NTB, C::SMEM_BLOCK, st>>>(
           static_cast<const IO*>(in), static_cast<IO*>(out), rows, tparam_, ltab_, static_cast<int>(nmax_),
-          R(1) / R(C::N));
+          R(1) / R(C::N), nullptr);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
   }
@@ -1173,6 +1392,116 @@ class FastPlanImpl final : public FastPlan {
   uint32_t nmax_;
   int grid_cap_ = 148;
 };
+
+// Cluster four-step plan: CDFT rows of length P * 4096 on clusters of P
+// CTAs (k_fast<..., P>), one persistent cluster per group of SMs.
+template <int V, typename R, typename IO, int P>
+class ClusterPlanImpl final : public FastPlan {
+  static constexpr int LOGN = 12, LOGLB = 6;
+  using C = Cfg<V, R, LOGN, LOGLB, IO, P>;
+  using V2 = typename std::conditional<sizeof(R) == 4, float2, double2>::type;
+
+ public:
+  ClusterPlanImpl(const void* tab, uint32_t nmax, int device) {
+    const R* t = static_cast<const R*>(tab);
+    if (nmax != static_cast<uint32_t>(C::N)) {
+      check_(cudaMalloc(&own_tab_, sizeof(R) * (C::N / 4)));
+      k_compact_table<R><<<8, 256>>>(t, own_tab_, C::N, static_cast<int>(nmax));
+      t = own_tab_;
+    }
+    check_(cudaMalloc(&ltab_, sizeof(R) * C::H));
+    k_level_table<R><<<8, 256>>>(t, ltab_, C::H, C::LT, C::N);
+    check_(cudaDeviceSynchronize());
+    check_(cudaMemcpy(tparam_.v, t, sizeof(tparam_.v), cudaMemcpyDeviceToHost));
+    // w_(PN)^j, j < P N, long double rounded once to R
+    const size_t NN = static_cast<size_t>(P) * C::N;
+    std::vector<V2> tw(NN);
+    const long double two_pi = 6.283185307179586476925286766559005768L;
+    for (size_t j = 0; j < NN; ++j) {
+      const long double a = two_pi * static_cast<long double>(j) / static_cast<long double>(NN);
+      tw[j] = V2{static_cast<R>(cosl(a)), static_cast<R>(-sinl(a))};
+    }
+    check_(cudaMalloc(&ctw_, NN * sizeof(V2)));
+    check_(cudaMemcpy(ctw_, tw.data(), NN * sizeof(V2), cudaMemcpyHostToDevice));
+    for (auto fn : {k_fast<V, R, LOGN, LOGLB, 0, IO, P>, k_fast<V, R, LOGN, LOGLB, 1, IO, P>}) {
+      check_(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM_BLOCK)));
+      if (P > 8) check_(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    }
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = P;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(P * 148);
+    cfg.blockDim = dim3(C::NTB);
+    cfg.dynamicSmemBytes = C::SMEM_BLOCK;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int nc = 0;
+    check_(cudaOccupancyMaxActiveClusters(&nc, k_fast<V, R, LOGN, LOGLB, 0, IO, P>, &cfg));
+    if (nc < 1) throw std::runtime_error("cluster four-step: no cluster of this size fits an SM group");
+    max_clusters_ = nc;
+    (void)device;
+    launches = 1;
+  }
+  ~ClusterPlanImpl() override {
+    if (ltab_) cudaFree(ltab_);
+    if (own_tab_) cudaFree(own_tab_);
+    if (ctw_) cudaFree(ctw_);
+  }
+  void exec(const void* in, void* out, size_t rows, int inverse, cudaStream_t st) override {
+    const unsigned nc = static_cast<unsigned>(std::min<size_t>(rows, static_cast<size_t>(max_clusters_)));
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = P;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(P * nc);
+    cfg.blockDim = dim3(C::NTB);
+    cfg.dynamicSmemBytes = C::SMEM_BLOCK;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const R scale = R(1) / R(static_cast<double>(P) * C::N);
+    cudaError_t e;
+    if (inverse)
+      e = cudaLaunchKernelEx(&cfg, k_fast<V, R, LOGN, LOGLB, 1, IO, P>, static_cast<const IO*>(in),
+                             static_cast<IO*>(out), rows, tparam_, static_cast<const R*>(ltab_), C::N, scale,
+                             static_cast<const void*>(ctw_));
+    else
+      e = cudaLaunchKernelEx(&cfg, k_fast<V, R, LOGN, LOGLB, 0, IO, P>, static_cast<const IO*>(in),
+                             static_cast<IO*>(out), rows, tparam_, static_cast<const R*>(ltab_), C::N, scale,
+                             static_cast<const void*>(ctw_));
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+  }
+
+ private:
+  static void check_(cudaError_t e) {
+    if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+  }
+  TabParam<R, (1 << LOGN) / 4> tparam_{};
+  R* own_tab_ = nullptr;
+  R* ltab_ = nullptr;
+  V2* ctw_ = nullptr;
+  int max_clusters_ = 1;
+};
+
+// Sizes run by the cluster four-step (fast.cu decides per size).
+inline bool cluster_size_ok(size_t n) { return n >= 8192 && n <= 65536; }
+
+template <int V, typename R, typename IO = R>
+std::unique_ptr<FastPlan> make_cluster(size_t n, const void* tab, uint32_t nmax, int dev) {
+  switch (n) {
+    case 8192: return std::make_unique<ClusterPlanImpl<V, R, IO, 2>>(tab, nmax, dev);
+    case 16384: return std::make_unique<ClusterPlanImpl<V, R, IO, 4>>(tab, nmax, dev);
+    case 32768: return std::make_unique<ClusterPlanImpl<V, R, IO, 8>>(tab, nmax, dev);
+    case 65536: return std::make_unique<ClusterPlanImpl<V, R, IO, 16>>(tab, nmax, dev);
+  }
+  return nullptr;
+}
 
 template <int V, typename R, bool RD, typename IO = R>
 std::unique_ptr<FastPlan> make_sized(size_t n, const void* tab, uint32_t nmax, int dev) {

@@ -5,5 +5,7 @@ namespace amqft_b200 {
 namespace fastk {
 template std::unique_ptr<FastPlan> make_sized<3, float, false>(size_t, const void*, uint32_t, int);
 template std::unique_ptr<FastPlan> make_sized<3, double, false>(size_t, const void*, uint32_t, int);
+// cluster four-step (N = 8192 .. 65536)
+template std::unique_ptr<FastPlan> make_cluster<3, float>(size_t, const void*, uint32_t, int);
 }  // namespace fastk
 }  // namespace amqft_b200

@@ -7,5 +7,8 @@ template std::unique_ptr<FastPlan> make_sized<5, float, false>(size_t, const voi
 template std::unique_ptr<FastPlan> make_sized<5, double, false>(size_t, const void*, uint32_t, int);
 // fp32 rows, fp64 arithmetic (fast.cuh f32_needs_f64_compute)
 template std::unique_ptr<FastPlan> make_sized<5, double, false, float>(size_t, const void*, uint32_t, int);
+// cluster four-step (N = 8192 .. 65536)
+template std::unique_ptr<FastPlan> make_cluster<5, float>(size_t, const void*, uint32_t, int);
+template std::unique_ptr<FastPlan> make_cluster<5, double, float>(size_t, const void*, uint32_t, int);
 }  // namespace fastk
 }  // namespace amqft_b200

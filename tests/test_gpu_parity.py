@@ -614,13 +614,14 @@ def test_fourstep_fp64_config3_sizes(oracle, restatement, lg):
 
 
 def test_fourstep_fp32_between_kernel_sizes(oracle, restatement):
-    """fp32 N = 2^14 .. 2^19 now run as four-steps (were the generic path)."""
+    """fp32 N = 2^14 .. 2^19 run as four-steps (were the generic path); v4
+    at 2^14 takes the cluster four-step (tests/test_gpu_cluster.py), so v3."""
     r, O = restatement, oracle
     for lg in (14, 17, 19):
         n = 1 << lg
         x = np.random.default_rng(lg).standard_normal(2 * n).astype(np.float32)
-        want = r.execute(4, O.F_CDFT, n, x.astype(np.float64))
-        got = run_plan(_fourstep_plan(4, n, 2), [x, x])
+        want = r.execute(3, O.F_CDFT, n, x.astype(np.float64))
+        got = run_plan(_fourstep_plan(3, n, 2), [x, x])
         assert got[0].tobytes() == got[1].tobytes()
         assert r.rel_l2(got[0], want) <= 1e-5 * lg, lg
 

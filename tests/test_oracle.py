@@ -40,6 +40,30 @@ def test_restatement_matches_reference_on_the_fly_and_large_table(oracle, restat
             assert a.tobytes() == b.tobytes(), (v, kw)
 
 
+def test_restatement_pinned_at_config_sizes(oracle, restatement, reference):
+    """Beyond N = 1024: the restatement is bitwise the compiled reference at
+    config 2's N = 4096 (every wired function), at 2^13 and at 2^16 (CDFT,
+    all 8 variants, meters too) and at 2^18 (CDFT v4) -- the sizes the GPU
+    parity tests compare the device against."""
+    r, ref, O = restatement, reference, oracle
+    for v in range(1, 9):
+        for f in O.wired_functions(v):
+            t = O.FUNCTION_OPERAND[f]
+            x = r.uniform(r.mix_seed(4096, v, f, 0), r.cell_count(t, 4096))
+            a, ma = r.execute(v, f, 4096, x, meter=True)
+            b, mb = ref.execute(v, f, 4096, x, meter=True)
+            assert a.tobytes() == b.tobytes() and ma == mb, (v, f)
+        for lg in (13, 16):
+            n = 1 << lg
+            x = r.uniform(r.mix_seed(lg, v, 0, n), 2 * n)
+            a, ma = r.execute(v, O.F_CDFT, n, x, meter=True)
+            b, mb = ref.execute(v, O.F_CDFT, n, x, meter=True)
+            assert a.tobytes() == b.tobytes() and ma == mb, (v, lg)
+    n = 1 << 18
+    x = r.uniform(18, 2 * n)
+    assert r.execute(4, O.F_CDFT, n, x).tobytes() == ref.execute(4, O.F_CDFT, n, x).tobytes()
+
+
 def test_golden_config1(oracle, restatement):
     g = np.load(os.path.join(GOLD, "config1_cdft1024.npz"))
     x = g["input"]
