@@ -372,8 +372,71 @@ def config4_accuracy(amqft, x, n, local, stream, args):
                 out[f"ms_{key}"] = _timed(lambda: p.forward(x, y, stream=stream), 5, 2, stream, 1, torch.device(f"cuda:{local}"))
             del p
         out[f"rel_l2_fp32_vs_fp64_{key}"] = errs
+    # direct spot checks (csrc/verify.cu): 64 bins of the fp64 reference and
+    # of the timed variant's fp32 result against their O(N) fp64 sums
+    bins = spot_bins(n, seed=24)
+    want = amqft.direct_bins(x, n, bins, stream=stream)
+    idx = torch.as_tensor(bins.astype(np.int64), device=x.device)
+
+    def pick(t):
+        c = t.view(-1, 2)[idx].double().cpu().numpy()
+        return c[:, 0] + 1j * c[:, 1]
+    p = amqft.Plan(args.variant, amqft.FunctionId.Cdft, n, 1, dtype="f32", order=amqft.Order.Fast, device=local)
+    p.forward(x, y, stream=stream)
+    torch.cuda.synchronize()
+    out["spot_bins"] = {"bins": int(len(bins)),
+                        "fp64_reference_rel_l2": float(np.linalg.norm(pick(y64) - want) / np.linalg.norm(want)),
+                        f"fp32_v{args.variant}_rel_l2": float(np.linalg.norm(pick(y) - want) / np.linalg.norm(want))}
     out["tolerance_fp32"] = 1e-5 * 24
     return out
+
+
+def spot_bins(n, count=64, seed=1):
+    """Bins for the direct spot checks: the edges plus seeded random bins."""
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    edge = [0, 1, 2, n // 4, n // 2 - 1, n // 2, n // 2 + 1, n - 1]
+    return np.unique(np.concatenate([edge, rng.integers(0, n, count - len(edge))])).astype(np.uint64)
+
+
+def config5_spot_check(amqft, d, a0, bufs, stream, world, rank, dev):
+    """Config 5 accuracy: 64 output bins of one more forward
+    against their direct O(N) sums over the 2^30 input samples on the device
+    (amqft_direct_bins: fp64, exact integer phase reduction), after the timed
+    region.  Multi-rank: each rank sums its input slab, the partial bins are
+    all-reduced, and the rank holding a bin's k1-slab reports it."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    n = d.n
+    bins = spot_bins(n, seed=30)
+    a = a0.clone()
+    z = d.forward(a, bufs=bufs, stream=stream)
+    torch.cuda.synchronize(dev)
+    part = amqft.direct_bins(a0, n, bins, rows=d.rows1, row_len=d.n1, row0=rank * d.rows1, stride=d.n2,
+                             stream=stream)
+    want = torch.tensor(np.stack([part.real, part.imag], 1), dtype=torch.float64, device=dev)
+    k1 = (bins % d.n1).astype(np.int64)
+    k2 = (bins // d.n1).astype(np.int64)
+    mine = (k1 // d.w) == rank
+    got = torch.zeros(len(bins), 2, dtype=torch.float64, device=dev)
+    if mine.any():
+        zz = z.view(d.w, d.n2, 2)
+        idx = np.nonzero(mine)[0]
+        got[torch.as_tensor(idx, device=dev)] = zz[torch.as_tensor(k1[idx] - rank * d.w, device=dev),
+                                                   torch.as_tensor(k2[idx], device=dev)].double()
+    if world > 1:
+        dist.all_reduce(want)
+        dist.all_reduce(got)
+    w = want.cpu().numpy()
+    g = got.cpu().numpy()
+    wc, gc = w[:, 0] + 1j * w[:, 1], g[:, 0] + 1j * g[:, 1]
+    return {"spot_bins": int(len(bins)),
+            "rel_l2_vs_direct_fp64_sums": float(np.linalg.norm(gc - wc) / np.linalg.norm(wc)),
+            "max_abs_err_over_rms_bin": float(np.max(np.abs(gc - wc)) / np.sqrt(np.mean(np.abs(wc) ** 2))),
+            "tolerance_1e-5_log2N": 3e-4,
+            "method": "direct fp64 sums over all 2^30 samples per bin, phase (n k) mod N in 64-bit integers "
+                      "(csrc/verify.cu), 64 bins incl. 0, 1, N/4, N/2, N-1"}
 
 
 def bench_single(args, world, rank, local):
@@ -453,7 +516,8 @@ def bench_single(args, world, rank, local):
         e2e = None
         extra = {"a2a_ms": a2a_ms, "a2a_bytes_sent_per_gpu": sent,
                  "nvlink_frac": (sent / (a2a_ms / 1000.0) / 900e9) if a2a_ms else None,
-                 "output_layout": "k1-slabs (rows k1 of length n2 per rank); no second all-to-all"}
+                 "output_layout": "k1-slabs (rows k1 of length n2 per rank); no second all-to-all",
+                 "accuracy": config5_spot_check(amqft, d, a0, bufs, stream, world, rank, dev)}
         cpu = None
     achieved = per_gpu_bytes / (ms / 1000.0) / 1e9
     if rank == 0:

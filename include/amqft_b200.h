@@ -196,6 +196,30 @@ amqft_status amqft_dist_twiddle_scatter_t(const void* d_rows, void* const* d_dst
                                           size_t n, size_t row0, int src_rank, int nparts, int trig_mode,
                                           size_t a, void* stream);
 
+/* ---- Verification (not a transform path): direct O(N)-per-bin DFT bins
+ * X[k] = sum_n x[n] w_N^((n k) mod N), the phase reduced exactly in
+ * integers first (the reference naive DFT's discipline, src/oracle.cpp:30-35).
+ *
+ * amqft_direct_bins: fp64 twiddles (sincospi of the reduced phase) and fp64
+ * sums, for spot checks of huge transforms (config 5, N = 2^30).  d_x is a
+ * device buffer of rows x row_len interleaved complex samples (dtype F32 or
+ * F64); sample (r, c) is x[(row0 + r + stride c) mod n] (a plain signal:
+ * rows = 1, row0 = 0, stride = 1).  bins: host array; out: host, {re, im}
+ * per bin.  Synchronises `stream`.
+ *
+ * amqft_direct_bins_extended: the extended-precision reference
+ * (src/oracle.cpp:155-158 computes it with long double twiddles and
+ * compensated long double sums): the same long double twiddles carried
+ * exactly as double-double, double-double products and sums.  x: host,
+ * n interleaved fp64 complex samples (n <= 2^22); reverse = 1 sums in
+ * descending n (the reference's self-gauge, oracle.cpp:160-163); out:
+ * host, {re hi, re lo, im hi, im lo} per bin. */
+amqft_status amqft_direct_bins(const void* d_x, int dtype, size_t rows, size_t row_len, size_t row0,
+                               size_t stride, size_t n, const uint64_t* bins, size_t nbins, double* out,
+                               void* stream);
+amqft_status amqft_direct_bins_extended(const double* x, size_t n, const uint64_t* bins, size_t nbins,
+                                        int reverse, double* out);
+
 /* Batched transpose of complex fp32 matrices: mats x [r][c] -> [c][r];
  * r and c multiples of 32. */
 amqft_status amqft_transpose_c64(const void* d_in, void* d_out, size_t mats, size_t r,

@@ -282,3 +282,21 @@ def schedule_dump(variant: int, function: int, n: int, capacity_cells: int = 1 <
                                 recs.ctypes.data, recs.size, C.byref(cnt), st.ctypes.data,
                                 nst.value, C.byref(nst), ops))
     return recs, st.reshape(-1, 2), tuple(int(v) for v in ops)
+
+
+def direct_bins(x, n: int, bins, *, rows: int = 1, row_len: int | None = None, row0: int = 0,
+                stride: int = 1, stream=None):
+    """Direct fp64 evaluation of selected DFT bins of a device signal
+    (amqft_direct_bins: O(N) per bin, exact integer phase reduction) -- the
+    verification utility for transforms too large for the CPU oracle
+    (config 5).  x: device tensor of interleaved complex samples, fp32 or
+    fp64, `rows` x `row_len` of them; sample (r, c) is the signal's element
+    (row0 + r + stride c) mod n.  Returns complex128 bins (numpy)."""
+    import torch
+    row_len = (x.numel() // 2) // rows if row_len is None else int(row_len)
+    dt = _native.F64 if x.dtype == torch.float64 else _native.F32
+    b = np.ascontiguousarray(bins, dtype=np.uint64)
+    out = np.zeros(2 * b.size, dtype=np.float64)
+    check(lib().amqft_direct_bins(int(x.data_ptr()), dt, int(rows), int(row_len), int(row0), int(stride), int(n),
+                                  b.ctypes.data, b.size, out.ctypes.data, Plan._stream(stream)))
+    return out[0::2] + 1j * out[1::2]
