@@ -232,16 +232,28 @@ class DistFourStep:
         """a: this rank's [n2/P][2 n1] slab (overwritten).  Returns z, this
         rank's [n1/P][2 n2] output slab."""
         send, recv, b, z = bufs if bufs is not None else self.buffers(a)
+        multi = self.world > 1 and dist.is_initialized()
+        if peer_recv is not None and multi:
+            # write-after-read: no rank may scatter into a peer's receive
+            # buffer while that peer still transposes the previous call's data
+            if a.is_cuda:
+                torch.cuda.synchronize(a.device)
+            dist.barrier(group=self.group)
         self.stage1(a, send, peer_recv, stream)
         if peer_recv is not None:
             # the scatter's stores were the exchange; order them before the
             # peers read their receive buffers
-            if self.world > 1 and dist.is_initialized():
+            if multi:
                 if a.is_cuda:
-                    torch.cuda.synchronize()
+                    torch.cuda.synchronize(a.device)
                 dist.barrier(group=self.group)
         elif self.world > 1:
-            dist.all_to_all_single(recv, send, group=self.group)
+            # the collective runs on the caller's stream, after the scatter
+            if a.is_cuda and stream is not None:
+                with torch.cuda.stream(stream):
+                    dist.all_to_all_single(recv, send, group=self.group)
+            else:
+                dist.all_to_all_single(recv, send, group=self.group)
         else:
             recv = send   # one part: the scatter already produced the layout
         return self.stage2(recv, b, z, stream)
