@@ -223,7 +223,8 @@ def ncu_traffic(args, n):
     is a capture of this exact kernel (variant, N, fp32, fast order)."""
     import glob
     logn = n.bit_length() - 1
-    want = f"k_fast<{args.variant},float,{logn},6,0>"
+    # k_fast<V, R, LOGN, LOGLB, MODE[, IO, P]>: the one-CTA-per-row fp32 instance
+    want = (f"k_fast<{args.variant},float,{logn},6,0>", f"k_fast<{args.variant},float,{logn},6,0,float,1>")
     if args.dtype != "f32" or args.order != "fast":
         return None, None
     for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_k_fast_*.json")), reverse=True):
@@ -231,7 +232,7 @@ def ncu_traffic(args, n):
             d = json.load(open(f))
         except (OSError, ValueError):
             continue
-        if want not in d.get("Kernel Name", "") or int(float(d.get("launch__grid_size", 0))) <= 0:
+        if not any(w in d.get("Kernel Name", "") for w in want) or int(float(d.get("launch__grid_size", 0))) <= 0:
             continue
         scale = {"Gbyte": 1e9, "Mbyte": 1e6, "byte": 1.0}
         rd = float(d["dram__bytes_read.sum"]) * scale.get(d.get("dram__bytes_read.sum [unit]", "Gbyte"), 1e9)
