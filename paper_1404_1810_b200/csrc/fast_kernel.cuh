@@ -233,34 +233,47 @@ __device__ __forceinline__ void chain_class(R* ch, int lam_c, int t, int r) {
   const int hi = (C::N >> (t + 1)) - lam_c;
   const int c0 = hi - rO;
   auto at = [&](int jj) -> R& { return ch[C::swz(c0 - jj * stride, lam_c)]; };
-  if (C::TM) {
-    // M1: cos asc/sub, sin desc/sub; M5: cos desc/add, sin asc/add
-    const bool addop = V == 5;
-    const bool desc = (V == 1) ? (lens == 1) : (lens == 0);
-    const int s0 = desc ? q - 1 : 0, d = desc ? -1 : 1;
-    R prev = A::mul(R(0.5), at(s0));
-    at(s0) = prev;
-    int p = s0;
-    for (int k = 1; k < q; ++k) {
-      p += d;
-      prev = addop ? A::add(at(p), prev) : A::sub(at(p), prev);
-      at(p) = prev;
+  // M1: cos asc/sub, sin desc/sub; M5: cos desc/add, sin asc/add (AM_B);
+  // M3: cos desc/sub, sin asc/sub; M7: cos asc/add, sin desc/add (AM_F)
+  const bool addop = C::TM ? (V == 5) : (V == 7);
+  const bool desc = C::TM ? ((V == 1) ? (lens == 1) : (lens == 0)) : ((V == 3) ? (lens == 0) : (lens == 1));
+  const int s0 = desc ? q - 1 : 0, d = desc ? -1 : 1;
+  // The recurrence runs in the reference's serial order (bitwise); the
+  // operands stream through registers a run of KC at a time (independent
+  // loads issued together), so each step costs one dependent add instead of
+  // a shared-memory round trip.
+  constexpr int KC = 8;
+  R prev = R(0);
+  auto step = [&](R& v, int k) {
+    if (C::TM) {            // y_0 = C_0 / 2, y_k = C_k -/+ y_(k-1)
+      prev = k == 0 ? A::mul(R(0.5), v) : (addop ? A::add(v, prev) : A::sub(v, prev));
+      v = prev;
+    } else if (k == 0) {    // y_0 = C_0, y_k = C_k -/+ y_(k-1), the last one halved
+      prev = v;
+    } else {
+      const R y = addop ? A::add(v, prev) : A::sub(v, prev);
+      v = k == q - 1 ? A::mul(R(0.5), y) : y;
+      prev = y;
+    }
+  };
+  if (q >= KC) {            // q is a power of two: whole runs, no predicates
+#pragma unroll 1
+    for (int k0 = 0; k0 < q; k0 += KC) {
+      R v[KC];
+#pragma unroll
+      for (int i = 0; i < KC; ++i) v[i] = at(s0 + (k0 + i) * d);
+#pragma unroll
+      for (int i = 0; i < KC; ++i) step(v[i], k0 + i);
+#pragma unroll
+      for (int i = 0; i < KC; ++i) at(s0 + (k0 + i) * d) = v[i];
     }
   } else {
-    // M3: cos desc/sub, sin asc/sub; M7: cos asc/add, sin desc/add
-    const bool addop = V == 7;
-    const bool desc = (V == 3) ? (lens == 0) : (lens == 1);
-    const int s0 = desc ? q - 1 : 0, d = desc ? -1 : 1;
-    R prev = at(s0);
-    int p = s0;
-    for (int k = 1; k < q - 1; ++k) {
-      p += d;
-      prev = addop ? A::add(at(p), prev) : A::sub(at(p), prev);
-      at(p) = prev;
+#pragma unroll 1
+    for (int k = 0; k < q; ++k) {
+      R v = at(s0 + k * d);
+      step(v, k);
+      at(s0 + k * d) = v;
     }
-    p += d;
-    const R tt = addop ? A::add(at(p), prev) : A::sub(at(p), prev);
-    at(p) = A::mul(R(0.5), tt);
   }
 }
 
