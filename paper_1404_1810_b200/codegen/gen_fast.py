@@ -1,5 +1,5 @@
 #!/usr/bin/env python3
-"""Generates csrc/fast_gen.cuh: straight-line per-thread code for the
+"""Generates csrc/gen/fast_gen.cuh (at build time, csrc/Makefile): straight-line per-thread code for the
 bottom of the AM-QFT recursion (see tests/fast_model.py for the proven
 formulation and csrc/fast.cu for the kernel that calls these functions).
 
@@ -20,7 +20,7 @@ Every emitted operation is one of the reference's add/sub/mul on the
 reference's operands (AR::add/sub/mul = __fadd_rn/__dadd_rn..., never
 contracted), so the fp64 instantiation is bitwise the reference recursion.
 
-  python3 paper_1404_1810_b200/codegen/gen_fast.py > paper_1404_1810_b200/csrc/fast_gen.cuh
+  python3 paper_1404_1810_b200/codegen/gen_fast.py > paper_1404_1810_b200/csrc/gen/fast_gen.cuh
 """
 from __future__ import annotations
 

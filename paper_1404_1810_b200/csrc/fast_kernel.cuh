@@ -39,7 +39,7 @@
 // The fused kernel reads the AM constant table from its parameter space:
 // the generated code's compile-time slots become constant-bank operands.
 #define AMQFT_TABLD(t, i) ((t)[i])
-#include "fast_gen.cuh"
+#include "gen/fast_gen.cuh"   // generated at build time by codegen/gen_fast.py
 #include "generic.cuh"
 #include "trig.hpp"
 

@@ -17,7 +17,21 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB = os.path.join(HERE, "native", "libgen_host.so")
 SRC = os.path.join(HERE, "native", "gen_host.cpp")
-GEN = os.path.join(os.path.dirname(HERE), "paper_1404_1810_b200", "csrc", "fast_gen.cuh")
+GEN = os.path.join(os.path.dirname(HERE), "paper_1404_1810_b200", "csrc", "gen", "fast_gen.cuh")
+GEN_PY = os.path.join(os.path.dirname(HERE), "paper_1404_1810_b200", "codegen", "gen_fast.py")
+
+
+def ensure_generated():
+    """The generated header normally comes from the library build; make it
+    here when the CPU tests run on a tree that was never built."""
+    if not os.path.exists(GEN) or os.path.getmtime(GEN) < os.path.getmtime(GEN_PY):
+        import subprocess
+        import sys
+        os.makedirs(os.path.dirname(GEN), exist_ok=True)
+        out = subprocess.run([sys.executable, GEN_PY], check=True, capture_output=True, text=True).stdout
+        with open(GEN + ".tmp", "w") as f:
+            f.write(out)
+        os.replace(GEN + ".tmp", GEN)
 
 _lib = None
 
@@ -25,6 +39,7 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
+        ensure_generated()
         if (not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(GEN)
                 or os.path.getmtime(LIB) < os.path.getmtime(SRC)):
             import subprocess

@@ -1,11 +1,11 @@
 // gen_host.cpp -- TEST HARNESS: compiles the generated device code
-// (paper_1404_1810_b200/csrc/fast_gen.cuh) as host C++ so the CPU test
+// (paper_1404_1810_b200/csrc/gen/fast_gen.cuh, generated at build time) as host C++ so the CPU test
 // suite can check every generated function against the fast-kernel model
 // (tests/fast_model.py) without a GPU.  fp64, -ffp-contract=off.
 #define __device__
 #define __forceinline__ inline
 #define __ldg(p) (*(p))
-#include "../../paper_1404_1810_b200/csrc/fast_gen.cuh"
+#include "../../paper_1404_1810_b200/csrc/gen/fast_gen.cuh"
 
 namespace {
 struct HA {

@@ -3,7 +3,7 @@
 * tests/fast_model.py -- recursive and phase-structured numpy models of the
   index-space formulation, bitwise against the oracle.
 * tests/kernel_emu.py -- the kernel's phases with the generated straight-
-  line functions (csrc/fast_gen.cuh compiled as host C++), bitwise.
+  line functions (csrc/gen/fast_gen.cuh, generated at build time, compiled as host C++), bitwise.
 """
 import pytest
 

@@ -1,5 +1,5 @@
 // bank_model.cpp -- DIAGNOSTIC: shared-memory bank model of the fast
-// kernel's generated phases.  Compiles fast_gen.cuh as host C++ with a
+// kernel's generated phases.  Compiles gen/fast_gen.cuh (build-time generated) as host C++ with a
 // tracking value type: every read/write of a shared-buffer cell is logged
 // per thread; threads are grouped into warps exactly as k_fast maps them,
 // and each memory instruction (k-th access of the straight-line code) is
@@ -40,7 +40,7 @@ struct TA {
   static TR mul(TR a, TR b) { return TR(a.v * b.v); }
 };
 
-#include "../paper_1404_1810_b200/csrc/fast_gen.cuh"
+#include "../paper_1404_1810_b200/csrc/gen/fast_gen.cuh"
 using namespace amqft_b200;
 
 static int V_, LOGN, N, H, LB = 64, LOGLB = 6, LT, HP, NSEG, CS, SINE;
