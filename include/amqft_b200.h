@@ -220,6 +220,25 @@ amqft_status amqft_direct_bins(const void* d_x, int dtype, size_t rows, size_t r
 amqft_status amqft_direct_bins_extended(const double* x, size_t n, const uint64_t* bins, size_t nbins,
                                         int reverse, double* out);
 
+/* ---- Distributed four-step plan (config 5): one plan per rank, owning its
+ * NCCL communicator (NCCL is loaded at run time).  n = n1 n2; rank p passes
+ * its column slab [n2/P][2 n1] (x[n2 i1 + i2] for i2 in its slab, interleaved
+ * fp32; overwritten) and receives [n1/P][2 n2] = X[k1 + n1 k2] for its
+ * k1-slab.  The exchange is grouped ncclSend / ncclRecv on `stream`
+ * (AMQFT_ENCCL on NCCL failures).  amqft_dist_unique_id (rank 0) makes the
+ * id every rank passes to amqft_dist_plan_create (the caller broadcasts
+ * it); id128 may be NULL for nparts = 1 (no communicator, no exchange).
+ * Replaces nothing in the reference (it is single-process,
+ * src/variants.cpp:404). */
+typedef struct amqft_dist_plan_s* amqft_dist_plan;
+amqft_status amqft_dist_unique_id(void* id128);
+amqft_status amqft_dist_plan_create(amqft_dist_plan* out, int variant, size_t n, int nparts, int rank,
+                                    int device, int trig_mode, const void* id128);
+amqft_status amqft_dist_plan_shape(amqft_dist_plan plan, size_t* n1, size_t* n2, size_t* rows_in,
+                                   size_t* rows_out);
+amqft_status amqft_dist_exec_forward(amqft_dist_plan plan, void* d_in, void* d_out, void* stream);
+amqft_status amqft_dist_plan_destroy(amqft_dist_plan plan);
+
 /* Batched transpose of complex fp32 matrices: mats x [r][c] -> [c][r];
  * r and c multiples of 32. */
 amqft_status amqft_transpose_c64(const void* d_in, void* d_out, size_t mats, size_t r,

@@ -78,6 +78,11 @@ def lib() -> C.CDLL:
     L.amqft_plan_create_with_constants.argtypes = [C.POINTER(vp), C.POINTER(PlanDesc), vp, sz]
     L.amqft_direct_bins.argtypes = [vp, C.c_int, sz, sz, sz, sz, sz, vp, sz, vp, vp]
     L.amqft_direct_bins_extended.argtypes = [vp, sz, vp, sz, C.c_int, vp]
+    L.amqft_dist_unique_id.argtypes = [vp]
+    L.amqft_dist_plan_create.argtypes = [C.POINTER(vp), C.c_int, sz, C.c_int, C.c_int, C.c_int, C.c_int, vp]
+    L.amqft_dist_plan_shape.argtypes = [vp, C.POINTER(sz), C.POINTER(sz), C.POINTER(sz), C.POINTER(sz)]
+    L.amqft_dist_exec_forward.argtypes = [vp, vp, vp, vp]
+    L.amqft_dist_plan_destroy.argtypes = [vp]
     L.amqft_plan_op_counts.argtypes = [vp, vp]
     L.amqft_plan_path.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
     L.amqft_plan_fourstep_factors.argtypes = [vp, C.POINTER(sz)]
@@ -90,7 +95,9 @@ def lib() -> C.CDLL:
     for name in ("amqft_plan_create", "amqft_plan_destroy", "amqft_exec_forward",
                  "amqft_exec_inverse", "amqft_exec_rows", "amqft_exec_host_rows", "amqft_execute_host",
                  "amqft_execute_host_constants", "amqft_execute_host_inverse", "amqft_plan_create_with_constants",
-                 "amqft_direct_bins", "amqft_direct_bins_extended",
+                 "amqft_direct_bins", "amqft_direct_bins_extended", "amqft_dist_unique_id",
+                 "amqft_dist_plan_create", "amqft_dist_plan_shape", "amqft_dist_exec_forward",
+                 "amqft_dist_plan_destroy",
                  "amqft_dist_twiddle_scatter", "amqft_transpose_c64", "amqft_plan_transposed_factor",
                  "amqft_exec_rows_transposed", "amqft_dist_twiddle_scatter_t",
                  "amqft_plan_op_counts", "amqft_plan_path", "amqft_plan_fourstep_factors", "amqft_plan_dump",

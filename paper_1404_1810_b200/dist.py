@@ -257,3 +257,49 @@ class DistFourStep:
         else:
             recv = send   # one part: the scatter already produced the layout
         return self.stage2(recv, b, z, stream)
+
+
+class DistPlan:
+    """The distributed four-step behind the C ABI (amqft_dist_*, csrc/dist.cpp):
+    one plan per rank owning its NCCL communicator, the same slab layouts as
+    DistFourStep.  Rank 0 makes the NCCL unique id; it reaches the other ranks
+    over the torch.distributed group (any backend).  With one rank and
+    use_nccl=False there is no communicator."""
+
+    def __init__(self, variant: int, n: int, *, device: int = 0, trig_mode=TrigMode.Precomputed, group=None,
+                 world: int | None = None, rank: int | None = None, use_nccl: bool = True):
+        self.world = world if world is not None else (dist.get_world_size(group) if dist.is_initialized() else 1)
+        self.rank = rank if rank is not None else (dist.get_rank(group) if dist.is_initialized() else 0)
+        uid = None
+        if use_nccl or self.world > 1:
+            buf = (C.c_ubyte * 128)()
+            if self.rank == 0:
+                check(lib().amqft_dist_unique_id(buf))
+            if self.world > 1:
+                t = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
+                obj = [t]
+                dist.broadcast_object_list(obj, src=0, group=group)
+                buf = (C.c_ubyte * 128)(*obj[0].tolist())
+            uid = buf
+        self._h = C.c_void_p()
+        check(lib().amqft_dist_plan_create(C.byref(self._h), int(variant), int(n), int(self.world), int(self.rank),
+                                           int(device), int(trig_mode), uid))
+        a, b, c, d = C.c_size_t(), C.c_size_t(), C.c_size_t(), C.c_size_t()
+        check(lib().amqft_dist_plan_shape(self._h, C.byref(a), C.byref(b), C.byref(c), C.byref(d)))
+        self.n, self.n1, self.n2, self.rows_in, self.rows_out = int(n), a.value, b.value, c.value, d.value
+
+    def forward(self, slab, out, stream=None):
+        """slab: [n2/P][2 n1] fp32 (overwritten); out: [n1/P][2 n2]."""
+        check(lib().amqft_dist_exec_forward(self._h, int(slab.data_ptr()), int(out.data_ptr()), Plan._stream(stream)))
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            lib().amqft_dist_plan_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

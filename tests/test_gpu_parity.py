@@ -930,3 +930,26 @@ def test_fp32_sine_variants_large_n(oracle, restatement, lg):
             ex = amqft.Plan(v, amqft.FunctionId.Cdft, n, 1, dtype="f32", order=amqft.Order.Exact)
             got = run_plan(ex, [x])[0]
             assert r.rel_l2(got, r.execute(v, O.F_CDFT, n, x)) <= tol, v
+
+
+def test_dist_plan_c_abi_world1_nccl():
+    """The C-ABI distributed plan (csrc/dist.cpp) with a one-rank NCCL
+    communicator (the exchange is a grouped send/recv to itself): the same
+    output as DistFourStep and numpy's FFT at N = 2^20."""
+    from paper_1404_1810_b200.dist import DistFourStep, DistPlan
+    n = 1 << 20
+    p = DistPlan(4, n, device=0, world=1, rank=0, use_nccl=True)
+    d = DistFourStep(4, n, device=0, world=1, rank=0)
+    assert (p.n1, p.n2) == (d.n1, d.n2)
+    g = torch.Generator(device=DEV).manual_seed(20)
+    x = torch.randn(2 * n, generator=g, device=DEV)
+    slab = d.local_input(x)
+    out = torch.empty(p.rows_out, 2 * p.n2, device=DEV)
+    p.forward(slab.clone(), out)
+    z = d.forward(slab.clone())
+    torch.cuda.synchronize()
+    assert torch.equal(out, z)
+    got = d.global_output([out.cpu().numpy()])
+    ref = numpy_dft(x.double().cpu().numpy())
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 1e-5 * 20
+    p.close()

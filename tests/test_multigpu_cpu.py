@@ -178,3 +178,15 @@ def test_dist_split_and_layout_helpers():
         k1, k2 = d.n1 - 1, 7
         src = parts[k1 // d.w].reshape(d.w, d.n2, 2)[k1 % d.w, k2]
         assert X[2 * (k1 + d.n1 * k2)] == src[0]
+
+
+def test_dist_plan_c_abi_rejects_bad_requests():
+    """amqft_dist_plan_create validates before touching a device or NCCL."""
+    import ctypes as C
+    from paper_1404_1810_b200 import _native
+    L = _native.lib()
+    h = C.c_void_p()
+    for args in ((4, 1 << 20, 0, 0), (4, 1 << 20, 2, 2), (4, 3 << 20, 1, 0), (4, 1 << 20, 2, 0)):
+        v, n, parts, rank = args
+        s = L.amqft_dist_plan_create(C.byref(h), v, n, parts, rank, 0, 0, None)
+        assert s == _native.EINVAL, args
