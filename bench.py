@@ -483,6 +483,13 @@ def bench_single(args, world, rank, local):
         # every launch reads and writes the whole signal once
         extra = {"hbm_passes": launches, "traffic_model_bytes": launches * 16 * n,
                  "factors": [fa, fb, fc]}
+        try:   # measured DRAM bytes per step (ncu, profiles/r02_ncu_c4_passes.json)
+            prof = json.load(open(os.path.join(ROOT, "profiles", "r02_ncu_c4_passes.json")))
+            if args.variant == 4 and len(prof["launches"]) == launches:
+                extra["traffic_step_bytes"] = prof["step_dram_bytes"]
+                extra["traffic_source"] = "profiles/r02_ncu_c4_passes.json"
+        except (OSError, ValueError, KeyError):
+            pass
         if rank == 0:
             extra["accuracy"] = config4_accuracy(amqft, x, n, local, stream, args)
         cpu = cpu_baseline_large(args.variant, n, 1 << 20) if (rank == 0 and not args.no_cpu_baseline) else None
@@ -530,7 +537,7 @@ def bench_single(args, world, rank, local):
             "config": {"workload": workload, "n": n, "variant": args.variant, "path": path,
                        "l2": "inputs >= 128 MiB > 126 MB L2; no flush"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": None, "peak_source": hbm_src,
+                         "frac": achieved / hbm, "traffic": extra.get("traffic_step_bytes"), "peak_source": hbm_src,
                          "algorithmic_bytes_per_gpu": per_gpu_bytes},
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches * args.steps if launches is not None else None,   # inside the timed region
