@@ -404,12 +404,15 @@ def gen_hmS(v, HP, LB, lam):
 
 
 # ------------------------------------------------------------- top levels
-def gen_top(LB, LT, direction, lam, sine, nlog):
+def gen_top(LB, LT, direction, lam, sine, nlog, kmode=None, collect=None):
     """Mirror levels 1..LT of one chain for the thread owning offset v in
     [1, LB): cells z_2k = kW + v, z_2k+1 = (k+1)W - v (W = 2 LB), closed
     under every top level.  direction 'fwd' = time-major forward fold,
     'bwd' = harmonic-major backward butterfly (levels LT..1).  Table size
-    nmax = N = 2^nlog (compile time).  Skewed addresses:
+    nmax = N = 2^nlog (compile time).  kmode "tm": the constants come from
+    the register array kk (filled from tensor memory, top_cols order)
+    instead of the per-level table; collect: a set receiving the (level,
+    offset, expression) keys.  Skewed addresses:
     PH(kW+v) = v + k(W+2), PH((k+1)W-v) = (k+1)(W+2) - v - 1."""
     W = 2 * LB
     K = 1 << (LT - 1)          # cells per parity
@@ -449,8 +452,11 @@ def gen_top(LB, LT, direction, lam, sine, nlog):
         sc = nmax >> lg2L
         # per-level compacted table: ltab[off_i + u] = f(pi u / L), u < L/2
         off_i = sum((H >> (j - 1)) // 2 for j in range(1, i))
-        em.emit(f"{{ const R* __restrict__ tp = ltab + {off_i} + v;")
-        em.emit(f"  const R* __restrict__ tm = ltab + {off_i} - v;")
+        if kmode == "tm":
+            em.emit("{")
+        else:
+            em.emit(f"{{ const R* __restrict__ tp = ltab + {off_i} + v;")
+            em.emit(f"  const R* __restrict__ tm = ltab + {off_i} - v;")
         done = set()
         for z in range(2 * K):
             if z in done:
@@ -480,6 +486,10 @@ def gen_top(LB, LT, direction, lam, sine, nlog):
             kexpr = f"__ldg({'tp' if lsg > 0 else 'tm'} + {u0})"
             if u0 == 0 and lsg > 0 and i == LT:
                 kexpr = f"(v == {LB // 2} ? base : {kexpr})"
+            if collect is not None:
+                collect.add((i, off_i, kexpr))
+            if kmode == "tm":
+                kexpr = f"kk[{top_cols(LB, LT, nlog).index((i, off_i, kexpr))}]"
             p_, q_ = x[jc], x[mcz]
             em.tmp += 1
             t = em.tmp
@@ -502,10 +512,45 @@ def gen_top(LB, LT, direction, lam, sine, nlog):
     for z in range(2 * K):
         b_, o_ = addr(z)
         em.emit(f"{b_}[{o_}] = x{z};")
+    if kmode == "tm":
+        sig = (f"template <typename R, typename AR>\n__device__ __forceinline__ void "
+               f"top_{direction}_lb{LB}_lt{LT}_n{nlog}_l{lam}_s{sine}_tm(R* __restrict__ B, int v, "
+               f"const R* kk)")
+        return sig + " {\n" + "\n".join(em.lines) + "\n}\n"
     sig = (f"template <typename R, typename AR>\n__device__ __forceinline__ void "
            f"top_{direction}_lb{LB}_lt{LT}_n{nlog}_l{lam}_s{sine}(R* __restrict__ B, int v, "
            f"const R* __restrict__ ltab, R base)")
     return sig + " {\n" + "\n".join(em.lines) + "\n}\n"
+
+
+_TOP_COLS = {}
+
+
+def top_cols(LB, LT, nlog):
+    """The distinct top-level constants of one thread, in column order:
+    (level, per-level table offset, expression).  They depend on v only
+    (not on the chain, lens or direction), so one fill serves every top."""
+    key = (LB, LT, nlog)
+    if key not in _TOP_COLS:
+        keys = set()
+        for direction in ("fwd", "bwd"):
+            for lam in (0, 1):
+                for sine in (0, 1):
+                    gen_top(LB, LT, direction, lam, sine, nlog, collect=keys)
+        _TOP_COLS[key] = sorted(keys)
+    return _TOP_COLS[key]
+
+
+def gen_top_fill(LB, LT, nlog):
+    """Evaluates the top_cols constants for offset v (the tensor-memory
+    fill, once per kernel); out[j] = column j."""
+    lines = []
+    for j, (i, off_i, kexpr) in enumerate(top_cols(LB, LT, nlog)):
+        lines.append(f"  {{ const R* __restrict__ tp = ltab + {off_i} + v; const R* __restrict__ tm = ltab + {off_i} - v; "
+                     f"(void)tp; (void)tm; out[{j}] = {kexpr}; }}")
+    sig = (f"template <typename R>\n__device__ __forceinline__ void "
+           f"top_fill_lb{LB}_lt{LT}_n{nlog}(R* out, int v, const R* __restrict__ ltab, R base)")
+    return sig + " {\n" + "\n".join(lines) + "\n}\n"
 
 
 def scaled_mnet(em, y, HP, lam, sine, direction, nlog, LB):
@@ -927,6 +972,8 @@ def main():
             for lam in (0, 1):
                 for sine in (0, 1):
                     out.append(gen_top(LB, LT, direction, lam, sine, nlog))
+                    out.append(gen_top(LB, LT, direction, lam, sine, nlog, kmode="tm"))
+        out.append(gen_top_fill(LB, LT, nlog))
         HP = 1 << LT
         for v in range(1, 9):
             for lam in (0, 1):
@@ -977,12 +1024,22 @@ def main():
         LT = nlog - 1 - (LB.bit_length() - 1)
         for sine in (0, 1):
             out.append(f"template <> struct Top<{LB}, {LT}, {nlog}, {sine}> {{")
+            out.append(f"  static constexpr int NK = {len(top_cols(LB, LT, nlog))};   // distinct constants per thread")
             for direction in ("fwd", "bwd"):
                 out.append("  template <typename R, typename AR>")
                 out.append(f"  static __device__ __forceinline__ void {direction}(int lam, R* B, int v, const R* ltab, R base) {{")
                 out.append(f"    if (lam == 0) gen::top_{direction}_lb{LB}_lt{LT}_n{nlog}_l0_s{sine}<R, AR>(B, v, ltab, base);")
                 out.append(f"    else gen::top_{direction}_lb{LB}_lt{LT}_n{nlog}_l1_s{sine}<R, AR>(B, v, ltab, base);")
                 out.append("  }")
+                out.append("  template <typename R, typename AR>")
+                out.append(f"  static __device__ __forceinline__ void {direction}_k(int lam, R* B, int v, const R* kk) {{")
+                out.append(f"    if (lam == 0) gen::top_{direction}_lb{LB}_lt{LT}_n{nlog}_l0_s{sine}_tm<R, AR>(B, v, kk);")
+                out.append(f"    else gen::top_{direction}_lb{LB}_lt{LT}_n{nlog}_l1_s{sine}_tm<R, AR>(B, v, kk);")
+                out.append("  }")
+            out.append("  template <typename R>")
+            out.append("  static __device__ __forceinline__ void fill(R* out, int v, const R* ltab, R base) {")
+            out.append(f"    gen::top_fill_lb{LB}_lt{LT}_n{nlog}<R>(out, v, ltab, base);")
+            out.append("  }")
             out.append("};")
     out.append("template <int V, int HP, int NLOG> struct SmallPar;")
     for LB, nlog in FULL_SIZES:

@@ -126,6 +126,11 @@ struct Cfg {
   // (re-associated; for the fp64-compute instance the difference to the
   // serial order is fp64 rounding, far below the fp32 output rounding).
   static constexpr bool SERIAL = CHAIN && sizeof(R) == 8 && std::is_same<IO, R>::value;
+  // top-level constants in tensor memory (fp32 instances, see tmem_ld)
+#ifndef AMQFT_TOP_TMEM
+#define AMQFT_TOP_TMEM 1
+#endif
+  static constexpr bool TOP_TMEM = AMQFT_TOP_TMEM && sizeof(R) == 4;
   // T, F (4 chains each) + the TMA staging buffer for the next row + mbarrier
   static constexpr size_t STAGE_OFF = 8 * CS * sizeof(R);
   // + mbarriers: the TMA stage (P == 1) / prefetch, staging-full, staging-free (P > 1)
@@ -648,6 +653,58 @@ __device__ __forceinline__ void bulk_wait_read_all() {   // smem source reusable
 __device__ __forceinline__ void bulk_wait_all() {        // global writes complete
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
+
+// ---- Tensor memory holds the top levels' constants (fp32 instances).
+// Each top thread needs Top::NK distinct constants f(pi (u0 +- v) / L) that
+// depend on its offset v only, the same for every row it processes; a
+// warp's tcgen05.ld reads its TMEM lane quadrant (warp % 4), and every warp
+// of a quadrant has the same v range (v = 32 (warp & 1) + lane), so one copy
+// per quadrant, written once per kernel, serves every row.  The per-row
+// constant loads leave the L1 / shared-memory data path (on which the
+// kernel is bound) for tensor memory's own.
+constexpr uint32_t kTmemCols = 64;
+__device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// one warp: allocate kTmemCols columns, address to *dst (shared memory)
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+               ::"r"(smem_u32(dst)), "n"(kTmemCols) : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kTmemCols) : "memory");
+}
+#define AMQFT_R8(a, o) "=r"(a[o]), "=r"(a[o + 1]), "=r"(a[o + 2]), "=r"(a[o + 3]), "=r"(a[o + 4]), "=r"(a[o + 5]), \
+                       "=r"(a[o + 6]), "=r"(a[o + 7])
+#define AMQFT_W8(a, o) "r"(a[o]), "r"(a[o + 1]), "r"(a[o + 2]), "r"(a[o + 3]), "r"(a[o + 4]), "r"(a[o + 5]), \
+                       "r"(a[o + 6]), "r"(a[o + 7])
+// 32x32b shape: lane l of the warp reads / writes columns [col, col + K) of
+// TMEM lane 32 (warp % 4) + l (taddr carries lane << 16 | column)
+template <int K>
+__device__ __forceinline__ void tmem_ld(uint32_t taddr, uint32_t (&r)[K]) {
+  static_assert(K == 8 || K == 16 || K == 32 || K == 64, "TMEM load width");
+  if constexpr (K == 8) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : AMQFT_R8(r, 0) : "r"(taddr));
+  } else {
+#pragma unroll
+    for (int c = 0; c < K; c += 8)   // x8 pieces: 8 registers per instruction
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : AMQFT_R8(r, c) : "r"(taddr + static_cast<uint32_t>(c)));
+  }
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+template <int K>
+__device__ __forceinline__ void tmem_st(uint32_t taddr, const uint32_t (&r)[K]) {
+#pragma unroll
+  for (int c = 0; c < K; c += 8)
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                 ::"r"(taddr + static_cast<uint32_t>(c)), AMQFT_W8(r, c) : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+#undef AMQFT_R8
+#undef AMQFT_W8
+constexpr int pow2_at_least_8(int k) { return k <= 8 ? 8 : k <= 16 ? 16 : k <= 32 ? 32 : 64; }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
@@ -905,6 +962,40 @@ k_fast(const IO* __restrict__ in, IO* __restrict__ out, size_t rows_in,
       __syncthreads();
   };
   const R base = tab[nmax / 4 - 1];
+  // TMEM: the slot-0 barrier block's spare word holds the allocation address
+  using TopT = Top<C::LB, C::LT, LOGN, C::SINE>;
+  constexpr int NKP = pow2_at_least_8(TopT::NK);
+  uint32_t tbase = 0;
+  if constexpr (C::TOP_TMEM) {
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(smraw + C::STAGE_OFF + 2 * C::N * sizeof(IO) + 8);
+    if (threadIdx.x < 32) tmem_alloc(tslot);
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    tbase = *tslot;
+    if (threadIdx.x < 128) {   // warp q fills quadrant q: v = 32 (q & 1) + lane
+      const int v = 32 * ((threadIdx.x >> 5) & 1) + (threadIdx.x & 31);
+      float kf[NKP];
+#pragma unroll
+      for (int j = 0; j < NKP; ++j) kf[j] = 0.0f;
+      TopT::template fill<float>(kf, v, reinterpret_cast<const float*>(ltab), static_cast<float>(base));
+      uint32_t kw[NKP];
+#pragma unroll
+      for (int j = 0; j < NKP; ++j) kw[j] = __float_as_uint(kf[j]);
+      tmem_st<NKP>(tbase + ((threadIdx.x & 96u) << 16), kw);
+    }
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+  }
+  // this warp's view of its quadrant's constants
+  auto top_consts = [&](float (&kk)[NKP]) {
+    uint32_t kw[NKP];
+    tmem_ld<NKP>(tbase + ((threadIdx.x & 96u) << 16), kw);
+#pragma unroll
+    for (int j = 0; j < NKP; ++j) kk[j] = __uint_as_float(kw[j]);
+  };
+  (void)top_consts;
   constexpr int N = C::N, H = C::H;
   constexpr uint32_t ROW_BYTES = 2 * N * sizeof(IO);
   // load/store: 256 threads, cells tid + 256 it; address steps per it
@@ -1062,7 +1153,13 @@ k_fast(const IO* __restrict__ in, IO* __restrict__ out, size_t rows_in,
       // top mirror levels (generated, 2^LT cells per thread) || small chains
       if (act && tid < 4 * C::LB) {
         const int c = tid >> LOGLB, v = tid & (C::LB - 1);
-        if (v > 0) Top<C::LB, C::LT, LOGN, C::SINE>::template fwd<R, A>(c & 1, Tb + C::coT(c), v, ltab, base);
+        if constexpr (C::TOP_TMEM) {
+          float kk[NKP];
+          top_consts(kk);   // the whole warp (tcgen05.ld is warp-collective)
+          if (v > 0) TopT::template fwd_k<R, A>(c & 1, Tb + C::coT(c), v, reinterpret_cast<const R*>(kk));
+        } else if (v > 0) {
+          TopT::template fwd<R, A>(c & 1, Tb + C::coT(c), v, ltab, base);
+        }
       }
     } else {
       // chain folds n = N .. 2N/LB (generated sets, cooperative k = 0 class)
@@ -1157,7 +1254,13 @@ k_fast(const IO* __restrict__ in, IO* __restrict__ out, size_t rows_in,
     } else {
       if (act && tid < 4 * C::LB) {
         const int c = tid >> LOGLB, v = tid & (C::LB - 1);
-        if (v > 0) Top<C::LB, C::LT, LOGN, C::SINE>::template bwd<R, A>(c & 1, Fb + C::coF(c), v, ltab, base);
+        if constexpr (C::TOP_TMEM) {
+          float kk[NKP];
+          top_consts(kk);
+          if (v > 0) TopT::template bwd_k<R, A>(c & 1, Fb + C::coF(c), v, reinterpret_cast<const R*>(kk));
+        } else if (v > 0) {
+          TopT::template bwd<R, A>(c & 1, Fb + C::coF(c), v, ltab, base);
+        }
       }
       WORK_MARK(4);
       row_sync();
@@ -1299,6 +1402,12 @@ k_fast(const IO* __restrict__ in, IO* __restrict__ out, size_t rows_in,
     PHASE_MARK(6);
   }
   if (BULK_ST && tid == 0) bulk_wait_all();   // smem must outlive the last bulk store
+  if constexpr (C::TOP_TMEM) {
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    if (threadIdx.x < 32) tmem_dealloc(tbase);
+  }
   if constexpr (P > 1) {   // no CTA leaves while a peer may still arrive on its barriers
     cluster_arrive();
     cluster_wait();
