@@ -10,6 +10,8 @@
 //   path 2  fused fast kernels (fast.cuh) for the CDFT hot path.
 //   path 3  four-step over the fused kernel (fourstep.cuh), large N, fp32.
 //   path 4  one thread per row (small_kernel.cuh), small CDFTs.
+//   path 6  four-step inside one CTA's shared memory (tile_kernel.cuh),
+//           fp32 CDFT N = 256 .. 4096, one pass over HBM.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -387,8 +389,12 @@ amqft_status create_plan(amqft_plan* out, const amqft_plan_desc* desc, const std
     }
     // Fast fused path where one exists for this request.
     if (desc->order == AMQFT_ORDER_FAST) {
-      P->fast = make_fast_plan(*desc, P->d_trig, P->nmax, P->d_trig64);
-      int fpath = 2;
+      int fpath = 6;
+      P->fast = make_tile_plan(*desc, P->d_trig, P->nmax);
+      if (!P->fast) {
+        P->fast = make_fast_plan(*desc, P->d_trig, P->nmax, P->d_trig64);
+        fpath = 2;
+      }
       OpCount small_ops{};
       if (!P->fast) {
         P->fast = make_small_plan(*desc, P->d_trig, P->nmax, &small_ops);
@@ -404,7 +410,10 @@ amqft_status create_plan(amqft_plan* out, const amqft_plan_desc* desc, const std
         P->c.fn = desc->function;
         P->c.n = n;
         P->c.cells = fn_cells(desc->function, n);
-        P->c.ops = fpath == 2 ? fast_op_counts(*desc) : fpath == 4 ? small_ops : fourstep_op_counts(*desc);
+        P->c.ops = fpath == 6   ? tile_op_counts(*desc)
+                   : fpath == 2 ? fast_op_counts(*desc)
+                   : fpath == 4 ? small_ops
+                                : fourstep_op_counts(*desc);
         P->launches = P->fast->launches;
         prepare_inverse(P.get(), host_tab);
         *out = P.release();
@@ -538,7 +547,7 @@ amqft_status amqft_exec_rows(amqft_plan P, const void* in, void* out, size_t row
   if (!in || !out) return set_err(AMQFT_EINVAL, "null data pointer");
   // the fused, four-step and small-CDFT kernels move rows with TMA bulk
   // copies and 16-byte vectors: their device buffers must be 16-byte aligned
-  if (P->path >= 2 && P->path <= 4 && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15u))
+  if (((P->path >= 2 && P->path <= 4) || P->path == 6) && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15u))
     return set_err(AMQFT_EINVAL, "device buffers of fast-order plans must be 16-byte aligned");
   try {
     ck(cudaSetDevice(P->d.device), "cudaSetDevice");

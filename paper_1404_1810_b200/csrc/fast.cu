@@ -112,6 +112,61 @@ std::unique_ptr<FastPlan> make_fast_plan(const amqft_plan_desc& d, const void* d
   return make_fast_typed<double>(d.variant, kind, d.n, d_trig, nmax, d.device);
 }
 
+namespace tilek {
+template <int V>
+std::unique_ptr<FastPlan> make_tile(size_t n, const void* tab, uint32_t nmax, int dev);
+// the split of tile_kernel.cuh make_tile: N1 (phase A) x N2 (phase B)
+static void tile_split(size_t n, size_t* n1, size_t* n2) {
+  int lg = 0;
+  for (size_t t = n; t > 1; t >>= 1) ++lg;
+  *n1 = size_t(1) << (lg / 2);
+  *n2 = n / *n1;
+}
+}  // namespace tilek
+
+bool tile_covers(const amqft_plan_desc& d) {
+  if (d.function != AMQFT_FN_CDFT || d.dtype != AMQFT_F32) return false;
+  if (d.n < 256 || d.n > 4096 || (d.n & (d.n - 1))) return false;
+  if (const char* e = std::getenv("AMQFT_AB_TILE"))
+    if (e[0] == 'n') return false;
+  return true;
+}
+
+std::unique_ptr<FastPlan> make_tile_plan(const amqft_plan_desc& d, const void* d_trig, uint32_t nmax) {
+  if (!tile_covers(d)) return nullptr;
+  using namespace tilek;
+  switch (d.variant) {
+    case 1: return make_tile<1>(d.n, d_trig, nmax, d.device);
+    case 2: return make_tile<2>(d.n, d_trig, nmax, d.device);
+    case 3: return make_tile<3>(d.n, d_trig, nmax, d.device);
+    case 4: return make_tile<4>(d.n, d_trig, nmax, d.device);
+    case 5: return make_tile<5>(d.n, d_trig, nmax, d.device);
+    case 6: return make_tile<6>(d.n, d_trig, nmax, d.device);
+    case 7: return make_tile<7>(d.n, d_trig, nmax, d.device);
+    case 8: return make_tile<8>(d.n, d_trig, nmax, d.device);
+  }
+  return nullptr;
+}
+
+namespace smallk {
+bool small_ops_n(int v, size_t n, bool f64, OpCount* o, int fn = AMQFT_FN_CDFT);
+}
+
+OpCount tile_op_counts(const amqft_plan_desc& d) {
+  // N2 sub-transforms of length N1 and N1 of length N2 (the reference DAG of
+  // each: the traced schedule's meter) plus one complex twiddle multiply
+  // per element (4 muls + 2 adds), as the four-step's accounting
+  size_t n1, n2;
+  tilek::tile_split(d.n, &n1, &n2);
+  OpCount c1, c2, c;
+  smallk::small_ops_n(d.variant, n1, false, &c1, AMQFT_FN_CDFT);
+  smallk::small_ops_n(d.variant, n2, false, &c2, AMQFT_FN_CDFT);
+  c.adds = n2 * c1.adds + n1 * c2.adds + 2 * d.n;
+  c.muls = n2 * c1.muls + n1 * c2.muls + 4 * d.n;
+  c.bt = n2 * c1.bt + n1 * c2.bt;
+  return c;
+}
+
 namespace smallk {
 template <int V, typename R>
 std::unique_ptr<FastPlan> make_small_sized(size_t n, const void* tab, uint32_t nmax, int dev);
@@ -120,7 +175,7 @@ std::unique_ptr<FastPlan> make_small_rdft(size_t n, const void* tab, uint32_t nm
 template <int V, typename R>
 std::unique_ptr<FastPlan> make_small_dctdst(int fn, size_t n, const void* tab, uint32_t nmax, int dev);
 
-bool small_ops_n(int v, size_t n, bool f64, OpCount* o, int fn = AMQFT_FN_CDFT) {
+bool small_ops_n(int v, size_t n, bool f64, OpCount* o, int fn) {
   for (const SmallOps& e : kSmallOps)
     if (e.v == v && e.fn == fn && (size_t(1) << e.logn) == n && e.f64 == static_cast<int>(f64)) {
       o->adds = e.a;

@@ -58,6 +58,15 @@ std::unique_ptr<FastPlan> make_fast_plan(const amqft_plan_desc& d,
                                          const void* d_trig64 = nullptr);
 OpCount fast_op_counts(const amqft_plan_desc& d);
 
+// In-shared-memory four-step (tile_kernel.cuh, path 6): fp32 CDFT rows,
+// N = 256 .. 4096, both factors one-thread-per-transform AM-QFTs (<= 64
+// points, stable in fp32 for all 8 variants), one pass over HBM.
+// AMQFT_AB_TILE=none disables it (A/B measurements against the fused
+// kernel, which keeps the whole length-N DAG).
+bool tile_covers(const amqft_plan_desc& d);
+std::unique_ptr<FastPlan> make_tile_plan(const amqft_plan_desc& d, const void* d_trig, uint32_t nmax);
+OpCount tile_op_counts(const amqft_plan_desc& d);
+
 // One-thread-per-row kernel for small CDFTs (small_kernel.cuh): fp32 N <= 64,
 // fp64 N <= 32.  nullptr when not covered; *ops receives the traced
 // schedule's op counts (= the reference meter).

@@ -1,0 +1,224 @@
+// tile_kernel.cuh -- four-step inside one CTA's shared memory (path 6).
+//
+// CDFT N = N1 N2 (fp32, N = 256 .. 4096, N1, N2 <= 64) in ONE pass over HBM:
+// both factors are one-thread-per-transform AM-QFTs kept in registers -- the
+// straight-line code codegen/gen_small.py traces from the plan compiler
+// (SmallGen<V, 0, LOGN, float>, every line one reference add/sub/mul,
+// variants.cpp:186-231 / elaborations.cpp), the same code k_small runs from
+// HBM rows.  Decimation in frequency, n = N2 n1 + n2, k = k1 + N1 k2:
+//   X[k1 + N1 k2] = sum_n2 w_N2^(n2 k2) [ w_N^(n2 k1) sum_n1 x[N2 n1 + n2] w_N1^(n1 k1) ]
+// phase A  thread = (row, n2): the N1 inputs x[N2 n1 + n2] straight from HBM
+//          (a warp's lanes take consecutive n2: every load instruction
+//          covers 256 contiguous bytes), AM-QFT of length N1 in registers,
+//          output k1 times w_N^(n2 k1) (host long double table, rounded once)
+//          into the padded tile P[k1][n2] in shared memory;
+// phase B  thread = (row, k1): row k1 of P (128-bit loads; the pitch of
+//          N2 + 2 complex values makes a quarter-warp hit 8 distinct bank
+//          groups), AM-QFT of length N2 in registers, output k2 straight to
+//          HBM at X[k1 + N1 k2] (lanes on consecutive k1: 256 contiguous
+//          bytes per store instruction).
+// Shared-memory traffic is one write and one read of the row (the fused
+// kernel of fast_kernel.cuh, which keeps the whole length-N DAG, makes six
+// such round trips and is bound by them); the arithmetic is the same within
+// 1 % (N2 ops(N1) + N1 ops(N2) + N twiddle multiplies vs ops(N)).  The AM-QFT
+// DAG is kept inside each factor, not across the split (the four-step's
+// convention, fourstep.cu), so the result is checked against the fp64 oracle
+// of the same variant within 1e-5 log2 N; sub-transforms of length <= 64 are
+// stable in fp32 for the sine-family variants 5-8 too (fast.cuh), so all 8
+// variants run in fp32.
+// The inverse is the swap trick, fused into phase A's loads and phase B's
+// stores.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <memory>
+#include <stdexcept>
+#include <vector>
+
+#include "fast.cuh"
+#include "generic.cuh"
+#include "small_kernel.cuh"
+
+namespace amqft_b200 {
+namespace tilek {
+
+using smallk::SmallGen;
+using smallk::TabP;
+
+template <int LG1, int LG2>
+struct TCfg {
+  static constexpr int N1 = 1 << LG1, N2 = 1 << LG2, N = N1 * N2;
+  static constexpr int LGM = LG1 > LG2 ? LG1 : LG2;
+  static constexpr int T = 64;                                   // threads per CTA
+  static constexpr int NMIN = N1 < N2 ? N1 : N2;
+  static constexpr int R = T / NMIN > 0 ? T / NMIN : 1;         // rows per tile
+  static constexpr int PITCH = N2 + 2;                           // complex values per P row
+  static constexpr int ROWP = N1 * PITCH;                        // complex values per tile row
+  static constexpr size_t SMEM = static_cast<size_t>(R) * ROWP * sizeof(float2);
+  static constexpr int NT1 = (N1 < 8 ? 8 : N1) / 4, NT2 = (N2 < 8 ? 8 : N2) / 4;
+  // CTAs per SM by registers: 64-point factors ~160, 32-point ~88, 16-point ~48
+  static constexpr int MINB = LGM >= 6 ? 6 : (LGM == 5 ? 10 : 16);
+};
+
+// phase A: chunk c = complex n1 = 2c, 2c+1 of column n2 (global), output
+// chunk c = k1 = 2c, 2c+1 times the twiddle, into P[k1][n2]
+template <int N2, int PITCH, bool INV>
+struct AIo {
+  const float2* __restrict__ gi;   // x + n2
+  float2* sp;                      // P + n2
+  const float2* __restrict__ tw;   // tw + n2: tw[k1 N2 + n2] = w_N^(n2 k1)
+  __device__ __forceinline__ void ld(int c, float& a, float& b, float& d, float& e) const {
+    const float2 u = __ldcs(gi + (2 * c) * N2), v = __ldcs(gi + (2 * c + 1) * N2);
+    if (INV) { a = u.y; b = u.x; d = v.y; e = v.x; }
+    else { a = u.x; b = u.y; d = v.x; e = v.y; }
+  }
+  __device__ __forceinline__ void st(int c, float a, float b, float d, float e) const {
+    if (c != 0) {   // k1 = 0: w = 1
+      const float2 w = __ldg(tw + (2 * c) * N2);
+      const float na = a * w.x - b * w.y, nb = a * w.y + b * w.x;
+      a = na;
+      b = nb;
+    }
+    const float2 w1 = __ldg(tw + (2 * c + 1) * N2);
+    const float nd = d * w1.x - e * w1.y, ne = d * w1.y + e * w1.x;
+    sp[(2 * c) * PITCH] = make_float2(a, b);
+    sp[(2 * c + 1) * PITCH] = make_float2(nd, ne);
+  }
+};
+
+// phase B: chunk c = P[k1][2c, 2c+1] (one 128-bit load), output chunk c =
+// k2 = 2c, 2c+1 at X[k1 + N1 k2]
+template <int N1, bool INV>
+struct BIo {
+  const float4* sp;   // P + k1 PITCH (16-byte aligned: PITCH is even)
+  float2* __restrict__ go;   // X + k1
+  float scale;
+  __device__ __forceinline__ void ld(int c, float& a, float& b, float& d, float& e) const {
+    const float4 v = sp[c];
+    a = v.x; b = v.y; d = v.z; e = v.w;
+  }
+  __device__ __forceinline__ void st(int c, float a, float b, float d, float e) const {
+    if (INV) {
+      __stcs(go + (2 * c) * N1, make_float2(b * scale, a * scale));
+      __stcs(go + (2 * c + 1) * N1, make_float2(e * scale, d * scale));
+    } else {
+      __stcs(go + (2 * c) * N1, make_float2(a, b));
+      __stcs(go + (2 * c + 1) * N1, make_float2(d, e));
+    }
+  }
+};
+
+template <int V, int LG1, int LG2, bool INV>
+__global__ void __launch_bounds__(TCfg<LG1, LG2>::T, TCfg<LG1, LG2>::MINB)
+k_tile(const float* __restrict__ in, float* __restrict__ out, size_t rows,
+       const __grid_constant__ TabP<float, TCfg<LG1, LG2>::NT1> t1,
+       const __grid_constant__ TabP<float, TCfg<LG1, LG2>::NT2> t2, const float2* __restrict__ tw, float scale) {
+  using C = TCfg<LG1, LG2>;
+  using G1 = SmallGen<V, 0, LG1, float>;
+  using G2 = SmallGen<V, 0, LG2, float>;
+  constexpr int N1 = C::N1, N2 = C::N2, N = C::N;
+  extern __shared__ __align__(128) unsigned char sm[];
+  float2* P = reinterpret_cast<float2*>(sm);
+  const int tid = threadIdx.x;
+  const size_t tiles = (rows + C::R - 1) / C::R;
+  for (size_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const size_t row0 = tile * C::R;
+    // ---- phase A: columns of x -> P (twiddled)
+#pragma unroll 1
+    for (int i = tid; i < C::R * N2; i += C::T) {
+      const int r = i / N2, n2 = i % N2;
+      if (row0 + r < rows) {
+        AIo<N2, C::PITCH, INV> io{reinterpret_cast<const float2*>(in) + (row0 + r) * N + n2, P + r * C::ROWP + n2,
+                                  tw + n2};
+        G1::template run<Arith<float>>(io, t1.v);
+      }
+    }
+    __syncthreads();
+    // ---- phase B: rows of P -> X
+#pragma unroll 1
+    for (int j = tid; j < C::R * N1; j += C::T) {
+      const int r = j / N1, k1 = j % N1;
+      if (row0 + r < rows) {
+        BIo<N1, INV> io{reinterpret_cast<const float4*>(P + r * C::ROWP + k1 * C::PITCH),
+                        reinterpret_cast<float2*>(out) + (row0 + r) * N + k1, scale};
+        G2::template run<Arith<float>>(io, t2.v);
+      }
+    }
+    __syncthreads();   // P is rewritten by the next tile's phase A
+  }
+}
+
+template <int V, int LG1, int LG2>
+class TilePlanImpl final : public FastPlan {
+  using C = TCfg<LG1, LG2>;
+
+ public:
+  TilePlanImpl(const void* tab, uint32_t nmax, int device) {
+    check_(smallk::fetch_table(t1_.v, C::NT1, tab, nmax));
+    check_(smallk::fetch_table(t2_.v, C::NT2, tab, nmax));
+    // tw[k1 N2 + n2] = w_N^(n2 k1), long double rounded once
+    std::vector<float2> tw(C::N);
+    const long double two_pi = 6.283185307179586476925286766559005768L;
+    for (int k1 = 0; k1 < C::N1; ++k1)
+      for (int n2 = 0; n2 < C::N2; ++n2) {
+        const long double a = two_pi * static_cast<long double>((k1 * n2) % C::N) / static_cast<long double>(C::N);
+        tw[k1 * C::N2 + n2] = float2{static_cast<float>(cosl(a)), static_cast<float>(-sinl(a))};
+      }
+    check_(cudaMalloc(&tw_, tw.size() * sizeof(float2)));
+    check_(cudaMemcpy(tw_, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice));
+    auto f0 = k_tile<V, LG1, LG2, false>;
+    auto f1 = k_tile<V, LG1, LG2, true>;
+    check_(cudaFuncSetAttribute(f0, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM)));
+    check_(cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM)));
+    int per_sm = 0;
+    check_(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f0, C::T, C::SMEM));
+    if (per_sm < 1) throw std::runtime_error("tile four-step kernel does not fit an SM");
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    grid_cap_ = per_sm * sms;
+    launches = 1;
+  }
+  ~TilePlanImpl() override {
+    if (tw_) cudaFree(tw_);
+  }
+  void exec(const void* in, void* out, size_t rows, int inverse, cudaStream_t st) override {
+    const size_t tiles = (rows + C::R - 1) / C::R;
+    const unsigned grid = static_cast<unsigned>(std::min<size_t>(tiles, static_cast<size_t>(grid_cap_)));
+    const float scale = 1.0f / static_cast<float>(C::N);
+    if (inverse)
+      k_tile<V, LG1, LG2, true><<<grid, C::T, C::SMEM, st>>>(static_cast<const float*>(in), static_cast<float*>(out),
+                                                             rows, t1_, t2_, tw_, scale);
+    else
+      k_tile<V, LG1, LG2, false><<<grid, C::T, C::SMEM, st>>>(static_cast<const float*>(in), static_cast<float*>(out),
+                                                              rows, t1_, t2_, tw_, scale);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+  }
+
+ private:
+  static void check_(cudaError_t e) {
+    if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+  }
+  TabP<float, C::NT1> t1_{};
+  TabP<float, C::NT2> t2_{};
+  float2* tw_ = nullptr;
+  int grid_cap_ = 148;
+};
+
+// The split per size: N1 (phase A, strided columns) x N2 (phase B, rows).
+template <int V>
+std::unique_ptr<FastPlan> make_tile(size_t n, const void* tab, uint32_t nmax, int dev) {
+  switch (n) {
+    case 256: return std::make_unique<TilePlanImpl<V, 4, 4>>(tab, nmax, dev);
+    case 512: return std::make_unique<TilePlanImpl<V, 4, 5>>(tab, nmax, dev);
+    case 1024: return std::make_unique<TilePlanImpl<V, 5, 5>>(tab, nmax, dev);
+    case 2048: return std::make_unique<TilePlanImpl<V, 5, 6>>(tab, nmax, dev);
+    case 4096: return std::make_unique<TilePlanImpl<V, 6, 6>>(tab, nmax, dev);
+  }
+  return nullptr;
+}
+
+}  // namespace tilek
+}  // namespace amqft_b200

@@ -1,0 +1,9 @@
+// tile_v8.cu -- in-shared-memory four-step instances for AM-QFT variant 8.
+#include "gen/small_gen_v8.cuh"
+#include "tile_kernel.cuh"
+
+namespace amqft_b200 {
+namespace tilek {
+template std::unique_ptr<FastPlan> make_tile<8>(size_t, const void*, uint32_t, int);
+}  // namespace tilek
+}  // namespace amqft_b200
