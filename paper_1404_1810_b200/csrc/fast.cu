@@ -115,11 +115,12 @@ std::unique_ptr<FastPlan> make_fast_plan(const amqft_plan_desc& d, const void* d
 namespace tilek {
 template <int V>
 std::unique_ptr<FastPlan> make_tile(size_t n, const void* tab, uint32_t nmax, int dev);
-// the split of tile_kernel.cuh make_tile: N1 (phase A) x N2 (phase B)
+// the split of tile_kernel.cuh make_tile: N1 (phase A) x N2 (phase B),
+// 16 x 16, 16 x 32, 32 x 32, 64 x 32, 64 x 64
 static void tile_split(size_t n, size_t* n1, size_t* n2) {
   int lg = 0;
   for (size_t t = n; t > 1; t >>= 1) ++lg;
-  *n1 = size_t(1) << (lg / 2);
+  *n1 = size_t(1) << (lg == 11 ? 6 : lg / 2);
   *n2 = n / *n1;
 }
 }  // namespace tilek
@@ -248,7 +249,20 @@ OpCount fast_op_counts(const amqft_plan_desc& d) {
   return c;
 }
 
+static amqft_plan_desc sub_desc(int variant, size_t n, int dtype) {
+  amqft_plan_desc d{};
+  d.variant = variant;
+  d.function = AMQFT_FN_CDFT;
+  d.n = n;
+  d.batch = 1;
+  d.dtype = dtype;
+  d.trig_mode = AMQFT_TRIG_TABLE;
+  d.order = AMQFT_ORDER_FAST;
+  return d;
+}
+
 bool fast_sub_covered(int dtype, size_t n, int variant) {
+  if (tile_covers(sub_desc(variant, n, dtype))) return true;   // fp32 256 .. 4096, every variant
   if (dtype == AMQFT_F32 && f32_needs_f64_compute(variant, n)) return n >= 1024 && n <= 4096;
   if (dtype == AMQFT_F32) return n >= 2 && n <= 8192;
   return n >= 2 && n <= 4096 && n != 512;
@@ -265,7 +279,8 @@ std::unique_ptr<FastPlan> make_fast_sub(int variant, size_t n, int dtype, const 
   d.trig_mode = AMQFT_TRIG_TABLE;
   d.order = AMQFT_ORDER_FAST;
   d.device = dev;
-  std::unique_ptr<FastPlan> p = make_fast_plan(d, tab, nmax, tab64);
+  std::unique_ptr<FastPlan> p = make_tile_plan(d, tab, nmax);
+  if (!p) p = make_fast_plan(d, tab, nmax, tab64);
   OpCount o;
   if (!p) p = make_small_plan(d, tab, nmax, &o);
   return p;
@@ -278,6 +293,7 @@ OpCount fast_sub_op_counts(int variant, size_t n, int dtype) {
   d.n = n;
   d.dtype = dtype;
   OpCount o;
+  if (tile_covers(sub_desc(variant, n, dtype))) return tile_op_counts(d);
   if (n >= 1024) return fast_op_counts(d);
   smallk::small_ops_n(variant, n, dtype == AMQFT_F64, &o);
   return o;

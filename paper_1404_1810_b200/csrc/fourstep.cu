@@ -343,6 +343,16 @@ double sub_tbs(int dtype, int lg, int variant) {
   static const double f64[13] = {0, 5.5, 5.5, 5.5, 5.5, 5.5, 5.4, 2.94, 2.06, 0.0, 2.27, 2.68, 2.88};
   // fp32 rows through the fp64 instance (variants 5-8, fast.cuh): half the fp64 row bytes
   static const double mixed[13] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1.13, 1.34, 1.44};
+  // in-shared-memory four-step (tile_kernel.cuh): fp32 N = 256 .. 4096, all variants
+  static const double tile[13] = {0, 0, 0, 0, 0, 0, 0, 0, 5.85, 6.3, 6.2, 5.5, 5.58};
+  if (dtype == AMQFT_F32 && lg >= 8 && lg <= 12) {
+    amqft_plan_desc d{};
+    d.function = AMQFT_FN_CDFT;
+    d.dtype = dtype;
+    d.n = size_t(1) << lg;
+    d.variant = variant;
+    if (tile_covers(d)) return tile[lg];
+  }
   if (dtype == AMQFT_F32 && lg < 13 && f32_needs_f64_compute(variant, size_t(1) << lg)) return mixed[lg];
   if (dtype == AMQFT_F32) return lg < 14 ? f32[lg] : 0.0;
   return lg < 13 ? f64[lg] : 0.0;

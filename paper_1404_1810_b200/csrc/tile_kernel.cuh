@@ -33,6 +33,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <memory>
 #include <stdexcept>
 #include <vector>
@@ -47,19 +49,30 @@ namespace tilek {
 using smallk::SmallGen;
 using smallk::TabP;
 
-template <int LG1, int LG2>
+// T: threads per CTA; MB: CTAs per SM the registers are budgeted for (0:
+// by factor size); PF: bulk L2 prefetch of the CTA's next tile (-1: where a
+// factor has 64 points).
+template <int LG1, int LG2, int T_ = 64, int MB_ = 0, int PF_ = -1>
 struct TCfg {
   static constexpr int N1 = 1 << LG1, N2 = 1 << LG2, N = N1 * N2;
   static constexpr int LGM = LG1 > LG2 ? LG1 : LG2;
-  static constexpr int T = 64;                                   // threads per CTA
+  static constexpr int T = T_;                                   // threads per CTA
   static constexpr int NMIN = N1 < N2 ? N1 : N2;
   static constexpr int R = T / NMIN > 0 ? T / NMIN : 1;         // rows per tile
   static constexpr int PITCH = N2 + 2;                           // complex values per P row
   static constexpr int ROWP = N1 * PITCH;                        // complex values per tile row
+  // Measured (B200, 2^28 reals per launch): the 64 x 64 kernel is bound by
+  // the latency of phase A's loads (4 CTAs of 2 warps per SM; long
+  // scoreboard is the top stall); with the next tile on its way into L2
+  // 0.912 -> 0.769 ms.  The small factors run 10-16 CTAs per SM and lose
+  // 2-6 % with it.
+  static constexpr bool PF = PF_ < 0 ? LGM >= 6 : PF_ != 0;
   static constexpr size_t SMEM = static_cast<size_t>(R) * ROWP * sizeof(float2);
   static constexpr int NT1 = (N1 < 8 ? 8 : N1) / 4, NT2 = (N2 < 8 ? 8 : N2) / 4;
-  // CTAs per SM by registers: 64-point factors ~160, 32-point ~88, 16-point ~48
-  static constexpr int MINB = LGM >= 6 ? 6 : (LGM == 5 ? 10 : 16);
+  // CTAs per SM by registers (64 threads): 64-point factors 4 (246
+  // registers: measured 0.906 ms against 1.07 ms at 6 CTAs / 168 registers,
+  // config 2), 32-point 10, 16-point 16
+  static constexpr int MINB = MB_ > 0 ? MB_ : (LGM >= 6 ? 4 : (LGM == 5 ? 10 : 16)) * 64 / T;
 };
 
 // phase A: chunk c = complex n1 = 2c, 2c+1 of column n2 (global), output
@@ -75,13 +88,13 @@ struct AIo {
     else { a = u.x; b = u.y; d = v.x; e = v.y; }
   }
   __device__ __forceinline__ void st(int c, float a, float b, float d, float e) const {
-    if (c != 0) {   // k1 = 0: w = 1
-      const float2 w = __ldg(tw + (2 * c) * N2);
+    const float2 w1 = __ldg(tw + (2 * c + 1) * N2);
+    if (c != 0) {
+      const float2 w = __ldg(tw + (2 * c) * N2);   // k1 = 0: w = 1
       const float na = a * w.x - b * w.y, nb = a * w.y + b * w.x;
       a = na;
       b = nb;
     }
-    const float2 w1 = __ldg(tw + (2 * c + 1) * N2);
     const float nd = d * w1.x - e * w1.y, ne = d * w1.y + e * w1.x;
     sp[(2 * c) * PITCH] = make_float2(a, b);
     sp[(2 * c + 1) * PITCH] = make_float2(nd, ne);
@@ -110,12 +123,12 @@ struct BIo {
   }
 };
 
-template <int V, int LG1, int LG2, bool INV>
-__global__ void __launch_bounds__(TCfg<LG1, LG2>::T, TCfg<LG1, LG2>::MINB)
+template <int V, bool INV, class C>
+__global__ void __launch_bounds__(C::T, C::MINB)
 k_tile(const float* __restrict__ in, float* __restrict__ out, size_t rows,
-       const __grid_constant__ TabP<float, TCfg<LG1, LG2>::NT1> t1,
-       const __grid_constant__ TabP<float, TCfg<LG1, LG2>::NT2> t2, const float2* __restrict__ tw, float scale) {
-  using C = TCfg<LG1, LG2>;
+       const __grid_constant__ TabP<float, C::NT1> t1, const __grid_constant__ TabP<float, C::NT2> t2,
+       const float2* __restrict__ tw, float scale) {
+  constexpr int LG1 = 31 - __builtin_clz(C::N1), LG2 = 31 - __builtin_clz(C::N2);
   using G1 = SmallGen<V, 0, LG1, float>;
   using G2 = SmallGen<V, 0, LG2, float>;
   constexpr int N1 = C::N1, N2 = C::N2, N = C::N;
@@ -125,6 +138,12 @@ k_tile(const float* __restrict__ in, float* __restrict__ out, size_t rows,
   const size_t tiles = (rows + C::R - 1) / C::R;
   for (size_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
     const size_t row0 = tile * C::R;
+    if constexpr (C::PF) {   // the CTA's next tile: one bulk prefetch into L2
+      const size_t nrow = (tile + gridDim.x) * C::R;
+      if (tid == 0 && nrow + C::R <= rows)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                     ::"l"(in + nrow * 2 * N), "n"(C::R * N * 8) : "memory");
+    }
     // ---- phase A: columns of x -> P (twiddled)
 #pragma unroll 1
     for (int i = tid; i < C::R * N2; i += C::T) {
@@ -150,9 +169,9 @@ k_tile(const float* __restrict__ in, float* __restrict__ out, size_t rows,
   }
 }
 
-template <int V, int LG1, int LG2>
+template <int V, int LG1, int LG2, int T = 64, int MB = 0, int PF = -1>
 class TilePlanImpl final : public FastPlan {
-  using C = TCfg<LG1, LG2>;
+  using C = TCfg<LG1, LG2, T, MB, PF>;
 
  public:
   TilePlanImpl(const void* tab, uint32_t nmax, int device) {
@@ -168,8 +187,8 @@ class TilePlanImpl final : public FastPlan {
       }
     check_(cudaMalloc(&tw_, tw.size() * sizeof(float2)));
     check_(cudaMemcpy(tw_, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice));
-    auto f0 = k_tile<V, LG1, LG2, false>;
-    auto f1 = k_tile<V, LG1, LG2, true>;
+    auto f0 = k_tile<V, false, C>;
+    auto f1 = k_tile<V, true, C>;
     check_(cudaFuncSetAttribute(f0, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM)));
     check_(cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM)));
     int per_sm = 0;
@@ -188,11 +207,11 @@ class TilePlanImpl final : public FastPlan {
     const unsigned grid = static_cast<unsigned>(std::min<size_t>(tiles, static_cast<size_t>(grid_cap_)));
     const float scale = 1.0f / static_cast<float>(C::N);
     if (inverse)
-      k_tile<V, LG1, LG2, true><<<grid, C::T, C::SMEM, st>>>(static_cast<const float*>(in), static_cast<float*>(out),
-                                                             rows, t1_, t2_, tw_, scale);
+      k_tile<V, true, C><<<grid, C::T, C::SMEM, st>>>(static_cast<const float*>(in), static_cast<float*>(out), rows,
+                                                      t1_, t2_, tw_, scale);
     else
-      k_tile<V, LG1, LG2, false><<<grid, C::T, C::SMEM, st>>>(static_cast<const float*>(in), static_cast<float*>(out),
-                                                              rows, t1_, t2_, tw_, scale);
+      k_tile<V, false, C><<<grid, C::T, C::SMEM, st>>>(static_cast<const float*>(in), static_cast<float*>(out), rows,
+                                                       t1_, t2_, tw_, scale);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
   }
@@ -210,11 +229,34 @@ class TilePlanImpl final : public FastPlan {
 // The split per size: N1 (phase A, strided columns) x N2 (phase B, rows).
 template <int V>
 std::unique_ptr<FastPlan> make_tile(size_t n, const void* tab, uint32_t nmax, int dev) {
+#ifdef AMQFT_TILE_AB   // A/B instances (diagnostic builds): AMQFT_TILE_KV = T,MB,PF
+  if (const char* kv = std::getenv("AMQFT_TILE_KV")) {
+    int t = 64, mb = 0, fl = 0;
+    std::sscanf(kv, "%d,%d,%d", &t, &mb, &fl);
+    if ((n == 2048 || n == 512) && std::getenv("AMQFT_TILE_SWAP")) n += 1;   // the swapped splits
+#define AMQFT_TILE_CASE(NN, A, B, TT, MM, FF) \
+    if (n == NN && t == TT && mb == MM && fl == FF) return std::make_unique<TilePlanImpl<V, A, B, TT, MM, FF>>(tab, nmax, dev);
+    AMQFT_TILE_CASE(4096, 6, 6, 64, 4, 0)
+    AMQFT_TILE_CASE(4096, 6, 6, 64, 4, 1)
+    AMQFT_TILE_CASE(4096, 6, 6, 64, 5, 1)
+    AMQFT_TILE_CASE(2048, 5, 6, 64, 4, 0)
+    AMQFT_TILE_CASE(2048, 5, 6, 64, 4, 1)
+    AMQFT_TILE_CASE(2048, 5, 6, 64, 6, 1)
+    AMQFT_TILE_CASE(2049, 6, 5, 64, 4, 0)
+    AMQFT_TILE_CASE(2049, 6, 5, 64, 4, 1)
+    AMQFT_TILE_CASE(2049, 6, 5, 64, 5, 1)
+    AMQFT_TILE_CASE(512, 4, 5, 64, 0, 1)
+    AMQFT_TILE_CASE(512, 4, 5, 64, 0, 0)
+    AMQFT_TILE_CASE(513, 5, 4, 64, 0, 0)
+#undef AMQFT_TILE_CASE
+    throw std::invalid_argument("AMQFT_TILE_KV: no such instance");
+  }
+#endif
   switch (n) {
     case 256: return std::make_unique<TilePlanImpl<V, 4, 4>>(tab, nmax, dev);
     case 512: return std::make_unique<TilePlanImpl<V, 4, 5>>(tab, nmax, dev);
     case 1024: return std::make_unique<TilePlanImpl<V, 5, 5>>(tab, nmax, dev);
-    case 2048: return std::make_unique<TilePlanImpl<V, 5, 6>>(tab, nmax, dev);
+    case 2048: return std::make_unique<TilePlanImpl<V, 6, 5>>(tab, nmax, dev);   // 0.780 vs 0.803 ms for 32 x 64
     case 4096: return std::make_unique<TilePlanImpl<V, 6, 6>>(tab, nmax, dev);
   }
   return nullptr;

@@ -1,4 +1,5 @@
 // tile_v4.cu -- in-shared-memory four-step instances for AM-QFT variant 4.
+#define AMQFT_TILE_AB 1
 #include "gen/small_gen_v4.cuh"
 #include "tile_kernel.cuh"
 

@@ -31,3 +31,12 @@ def reference(oracle):
     if ref is None:
         pytest.skip("oracle/_ref/libamqft_ref.so not built (reference sources absent)")
     return ref
+
+
+@pytest.fixture
+def no_tile(monkeypatch):
+    """Plans created under this fixture skip the in-shared-memory four-step
+    (path 6, tile_kernel.cuh) so the tests of the kernels it displaced as the
+    default for fp32 CDFT N = 256-4096 (fused, cooperative, four-step) keep
+    exercising them: the library reads AMQFT_AB_TILE at plan creation."""
+    monkeypatch.setenv("AMQFT_AB_TILE", "none")

@@ -80,7 +80,7 @@ def test_cluster_rows_independent_and_deterministic():
     assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 1.4e-4
 
 
-def test_cluster_op_counts(all_cluster_sizes):
+def test_cluster_op_counts(all_cluster_sizes, no_tile):
     """Meter of the executed schedule: P rows of the 4096-point AM-QFT DAG
     (reference closed forms) + the radix-2 P-point DFTs + (2P-3) N/P twiddle
     multiplies (the twiddles and their powers)."""

@@ -190,7 +190,7 @@ def test_fast_kernel_fp64_bitwise(oracle, restatement, n):
 
 
 @pytest.mark.parametrize("n", [1024, 2048, 4096, 8192])
-def test_fast_kernel_fp32_tolerance(oracle, restatement, n):
+def test_fast_kernel_fp32_tolerance(oracle, restatement, n, no_tile):
     r, O = restatement, oracle
     rng = np.random.default_rng(n)
     xs = rng.standard_normal((4, 2 * n)).astype(np.float32)
@@ -519,7 +519,7 @@ SMALL_SIZES = {"f64": (2, 4, 8, 16, 32, 64, 128, 256), "f32": (2, 4, 8, 16, 32, 
 
 
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
-def test_small_kernel_parity(oracle, restatement, dtype):
+def test_small_kernel_parity(oracle, restatement, dtype, no_tile):
     """fp64: bitwise the oracle, forward and swap-trick inverse, all 8
     variants; fp32: bitwise the fp32 exact-order generic path (same ops, same
     order) and within 1e-5 log2 N of the fp64 oracle for variants 1-4.  300
@@ -882,7 +882,7 @@ def test_distributed_fourstep_transposed_scatter():
 
 # ---- fp32 plans of the sine-family variants (5-8): fp64 compute from N = 512
 @pytest.mark.parametrize("n", [512, 1024, 2048, 4096])
-def test_fp32_sine_variants_match_cpu(oracle, restatement, n):
+def test_fp32_sine_variants_match_cpu(oracle, restatement, n, no_tile):
     """fp32 rows in and out, every function the plan covers at this size:
     CDFT (fast: the fused kernel's fp64 instance with fp32 I/O at N =
     1024-4096, a four-step at 512; exact: fp32 rows through the fp64 exact

@@ -1,0 +1,132 @@
+"""In-shared-memory four-step (path 6, tile_kernel.cuh): fp32 CDFT N = 256 ..
+4096 as N1 x N2 register-resident AM-QFT factors, one pass over HBM -- the
+default fast-order path for these sizes (config 2 is N = 4096).
+
+Checked for ALL 8 variants against the fp64 CPU reference of the same variant
+(tolerance 1e-5 log2 N, BASELINE north_star; the factors are <= 64 points, where
+the sine-family variants 5-8 are stable in fp32, so no variant needs fp64
+compute here), against numpy's fp64 FFT, against the compiled reference
+library (oracle/_ref) at config 2's size, inverse round trips, in-place rows,
+ragged batches (rows not a multiple of the tile, fewer rows than CTAs, more
+rows than one wave), and the op meter of the executed schedule."""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_1404_1810_b200 as amqft  # noqa: E402
+from test_gpu_parity import DEV, numpy_dft, run_plan  # noqa: E402
+
+SIZES = [256, 512, 1024, 2048, 4096]
+# the kernel's split (tile_kernel.cuh make_tile): N1 (phase A) x N2 (phase B)
+SPLIT = {256: (16, 16), 512: (16, 32), 1024: (32, 32), 2048: (64, 32), 4096: (64, 64)}
+# measured on the B200: 1e-7 .. 4e-7 (v1-4), up to 6e-7 vs numpy for v5-8;
+# the bar below is 10x tighter than the north-star tolerance
+TIGHT = 2e-6
+
+
+def _plan(v, n, batch):
+    p = amqft.Plan(v, amqft.FunctionId.Cdft, n, batch, dtype="f32", order=amqft.Order.Fast)
+    assert p.path() == (6, 1), "in-shared-memory four-step expected (one launch)"
+    return p
+
+
+@pytest.mark.parametrize("n", SIZES)
+def test_tile_all_variants_match_cpu(oracle, restatement, n):
+    r, O = restatement, oracle
+    rows = 5
+    xs = np.random.default_rng(n).standard_normal((rows, 2 * n)).astype(np.float32).astype(np.float64)
+    tol = 1e-5 * math.log2(n)
+    for v in range(1, 9):
+        plan = _plan(v, n, rows)
+        got = run_plan(plan, xs)
+        for row in (0, rows - 1):
+            want = r.execute(v, O.F_CDFT, n, xs[row])
+            err = r.rel_l2(got[row], want)
+            # the reference's own fp64 v5-8 result is ~1e-6 from the DFT at 4096
+            assert err <= (tol if v >= 5 else TIGHT), (v, n, err)
+            assert r.rel_l2(got[row], numpy_dft(xs[row])) <= TIGHT, (v, n)
+        back = run_plan(plan, got.astype(np.float32), inverse=True)
+        assert r.rel_l2(back.ravel(), xs.ravel()) <= TIGHT, (v, n)
+
+
+def test_tile_matches_reference_library_config2(oracle, reference, restatement):
+    """Config 2's size against the compiled reference itself (oracle/_ref)."""
+    n = 4096
+    x = np.random.default_rng(2).standard_normal(2 * n).astype(np.float32).astype(np.float64)
+    for v in range(1, 9):
+        got = run_plan(_plan(v, n, 1), [x])[0]
+        want = reference.execute(v, oracle.F_CDFT, n, x)
+        assert restatement.rel_l2(got, want) <= 1e-5 * 12, v
+
+
+@pytest.mark.parametrize("n", SIZES)
+def test_tile_ragged_batches_and_rows_independent(n):
+    """Row counts around the tile size (R = 64 / min(N1, N2) rows per CTA
+    iteration) and beyond one wave of CTAs: every row equals the same row
+    transformed alone (bitwise: a row's arithmetic does not depend on its
+    position in the batch)."""
+    n1, n2 = SPLIT[n]
+    R = max(1, 64 // min(n1, n2))
+    big = 148 * 16 * R + R + 1          # more tiles than resident CTAs, last tile partial
+    rng = np.random.default_rng(n + 1)
+    x = torch.tensor(rng.standard_normal((big, 2 * n)), dtype=torch.float32, device=DEV)
+    plan = _plan(4, n, big)
+    y = torch.empty_like(x)
+    plan.forward(x, y)
+    torch.cuda.synchronize()
+    single = _plan(4, n, 1)
+    for row in (0, 1, R - 1, R, big // 2, big - 2, big - 1):
+        z = torch.empty_like(x[row:row + 1])
+        single.forward(x[row:row + 1].contiguous(), z)
+        torch.cuda.synchronize()
+        assert torch.equal(z[0], y[row]), (n, row)
+    for rows in (1, R - 1 if R > 1 else 1, R + 1, 3 * R + 2):
+        z = torch.full_like(x[:rows + 1], float("nan"))
+        plan.forward(x[:rows].contiguous(), z, rows=rows)
+        torch.cuda.synchronize()
+        assert torch.equal(z[:rows], y[:rows]), (n, rows)
+        assert torch.isnan(z[rows]).all(), "rows past the batch must not be written"
+
+
+@pytest.mark.parametrize("n", [256, 4096])
+def test_tile_in_place(n):
+    x = torch.tensor(np.random.default_rng(n + 2).standard_normal((37, 2 * n)), dtype=torch.float32, device=DEV)
+    plan = _plan(2, n, 37)
+    y = torch.empty_like(x)
+    plan.forward(x, y)
+    z = x.clone()
+    plan.forward(z, z)
+    torch.cuda.synchronize()
+    assert torch.equal(y, z)
+    plan.inverse(z, z)
+    torch.cuda.synchronize()
+    assert float((z - x).norm() / x.norm()) <= TIGHT
+
+
+@pytest.mark.parametrize("n", SIZES)
+def test_tile_op_counts(oracle, restatement, n):
+    """Meter of the executed schedule: N2 reference DAGs of length N1, N1 of
+    length N2 (the reference meter of each) and one complex twiddle multiply
+    per element (4 muls + 2 adds), the four-step's accounting."""
+    r, O = restatement, oracle
+    n1, n2 = SPLIT[n]
+    for v in (1, 4, 6):
+        m1 = r.execute(v, O.F_CDFT, n1, np.zeros(2 * n1), meter=True)[1]
+        m2 = r.execute(v, O.F_CDFT, n2, np.zeros(2 * n2), meter=True)[1]
+        want = (n2 * m1[0] + n1 * m2[0] + 2 * n, n2 * m1[1] + n1 * m2[1] + 4 * n, n2 * m1[2] + n1 * m2[2])
+        assert _plan(v, n, 1).op_counts() == want, (v, n)
+
+
+def test_tile_rejects_misaligned_buffers():
+    """Device buffers of fast-order plans must be 16-byte aligned (the C ABI's
+    contract for every fast path); the host-buffer pipeline of this path is
+    covered by test_gpu_parity.py::test_host_pipeline_matches_device_path."""
+    n = 4096
+    plan = _plan(4, n, 1)
+    x = torch.zeros(2 * n + 2, dtype=torch.float32, device=DEV)
+    with pytest.raises(amqft.InvalidArgument):
+        plan.forward(x[1:2 * n + 1], x[1:2 * n + 1], rows=1)
