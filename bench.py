@@ -217,22 +217,33 @@ def bench_reference(args, rank):
     return line
 
 
-def ncu_traffic(args, n):
-    """DRAM bytes per launch of the fused kernel from the committed ncu
+def ncu_traffic(args, n, path=2):
+    """DRAM bytes per launch of the timed kernel from the committed ncu
     --set full capture (profiles/, made by tools/profile_round.sh), when it
-    is a capture of this exact kernel (variant, N, fp32, fast order)."""
+    is a capture of this exact kernel (variant, N, fp32, fast order): k_tile
+    (path 6, the in-shared-memory four-step) or k_fast (path 2)."""
     import glob
     logn = n.bit_length() - 1
-    # k_fast<V, R, LOGN, LOGLB, MODE[, IO, P]>: the one-CTA-per-row fp32 instance
-    want = (f"k_fast<{args.variant},float,{logn},6,0>", f"k_fast<{args.variant},float,{logn},6,0,float,1>")
     if args.dtype != "f32" or args.order != "fast":
         return None, None
-    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_k_fast_*.json")), reverse=True):
+    if path == 6:
+        # k_tile<V, INV, TCfg<LG1, LG2, ...>>: N1 x N2 = 64 x 64 at N = 4096 (tile_kernel.cuh make_tile)
+        lg1 = 6 if logn == 11 else logn // 2
+        want = (f"k_tile<{args.variant},false,TCfg<{lg1},{logn - lg1},", f"k_tile<{args.variant},0,TCfg<{lg1},{logn - lg1},")
+        pattern = "r*_ncu_k_tile_*.json"
+    else:
+        # k_fast<V, R, LOGN, LOGLB, MODE[, IO, P]>: the one-CTA-per-row fp32 instance
+        want = (f"k_fast<{args.variant},float,{logn},6,0>", f"k_fast<{args.variant},float,{logn},6,0,float,1>")
+        pattern = "r*_ncu_k_fast_*.json"
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", pattern)), reverse=True):
         try:
             d = json.load(open(f))
         except (OSError, ValueError):
             continue
-        if not any(w in d.get("Kernel Name", "") for w in want) or int(float(d.get("launch__grid_size", 0))) <= 0:
+        name = d.get("Kernel Name", "")
+        for junk in (" ", "(bool)", "(int)", "amqft_b200::tilek::", "amqft_b200::fastk::"):
+            name = name.replace(junk, "")
+        if not any(w in name for w in want) or int(float(d.get("launch__grid_size", 0))) <= 0:
             continue
         scale = {"Gbyte": 1e9, "Mbyte": 1e6, "byte": 1.0}
         rd = float(d["dram__bytes_read.sum"]) * scale.get(d.get("dram__bytes_read.sum [unit]", "Gbyte"), 1e9)
@@ -621,13 +632,13 @@ def main():
     ms_per_step = ms / args.steps
     value = world * batch * args.steps / (ms / 1000.0)
 
-    # Dominant-kernel roofline: the exec call is one kernel on path 0/2;
+    # Dominant-kernel roofline: the exec call is one kernel on paths 0/2/6;
     # per-launch duration from CUDA events on the launching stream.
     hbm, hbm_src = peaks()
     alg_bytes = 2 * (2 * n * esize) * batch  # one read + one write per transform
     kernel_ms = ms_per_step / max(1, launches) if path != 1 else ms_per_step
     achieved = alg_bytes / (kernel_ms / 1000.0) / 1e9
-    traffic, traffic_src = ncu_traffic(args, n)
+    traffic, traffic_src = ncu_traffic(args, n, path)
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm, "traffic": traffic, "traffic_unit": "bytes per launch (DRAM read + write)",
             "traffic_source": traffic_src,

@@ -13,6 +13,9 @@ src, dst, tag = sys.argv[1], sys.argv[2], sys.argv[3]
 
 
 def short(name):
+    m = re.search(r"k_tile<(.*>)>", name)
+    if m:
+        return f"k_tile<{m.group(1).replace(' ', '')}> (AM-QFT in-shared-memory four-step CDFT)"
     m = re.search(r"k_fast<(.*?)>", name)
     if m:
         return f"k_fast<{m.group(1).replace(' ', '')}> (AM-QFT fused CDFT)"
@@ -53,12 +56,17 @@ want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
         "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio",
         "smsp__average_warps_issue_stalled_mio_throttle_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_lg_throttle_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_not_selected_per_issue_active.ratio",
+        "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct",
         "launch__grid_size", "launch__block_size", "launch__shared_mem_per_block_dynamic"]
-raw = subprocess.run(["ncu", "-i", f"{src}/k_fast_full.ncu-rep", "--page", "raw", "--csv"],
+import os  # noqa: E402
+rep = f"{src}/k_top_full.ncu-rep" if os.path.exists(f"{src}/k_top_full.ncu-rep") else f"{src}/k_fast_full.ncu-rep"
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"],
                      capture_output=True, text=True, check=True).stdout
 rr = list(csv.reader(raw.splitlines()))
 h, units = rr[0], rr[1]
-row = next(r for r in rr[2:] if any("k_fast" in c for c in r))
+row = next(r for r in rr[2:] if any("k_fast" in c or "k_tile" in c for c in r))
 out = {"Kernel Name": short(row[h.index("Kernel Name")])}
 for k in want:
     if k in h:
@@ -66,7 +74,8 @@ for k in want:
         out[k + " [unit]"] = units[h.index(k)]
 rd = float(out["dram__bytes_read.sum"]) if "dram__bytes_read.sum" in out else None
 wr = float(out["dram__bytes_write.sum"]) if "dram__bytes_write.sum" in out else None
-out["_source"] = ("ncu --set full --clock-control none --import-source on -k regex:k_fast -s 3 -c 1, "
+out["_source"] = ("ncu --set full --clock-control none --import-source on -k 'regex:k_tile|k_fast' -s 3 -c 1, "
                   "python bench.py --steps 2 --warmup 3 --e2e-steps 0 --no-cpu-baseline (B200, tools/profile_round.sh)")
-json.dump(out, open(f"{dst}/{tag}_ncu_k_fast_v4_n4096.json", "w"), indent=1)
+kname = "k_tile" if "k_tile" in out["Kernel Name"] else "k_fast"
+json.dump(out, open(f"{dst}/{tag}_ncu_{kname}_v4_n4096.json", "w"), indent=1)
 print(json.dumps({k: out[k] for k in list(out)[:12]}, indent=1))
