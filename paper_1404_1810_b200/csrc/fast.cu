@@ -2,6 +2,7 @@
 // per-variant instances: fast_v1.cu .. fast_v8.cu).
 #include "fast.cuh"
 
+#include <cstdio>
 #include <cstdlib>
 #include <type_traits>
 
@@ -58,24 +59,19 @@ std::unique_ptr<FastPlan> make_fast_mixed(int v, int kind, size_t n, const void*
 
 // Cluster four-step (fast_kernel.cuh, k_fast<..., P>): CDFT N = P * 4096
 // as P fused rows on one cluster of P CTAs, one pass over HBM.  fp32, and
-// fp32 rows computed in fp64 for variants 5-8.  Used where it beats the
-// alternative (B200, tools/cluster_ab.sh, profiles/r02_cluster_ab.log):
-// N = 2^14 for variants 2 and 4 (+7-8 % over the three-factor four-step)
-// and N = 8192 for the serial-recurrence variants 1 and 3 (+31 % over the
-// single-CTA 8192 kernel).  Elsewhere it loses: the per-row DSMEM exchange
-// makes a cluster run in lockstep with its slowest CTA (worse with P = 8 /
-// 16, and 16-CTA clusters leave a quarter of the SMs idle), and the fp64-
-// compute instance of variants 5-8 fits one CTA per SM.
-// AMQFT_AB_CLUSTER=all|none overrides the choice (A/B measurements only).
+// fp32 rows computed in fp64 for variants 5-8.  Measured (B200,
+// profiles/r02_cluster_ab.log): 1.55-1.85 TB/s at N = 2^13 / 2^14, 1.3 /
+// 0.77 TB/s at 2^15 / 2^16 (the per-row DSMEM exchange makes a cluster run in
+// lockstep with its slowest CTA, and 16-CTA clusters leave a quarter of the
+// SMs idle).  The in-shared-memory four-step (tile_kernel.cuh) now runs N <=
+// 2^14 in one pass at 5.1-5.7 TB/s and the multi-pass four-step built on it
+// 2^15 / 2^16 at 2.0 TB/s, so no plan picks the cluster kernel by default;
+// AMQFT_AB_CLUSTER=all selects it (A/B measurements and its tests).
 bool uses_cluster(const amqft_plan_desc& d) {
   if (d.function != AMQFT_FN_CDFT || d.dtype != AMQFT_F32) return false;
   if (d.n < 8192 || d.n > 65536 || (d.n & (d.n - 1))) return false;
-  if (const char* e = std::getenv("AMQFT_AB_CLUSTER")) {
-    if (e[0] == 'a') return true;
-    if (e[0] == 'n') return false;
-  }
-  const int v = d.variant;
-  return (d.n == 16384 && (v == 2 || v == 4)) || (d.n == 8192 && (v == 1 || v == 3));
+  if (const char* e = std::getenv("AMQFT_AB_CLUSTER")) return e[0] == 'a';
+  return false;
 }
 
 template <typename R, typename IO = R>
@@ -116,10 +112,18 @@ namespace tilek {
 template <int V>
 std::unique_ptr<FastPlan> make_tile(size_t n, const void* tab, uint32_t nmax, int dev);
 // the split of tile_kernel.cuh make_tile: N1 (phase A) x N2 (phase B),
-// 16 x 16, 16 x 32, 32 x 32, 64 x 32, 64 x 64
-static void tile_split(size_t n, size_t* n1, size_t* n2) {
+// 4 x 4, 4 x 8, 8 x 8, 8 x 16, 16 x 16, 16 x 32, 32 x 32, 64 x 32, 64 x 64
+// and the three-factor 32 x 16 x 16, 32 x 16 x 32 (n3 = 1: two factors)
+static void tile_split(size_t n, size_t* n1, size_t* n2, size_t* n3) {
   int lg = 0;
   for (size_t t = n; t > 1; t >>= 1) ++lg;
+  *n3 = 1;
+  if (lg >= 13) {   // 32 x 16 x 16, 32 x 16 x 32
+    *n1 = 32;
+    *n2 = 16;
+    *n3 = n / (32 * 16);
+    return;
+  }
   *n1 = size_t(1) << (lg == 11 ? 6 : lg / 2);
   *n2 = n / *n1;
 }
@@ -127,10 +131,15 @@ static void tile_split(size_t n, size_t* n1, size_t* n2) {
 
 bool tile_covers(const amqft_plan_desc& d) {
   if (d.function != AMQFT_FN_CDFT || d.dtype != AMQFT_F32) return false;
-  if (d.n < 256 || d.n > 4096 || (d.n & (d.n - 1))) return false;
-  if (const char* e = std::getenv("AMQFT_AB_TILE"))
+  if (d.n < 16 || d.n > 16384 || (d.n & (d.n - 1))) return false;
+  size_t lo = 16, hi = 16384;
+  if (const char* e = std::getenv("AMQFT_AB_TILE")) {
     if (e[0] == 'n') return false;
-  return true;
+    // A/B measurements: AMQFT_AB_TILE=lo,hi restricts the sizes it takes
+    unsigned long a = 0, b = 0;
+    if (std::sscanf(e, "%lu,%lu", &a, &b) == 2) lo = a, hi = b;
+  }
+  return d.n >= lo && d.n <= hi;
 }
 
 std::unique_ptr<FastPlan> make_tile_plan(const amqft_plan_desc& d, const void* d_trig, uint32_t nmax) {
@@ -157,11 +166,18 @@ OpCount tile_op_counts(const amqft_plan_desc& d) {
   // N2 sub-transforms of length N1 and N1 of length N2 (the reference DAG of
   // each: the traced schedule's meter) plus one complex twiddle multiply
   // per element (4 muls + 2 adds), as the four-step's accounting
-  size_t n1, n2;
-  tilek::tile_split(d.n, &n1, &n2);
-  OpCount c1, c2, c;
+  size_t n1, n2, n3;
+  tilek::tile_split(d.n, &n1, &n2, &n3);
+  OpCount c1, c2, c3, c;
   smallk::small_ops_n(d.variant, n1, false, &c1, AMQFT_FN_CDFT);
   smallk::small_ops_n(d.variant, n2, false, &c2, AMQFT_FN_CDFT);
+  if (n3 > 1) {   // three factors, two twiddle passes
+    smallk::small_ops_n(d.variant, n3, false, &c3, AMQFT_FN_CDFT);
+    c.adds = n2 * n3 * c1.adds + n1 * n3 * c2.adds + n1 * n2 * c3.adds + 2 * 2 * d.n;
+    c.muls = n2 * n3 * c1.muls + n1 * n3 * c2.muls + n1 * n2 * c3.muls + 2 * 4 * d.n;
+    c.bt = n2 * n3 * c1.bt + n1 * n3 * c2.bt + n1 * n2 * c3.bt;
+    return c;
+  }
   c.adds = n2 * c1.adds + n1 * c2.adds + 2 * d.n;
   c.muls = n2 * c1.muls + n1 * c2.muls + 4 * d.n;
   c.bt = n2 * c1.bt + n1 * c2.bt;
@@ -262,14 +278,14 @@ static amqft_plan_desc sub_desc(int variant, size_t n, int dtype) {
 }
 
 bool fast_sub_covered(int dtype, size_t n, int variant) {
-  if (tile_covers(sub_desc(variant, n, dtype))) return true;   // fp32 256 .. 4096, every variant
+  if (tile_covers(sub_desc(variant, n, dtype))) return true;   // fp32 16 .. 16384, every variant
   if (dtype == AMQFT_F32 && f32_needs_f64_compute(variant, n)) return n >= 1024 && n <= 4096;
   if (dtype == AMQFT_F32) return n >= 2 && n <= 8192;
   return n >= 2 && n <= 4096 && n != 512;
 }
 
 std::unique_ptr<FastPlan> make_fast_sub(int variant, size_t n, int dtype, const void* tab, uint32_t nmax, int dev,
-                                        const void* tab64) {
+                                        const void* tab64, bool columns) {
   amqft_plan_desc d{};
   d.variant = variant;
   d.function = AMQFT_FN_CDFT;
@@ -279,21 +295,26 @@ std::unique_ptr<FastPlan> make_fast_sub(int variant, size_t n, int dtype, const 
   d.trig_mode = AMQFT_TRIG_TABLE;
   d.order = AMQFT_ORDER_FAST;
   d.device = dev;
-  std::unique_ptr<FastPlan> p = make_tile_plan(d, tab, nmax);
+  std::unique_ptr<FastPlan> p;
+  if (columns) {   // column mode: the one-thread-per-row kernel (N <= 64 fp32, 32 fp64)
+    OpCount oc;
+    return make_small_plan(d, tab, nmax, &oc);
+  }
+  p = make_tile_plan(d, tab, nmax);
   if (!p) p = make_fast_plan(d, tab, nmax, tab64);
   OpCount o;
   if (!p) p = make_small_plan(d, tab, nmax, &o);
   return p;
 }
 
-OpCount fast_sub_op_counts(int variant, size_t n, int dtype) {
+OpCount fast_sub_op_counts(int variant, size_t n, int dtype, bool columns) {
   amqft_plan_desc d{};
   d.variant = variant;
   d.function = AMQFT_FN_CDFT;
   d.n = n;
   d.dtype = dtype;
   OpCount o;
-  if (tile_covers(sub_desc(variant, n, dtype))) return tile_op_counts(d);
+  if (!columns && tile_covers(sub_desc(variant, n, dtype))) return tile_op_counts(d);
   if (n >= 1024) return fast_op_counts(d);
   smallk::small_ops_n(variant, n, dtype == AMQFT_F64, &o);
   return o;

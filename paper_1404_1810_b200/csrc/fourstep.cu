@@ -338,14 +338,14 @@ int lg2(size_t v) {
 // minimising the two DFT passes' and the transposes' time by the measured HBM
 // throughput of each sub-size (B200, TB/s; tools/sweep_c3.py,
 // tools/prof_fast.py).
-double sub_tbs(int dtype, int lg, int variant) {
+double sub_tbs(int dtype, int lg, int variant, bool col = false) {
   static const double f32[14] = {0, 5.0, 5.0, 5.0, 5.0, 5.0, 5.0, 3.9, 1.78, 1.26, 1.72, 2.43, 3.17, 2.09};
   static const double f64[13] = {0, 5.5, 5.5, 5.5, 5.5, 5.5, 5.4, 2.94, 2.06, 0.0, 2.27, 2.68, 2.88};
   // fp32 rows through the fp64 instance (variants 5-8, fast.cuh): half the fp64 row bytes
   static const double mixed[13] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1.13, 1.34, 1.44};
-  // in-shared-memory four-step (tile_kernel.cuh): fp32 N = 256 .. 4096, all variants
-  static const double tile[13] = {0, 0, 0, 0, 0, 0, 0, 0, 5.85, 6.3, 6.2, 5.5, 5.58};
-  if (dtype == AMQFT_F32 && lg >= 8 && lg <= 12) {
+  // in-shared-memory four-step (tile_kernel.cuh): fp32 N = 16 .. 16384, all variants
+  static const double tile[15] = {0, 0, 0, 0, 5.18, 6.5, 5.78, 6.25, 5.85, 6.3, 6.2, 5.5, 5.63, 5.75, 5.09};
+  if (!col && dtype == AMQFT_F32 && lg >= 4 && lg <= 14) {
     amqft_plan_desc d{};
     d.function = AMQFT_FN_CDFT;
     d.dtype = dtype;
@@ -371,10 +371,11 @@ bool fourstep_split(int dtype, size_t n, int variant, size_t* n1, size_t* n2, bo
     const int l2 = lg - l1;
     if (!fast_sub_covered(dtype, size_t(1) << l1, variant) || !fast_sub_covered(dtype, size_t(1) << l2, variant))
       continue;
-    const double a = sub_tbs(dtype, l1, variant), b = sub_tbs(dtype, l2, variant);
-    if (a <= 0.0 || b <= 0.0) continue;
+    const double b = sub_tbs(dtype, l2, variant);
     for (int c = 0; c < 2; ++c) {
       if (c == 1 && !col_capable(dtype, l1)) continue;
+      const double a = sub_tbs(dtype, l1, variant, c == 1);
+      if (a <= 0.0 || b <= 0.0) continue;
       // tiled transposes need both sides >= 32 from N = 2^10 on (column
       // mode: only the last transpose, N1 x N2)
       if (c == 0 && (l1 < 5 || l2 < 5) && lg >= 10) continue;
@@ -407,7 +408,7 @@ bool fourstep_split3(int dtype, size_t n, int variant, size_t* a, size_t* b, siz
       const int lc = lg - la - lb;
       if (lc < 5 || !col_capable(dtype, la) || !col_capable(dtype, lb)) continue;
       if (!fast_sub_covered(dtype, size_t(1) << lc, variant)) continue;
-      const double ta = sub_tbs(dtype, la, variant), tb = sub_tbs(dtype, lb, variant),
+      const double ta = sub_tbs(dtype, la, variant, true), tb = sub_tbs(dtype, lb, variant, true),
                    tc = sub_tbs(dtype, lc, variant);
       if (ta <= 0.0 || tb <= 0.0 || tc <= 0.0) continue;
       const double cst = 1.0 / ta + 1.0 / tb + 1.0 / tc + 1.0 / kTransposeTBs;
@@ -423,7 +424,7 @@ bool fourstep_split3(int dtype, size_t n, int variant, size_t* a, size_t* b, siz
 }
 
 double fourstep_cost2(int dtype, int variant, size_t n1, size_t n2, bool col) {
-  return 1.0 / sub_tbs(dtype, lg2(n1), variant) + 1.0 / sub_tbs(dtype, lg2(n2), variant) + (col ? 1.0 : 3.0) / 6.9;
+  return 1.0 / sub_tbs(dtype, lg2(n1), variant, col) + 1.0 / sub_tbs(dtype, lg2(n2), variant) + (col ? 1.0 : 3.0) / 6.9;
 }
 
 // The factors a four-step plan runs: two-factor (n1 x n2, column mode or
@@ -469,10 +470,10 @@ class FourStepPlan final : public FastPlan {
     col_ = sh.col;
     three_ = sh.three;
     if (three_) {   // p1_: A columns, pb_: B columns, p2_: C rows
-      pb_ = make_fast_sub(variant, nb_, dtype, tab, nmax, dev, tab64);
+      pb_ = make_fast_sub(variant, nb_, dtype, tab, nmax, dev, tab64, true);
       if (!pb_) throw std::invalid_argument("four-step: no kernel for the middle factor");
     }
-    p1_ = make_fast_sub(variant, n1_, dtype, tab, nmax, dev, tab64);
+    p1_ = make_fast_sub(variant, n1_, dtype, tab, nmax, dev, tab64, col_);
     p2_ = make_fast_sub(variant, n2_, dtype, tab, nmax, dev, tab64);
     if (!p1_ || !p2_) throw std::invalid_argument("four-step: no fused kernel for the sub-transform sizes");
     // half-size twiddle tables: w^(jh B), w^(jl), long double -> double
@@ -704,15 +705,15 @@ OpCount fourstep_op_counts(const amqft_plan_desc& d) {
   OpCount c;
   if (sh.three) {
     const size_t a = sh.n1, b = sh.nb, cc = sh.n2;
-    const OpCount ca = fast_sub_op_counts(d.variant, a, d.dtype), cb = fast_sub_op_counts(d.variant, b, d.dtype),
-                  ccc = fast_sub_op_counts(d.variant, cc, d.dtype);
+    const OpCount ca = fast_sub_op_counts(d.variant, a, d.dtype, true),
+                  cb = fast_sub_op_counts(d.variant, b, d.dtype, true), ccc = fast_sub_op_counts(d.variant, cc, d.dtype);
     c.adds = b * cc * ca.adds + a * cc * cb.adds + a * b * ccc.adds + 2 * 2 * d.n;
     c.muls = b * cc * ca.muls + a * cc * cb.muls + a * b * ccc.muls + 2 * 4 * d.n;
     c.bt = b * cc * ca.bt + a * cc * cb.bt + a * b * ccc.bt;
     return c;
   }
   const size_t n1 = sh.n1, n2 = sh.n2;
-  const OpCount c1 = fast_sub_op_counts(d.variant, n1, d.dtype), c2 = fast_sub_op_counts(d.variant, n2, d.dtype);
+  const OpCount c1 = fast_sub_op_counts(d.variant, n1, d.dtype, sh.col), c2 = fast_sub_op_counts(d.variant, n2, d.dtype);
   c.adds = n2 * c1.adds + n1 * c2.adds + 2 * d.n;
   c.muls = n2 * c1.muls + n1 * c2.muls + 4 * d.n;
   c.bt = n2 * c1.bt + n1 * c2.bt;

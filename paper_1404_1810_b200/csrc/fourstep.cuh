@@ -12,9 +12,11 @@ namespace amqft_b200 {
 
 // Fused / small-CDFT plan for one sub-transform size (nullptr if none),
 // its op counts, and whether a single kernel covers n: fast.cu.
+// columns: the factor runs in column mode (FastPlan::exec_columns), which
+// only the one-thread-per-row kernels have.
 std::unique_ptr<FastPlan> make_fast_sub(int variant, size_t n, int dtype, const void* tab, uint32_t nmax, int dev,
-                                        const void* tab64 = nullptr);
-OpCount fast_sub_op_counts(int variant, size_t n, int dtype);
+                                        const void* tab64 = nullptr, bool columns = false);
+OpCount fast_sub_op_counts(int variant, size_t n, int dtype, bool columns = false);
 bool fast_sub_covered(int dtype, size_t n, int variant);
 
 // CDFT, fast order, N up to 2^26 beyond the single-kernel sizes.

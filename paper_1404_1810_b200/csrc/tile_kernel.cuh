@@ -1,6 +1,7 @@
 // tile_kernel.cuh -- four-step inside one CTA's shared memory (path 6).
 //
-// CDFT N = N1 N2 (fp32, N = 256 .. 4096, N1, N2 <= 64) in ONE pass over HBM:
+// CDFT N = N1 N2 (fp32, N = 16 .. 4096, N1, N2 <= 64; N = 8192 and 16384 as
+// three factors, k_tile3 below) in ONE pass over HBM:
 // both factors are one-thread-per-transform AM-QFTs kept in registers -- the
 // straight-line code codegen/gen_small.py traces from the plan compiler
 // (SmallGen<V, 0, LOGN, float>, every line one reference add/sub/mul,
@@ -226,6 +227,181 @@ class TilePlanImpl final : public FastPlan {
   int grid_cap_ = 148;
 };
 
+// ---- Three factors, N = N1 N2 N3 (N = 8192, 16384: the row no longer
+// fits two register-resident factors of <= 64 points).  n = N2 N3 n1 + N3 n2
+// + n3, k = k1 + N1 k2 + N1 N2 k3, M = N2 N3:
+// phase A  thread = m = N3 n2 + n3: x[M n1 + m] from HBM (coalesced over m),
+//          AM-QFT of length N1, times w_N^(m k1), into Y[k1][n2][n3];
+// phase B  thread = (k1, n3): column n2 of Y[k1] in place (a thread reads
+//          and rewrites its own cells), AM-QFT of length N2, times
+//          w_M^(n3 k2);
+// phase C  thread = (k2, k1), k1 fastest: row Y[k1][k2][.] with 128-bit
+//          loads (pitches N3 + 2 per k2 and N2 (N3 + 2) + 2 per k1: both
+//          halves odd, a quarter-warp hits 8 distinct bank groups), AM-QFT
+//          of length N3, output k3 to X[k1 + N1 (k2 + N2 k3)] (lanes on
+//          consecutive k1).
+template <int LG1, int LG2, int LG3, int T_, int MB_>
+struct T3Cfg {
+  static constexpr int N1 = 1 << LG1, N2 = 1 << LG2, N3 = 1 << LG3, M = N2 * N3, N = N1 * M;
+  static constexpr int T = T_, MINB = MB_;
+  static constexpr int P3 = N3 + 2;              // complex values per (k1, k2) row
+  static constexpr int PM = N2 * P3 + 2;         // complex values per k1 plane
+  static constexpr int ROWP = N1 * PM;
+  static constexpr size_t SMEM = static_cast<size_t>(ROWP) * sizeof(float2);
+  static constexpr int NT1 = (N1 < 8 ? 8 : N1) / 4, NT2 = (N2 < 8 ? 8 : N2) / 4, NT3 = (N3 < 8 ? 8 : N3) / 4;
+  static_assert((P3 / 2) % 2 == 1 && (PM / 2) % 2 == 1, "bank-group spread of the 128-bit row loads");
+};
+
+template <int M, int PM, bool INV>
+struct A3Io {
+  const float2* __restrict__ gi;   // x + m
+  float2* sp;                      // Y + n2 P3 + n3
+  const float2* __restrict__ tw;   // tw1 + m: tw1[k1 M + m] = w_N^(m k1)
+  __device__ __forceinline__ void ld(int c, float& a, float& b, float& d, float& e) const {
+    const float2 u = __ldcs(gi + (2 * c) * M), v = __ldcs(gi + (2 * c + 1) * M);
+    if (INV) { a = u.y; b = u.x; d = v.y; e = v.x; }
+    else { a = u.x; b = u.y; d = v.x; e = v.y; }
+  }
+  __device__ __forceinline__ void st(int c, float a, float b, float d, float e) const {
+    const float2 w1 = __ldg(tw + (2 * c + 1) * M);
+    if (c != 0) {
+      const float2 w = __ldg(tw + (2 * c) * M);
+      const float na = a * w.x - b * w.y, nb = a * w.y + b * w.x;
+      a = na;
+      b = nb;
+    }
+    sp[(2 * c) * PM] = make_float2(a, b);
+    sp[(2 * c + 1) * PM] = make_float2(d * w1.x - e * w1.y, d * w1.y + e * w1.x);
+  }
+};
+
+template <int N3, int P3>
+struct B3Io {
+  float2* sp;                      // Y + k1 PM + n3
+  const float2* __restrict__ tw;   // tw2 + n3: tw2[k2 N3 + n3] = w_M^(n3 k2)
+  __device__ __forceinline__ void ld(int c, float& a, float& b, float& d, float& e) const {
+    const float2 u = sp[(2 * c) * P3], v = sp[(2 * c + 1) * P3];
+    a = u.x; b = u.y; d = v.x; e = v.y;
+  }
+  __device__ __forceinline__ void st(int c, float a, float b, float d, float e) const {
+    const float2 w1 = __ldg(tw + (2 * c + 1) * N3);
+    if (c != 0) {
+      const float2 w = __ldg(tw + (2 * c) * N3);
+      const float na = a * w.x - b * w.y, nb = a * w.y + b * w.x;
+      a = na;
+      b = nb;
+    }
+    sp[(2 * c) * P3] = make_float2(a, b);
+    sp[(2 * c + 1) * P3] = make_float2(d * w1.x - e * w1.y, d * w1.y + e * w1.x);
+  }
+};
+
+template <int V, bool INV, class C>
+__global__ void __launch_bounds__(C::T, C::MINB)
+k_tile3(const float* __restrict__ in, float* __restrict__ out, size_t rows,
+        const __grid_constant__ TabP<float, C::NT1> t1, const __grid_constant__ TabP<float, C::NT2> t2,
+        const __grid_constant__ TabP<float, C::NT3> t3, const float2* __restrict__ tw1,
+        const float2* __restrict__ tw2, float scale) {
+  constexpr int LG1 = 31 - __builtin_clz(C::N1), LG2 = 31 - __builtin_clz(C::N2), LG3 = 31 - __builtin_clz(C::N3);
+  using G1 = SmallGen<V, 0, LG1, float>;
+  using G2 = SmallGen<V, 0, LG2, float>;
+  using G3 = SmallGen<V, 0, LG3, float>;
+  constexpr int N1 = C::N1, N2 = C::N2, N3 = C::N3, M = C::M, N = C::N;
+  extern __shared__ __align__(128) unsigned char sm[];
+  float2* Y = reinterpret_cast<float2*>(sm);
+  const int tid = threadIdx.x;
+  for (size_t row = blockIdx.x; row < rows; row += gridDim.x) {
+    if (tid == 0 && row + gridDim.x < rows)   // the CTA's next row: one bulk prefetch into L2
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                   ::"l"(in + (row + gridDim.x) * 2 * N), "n"(N * 8) : "memory");
+    const float2* x = reinterpret_cast<const float2*>(in) + row * N;
+#pragma unroll 1
+    for (int m = tid; m < M; m += C::T) {
+      A3Io<M, C::PM, INV> io{x + m, Y + (m / N3) * C::P3 + m % N3, tw1 + m};
+      G1::template run<Arith<float>>(io, t1.v);
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int j = tid; j < N1 * N3; j += C::T) {
+      const int n3 = j % N3, k1 = j / N3;
+      B3Io<N3, C::P3> io{Y + k1 * C::PM + n3, tw2 + n3};
+      G2::template run<Arith<float>>(io, t2.v);
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int j = tid; j < N1 * N2; j += C::T) {
+      const int k1 = j % N1, k2 = j / N1;
+      BIo<N1 * N2, INV> io{reinterpret_cast<const float4*>(Y + k1 * C::PM + k2 * C::P3),
+                           reinterpret_cast<float2*>(out) + row * N + k1 + N1 * k2, scale};
+      G3::template run<Arith<float>>(io, t3.v);
+    }
+    __syncthreads();   // Y is rewritten by the next row's phase A
+  }
+}
+
+template <int V, int LG1, int LG2, int LG3, int T, int MB>
+class Tile3PlanImpl final : public FastPlan {
+  using C = T3Cfg<LG1, LG2, LG3, T, MB>;
+
+ public:
+  Tile3PlanImpl(const void* tab, uint32_t nmax, int device) {
+    check_(smallk::fetch_table(t1_.v, C::NT1, tab, nmax));
+    check_(smallk::fetch_table(t2_.v, C::NT2, tab, nmax));
+    check_(smallk::fetch_table(t3_.v, C::NT3, tab, nmax));
+    // tw1[k1 M + m] = w_N^(m k1), tw2[k2 N3 + n3] = w_M^(n3 k2): long double, rounded once
+    const long double two_pi = 6.283185307179586476925286766559005768L;
+    std::vector<float2> tw(static_cast<size_t>(C::N) + C::M);
+    for (int k1 = 0; k1 < C::N1; ++k1)
+      for (int m = 0; m < C::M; ++m) {
+        const long double a = two_pi * static_cast<long double>((k1 * m) % C::N) / static_cast<long double>(C::N);
+        tw[static_cast<size_t>(k1) * C::M + m] = float2{static_cast<float>(cosl(a)), static_cast<float>(-sinl(a))};
+      }
+    for (int k2 = 0; k2 < C::N2; ++k2)
+      for (int n3 = 0; n3 < C::N3; ++n3) {
+        const long double a = two_pi * static_cast<long double>((k2 * n3) % C::M) / static_cast<long double>(C::M);
+        tw[static_cast<size_t>(C::N) + k2 * C::N3 + n3] = float2{static_cast<float>(cosl(a)), static_cast<float>(-sinl(a))};
+      }
+    check_(cudaMalloc(&tw_, tw.size() * sizeof(float2)));
+    check_(cudaMemcpy(tw_, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice));
+    auto f0 = k_tile3<V, false, C>;
+    auto f1 = k_tile3<V, true, C>;
+    check_(cudaFuncSetAttribute(f0, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM)));
+    check_(cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM)));
+    int per_sm = 0;
+    check_(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f0, C::T, C::SMEM));
+    if (per_sm < 1) throw std::runtime_error("three-factor tile kernel does not fit an SM");
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    grid_cap_ = per_sm * sms;
+    launches = 1;
+  }
+  ~Tile3PlanImpl() override {
+    if (tw_) cudaFree(tw_);
+  }
+  void exec(const void* in, void* out, size_t rows, int inverse, cudaStream_t st) override {
+    const unsigned grid = static_cast<unsigned>(std::min<size_t>(rows, static_cast<size_t>(grid_cap_)));
+    const float scale = 1.0f / static_cast<float>(C::N);
+    if (inverse)
+      k_tile3<V, true, C><<<grid, C::T, C::SMEM, st>>>(static_cast<const float*>(in), static_cast<float*>(out), rows,
+                                                       t1_, t2_, t3_, tw_, tw_ + C::N, scale);
+    else
+      k_tile3<V, false, C><<<grid, C::T, C::SMEM, st>>>(static_cast<const float*>(in), static_cast<float*>(out), rows,
+                                                        t1_, t2_, t3_, tw_, tw_ + C::N, scale);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+  }
+
+ private:
+  static void check_(cudaError_t e) {
+    if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+  }
+  TabP<float, C::NT1> t1_{};
+  TabP<float, C::NT2> t2_{};
+  TabP<float, C::NT3> t3_{};
+  float2* tw_ = nullptr;
+  int grid_cap_ = 148;
+};
+
 // The split per size: N1 (phase A, strided columns) x N2 (phase B, rows).
 template <int V>
 std::unique_ptr<FastPlan> make_tile(size_t n, const void* tab, uint32_t nmax, int dev) {
@@ -236,6 +412,8 @@ std::unique_ptr<FastPlan> make_tile(size_t n, const void* tab, uint32_t nmax, in
     if ((n == 2048 || n == 512) && std::getenv("AMQFT_TILE_SWAP")) n += 1;   // the swapped splits
 #define AMQFT_TILE_CASE(NN, A, B, TT, MM, FF) \
     if (n == NN && t == TT && mb == MM && fl == FF) return std::make_unique<TilePlanImpl<V, A, B, TT, MM, FF>>(tab, nmax, dev);
+    if (n == 8192 && t == 256) return std::make_unique<Tile3PlanImpl<V, 4, 4, 5, 256, 2>>(tab, nmax, dev);
+    if (n == 16384 && t == 256) return std::make_unique<Tile3PlanImpl<V, 4, 5, 5, 512, 1>>(tab, nmax, dev);
     AMQFT_TILE_CASE(4096, 6, 6, 64, 4, 0)
     AMQFT_TILE_CASE(4096, 6, 6, 64, 4, 1)
     AMQFT_TILE_CASE(4096, 6, 6, 64, 5, 1)
@@ -253,11 +431,19 @@ std::unique_ptr<FastPlan> make_tile(size_t n, const void* tab, uint32_t nmax, in
   }
 #endif
   switch (n) {
+    case 16: return std::make_unique<TilePlanImpl<V, 2, 2>>(tab, nmax, dev);
+    case 32: return std::make_unique<TilePlanImpl<V, 2, 3>>(tab, nmax, dev);
+    case 64: return std::make_unique<TilePlanImpl<V, 3, 3>>(tab, nmax, dev);
+    case 128: return std::make_unique<TilePlanImpl<V, 3, 4>>(tab, nmax, dev);
     case 256: return std::make_unique<TilePlanImpl<V, 4, 4>>(tab, nmax, dev);
     case 512: return std::make_unique<TilePlanImpl<V, 4, 5>>(tab, nmax, dev);
     case 1024: return std::make_unique<TilePlanImpl<V, 5, 5>>(tab, nmax, dev);
     case 2048: return std::make_unique<TilePlanImpl<V, 6, 5>>(tab, nmax, dev);   // 0.780 vs 0.803 ms for 32 x 64
     case 4096: return std::make_unique<TilePlanImpl<V, 6, 6>>(tab, nmax, dev);
+    // measured (B200, ms per 2^28 reals): 32 x 16 x 16 at 256 threads x 2 CTAs 0.747; 16 x 16 x 32 0.802
+    case 8192: return std::make_unique<Tile3PlanImpl<V, 5, 4, 4, 256, 2>>(tab, nmax, dev);
+    // 32 x 16 x 32 at 512 threads 0.843; 16 x 32 x 32 0.959; 32 x 32 x 16 0.928
+    case 16384: return std::make_unique<Tile3PlanImpl<V, 5, 4, 5, 512, 1>>(tab, nmax, dev);
   }
   return nullptr;
 }

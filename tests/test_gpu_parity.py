@@ -614,10 +614,10 @@ def test_fourstep_fp64_config3_sizes(oracle, restatement, lg):
 
 
 def test_fourstep_fp32_between_kernel_sizes(oracle, restatement):
-    """fp32 N = 2^14 .. 2^19 run as four-steps (were the generic path); v4
-    at 2^14 takes the cluster four-step (tests/test_gpu_cluster.py), so v3."""
+    """fp32 N = 2^15 .. 2^19 run as multi-pass four-steps (N <= 2^14: the
+    in-shared-memory four-step, tests/test_gpu_tile.py)."""
     r, O = restatement, oracle
-    for lg in (14, 17, 19):
+    for lg in (15, 17, 19):
         n = 1 << lg
         x = np.random.default_rng(lg).standard_normal(2 * n).astype(np.float32)
         want = r.execute(3, O.F_CDFT, n, x.astype(np.float64))
@@ -754,7 +754,7 @@ def test_real_inverse_fp32_round_trip():
         assert float((z - x).norm() / x.norm()) < 1e-5 * math.log2(n), (f, n)
 
 
-def test_small_kernels_in_place():
+def test_small_kernels_in_place(no_tile):
     """d_in == d_out on the small kernels' global-memory paths (CDFT rows of
     <= 64 B, DCT/DST rows past the last full tile) and the staged paths:
     bitwise the out-of-place result (regression: the row I/O must not be
@@ -923,7 +923,8 @@ def test_fp32_sine_variants_large_n(oracle, restatement, lg):
     ref = numpy_dft(x)
     for v in range(5, 9):
         plan = amqft.Plan(v, amqft.FunctionId.Cdft, n, 1, dtype="f32", order=amqft.Order.Fast)
-        assert plan.path()[0] == 3
+        # one pass in shared memory up to 2^14 (tile_kernel.cuh), the multi-pass four-step above
+        assert plan.path()[0] == (6 if lg <= 14 else 3)
         got = run_plan(plan, [x])[0]
         assert r.rel_l2(got, ref) <= tol, (v, lg)
         if lg == 13:

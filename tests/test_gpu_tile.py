@@ -1,6 +1,7 @@
-"""In-shared-memory four-step (path 6, tile_kernel.cuh): fp32 CDFT N = 256 ..
-4096 as N1 x N2 register-resident AM-QFT factors, one pass over HBM -- the
-default fast-order path for these sizes (config 2 is N = 4096).
+"""In-shared-memory four-step (path 6, tile_kernel.cuh): fp32 CDFT N = 16 ..
+16384 as N1 x N2 (x N3 from N = 8192) register-resident AM-QFT factors, one
+pass over HBM -- the default fast-order path for these sizes (config 2 is
+N = 4096).
 
 Checked for ALL 8 variants against the fp64 CPU reference of the same variant
 (tolerance 1e-5 log2 N, BASELINE north_star; the factors are <= 64 points, where
@@ -20,9 +21,14 @@ pytestmark = pytest.mark.gpu
 import paper_1404_1810_b200 as amqft  # noqa: E402
 from test_gpu_parity import DEV, numpy_dft, run_plan  # noqa: E402
 
-SIZES = [256, 512, 1024, 2048, 4096]
-# the kernel's split (tile_kernel.cuh make_tile): N1 (phase A) x N2 (phase B)
-SPLIT = {256: (16, 16), 512: (16, 32), 1024: (32, 32), 2048: (64, 32), 4096: (64, 64)}
+SIZES = [16, 32, 64, 128, 256, 512, 1024, 2048, 4096, 8192, 16384]
+# the kernel's split (tile_kernel.cuh make_tile): N1 (phase A) x N2 (phase B) [x N3 (phase C)]
+SPLIT = {16: (4, 4), 32: (4, 8), 64: (8, 8), 128: (8, 16), 256: (16, 16), 512: (16, 32), 1024: (32, 32),
+         2048: (64, 32), 4096: (64, 64), 8192: (32, 16, 16), 16384: (32, 16, 32)}
+
+
+def rows_per_tile(n):
+    return 1 if len(SPLIT[n]) == 3 else max(1, 64 // min(SPLIT[n]))
 # measured on the B200: 1e-7 .. 4e-7 (v1-4), up to 6e-7 vs numpy for v5-8;
 # the bar below is 10x tighter than the north-star tolerance
 TIGHT = 2e-6
@@ -44,11 +50,13 @@ def test_tile_all_variants_match_cpu(oracle, restatement, n):
         plan = _plan(v, n, rows)
         got = run_plan(plan, xs)
         for row in (0, rows - 1):
+            assert r.rel_l2(got[row], numpy_dft(xs[row])) <= TIGHT, (v, n)
+            if v >= 5 and n > 4096:
+                continue   # the reference's own fp64 v5-8 drift from the DFT (1e-3 at 2^13, O(1) at 2^14)
             want = r.execute(v, O.F_CDFT, n, xs[row])
             err = r.rel_l2(got[row], want)
             # the reference's own fp64 v5-8 result is ~1e-6 from the DFT at 4096
             assert err <= (tol if v >= 5 else TIGHT), (v, n, err)
-            assert r.rel_l2(got[row], numpy_dft(xs[row])) <= TIGHT, (v, n)
         back = run_plan(plan, got.astype(np.float32), inverse=True)
         assert r.rel_l2(back.ravel(), xs.ravel()) <= TIGHT, (v, n)
 
@@ -69,9 +77,8 @@ def test_tile_ragged_batches_and_rows_independent(n):
     iteration) and beyond one wave of CTAs: every row equals the same row
     transformed alone (bitwise: a row's arithmetic does not depend on its
     position in the batch)."""
-    n1, n2 = SPLIT[n]
-    R = max(1, 64 // min(n1, n2))
-    big = 148 * 16 * R + R + 1          # more tiles than resident CTAs, last tile partial
+    R = rows_per_tile(n)
+    big = min(148 * 16 * R + R + 1, (1 << 27) // n)   # more tiles than resident CTAs, last tile partial
     rng = np.random.default_rng(n + 1)
     x = torch.tensor(rng.standard_normal((big, 2 * n)), dtype=torch.float32, device=DEV)
     plan = _plan(4, n, big)
@@ -111,14 +118,19 @@ def test_tile_in_place(n):
 def test_tile_op_counts(oracle, restatement, n):
     """Meter of the executed schedule: N2 reference DAGs of length N1, N1 of
     length N2 (the reference meter of each) and one complex twiddle multiply
-    per element (4 muls + 2 adds), the four-step's accounting."""
+    per element (4 muls + 2 adds), the four-step's accounting (three factors:
+    two twiddle passes)."""
     r, O = restatement, oracle
-    n1, n2 = SPLIT[n]
+    f = SPLIT[n]
     for v in (1, 4, 6):
-        m1 = r.execute(v, O.F_CDFT, n1, np.zeros(2 * n1), meter=True)[1]
-        m2 = r.execute(v, O.F_CDFT, n2, np.zeros(2 * n2), meter=True)[1]
-        want = (n2 * m1[0] + n1 * m2[0] + 2 * n, n2 * m1[1] + n1 * m2[1] + 4 * n, n2 * m1[2] + n1 * m2[2])
-        assert _plan(v, n, 1).op_counts() == want, (v, n)
+        want = [0, 0, 0]
+        for nf in f:   # n / nf reference DAGs of length nf per factor
+            m = r.execute(v, O.F_CDFT, nf, np.zeros(2 * nf), meter=True)[1]
+            for i in range(3):
+                want[i] += (n // nf) * m[i]
+        want[0] += 2 * n * (len(f) - 1)   # one twiddle pass per extra factor
+        want[1] += 4 * n * (len(f) - 1)
+        assert _plan(v, n, 1).op_counts() == tuple(want), (v, n)
 
 
 def test_tile_rejects_misaligned_buffers():
