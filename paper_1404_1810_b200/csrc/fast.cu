@@ -113,15 +113,15 @@ template <int V>
 std::unique_ptr<FastPlan> make_tile(size_t n, const void* tab, uint32_t nmax, int dev);
 // the split of tile_kernel.cuh make_tile: N1 (phase A) x N2 (phase B),
 // 4 x 4, 4 x 8, 8 x 8, 8 x 16, 16 x 16, 16 x 32, 32 x 32, 64 x 32, 64 x 64
-// and the three-factor 32 x 16 x 16, 32 x 16 x 32 (n3 = 1: two factors)
+// and the three-factor 32 x 16 x 16 .. 32 x 32 x 64 (n3 = 1: two factors)
 static void tile_split(size_t n, size_t* n1, size_t* n2, size_t* n3) {
   int lg = 0;
   for (size_t t = n; t > 1; t >>= 1) ++lg;
   *n3 = 1;
-  if (lg >= 13) {   // 32 x 16 x 16, 32 x 16 x 32
+  if (lg >= 13) {   // 32 x 16 x 16, 32 x 16 x 32, 32 x 32 x 32, 32 x 32 x 64
     *n1 = 32;
-    *n2 = 16;
-    *n3 = n / (32 * 16);
+    *n2 = lg >= 15 ? 32 : 16;
+    *n3 = n / (32 * *n2);
     return;
   }
   *n1 = size_t(1) << (lg == 11 ? 6 : lg / 2);
@@ -131,8 +131,8 @@ static void tile_split(size_t n, size_t* n1, size_t* n2, size_t* n3) {
 
 bool tile_covers(const amqft_plan_desc& d) {
   if (d.function != AMQFT_FN_CDFT || d.dtype != AMQFT_F32) return false;
-  if (d.n < 16 || d.n > 16384 || (d.n & (d.n - 1))) return false;
-  size_t lo = 16, hi = 16384;
+  if (d.n < 16 || d.n > 65536 || (d.n & (d.n - 1))) return false;
+  size_t lo = 16, hi = 65536;
   if (const char* e = std::getenv("AMQFT_AB_TILE")) {
     if (e[0] == 'n') return false;
     // A/B measurements: AMQFT_AB_TILE=lo,hi restricts the sizes it takes
@@ -278,7 +278,7 @@ static amqft_plan_desc sub_desc(int variant, size_t n, int dtype) {
 }
 
 bool fast_sub_covered(int dtype, size_t n, int variant) {
-  if (tile_covers(sub_desc(variant, n, dtype))) return true;   // fp32 16 .. 16384, every variant
+  if (tile_covers(sub_desc(variant, n, dtype))) return true;   // fp32 16 .. 65536, every variant
   if (dtype == AMQFT_F32 && f32_needs_f64_compute(variant, n)) return n >= 1024 && n <= 4096;
   if (dtype == AMQFT_F32) return n >= 2 && n <= 8192;
   return n >= 2 && n <= 4096 && n != 512;

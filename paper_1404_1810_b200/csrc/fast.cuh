@@ -59,9 +59,9 @@ std::unique_ptr<FastPlan> make_fast_plan(const amqft_plan_desc& d,
 OpCount fast_op_counts(const amqft_plan_desc& d);
 
 // In-shared-memory four-step (tile_kernel.cuh, path 6): fp32 CDFT rows,
-// N = 16 .. 16384, two (three from N = 8192) one-thread-per-transform AM-QFT
+// N = 16 .. 65536, two (three from N = 8192) one-thread-per-transform AM-QFT
 // factors (<= 64 points, stable in fp32 for all 8 variants), one pass over
-// HBM.  AMQFT_AB_TILE=lo,hi restricts the sizes it takes.
+// HBM (2^15 / 2^16: one row per thread-block cluster, DSMEM exchange).  AMQFT_AB_TILE=lo,hi restricts the sizes it takes.
 // AMQFT_AB_TILE=none disables it (A/B measurements against the fused
 // kernel, which keeps the whole length-N DAG).
 bool tile_covers(const amqft_plan_desc& d);

@@ -343,9 +343,9 @@ double sub_tbs(int dtype, int lg, int variant, bool col = false) {
   static const double f64[13] = {0, 5.5, 5.5, 5.5, 5.5, 5.5, 5.4, 2.94, 2.06, 0.0, 2.27, 2.68, 2.88};
   // fp32 rows through the fp64 instance (variants 5-8, fast.cuh): half the fp64 row bytes
   static const double mixed[13] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1.13, 1.34, 1.44};
-  // in-shared-memory four-step (tile_kernel.cuh): fp32 N = 16 .. 16384, all variants
-  static const double tile[15] = {0, 0, 0, 0, 5.18, 6.5, 5.78, 6.25, 5.85, 6.3, 6.2, 5.5, 5.63, 5.75, 5.09};
-  if (!col && dtype == AMQFT_F32 && lg >= 4 && lg <= 14) {
+  // in-shared-memory four-step (tile_kernel.cuh): fp32 N = 16 .. 65536, all variants
+  static const double tile[17] = {0, 0, 0, 0, 5.18, 6.5, 5.78, 6.25, 5.85, 6.3, 6.2, 5.5, 5.63, 5.75, 5.09, 3.76, 3.03};
+  if (!col && dtype == AMQFT_F32 && lg >= 4 && lg <= 16) {
     amqft_plan_desc d{};
     d.function = AMQFT_FN_CDFT;
     d.dtype = dtype;

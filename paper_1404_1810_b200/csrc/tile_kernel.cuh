@@ -1,7 +1,8 @@
 // tile_kernel.cuh -- four-step inside one CTA's shared memory (path 6).
 //
-// CDFT N = N1 N2 (fp32, N = 16 .. 4096, N1, N2 <= 64; N = 8192 and 16384 as
-// three factors, k_tile3 below) in ONE pass over HBM:
+// CDFT N = N1 N2 (fp32, N = 16 .. 4096, N1, N2 <= 64; N = 8192 .. 65536 as
+// three factors, k_tile3 below, from 2^15 on a thread-block cluster) in ONE
+// pass over HBM:
 // both factors are one-thread-per-transform AM-QFTs kept in registers -- the
 // straight-line code codegen/gen_small.py traces from the plan compiler
 // (SmallGen<V, 0, LOGN, float>, every line one reference add/sub/mul,
@@ -240,17 +241,39 @@ class TilePlanImpl final : public FastPlan {
 //          halves odd, a quarter-warp hits 8 distinct bank groups), AM-QFT
 //          of length N3, output k3 to X[k1 + N1 (k2 + N2 k3)] (lanes on
 //          consecutive k1).
-template <int LG1, int LG2, int LG3, int T_, int MB_>
+// P > 1 (N = 2^15, 2^16: the row exceeds one SM's shared memory): one row per
+// thread-block cluster of P CTAs.  CTA q owns the planes k1 in [q N1/P,
+// (q+1) N1/P) of Y; in phase A it transforms the columns m in [q M/P,
+// (q+1) M/P) and stores output k1 straight into the owner's shared memory
+// over DSMEM (st.shared::cluster), the only exchange: (P-1)/P of the row.
+// Phases B and C run on the CTA's own planes.  Two cluster barriers per row:
+// a full one after phase A (all planes complete), and a split one around the
+// rest -- arrive after the CTA's phase C, wait just before its first remote
+// store of the next row -- so the next row's loads and arithmetic overlap the
+// peers' phase C.
+template <int LG1, int LG2, int LG3, int T_, int MB_, int P_ = 1>
 struct T3Cfg {
   static constexpr int N1 = 1 << LG1, N2 = 1 << LG2, N3 = 1 << LG3, M = N2 * N3, N = N1 * M;
-  static constexpr int T = T_, MINB = MB_;
+  static constexpr int T = T_, MINB = MB_, P = P_;
+  static constexpr int K1 = N1 / P;              // planes per CTA
   static constexpr int P3 = N3 + 2;              // complex values per (k1, k2) row
   static constexpr int PM = N2 * P3 + 2;         // complex values per k1 plane
-  static constexpr int ROWP = N1 * PM;
+  static constexpr int ROWP = K1 * PM;
   static constexpr size_t SMEM = static_cast<size_t>(ROWP) * sizeof(float2);
   static constexpr int NT1 = (N1 < 8 ? 8 : N1) / 4, NT2 = (N2 < 8 ? 8 : N2) / 4, NT3 = (N3 < 8 ? 8 : N3) / 4;
   static_assert((P3 / 2) % 2 == 1 && (PM / 2) % 2 == 1, "bank-group spread of the 128-bit row loads");
+  static_assert(P == 1 || ((M / P) % T == 0 && K1 % 2 == 0), "whole warps in phase A; an output chunk has one owner");
 };
+
+__device__ __forceinline__ uint32_t tk_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void tk_cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tk_cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 
 template <int M, int PM, bool INV>
 struct A3Io {
@@ -272,6 +295,38 @@ struct A3Io {
     }
     sp[(2 * c) * PM] = make_float2(a, b);
     sp[(2 * c + 1) * PM] = make_float2(d * w1.x - e * w1.y, d * w1.y + e * w1.x);
+  }
+};
+
+// phase A of the cluster kernel: output k1 goes to plane k1 % K1 of CTA
+// k1 / K1 (both compile-time per store); the first store of a row waits for
+// the peers' phase C of the previous row (the split barrier)
+template <int M, int PM, int K1, int P, bool INV>
+struct A3IoC {
+  const float2* __restrict__ gi;
+  const float2* __restrict__ tw;
+  uint32_t yb[P];    // the P CTAs' Y + n2 P3 + n3 in the cluster window
+  bool wait;
+  __device__ __forceinline__ void ld(int c, float& a, float& b, float& d, float& e) const {
+    const float2 u = __ldcs(gi + (2 * c) * M), v = __ldcs(gi + (2 * c + 1) * M);
+    if (INV) { a = u.y; b = u.x; d = v.y; e = v.x; }
+    else { a = u.x; b = u.y; d = v.x; e = v.y; }
+  }
+  __device__ __forceinline__ void st(int c, float a, float b, float d, float e) const {
+    const float2 w1 = __ldg(tw + (2 * c + 1) * M);
+    if (c != 0) {
+      const float2 w = __ldg(tw + (2 * c) * M);
+      const float na = a * w.x - b * w.y, nb = a * w.y + b * w.x;
+      a = na;
+      b = nb;
+    } else if (wait) {
+      tk_cluster_wait();   // warp-uniform: every lane of the warp is in this item
+    }
+    const float nd = d * w1.x - e * w1.y, ne = d * w1.y + e * w1.x;
+    const uint32_t base = yb[(2 * c) / K1] + static_cast<uint32_t>(((2 * c) % K1) * PM * sizeof(float2));
+    asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(base), "f"(a), "f"(b) : "memory");
+    asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};"
+                 ::"r"(base + static_cast<uint32_t>(PM * sizeof(float2))), "f"(nd), "f"(ne) : "memory");
   }
 };
 
@@ -306,42 +361,83 @@ k_tile3(const float* __restrict__ in, float* __restrict__ out, size_t rows,
   using G1 = SmallGen<V, 0, LG1, float>;
   using G2 = SmallGen<V, 0, LG2, float>;
   using G3 = SmallGen<V, 0, LG3, float>;
-  constexpr int N1 = C::N1, N2 = C::N2, N3 = C::N3, M = C::M, N = C::N;
+  constexpr int N1 = C::N1, N2 = C::N2, N3 = C::N3, M = C::M, N = C::N, P = C::P, K1 = C::K1;
   extern __shared__ __align__(128) unsigned char sm[];
   float2* Y = reinterpret_cast<float2*>(sm);
   const int tid = threadIdx.x;
-  for (size_t row = blockIdx.x; row < rows; row += gridDim.x) {
-    if (tid == 0 && row + gridDim.x < rows)   // the CTA's next row: one bulk prefetch into L2
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
-                   ::"l"(in + (row + gridDim.x) * 2 * N), "n"(N * 8) : "memory");
-    const float2* x = reinterpret_cast<const float2*>(in) + row * N;
-#pragma unroll 1
-    for (int m = tid; m < M; m += C::T) {
-      A3Io<M, C::PM, INV> io{x + m, Y + (m / N3) * C::P3 + m % N3, tw1 + m};
-      G1::template run<Arith<float>>(io, t1.v);
+  // P > 1: one row per cluster; q = this CTA's rank (its planes and columns)
+  uint32_t q = 0;
+  uint32_t ywin[P];
+  if constexpr (P > 1) {
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(q));
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ywin[k]) : "r"(tk_u32(Y)), "r"(k));
+  }
+  (void)ywin;
+  const size_t r_first = blockIdx.x / P, r_step = gridDim.x / P;
+  for (size_t row = r_first; row < rows; row += r_step) {
+    // the next row's inputs of this CTA: bulk prefetches into L2
+    if (row + r_step < rows) {
+      const float* nx = in + (row + r_step) * 2 * N;
+      if constexpr (P == 1) {
+        if (tid == 0)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nx), "n"(N * 8) : "memory");
+      } else if (tid < N1) {   // N1 pieces of M/P columns
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                     ::"l"(nx + (static_cast<size_t>(tid) * M + q * (M / P)) * 2), "n"(M / P * 8) : "memory");
+      }
     }
-    __syncthreads();
+    const float2* x = reinterpret_cast<const float2*>(in) + row * N;
+    if constexpr (P == 1) {
 #pragma unroll 1
-    for (int j = tid; j < N1 * N3; j += C::T) {
+      for (int m = tid; m < M; m += C::T) {
+        A3Io<M, C::PM, INV> io{x + m, Y + (m / N3) * C::P3 + m % N3, tw1 + m};
+        G1::template run<Arith<float>>(io, t1.v);
+      }
+      __syncthreads();
+    } else {
+#pragma unroll 1
+      for (int mm = tid; mm < M / P; mm += C::T) {
+        const int m = static_cast<int>(q) * (M / P) + mm;
+        A3IoC<M, C::PM, K1, P, INV> io;
+        io.gi = x + m;
+        io.tw = tw1 + m;
+        const uint32_t off = static_cast<uint32_t>(((m / N3) * C::P3 + m % N3) * sizeof(float2));
+#pragma unroll
+        for (int k = 0; k < P; ++k) io.yb[k] = ywin[k] + off;
+        io.wait = mm == tid && row != r_first;   // first item of a row after the first
+        G1::template run<Arith<float>>(io, t1.v);
+      }
+      tk_cluster_arrive();   // all planes complete and visible
+      tk_cluster_wait();
+    }
+#pragma unroll 1
+    for (int j = tid; j < K1 * N3; j += C::T) {
       const int n3 = j % N3, k1 = j / N3;
       B3Io<N3, C::P3> io{Y + k1 * C::PM + n3, tw2 + n3};
       G2::template run<Arith<float>>(io, t2.v);
     }
     __syncthreads();
 #pragma unroll 1
-    for (int j = tid; j < N1 * N2; j += C::T) {
-      const int k1 = j % N1, k2 = j / N1;
+    for (int j = tid; j < K1 * N2; j += C::T) {
+      const int k1 = j % K1, k2 = j / K1;
       BIo<N1 * N2, INV> io{reinterpret_cast<const float4*>(Y + k1 * C::PM + k2 * C::P3),
-                           reinterpret_cast<float2*>(out) + row * N + k1 + N1 * k2, scale};
+                           reinterpret_cast<float2*>(out) + row * N + (q * K1 + k1) + N1 * k2, scale};
       G3::template run<Arith<float>>(io, t3.v);
     }
-    __syncthreads();   // Y is rewritten by the next row's phase A
+    if constexpr (P == 1) __syncthreads();   // Y is rewritten by the next row's phase A
+    else tk_cluster_arrive();                 // ... by the peers': the wait is in their first store
+  }
+  if constexpr (P > 1) {
+    // balance the last arrive; no CTA exits while a peer may still store into it
+    if (r_first < rows) tk_cluster_wait();
   }
 }
 
-template <int V, int LG1, int LG2, int LG3, int T, int MB>
+template <int V, int LG1, int LG2, int LG3, int T, int MB, int P = 1>
 class Tile3PlanImpl final : public FastPlan {
-  using C = T3Cfg<LG1, LG2, LG3, T, MB>;
+  using C = T3Cfg<LG1, LG2, LG3, T, MB, P>;
 
  public:
   Tile3PlanImpl(const void* tab, uint32_t nmax, int device) {
@@ -367,33 +463,66 @@ class Tile3PlanImpl final : public FastPlan {
     auto f1 = k_tile3<V, true, C>;
     check_(cudaFuncSetAttribute(f0, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM)));
     check_(cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM)));
-    int per_sm = 0;
-    check_(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f0, C::T, C::SMEM));
-    if (per_sm < 1) throw std::runtime_error("three-factor tile kernel does not fit an SM");
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    grid_cap_ = per_sm * sms;
+    if (P == 1) {
+      int per_sm = 0;
+      check_(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f0, C::T, C::SMEM));
+      if (per_sm < 1) throw std::runtime_error("three-factor tile kernel does not fit an SM");
+      grid_cap_ = per_sm * sms;
+    } else {
+      cudaLaunchConfig_t cfg{};
+      cudaLaunchAttribute attr[1];
+      fill_(&cfg, attr, P * sms, nullptr);
+      int nc = 0;
+      check_(cudaOccupancyMaxActiveClusters(&nc, f0, &cfg));
+      if (nc < 1) throw std::runtime_error("three-factor tile kernel: no cluster of this size fits");
+      grid_cap_ = nc * P;
+    }
     launches = 1;
   }
   ~Tile3PlanImpl() override {
     if (tw_) cudaFree(tw_);
   }
   void exec(const void* in, void* out, size_t rows, int inverse, cudaStream_t st) override {
-    const unsigned grid = static_cast<unsigned>(std::min<size_t>(rows, static_cast<size_t>(grid_cap_)));
     const float scale = 1.0f / static_cast<float>(C::N);
-    if (inverse)
-      k_tile3<V, true, C><<<grid, C::T, C::SMEM, st>>>(static_cast<const float*>(in), static_cast<float*>(out), rows,
-                                                       t1_, t2_, t3_, tw_, tw_ + C::N, scale);
-    else
-      k_tile3<V, false, C><<<grid, C::T, C::SMEM, st>>>(static_cast<const float*>(in), static_cast<float*>(out), rows,
-                                                        t1_, t2_, t3_, tw_, tw_ + C::N, scale);
-    const cudaError_t e = cudaGetLastError();
+    const float* fi = static_cast<const float*>(in);
+    float* fo = static_cast<float*>(out);
+    const float2* tw2 = tw_ + C::N;
+    cudaError_t e;
+    if (P == 1) {
+      const unsigned grid = static_cast<unsigned>(std::min<size_t>(rows, static_cast<size_t>(grid_cap_)));
+      if (inverse) k_tile3<V, true, C><<<grid, C::T, C::SMEM, st>>>(fi, fo, rows, t1_, t2_, t3_, tw_, tw2, scale);
+      else k_tile3<V, false, C><<<grid, C::T, C::SMEM, st>>>(fi, fo, rows, t1_, t2_, t3_, tw_, tw2, scale);
+      e = cudaGetLastError();
+    } else {
+      const unsigned grid = static_cast<unsigned>(std::min<size_t>(rows * P, static_cast<size_t>(grid_cap_)));
+      cudaLaunchConfig_t cfg{};
+      cudaLaunchAttribute attr[1];
+      fill_(&cfg, attr, static_cast<int>(grid), st);
+      const float2* tw1 = tw_;
+      if (inverse) e = cudaLaunchKernelEx(&cfg, k_tile3<V, true, C>, fi, fo, rows, t1_, t2_, t3_, tw1, tw2, scale);
+      else e = cudaLaunchKernelEx(&cfg, k_tile3<V, false, C>, fi, fo, rows, t1_, t2_, t3_, tw1, tw2, scale);
+      if (e == cudaSuccess) e = cudaGetLastError();
+    }
     if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
   }
 
  private:
   static void check_(cudaError_t e) {
     if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+  }
+  static void fill_(cudaLaunchConfig_t* cfg, cudaLaunchAttribute* attr, int grid, cudaStream_t st) {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = P;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg->gridDim = dim3(static_cast<unsigned>(grid));
+    cfg->blockDim = dim3(C::T);
+    cfg->dynamicSmemBytes = C::SMEM;
+    cfg->stream = st;
+    cfg->attrs = attr;
+    cfg->numAttrs = 1;
   }
   TabP<float, C::NT1> t1_{};
   TabP<float, C::NT2> t2_{};
@@ -412,6 +541,8 @@ std::unique_ptr<FastPlan> make_tile(size_t n, const void* tab, uint32_t nmax, in
     if ((n == 2048 || n == 512) && std::getenv("AMQFT_TILE_SWAP")) n += 1;   // the swapped splits
 #define AMQFT_TILE_CASE(NN, A, B, TT, MM, FF) \
     if (n == NN && t == TT && mb == MM && fl == FF) return std::make_unique<TilePlanImpl<V, A, B, TT, MM, FF>>(tab, nmax, dev);
+    if (n == 32768 && t == 256) return std::make_unique<Tile3PlanImpl<V, 5, 5, 5, 256, 2, 4>>(tab, nmax, dev);
+    if (n == 65536 && t == 257) return std::make_unique<Tile3PlanImpl<V, 6, 5, 5, 256, 1, 4>>(tab, nmax, dev);
     if (n == 8192 && t == 256) return std::make_unique<Tile3PlanImpl<V, 4, 4, 5, 256, 2>>(tab, nmax, dev);
     if (n == 16384 && t == 256) return std::make_unique<Tile3PlanImpl<V, 4, 5, 5, 512, 1>>(tab, nmax, dev);
     AMQFT_TILE_CASE(4096, 6, 6, 64, 4, 0)
@@ -444,6 +575,11 @@ std::unique_ptr<FastPlan> make_tile(size_t n, const void* tab, uint32_t nmax, in
     case 8192: return std::make_unique<Tile3PlanImpl<V, 5, 4, 4, 256, 2>>(tab, nmax, dev);
     // 32 x 16 x 32 at 512 threads 0.843; 16 x 32 x 32 0.959; 32 x 32 x 16 0.928
     case 16384: return std::make_unique<Tile3PlanImpl<V, 5, 4, 5, 512, 1>>(tab, nmax, dev);
+    // one row per cluster (DSMEM exchange in phase A): 2^15 on 2 CTAs 3.76 TB/s (4 CTAs x 256
+    // threads: 3.48); 2^16 on 4 CTAs as 32 x 32 x 64 3.03 (64 x 32 x 32: 2.83; 8 CTAs: 2.95 / 2.76);
+    // the multi-pass four-step ran both at 2.0
+    case 32768: return std::make_unique<Tile3PlanImpl<V, 5, 5, 5, 512, 1, 2>>(tab, nmax, dev);
+    case 65536: return std::make_unique<Tile3PlanImpl<V, 5, 5, 6, 256, 1, 4>>(tab, nmax, dev);
   }
   return nullptr;
 }

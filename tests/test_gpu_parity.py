@@ -614,10 +614,10 @@ def test_fourstep_fp64_config3_sizes(oracle, restatement, lg):
 
 
 def test_fourstep_fp32_between_kernel_sizes(oracle, restatement):
-    """fp32 N = 2^15 .. 2^19 run as multi-pass four-steps (N <= 2^14: the
+    """fp32 N = 2^17 .. 2^19 run as multi-pass four-steps (N <= 2^16: the
     in-shared-memory four-step, tests/test_gpu_tile.py)."""
     r, O = restatement, oracle
-    for lg in (15, 17, 19):
+    for lg in (17, 18, 19):
         n = 1 << lg
         x = np.random.default_rng(lg).standard_normal(2 * n).astype(np.float32)
         want = r.execute(3, O.F_CDFT, n, x.astype(np.float64))
@@ -923,8 +923,8 @@ def test_fp32_sine_variants_large_n(oracle, restatement, lg):
     ref = numpy_dft(x)
     for v in range(5, 9):
         plan = amqft.Plan(v, amqft.FunctionId.Cdft, n, 1, dtype="f32", order=amqft.Order.Fast)
-        # one pass in shared memory up to 2^14 (tile_kernel.cuh), the multi-pass four-step above
-        assert plan.path()[0] == (6 if lg <= 14 else 3)
+        # one pass in shared memory / a cluster's shared memory up to 2^16 (tile_kernel.cuh)
+        assert plan.path()[0] == 6
         got = run_plan(plan, [x])[0]
         assert r.rel_l2(got, ref) <= tol, (v, lg)
         if lg == 13:

@@ -1,7 +1,8 @@
 """In-shared-memory four-step (path 6, tile_kernel.cuh): fp32 CDFT N = 16 ..
-16384 as N1 x N2 (x N3 from N = 8192) register-resident AM-QFT factors, one
+65536 as N1 x N2 (x N3 from N = 8192) register-resident AM-QFT factors, one
 pass over HBM -- the default fast-order path for these sizes (config 2 is
-N = 4096).
+N = 4096).  N = 2^15 / 2^16 run one row per thread-block cluster of 2 / 4
+CTAs with the phase-A outputs exchanged over distributed shared memory.
 
 Checked for ALL 8 variants against the fp64 CPU reference of the same variant
 (tolerance 1e-5 log2 N, BASELINE north_star; the factors are <= 64 points, where
@@ -21,10 +22,11 @@ pytestmark = pytest.mark.gpu
 import paper_1404_1810_b200 as amqft  # noqa: E402
 from test_gpu_parity import DEV, numpy_dft, run_plan  # noqa: E402
 
-SIZES = [16, 32, 64, 128, 256, 512, 1024, 2048, 4096, 8192, 16384]
+SIZES = [16, 32, 64, 128, 256, 512, 1024, 2048, 4096, 8192, 16384, 32768, 65536]
 # the kernel's split (tile_kernel.cuh make_tile): N1 (phase A) x N2 (phase B) [x N3 (phase C)]
 SPLIT = {16: (4, 4), 32: (4, 8), 64: (8, 8), 128: (8, 16), 256: (16, 16), 512: (16, 32), 1024: (32, 32),
-         2048: (64, 32), 4096: (64, 64), 8192: (32, 16, 16), 16384: (32, 16, 32)}
+         2048: (64, 32), 4096: (64, 64), 8192: (32, 16, 16), 16384: (32, 16, 32), 32768: (32, 32, 32),
+         65536: (32, 32, 64)}
 
 
 def rows_per_tile(n):
@@ -78,7 +80,7 @@ def test_tile_ragged_batches_and_rows_independent(n):
     transformed alone (bitwise: a row's arithmetic does not depend on its
     position in the batch)."""
     R = rows_per_tile(n)
-    big = min(148 * 16 * R + R + 1, (1 << 27) // n)   # more tiles than resident CTAs, last tile partial
+    big = min(148 * 16 * R + R + 1, (1 << 27) // n + 3)   # more tiles than resident CTAs / clusters, last tile partial
     rng = np.random.default_rng(n + 1)
     x = torch.tensor(rng.standard_normal((big, 2 * n)), dtype=torch.float32, device=DEV)
     plan = _plan(4, n, big)
