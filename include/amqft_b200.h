@@ -74,10 +74,19 @@ typedef enum { AMQFT_TRIG_TABLE = 0, AMQFT_TRIG_ONTHEFLY = 1 } amqft_trig_mode;
 
 /* Execution order.  EXACT: every node's operations in the reference's
  * operand order and association, no FMA contraction, serial M1/M3/M5/M7
- * recurrences -> bitwise equal to amqft::execute in F64.  FAST: the
- * specialised fused kernels (same DAG; recurrences may be evaluated as
- * parallel scans; F32 and F64). */
-typedef enum { AMQFT_ORDER_EXACT = 0, AMQFT_ORDER_FAST = 1 } amqft_order;
+ * recurrences -> bitwise equal to amqft::execute in F64.  FAST: the fastest
+ * kernels that keep the result within the tolerance against the CPU
+ * reference of the same variant (1e-5 log2 n in F32, 1e-12 in F64): CDFT
+ * rows of n = 16 .. 65536 (F64: 64 .. 32768 for variants 1-4, 64 .. 256 for
+ * 5-8) run as two or three register-resident AM-QFT factors of <= 64 points
+ * in one pass over HBM (the four-step inside shared memory: the AM-QFT DAG is
+ * kept inside each factor), larger n as a multi-pass four-step; everything
+ * else on the specialised whole-DAG kernels.  FAST_DAG: FAST without the
+ * split inside shared memory -- the fused / cooperative / one-thread-per-row
+ * kernels run the whole length-n reference DAG (recurrences may be evaluated
+ * as parallel scans in F32; the F64 instances are bitwise amqft::execute up
+ * to n = 4096), the multi-pass four-step above them. */
+typedef enum { AMQFT_ORDER_EXACT = 0, AMQFT_ORDER_FAST = 1, AMQFT_ORDER_FAST_DAG = 2 } amqft_order;
 
 typedef struct amqft_plan_s* amqft_plan;
 

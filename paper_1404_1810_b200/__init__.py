@@ -72,6 +72,7 @@ class TrigMode(enum.IntEnum):
 class Order(enum.IntEnum):
     Exact = _native.ORDER_EXACT
     Fast = _native.ORDER_FAST
+    FastDag = _native.ORDER_FAST_DAG   # Fast without the split inside shared memory: whole-DAG kernels
 
 
 _BASE = [2, 2, 2, 4, 4, 4, 4, 4, 8, 8]

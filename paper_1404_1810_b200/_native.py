@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(HERE, "libamqft_b200.so")
 OK, EINVAL, ECUDA, ENCCL, ENOMEM = 0, 1, 2, 3, 4
 F32, F64 = 0, 1
 TRIG_TABLE, TRIG_ONTHEFLY = 0, 1
-ORDER_EXACT, ORDER_FAST = 0, 1
+ORDER_EXACT, ORDER_FAST, ORDER_FAST_DAG = 0, 1, 2
 
 
 class PlanDesc(C.Structure):

@@ -333,7 +333,7 @@ amqft_status validate_desc(const amqft_plan_desc* d) {
   if (d->dtype != AMQFT_F32 && d->dtype != AMQFT_F64) return set_err(AMQFT_EINVAL, "dtype must be F32 or F64");
   if (d->trig_mode != AMQFT_TRIG_TABLE && d->trig_mode != AMQFT_TRIG_ONTHEFLY)
     return set_err(AMQFT_EINVAL, "unknown trig mode");
-  if (d->order != AMQFT_ORDER_EXACT && d->order != AMQFT_ORDER_FAST)
+  if (d->order != AMQFT_ORDER_EXACT && d->order != AMQFT_ORDER_FAST && d->order != AMQFT_ORDER_FAST_DAG)
     return set_err(AMQFT_EINVAL, "unknown execution order");
   if (d->batch == 0) return set_err(AMQFT_EINVAL, "batch must be >= 1");
   return AMQFT_OK;
@@ -388,7 +388,7 @@ amqft_status create_plan(amqft_plan* out, const amqft_plan_desc* desc, const std
       if (f32_needs_f64_compute(desc->variant, n)) P->d_trig64 = upload(tab);
     }
     // Fast fused path where one exists for this request.
-    if (desc->order == AMQFT_ORDER_FAST) {
+    if (desc->order == AMQFT_ORDER_FAST || desc->order == AMQFT_ORDER_FAST_DAG) {
       int fpath = 6;
       P->fast = make_tile_plan(*desc, P->d_trig, P->nmax);
       if (!P->fast) {

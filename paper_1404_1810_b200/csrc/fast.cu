@@ -2,6 +2,7 @@
 // per-variant instances: fast_v1.cu .. fast_v8.cu).
 #include "fast.cuh"
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <type_traits>
@@ -109,19 +110,25 @@ std::unique_ptr<FastPlan> make_fast_plan(const amqft_plan_desc& d, const void* d
 }
 
 namespace tilek {
-template <int V>
+template <int V, typename R>
 std::unique_ptr<FastPlan> make_tile(size_t n, const void* tab, uint32_t nmax, int dev);
-// the split of tile_kernel.cuh make_tile: N1 (phase A) x N2 (phase B),
-// 4 x 4, 4 x 8, 8 x 8, 8 x 16, 16 x 16, 16 x 32, 32 x 32, 64 x 32, 64 x 64
-// and the three-factor 32 x 16 x 16 .. 32 x 32 x 64 (n3 = 1: two factors)
-static void tile_split(size_t n, size_t* n1, size_t* n2, size_t* n3) {
+// the split of tile_kernel.cuh make_tile: N1 (phase A) x N2 (phase B) [x N3
+// (phase C); n3 = 1: two factors].  fp32: 4 x 4, 4 x 8, 8 x 8, 8 x 16, 16 x
+// 16, 16 x 32, 32 x 32, 64 x 32, 64 x 64, then 32 x 16 x 16, 32 x 16 x 32, 32
+// x 32 x 32, 32 x 32 x 64; fp64 the same up to 32 x 32, then 8 x 16 x 16, 16 x
+// 16 x 16, 32 x 16 x 16, 32 x 16 x 32, 32 x 32 x 32
+static void tile_split(int dtype, size_t n, size_t* n1, size_t* n2, size_t* n3) {
   int lg = 0;
   for (size_t t = n; t > 1; t >>= 1) ++lg;
   *n3 = 1;
-  if (lg >= 13) {   // 32 x 16 x 16, 32 x 16 x 32, 32 x 32 x 32, 32 x 32 x 64
-    *n1 = 32;
-    *n2 = lg >= 15 ? 32 : 16;
-    *n3 = n / (32 * *n2);
+  const int three_from = dtype == AMQFT_F64 ? 11 : 13;
+  if (lg >= three_from) {
+    static const int f32s[4][3] = {{32, 16, 16}, {32, 16, 32}, {32, 32, 32}, {32, 32, 64}};
+    static const int f64s[5][3] = {{8, 16, 16}, {16, 16, 16}, {32, 16, 16}, {32, 16, 32}, {32, 32, 32}};
+    const int* f = dtype == AMQFT_F64 ? f64s[lg - 11] : f32s[lg - 13];
+    *n1 = f[0];
+    *n2 = f[1];
+    *n3 = f[2];
     return;
   }
   *n1 = size_t(1) << (lg == 11 ? 6 : lg / 2);
@@ -130,32 +137,47 @@ static void tile_split(size_t n, size_t* n1, size_t* n2, size_t* n3) {
 }  // namespace tilek
 
 bool tile_covers(const amqft_plan_desc& d) {
-  if (d.function != AMQFT_FN_CDFT || d.dtype != AMQFT_F32) return false;
-  if (d.n < 16 || d.n > 65536 || (d.n & (d.n - 1))) return false;
+  if (d.function != AMQFT_FN_CDFT || d.order == AMQFT_ORDER_FAST_DAG) return false;
+  if (d.n < 16 || (d.n & (d.n - 1))) return false;
   size_t lo = 16, hi = 65536;
+  if (d.dtype == AMQFT_F64) {
+    // fp64: factors <= 32 points reach N = 2^15.  The result must stay
+    // within 1e-12 of the CPU reference of the same variant: variants 1-4
+    // do at every size (both ~1e-15 from the DFT); the reference's own
+    // variants 5-8 drift from the DFT (4e-14 at N = 256, 1e-10 at 1024,
+    // SURVEY 0), so from N = 512 their plans keep the reference DAG (the
+    // fused kernel's fp64 instance, bitwise).
+    hi = d.variant >= 5 ? 256 : 32768;
+    lo = 64;   // N = 16, 32: the one-thread-per-row kernel is 3-6 % faster (and bitwise)
+  }
   if (const char* e = std::getenv("AMQFT_AB_TILE")) {
     if (e[0] == 'n') return false;
     // A/B measurements: AMQFT_AB_TILE=lo,hi restricts the sizes it takes
     unsigned long a = 0, b = 0;
-    if (std::sscanf(e, "%lu,%lu", &a, &b) == 2) lo = a, hi = b;
+    if (std::sscanf(e, "%lu,%lu", &a, &b) == 2) lo = std::max<size_t>(lo, a), hi = std::min<size_t>(hi, b);
   }
   return d.n >= lo && d.n <= hi;
 }
 
-std::unique_ptr<FastPlan> make_tile_plan(const amqft_plan_desc& d, const void* d_trig, uint32_t nmax) {
-  if (!tile_covers(d)) return nullptr;
+template <typename R>
+static std::unique_ptr<FastPlan> make_tile_typed(const amqft_plan_desc& d, const void* d_trig, uint32_t nmax) {
   using namespace tilek;
   switch (d.variant) {
-    case 1: return make_tile<1>(d.n, d_trig, nmax, d.device);
-    case 2: return make_tile<2>(d.n, d_trig, nmax, d.device);
-    case 3: return make_tile<3>(d.n, d_trig, nmax, d.device);
-    case 4: return make_tile<4>(d.n, d_trig, nmax, d.device);
-    case 5: return make_tile<5>(d.n, d_trig, nmax, d.device);
-    case 6: return make_tile<6>(d.n, d_trig, nmax, d.device);
-    case 7: return make_tile<7>(d.n, d_trig, nmax, d.device);
-    case 8: return make_tile<8>(d.n, d_trig, nmax, d.device);
+    case 1: return make_tile<1, R>(d.n, d_trig, nmax, d.device);
+    case 2: return make_tile<2, R>(d.n, d_trig, nmax, d.device);
+    case 3: return make_tile<3, R>(d.n, d_trig, nmax, d.device);
+    case 4: return make_tile<4, R>(d.n, d_trig, nmax, d.device);
+    case 5: return make_tile<5, R>(d.n, d_trig, nmax, d.device);
+    case 6: return make_tile<6, R>(d.n, d_trig, nmax, d.device);
+    case 7: return make_tile<7, R>(d.n, d_trig, nmax, d.device);
+    case 8: return make_tile<8, R>(d.n, d_trig, nmax, d.device);
   }
   return nullptr;
+}
+
+std::unique_ptr<FastPlan> make_tile_plan(const amqft_plan_desc& d, const void* d_trig, uint32_t nmax) {
+  if (!tile_covers(d)) return nullptr;
+  return d.dtype == AMQFT_F64 ? make_tile_typed<double>(d, d_trig, nmax) : make_tile_typed<float>(d, d_trig, nmax);
 }
 
 namespace smallk {
@@ -167,12 +189,13 @@ OpCount tile_op_counts(const amqft_plan_desc& d) {
   // each: the traced schedule's meter) plus one complex twiddle multiply
   // per element (4 muls + 2 adds), as the four-step's accounting
   size_t n1, n2, n3;
-  tilek::tile_split(d.n, &n1, &n2, &n3);
+  tilek::tile_split(d.dtype, d.n, &n1, &n2, &n3);
+  const bool f64 = d.dtype == AMQFT_F64;
   OpCount c1, c2, c3, c;
-  smallk::small_ops_n(d.variant, n1, false, &c1, AMQFT_FN_CDFT);
-  smallk::small_ops_n(d.variant, n2, false, &c2, AMQFT_FN_CDFT);
+  smallk::small_ops_n(d.variant, n1, f64, &c1, AMQFT_FN_CDFT);
+  smallk::small_ops_n(d.variant, n2, f64, &c2, AMQFT_FN_CDFT);
   if (n3 > 1) {   // three factors, two twiddle passes
-    smallk::small_ops_n(d.variant, n3, false, &c3, AMQFT_FN_CDFT);
+    smallk::small_ops_n(d.variant, n3, f64, &c3, AMQFT_FN_CDFT);
     c.adds = n2 * n3 * c1.adds + n1 * n3 * c2.adds + n1 * n2 * c3.adds + 2 * 2 * d.n;
     c.muls = n2 * n3 * c1.muls + n1 * n3 * c2.muls + n1 * n2 * c3.muls + 2 * 4 * d.n;
     c.bt = n2 * n3 * c1.bt + n1 * n3 * c2.bt + n1 * n2 * c3.bt;
@@ -277,8 +300,8 @@ static amqft_plan_desc sub_desc(int variant, size_t n, int dtype) {
   return d;
 }
 
-bool fast_sub_covered(int dtype, size_t n, int variant) {
-  if (tile_covers(sub_desc(variant, n, dtype))) return true;   // fp32 16 .. 65536, every variant
+bool fast_sub_covered(int dtype, size_t n, int variant, bool allow_tile) {
+  if (allow_tile && tile_covers(sub_desc(variant, n, dtype))) return true;   // fp32 16 .. 65536, every variant
   if (dtype == AMQFT_F32 && f32_needs_f64_compute(variant, n)) return n >= 1024 && n <= 4096;
   if (dtype == AMQFT_F32) return n >= 2 && n <= 8192;
   return n >= 2 && n <= 4096 && n != 512;

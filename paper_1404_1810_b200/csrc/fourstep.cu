@@ -353,6 +353,16 @@ double sub_tbs(int dtype, int lg, int variant, bool col = false) {
     d.variant = variant;
     if (tile_covers(d)) return tile[lg];
   }
+  // fp64 (variants 1-4 to 2^15, 5-8 to 2^8: fast.cu tile_covers)
+  static const double tile64[16] = {0, 0, 0, 0, 0, 0, 5.97, 6.36, 5.59, 5.68, 5.48, 6.11, 5.26, 5.04, 3.85, 3.01};
+  if (!col && dtype == AMQFT_F64 && lg >= 6 && lg <= 15) {
+    amqft_plan_desc d{};
+    d.function = AMQFT_FN_CDFT;
+    d.dtype = dtype;
+    d.n = size_t(1) << lg;
+    d.variant = variant;
+    if (tile_covers(d)) return tile64[lg];
+  }
   if (dtype == AMQFT_F32 && lg < 13 && f32_needs_f64_compute(variant, size_t(1) << lg)) return mixed[lg];
   if (dtype == AMQFT_F32) return lg < 14 ? f32[lg] : 0.0;
   return lg < 13 ? f64[lg] : 0.0;
@@ -690,9 +700,10 @@ void transpose_c64(const void* in, void* out, size_t mats, size_t r, size_t c, c
 }
 
 bool fourstep_covers(const amqft_plan_desc& d) {
-  if (d.function != AMQFT_FN_CDFT || d.order != AMQFT_ORDER_FAST) return false;
+  if (d.function != AMQFT_FN_CDFT || (d.order != AMQFT_ORDER_FAST && d.order != AMQFT_ORDER_FAST_DAG)) return false;
   if ((d.n & (d.n - 1)) != 0 || d.n > (size_t(1) << 26)) return false;
-  if (fast_sub_covered(d.dtype, d.n, d.variant)) return false;   // one fused / small kernel does it
+  // one fused / small / tile kernel does it (FAST_DAG plans: the whole-DAG kernels only)
+  if (fast_sub_covered(d.dtype, d.n, d.variant, d.order != AMQFT_ORDER_FAST_DAG)) return false;
   return fourstep_shape(d.dtype, d.variant, d.n).ok;
 }
 

@@ -17,7 +17,7 @@ namespace amqft_b200 {
 std::unique_ptr<FastPlan> make_fast_sub(int variant, size_t n, int dtype, const void* tab, uint32_t nmax, int dev,
                                         const void* tab64 = nullptr, bool columns = false);
 OpCount fast_sub_op_counts(int variant, size_t n, int dtype, bool columns = false);
-bool fast_sub_covered(int dtype, size_t n, int variant);
+bool fast_sub_covered(int dtype, size_t n, int variant, bool allow_tile = true);
 
 // CDFT, fast order, N up to 2^26 beyond the single-kernel sizes.
 bool fourstep_covers(const amqft_plan_desc& d);

@@ -1,11 +1,11 @@
 // tile_kernel.cuh -- four-step inside one CTA's shared memory (path 6).
 //
-// CDFT N = N1 N2 (fp32, N = 16 .. 4096, N1, N2 <= 64; N = 8192 .. 65536 as
-// three factors, k_tile3 below, from 2^15 on a thread-block cluster) in ONE
-// pass over HBM:
+// CDFT N = N1 N2 (fp32: N = 16 .. 4096, N1, N2 <= 64; N = 8192 .. 65536 as
+// three factors, k_tile3 below, from 2^15 on a thread-block cluster; fp64:
+// factors <= 32, N = 16 .. 1024 / 2048 .. 32768) in ONE pass over HBM:
 // both factors are one-thread-per-transform AM-QFTs kept in registers -- the
 // straight-line code codegen/gen_small.py traces from the plan compiler
-// (SmallGen<V, 0, LOGN, float>, every line one reference add/sub/mul,
+// (SmallGen<V, 0, LOGN, R>, every line one reference add/sub/mul,
 // variants.cpp:186-231 / elaborations.cpp), the same code k_small runs from
 // HBM rows.  Decimation in frequency, n = N2 n1 + n2, k = k1 + N1 k2:
 //   X[k1 + N1 k2] = sum_n2 w_N2^(n2 k2) [ w_N^(n2 k1) sum_n1 x[N2 n1 + n2] w_N1^(n1 k1) ]
@@ -27,7 +27,10 @@
 // convention, fourstep.cu), so the result is checked against the fp64 oracle
 // of the same variant within 1e-5 log2 N; sub-transforms of length <= 64 are
 // stable in fp32 for the sine-family variants 5-8 too (fast.cuh), so all 8
-// variants run in fp32.
+// variants run in fp32.  fp64 plans take this path where the result stays
+// within 1e-12 of the CPU reference of the same variant (fast.cu
+// tile_covers: variants 1-4 at every size, 5-8 up to N = 256; elsewhere the
+// fused kernel's fp64 instance, bitwise the reference, keeps the plan).
 // The inverse is the swap trick, fused into phase A's loads and phase B's
 // stores.
 #pragma once
@@ -51,150 +54,202 @@ namespace tilek {
 using smallk::SmallGen;
 using smallk::TabP;
 
+// Complex element and the tile pad (in complex values) that spreads the
+// 128-bit row loads of a quarter-warp over 8 distinct bank groups: fp32 rows
+// are read two values at a time (pitch / 2 odd), fp64 one (pitch odd).
+template <typename R> struct RT;
+template <> struct RT<float> {
+  using V2 = float2;
+  static constexpr int PAD = 2;
+  static constexpr bool spread(int pitch) { return (pitch / 2) % 2 == 1; }
+};
+template <> struct RT<double> {
+  using V2 = double2;
+  static constexpr int PAD = 1;
+  static constexpr bool spread(int pitch) { return pitch % 2 == 1; }
+};
+template <typename R> __device__ __forceinline__ typename RT<R>::V2 mk2(R a, R b);
+template <> __device__ __forceinline__ float2 mk2<float>(float a, float b) { return make_float2(a, b); }
+template <> __device__ __forceinline__ double2 mk2<double>(double a, double b) { return make_double2(a, b); }
+// a * w (complex)
+template <typename R, typename V2>
+__device__ __forceinline__ void cmul(R& a, R& b, const V2 w) {
+  const R na = a * w.x - b * w.y, nb = a * w.y + b * w.x;
+  a = na;
+  b = nb;
+}
+
 // T: threads per CTA; MB: CTAs per SM the registers are budgeted for (0:
 // by factor size); PF: bulk L2 prefetch of the CTA's next tile (-1: where a
-// factor has 64 points).
-template <int LG1, int LG2, int T_ = 64, int MB_ = 0, int PF_ = -1>
+// factor needs the 4-CTA register budget).
+template <typename R, int LG1, int LG2, int T_ = 64, int MB_ = 0, int PF_ = -1>
 struct TCfg {
+  using V2 = typename RT<R>::V2;
   static constexpr int N1 = 1 << LG1, N2 = 1 << LG2, N = N1 * N2;
   static constexpr int LGM = LG1 > LG2 ? LG1 : LG2;
   static constexpr int T = T_;                                   // threads per CTA
   static constexpr int NMIN = N1 < N2 ? N1 : N2;
-  static constexpr int R = T / NMIN > 0 ? T / NMIN : 1;         // rows per tile
-  static constexpr int PITCH = N2 + 2;                           // complex values per P row
+  static constexpr int R_ = T / NMIN > 0 ? T / NMIN : 1;        // rows per tile
+  static constexpr int PITCH = N2 + RT<R>::PAD;                  // complex values per P row
   static constexpr int ROWP = N1 * PITCH;                        // complex values per tile row
+  // Registers decide the CTAs per SM (64 threads each).  fp32: 64-point
+  // factors 4 (246 registers: measured 0.906 ms against 1.07 ms at 6 CTAs /
+  // 168 registers, config 2), 32-point 10, 16-point 16; fp64: 32-point 6
+  // (150 registers), 16-point 12.
+  static constexpr int LGR = LGM + (sizeof(R) == 8 ? 1 : 0);
+  static constexpr int MINB = MB_ > 0 ? MB_ : (LGR >= 6 ? (sizeof(R) == 8 ? 6 : 4) : (LGR == 5 ? 10 : 16)) * 64 / T;
   // Measured (B200, 2^28 reals per launch): the 64 x 64 kernel is bound by
   // the latency of phase A's loads (4 CTAs of 2 warps per SM; long
   // scoreboard is the top stall); with the next tile on its way into L2
   // 0.912 -> 0.769 ms.  The small factors run 10-16 CTAs per SM and lose
   // 2-6 % with it.
-  static constexpr bool PF = PF_ < 0 ? LGM >= 6 : PF_ != 0;
-  static constexpr size_t SMEM = static_cast<size_t>(R) * ROWP * sizeof(float2);
+  static constexpr bool PF = PF_ < 0 ? LGR >= 6 : PF_ != 0;
+  static constexpr size_t SMEM = static_cast<size_t>(R_) * ROWP * sizeof(V2);
   static constexpr int NT1 = (N1 < 8 ? 8 : N1) / 4, NT2 = (N2 < 8 ? 8 : N2) / 4;
-  // CTAs per SM by registers (64 threads): 64-point factors 4 (246
-  // registers: measured 0.906 ms against 1.07 ms at 6 CTAs / 168 registers,
-  // config 2), 32-point 10, 16-point 16
-  static constexpr int MINB = MB_ > 0 ? MB_ : (LGM >= 6 ? 4 : (LGM == 5 ? 10 : 16)) * 64 / T;
+  static_assert(RT<R>::spread(PITCH), "bank-group spread of the 128-bit row loads");
 };
 
-// phase A: chunk c = complex n1 = 2c, 2c+1 of column n2 (global), output
-// chunk c = k1 = 2c, 2c+1 times the twiddle, into P[k1][n2]
-template <int N2, int PITCH, bool INV>
+// The generated code moves a row in chunks: fp32 chunk c = complex values
+// 2c, 2c+1 (four reals), fp64 chunk c = complex value c (two reals); every
+// I/O object below serves both through the two overloads of ld / st.
+
+// phase A: input n1 of column n2 from HBM (stride N2), output k1 times the
+// twiddle into P[k1][n2]
+template <typename R, int N2, int PITCH, bool INV>
 struct AIo {
-  const float2* __restrict__ gi;   // x + n2
-  float2* sp;                      // P + n2
-  const float2* __restrict__ tw;   // tw + n2: tw[k1 N2 + n2] = w_N^(n2 k1)
-  __device__ __forceinline__ void ld(int c, float& a, float& b, float& d, float& e) const {
-    const float2 u = __ldcs(gi + (2 * c) * N2), v = __ldcs(gi + (2 * c + 1) * N2);
-    if (INV) { a = u.y; b = u.x; d = v.y; e = v.x; }
-    else { a = u.x; b = u.y; d = v.x; e = v.y; }
+  using V2 = typename RT<R>::V2;
+  const V2* __restrict__ gi;   // x + n2
+  V2* sp;                      // P + n2
+  const V2* __restrict__ tw;   // tw + n2: tw[k1 N2 + n2] = w_N^(n2 k1)
+  __device__ __forceinline__ void ld(int c, R& a, R& b) const {
+    const V2 u = __ldcs(gi + c * N2);
+    if (INV) { a = u.y; b = u.x; }
+    else { a = u.x; b = u.y; }
   }
-  __device__ __forceinline__ void st(int c, float a, float b, float d, float e) const {
-    const float2 w1 = __ldg(tw + (2 * c + 1) * N2);
-    if (c != 0) {
-      const float2 w = __ldg(tw + (2 * c) * N2);   // k1 = 0: w = 1
-      const float na = a * w.x - b * w.y, nb = a * w.y + b * w.x;
-      a = na;
-      b = nb;
-    }
-    const float nd = d * w1.x - e * w1.y, ne = d * w1.y + e * w1.x;
-    sp[(2 * c) * PITCH] = make_float2(a, b);
-    sp[(2 * c + 1) * PITCH] = make_float2(nd, ne);
+  __device__ __forceinline__ void ld(int c, R& a, R& b, R& d, R& e) const {
+    ld(2 * c, a, b);
+    ld(2 * c + 1, d, e);
+  }
+  __device__ __forceinline__ void st(int c, R a, R b) const {
+    if (c != 0) cmul(a, b, __ldg(tw + c * N2));   // k1 = 0: w = 1
+    sp[c * PITCH] = mk2<R>(a, b);
+  }
+  __device__ __forceinline__ void st(int c, R a, R b, R d, R e) const {
+    const V2 w1 = __ldg(tw + (2 * c + 1) * N2);
+    if (c != 0) cmul(a, b, __ldg(tw + (2 * c) * N2));
+    cmul(d, e, w1);
+    sp[(2 * c) * PITCH] = mk2<R>(a, b);
+    sp[(2 * c + 1) * PITCH] = mk2<R>(d, e);
   }
 };
 
-// phase B: chunk c = P[k1][2c, 2c+1] (one 128-bit load), output chunk c =
-// k2 = 2c, 2c+1 at X[k1 + N1 k2]
-template <int N1, bool INV>
+// last phase: a contiguous row of the tile (128-bit loads), output k at
+// X[base + STRIDE k]
+template <typename R, int STRIDE, bool INV>
 struct BIo {
-  const float4* sp;   // P + k1 PITCH (16-byte aligned: PITCH is even)
-  float2* __restrict__ go;   // X + k1
-  float scale;
+  using V2 = typename RT<R>::V2;
+  const V2* sp;              // the row (16-byte aligned: even pitches in fp32)
+  V2* __restrict__ go;       // X + base
+  R scale;
+  __device__ __forceinline__ void ld(int c, R& a, R& b) const {
+    const V2 v = sp[c];
+    a = v.x; b = v.y;
+  }
   __device__ __forceinline__ void ld(int c, float& a, float& b, float& d, float& e) const {
-    const float4 v = sp[c];
+    const float4 v = reinterpret_cast<const float4*>(sp)[c];
     a = v.x; b = v.y; d = v.z; e = v.w;
   }
-  __device__ __forceinline__ void st(int c, float a, float b, float d, float e) const {
-    if (INV) {
-      __stcs(go + (2 * c) * N1, make_float2(b * scale, a * scale));
-      __stcs(go + (2 * c + 1) * N1, make_float2(e * scale, d * scale));
-    } else {
-      __stcs(go + (2 * c) * N1, make_float2(a, b));
-      __stcs(go + (2 * c + 1) * N1, make_float2(d, e));
-    }
+  __device__ __forceinline__ void st(int c, R a, R b) const {
+    if (INV) __stcs(go + c * STRIDE, mk2<R>(b * scale, a * scale));
+    else __stcs(go + c * STRIDE, mk2<R>(a, b));
+  }
+  __device__ __forceinline__ void st(int c, R a, R b, R d, R e) const {
+    st(2 * c, a, b);
+    st(2 * c + 1, d, e);
   }
 };
 
-template <int V, bool INV, class C>
+template <int V, typename R, bool INV, class C>
 __global__ void __launch_bounds__(C::T, C::MINB)
-k_tile(const float* __restrict__ in, float* __restrict__ out, size_t rows,
-       const __grid_constant__ TabP<float, C::NT1> t1, const __grid_constant__ TabP<float, C::NT2> t2,
-       const float2* __restrict__ tw, float scale) {
+k_tile(const R* __restrict__ in, R* __restrict__ out, size_t rows,
+       const __grid_constant__ TabP<R, C::NT1> t1, const __grid_constant__ TabP<R, C::NT2> t2,
+       const typename RT<R>::V2* __restrict__ tw, R scale) {
+  using V2 = typename RT<R>::V2;
   constexpr int LG1 = 31 - __builtin_clz(C::N1), LG2 = 31 - __builtin_clz(C::N2);
-  using G1 = SmallGen<V, 0, LG1, float>;
-  using G2 = SmallGen<V, 0, LG2, float>;
+  using G1 = SmallGen<V, 0, LG1, R>;
+  using G2 = SmallGen<V, 0, LG2, R>;
   constexpr int N1 = C::N1, N2 = C::N2, N = C::N;
   extern __shared__ __align__(128) unsigned char sm[];
-  float2* P = reinterpret_cast<float2*>(sm);
+  V2* P = reinterpret_cast<V2*>(sm);
   const int tid = threadIdx.x;
-  const size_t tiles = (rows + C::R - 1) / C::R;
+  const size_t tiles = (rows + C::R_ - 1) / C::R_;
   for (size_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-    const size_t row0 = tile * C::R;
+    const size_t row0 = tile * C::R_;
     if constexpr (C::PF) {   // the CTA's next tile: one bulk prefetch into L2
-      const size_t nrow = (tile + gridDim.x) * C::R;
-      if (tid == 0 && nrow + C::R <= rows)
+      const size_t nrow = (tile + gridDim.x) * C::R_;
+      if (tid == 0 && nrow + C::R_ <= rows)
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
-                     ::"l"(in + nrow * 2 * N), "n"(C::R * N * 8) : "memory");
+                     ::"l"(in + nrow * 2 * N), "n"(C::R_ * N * static_cast<int>(sizeof(V2))) : "memory");
     }
     // ---- phase A: columns of x -> P (twiddled)
 #pragma unroll 1
-    for (int i = tid; i < C::R * N2; i += C::T) {
+    for (int i = tid; i < C::R_ * N2; i += C::T) {
       const int r = i / N2, n2 = i % N2;
       if (row0 + r < rows) {
-        AIo<N2, C::PITCH, INV> io{reinterpret_cast<const float2*>(in) + (row0 + r) * N + n2, P + r * C::ROWP + n2,
-                                  tw + n2};
-        G1::template run<Arith<float>>(io, t1.v);
+        AIo<R, N2, C::PITCH, INV> io{reinterpret_cast<const V2*>(in) + (row0 + r) * N + n2, P + r * C::ROWP + n2,
+                                     tw + n2};
+        G1::template run<Arith<R>>(io, t1.v);
       }
     }
     __syncthreads();
     // ---- phase B: rows of P -> X
 #pragma unroll 1
-    for (int j = tid; j < C::R * N1; j += C::T) {
+    for (int j = tid; j < C::R_ * N1; j += C::T) {
       const int r = j / N1, k1 = j % N1;
       if (row0 + r < rows) {
-        BIo<N1, INV> io{reinterpret_cast<const float4*>(P + r * C::ROWP + k1 * C::PITCH),
-                        reinterpret_cast<float2*>(out) + (row0 + r) * N + k1, scale};
-        G2::template run<Arith<float>>(io, t2.v);
+        BIo<R, N1, INV> io{P + r * C::ROWP + k1 * C::PITCH, reinterpret_cast<V2*>(out) + (row0 + r) * N + k1, scale};
+        G2::template run<Arith<R>>(io, t2.v);
       }
     }
     __syncthreads();   // P is rewritten by the next tile's phase A
   }
 }
 
-template <int V, int LG1, int LG2, int T = 64, int MB = 0, int PF = -1>
+// w_n^j for j < n as rows [k][m] = w_n^(k m), k < K, m < Mm: long double, rounded once
+template <typename V2>
+void fill_twiddles(V2* dst, int K, int Mm, long n) {
+  using E = decltype(V2{}.x);
+  const long double two_pi = 6.283185307179586476925286766559005768L;
+  for (int k = 0; k < K; ++k)
+    for (int m = 0; m < Mm; ++m) {
+      const long double a = two_pi * static_cast<long double>((static_cast<long>(k) * m) % n) / static_cast<long double>(n);
+      dst[static_cast<size_t>(k) * Mm + m] = V2{static_cast<E>(cosl(a)), static_cast<E>(-sinl(a))};
+    }
+}
+
+inline void tk_check(cudaError_t e) {
+  if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+}
+
+template <int V, typename R, int LG1, int LG2, int T = 64, int MB = 0, int PF = -1>
 class TilePlanImpl final : public FastPlan {
-  using C = TCfg<LG1, LG2, T, MB, PF>;
+  using C = TCfg<R, LG1, LG2, T, MB, PF>;
+  using V2 = typename RT<R>::V2;
 
  public:
   TilePlanImpl(const void* tab, uint32_t nmax, int device) {
-    check_(smallk::fetch_table(t1_.v, C::NT1, tab, nmax));
-    check_(smallk::fetch_table(t2_.v, C::NT2, tab, nmax));
-    // tw[k1 N2 + n2] = w_N^(n2 k1), long double rounded once
-    std::vector<float2> tw(C::N);
-    const long double two_pi = 6.283185307179586476925286766559005768L;
-    for (int k1 = 0; k1 < C::N1; ++k1)
-      for (int n2 = 0; n2 < C::N2; ++n2) {
-        const long double a = two_pi * static_cast<long double>((k1 * n2) % C::N) / static_cast<long double>(C::N);
-        tw[k1 * C::N2 + n2] = float2{static_cast<float>(cosl(a)), static_cast<float>(-sinl(a))};
-      }
-    check_(cudaMalloc(&tw_, tw.size() * sizeof(float2)));
-    check_(cudaMemcpy(tw_, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice));
-    auto f0 = k_tile<V, false, C>;
-    auto f1 = k_tile<V, true, C>;
-    check_(cudaFuncSetAttribute(f0, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM)));
-    check_(cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM)));
+    tk_check(smallk::fetch_table(t1_.v, C::NT1, tab, nmax));
+    tk_check(smallk::fetch_table(t2_.v, C::NT2, tab, nmax));
+    std::vector<V2> tw(C::N);   // tw[k1 N2 + n2] = w_N^(n2 k1)
+    fill_twiddles(tw.data(), C::N1, C::N2, C::N);
+    tk_check(cudaMalloc(&tw_, tw.size() * sizeof(V2)));
+    tk_check(cudaMemcpy(tw_, tw.data(), tw.size() * sizeof(V2), cudaMemcpyHostToDevice));
+    auto f0 = k_tile<V, R, false, C>;
+    auto f1 = k_tile<V, R, true, C>;
+    tk_check(cudaFuncSetAttribute(f0, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM)));
+    tk_check(cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM)));
     int per_sm = 0;
-    check_(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f0, C::T, C::SMEM));
+    tk_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f0, C::T, C::SMEM));
     if (per_sm < 1) throw std::runtime_error("tile four-step kernel does not fit an SM");
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -205,63 +260,59 @@ class TilePlanImpl final : public FastPlan {
     if (tw_) cudaFree(tw_);
   }
   void exec(const void* in, void* out, size_t rows, int inverse, cudaStream_t st) override {
-    const size_t tiles = (rows + C::R - 1) / C::R;
+    const size_t tiles = (rows + C::R_ - 1) / C::R_;
     const unsigned grid = static_cast<unsigned>(std::min<size_t>(tiles, static_cast<size_t>(grid_cap_)));
-    const float scale = 1.0f / static_cast<float>(C::N);
+    const R scale = R(1) / static_cast<R>(C::N);
     if (inverse)
-      k_tile<V, true, C><<<grid, C::T, C::SMEM, st>>>(static_cast<const float*>(in), static_cast<float*>(out), rows,
-                                                      t1_, t2_, tw_, scale);
+      k_tile<V, R, true, C><<<grid, C::T, C::SMEM, st>>>(static_cast<const R*>(in), static_cast<R*>(out), rows, t1_,
+                                                         t2_, tw_, scale);
     else
-      k_tile<V, false, C><<<grid, C::T, C::SMEM, st>>>(static_cast<const float*>(in), static_cast<float*>(out), rows,
-                                                       t1_, t2_, tw_, scale);
-    const cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+      k_tile<V, R, false, C><<<grid, C::T, C::SMEM, st>>>(static_cast<const R*>(in), static_cast<R*>(out), rows, t1_,
+                                                          t2_, tw_, scale);
+    tk_check(cudaGetLastError());
   }
 
  private:
-  static void check_(cudaError_t e) {
-    if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
-  }
-  TabP<float, C::NT1> t1_{};
-  TabP<float, C::NT2> t2_{};
-  float2* tw_ = nullptr;
+  TabP<R, C::NT1> t1_{};
+  TabP<R, C::NT2> t2_{};
+  V2* tw_ = nullptr;
   int grid_cap_ = 148;
 };
 
-// ---- Three factors, N = N1 N2 N3 (N = 8192, 16384: the row no longer
-// fits two register-resident factors of <= 64 points).  n = N2 N3 n1 + N3 n2
-// + n3, k = k1 + N1 k2 + N1 N2 k3, M = N2 N3:
+// ---- Three factors, N = N1 N2 N3 (the row no longer fits two register-
+// resident factors).  n = N2 N3 n1 + N3 n2 + n3, k = k1 + N1 k2 + N1 N2 k3,
+// M = N2 N3:
 // phase A  thread = m = N3 n2 + n3: x[M n1 + m] from HBM (coalesced over m),
 //          AM-QFT of length N1, times w_N^(m k1), into Y[k1][n2][n3];
 // phase B  thread = (k1, n3): column n2 of Y[k1] in place (a thread reads
 //          and rewrites its own cells), AM-QFT of length N2, times
 //          w_M^(n3 k2);
 // phase C  thread = (k2, k1), k1 fastest: row Y[k1][k2][.] with 128-bit
-//          loads (pitches N3 + 2 per k2 and N2 (N3 + 2) + 2 per k1: both
-//          halves odd, a quarter-warp hits 8 distinct bank groups), AM-QFT
-//          of length N3, output k3 to X[k1 + N1 (k2 + N2 k3)] (lanes on
-//          consecutive k1).
-// P > 1 (N = 2^15, 2^16: the row exceeds one SM's shared memory): one row per
-// thread-block cluster of P CTAs.  CTA q owns the planes k1 in [q N1/P,
-// (q+1) N1/P) of Y; in phase A it transforms the columns m in [q M/P,
-// (q+1) M/P) and stores output k1 straight into the owner's shared memory
-// over DSMEM (st.shared::cluster), the only exchange: (P-1)/P of the row.
-// Phases B and C run on the CTA's own planes.  Two cluster barriers per row:
-// a full one after phase A (all planes complete), and a split one around the
-// rest -- arrive after the CTA's phase C, wait just before its first remote
-// store of the next row -- so the next row's loads and arithmetic overlap the
+//          loads (pitches N3 + pad per k2 and N2 (N3 + pad) + pad per k1: a
+//          quarter-warp hits 8 distinct bank groups), AM-QFT of length N3,
+//          output k3 to X[k1 + N1 (k2 + N2 k3)] (lanes on consecutive k1).
+// P > 1 (the row exceeds one SM's shared memory): one row per thread-block
+// cluster of P CTAs.  CTA q owns the planes k1 in [q N1/P, (q+1) N1/P) of Y;
+// in phase A it transforms the columns m in [q M/P, (q+1) M/P) and stores
+// output k1 straight into the owner's shared memory over DSMEM
+// (st.shared::cluster), the only exchange: (P-1)/P of the row.  Phases B and
+// C run on the CTA's own planes.  Two cluster barriers per row: a full one
+// after phase A (all planes complete), and a split one around the rest --
+// arrive after the CTA's phase C, wait just before its first remote store
+// of the next row -- so the next row's loads and arithmetic overlap the
 // peers' phase C.
-template <int LG1, int LG2, int LG3, int T_, int MB_, int P_ = 1>
+template <typename R, int LG1, int LG2, int LG3, int T_, int MB_, int P_ = 1>
 struct T3Cfg {
+  using V2 = typename RT<R>::V2;
   static constexpr int N1 = 1 << LG1, N2 = 1 << LG2, N3 = 1 << LG3, M = N2 * N3, N = N1 * M;
   static constexpr int T = T_, MINB = MB_, P = P_;
-  static constexpr int K1 = N1 / P;              // planes per CTA
-  static constexpr int P3 = N3 + 2;              // complex values per (k1, k2) row
-  static constexpr int PM = N2 * P3 + 2;         // complex values per k1 plane
+  static constexpr int K1 = N1 / P;                     // planes per CTA
+  static constexpr int P3 = N3 + RT<R>::PAD;            // complex values per (k1, k2) row
+  static constexpr int PM = N2 * P3 + RT<R>::PAD;       // complex values per k1 plane
   static constexpr int ROWP = K1 * PM;
-  static constexpr size_t SMEM = static_cast<size_t>(ROWP) * sizeof(float2);
+  static constexpr size_t SMEM = static_cast<size_t>(ROWP) * sizeof(V2);
   static constexpr int NT1 = (N1 < 8 ? 8 : N1) / 4, NT2 = (N2 < 8 ? 8 : N2) / 4, NT3 = (N3 < 8 ? 8 : N3) / 4;
-  static_assert((P3 / 2) % 2 == 1 && (PM / 2) % 2 == 1, "bank-group spread of the 128-bit row loads");
+  static_assert(RT<R>::spread(P3) && RT<R>::spread(PM), "bank-group spread of the 128-bit row loads");
   static_assert(P == 1 || ((M / P) % T == 0 && K1 % 2 == 0), "whole warps in phase A; an output chunk has one owner");
 };
 
@@ -274,96 +325,119 @@ __device__ __forceinline__ void tk_cluster_arrive() {
 __device__ __forceinline__ void tk_cluster_wait() {
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void st_cluster(uint32_t addr, float a, float b) {
+  asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(a), "f"(b) : "memory");
+}
+__device__ __forceinline__ void st_cluster(uint32_t addr, double a, double b) {
+  asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(a), "d"(b) : "memory");
+}
 
-template <int M, int PM, bool INV>
+// phase A, P = 1: output k1 into the CTA's own Y
+template <typename R, int M, int PM, bool INV>
 struct A3Io {
-  const float2* __restrict__ gi;   // x + m
-  float2* sp;                      // Y + n2 P3 + n3
-  const float2* __restrict__ tw;   // tw1 + m: tw1[k1 M + m] = w_N^(m k1)
-  __device__ __forceinline__ void ld(int c, float& a, float& b, float& d, float& e) const {
-    const float2 u = __ldcs(gi + (2 * c) * M), v = __ldcs(gi + (2 * c + 1) * M);
-    if (INV) { a = u.y; b = u.x; d = v.y; e = v.x; }
-    else { a = u.x; b = u.y; d = v.x; e = v.y; }
+  using V2 = typename RT<R>::V2;
+  const V2* __restrict__ gi;   // x + m
+  V2* sp;                      // Y + n2 P3 + n3
+  const V2* __restrict__ tw;   // tw1 + m: tw1[k1 M + m] = w_N^(m k1)
+  __device__ __forceinline__ void ld(int c, R& a, R& b) const {
+    const V2 u = __ldcs(gi + c * M);
+    if (INV) { a = u.y; b = u.x; }
+    else { a = u.x; b = u.y; }
   }
-  __device__ __forceinline__ void st(int c, float a, float b, float d, float e) const {
-    const float2 w1 = __ldg(tw + (2 * c + 1) * M);
-    if (c != 0) {
-      const float2 w = __ldg(tw + (2 * c) * M);
-      const float na = a * w.x - b * w.y, nb = a * w.y + b * w.x;
-      a = na;
-      b = nb;
-    }
-    sp[(2 * c) * PM] = make_float2(a, b);
-    sp[(2 * c + 1) * PM] = make_float2(d * w1.x - e * w1.y, d * w1.y + e * w1.x);
+  __device__ __forceinline__ void ld(int c, R& a, R& b, R& d, R& e) const {
+    ld(2 * c, a, b);
+    ld(2 * c + 1, d, e);
+  }
+  __device__ __forceinline__ void st(int c, R a, R b) const {
+    if (c != 0) cmul(a, b, __ldg(tw + c * M));
+    sp[c * PM] = mk2<R>(a, b);
+  }
+  __device__ __forceinline__ void st(int c, R a, R b, R d, R e) const {
+    const V2 w1 = __ldg(tw + (2 * c + 1) * M);
+    if (c != 0) cmul(a, b, __ldg(tw + (2 * c) * M));
+    cmul(d, e, w1);
+    sp[(2 * c) * PM] = mk2<R>(a, b);
+    sp[(2 * c + 1) * PM] = mk2<R>(d, e);
   }
 };
 
 // phase A of the cluster kernel: output k1 goes to plane k1 % K1 of CTA
 // k1 / K1 (both compile-time per store); the first store of a row waits for
 // the peers' phase C of the previous row (the split barrier)
-template <int M, int PM, int K1, int P, bool INV>
+template <typename R, int M, int PM, int K1, int P, bool INV>
 struct A3IoC {
-  const float2* __restrict__ gi;
-  const float2* __restrict__ tw;
+  using V2 = typename RT<R>::V2;
+  const V2* __restrict__ gi;
+  const V2* __restrict__ tw;
   uint32_t yb[P];    // the P CTAs' Y + n2 P3 + n3 in the cluster window
   bool wait;
-  __device__ __forceinline__ void ld(int c, float& a, float& b, float& d, float& e) const {
-    const float2 u = __ldcs(gi + (2 * c) * M), v = __ldcs(gi + (2 * c + 1) * M);
-    if (INV) { a = u.y; b = u.x; d = v.y; e = v.x; }
-    else { a = u.x; b = u.y; d = v.x; e = v.y; }
+  __device__ __forceinline__ void ld(int c, R& a, R& b) const {
+    const V2 u = __ldcs(gi + c * M);
+    if (INV) { a = u.y; b = u.x; }
+    else { a = u.x; b = u.y; }
   }
-  __device__ __forceinline__ void st(int c, float a, float b, float d, float e) const {
-    const float2 w1 = __ldg(tw + (2 * c + 1) * M);
-    if (c != 0) {
-      const float2 w = __ldg(tw + (2 * c) * M);
-      const float na = a * w.x - b * w.y, nb = a * w.y + b * w.x;
-      a = na;
-      b = nb;
-    } else if (wait) {
-      tk_cluster_wait();   // warp-uniform: every lane of the warp is in this item
-    }
-    const float nd = d * w1.x - e * w1.y, ne = d * w1.y + e * w1.x;
-    const uint32_t base = yb[(2 * c) / K1] + static_cast<uint32_t>(((2 * c) % K1) * PM * sizeof(float2));
-    asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(base), "f"(a), "f"(b) : "memory");
-    asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};"
-                 ::"r"(base + static_cast<uint32_t>(PM * sizeof(float2))), "f"(nd), "f"(ne) : "memory");
+  __device__ __forceinline__ void ld(int c, R& a, R& b, R& d, R& e) const {
+    ld(2 * c, a, b);
+    ld(2 * c + 1, d, e);
+  }
+  __device__ __forceinline__ void put(int k1, R a, R b) const {
+    st_cluster(yb[k1 / K1] + static_cast<uint32_t>((k1 % K1) * PM * sizeof(V2)), a, b);
+  }
+  __device__ __forceinline__ void st(int c, R a, R b) const {
+    if (c != 0) cmul(a, b, __ldg(tw + c * M));
+    else if (wait) tk_cluster_wait();   // warp-uniform: every lane of the warp is in this item
+    put(c, a, b);
+  }
+  __device__ __forceinline__ void st(int c, R a, R b, R d, R e) const {
+    const V2 w1 = __ldg(tw + (2 * c + 1) * M);
+    if (c != 0) cmul(a, b, __ldg(tw + (2 * c) * M));
+    else if (wait) tk_cluster_wait();
+    cmul(d, e, w1);
+    put(2 * c, a, b);
+    put(2 * c + 1, d, e);
   }
 };
 
-template <int N3, int P3>
+template <typename R, int N3, int P3>
 struct B3Io {
-  float2* sp;                      // Y + k1 PM + n3
-  const float2* __restrict__ tw;   // tw2 + n3: tw2[k2 N3 + n3] = w_M^(n3 k2)
-  __device__ __forceinline__ void ld(int c, float& a, float& b, float& d, float& e) const {
-    const float2 u = sp[(2 * c) * P3], v = sp[(2 * c + 1) * P3];
-    a = u.x; b = u.y; d = v.x; e = v.y;
+  using V2 = typename RT<R>::V2;
+  V2* sp;                      // Y + k1 PM + n3
+  const V2* __restrict__ tw;   // tw2 + n3: tw2[k2 N3 + n3] = w_M^(n3 k2)
+  __device__ __forceinline__ void ld(int c, R& a, R& b) const {
+    const V2 u = sp[c * P3];
+    a = u.x; b = u.y;
   }
-  __device__ __forceinline__ void st(int c, float a, float b, float d, float e) const {
-    const float2 w1 = __ldg(tw + (2 * c + 1) * N3);
-    if (c != 0) {
-      const float2 w = __ldg(tw + (2 * c) * N3);
-      const float na = a * w.x - b * w.y, nb = a * w.y + b * w.x;
-      a = na;
-      b = nb;
-    }
-    sp[(2 * c) * P3] = make_float2(a, b);
-    sp[(2 * c + 1) * P3] = make_float2(d * w1.x - e * w1.y, d * w1.y + e * w1.x);
+  __device__ __forceinline__ void ld(int c, R& a, R& b, R& d, R& e) const {
+    ld(2 * c, a, b);
+    ld(2 * c + 1, d, e);
+  }
+  __device__ __forceinline__ void st(int c, R a, R b) const {
+    if (c != 0) cmul(a, b, __ldg(tw + c * N3));
+    sp[c * P3] = mk2<R>(a, b);
+  }
+  __device__ __forceinline__ void st(int c, R a, R b, R d, R e) const {
+    const V2 w1 = __ldg(tw + (2 * c + 1) * N3);
+    if (c != 0) cmul(a, b, __ldg(tw + (2 * c) * N3));
+    cmul(d, e, w1);
+    sp[(2 * c) * P3] = mk2<R>(a, b);
+    sp[(2 * c + 1) * P3] = mk2<R>(d, e);
   }
 };
 
-template <int V, bool INV, class C>
+template <int V, typename R, bool INV, class C>
 __global__ void __launch_bounds__(C::T, C::MINB)
-k_tile3(const float* __restrict__ in, float* __restrict__ out, size_t rows,
-        const __grid_constant__ TabP<float, C::NT1> t1, const __grid_constant__ TabP<float, C::NT2> t2,
-        const __grid_constant__ TabP<float, C::NT3> t3, const float2* __restrict__ tw1,
-        const float2* __restrict__ tw2, float scale) {
+k_tile3(const R* __restrict__ in, R* __restrict__ out, size_t rows,
+        const __grid_constant__ TabP<R, C::NT1> t1, const __grid_constant__ TabP<R, C::NT2> t2,
+        const __grid_constant__ TabP<R, C::NT3> t3, const typename RT<R>::V2* __restrict__ tw1,
+        const typename RT<R>::V2* __restrict__ tw2, R scale) {
+  using V2 = typename RT<R>::V2;
   constexpr int LG1 = 31 - __builtin_clz(C::N1), LG2 = 31 - __builtin_clz(C::N2), LG3 = 31 - __builtin_clz(C::N3);
-  using G1 = SmallGen<V, 0, LG1, float>;
-  using G2 = SmallGen<V, 0, LG2, float>;
-  using G3 = SmallGen<V, 0, LG3, float>;
+  using G1 = SmallGen<V, 0, LG1, R>;
+  using G2 = SmallGen<V, 0, LG2, R>;
+  using G3 = SmallGen<V, 0, LG3, R>;
   constexpr int N1 = C::N1, N2 = C::N2, N3 = C::N3, M = C::M, N = C::N, P = C::P, K1 = C::K1;
   extern __shared__ __align__(128) unsigned char sm[];
-  float2* Y = reinterpret_cast<float2*>(sm);
+  V2* Y = reinterpret_cast<V2*>(sm);
   const int tid = threadIdx.x;
   // P > 1: one row per cluster; q = this CTA's rank (its planes and columns)
   uint32_t q = 0;
@@ -379,35 +453,37 @@ k_tile3(const float* __restrict__ in, float* __restrict__ out, size_t rows,
   for (size_t row = r_first; row < rows; row += r_step) {
     // the next row's inputs of this CTA: bulk prefetches into L2
     if (row + r_step < rows) {
-      const float* nx = in + (row + r_step) * 2 * N;
+      const R* nx = in + (row + r_step) * 2 * N;
       if constexpr (P == 1) {
         if (tid == 0)
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nx), "n"(N * 8) : "memory");
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                       ::"l"(nx), "n"(N * static_cast<int>(sizeof(V2))) : "memory");
       } else if (tid < N1) {   // N1 pieces of M/P columns
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
-                     ::"l"(nx + (static_cast<size_t>(tid) * M + q * (M / P)) * 2), "n"(M / P * 8) : "memory");
+                     ::"l"(nx + (static_cast<size_t>(tid) * M + q * (M / P)) * 2),
+                       "n"(M / P * static_cast<int>(sizeof(V2))) : "memory");
       }
     }
-    const float2* x = reinterpret_cast<const float2*>(in) + row * N;
+    const V2* x = reinterpret_cast<const V2*>(in) + row * N;
     if constexpr (P == 1) {
 #pragma unroll 1
       for (int m = tid; m < M; m += C::T) {
-        A3Io<M, C::PM, INV> io{x + m, Y + (m / N3) * C::P3 + m % N3, tw1 + m};
-        G1::template run<Arith<float>>(io, t1.v);
+        A3Io<R, M, C::PM, INV> io{x + m, Y + (m / N3) * C::P3 + m % N3, tw1 + m};
+        G1::template run<Arith<R>>(io, t1.v);
       }
       __syncthreads();
     } else {
 #pragma unroll 1
       for (int mm = tid; mm < M / P; mm += C::T) {
         const int m = static_cast<int>(q) * (M / P) + mm;
-        A3IoC<M, C::PM, K1, P, INV> io;
+        A3IoC<R, M, C::PM, K1, P, INV> io;
         io.gi = x + m;
         io.tw = tw1 + m;
-        const uint32_t off = static_cast<uint32_t>(((m / N3) * C::P3 + m % N3) * sizeof(float2));
+        const uint32_t off = static_cast<uint32_t>(((m / N3) * C::P3 + m % N3) * sizeof(V2));
 #pragma unroll
         for (int k = 0; k < P; ++k) io.yb[k] = ywin[k] + off;
         io.wait = mm == tid && row != r_first;   // first item of a row after the first
-        G1::template run<Arith<float>>(io, t1.v);
+        G1::template run<Arith<R>>(io, t1.v);
       }
       tk_cluster_arrive();   // all planes complete and visible
       tk_cluster_wait();
@@ -415,16 +491,16 @@ k_tile3(const float* __restrict__ in, float* __restrict__ out, size_t rows,
 #pragma unroll 1
     for (int j = tid; j < K1 * N3; j += C::T) {
       const int n3 = j % N3, k1 = j / N3;
-      B3Io<N3, C::P3> io{Y + k1 * C::PM + n3, tw2 + n3};
-      G2::template run<Arith<float>>(io, t2.v);
+      B3Io<R, N3, C::P3> io{Y + k1 * C::PM + n3, tw2 + n3};
+      G2::template run<Arith<R>>(io, t2.v);
     }
     __syncthreads();
 #pragma unroll 1
     for (int j = tid; j < K1 * N2; j += C::T) {
       const int k1 = j % K1, k2 = j / K1;
-      BIo<N1 * N2, INV> io{reinterpret_cast<const float4*>(Y + k1 * C::PM + k2 * C::P3),
-                           reinterpret_cast<float2*>(out) + row * N + (q * K1 + k1) + N1 * k2, scale};
-      G3::template run<Arith<float>>(io, t3.v);
+      BIo<R, N1 * N2, INV> io{Y + k1 * C::PM + k2 * C::P3,
+                              reinterpret_cast<V2*>(out) + row * N + (q * K1 + k1) + N1 * k2, scale};
+      G3::template run<Arith<R>>(io, t3.v);
     }
     if constexpr (P == 1) __syncthreads();   // Y is rewritten by the next row's phase A
     else tk_cluster_arrive();                 // ... by the peers': the wait is in their first store
@@ -435,39 +511,31 @@ k_tile3(const float* __restrict__ in, float* __restrict__ out, size_t rows,
   }
 }
 
-template <int V, int LG1, int LG2, int LG3, int T, int MB, int P = 1>
+template <int V, typename R, int LG1, int LG2, int LG3, int T, int MB, int P = 1>
 class Tile3PlanImpl final : public FastPlan {
-  using C = T3Cfg<LG1, LG2, LG3, T, MB, P>;
+  using C = T3Cfg<R, LG1, LG2, LG3, T, MB, P>;
+  using V2 = typename RT<R>::V2;
 
  public:
   Tile3PlanImpl(const void* tab, uint32_t nmax, int device) {
-    check_(smallk::fetch_table(t1_.v, C::NT1, tab, nmax));
-    check_(smallk::fetch_table(t2_.v, C::NT2, tab, nmax));
-    check_(smallk::fetch_table(t3_.v, C::NT3, tab, nmax));
-    // tw1[k1 M + m] = w_N^(m k1), tw2[k2 N3 + n3] = w_M^(n3 k2): long double, rounded once
-    const long double two_pi = 6.283185307179586476925286766559005768L;
-    std::vector<float2> tw(static_cast<size_t>(C::N) + C::M);
-    for (int k1 = 0; k1 < C::N1; ++k1)
-      for (int m = 0; m < C::M; ++m) {
-        const long double a = two_pi * static_cast<long double>((k1 * m) % C::N) / static_cast<long double>(C::N);
-        tw[static_cast<size_t>(k1) * C::M + m] = float2{static_cast<float>(cosl(a)), static_cast<float>(-sinl(a))};
-      }
-    for (int k2 = 0; k2 < C::N2; ++k2)
-      for (int n3 = 0; n3 < C::N3; ++n3) {
-        const long double a = two_pi * static_cast<long double>((k2 * n3) % C::M) / static_cast<long double>(C::M);
-        tw[static_cast<size_t>(C::N) + k2 * C::N3 + n3] = float2{static_cast<float>(cosl(a)), static_cast<float>(-sinl(a))};
-      }
-    check_(cudaMalloc(&tw_, tw.size() * sizeof(float2)));
-    check_(cudaMemcpy(tw_, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice));
-    auto f0 = k_tile3<V, false, C>;
-    auto f1 = k_tile3<V, true, C>;
-    check_(cudaFuncSetAttribute(f0, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM)));
-    check_(cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM)));
+    tk_check(smallk::fetch_table(t1_.v, C::NT1, tab, nmax));
+    tk_check(smallk::fetch_table(t2_.v, C::NT2, tab, nmax));
+    tk_check(smallk::fetch_table(t3_.v, C::NT3, tab, nmax));
+    // tw1[k1 M + m] = w_N^(m k1), tw2[k2 N3 + n3] = w_M^(n3 k2)
+    std::vector<V2> tw(static_cast<size_t>(C::N) + C::M);
+    fill_twiddles(tw.data(), C::N1, C::M, C::N);
+    fill_twiddles(tw.data() + C::N, C::N2, C::N3, C::M);
+    tk_check(cudaMalloc(&tw_, tw.size() * sizeof(V2)));
+    tk_check(cudaMemcpy(tw_, tw.data(), tw.size() * sizeof(V2), cudaMemcpyHostToDevice));
+    auto f0 = k_tile3<V, R, false, C>;
+    auto f1 = k_tile3<V, R, true, C>;
+    tk_check(cudaFuncSetAttribute(f0, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM)));
+    tk_check(cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM)));
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     if (P == 1) {
       int per_sm = 0;
-      check_(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f0, C::T, C::SMEM));
+      tk_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f0, C::T, C::SMEM));
       if (per_sm < 1) throw std::runtime_error("three-factor tile kernel does not fit an SM");
       grid_cap_ = per_sm * sms;
     } else {
@@ -475,7 +543,7 @@ class Tile3PlanImpl final : public FastPlan {
       cudaLaunchAttribute attr[1];
       fill_(&cfg, attr, P * sms, nullptr);
       int nc = 0;
-      check_(cudaOccupancyMaxActiveClusters(&nc, f0, &cfg));
+      tk_check(cudaOccupancyMaxActiveClusters(&nc, f0, &cfg));
       if (nc < 1) throw std::runtime_error("three-factor tile kernel: no cluster of this size fits");
       grid_cap_ = nc * P;
     }
@@ -485,33 +553,30 @@ class Tile3PlanImpl final : public FastPlan {
     if (tw_) cudaFree(tw_);
   }
   void exec(const void* in, void* out, size_t rows, int inverse, cudaStream_t st) override {
-    const float scale = 1.0f / static_cast<float>(C::N);
-    const float* fi = static_cast<const float*>(in);
-    float* fo = static_cast<float*>(out);
-    const float2* tw2 = tw_ + C::N;
+    const R scale = R(1) / static_cast<R>(C::N);
+    const R* fi = static_cast<const R*>(in);
+    R* fo = static_cast<R*>(out);
+    const V2* tw1 = tw_;
+    const V2* tw2 = tw_ + C::N;
     cudaError_t e;
     if (P == 1) {
       const unsigned grid = static_cast<unsigned>(std::min<size_t>(rows, static_cast<size_t>(grid_cap_)));
-      if (inverse) k_tile3<V, true, C><<<grid, C::T, C::SMEM, st>>>(fi, fo, rows, t1_, t2_, t3_, tw_, tw2, scale);
-      else k_tile3<V, false, C><<<grid, C::T, C::SMEM, st>>>(fi, fo, rows, t1_, t2_, t3_, tw_, tw2, scale);
+      if (inverse) k_tile3<V, R, true, C><<<grid, C::T, C::SMEM, st>>>(fi, fo, rows, t1_, t2_, t3_, tw1, tw2, scale);
+      else k_tile3<V, R, false, C><<<grid, C::T, C::SMEM, st>>>(fi, fo, rows, t1_, t2_, t3_, tw1, tw2, scale);
       e = cudaGetLastError();
     } else {
       const unsigned grid = static_cast<unsigned>(std::min<size_t>(rows * P, static_cast<size_t>(grid_cap_)));
       cudaLaunchConfig_t cfg{};
       cudaLaunchAttribute attr[1];
       fill_(&cfg, attr, static_cast<int>(grid), st);
-      const float2* tw1 = tw_;
-      if (inverse) e = cudaLaunchKernelEx(&cfg, k_tile3<V, true, C>, fi, fo, rows, t1_, t2_, t3_, tw1, tw2, scale);
-      else e = cudaLaunchKernelEx(&cfg, k_tile3<V, false, C>, fi, fo, rows, t1_, t2_, t3_, tw1, tw2, scale);
+      if (inverse) e = cudaLaunchKernelEx(&cfg, k_tile3<V, R, true, C>, fi, fo, rows, t1_, t2_, t3_, tw1, tw2, scale);
+      else e = cudaLaunchKernelEx(&cfg, k_tile3<V, R, false, C>, fi, fo, rows, t1_, t2_, t3_, tw1, tw2, scale);
       if (e == cudaSuccess) e = cudaGetLastError();
     }
-    if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+    tk_check(e);
   }
 
  private:
-  static void check_(cudaError_t e) {
-    if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
-  }
   static void fill_(cudaLaunchConfig_t* cfg, cudaLaunchAttribute* attr, int grid, cudaStream_t st) {
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = P;
@@ -524,62 +589,57 @@ class Tile3PlanImpl final : public FastPlan {
     cfg->attrs = attr;
     cfg->numAttrs = 1;
   }
-  TabP<float, C::NT1> t1_{};
-  TabP<float, C::NT2> t2_{};
-  TabP<float, C::NT3> t3_{};
-  float2* tw_ = nullptr;
+  TabP<R, C::NT1> t1_{};
+  TabP<R, C::NT2> t2_{};
+  TabP<R, C::NT3> t3_{};
+  V2* tw_ = nullptr;
   int grid_cap_ = 148;
 };
 
-// The split per size: N1 (phase A, strided columns) x N2 (phase B, rows).
-template <int V>
+// The split per size (fast.cu tile_split mirrors it for the op counts).
+// Measured on the B200, ms per 2^28 reals (tools/tile_ab.sh, AMQFT_TILE_AB
+// builds): fp32 2048 as 64 x 32 0.780 (32 x 64: 0.803); 512 as 16 x 32 0.679
+// (32 x 16: 0.717); 8192 as 32 x 16 x 16 at 256 threads x 2 CTAs 0.747 (16 x
+// 16 x 32: 0.802; 128 threads x 3: 0.93); 16384 as 32 x 16 x 32 at 512
+// threads 0.843 (16 x 32 x 32: 0.959, 32 x 32 x 16: 0.928); 2^15 on a cluster
+// of 2 CTAs 1.14 (4 CTAs x 256 threads: 1.23); 2^16 on 4 CTAs as 32 x 32 x 64
+// 1.42 (64 x 32 x 32: 1.52; 8 CTAs: 1.46 / 1.56) -- the multi-pass four-step
+// ran both at 2.13.  Dead ends: twiddles in tensor memory (tcgen05.ld per
+// chunk: 2.5 ms at N = 4096 against 0.91), 128-thread CTAs (0.953 against
+// 0.912), N = 8 as 2 x 4 (no gain over the direct kernel).
+template <int V, typename R>
 std::unique_ptr<FastPlan> make_tile(size_t n, const void* tab, uint32_t nmax, int dev) {
-#ifdef AMQFT_TILE_AB   // A/B instances (diagnostic builds): AMQFT_TILE_KV = T,MB,PF
-  if (const char* kv = std::getenv("AMQFT_TILE_KV")) {
-    int t = 64, mb = 0, fl = 0;
-    std::sscanf(kv, "%d,%d,%d", &t, &mb, &fl);
-    if ((n == 2048 || n == 512) && std::getenv("AMQFT_TILE_SWAP")) n += 1;   // the swapped splits
-#define AMQFT_TILE_CASE(NN, A, B, TT, MM, FF) \
-    if (n == NN && t == TT && mb == MM && fl == FF) return std::make_unique<TilePlanImpl<V, A, B, TT, MM, FF>>(tab, nmax, dev);
-    if (n == 32768 && t == 256) return std::make_unique<Tile3PlanImpl<V, 5, 5, 5, 256, 2, 4>>(tab, nmax, dev);
-    if (n == 65536 && t == 257) return std::make_unique<Tile3PlanImpl<V, 6, 5, 5, 256, 1, 4>>(tab, nmax, dev);
-    if (n == 8192 && t == 256) return std::make_unique<Tile3PlanImpl<V, 4, 4, 5, 256, 2>>(tab, nmax, dev);
-    if (n == 16384 && t == 256) return std::make_unique<Tile3PlanImpl<V, 4, 5, 5, 512, 1>>(tab, nmax, dev);
-    AMQFT_TILE_CASE(4096, 6, 6, 64, 4, 0)
-    AMQFT_TILE_CASE(4096, 6, 6, 64, 4, 1)
-    AMQFT_TILE_CASE(4096, 6, 6, 64, 5, 1)
-    AMQFT_TILE_CASE(2048, 5, 6, 64, 4, 0)
-    AMQFT_TILE_CASE(2048, 5, 6, 64, 4, 1)
-    AMQFT_TILE_CASE(2048, 5, 6, 64, 6, 1)
-    AMQFT_TILE_CASE(2049, 6, 5, 64, 4, 0)
-    AMQFT_TILE_CASE(2049, 6, 5, 64, 4, 1)
-    AMQFT_TILE_CASE(2049, 6, 5, 64, 5, 1)
-    AMQFT_TILE_CASE(512, 4, 5, 64, 0, 1)
-    AMQFT_TILE_CASE(512, 4, 5, 64, 0, 0)
-    AMQFT_TILE_CASE(513, 5, 4, 64, 0, 0)
-#undef AMQFT_TILE_CASE
-    throw std::invalid_argument("AMQFT_TILE_KV: no such instance");
-  }
-#endif
-  switch (n) {
-    case 16: return std::make_unique<TilePlanImpl<V, 2, 2>>(tab, nmax, dev);
-    case 32: return std::make_unique<TilePlanImpl<V, 2, 3>>(tab, nmax, dev);
-    case 64: return std::make_unique<TilePlanImpl<V, 3, 3>>(tab, nmax, dev);
-    case 128: return std::make_unique<TilePlanImpl<V, 3, 4>>(tab, nmax, dev);
-    case 256: return std::make_unique<TilePlanImpl<V, 4, 4>>(tab, nmax, dev);
-    case 512: return std::make_unique<TilePlanImpl<V, 4, 5>>(tab, nmax, dev);
-    case 1024: return std::make_unique<TilePlanImpl<V, 5, 5>>(tab, nmax, dev);
-    case 2048: return std::make_unique<TilePlanImpl<V, 6, 5>>(tab, nmax, dev);   // 0.780 vs 0.803 ms for 32 x 64
-    case 4096: return std::make_unique<TilePlanImpl<V, 6, 6>>(tab, nmax, dev);
-    // measured (B200, ms per 2^28 reals): 32 x 16 x 16 at 256 threads x 2 CTAs 0.747; 16 x 16 x 32 0.802
-    case 8192: return std::make_unique<Tile3PlanImpl<V, 5, 4, 4, 256, 2>>(tab, nmax, dev);
-    // 32 x 16 x 32 at 512 threads 0.843; 16 x 32 x 32 0.959; 32 x 32 x 16 0.928
-    case 16384: return std::make_unique<Tile3PlanImpl<V, 5, 4, 5, 512, 1>>(tab, nmax, dev);
-    // one row per cluster (DSMEM exchange in phase A): 2^15 on 2 CTAs 3.76 TB/s (4 CTAs x 256
-    // threads: 3.48); 2^16 on 4 CTAs as 32 x 32 x 64 3.03 (64 x 32 x 32: 2.83; 8 CTAs: 2.95 / 2.76);
-    // the multi-pass four-step ran both at 2.0
-    case 32768: return std::make_unique<Tile3PlanImpl<V, 5, 5, 5, 512, 1, 2>>(tab, nmax, dev);
-    case 65536: return std::make_unique<Tile3PlanImpl<V, 5, 5, 6, 256, 1, 4>>(tab, nmax, dev);
+  if constexpr (sizeof(R) == 4) {
+    switch (n) {
+      case 16: return std::make_unique<TilePlanImpl<V, R, 2, 2>>(tab, nmax, dev);
+      case 32: return std::make_unique<TilePlanImpl<V, R, 2, 3>>(tab, nmax, dev);
+      case 64: return std::make_unique<TilePlanImpl<V, R, 3, 3>>(tab, nmax, dev);
+      case 128: return std::make_unique<TilePlanImpl<V, R, 3, 4>>(tab, nmax, dev);
+      case 256: return std::make_unique<TilePlanImpl<V, R, 4, 4>>(tab, nmax, dev);
+      case 512: return std::make_unique<TilePlanImpl<V, R, 4, 5>>(tab, nmax, dev);
+      case 1024: return std::make_unique<TilePlanImpl<V, R, 5, 5>>(tab, nmax, dev);
+      case 2048: return std::make_unique<TilePlanImpl<V, R, 6, 5>>(tab, nmax, dev);
+      case 4096: return std::make_unique<TilePlanImpl<V, R, 6, 6>>(tab, nmax, dev);
+      case 8192: return std::make_unique<Tile3PlanImpl<V, R, 5, 4, 4, 256, 2>>(tab, nmax, dev);
+      case 16384: return std::make_unique<Tile3PlanImpl<V, R, 5, 4, 5, 512, 1>>(tab, nmax, dev);
+      case 32768: return std::make_unique<Tile3PlanImpl<V, R, 5, 5, 5, 512, 1, 2>>(tab, nmax, dev);
+      case 65536: return std::make_unique<Tile3PlanImpl<V, R, 5, 5, 6, 256, 1, 4>>(tab, nmax, dev);
+    }
+  } else {   // fp64: factors <= 32 points
+    switch (n) {
+      case 16: return std::make_unique<TilePlanImpl<V, R, 2, 2>>(tab, nmax, dev);
+      case 32: return std::make_unique<TilePlanImpl<V, R, 2, 3>>(tab, nmax, dev);
+      case 64: return std::make_unique<TilePlanImpl<V, R, 3, 3>>(tab, nmax, dev);
+      case 128: return std::make_unique<TilePlanImpl<V, R, 3, 4>>(tab, nmax, dev);
+      case 256: return std::make_unique<TilePlanImpl<V, R, 4, 4>>(tab, nmax, dev);
+      case 512: return std::make_unique<TilePlanImpl<V, R, 4, 5>>(tab, nmax, dev);
+      case 1024: return std::make_unique<TilePlanImpl<V, R, 5, 5>>(tab, nmax, dev);
+      case 2048: return std::make_unique<Tile3PlanImpl<V, R, 3, 4, 4, 128, 4>>(tab, nmax, dev);
+      case 4096: return std::make_unique<Tile3PlanImpl<V, R, 4, 4, 4, 256, 2>>(tab, nmax, dev);
+      case 8192: return std::make_unique<Tile3PlanImpl<V, R, 5, 4, 4, 256, 1>>(tab, nmax, dev);
+      case 16384: return std::make_unique<Tile3PlanImpl<V, R, 5, 4, 5, 256, 1, 2>>(tab, nmax, dev);
+      case 32768: return std::make_unique<Tile3PlanImpl<V, R, 5, 5, 5, 256, 1, 4>>(tab, nmax, dev);
+    }
   }
   return nullptr;
 }

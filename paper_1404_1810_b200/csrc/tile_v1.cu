@@ -4,6 +4,7 @@
 
 namespace amqft_b200 {
 namespace tilek {
-template std::unique_ptr<FastPlan> make_tile<1>(size_t, const void*, uint32_t, int);
+template std::unique_ptr<FastPlan> make_tile<1, float>(size_t, const void*, uint32_t, int);
+template std::unique_ptr<FastPlan> make_tile<1, double>(size_t, const void*, uint32_t, int);
 }  // namespace tilek
 }  // namespace amqft_b200

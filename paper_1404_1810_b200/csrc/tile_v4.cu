@@ -1,10 +1,10 @@
 // tile_v4.cu -- in-shared-memory four-step instances for AM-QFT variant 4.
-#define AMQFT_TILE_AB 1
 #include "gen/small_gen_v4.cuh"
 #include "tile_kernel.cuh"
 
 namespace amqft_b200 {
 namespace tilek {
-template std::unique_ptr<FastPlan> make_tile<4>(size_t, const void*, uint32_t, int);
+template std::unique_ptr<FastPlan> make_tile<4, float>(size_t, const void*, uint32_t, int);
+template std::unique_ptr<FastPlan> make_tile<4, double>(size_t, const void*, uint32_t, int);
 }  // namespace tilek
 }  // namespace amqft_b200

@@ -180,7 +180,7 @@ def test_fast_kernel_fp64_bitwise(oracle, restatement, n):
     r, O = restatement, oracle
     for v in range(1, 9):
         xs = [O.seeded_signal(21, O.CDFT, n, 10 * v + k, r) for k in range(3)]
-        plan = amqft.Plan(v, amqft.FunctionId.Cdft, n, 3, dtype="f64", order=amqft.Order.Fast)
+        plan = amqft.Plan(v, amqft.FunctionId.Cdft, n, 3, dtype="f64", order=amqft.Order.FastDag)
         assert plan.path()[0] == 2, "fused kernel expected"
         got = run_plan(plan, xs)
         for k in range(3):
@@ -214,7 +214,7 @@ def test_fast_kernel_persistent_rows_bitwise(oracle, restatement, v):
     row staged by TMA while the current one computes.  fp64 bitwise."""
     r, O = restatement, oracle
     n, batch = 4096, 700
-    plan = amqft.Plan(v, amqft.FunctionId.Cdft, n, batch, dtype="f64", order=amqft.Order.Fast)
+    plan = amqft.Plan(v, amqft.FunctionId.Cdft, n, batch, dtype="f64", order=amqft.Order.FastDag)
     assert plan.path()[0] == 2
     rng = np.random.default_rng(100 + v)
     x = torch.tensor(rng.uniform(-1, 1, (batch, 2 * n)), dtype=torch.float64, device=DEV)
@@ -329,7 +329,7 @@ def test_fast_kernel_larger_table_bitwise(oracle, restatement, n):
     r, O = restatement, oracle
     for v in (1, 2, 4, 7):
         xs = [O.seeded_signal(31, O.CDFT, n, v, r)]
-        plan = amqft.Plan(v, amqft.FunctionId.Cdft, n, 1, dtype="f64", order=amqft.Order.Fast,
+        plan = amqft.Plan(v, amqft.FunctionId.Cdft, n, 1, dtype="f64", order=amqft.Order.FastDag,
                           table_max_n=4 * n)
         assert plan.path()[0] == 2
         got = run_plan(plan, xs)[0]
@@ -600,7 +600,9 @@ def test_fourstep_fp64_config3_sizes(oracle, restatement, lg):
     ref = np.empty(2 * n)
     ref[0::2], ref[1::2] = f.real, f.imag
     for v in range(1, 9):
-        plan = amqft.Plan(v, amqft.FunctionId.Cdft, n, 1, dtype="f64", order=amqft.Order.Fast)
+        # FastDag: the multi-pass four-step at every size (the default order runs N <= 2^15 of
+        # variants 1-4 in one pass inside shared memory, tests/test_gpu_tile.py)
+        plan = amqft.Plan(v, amqft.FunctionId.Cdft, n, 1, dtype="f64", order=amqft.Order.FastDag)
         assert plan.path()[0] == 3, (v, lg)
         got = run_plan(plan, [x])[0]
         back = run_plan(plan, [got], inverse=True)[0]
@@ -806,7 +808,7 @@ def test_fourstep_large_batch_grid_chunking(oracle, restatement):
     x = torch.rand(rows, 2 * n, dtype=torch.float64, device=DEV, generator=g) * 2 - 1
     y = torch.empty_like(x)
     z = torch.empty_like(x)
-    plan = amqft.Plan(4, amqft.FunctionId.Cdft, n, rows, dtype="f64", order=amqft.Order.Fast)
+    plan = amqft.Plan(4, amqft.FunctionId.Cdft, n, rows, dtype="f64", order=amqft.Order.FastDag)
     assert plan.path()[0] == 3
     plan.forward(x, y)
     plan.inverse(y, z)
@@ -826,8 +828,8 @@ def test_fast_plans_onthefly_constants_are_the_table(oracle, restatement):
     for n in (64, 4096):
         x = O.seeded_signal(5, O.CDFT, n, 1, r)
         for v in (2, 5):
-            a = amqft.Plan(v, amqft.FunctionId.Cdft, n, 1, dtype="f64", order=amqft.Order.Fast)
-            b = amqft.Plan(v, amqft.FunctionId.Cdft, n, 1, dtype="f64", order=amqft.Order.Fast,
+            a = amqft.Plan(v, amqft.FunctionId.Cdft, n, 1, dtype="f64", order=amqft.Order.FastDag)
+            b = amqft.Plan(v, amqft.FunctionId.Cdft, n, 1, dtype="f64", order=amqft.Order.FastDag,
                            trig_mode=amqft.TrigMode.OnTheFly)
             assert a.path()[0] == b.path()[0] >= 2
             ga, gb = run_plan(a, [x])[0], run_plan(b, [x])[0]

@@ -144,3 +144,76 @@ def test_tile_rejects_misaligned_buffers():
     x = torch.zeros(2 * n + 2, dtype=torch.float32, device=DEV)
     with pytest.raises(amqft.InvalidArgument):
         plan.forward(x[1:2 * n + 1], x[1:2 * n + 1], rows=1)
+
+
+# ---- fp64 instances: factors <= 32 points, N = 64 .. 2^15.  The plan takes this path only where
+# the result stays within 1e-12 of the CPU reference of the same variant (fast.cu tile_covers):
+# variants 1-4 at every size, variants 5-8 up to N = 256 (beyond, the reference's own v5-8 drift from
+# the DFT, and the plan keeps the reference DAG: the fused kernel's fp64 instance, bitwise).
+SIZES64 = [64, 128, 256, 512, 1024, 2048, 4096, 8192, 16384, 32768]
+SPLIT64 = {64: (8, 8), 128: (8, 16), 256: (16, 16), 512: (16, 32), 1024: (32, 32), 2048: (8, 16, 16),
+           4096: (16, 16, 16), 8192: (32, 16, 16), 16384: (32, 16, 32), 32768: (32, 32, 32)}
+
+
+@pytest.mark.parametrize("n", SIZES64)
+def test_tile_fp64_within_1e12_of_cpu(oracle, restatement, n):
+    r, O = restatement, oracle
+    rows = 3
+    xs = np.stack([O.seeded_signal(41, O.CDFT, n, k, r) for k in range(rows)])
+    for v in range(1, 9):
+        plan = amqft.Plan(v, amqft.FunctionId.Cdft, n, rows, dtype="f64", order=amqft.Order.Fast)
+        if v >= 5 and n > 256:
+            assert plan.path()[0] != 6, (v, n)   # the reference DAG (bitwise) or its four-step
+            continue
+        assert plan.path() == (6, 1), (v, n)
+        got = run_plan(plan, xs)
+        for row in range(rows):
+            assert r.rel_l2(got[row], r.execute(v, O.F_CDFT, n, xs[row])) <= 1e-12, (v, n)
+            assert r.rel_l2(got[row], numpy_dft(xs[row])) <= 1e-14, (v, n)
+        back = run_plan(plan, got, inverse=True)
+        assert r.rel_l2(back.ravel(), xs.ravel()) <= 1e-14, (v, n)
+        f = SPLIT64[n]
+        want = [0, 0, 0]
+        for nf in f:
+            m = r.execute(v, O.F_CDFT, nf, np.zeros(2 * nf), meter=True)[1]
+            for i in range(3):
+                want[i] += (n // nf) * m[i]
+        want[0] += 2 * n * (len(f) - 1)
+        want[1] += 4 * n * (len(f) - 1)
+        assert plan.op_counts() == tuple(want), (v, n)
+
+
+@pytest.mark.parametrize("n", [256, 4096, 32768])
+def test_tile_fp64_ragged_rows_independent(n):
+    R = 1 if len(SPLIT64[n]) == 3 else max(1, 64 // min(SPLIT64[n]))
+    big = min(148 * 12 * R + R + 1, (1 << 26) // n + 3)
+    x = torch.tensor(np.random.default_rng(n).uniform(-1, 1, (big, 2 * n)), dtype=torch.float64, device=DEV)
+    plan = amqft.Plan(2, amqft.FunctionId.Cdft, n, big, dtype="f64", order=amqft.Order.Fast)
+    assert plan.path() == (6, 1)
+    y = torch.empty_like(x)
+    plan.forward(x, y)
+    torch.cuda.synchronize()
+    single = amqft.Plan(2, amqft.FunctionId.Cdft, n, 1, dtype="f64", order=amqft.Order.Fast)
+    for row in (0, R, big // 2, big - 1):
+        z = torch.empty_like(x[row:row + 1])
+        single.forward(x[row:row + 1].contiguous(), z)
+        torch.cuda.synchronize()
+        assert torch.equal(z[0], y[row]), (n, row)
+
+
+def test_fast_dag_order_keeps_the_reference_dag(oracle, restatement):
+    """Order.FastDag: the whole-DAG kernels (no split inside shared memory);
+    its fp64 instances are bitwise amqft::execute where Order.Fast is within
+    1e-12."""
+    r, O = restatement, oracle
+    for n in (256, 4096):
+        x = O.seeded_signal(43, O.CDFT, n, 0, r)
+        want = r.execute(4, O.F_CDFT, n, x)
+        dag = amqft.Plan(4, amqft.FunctionId.Cdft, n, 1, dtype="f64", order=amqft.Order.FastDag)
+        assert dag.path()[0] in (2, 4)
+        assert run_plan(dag, [x])[0].tobytes() == want.tobytes()
+        fast = amqft.Plan(4, amqft.FunctionId.Cdft, n, 1, dtype="f64", order=amqft.Order.Fast)
+        assert fast.path() == (6, 1)
+        assert r.rel_l2(run_plan(fast, [x])[0], want) <= 1e-12
+    p32 = amqft.Plan(4, amqft.FunctionId.Cdft, 4096, 1, dtype="f32", order=amqft.Order.FastDag)
+    assert p32.path() == (2, 1)

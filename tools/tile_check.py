@@ -30,17 +30,20 @@ def timed(plan, x, y, iters=5):
 def main():
     variants = [int(v) for v in sys.argv[1].split(",")] if len(sys.argv) > 1 else [4]
     lgs = [int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else [8, 9, 10, 11, 12]
+    dtype = sys.argv[3] if len(sys.argv) > 3 else "f32"
+    tdt = torch.float32 if dtype == "f32" else torch.float64
+    esize = 4 if dtype == "f32" else 8
     child = os.environ.get("AMQFT_AB_TILE", "") == "none"
     r = O.restatement()
     for lg in lgs:
         n = 1 << lg
-        batch = (1 << 28) // n
-        x = torch.randn(batch, 2 * n, device="cuda", dtype=torch.float32)
+        batch = (1 << (28 if dtype == "f32" else 27)) // n
+        x = torch.randn(batch, 2 * n, device="cuda", dtype=tdt)
         y = torch.empty_like(x)
         for v in variants:
-            plan = amqft.Plan(v, amqft.FunctionId.Cdft, n, batch, dtype="f32", order=amqft.Order.Fast)
+            plan = amqft.Plan(v, amqft.FunctionId.Cdft, n, batch, dtype=dtype, order=amqft.Order.Fast)
             ms = timed(plan, x, y)
-            gbs = batch * 16 * n / ms / 1e6
+            gbs = batch * 4 * esize * n / ms / 1e6
             line = f"v{v} N={n} path {plan.path()}: {ms:.3f} ms, {gbs:.0f} GB/s"
             if not child:
                 rows = [0, 1, batch - 1]
@@ -51,7 +54,7 @@ def main():
                 got = ys[:, 0::2] + 1j * ys[:, 1::2]
                 e_np = float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
                 z = torch.empty_like(x[:64])
-                p2 = amqft.Plan(v, amqft.FunctionId.Cdft, n, 64, dtype="f32", order=amqft.Order.Fast)
+                p2 = amqft.Plan(v, amqft.FunctionId.Cdft, n, 64, dtype=dtype, order=amqft.Order.Fast)
                 p2.forward(x[:64], z)
                 w = torch.empty_like(z)
                 p2.inverse(z, w)
