@@ -110,11 +110,11 @@ typedef struct {
  * are stream-ordered (CUDA-graph capturable).  amqft_exec_host_rows creates
  * its pipeline slots and streams on its first call (serialised per plan).
  *
- * fp32 plans of variants 5-8 at n >= 512 compute in fp64 (their fp32
+ * fp32 plans of variants 5-8 at n >= 512 that keep the whole DAG (EXACT and
+ * FAST_DAG orders, RDFT / DCT / DST rows) compute in fp64 (their fp32
  * recursion amplifies rounding beyond 1e-5 log2 n): fp32 rows in and out,
- * the reference's fp64 DAG inside where the plan runs it (the fused kernel
- * at n = 1024-4096, the exact order), a four-step over stable
- * sub-transforms elsewhere in the fast order. */
+ * the reference's fp64 DAG inside.  FAST CDFT plans split n into factors of
+ * <= 64 points, which are stable in fp32 for every variant. */
 amqft_status amqft_plan_create(amqft_plan* out, const amqft_plan_desc* desc);
 amqft_status amqft_plan_destroy(amqft_plan plan);
 
