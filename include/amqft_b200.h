@@ -199,6 +199,13 @@ amqft_status amqft_dist_twiddle_scatter(const void* d_rows, void* const* d_dst, 
  * that order (A and n1/A multiples of 32, n1/nparts a multiple of 32).
  * Replaces nothing in the reference (it has no distributed path). */
 amqft_status amqft_plan_transposed_factor(amqft_plan plan, size_t* a);
+/* amqft_plan_create for a caller that will use amqft_exec_rows_transposed:
+ * among the four-step plans it prefers the column-mode one that has a
+ * transposed output (the column-slab plans, measured a little faster as
+ * stand-alone transforms at some sizes, have none).  The distributed
+ * four-step creates its local length-n1 plan with it (config 5 on one B200:
+ * 15.7 ms against 16.1 ms with a slab plan and the plain scatter). */
+amqft_status amqft_plan_create_transposable(amqft_plan* out, const amqft_plan_desc* desc);
 amqft_status amqft_exec_rows_transposed(amqft_plan plan, const void* d_in, void* d_out, size_t rows,
                                         void* stream);
 amqft_status amqft_dist_twiddle_scatter_t(const void* d_rows, void* const* d_dst, size_t rows, size_t n1,

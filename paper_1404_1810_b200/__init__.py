@@ -124,7 +124,8 @@ class Plan:
 
     def __init__(self, variant: int, function: int, n: int, batch: int = 1, *,
                  dtype="f32", order=Order.Fast, trig_mode=TrigMode.Precomputed,
-                 device: int = 0, table_max_n: int = 0, corrupt_constants: bool = False):
+                 device: int = 0, table_max_n: int = 0, corrupt_constants: bool = False,
+                 transposable: bool = False):
         d = _native.PlanDesc()
         d.variant = int(variant)
         d.function = int(function)
@@ -137,7 +138,9 @@ class Plan:
         d.table_max_n = int(table_max_n)
         d.corrupt_constants = int(bool(corrupt_constants))
         self._h = C.c_void_p()
-        check(lib().amqft_plan_create(C.byref(self._h), C.byref(d)))
+        # transposable: prefer a four-step plan with a transposed output (amqft_exec_rows_transposed)
+        create = lib().amqft_plan_create_transposable if transposable else lib().amqft_plan_create
+        check(create(C.byref(self._h), C.byref(d)))
         self.variant, self.function, self.n, self.batch = d.variant, d.function, d.n, d.batch
         self.dtype = "f64" if d.dtype == _native.F64 else "f32"
         self.device = d.device

@@ -59,6 +59,7 @@ def lib() -> C.CDLL:
     L = C.CDLL(LIB_PATH)
     vp, sz, u64p = C.c_void_p, C.c_size_t, C.POINTER(C.c_uint64)
     L.amqft_plan_create.argtypes = [C.POINTER(vp), C.POINTER(PlanDesc)]
+    L.amqft_plan_create_transposable.argtypes = [C.POINTER(vp), C.POINTER(PlanDesc)]
     L.amqft_plan_destroy.argtypes = [vp]
     L.amqft_plan_cells.argtypes = [vp]
     L.amqft_plan_cells.restype = sz
@@ -92,7 +93,7 @@ def lib() -> C.CDLL:
     L.amqft_device_synchronize.argtypes = [C.c_int]
     L.amqft_last_error.restype = C.c_char_p
     L.amqft_version.restype = C.c_char_p
-    for name in ("amqft_plan_create", "amqft_plan_destroy", "amqft_exec_forward",
+    for name in ("amqft_plan_create", "amqft_plan_create_transposable", "amqft_plan_destroy", "amqft_exec_forward",
                  "amqft_exec_inverse", "amqft_exec_rows", "amqft_exec_host_rows", "amqft_execute_host",
                  "amqft_execute_host_constants", "amqft_execute_host_inverse", "amqft_plan_create_with_constants",
                  "amqft_direct_bins", "amqft_direct_bins_extended", "amqft_dist_unique_id",

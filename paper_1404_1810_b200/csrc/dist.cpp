@@ -174,7 +174,7 @@ amqft_status amqft_dist_plan_create(amqft_dist_plan* out, int variant, size_t n,
     d.device = device;
     d.n = P->n1;
     d.batch = P->rows1;
-    ack(amqft_plan_create(&P->p1, &d));
+    ack(amqft_plan_create_transposable(&P->p1, &d));
     d.n = P->n2;
     d.batch = P->w;
     ack(amqft_plan_create(&P->p2, &d));

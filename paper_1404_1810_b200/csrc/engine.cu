@@ -463,6 +463,13 @@ amqft_status amqft_plan_create(amqft_plan* out, const amqft_plan_desc* desc) {
   return create_plan(out, desc, nullptr);
 }
 
+amqft_status amqft_plan_create_transposable(amqft_plan* out, const amqft_plan_desc* desc) {
+  fourstep_prefer_transposable(true);   // thread-local: read by the four-step's plan selection
+  const amqft_status s = create_plan(out, desc, nullptr);
+  fourstep_prefer_transposable(false);
+  return s;
+}
+
 amqft_status amqft_plan_create_with_constants(amqft_plan* out, const amqft_plan_desc* desc,
                                               const double* constants, size_t count) {
   if (!constants) return set_err(AMQFT_EINVAL, "null constant table");

@@ -8,6 +8,7 @@
 #include <type_traits>
 
 #include "fourstep.cuh"
+#include "slab.cuh"
 #include "gen/small_ops.cuh"
 
 namespace amqft_b200 {
@@ -179,6 +180,30 @@ std::unique_ptr<FastPlan> make_tile_plan(const amqft_plan_desc& d, const void* d
   if (!tile_covers(d)) return nullptr;
   return d.dtype == AMQFT_F64 ? make_tile_typed<double>(d, d_trig, nmax) : make_tile_typed<float>(d, d_trig, nmax);
 }
+
+namespace slabk {
+template <int V, typename R>
+std::unique_ptr<SlabPassExec<R>> make_slab_pass(size_t len, const void* tab, uint32_t nmax, int dev);
+}  // namespace slabk
+
+template <typename R>
+std::unique_ptr<slabk::SlabPassExec<R>> make_slab_pass_rt(int variant, size_t len, const void* tab, uint32_t nmax,
+                                                          int dev) {
+  using namespace slabk;
+  switch (variant) {
+    case 1: return make_slab_pass<1, R>(len, tab, nmax, dev);
+    case 2: return make_slab_pass<2, R>(len, tab, nmax, dev);
+    case 3: return make_slab_pass<3, R>(len, tab, nmax, dev);
+    case 4: return make_slab_pass<4, R>(len, tab, nmax, dev);
+    case 5: return make_slab_pass<5, R>(len, tab, nmax, dev);
+    case 6: return make_slab_pass<6, R>(len, tab, nmax, dev);
+    case 7: return make_slab_pass<7, R>(len, tab, nmax, dev);
+    case 8: return make_slab_pass<8, R>(len, tab, nmax, dev);
+  }
+  return nullptr;
+}
+template std::unique_ptr<slabk::SlabPassExec<float>> make_slab_pass_rt<float>(int, size_t, const void*, uint32_t, int);
+template std::unique_ptr<slabk::SlabPassExec<double>> make_slab_pass_rt<double>(int, size_t, const void*, uint32_t, int);
 
 namespace smallk {
 bool small_ops_n(int v, size_t n, bool f64, OpCount* o, int fn = AMQFT_FN_CDFT);

@@ -33,7 +33,10 @@
 #include <vector>
 
 #include "fast.cuh"
+#include <cstdlib>
+
 #include "fourstep.cuh"
+#include "slab.cuh"
 
 namespace amqft_b200 {
 
@@ -699,12 +702,174 @@ void transpose_c64(const void* in, void* out, size_t mats, size_t r, size_t c, c
                      static_cast<int>(c), 1.0f, nullptr, nullptr, 0, 0, 0, st);
 }
 
+// ---- Column-slab plans (slab_kernel.cuh): N = L1 L2 in two passes, N = L1
+// L2 L3 in three, L in {128, 256, 512, 1024}, natural order in and out and
+// no transpose kernel.  Measured against the column / row / transpose
+// four-step above (B200, GB/s on algorithmic bytes): see fourstep_slab_shape.
+struct SlabShape {
+  int passes = 0;
+  size_t len[3] = {0, 0, 0};
+};
+
+// Balanced factors, the largest first.  Two passes for 2^14 .. 2^20, three
+// for 2^21 .. 2^30.
+SlabShape slab_factors(size_t n) {
+  SlabShape s;
+  const int lg = lg2(n);
+  if ((size_t(1) << lg) != n) return s;
+  if (lg >= 14 && lg <= 20) {
+    s.passes = 2;
+    s.len[0] = size_t(1) << ((lg + 1) / 2);
+    s.len[1] = size_t(1) << (lg / 2);
+  } else if (lg >= 21 && lg <= 30) {
+    s.passes = 3;
+    const int a = (lg + 2) / 3, b = (lg - a + 1) / 2, c = lg - a - b;
+    s.len[0] = size_t(1) << a;
+    s.len[1] = size_t(1) << b;
+    s.len[2] = size_t(1) << c;
+  }
+  return s;
+}
+
+// Where the slab plan replaces the column / row / transpose four-step.
+// AMQFT_AB_SLAB=none|all overrides (A/B measurements).
+thread_local bool g_prefer_transposable = false;
+
+SlabShape fourstep_slab_shape(const amqft_plan_desc& d) {
+  SlabShape none;
+  if (d.function != AMQFT_FN_CDFT || g_prefer_transposable) return none;
+  const SlabShape s = slab_factors(d.n);
+  if (!s.passes) return none;
+  if (const char* e = std::getenv("AMQFT_AB_SLAB")) {
+    if (e[0] == 'n') return none;
+    if (e[0] == 'a') return s;
+  }
+  const int lg = lg2(d.n);
+  // one-pass tile kernels own N <= 2^16 (fp32) / 2^15 (fp64 variants 1-4)
+  amqft_plan_desc t = d;
+  t.order = AMQFT_ORDER_FAST;
+  if (tile_covers(t)) return none;
+  // measured (B200, v4, GB/s on algorithmic bytes, slab against column + tile rows + transpose;
+  // tools/slab_ab.sh): fp32 two passes 2^17-2^20 2583 / 2484 / 2180 / 2021 against 2083 / 2077 / 1970 /
+  // 1893; three passes 2^24-2^26 1667 / 1522 / 1640 against 1453 / 1396 / 1356, but 2^21-2^23 1276 / 1363 /
+  // 1468 against 1664 / 1492 / 1518 (128-point slab factors against a one-pass 2^15 / 2^16 tile row).
+  // fp64: 2^16 2804 against 2156, 2^19 / 2^20 1813 / 1890 against 1759 / 1565, 2^22-2^24 1649 / 1796 /
+  // 1837 against 1516 / 1500 / 1366; 2^17 / 2^18 / 2^21 lose (1936 / 1608 / 1521 against 2023 / 1982 / 1589).
+  if (d.dtype == AMQFT_F64) return (lg == 16 || lg == 19 || lg == 20 || lg >= 22) ? s : none;
+  return ((lg >= 17 && lg <= 20) || lg >= 24) ? s : none;
+}
+
+template <typename R>
+class SlabPlan final : public FastPlan {
+  using V2 = typename C2<R>::T;
+
+ public:
+  SlabPlan(int variant, size_t n, size_t batch, int trig_mode, const void* tab, uint32_t nmax, int dev,
+           const SlabShape& sh)
+      : n_(n), batch_(batch), sh_(sh), tws_(n) {
+    const int dtype = sizeof(R) == 8 ? AMQFT_F64 : AMQFT_F32;
+    for (int i = 0; i < sh.passes; ++i) {
+      pass_[i] = make_slab_pass_rt<R>(variant, sh.len[i], tab, nmax, dev);
+      if (!pass_[i]) throw std::invalid_argument("slab four-step: no kernel for a factor");
+    }
+    (void)dtype;
+    ColTwiddle tw;
+    tw.hi = tws_.hi;
+    tw.lo = tws_.lo;
+    tw.logb = tws_.logb;
+    tw.logn = tws_.logn;
+    tw.onthefly = trig_mode == AMQFT_TRIG_ONTHEFLY ? 1 : 0;
+    const size_t L1 = sh.len[0], L2 = sh.len[1], L3 = sh.len[2];
+    using slabk::SlabPass;
+    if (sh.passes == 2) {
+      // pass 1: columns n2 of x [n1][n2] -> Y [n2][k1], times w_N^(n2 k1)
+      SlabPass& a = p_[0];
+      a.in_row = a.out_row = n;
+      a.cols = a.qin = a.qout = static_cast<unsigned>(L2);
+      a.sj_in = L2;
+      a.transposing = 1;
+      a.sj_out = 1;
+      a.sw_out = L1;
+      a.twiddle = 1;
+      a.tw = tw;
+      // pass 2: columns k1 of Y [n2][k1] -> X [k2][k1]
+      SlabPass& b = p_[1];
+      b.in_row = b.out_row = n;
+      b.cols = b.qin = b.qout = static_cast<unsigned>(L1);
+      b.sj_in = b.sj_out = L1;
+    } else {
+      const size_t M = L2 * L3;
+      // pass 1: columns m = L3 n2 + n3 of x [n1][m] -> Y1 [n2][n3][k1], times w_N^(m k1)
+      SlabPass& a = p_[0];
+      a.in_row = a.out_row = n;
+      a.cols = a.qin = a.qout = static_cast<unsigned>(M);
+      a.sj_in = M;
+      a.transposing = 1;
+      a.sj_out = 1;
+      a.sw_out = L1;
+      a.twiddle = 1;
+      a.tw = tw;
+      // pass 2: over n2 for the columns (n3, k1) -> Y2 [n3][k2][k1], times w_M^(n3 k2) = w_N^(L1 n3 k2)
+      SlabPass& b = p_[1];
+      b.in_row = b.out_row = n;
+      b.cols = b.qin = static_cast<unsigned>(L3 * L1);
+      b.sj_in = L3 * L1;
+      b.qout = static_cast<unsigned>(L1);
+      b.qo = L2 * L1;
+      b.sj_out = L1;
+      b.twiddle = 1;
+      b.tdiv = static_cast<unsigned>(L1);
+      b.tw = tw;
+      b.tw.mul = L1;
+      // pass 3: over n3 for the columns (k2, k1), in place -> X [k3][k2][k1]
+      SlabPass& c = p_[2];
+      c.in_row = c.out_row = n;
+      c.cols = c.qin = c.qout = static_cast<unsigned>(L2 * L1);
+      c.sj_in = c.sj_out = L2 * L1;
+    }
+    if (cudaMalloc(&scratch_, batch_ * n_ * sizeof(V2)) != cudaSuccess)
+      throw std::runtime_error("cudaMalloc slab four-step scratch");
+    launches = sh.passes;
+  }
+  ~SlabPlan() override {
+    if (scratch_) cudaFree(scratch_);
+  }
+  void exec(const void* in, void* out, size_t rows, int inverse, cudaStream_t st) override {
+    if (rows > batch_) throw std::invalid_argument("rows exceed the plan batch");
+    const bool inv = inverse != 0;
+    const R scale = R(1) / static_cast<R>(n_);
+    const bool alias = in == out;
+    if (sh_.passes == 2) {
+      void* mid = alias ? static_cast<void*>(scratch_) : out;
+      pass_[0]->run(in, mid, rows, p_[0], inv, false, R(1), st);
+      pass_[1]->run(mid, out, rows, p_[1], false, inv, scale, st);
+      return;
+    }
+    // three passes: in -> a -> b -> out with a != in, b != a; the last pass may run in place
+    void* a = alias ? static_cast<void*>(scratch_) : out;
+    void* b = alias ? out : static_cast<void*>(scratch_);
+    pass_[0]->run(in, a, rows, p_[0], inv, false, R(1), st);
+    pass_[1]->run(a, b, rows, p_[1], false, false, R(1), st);
+    pass_[2]->run(b, out, rows, p_[2], false, inv, scale, st);
+  }
+
+ private:
+  size_t n_, batch_;
+  SlabShape sh_;
+  Twiddles tws_;
+  std::unique_ptr<slabk::SlabPassExec<R>> pass_[3];
+  slabk::SlabPass p_[3];
+  V2* scratch_ = nullptr;
+};
+
+void fourstep_prefer_transposable(bool on) { g_prefer_transposable = on; }
+
 bool fourstep_covers(const amqft_plan_desc& d) {
   if (d.function != AMQFT_FN_CDFT || (d.order != AMQFT_ORDER_FAST && d.order != AMQFT_ORDER_FAST_DAG)) return false;
   if ((d.n & (d.n - 1)) != 0 || d.n > (size_t(1) << 26)) return false;
   // one fused / small / tile kernel does it (FAST_DAG plans: the whole-DAG kernels only)
   if (fast_sub_covered(d.dtype, d.n, d.variant, d.order != AMQFT_ORDER_FAST_DAG)) return false;
-  return fourstep_shape(d.dtype, d.variant, d.n).ok;
+  return fourstep_slab_shape(d).passes > 0 || fourstep_shape(d.dtype, d.variant, d.n).ok;
 }
 
 OpCount fourstep_op_counts(const amqft_plan_desc& d) {
@@ -712,6 +877,23 @@ OpCount fourstep_op_counts(const amqft_plan_desc& d) {
   // reference DAG of each), plus one complex twiddle multiply per element
   // (4 muls + 2 adds).  Three-factor A x B x C: B C of length A, A C of
   // length B, A B of length C, and two twiddle passes.
+  if (const SlabShape ss = fourstep_slab_shape(d); ss.passes) {
+    // per pass N / L columns of the two-factor length-L schedule (tile_op_counts), one twiddle
+    // multiply per element between passes
+    OpCount c;
+    for (int i = 0; i < ss.passes; ++i) {
+      amqft_plan_desc t = d;
+      t.n = ss.len[i];
+      const OpCount f = tile_op_counts(t);
+      const uint64_t cols = d.n / ss.len[i];
+      c.adds += cols * f.adds;
+      c.muls += cols * f.muls;
+      c.bt += cols * f.bt;
+    }
+    c.adds += static_cast<uint64_t>(ss.passes - 1) * 2 * d.n;
+    c.muls += static_cast<uint64_t>(ss.passes - 1) * 4 * d.n;
+    return c;
+  }
   const FourStepShape sh = fourstep_shape(d.dtype, d.variant, d.n);
   OpCount c;
   if (sh.three) {
@@ -732,6 +914,12 @@ OpCount fourstep_op_counts(const amqft_plan_desc& d) {
 }
 
 amqft_status fourstep_factors(const amqft_plan_desc& d, size_t* f3) {
+  if (const SlabShape ss = fourstep_slab_shape(d); ss.passes) {
+    f3[0] = ss.len[0];
+    f3[1] = ss.passes == 3 ? ss.len[1] : 1;
+    f3[2] = ss.passes == 3 ? ss.len[2] : ss.len[1];
+    return AMQFT_OK;
+  }
   const FourStepShape sh = fourstep_shape(d.dtype, d.variant, d.n);
   if (!sh.ok) return AMQFT_EINVAL;
   f3[0] = sh.n1;
@@ -743,6 +931,11 @@ amqft_status fourstep_factors(const amqft_plan_desc& d, size_t* f3) {
 std::unique_ptr<FastPlan> make_fourstep_plan(const amqft_plan_desc& d, const void* d_trig, uint32_t nmax,
                                              const void* d_trig64) {
   if (!fourstep_covers(d)) return nullptr;
+  if (const SlabShape ss = fourstep_slab_shape(d); ss.passes) {
+    if (d.dtype == AMQFT_F64)
+      return std::make_unique<SlabPlan<double>>(d.variant, d.n, d.batch, d.trig_mode, d_trig, nmax, d.device, ss);
+    return std::make_unique<SlabPlan<float>>(d.variant, d.n, d.batch, d.trig_mode, d_trig, nmax, d.device, ss);
+  }
   if (d.dtype == AMQFT_F64)
     return std::make_unique<FourStepPlan<double>>(d.variant, d.n, d.batch, d.trig_mode, d_trig, nmax, d.device,
                                                    d_trig64);

@@ -18,6 +18,9 @@ std::unique_ptr<FastPlan> make_fast_sub(int variant, size_t n, int dtype, const 
                                         const void* tab64 = nullptr, bool columns = false);
 OpCount fast_sub_op_counts(int variant, size_t n, int dtype, bool columns = false);
 bool fast_sub_covered(int dtype, size_t n, int variant, bool allow_tile = true);
+// Plans created while set (on this thread) skip the column-slab plans, which have no transposed
+// output (amqft_plan_create_transposable).
+void fourstep_prefer_transposable(bool on);
 
 // CDFT, fast order, N up to 2^26 beyond the single-kernel sizes.
 bool fourstep_covers(const amqft_plan_desc& d);

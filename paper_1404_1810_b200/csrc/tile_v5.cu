@@ -1,5 +1,6 @@
-// tile_v5.cu -- in-shared-memory four-step instances for AM-QFT variant 5.
+// tile_v5.cu -- in-shared-memory four-step and column-slab instances for AM-QFT variant 5.
 #include "gen/small_gen_v5.cuh"
+#include "slab_kernel.cuh"
 #include "tile_kernel.cuh"
 
 namespace amqft_b200 {
@@ -7,4 +8,8 @@ namespace tilek {
 template std::unique_ptr<FastPlan> make_tile<5, float>(size_t, const void*, uint32_t, int);
 template std::unique_ptr<FastPlan> make_tile<5, double>(size_t, const void*, uint32_t, int);
 }  // namespace tilek
+namespace slabk {
+template std::unique_ptr<SlabPassExec<float>> make_slab_pass<5, float>(size_t, const void*, uint32_t, int);
+template std::unique_ptr<SlabPassExec<double>> make_slab_pass<5, double>(size_t, const void*, uint32_t, int);
+}  // namespace slabk
 }  // namespace amqft_b200

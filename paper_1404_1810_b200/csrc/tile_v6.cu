@@ -1,5 +1,6 @@
-// tile_v6.cu -- in-shared-memory four-step instances for AM-QFT variant 6.
+// tile_v6.cu -- in-shared-memory four-step and column-slab instances for AM-QFT variant 6.
 #include "gen/small_gen_v6.cuh"
+#include "slab_kernel.cuh"
 #include "tile_kernel.cuh"
 
 namespace amqft_b200 {
@@ -7,4 +8,8 @@ namespace tilek {
 template std::unique_ptr<FastPlan> make_tile<6, float>(size_t, const void*, uint32_t, int);
 template std::unique_ptr<FastPlan> make_tile<6, double>(size_t, const void*, uint32_t, int);
 }  // namespace tilek
+namespace slabk {
+template std::unique_ptr<SlabPassExec<float>> make_slab_pass<6, float>(size_t, const void*, uint32_t, int);
+template std::unique_ptr<SlabPassExec<double>> make_slab_pass<6, double>(size_t, const void*, uint32_t, int);
+}  // namespace slabk
 }  // namespace amqft_b200

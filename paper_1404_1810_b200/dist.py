@@ -111,7 +111,7 @@ class CudaLocalOps:
         self.trig_mode = int(trig_mode)
         # the local sub-plans use the same twiddle set (a four-step's own twiddles)
         self.p1 = Plan(variant, FunctionId.Cdft, n1, n2 // world, dtype="f32", order=Order.Fast,
-                       device=device, trig_mode=trig_mode)
+                       device=device, trig_mode=trig_mode, transposable=True)
         self.p2 = Plan(variant, FunctionId.Cdft, n2, n1 // world, dtype="f32", order=Order.Fast,
                        device=device, trig_mode=trig_mode)
 
