@@ -479,9 +479,12 @@ def bench_single(args, world, rank, local):
         path, launches = plan.path()
         fa, fb, fc = plan.fourstep_factors()
         shape = f"three-factor {fa} x {fb} x {fc}" if fb > 1 else f"two-factor {fa} x {fc}"
-        workload = (f"config 4: one complex forward DFT N=2^24 fp32, four-step {shape} "
-                    f"(column passes + fused-kernel rows + one transpose), on-the-fly twiddles, "
-                    f"variant {args.variant}")
+        # one launch per factor: the column-slab plan (no transposes); else column passes + rows + transpose
+        slab = launches == (3 if fb > 1 else 2)
+        kind = ("column-slab passes, natural order in and out, no transpose" if slab
+                else "column passes + tile-kernel rows + one transpose")
+        workload = (f"config 4: one complex forward DFT N=2^24 fp32, four-step {shape} ({kind}), "
+                    f"on-the-fly twiddles, variant {args.variant}")
         per_gpu_bytes = 16 * n
         value = world / (ms / 1000.0)
         hx = torch.empty(1, 2 * n, pin_memory=True)
