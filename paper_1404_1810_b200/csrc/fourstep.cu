@@ -750,13 +750,13 @@ SlabShape fourstep_slab_shape(const amqft_plan_desc& d) {
   t.order = AMQFT_ORDER_FAST;
   if (tile_covers(t)) return none;
   // measured (B200, v4, GB/s on algorithmic bytes, slab against column + tile rows + transpose;
-  // tools/slab_ab.sh): fp32 two passes 2^17-2^20 2583 / 2484 / 2180 / 2021 against 2083 / 2077 / 1970 /
-  // 1893; three passes 2^24-2^26 1667 / 1522 / 1640 against 1453 / 1396 / 1356, but 2^21-2^23 1276 / 1363 /
-  // 1468 against 1664 / 1492 / 1518 (128-point slab factors against a one-pass 2^15 / 2^16 tile row).
-  // fp64: 2^16 2804 against 2156, 2^19 / 2^20 1813 / 1890 against 1759 / 1565, 2^22-2^24 1649 / 1796 /
-  // 1837 against 1516 / 1500 / 1366; 2^17 / 2^18 / 2^21 lose (1936 / 1608 / 1521 against 2023 / 1982 / 1589).
-  if (d.dtype == AMQFT_F64) return (lg == 16 || lg == 19 || lg == 20 || lg >= 22) ? s : none;
-  return ((lg >= 17 && lg <= 20) || lg >= 24) ? s : none;
+  // tools/slab_ab.sh): fp32 two passes 2^17-2^20 2553 / 2467 / 2178 / 2016 against 2083 / 2077 / 1970 /
+  // 1893; three passes 2^22-2^26 1591 / 1604 / 1676 / 1522 / 1640 against 1504 / 1518 / 1453 / 1396 /
+  // 1356; 2^21 (128 x 128 x 128) 1534 against 1656 (a 32-column pass and a one-pass 2^16 tile row).
+  // fp64: 2^16 2804 against 2156, 2^19 / 2^20 1813 / 1890 against 1759 / 1565, 2^21-2^24 1603 / 1676 /
+  // 1770 / 1837 against 1587 / 1512 / 1493 / 1366; 2^17 / 2^18 lose (1936 / 1608 against 2023 / 1982).
+  if (d.dtype == AMQFT_F64) return (lg == 16 || lg == 19 || lg >= 20) ? s : none;
+  return ((lg >= 17 && lg <= 20) || lg >= 22) ? s : none;
 }
 
 template <typename R>

@@ -43,6 +43,10 @@ using tilek::RT;
 
 template <typename R, int LGA, int LGB, int W_, int T_ = 256>
 struct SCfg {
+  // L2 prefetch of the CTA's next slab: measured (B200, fp32, GB/s) +21 / +16 / +7 % on 2^21 / 2^22 /
+  // 2^23, whose plans have 128-point passes (8 loads in flight per thread), and -7 .. -10 % on the
+  // 256- to 1024-point passes (2^17 .. 2^20, 2^24), so only the 128-point instances issue it
+  static constexpr bool PF = LGA + LGB == 7;
   using V2 = typename RT<R>::V2;
   static constexpr int NA = 1 << LGA, NB = 1 << LGB, L = NA * NB, W = W_, T = T_;
   static constexpr int KP = NB * W + 1;                     // ka pitch: odd, lanes on ka hit distinct banks
@@ -149,6 +153,15 @@ k_slab(const R* __restrict__ in, R* __restrict__ out, size_t rows, const __grid_
     const size_t g = s / per_row;
     const unsigned c0 = static_cast<unsigned>(s - g * per_row) * W;
     const V2* x = reinterpret_cast<const V2*>(in) + g * p.in_row + (c0 / p.qin) * p.qi + c0 % p.qin;
+    // the CTA's next slab on its way into L2: one bulk prefetch per row of the slab (W contiguous values)
+    if (C::PF && s + gridDim.x < slabs) {
+      const size_t s2 = s + gridDim.x, g2 = s2 / per_row;
+      const unsigned n0 = static_cast<unsigned>(s2 - g2 * per_row) * W;
+      const V2* nx = reinterpret_cast<const V2*>(in) + g2 * p.in_row + (n0 / p.qin) * p.qi + n0 % p.qin;
+      for (int j = tid; j < C::L; j += C::T)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                     ::"l"(nx + j * p.sj_in), "n"(W * static_cast<int>(sizeof(V2))) : "memory");
+    }
     // ---- phase A
 #pragma unroll 1
     for (int i = tid; i < W * NB; i += C::T) {
