@@ -227,9 +227,9 @@ def ncu_traffic(args, n, path=2):
     if args.dtype != "f32" or args.order != "fast":
         return None, None
     if path == 6:
-        # k_tile<V, INV, TCfg<LG1, LG2, ...>>: N1 x N2 = 64 x 64 at N = 4096 (tile_kernel.cuh make_tile)
+        # k_tile<V, R, INV, TCfg<R, LG1, LG2, ...>>: N1 x N2 = 64 x 64 at N = 4096 (tile_kernel.cuh make_tile)
         lg1 = 6 if logn == 11 else logn // 2
-        want = (f"k_tile<{args.variant},false,TCfg<{lg1},{logn - lg1},", f"k_tile<{args.variant},0,TCfg<{lg1},{logn - lg1},")
+        want = tuple(f"k_tile<{args.variant},float,{b},TCfg<float,{lg1},{logn - lg1}," for b in ("false", "0"))
         pattern = "r*_ncu_k_tile_*.json"
     else:
         # k_fast<V, R, LOGN, LOGLB, MODE[, IO, P]>: the one-CTA-per-row fp32 instance
