@@ -167,7 +167,7 @@ k_slab(const R* __restrict__ in, R* __restrict__ out, size_t rows, const __grid_
     for (int i = tid; i < W * NB; i += C::T) {
       const int w = i % W, jb = i / W;
       AIo<R, NB, W, C::KP, INV_IN> io{x + w + jb * p.sj_in, NB * p.sj_in, P + jb * W + w, twl + jb};
-      GA::template run<Arith<R>>(io, ta.v);
+      GA::template run<tilek::TArith<R>>(io, ta.v);
     }
     __syncthreads();
     // ---- phase B
@@ -191,7 +191,7 @@ k_slab(const R* __restrict__ in, R* __restrict__ out, size_t rows, const __grid_
         smallk::twiddle_d(io.col * static_cast<unsigned long long>(ka), p.tw, io.cr, io.ci);
         smallk::twiddle_d(io.col * static_cast<unsigned long long>(NA), p.tw, io.sr, io.si);
       }
-      GB::template run<Arith<R>>(io, tb.v);
+      GB::template run<tilek::TArith<R>>(io, tb.v);
     }
     __syncthreads();   // P is rewritten by the next slab's phase A
   }

@@ -71,6 +71,17 @@ template <> struct RT<double> {
 template <typename R> __device__ __forceinline__ typename RT<R>::V2 mk2(R a, R b);
 template <> __device__ __forceinline__ float2 mk2<float>(float a, float b) { return make_float2(a, b); }
 template <> __device__ __forceinline__ double2 mk2<double>(double a, double b) { return make_double2(a, b); }
+// Arithmetic of the factors.  The split paths are held to the tolerance, not
+// to bitwise equality with the reference, so the operators are plain ones
+// that nvcc may contract into FMAs where a constant multiply feeds an add /
+// subtract (one rounding less, one instruction less; config 2: 0.765 ->
+// 0.744 ms).
+template <typename R> struct TArith {
+  static __device__ __forceinline__ R add(R a, R b) { return a + b; }
+  static __device__ __forceinline__ R sub(R a, R b) { return a - b; }
+  static __device__ __forceinline__ R mul(R a, R b) { return a * b; }
+};
+
 // a * w (complex)
 template <typename R, typename V2>
 __device__ __forceinline__ void cmul(R& a, R& b, const V2 w) {
@@ -198,7 +209,7 @@ k_tile(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       if (row0 + r < rows) {
         AIo<R, N2, C::PITCH, INV> io{reinterpret_cast<const V2*>(in) + (row0 + r) * N + n2, P + r * C::ROWP + n2,
                                      tw + n2};
-        G1::template run<Arith<R>>(io, t1.v);
+        G1::template run<TArith<R>>(io, t1.v);
       }
     }
     __syncthreads();
@@ -208,7 +219,7 @@ k_tile(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       const int r = j / N1, k1 = j % N1;
       if (row0 + r < rows) {
         BIo<R, N1, INV> io{P + r * C::ROWP + k1 * C::PITCH, reinterpret_cast<V2*>(out) + (row0 + r) * N + k1, scale};
-        G2::template run<Arith<R>>(io, t2.v);
+        G2::template run<TArith<R>>(io, t2.v);
       }
     }
     __syncthreads();   // P is rewritten by the next tile's phase A
@@ -298,9 +309,9 @@ class TilePlanImpl final : public FastPlan {
 // (st.shared::cluster), the only exchange: (P-1)/P of the row.  Phases B and
 // C run on the CTA's own planes.  Two cluster barriers per row: a full one
 // after phase A (all planes complete), and a split one around the rest --
-// arrive after the CTA's phase C, wait just before its first remote store
-// of the next row -- so the next row's loads and arithmetic overlap the
-// peers' phase C.
+// a relaxed arrive after the CTA's phase C, the wait just before its first
+// remote store of the next row -- so the next row's loads and arithmetic
+// overlap the peers' phase C.
 template <typename R, int LG1, int LG2, int LG3, int T_, int MB_, int P_ = 1>
 struct T3Cfg {
   using V2 = typename RT<R>::V2;
@@ -321,6 +332,14 @@ __device__ __forceinline__ uint32_t tk_u32(const void* p) {
 }
 __device__ __forceinline__ void tk_cluster_arrive() {
   asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+// no fence: orders execution only ("this CTA has finished READING its planes"; the loads' values
+// have been consumed).  The releasing form also waits for the thread's outstanding global stores
+// of phase C -- ncu showed membar as the second stall of the 2^15 kernel (2.0 per issue): 3712 ->
+// 3843 GB/s.  (Asynchronous DSMEM stores completing on the owner's mbarrier instead of the full
+// barrier after phase A: correct, but slower -- 3384 GB/s at 2^15, fp64 2^14 3467 against 4112.)
+__device__ __forceinline__ void tk_cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void tk_cluster_wait() {
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -469,7 +488,7 @@ k_tile3(const R* __restrict__ in, R* __restrict__ out, size_t rows,
 #pragma unroll 1
       for (int m = tid; m < M; m += C::T) {
         A3Io<R, M, C::PM, INV> io{x + m, Y + (m / N3) * C::P3 + m % N3, tw1 + m};
-        G1::template run<Arith<R>>(io, t1.v);
+        G1::template run<TArith<R>>(io, t1.v);
       }
       __syncthreads();
     } else {
@@ -483,7 +502,7 @@ k_tile3(const R* __restrict__ in, R* __restrict__ out, size_t rows,
 #pragma unroll
         for (int k = 0; k < P; ++k) io.yb[k] = ywin[k] + off;
         io.wait = mm == tid && row != r_first;   // first item of a row after the first
-        G1::template run<Arith<R>>(io, t1.v);
+        G1::template run<TArith<R>>(io, t1.v);
       }
       tk_cluster_arrive();   // all planes complete and visible
       tk_cluster_wait();
@@ -492,7 +511,7 @@ k_tile3(const R* __restrict__ in, R* __restrict__ out, size_t rows,
     for (int j = tid; j < K1 * N3; j += C::T) {
       const int n3 = j % N3, k1 = j / N3;
       B3Io<R, N3, C::P3> io{Y + k1 * C::PM + n3, tw2 + n3};
-      G2::template run<Arith<R>>(io, t2.v);
+      G2::template run<TArith<R>>(io, t2.v);
     }
     __syncthreads();
 #pragma unroll 1
@@ -500,10 +519,10 @@ k_tile3(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       const int k1 = j % K1, k2 = j / K1;
       BIo<R, N1 * N2, INV> io{Y + k1 * C::PM + k2 * C::P3,
                               reinterpret_cast<V2*>(out) + row * N + (q * K1 + k1) + N1 * k2, scale};
-      G3::template run<Arith<R>>(io, t3.v);
+      G3::template run<TArith<R>>(io, t3.v);
     }
     if constexpr (P == 1) __syncthreads();   // Y is rewritten by the next row's phase A
-    else tk_cluster_arrive();                 // ... by the peers': the wait is in their first store
+    else tk_cluster_arrive_relaxed();         // ... by the peers': the wait is in their first store
   }
   if constexpr (P > 1) {
     // balance the last arrive; no CTA exits while a peer may still store into it
