@@ -529,9 +529,13 @@ def bench_single(args, world, rank, local):
         # folded into the scatter when it runs transposed), the twiddle-scatter,
         # the transpose, the length-n2 plan
         l1 = d.ops.p1.path()[1] - (1 if d.ops.a_t else 0)
-        path, launches = 3, l1 + 2 + d.ops.p2.path()[1]
+        # one GPU: no exchange to make, the scatter writes each value to its final place (scatter +
+        # transpose in one kernel: DistFourStep.forward's direct mode); several: scatter, all-to-all, transpose
+        direct = world == 1 and d.ops.direct_ok(d.rows1)
+        path, launches = 3, l1 + (1 if direct else 2) + d.ops.p2.path()[1]
+        exch = "direct twiddle-scatter into the row buffer (no exchange on one GPU)" if direct else "one all-to-all"
         workload = (f"config 5: one complex forward DFT N=2^30 fp32 over {world} GPU(s), distributed four-step "
-                    f"n1=2^{d.n1.bit_length() - 1} x n2=2^{d.n2.bit_length() - 1}, one all-to-all, on-the-fly twiddles, "
+                    f"n1=2^{d.n1.bit_length() - 1} x n2=2^{d.n2.bit_length() - 1}, {exch}, on-the-fly twiddles, "
                     f"variant {args.variant}")
         per_gpu_bytes = 16 * n // world
         value = 1.0 / (ms / 1000.0)

@@ -198,6 +198,17 @@ amqft_status amqft_dist_twiddle_scatter(const void* d_rows, void* const* d_dst, 
  * amqft_dist_twiddle_scatter_t is amqft_dist_twiddle_scatter for rows in
  * that order (A and n1/A multiples of 32, n1/nparts a multiple of 32).
  * Replaces nothing in the reference (it has no distributed path). */
+/* The scatter and the exchange-side transpose in one kernel: element
+ * (n2, k1) of the local rows goes straight to its place in the destination
+ * rank's [n1 / nparts][n / n1] rows -- d_dst[q] is rank q's row buffer, mapped
+ * into this process (CUDA IPC / a registered window), or the rank's own with
+ * one part -- times w_N^(n2 k1); the length-n2 plan then runs on those rows
+ * with no transpose in between.  a: the local plan's transposed factor (rows
+ * in amqft_exec_rows_transposed order), or 0 for plain rows; rows and
+ * n1 / max(a, 1) multiples of 32.  Config 5 on one B200: one pass less. */
+amqft_status amqft_dist_twiddle_scatter_direct(const void* d_rows, void* const* d_dst, size_t rows, size_t n1,
+                                               size_t n, size_t row0, int nparts, int trig_mode, size_t a,
+                                               void* stream);
 amqft_status amqft_plan_transposed_factor(amqft_plan plan, size_t* a);
 /* amqft_plan_create for a caller that will use amqft_exec_rows_transposed:
  * among the four-step plans it prefers the column-mode one that has a

@@ -71,6 +71,7 @@ def lib() -> C.CDLL:
     L.amqft_transpose_c64.argtypes = [vp, vp, sz, sz, sz, vp]
     L.amqft_plan_transposed_factor.argtypes = [vp, C.POINTER(sz)]
     L.amqft_exec_rows_transposed.argtypes = [vp, vp, vp, sz, vp]
+    L.amqft_dist_twiddle_scatter_direct.argtypes = [vp, C.POINTER(vp), sz, sz, sz, sz, C.c_int, C.c_int, sz, vp]
     L.amqft_dist_twiddle_scatter_t.argtypes = [vp, C.POINTER(vp), sz, sz, sz, sz, C.c_int, C.c_int, C.c_int, sz,
                                                vp]
     L.amqft_execute_host.argtypes = [C.c_int, C.c_int, sz, vp, vp, C.c_int, sz, C.c_int, vp]
@@ -93,7 +94,7 @@ def lib() -> C.CDLL:
     L.amqft_device_synchronize.argtypes = [C.c_int]
     L.amqft_last_error.restype = C.c_char_p
     L.amqft_version.restype = C.c_char_p
-    for name in ("amqft_plan_create", "amqft_plan_create_transposable", "amqft_plan_destroy", "amqft_exec_forward",
+    for name in ("amqft_plan_create", "amqft_plan_create_transposable", "amqft_dist_twiddle_scatter_direct", "amqft_plan_destroy", "amqft_exec_forward",
                  "amqft_exec_inverse", "amqft_exec_rows", "amqft_exec_host_rows", "amqft_execute_host",
                  "amqft_execute_host_constants", "amqft_execute_host_inverse", "amqft_plan_create_with_constants",
                  "amqft_direct_bins", "amqft_direct_bins_extended", "amqft_dist_unique_id",

@@ -222,6 +222,15 @@ amqft_status amqft_dist_exec_forward(amqft_dist_plan P, void* d_in, void* d_out,
       ack(amqft_exec_rows_transposed(P->p1, d_in, d_in, P->rows1, stream));
     else
       ack(amqft_exec_rows(P->p1, d_in, d_in, P->rows1, 0, stream));
+    // one rank, no communicator: no exchange to make -- the scatter writes each value to its final
+    // place in the row buffer (scatter + transpose in one kernel), then the length-n2 transforms
+    const size_t a1 = P->a_t ? P->a_t : 1;
+    if (!P->comm && parts == 1 && P->rows1 % 32 == 0 && (P->n1 / a1) % 32 == 0 && P->rows1 / 32 <= 65535) {
+      void* rows[1] = {P->b};
+      ack(amqft_dist_twiddle_scatter_direct(d_in, rows, P->rows1, P->n1, P->n, 0, 1, P->trig, P->a_t, stream));
+      ack(amqft_exec_rows(P->p2, P->b, d_out, P->w, 0, stream));
+      return AMQFT_OK;
+    }
     // 2. twiddle + scatter by k1-slab: into the send slots, or with no
     //    communicator straight into the receive slots
     void* dst = P->comm ? P->send : P->recv;

@@ -661,6 +661,21 @@ amqft_status amqft_dist_twiddle_scatter(const void* d_rows, void* const* d_dst, 
   return AMQFT_OK;
 }
 
+amqft_status amqft_dist_twiddle_scatter_direct(const void* d_rows, void* const* d_dst, size_t rows, size_t n1,
+                                               size_t n, size_t row0, int nparts, int trig_mode, size_t a,
+                                               void* stream) {
+  if (!d_rows || !d_dst) return set_err(AMQFT_EINVAL, "null pointer");
+  if (n == 0 || (n & (n - 1)) || n1 == 0 || (n1 & (n1 - 1)) || n % n1 || n > (size_t(1) << 40))
+    return set_err(AMQFT_EINVAL, "n and n1 must be powers of two with n1 | n");
+  try {
+    dist_twiddle_scatter_direct(d_rows, d_dst, rows, n1, n, row0, nparts, trig_mode, a,
+                                static_cast<cudaStream_t>(stream));
+  } catch (...) {
+    return from_exception();
+  }
+  return AMQFT_OK;
+}
+
 amqft_status amqft_plan_transposed_factor(amqft_plan P, size_t* a) {
   if (!P || !a) return set_err(AMQFT_EINVAL, "null argument");
   *a = (P->path == 3 && P->fast) ? P->fast->transposed_factor() : 0;

@@ -329,6 +329,49 @@ __global__ void __launch_bounds__(256) k_twiddle_scatter_t(const float2* __restr
   }
 }
 
+// The scatter and the exchange-side transpose in one kernel ("direct" mode):
+// element (n2, k1) of the local rows goes straight to its place in the
+// destination rank's [n1 / parts][n2_total] rows, dst[k1 / w][(k1 % w)
+// n2_total + n2], times w_N^(n2 k1) -- into the peers' mapped buffers, or the
+// rank's own when there is one part.  The rows come in the column-mode
+// four-step's transposed order in[r][ka][kb], k1 = ka + A kb (A = 1: plain
+// rows).  32 x 32 tiles (r, kb) for a fixed ka: reads coalesced along kb,
+// writes along n2; per thread 4 elements kb + 8 j share one twiddle
+// evaluation and a recurrence (step w^(8 A n2)).
+__global__ void __launch_bounds__(256) k_twiddle_scatter_direct(const float2* __restrict__ in, const DstPtrs dst,
+                                                                int n1, int A, int logn, long long row0,
+                                                                long long n2_total, int nparts,
+                                                                const double2* __restrict__ twh,
+                                                                const double2* __restrict__ twl, int logb,
+                                                                int onthefly) {
+  __shared__ float2 tile[32][33];
+  const int B = n1 / A, w = n1 / nparts;
+  const int ka = blockIdx.z;
+  const int kb0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
+#pragma unroll
+  for (int j = 0; j < 32; j += 8)
+    tile[ty + j][tx] = in[static_cast<long long>(r0 + ty + j) * n1 + static_cast<long long>(ka) * B + kb0 + tx];
+  __syncthreads();
+  const unsigned long long n2 = static_cast<unsigned long long>(row0 + r0 + tx);
+  double cr, ci, sr, si;
+  scatter_tw(n2 * static_cast<unsigned long long>(ka + A * (kb0 + ty)), logn, twh, twl, logb, onthefly, cr, ci);
+  scatter_tw(n2 * static_cast<unsigned long long>(8 * A), logn, twh, twl, logb, onthefly, sr, si);
+#pragma unroll
+  for (int j = 0; j < 32; j += 8) {
+    const int kb = kb0 + ty + j;
+    const float2 v = tile[tx][ty + j];
+    const float fr = static_cast<float>(cr), fi = static_cast<float>(ci);
+    const int k1 = ka + A * kb;
+    const int q = k1 / w, kl = k1 - q * w;
+    dst.p[q][static_cast<long long>(kl) * n2_total + static_cast<long long>(n2)] =
+        make_float2(v.x * fr - v.y * fi, v.x * fi + v.y * fr);
+    const double t0 = cr * sr - ci * si, t1 = cr * si + ci * sr;
+    cr = t0;
+    ci = t1;
+  }
+}
+
 int lg2(size_t v) {
   int l = 0;
   while ((size_t(1) << l) < v) ++l;
@@ -694,6 +737,32 @@ void dist_twiddle_scatter_t(const void* in, void* const* d_dst, size_t rows, siz
                                                      tw->logb, trig_mode == AMQFT_TRIG_ONTHEFLY ? 1 : 0);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("k_twiddle_scatter_t: ") + cudaGetErrorString(e));
+}
+
+void dist_twiddle_scatter_direct(const void* in, void* const* d_dst, size_t rows, size_t n1, size_t n, size_t row0,
+                                 int nparts, int trig_mode, size_t a, cudaStream_t st) {
+  static thread_local std::unique_ptr<Twiddles> tw;
+  static thread_local int tw_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!tw || (size_t(1) << tw->logn) != n || tw_dev != dev) {
+    tw.reset(new Twiddles(n));
+    tw_dev = dev;
+  }
+  if (a == 0) a = 1;   // plain rows
+  if (nparts < 1 || nparts > kMaxParts || n1 % nparts)
+    throw std::invalid_argument("twiddle_scatter_direct: n1 must divide over the parts");
+  if (n1 % a || (n1 / a) % 32 || rows % 32 || a > 65535 || rows / 32 > 65535)
+    throw std::invalid_argument("twiddle_scatter_direct: n1 / A and rows must be multiples of 32");
+  DstPtrs dp{};
+  for (int q = 0; q < nparts; ++q) dp.p[q] = static_cast<float2*>(d_dst[q]);
+  const dim3 grid(static_cast<unsigned>(n1 / a / 32), static_cast<unsigned>(rows / 32), static_cast<unsigned>(a));
+  k_twiddle_scatter_direct<<<grid, dim3(32, 8), 0, st>>>(static_cast<const float2*>(in), dp, static_cast<int>(n1),
+                                                          static_cast<int>(a), tw->logn, static_cast<long long>(row0),
+                                                          static_cast<long long>(n / n1), nparts, tw->hi, tw->lo,
+                                                          tw->logb, trig_mode == AMQFT_TRIG_ONTHEFLY ? 1 : 0);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string("k_twiddle_scatter_direct: ") + cudaGetErrorString(e));
 }
 
 void transpose_c64(const void* in, void* out, size_t mats, size_t r, size_t c, cudaStream_t st) {

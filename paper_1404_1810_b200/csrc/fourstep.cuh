@@ -36,6 +36,8 @@ amqft_status fourstep_factors(const amqft_plan_desc& d, size_t* f3);
 void dist_twiddle_scatter(const void* in, void* const* d_dst, size_t rows, size_t n1, size_t n, size_t row0,
                           int src, int nparts, int trig_mode, cudaStream_t st);
 void transpose_c64(const void* in, void* out, size_t mats, size_t r, size_t c, cudaStream_t st);
+void dist_twiddle_scatter_direct(const void* in, void* const* d_dst, size_t rows, size_t n1, size_t n, size_t row0,
+                                 int nparts, int trig_mode, size_t a, cudaStream_t st);
 void dist_twiddle_scatter_t(const void* in, void* const* d_dst, size_t rows, size_t n1, size_t n, size_t row0,
                             int src, int nparts, int trig_mode, size_t a, cudaStream_t st);
 

@@ -139,6 +139,18 @@ class CudaLocalOps:
             check(lib().amqft_dist_twiddle_scatter(int(a.data_ptr()), arr, rows, self.n1, self.n, row0, src,
                                                    nparts, self.trig_mode, Plan._stream(stream)))
 
+    def direct_ok(self, rows):
+        """The direct scatter's tiling: 32 x 32 tiles over (rows, kb)."""
+        a = self.a_t or 1
+        return rows % 32 == 0 and (self.n1 // a) % 32 == 0 and rows // 32 <= 65535
+
+    def twiddle_scatter_direct(self, a, dst_ptrs, rows, row0, nparts, stream=None):
+        """Scatter + exchange-side transpose in one kernel: straight into the
+        destination ranks' [n1/P][n2] row buffers (amqft_dist_twiddle_scatter_direct)."""
+        arr = (C.c_void_p * nparts)(*[int(p) for p in dst_ptrs])
+        check(lib().amqft_dist_twiddle_scatter_direct(int(a.data_ptr()), arr, rows, self.n1, self.n, row0, nparts,
+                                                      self.trig_mode, self.a_t, Plan._stream(stream)))
+
     def transpose(self, inp, out, r, c, stream=None):
         check(lib().amqft_transpose_c64(int(inp.data_ptr()), int(out.data_ptr()), 1, r, c,
                                         Plan._stream(stream)))
@@ -228,11 +240,33 @@ class DistFourStep:
         self.ops.dft_rows2(b, z, stream)
         return z
 
-    def forward(self, a, bufs=None, peer_recv=None, stream=None):
+    def forward(self, a, bufs=None, peer_recv=None, stream=None, peer_rows=None):
         """a: this rank's [n2/P][2 n1] slab (overwritten).  Returns z, this
-        rank's [n1/P][2 n2] output slab."""
+        rank's [n1/P][2 n2] output slab.
+
+        peer_rows: every rank's `b` row buffer ([n1/P][2 n2], bufs[2]) mapped
+        into this process: the scatter writes each value straight to its
+        final place there (scatter + exchange + transpose in one kernel, the
+        "direct" mode).  With one rank the mode is the default: the rank's own
+        buffer, no exchange to make."""
         send, recv, b, z = bufs if bufs is not None else self.buffers(a)
         multi = self.world > 1 and dist.is_initialized()
+        direct = getattr(self.ops, "direct_ok", None)
+        if peer_rows is None and self.world == 1 and peer_recv is None and direct and direct(self.rows1):
+            peer_rows = [b.data_ptr()]
+        if peer_rows is not None:
+            if multi:   # write-after-read on the peers' row buffers
+                if a.is_cuda:
+                    torch.cuda.synchronize(a.device)
+                dist.barrier(group=self.group)
+            self.ops.dft_rows1(a, stream)
+            self.ops.twiddle_scatter_direct(a, peer_rows, self.rows1, self.rank * self.rows1, self.world, stream)
+            if multi:   # the stores were the exchange: order them before the peers read
+                if a.is_cuda:
+                    torch.cuda.synchronize(a.device)
+                dist.barrier(group=self.group)
+            self.ops.dft_rows2(b, z, stream)
+            return z
         if peer_recv is not None and multi:
             # write-after-read: no rank may scatter into a peer's receive
             # buffer while that peer still transposes the previous call's data

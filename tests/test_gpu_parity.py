@@ -346,6 +346,16 @@ def _dist_run_sim(n, world, mode, x):
     xt = torch.tensor(x)
     slabs = [r.local_input(xt).to(DEV) for r in ranks]
     bufs = [r.buffers(slabs[0]) for r in ranks]
+    if mode == "direct":
+        # scatter + exchange + transpose in one kernel: straight into every rank's row buffer
+        rows = [int(b[2].data_ptr()) for b in bufs]
+        for r, a in zip(ranks, slabs):
+            r.ops.dft_rows1(a)
+            r.ops.twiddle_scatter_direct(a, rows, r.rows1, r.rank * r.rows1, world)
+        torch.cuda.synchronize()
+        outs = [r.ops.dft_rows2(b[2], b[3]) or b[3] for r, b in zip(ranks, bufs)]
+        torch.cuda.synchronize()
+        return ranks[0].global_output([o.cpu().numpy() for o in outs])
     if mode == "peer":
         peer = [int(b[1].data_ptr()) for b in bufs]
         for r, a, b in zip(ranks, slabs, bufs):
@@ -373,9 +383,16 @@ def test_distributed_fourstep_single_gpu_simulation(oracle, restatement):
     want = r.execute(4, O.F_CDFT, n, x.astype(np.float64))
     assert r.rel_l2(base.astype(np.float64), want) <= 1e-5 * 20
     for world in (2, 4):
-        for mode in ("a2a", "peer"):
+        for mode in ("a2a", "peer", "direct"):
             got = _dist_run_sim(n, world, mode, x)
             assert got.tobytes() == base.tobytes(), (world, mode)
+    # world 1 through forward(): the direct mode is the default (no exchange to make)
+    from paper_1404_1810_b200.dist import DistFourStep
+    d = DistFourStep(4, n, world=1, rank=0, device=0)
+    a = d.local_input(torch.tensor(x)).to(DEV)
+    z = d.forward(a)
+    torch.cuda.synchronize()
+    assert d.global_output([z.cpu().numpy()]).tobytes() == base.tobytes()
 
 
 def test_distributed_fourstep_world1_process_group():
