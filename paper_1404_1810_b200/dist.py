@@ -221,6 +221,22 @@ class DistFourStep:
         z = like.new_empty((self.w, 2 * self.n2))
         return send, recv, b, z
 
+    def map_peer_rows(self, b):
+        """Every rank's `b` row buffer (bufs[2]) mapped into this process: the
+        `peer_rows` list of forward()'s direct mode.  The buffers travel as
+        CUDA IPC handles (torch's shared-storage reduction, cudaIpcGetMemHandle
+        / cudaIpcOpenMemHandle underneath) over the process group, so the ranks
+        may be separate processes -- on NVLink-connected GPUs of one node, or
+        on one GPU.  Collective; the mapped tensors are kept alive on self."""
+        from torch.multiprocessing.reductions import reduce_tensor
+        if self.world == 1 or not dist.is_initialized():
+            self._peer_row_tensors = [b]
+            return [b.data_ptr()]
+        handles = [None] * self.world
+        dist.all_gather_object(handles, reduce_tensor(b), group=self.group)
+        self._peer_row_tensors = [b if q == self.rank else fn(*args) for q, (fn, args) in enumerate(handles)]
+        return [t.data_ptr() for t in self._peer_row_tensors]
+
     def stage1(self, a, send, peer_recv=None, stream=None):
         """Length-n1 transforms of the local rows, then twiddle + scatter by
         k1-slab into the send slots, or into the peers' receive buffers."""

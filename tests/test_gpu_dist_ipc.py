@@ -1,0 +1,27 @@
+"""The distributed four-step's direct mode ACROSS PROCESSES: two ranks, two
+processes, peer row buffers mapped with CUDA IPC (DistFourStep.map_peer_rows)
+-- the scatter kernel of each process stores straight into the other
+process's buffer.  Both processes share the one GPU of the test box (IPC works
+between processes on one device); they synchronise on the host only."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def test_direct_mode_between_two_processes(tmp_path):
+    out = str(tmp_path / "err.npy")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29731",
+           os.path.join(HERE, "dist_ipc_worker.py"), out, "20"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    err = float(np.load(out)[0])
+    assert err <= 1e-5 * 20, err
