@@ -782,11 +782,15 @@ struct SlabShape {
 
 // Balanced factors, the largest first.  Two passes for 2^14 .. 2^20, three
 // for 2^21 .. 2^30.
-SlabShape slab_factors(size_t n) {
+SlabShape slab_factors(size_t n, int dtype) {
   SlabShape s;
   const int lg = lg2(n);
   if ((size_t(1) << lg) != n) return s;
-  if (lg >= 14 && lg <= 20) {
+  // fp32 has 2048- and 4096-point slab passes (64-point factors, 8- / 4-column slabs): two passes
+  // for 2^21 .. 2^23 (measured 1875 / 1745 / 1717 GB/s against 1686 / 1603 / 1614 for the best
+  // alternative; 2^24 as 4096 x 4096 loses to three 256-point passes, 1492 against 1694)
+  const bool two_long = dtype == AMQFT_F32 && lg >= 21 && lg <= 23;
+  if ((lg >= 14 && lg <= 20) || two_long) {
     s.passes = 2;
     s.len[0] = size_t(1) << ((lg + 1) / 2);
     s.len[1] = size_t(1) << (lg / 2);
@@ -807,7 +811,7 @@ thread_local bool g_prefer_transposable = false;
 SlabShape fourstep_slab_shape(const amqft_plan_desc& d) {
   SlabShape none;
   if (d.function != AMQFT_FN_CDFT || g_prefer_transposable) return none;
-  const SlabShape s = slab_factors(d.n);
+  const SlabShape s = slab_factors(d.n, d.dtype);
   if (!s.passes) return none;
   if (const char* e = std::getenv("AMQFT_AB_SLAB")) {
     if (e[0] == 'n') return none;
@@ -820,12 +824,12 @@ SlabShape fourstep_slab_shape(const amqft_plan_desc& d) {
   if (tile_covers(t)) return none;
   // measured (B200, v4, GB/s on algorithmic bytes, slab against column + tile rows + transpose;
   // tools/slab_ab.sh): fp32 two passes 2^17-2^20 2553 / 2467 / 2178 / 2016 against 2083 / 2077 / 1970 /
-  // 1893; three passes 2^22-2^26 1591 / 1604 / 1676 / 1522 / 1640 against 1504 / 1518 / 1453 / 1396 /
-  // 1356; 2^21 (128 x 128 x 128) 1534 against 1656 (a 32-column pass and a one-pass 2^16 tile row).
+  // 1893; two long passes 2^21-2^23 (slab_factors); three passes 2^24-2^26 1676 / 1522 / 1640 against
+  // 1453 / 1396 / 1356.
   // fp64: 2^16 2804 against 2156, 2^19 / 2^20 1813 / 1890 against 1759 / 1565, 2^21-2^24 1603 / 1676 /
   // 1770 / 1837 against 1587 / 1512 / 1493 / 1366; 2^17 / 2^18 lose (1936 / 1608 against 2023 / 1982).
   if (d.dtype == AMQFT_F64) return (lg == 16 || lg == 19 || lg >= 20) ? s : none;
-  return ((lg >= 17 && lg <= 20) || lg >= 22) ? s : none;
+  return lg >= 17 ? s : none;
 }
 
 template <typename R>

@@ -260,6 +260,9 @@ std::unique_ptr<SlabPassExec<R>> make_slab_pass(size_t len, const void* tab, uin
       case 256: return std::make_unique<SlabPassImpl<V, R, 4, 4, 32>>(tab, nmax, dev);
       case 512: return std::make_unique<SlabPassImpl<V, R, 4, 5, 16>>(tab, nmax, dev);
       case 1024: return std::make_unique<SlabPassImpl<V, R, 5, 5, 16>>(tab, nmax, dev);
+      // 64-point factors: 8- and 4-column slabs (64- and 32-byte runs) in 131 KB
+      case 2048: return std::make_unique<SlabPassImpl<V, R, 6, 5, 8>>(tab, nmax, dev);
+      case 4096: return std::make_unique<SlabPassImpl<V, R, 6, 6, 4>>(tab, nmax, dev);
     }
   } else {
     switch (len) {
