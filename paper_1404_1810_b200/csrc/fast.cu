@@ -113,6 +113,8 @@ std::unique_ptr<FastPlan> make_fast_plan(const amqft_plan_desc& d, const void* d
 namespace tilek {
 template <int V, typename R>
 std::unique_ptr<FastPlan> make_tile(size_t n, const void* tab, uint32_t nmax, int dev);
+template <int V, typename R>
+std::unique_ptr<FastPlan> make_tile_rdft(size_t n, const void* tab, uint32_t nmax, int dev);
 // the split of tile_kernel.cuh make_tile: N1 (phase A) x N2 (phase B) [x N3
 // (phase C); n3 = 1: two factors].  fp32: 4 x 4, 4 x 8, 8 x 8, 8 x 16, 16 x
 // 16, 16 x 32, 32 x 32, 64 x 32, 64 x 64, then 32 x 16 x 16, 32 x 16 x 32, 32
@@ -136,6 +138,19 @@ static void tile_split(int dtype, size_t n, size_t* n1, size_t* n2, size_t* n3) 
   *n2 = n / *n1;
 }
 }  // namespace tilek
+
+// RDFT rows on the two-factor kernel (tile_kernel.cuh make_tile_rdft), at the sizes where it beats
+// the whole-DAG RDFT kernels or only the generic interpreter is left: fp32 N = 256 .. 4096 (measured
+// 5467 / 4642 / 5367 / 5084 GB/s at 256 .. 2048 against 57 / 53 on the generic interpreter and 1770 /
+// 2349 on the fused kernel; the one-thread-per-row kernel runs N <= 128 at 5 TB/s, the fused kernel
+// 8192), fp64 N = 128 .. 1024 under the same tolerance rule as the CDFT rows.
+bool tile_rdft_covers(const amqft_plan_desc& d) {
+  if (d.function != AMQFT_FN_RDFT || d.order != AMQFT_ORDER_FAST || (d.n & (d.n - 1))) return false;
+  if (const char* e = std::getenv("AMQFT_AB_TILE"))
+    if (e[0] == 'n') return false;
+  if (d.dtype == AMQFT_F64) return d.n >= 128 && d.n <= (d.variant >= 5 ? 256u : 1024u);
+  return d.n >= 256 && d.n <= 4096;
+}
 
 bool tile_covers(const amqft_plan_desc& d) {
   if (d.function != AMQFT_FN_CDFT || d.order == AMQFT_ORDER_FAST_DAG) return false;
@@ -163,6 +178,19 @@ bool tile_covers(const amqft_plan_desc& d) {
 template <typename R>
 static std::unique_ptr<FastPlan> make_tile_typed(const amqft_plan_desc& d, const void* d_trig, uint32_t nmax) {
   using namespace tilek;
+  if (d.function == AMQFT_FN_RDFT) {
+    switch (d.variant) {
+      case 1: return make_tile_rdft<1, R>(d.n, d_trig, nmax, d.device);
+      case 2: return make_tile_rdft<2, R>(d.n, d_trig, nmax, d.device);
+      case 3: return make_tile_rdft<3, R>(d.n, d_trig, nmax, d.device);
+      case 4: return make_tile_rdft<4, R>(d.n, d_trig, nmax, d.device);
+      case 5: return make_tile_rdft<5, R>(d.n, d_trig, nmax, d.device);
+      case 6: return make_tile_rdft<6, R>(d.n, d_trig, nmax, d.device);
+      case 7: return make_tile_rdft<7, R>(d.n, d_trig, nmax, d.device);
+      case 8: return make_tile_rdft<8, R>(d.n, d_trig, nmax, d.device);
+    }
+    return nullptr;
+  }
   switch (d.variant) {
     case 1: return make_tile<1, R>(d.n, d_trig, nmax, d.device);
     case 2: return make_tile<2, R>(d.n, d_trig, nmax, d.device);
@@ -177,7 +205,7 @@ static std::unique_ptr<FastPlan> make_tile_typed(const amqft_plan_desc& d, const
 }
 
 std::unique_ptr<FastPlan> make_tile_plan(const amqft_plan_desc& d, const void* d_trig, uint32_t nmax) {
-  if (!tile_covers(d)) return nullptr;
+  if (!tile_covers(d) && !tile_rdft_covers(d)) return nullptr;
   return d.dtype == AMQFT_F64 ? make_tile_typed<double>(d, d_trig, nmax) : make_tile_typed<float>(d, d_trig, nmax);
 }
 

@@ -65,6 +65,7 @@ OpCount fast_op_counts(const amqft_plan_desc& d);
 // AMQFT_AB_TILE=none disables it (A/B measurements against the fused
 // kernel, which keeps the whole length-N DAG).
 bool tile_covers(const amqft_plan_desc& d);
+bool tile_rdft_covers(const amqft_plan_desc& d);   // RDFT rows as the CDFT of x + 0 i (fp32 256 .. 4096)
 std::unique_ptr<FastPlan> make_tile_plan(const amqft_plan_desc& d, const void* d_trig, uint32_t nmax);
 OpCount tile_op_counts(const amqft_plan_desc& d);
 

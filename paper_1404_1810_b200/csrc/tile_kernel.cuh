@@ -126,13 +126,22 @@ struct TCfg {
 
 // phase A: input n1 of column n2 from HBM (stride N2), output k1 times the
 // twiddle into P[k1][n2]
-template <typename R, int N2, int PITCH, bool INV>
+// FN = 1 (RDFT rows, signal.hpp:122-124): the row is N reals, read as x + 0 i;
+// the CDFT of a real row is C - i S, and the packed spectrum P[k] = C[k] (k <=
+// N/2), P[N - k] = S[k] is Re X[k] for k <= N/2 and Im X[k] above (conjugate
+// symmetry), so the last phase stores one real per output index.
+template <typename R, int N2, int PITCH, bool INV, int FN = 0>
 struct AIo {
   using V2 = typename RT<R>::V2;
-  const V2* __restrict__ gi;   // x + n2
+  const V2* __restrict__ gi;   // x + n2 (FN = 1: a pointer to reals)
   V2* sp;                      // P + n2
   const V2* __restrict__ tw;   // tw + n2: tw[k1 N2 + n2] = w_N^(n2 k1)
   __device__ __forceinline__ void ld(int c, R& a, R& b) const {
+    if constexpr (FN == 1) {
+      a = __ldcs(reinterpret_cast<const R*>(gi) + c * N2);
+      b = R(0);
+      return;
+    }
     const V2 u = __ldcs(gi + c * N2);
     if (INV) { a = u.y; b = u.x; }
     else { a = u.x; b = u.y; }
@@ -156,12 +165,13 @@ struct AIo {
 
 // last phase: a contiguous row of the tile (128-bit loads), output k at
 // X[base + STRIDE k]
-template <typename R, int STRIDE, bool INV>
+template <typename R, int STRIDE, bool INV, int FN = 0>
 struct BIo {
   using V2 = typename RT<R>::V2;
   const V2* sp;              // the row (16-byte aligned: even pitches in fp32)
-  V2* __restrict__ go;       // X + base
+  V2* __restrict__ go;       // X + base (FN = 1: a pointer to reals, P + base)
   R scale;
+  int base = 0, half = 0;    // FN = 1: output index base + STRIDE c against N / 2
   __device__ __forceinline__ void ld(int c, R& a, R& b) const {
     const V2 v = sp[c];
     a = v.x; b = v.y;
@@ -171,6 +181,10 @@ struct BIo {
     a = v.x; b = v.y; d = v.z; e = v.w;
   }
   __device__ __forceinline__ void st(int c, R a, R b) const {
+    if constexpr (FN == 1) {
+      __stcs(reinterpret_cast<R*>(go) + c * STRIDE, base + c * STRIDE <= half ? a : b);
+      return;
+    }
     if (INV) __stcs(go + c * STRIDE, mk2<R>(b * scale, a * scale));
     else __stcs(go + c * STRIDE, mk2<R>(a, b));
   }
@@ -180,7 +194,7 @@ struct BIo {
   }
 };
 
-template <int V, typename R, bool INV, class C>
+template <int V, typename R, bool INV, class C, int FN = 0>
 __global__ void __launch_bounds__(C::T, C::MINB)
 k_tile(const R* __restrict__ in, R* __restrict__ out, size_t rows,
        const __grid_constant__ TabP<R, C::NT1> t1, const __grid_constant__ TabP<R, C::NT2> t2,
@@ -200,15 +214,18 @@ k_tile(const R* __restrict__ in, R* __restrict__ out, size_t rows,
       const size_t nrow = (tile + gridDim.x) * C::R_;
       if (tid == 0 && nrow + C::R_ <= rows)
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
-                     ::"l"(in + nrow * 2 * N), "n"(C::R_ * N * static_cast<int>(sizeof(V2))) : "memory");
+                     ::"l"(in + nrow * (FN == 1 ? 1 : 2) * N),
+                       "n"(C::R_ * N * static_cast<int>(FN == 1 ? sizeof(R) : sizeof(V2))) : "memory");
     }
     // ---- phase A: columns of x -> P (twiddled)
 #pragma unroll 1
     for (int i = tid; i < C::R_ * N2; i += C::T) {
       const int r = i / N2, n2 = i % N2;
       if (row0 + r < rows) {
-        AIo<R, N2, C::PITCH, INV> io{reinterpret_cast<const V2*>(in) + (row0 + r) * N + n2, P + r * C::ROWP + n2,
-                                     tw + n2};
+        // FN = 1: rows of N reals (the pointer is reinterpreted in the loads)
+        const V2* src = FN == 1 ? reinterpret_cast<const V2*>(in + (row0 + r) * N + n2)
+                                : reinterpret_cast<const V2*>(in) + (row0 + r) * N + n2;
+        AIo<R, N2, C::PITCH, INV, FN> io{src, P + r * C::ROWP + n2, tw + n2};
         G1::template run<TArith<R>>(io, t1.v);
       }
     }
@@ -218,7 +235,9 @@ k_tile(const R* __restrict__ in, R* __restrict__ out, size_t rows,
     for (int j = tid; j < C::R_ * N1; j += C::T) {
       const int r = j / N1, k1 = j % N1;
       if (row0 + r < rows) {
-        BIo<R, N1, INV> io{P + r * C::ROWP + k1 * C::PITCH, reinterpret_cast<V2*>(out) + (row0 + r) * N + k1, scale};
+        V2* dst = FN == 1 ? reinterpret_cast<V2*>(out + (row0 + r) * N + k1)
+                          : reinterpret_cast<V2*>(out) + (row0 + r) * N + k1;
+        BIo<R, N1, INV, FN> io{P + r * C::ROWP + k1 * C::PITCH, dst, scale, k1, N / 2};
         G2::template run<TArith<R>>(io, t2.v);
       }
     }
@@ -242,7 +261,7 @@ inline void tk_check(cudaError_t e) {
   if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
 }
 
-template <int V, typename R, int LG1, int LG2, int T = 64, int MB = 0, int PF = -1>
+template <int V, typename R, int LG1, int LG2, int T = 64, int MB = 0, int PF = -1, int FN = 0>
 class TilePlanImpl final : public FastPlan {
   using C = TCfg<R, LG1, LG2, T, MB, PF>;
   using V2 = typename RT<R>::V2;
@@ -255,10 +274,12 @@ class TilePlanImpl final : public FastPlan {
     fill_twiddles(tw.data(), C::N1, C::N2, C::N);
     tk_check(cudaMalloc(&tw_, tw.size() * sizeof(V2)));
     tk_check(cudaMemcpy(tw_, tw.data(), tw.size() * sizeof(V2), cudaMemcpyHostToDevice));
-    auto f0 = k_tile<V, R, false, C>;
-    auto f1 = k_tile<V, R, true, C>;
+    auto f0 = k_tile<V, R, false, C, FN>;
     tk_check(cudaFuncSetAttribute(f0, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM)));
-    tk_check(cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM)));
+    if constexpr (FN == 0) {
+      auto f1 = k_tile<V, R, true, C, 0>;
+      tk_check(cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM)));
+    }
     int per_sm = 0;
     tk_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f0, C::T, C::SMEM));
     if (per_sm < 1) throw std::runtime_error("tile four-step kernel does not fit an SM");
@@ -274,12 +295,17 @@ class TilePlanImpl final : public FastPlan {
     const size_t tiles = (rows + C::R_ - 1) / C::R_;
     const unsigned grid = static_cast<unsigned>(std::min<size_t>(tiles, static_cast<size_t>(grid_cap_)));
     const R scale = R(1) / static_cast<R>(C::N);
-    if (inverse)
-      k_tile<V, R, true, C><<<grid, C::T, C::SMEM, st>>>(static_cast<const R*>(in), static_cast<R*>(out), rows, t1_,
-                                                         t2_, tw_, scale);
-    else
-      k_tile<V, R, false, C><<<grid, C::T, C::SMEM, st>>>(static_cast<const R*>(in), static_cast<R*>(out), rows, t1_,
-                                                          t2_, tw_, scale);
+    if constexpr (FN == 1) {   // RDFT rows: forward only (the engine builds the inverse on DCT / DST plans)
+      if (inverse) throw std::invalid_argument("the tile kernel's RDFT rows have no inverse");
+      k_tile<V, R, false, C, 1><<<grid, C::T, C::SMEM, st>>>(static_cast<const R*>(in), static_cast<R*>(out), rows,
+                                                             t1_, t2_, tw_, scale);
+    } else if (inverse) {
+      k_tile<V, R, true, C, 0><<<grid, C::T, C::SMEM, st>>>(static_cast<const R*>(in), static_cast<R*>(out), rows,
+                                                            t1_, t2_, tw_, scale);
+    } else {
+      k_tile<V, R, false, C, 0><<<grid, C::T, C::SMEM, st>>>(static_cast<const R*>(in), static_cast<R*>(out), rows,
+                                                             t1_, t2_, tw_, scale);
+    }
     tk_check(cudaGetLastError());
   }
 
@@ -659,6 +685,26 @@ std::unique_ptr<FastPlan> make_tile(size_t n, const void* tab, uint32_t nmax, in
       case 16384: return std::make_unique<Tile3PlanImpl<V, R, 5, 4, 5, 256, 1, 2>>(tab, nmax, dev);
       case 32768: return std::make_unique<Tile3PlanImpl<V, R, 5, 5, 5, 256, 1, 4>>(tab, nmax, dev);
     }
+  }
+  return nullptr;
+}
+
+// RDFT rows (FunctionId::Rdft) as the CDFT of x + 0 i on the two-factor
+// kernel: twice the arithmetic of the reference's RDFT (half a CDFT), but one
+// pass over HBM at sizes whose only other path is the generic interpreter.
+template <int V, typename R>
+std::unique_ptr<FastPlan> make_tile_rdft(size_t n, const void* tab, uint32_t nmax, int dev) {
+  switch (n) {
+    case 128: return std::make_unique<TilePlanImpl<V, R, 3, 4, 64, 0, -1, 1>>(tab, nmax, dev);
+    case 256: return std::make_unique<TilePlanImpl<V, R, 4, 4, 64, 0, -1, 1>>(tab, nmax, dev);
+    case 512: return std::make_unique<TilePlanImpl<V, R, 4, 5, 64, 0, -1, 1>>(tab, nmax, dev);
+    case 1024: return std::make_unique<TilePlanImpl<V, R, 5, 5, 64, 0, -1, 1>>(tab, nmax, dev);
+    case 2048:
+      if constexpr (sizeof(R) == 4) return std::make_unique<TilePlanImpl<V, R, 6, 5, 64, 0, -1, 1>>(tab, nmax, dev);
+      break;
+    case 4096:
+      if constexpr (sizeof(R) == 4) return std::make_unique<TilePlanImpl<V, R, 6, 6, 64, 0, -1, 1>>(tab, nmax, dev);
+      break;
   }
   return nullptr;
 }

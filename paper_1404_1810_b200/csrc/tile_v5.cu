@@ -7,6 +7,8 @@ namespace amqft_b200 {
 namespace tilek {
 template std::unique_ptr<FastPlan> make_tile<5, float>(size_t, const void*, uint32_t, int);
 template std::unique_ptr<FastPlan> make_tile<5, double>(size_t, const void*, uint32_t, int);
+template std::unique_ptr<FastPlan> make_tile_rdft<5, float>(size_t, const void*, uint32_t, int);
+template std::unique_ptr<FastPlan> make_tile_rdft<5, double>(size_t, const void*, uint32_t, int);
 }  // namespace tilek
 namespace slabk {
 template std::unique_ptr<SlabPassExec<float>> make_slab_pass<5, float>(size_t, const void*, uint32_t, int);

@@ -439,7 +439,7 @@ def test_fast_kernel_rdft_fp64_bitwise(oracle, restatement, n):
     r, O = restatement, oracle
     for v in range(1, 9):
         xs = [r.uniform(r.mix_seed(40, v, n, k), n) * 2 - 1 for k in range(5)]
-        plan = amqft.Plan(v, amqft.FunctionId.Rdft, n, 5, dtype="f64", order=amqft.Order.Fast)
+        plan = amqft.Plan(v, amqft.FunctionId.Rdft, n, 5, dtype="f64", order=amqft.Order.FastDag)
         assert plan.path()[0] == 2, "fused kernel expected for RDFT"
         got = run_plan(plan, xs)
         for k in range(5):

@@ -217,3 +217,34 @@ def test_fast_dag_order_keeps_the_reference_dag(oracle, restatement):
         assert r.rel_l2(run_plan(fast, [x])[0], want) <= 1e-12
     p32 = amqft.Plan(4, amqft.FunctionId.Cdft, 4096, 1, dtype="f32", order=amqft.Order.FastDag)
     assert p32.path() == (2, 1)
+
+
+# ---- RDFT rows (FunctionId::Rdft) on the two-factor kernel: the CDFT of x + 0 i,
+# stored as the packed spectrum (signal.hpp:122-124).  fp32 N = 256 .. 4096 (only the generic
+# interpreter covered 256 / 512 before), fp64 N = 128 .. 1024.
+@pytest.mark.parametrize("n,dtype", [(256, "f32"), (512, "f32"), (1024, "f32"), (2048, "f32"), (4096, "f32"),
+                                     (128, "f64"), (256, "f64"), (1024, "f64")])
+def test_tile_rdft_rows_match_cpu(oracle, restatement, n, dtype):
+    r, O = restatement, oracle
+    rows = 70                                    # partial last tile
+    xs = np.random.default_rng(n + 9).standard_normal((rows, n))
+    if dtype == "f32":
+        xs = xs.astype(np.float32).astype(np.float64)
+    for v in range(1, 9):
+        plan = amqft.Plan(v, amqft.FunctionId.Rdft, n, rows, dtype=dtype, order=amqft.Order.Fast)
+        if dtype == "f64" and v >= 5 and n > 256:
+            assert plan.path()[0] != 6          # the whole-DAG kernel (bitwise) keeps these
+            continue
+        assert plan.path() == (6, 1), (v, n, dtype)
+        got = run_plan(plan, xs)
+        for row in (0, rows - 1):
+            want = r.execute(v, O.F_RDFT, n, xs[row])
+            err = r.rel_l2(got[row], want)
+            assert err <= (1e-5 * math.log2(n) if dtype == "f32" else 1e-12), (v, n, dtype, err)
+        # the packed spectrum against numpy: P[k] = Re X[k] (k <= N/2), P[N - k] = -Im X[k]
+        f = np.fft.fft(xs[0])
+        ref = np.concatenate([f.real[:n // 2 + 1], (-f.imag[1:n // 2])[::-1]])
+        assert r.rel_l2(got[0], ref) <= (2e-6 if dtype == "f32" else 1e-13), (v, n, dtype)
+        # inverse (DCT-0 / DST-0 sub-plans, csrc/inverse.cu) round trip
+        back = run_plan(plan, got.astype(np.float32) if dtype == "f32" else got, inverse=True)
+        assert r.rel_l2(back.ravel(), xs.ravel()) <= (1e-5 * math.log2(n) if dtype == "f32" else 1e-9), (v, n, dtype)
