@@ -13,7 +13,7 @@ src, dst, tag = sys.argv[1], sys.argv[2], sys.argv[3]
 
 
 def short(name):
-    m = re.search(r"k_tile<(.*>)>", name)
+    m = re.search(r"k_tile<(.*)>(?=\(const)", name)
     if m:
         return f"k_tile<{m.group(1).replace(' ', '')}> (AM-QFT in-shared-memory four-step CDFT)"
     m = re.search(r"k_fast<(.*?)>", name)
