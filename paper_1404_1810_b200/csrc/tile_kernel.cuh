@@ -130,12 +130,29 @@ struct TCfg {
 // the CDFT of a real row is C - i S, and the packed spectrum P[k] = C[k] (k <=
 // N/2), P[N - k] = S[k] is Re X[k] for k <= N/2 and Im X[k] above (conjugate
 // symmetry), so the last phase stores one real per output index.
+// FN = 2 (A/B instance only, AMQFT_AB_TILE_TW=fly): CDFT rows with the twiddle
+// w_N^(n2 k1) computed on the fly (sincospif of the exact integer phase)
+// instead of read from the table -- the north-star's "computed on the fly or
+// held in a table, chosen by measured GB/s": config 2 runs 0.738 ms (5822
+// GB/s) with the table and 0.763 ms (5631 GB/s) on the fly, both 1.9e-7 from
+// the CPU reference (profiles/r02_tile_twiddle_ab.log), so the table it is.
 template <typename R, int N2, int PITCH, bool INV, int FN = 0>
 struct AIo {
   using V2 = typename RT<R>::V2;
   const V2* __restrict__ gi;   // x + n2 (FN = 1: a pointer to reals)
   V2* sp;                      // P + n2
   const V2* __restrict__ tw;   // tw + n2: tw[k1 N2 + n2] = w_N^(n2 k1)
+  int n2 = 0, lgn = 0;         // FN = 2: the thread's column and log2 N
+  __device__ __forceinline__ V2 twiddle(int k1) const {
+    if constexpr (FN == 2) {
+      const unsigned e = (static_cast<unsigned>(n2) * static_cast<unsigned>(k1)) & ((1u << lgn) - 1u);
+      float sn, cs;
+      sincospif(static_cast<float>(e) * (2.0f / static_cast<float>(1u << lgn)), &sn, &cs);
+      return mk2<R>(static_cast<R>(cs), static_cast<R>(-sn));
+    } else {
+      return __ldg(tw + k1 * N2);
+    }
+  }
   __device__ __forceinline__ void ld(int c, R& a, R& b) const {
     if constexpr (FN == 1) {
       a = __ldcs(reinterpret_cast<const R*>(gi) + c * N2);
@@ -151,12 +168,12 @@ struct AIo {
     ld(2 * c + 1, d, e);
   }
   __device__ __forceinline__ void st(int c, R a, R b) const {
-    if (c != 0) cmul(a, b, __ldg(tw + c * N2));   // k1 = 0: w = 1
+    if (c != 0) cmul(a, b, twiddle(c));   // k1 = 0: w = 1
     sp[c * PITCH] = mk2<R>(a, b);
   }
   __device__ __forceinline__ void st(int c, R a, R b, R d, R e) const {
-    const V2 w1 = __ldg(tw + (2 * c + 1) * N2);
-    if (c != 0) cmul(a, b, __ldg(tw + (2 * c) * N2));
+    const V2 w1 = twiddle(2 * c + 1);
+    if (c != 0) cmul(a, b, twiddle(2 * c));
     cmul(d, e, w1);
     sp[(2 * c) * PITCH] = mk2<R>(a, b);
     sp[(2 * c + 1) * PITCH] = mk2<R>(d, e);
@@ -225,7 +242,7 @@ k_tile(const R* __restrict__ in, R* __restrict__ out, size_t rows,
         // FN = 1: rows of N reals (the pointer is reinterpreted in the loads)
         const V2* src = FN == 1 ? reinterpret_cast<const V2*>(in + (row0 + r) * N + n2)
                                 : reinterpret_cast<const V2*>(in) + (row0 + r) * N + n2;
-        AIo<R, N2, C::PITCH, INV, FN> io{src, P + r * C::ROWP + n2, tw + n2};
+        AIo<R, N2, C::PITCH, INV, FN> io{src, P + r * C::ROWP + n2, tw + n2, n2, LG1 + LG2};
         G1::template run<TArith<R>>(io, t1.v);
       }
     }
@@ -276,8 +293,8 @@ class TilePlanImpl final : public FastPlan {
     tk_check(cudaMemcpy(tw_, tw.data(), tw.size() * sizeof(V2), cudaMemcpyHostToDevice));
     auto f0 = k_tile<V, R, false, C, FN>;
     tk_check(cudaFuncSetAttribute(f0, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM)));
-    if constexpr (FN == 0) {
-      auto f1 = k_tile<V, R, true, C, 0>;
+    if constexpr (FN != 1) {
+      auto f1 = k_tile<V, R, true, C, FN>;
       tk_check(cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM)));
     }
     int per_sm = 0;
@@ -300,11 +317,11 @@ class TilePlanImpl final : public FastPlan {
       k_tile<V, R, false, C, 1><<<grid, C::T, C::SMEM, st>>>(static_cast<const R*>(in), static_cast<R*>(out), rows,
                                                              t1_, t2_, tw_, scale);
     } else if (inverse) {
-      k_tile<V, R, true, C, 0><<<grid, C::T, C::SMEM, st>>>(static_cast<const R*>(in), static_cast<R*>(out), rows,
-                                                            t1_, t2_, tw_, scale);
-    } else {
-      k_tile<V, R, false, C, 0><<<grid, C::T, C::SMEM, st>>>(static_cast<const R*>(in), static_cast<R*>(out), rows,
+      k_tile<V, R, true, C, FN><<<grid, C::T, C::SMEM, st>>>(static_cast<const R*>(in), static_cast<R*>(out), rows,
                                                              t1_, t2_, tw_, scale);
+    } else {
+      k_tile<V, R, false, C, FN><<<grid, C::T, C::SMEM, st>>>(static_cast<const R*>(in), static_cast<R*>(out), rows,
+                                                              t1_, t2_, tw_, scale);
     }
     tk_check(cudaGetLastError());
   }
@@ -654,6 +671,10 @@ class Tile3PlanImpl final : public FastPlan {
 // 0.912), N = 8 as 2 x 4 (no gain over the direct kernel).
 template <int V, typename R>
 std::unique_ptr<FastPlan> make_tile(size_t n, const void* tab, uint32_t nmax, int dev) {
+  if constexpr (sizeof(R) == 4 && V == 4) {   // A/B: config 2's twiddles on the fly (variant 4 only)
+    const char* e = std::getenv("AMQFT_AB_TILE_TW");
+    if (n == 4096 && e && e[0] == 'f') return std::make_unique<TilePlanImpl<V, R, 6, 6, 64, 0, -1, 2>>(tab, nmax, dev);
+  }
   if constexpr (sizeof(R) == 4) {
     switch (n) {
       case 16: return std::make_unique<TilePlanImpl<V, R, 2, 2>>(tab, nmax, dev);
