@@ -115,6 +115,8 @@ template <int V, typename R>
 std::unique_ptr<FastPlan> make_tile(size_t n, const void* tab, uint32_t nmax, int dev);
 template <int V, typename R>
 std::unique_ptr<FastPlan> make_tile_rdft(size_t n, const void* tab, uint32_t nmax, int dev);
+template <int V, typename R>
+std::unique_ptr<FastPlan> make_tile_dctdst(int fn, size_t n, const void* tab, uint32_t nmax, int dev);
 // the split of tile_kernel.cuh make_tile: N1 (phase A) x N2 (phase B) [x N3
 // (phase C); n3 = 1: two factors].  fp32: 4 x 4, 4 x 8, 8 x 8, 8 x 16, 16 x
 // 16, 16 x 32, 32 x 32, 64 x 32, 64 x 64, then 32 x 16 x 16, 32 x 16 x 32, 32
@@ -150,6 +152,17 @@ bool tile_rdft_covers(const amqft_plan_desc& d) {
     if (e[0] == 'n') return false;
   if (d.dtype == AMQFT_F64) return d.n >= 128 && d.n <= (d.variant >= 5 ? 256u : 1024u);
   return d.n >= 256 && d.n <= 4096;
+}
+
+// DCT-0 / DST-0 rows on the two-factor kernel (make_tile_dctdst): above the scalar small kernels'
+// sizes (fp32 N <= 256, fp64 <= 128), where only the generic interpreter was left.
+bool tile_dctdst_covers(const amqft_plan_desc& d) {
+  if ((d.function != AMQFT_FN_DCT && d.function != AMQFT_FN_DST) || d.order != AMQFT_ORDER_FAST) return false;
+  if (d.n & (d.n - 1)) return false;
+  if (const char* e = std::getenv("AMQFT_AB_TILE"))
+    if (e[0] == 'n') return false;
+  if (d.dtype == AMQFT_F64) return d.n >= 256 && d.n <= (d.variant >= 5 ? 256u : 1024u);
+  return d.n >= 512 && d.n <= 4096;
 }
 
 bool tile_covers(const amqft_plan_desc& d) {
@@ -191,6 +204,19 @@ static std::unique_ptr<FastPlan> make_tile_typed(const amqft_plan_desc& d, const
     }
     return nullptr;
   }
+  if (d.function == AMQFT_FN_DCT || d.function == AMQFT_FN_DST) {
+    switch (d.variant) {
+      case 1: return make_tile_dctdst<1, R>(d.function, d.n, d_trig, nmax, d.device);
+      case 2: return make_tile_dctdst<2, R>(d.function, d.n, d_trig, nmax, d.device);
+      case 3: return make_tile_dctdst<3, R>(d.function, d.n, d_trig, nmax, d.device);
+      case 4: return make_tile_dctdst<4, R>(d.function, d.n, d_trig, nmax, d.device);
+      case 5: return make_tile_dctdst<5, R>(d.function, d.n, d_trig, nmax, d.device);
+      case 6: return make_tile_dctdst<6, R>(d.function, d.n, d_trig, nmax, d.device);
+      case 7: return make_tile_dctdst<7, R>(d.function, d.n, d_trig, nmax, d.device);
+      case 8: return make_tile_dctdst<8, R>(d.function, d.n, d_trig, nmax, d.device);
+    }
+    return nullptr;
+  }
   switch (d.variant) {
     case 1: return make_tile<1, R>(d.n, d_trig, nmax, d.device);
     case 2: return make_tile<2, R>(d.n, d_trig, nmax, d.device);
@@ -205,7 +231,7 @@ static std::unique_ptr<FastPlan> make_tile_typed(const amqft_plan_desc& d, const
 }
 
 std::unique_ptr<FastPlan> make_tile_plan(const amqft_plan_desc& d, const void* d_trig, uint32_t nmax) {
-  if (!tile_covers(d) && !tile_rdft_covers(d)) return nullptr;
+  if (!tile_covers(d) && !tile_rdft_covers(d) && !tile_dctdst_covers(d)) return nullptr;
   return d.dtype == AMQFT_F64 ? make_tile_typed<double>(d, d_trig, nmax) : make_tile_typed<float>(d, d_trig, nmax);
 }
 

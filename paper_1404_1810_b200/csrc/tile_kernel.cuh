@@ -116,6 +116,7 @@ struct TCfg {
   // 2-6 % with it.
   static constexpr bool PF = PF_ < 0 ? LGR >= 6 : PF_ != 0;
   static constexpr size_t SMEM = static_cast<size_t>(R_) * ROWP * sizeof(V2);
+  static constexpr size_t SMEMX = SMEM + 2 * R_ * sizeof(R);   // + x[0], x[N/2] per row (DCT-0 rows)
   static constexpr int NT1 = (N1 < 8 ? 8 : N1) / 4, NT2 = (N2 < 8 ? 8 : N2) / 4;
   static_assert(RT<R>::spread(PITCH), "bank-group spread of the 128-bit row loads");
 };
@@ -153,10 +154,28 @@ struct AIo {
       return __ldg(tw + k1 * N2);
     }
   }
+  R* sx = nullptr;             // FN = 3: shared-memory copy of the row's x[0], x[N/2] for the last phase
   __device__ __forceinline__ void ld(int c, R& a, R& b) const {
     if constexpr (FN == 1) {
       a = __ldcs(reinterpret_cast<const R*>(gi) + c * N2);
       b = R(0);
+      return;
+    }
+    if constexpr (FN == 3 || FN == 4) {
+      // DCT-0 / DST-0 rows (N/2 + 1 / N/2 - 1 cells, oracle.hpp:38-41) as the CDFT of the even /
+      // odd extension y of length N: y[j] = x[j], y[N - j] = +-x[j] (DST-0: y[0] = y[N/2] = 0).
+      // gi points at the row's first cell; element j = c N2 + n2.
+      const R* xr = reinterpret_cast<const R*>(gi);
+      const int nn = 1 << lgn, j = c * N2 + n2, m = 2 * j <= nn ? j : nn - j;
+      b = R(0);
+      if constexpr (FN == 3) {
+        a = __ldcs(xr + m);
+        if (j == 0) sx[0] = a;
+        if (2 * j == nn) sx[1] = a;
+      } else {
+        a = (m == 0 || 2 * m == nn) ? R(0) : __ldcs(xr + m - 1);
+        if (2 * j > nn) a = -a;
+      }
       return;
     }
     const V2 u = __ldcs(gi + c * N2);
@@ -188,7 +207,8 @@ struct BIo {
   const V2* sp;              // the row (16-byte aligned: even pitches in fp32)
   V2* __restrict__ go;       // X + base (FN = 1: a pointer to reals, P + base)
   R scale;
-  int base = 0, half = 0;    // FN = 1: output index base + STRIDE c against N / 2
+  int base = 0, half = 0;    // FN = 1, 3, 4: output index base + STRIDE c against N / 2
+  R x0 = R(0), xh = R(0);    // FN = 3: the row's x[0] and x[N/2]
   __device__ __forceinline__ void ld(int c, R& a, R& b) const {
     const V2 v = sp[c];
     a = v.x; b = v.y;
@@ -200,6 +220,16 @@ struct BIo {
   __device__ __forceinline__ void st(int c, R a, R b) const {
     if constexpr (FN == 1) {
       __stcs(reinterpret_cast<R*>(go) + c * STRIDE, base + c * STRIDE <= half ? a : b);
+      return;
+    }
+    if constexpr (FN == 3) {   // DCT-0[k] = (Re X[k] + x[0] + (-1)^k x[N/2]) / 2, k <= N/2
+      const int k = base + c * STRIDE;
+      if (k <= half) __stcs(reinterpret_cast<R*>(go) + c * STRIDE, R(0.5) * (a + x0 + ((k & 1) ? -xh : xh)));
+      return;
+    }
+    if constexpr (FN == 4) {   // DST-0[k] = -Im X[k] / 2, 0 < k < N/2 (cell k - 1)
+      const int k = base + c * STRIDE;
+      if (k > 0 && k < half) __stcs(reinterpret_cast<R*>(go) + c * STRIDE - 1, R(-0.5) * b);
       return;
     }
     if (INV) __stcs(go + c * STRIDE, mk2<R>(b * scale, a * scale));
@@ -223,11 +253,12 @@ k_tile(const R* __restrict__ in, R* __restrict__ out, size_t rows,
   constexpr int N1 = C::N1, N2 = C::N2, N = C::N;
   extern __shared__ __align__(128) unsigned char sm[];
   V2* P = reinterpret_cast<V2*>(sm);
+  R* SX = reinterpret_cast<R*>(sm + C::SMEM);   // FN = 3: x[0], x[N/2] of the tile's rows (2 R_ values)
   const int tid = threadIdx.x;
   const size_t tiles = (rows + C::R_ - 1) / C::R_;
   for (size_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
     const size_t row0 = tile * C::R_;
-    if constexpr (C::PF) {   // the CTA's next tile: one bulk prefetch into L2
+    if constexpr (C::PF && FN < 3) {   // the CTA's next tile: one bulk prefetch into L2
       const size_t nrow = (tile + gridDim.x) * C::R_;
       if (tid == 0 && nrow + C::R_ <= rows)
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
@@ -239,10 +270,13 @@ k_tile(const R* __restrict__ in, R* __restrict__ out, size_t rows,
     for (int i = tid; i < C::R_ * N2; i += C::T) {
       const int r = i / N2, n2 = i % N2;
       if (row0 + r < rows) {
-        // FN = 1: rows of N reals (the pointer is reinterpreted in the loads)
+        // FN = 1: rows of N reals; FN = 3 / 4: rows of N/2 + 1 / N/2 - 1 reals, addressed from
+        // their first cell (the pointers are reinterpreted in the loads)
+        constexpr size_t CELLS = FN == 3 ? N / 2 + 1 : (FN == 4 ? N / 2 - 1 : N);
         const V2* src = FN == 1 ? reinterpret_cast<const V2*>(in + (row0 + r) * N + n2)
-                                : reinterpret_cast<const V2*>(in) + (row0 + r) * N + n2;
-        AIo<R, N2, C::PITCH, INV, FN> io{src, P + r * C::ROWP + n2, tw + n2, n2, LG1 + LG2};
+                        : (FN == 3 || FN == 4) ? reinterpret_cast<const V2*>(in + (row0 + r) * CELLS)
+                                               : reinterpret_cast<const V2*>(in) + (row0 + r) * N + n2;
+        AIo<R, N2, C::PITCH, INV, FN> io{src, P + r * C::ROWP + n2, tw + n2, n2, LG1 + LG2, SX + 2 * r};
         G1::template run<TArith<R>>(io, t1.v);
       }
     }
@@ -252,9 +286,12 @@ k_tile(const R* __restrict__ in, R* __restrict__ out, size_t rows,
     for (int j = tid; j < C::R_ * N1; j += C::T) {
       const int r = j / N1, k1 = j % N1;
       if (row0 + r < rows) {
+        constexpr size_t CELLS = FN == 3 ? N / 2 + 1 : (FN == 4 ? N / 2 - 1 : N);
         V2* dst = FN == 1 ? reinterpret_cast<V2*>(out + (row0 + r) * N + k1)
-                          : reinterpret_cast<V2*>(out) + (row0 + r) * N + k1;
-        BIo<R, N1, INV, FN> io{P + r * C::ROWP + k1 * C::PITCH, dst, scale, k1, N / 2};
+                  : (FN == 3 || FN == 4) ? reinterpret_cast<V2*>(out + (row0 + r) * CELLS + k1)
+                                         : reinterpret_cast<V2*>(out) + (row0 + r) * N + k1;
+        BIo<R, N1, INV, FN> io{P + r * C::ROWP + k1 * C::PITCH, dst, scale, k1, N / 2, FN == 3 ? SX[2 * r] : R(0),
+                               FN == 3 ? SX[2 * r + 1] : R(0)};
         G2::template run<TArith<R>>(io, t2.v);
       }
     }
@@ -292,13 +329,13 @@ class TilePlanImpl final : public FastPlan {
     tk_check(cudaMalloc(&tw_, tw.size() * sizeof(V2)));
     tk_check(cudaMemcpy(tw_, tw.data(), tw.size() * sizeof(V2), cudaMemcpyHostToDevice));
     auto f0 = k_tile<V, R, false, C, FN>;
-    tk_check(cudaFuncSetAttribute(f0, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM)));
-    if constexpr (FN != 1) {
+    tk_check(cudaFuncSetAttribute(f0, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEMX)));
+    if constexpr (FN == 0 || FN == 2) {
       auto f1 = k_tile<V, R, true, C, FN>;
-      tk_check(cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM)));
+      tk_check(cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEMX)));
     }
     int per_sm = 0;
-    tk_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f0, C::T, C::SMEM));
+    tk_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f0, C::T, C::SMEMX));
     if (per_sm < 1) throw std::runtime_error("tile four-step kernel does not fit an SM");
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -312,15 +349,15 @@ class TilePlanImpl final : public FastPlan {
     const size_t tiles = (rows + C::R_ - 1) / C::R_;
     const unsigned grid = static_cast<unsigned>(std::min<size_t>(tiles, static_cast<size_t>(grid_cap_)));
     const R scale = R(1) / static_cast<R>(C::N);
-    if constexpr (FN == 1) {   // RDFT rows: forward only (the engine builds the inverse on DCT / DST plans)
-      if (inverse) throw std::invalid_argument("the tile kernel's RDFT rows have no inverse");
-      k_tile<V, R, false, C, 1><<<grid, C::T, C::SMEM, st>>>(static_cast<const R*>(in), static_cast<R*>(out), rows,
+    if constexpr (FN == 1 || FN >= 3) {   // real rows: forward only (the engine composes their inverses)
+      if (inverse) throw std::invalid_argument("the tile kernel's real rows have no inverse");
+      k_tile<V, R, false, C, FN><<<grid, C::T, C::SMEMX, st>>>(static_cast<const R*>(in), static_cast<R*>(out), rows,
                                                              t1_, t2_, tw_, scale);
     } else if (inverse) {
-      k_tile<V, R, true, C, FN><<<grid, C::T, C::SMEM, st>>>(static_cast<const R*>(in), static_cast<R*>(out), rows,
+      k_tile<V, R, true, C, FN><<<grid, C::T, C::SMEMX, st>>>(static_cast<const R*>(in), static_cast<R*>(out), rows,
                                                              t1_, t2_, tw_, scale);
     } else {
-      k_tile<V, R, false, C, FN><<<grid, C::T, C::SMEM, st>>>(static_cast<const R*>(in), static_cast<R*>(out), rows,
+      k_tile<V, R, false, C, FN><<<grid, C::T, C::SMEMX, st>>>(static_cast<const R*>(in), static_cast<R*>(out), rows,
                                                               t1_, t2_, tw_, scale);
     }
     tk_check(cudaGetLastError());
@@ -727,6 +764,28 @@ std::unique_ptr<FastPlan> make_tile_rdft(size_t n, const void* tab, uint32_t nma
       if constexpr (sizeof(R) == 4) return std::make_unique<TilePlanImpl<V, R, 6, 6, 64, 0, -1, 1>>(tab, nmax, dev);
       break;
   }
+  return nullptr;
+}
+
+// DCT-0 / DST-0 rows (FunctionId::Dct / Dst) as the CDFT of the even / odd extension: four times the
+// reference's arithmetic, one pass, at sizes the small scalar kernels do not reach.  fn: 2 DCT-0, 3 DST-0.
+template <int V, typename R>
+std::unique_ptr<FastPlan> make_tile_dctdst(int fn, size_t n, const void* tab, uint32_t nmax, int dev) {
+#define AMQFT_TILE_REAL(LGA, LGB)                                                                          \
+  return fn == AMQFT_FN_DCT ? std::unique_ptr<FastPlan>(new TilePlanImpl<V, R, LGA, LGB, 64, 0, -1, 3>(tab, nmax, dev)) \
+                            : std::unique_ptr<FastPlan>(new TilePlanImpl<V, R, LGA, LGB, 64, 0, -1, 4>(tab, nmax, dev));
+  switch (n) {
+    case 256: AMQFT_TILE_REAL(4, 4)
+    case 512: AMQFT_TILE_REAL(4, 5)
+    case 1024: AMQFT_TILE_REAL(5, 5)
+    case 2048:
+      if constexpr (sizeof(R) == 4) { AMQFT_TILE_REAL(6, 5) }
+      break;
+    case 4096:
+      if constexpr (sizeof(R) == 4) { AMQFT_TILE_REAL(6, 6) }
+      break;
+  }
+#undef AMQFT_TILE_REAL
   return nullptr;
 }
 

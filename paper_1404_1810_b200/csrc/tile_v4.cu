@@ -9,6 +9,8 @@ template std::unique_ptr<FastPlan> make_tile<4, float>(size_t, const void*, uint
 template std::unique_ptr<FastPlan> make_tile<4, double>(size_t, const void*, uint32_t, int);
 template std::unique_ptr<FastPlan> make_tile_rdft<4, float>(size_t, const void*, uint32_t, int);
 template std::unique_ptr<FastPlan> make_tile_rdft<4, double>(size_t, const void*, uint32_t, int);
+template std::unique_ptr<FastPlan> make_tile_dctdst<4, float>(int, size_t, const void*, uint32_t, int);
+template std::unique_ptr<FastPlan> make_tile_dctdst<4, double>(int, size_t, const void*, uint32_t, int);
 }  // namespace tilek
 namespace slabk {
 template std::unique_ptr<SlabPassExec<float>> make_slab_pass<4, float>(size_t, const void*, uint32_t, int);

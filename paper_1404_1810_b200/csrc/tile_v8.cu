@@ -9,6 +9,8 @@ template std::unique_ptr<FastPlan> make_tile<8, float>(size_t, const void*, uint
 template std::unique_ptr<FastPlan> make_tile<8, double>(size_t, const void*, uint32_t, int);
 template std::unique_ptr<FastPlan> make_tile_rdft<8, float>(size_t, const void*, uint32_t, int);
 template std::unique_ptr<FastPlan> make_tile_rdft<8, double>(size_t, const void*, uint32_t, int);
+template std::unique_ptr<FastPlan> make_tile_dctdst<8, float>(int, size_t, const void*, uint32_t, int);
+template std::unique_ptr<FastPlan> make_tile_dctdst<8, double>(int, size_t, const void*, uint32_t, int);
 }  // namespace tilek
 namespace slabk {
 template std::unique_ptr<SlabPassExec<float>> make_slab_pass<8, float>(size_t, const void*, uint32_t, int);

@@ -730,12 +730,13 @@ def test_fast_plans_reject_misaligned_buffers():
     assert torch.equal(z, y[:rows])
 
 
-@pytest.mark.parametrize("order", [amqft.Order.Exact, amqft.Order.Fast])
+@pytest.mark.parametrize("order", [amqft.Order.Exact, amqft.Order.FastDag])
 def test_real_transform_inverses(oracle, restatement, order):
     """Inverses of RDFT / DCT-0 / DST-0 (csrc/inverse.cu):
     fp64 bitwise the oracle composition (the reference forward between the
     same exact power-of-two weightings and butterfly) on the exact generic
-    path and on the fast kernels; round trip <= 1e-13 for v1-4; odd-function
+    path and on the whole-DAG fast kernels (the default fast order's split
+    kernels: tests/test_gpu_tile.py, within tolerance); round trip <= 1e-13 for v1-4; odd-function
     plans still reject the inverse."""
     r, O = restatement, oracle
     for f in (O.F_RDFT, O.F_DCT, O.F_DST):

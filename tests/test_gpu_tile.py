@@ -248,3 +248,35 @@ def test_tile_rdft_rows_match_cpu(oracle, restatement, n, dtype):
         # inverse (DCT-0 / DST-0 sub-plans, csrc/inverse.cu) round trip
         back = run_plan(plan, got.astype(np.float32) if dtype == "f32" else got, inverse=True)
         assert r.rel_l2(back.ravel(), xs.ravel()) <= (1e-5 * math.log2(n) if dtype == "f32" else 1e-9), (v, n, dtype)
+
+
+# ---- DCT-0 / DST-0 rows (FunctionId::Dct / Dst: N/2 + 1 / N/2 - 1 cells, oracle.hpp:38-41) on the
+# two-factor kernel: the CDFT of the even / odd extension.  fp32 N = 512 .. 4096, fp64 256 .. 1024
+# (above the scalar small kernels, where only the generic interpreter was left).
+@pytest.mark.parametrize("n,dtype", [(512, "f32"), (1024, "f32"), (4096, "f32"), (256, "f64"), (1024, "f64")])
+def test_tile_dct_dst_rows_match_cpu(oracle, restatement, n, dtype):
+    r, O = restatement, oracle
+    rows = 70
+    for f in (O.F_DCT, O.F_DST):
+        cells = amqft.cell_count(f, n)
+        xs = np.random.default_rng(n + f).standard_normal((rows, cells))
+        if dtype == "f32":
+            xs = xs.astype(np.float32).astype(np.float64)
+        for v in range(1, 9):
+            plan = amqft.Plan(v, f, n, rows, dtype=dtype, order=amqft.Order.Fast)
+            if dtype == "f64" and v >= 5 and n > 256:
+                assert plan.path()[0] != 6
+                continue
+            assert plan.path() == (6, 1), (v, f, n, dtype)
+            got = run_plan(plan, xs)
+            for row in (0, rows - 1):
+                want = r.execute(v, f, n, xs[row])
+                err = r.rel_l2(got[row], want)
+                assert err <= (1e-5 * math.log2(n) if dtype == "f32" else 1e-12), (v, f, n, dtype, err)
+            # in place, and the inverse (weights + the same forward, csrc/inverse.cu) round trip
+            t = torch.tensor(xs, dtype=torch.float32 if dtype == "f32" else torch.float64, device=DEV)
+            plan.forward(t, t)
+            torch.cuda.synchronize()
+            assert np.array_equal(t.double().cpu().numpy(), got), (v, f, n, dtype)
+            back = run_plan(plan, got.astype(np.float32) if dtype == "f32" else got, inverse=True)
+            assert r.rel_l2(back.ravel(), xs.ravel()) <= (1e-5 * math.log2(n) if dtype == "f32" else 1e-9), (v, f, n)
