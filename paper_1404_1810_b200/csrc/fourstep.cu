@@ -828,6 +828,10 @@ SlabShape fourstep_slab_shape(const amqft_plan_desc& d) {
   // 1453 / 1396 / 1356.
   // fp64: 2^16 2804 against 2156, 2^19 / 2^20 1813 / 1890 against 1759 / 1565, 2^21-2^24 1603 / 1676 /
   // 1770 / 1837 against 1587 / 1512 / 1493 / 1366; 2^17 / 2^18 lose (1936 / 1608 against 2023 / 1982).
+  // fp64 variants 5-8 have no one-pass tile rows above N = 256 (fast.cu tile_covers), so the older plan
+  // runs on the whole-DAG kernels: slab 2^14 / 2^15 / 2^17 / 2^18 2642 / 2863 / 1979 / 1642 against 1605 /
+  // 1581 / 1622 / 1575 (v6)
+  if (d.dtype == AMQFT_F64 && d.variant >= 5) return lg >= 14 ? s : none;
   if (d.dtype == AMQFT_F64) return (lg == 16 || lg == 19 || lg >= 20) ? s : none;
   return lg >= 17 ? s : none;
 }
