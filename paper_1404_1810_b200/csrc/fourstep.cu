@@ -338,29 +338,34 @@ __global__ void __launch_bounds__(256) k_twiddle_scatter_t(const float2* __restr
 // rows).  32 x 32 tiles (r, kb) for a fixed ka: reads coalesced along kb,
 // writes along n2; per thread 4 elements kb + 8 j share one twiddle
 // evaluation and a recurrence (step w^(8 A n2)).
+template <int KB>   // kb per tile: 32, or 64 (8 elements per twiddle evaluation) where n1 / A allows
 __global__ void __launch_bounds__(256) k_twiddle_scatter_direct(const float2* __restrict__ in, const DstPtrs dst,
                                                                 int n1, int A, int logn, long long row0,
                                                                 long long n2_total, int nparts,
                                                                 const double2* __restrict__ twh,
                                                                 const double2* __restrict__ twl, int logb,
                                                                 int onthefly) {
-  __shared__ float2 tile[32][33];
+  __shared__ float2 tile[KB][33];
   const int B = n1 / A, w = n1 / nparts;
   const int ka = blockIdx.z;
-  const int kb0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  const int kb0 = blockIdx.x * KB, r0 = blockIdx.y * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
+  // tile[kb][r]: rows read along kb (coalesced), 32 kb per pass
 #pragma unroll
-  for (int j = 0; j < 32; j += 8)
-    tile[ty + j][tx] = in[static_cast<long long>(r0 + ty + j) * n1 + static_cast<long long>(ka) * B + kb0 + tx];
+  for (int h = 0; h < KB; h += 32)
+#pragma unroll
+    for (int j = 0; j < 32; j += 8)
+      tile[h + tx][ty + j] =
+          in[static_cast<long long>(r0 + ty + j) * n1 + static_cast<long long>(ka) * B + kb0 + h + tx];
   __syncthreads();
   const unsigned long long n2 = static_cast<unsigned long long>(row0 + r0 + tx);
   double cr, ci, sr, si;
   scatter_tw(n2 * static_cast<unsigned long long>(ka + A * (kb0 + ty)), logn, twh, twl, logb, onthefly, cr, ci);
   scatter_tw(n2 * static_cast<unsigned long long>(8 * A), logn, twh, twl, logb, onthefly, sr, si);
 #pragma unroll
-  for (int j = 0; j < 32; j += 8) {
+  for (int j = 0; j < KB; j += 8) {
     const int kb = kb0 + ty + j;
-    const float2 v = tile[tx][ty + j];
+    const float2 v = tile[ty + j][tx];
     const float fr = static_cast<float>(cr), fi = static_cast<float>(ci);
     const int k1 = ka + A * kb;
     const int q = k1 / w, kl = k1 - q * w;
@@ -756,11 +761,13 @@ void dist_twiddle_scatter_direct(const void* in, void* const* d_dst, size_t rows
     throw std::invalid_argument("twiddle_scatter_direct: n1 / A and rows must be multiples of 32");
   DstPtrs dp{};
   for (int q = 0; q < nparts; ++q) dp.p[q] = static_cast<float2*>(d_dst[q]);
-  const dim3 grid(static_cast<unsigned>(n1 / a / 32), static_cast<unsigned>(rows / 32), static_cast<unsigned>(a));
-  k_twiddle_scatter_direct<<<grid, dim3(32, 8), 0, st>>>(static_cast<const float2*>(in), dp, static_cast<int>(n1),
-                                                          static_cast<int>(a), tw->logn, static_cast<long long>(row0),
-                                                          static_cast<long long>(n / n1), nparts, tw->hi, tw->lo,
-                                                          tw->logb, trig_mode == AMQFT_TRIG_ONTHEFLY ? 1 : 0);
+  const bool wide = (n1 / a) % 64 == 0;
+  const dim3 grid(static_cast<unsigned>(n1 / a / (wide ? 64 : 32)), static_cast<unsigned>(rows / 32),
+                  static_cast<unsigned>(a));
+  auto kern = wide ? k_twiddle_scatter_direct<64> : k_twiddle_scatter_direct<32>;
+  kern<<<grid, dim3(32, 8), 0, st>>>(static_cast<const float2*>(in), dp, static_cast<int>(n1), static_cast<int>(a),
+                                      tw->logn, static_cast<long long>(row0), static_cast<long long>(n / n1), nparts,
+                                      tw->hi, tw->lo, tw->logb, trig_mode == AMQFT_TRIG_ONTHEFLY ? 1 : 0);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("k_twiddle_scatter_direct: ") + cudaGetErrorString(e));
 }
