@@ -294,20 +294,24 @@ __global__ void __launch_bounds__(256) k_twiddle_scatter(const float2* __restric
 // order in[r][ka][kb] = row value at k1 = ka + A kb (A x B, B = n1 / A):
 // the four-step's final transpose folded in.  32 x 32 tiles (ka, kb) per
 // row: reads coalesced along kb, writes along ka (consecutive k1, one
-// slab when w is a multiple of 32); per thread 4 elements kb + 8 j share
-// one twiddle evaluation and a recurrence (step w^(8 A n2)).
+// slab when w is a multiple of 32); per thread 4 (8 on 64-wide tiles) elements
+// kb + 8 j share one twiddle evaluation and a recurrence (step w^(8 A n2)).
+template <int KB>   // kb per tile: 32, or 64 (8 elements per twiddle evaluation) where n1 / A allows
 __global__ void __launch_bounds__(256) k_twiddle_scatter_t(const float2* __restrict__ in, const DstPtrs dst,
                                                            int rows, int n1, int A, int logn, long long row0,
                                                            int src, int nparts, const double2* __restrict__ twh,
                                                            const double2* __restrict__ twl, int logb, int onthefly) {
-  __shared__ float2 tile[32][33];
+  __shared__ float2 tile[KB][33];   // [kb][ka]
   const int B = n1 / A, w = n1 / nparts;
   const int r = blockIdx.z;
-  const int kb0 = blockIdx.x * 32, ka0 = blockIdx.y * 32;
+  const int kb0 = blockIdx.x * KB, ka0 = blockIdx.y * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
   const float2* row = in + static_cast<long long>(r) * n1;
 #pragma unroll
-  for (int j = 0; j < 32; j += 8) tile[ty + j][tx] = row[static_cast<long long>(ka0 + ty + j) * B + kb0 + tx];
+  for (int h = 0; h < KB; h += 32)
+#pragma unroll
+    for (int j = 0; j < 32; j += 8)
+      tile[h + tx][ty + j] = row[static_cast<long long>(ka0 + ty + j) * B + kb0 + h + tx];
   __syncthreads();
   const unsigned long long n2 = static_cast<unsigned long long>(row0 + r);
   const int ka = ka0 + tx;
@@ -315,9 +319,9 @@ __global__ void __launch_bounds__(256) k_twiddle_scatter_t(const float2* __restr
   scatter_tw(n2 * static_cast<unsigned long long>(ka + A * (kb0 + ty)), logn, twh, twl, logb, onthefly, cr, ci);
   scatter_tw(n2 * static_cast<unsigned long long>(8 * A), logn, twh, twl, logb, onthefly, sr, si);
 #pragma unroll
-  for (int j = 0; j < 32; j += 8) {
+  for (int j = 0; j < KB; j += 8) {
     const int kb = kb0 + ty + j;
-    const float2 v = tile[tx][ty + j];
+    const float2 v = tile[ty + j][tx];
     const float fr = static_cast<float>(cr), fi = static_cast<float>(ci);
     const int k1 = ka + A * kb;
     const int q = k1 / w, kl = k1 - q * w;
@@ -735,11 +739,13 @@ void dist_twiddle_scatter_t(const void* in, void* const* d_dst, size_t rows, siz
     throw std::invalid_argument("twiddle_scatter_t: A and n1 / A must be multiples of 32, rows <= 65535");
   DstPtrs dp{};
   for (int q = 0; q < nparts; ++q) dp.p[q] = static_cast<float2*>(d_dst[q]);
-  const dim3 grid(static_cast<unsigned>(n1 / a / 32), static_cast<unsigned>(a / 32), static_cast<unsigned>(rows));
-  k_twiddle_scatter_t<<<grid, dim3(32, 8), 0, st>>>(static_cast<const float2*>(in), dp, static_cast<int>(rows),
-                                                     static_cast<int>(n1), static_cast<int>(a), tw->logn,
-                                                     static_cast<long long>(row0), src, nparts, tw->hi, tw->lo,
-                                                     tw->logb, trig_mode == AMQFT_TRIG_ONTHEFLY ? 1 : 0);
+  const bool wide = (n1 / a) % 64 == 0;
+  const dim3 grid(static_cast<unsigned>(n1 / a / (wide ? 64 : 32)), static_cast<unsigned>(a / 32),
+                  static_cast<unsigned>(rows));
+  auto kern = wide ? k_twiddle_scatter_t<64> : k_twiddle_scatter_t<32>;
+  kern<<<grid, dim3(32, 8), 0, st>>>(static_cast<const float2*>(in), dp, static_cast<int>(rows), static_cast<int>(n1),
+                                      static_cast<int>(a), tw->logn, static_cast<long long>(row0), src, nparts,
+                                      tw->hi, tw->lo, tw->logb, trig_mode == AMQFT_TRIG_ONTHEFLY ? 1 : 0);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("k_twiddle_scatter_t: ") + cudaGetErrorString(e));
 }
