@@ -696,8 +696,8 @@ class Tile3PlanImpl final : public FastPlan {
 };
 
 // The split per size (fast.cu tile_split mirrors it for the op counts).
-// Measured on the B200, ms per 2^28 reals (tools/tile_ab.sh, AMQFT_TILE_AB
-// builds): fp32 2048 as 64 x 32 0.780 (32 x 64: 0.803); 512 as 16 x 32 0.679
+// Measured on the B200, ms per 2^28 reals (A/B instances built during
+// development, tools/prof_fast.py): fp32 2048 as 64 x 32 0.780 (32 x 64: 0.803); 512 as 16 x 32 0.679
 // (32 x 16: 0.717); 8192 as 32 x 16 x 16 at 256 threads x 2 CTAs 0.747 (16 x
 // 16 x 32: 0.802; 128 threads x 3: 0.93); 16384 as 32 x 16 x 32 at 512
 // threads 0.843 (16 x 32 x 32: 0.959, 32 x 32 x 16: 0.928); 2^15 on a cluster
