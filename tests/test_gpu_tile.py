@@ -280,3 +280,33 @@ def test_tile_dct_dst_rows_match_cpu(oracle, restatement, n, dtype):
             assert np.array_equal(t.double().cpu().numpy(), got), (v, f, n, dtype)
             back = run_plan(plan, got.astype(np.float32) if dtype == "f32" else got, inverse=True)
             assert r.rel_l2(back.ravel(), xs.ravel()) <= (1e-5 * math.log2(n) if dtype == "f32" else 1e-9), (v, f, n)
+
+
+@pytest.mark.parametrize("n", [4096, 1 << 15, 1 << 18])
+def test_exec_is_cuda_graph_capturable(n):
+    """include/amqft_b200.h: the device entry points allocate nothing and are
+    stream-ordered -- a forward of the tile kernel (4096), the cluster tile
+    kernel (2^15, cudaLaunchKernelEx) and the column-slab plan (2^18, two
+    launches through the plan's scratch) captures into a CUDA graph and replays
+    with the same bits."""
+    rows = 6
+    x = torch.tensor(np.random.default_rng(n + 5).standard_normal((rows, 2 * n)), dtype=torch.float32, device=DEV)
+    plan = amqft.Plan(4, amqft.FunctionId.Cdft, n, rows, dtype="f32", order=amqft.Order.Fast)
+    want = torch.empty_like(x)
+    plan.forward(x, want)
+    torch.cuda.synchronize()
+    y = torch.zeros_like(x)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(side):
+        plan.forward(x, y, stream=side)          # warm-up on the capture stream
+        side.synchronize()
+        y.zero_()
+        with torch.cuda.graph(g, stream=side):
+            plan.forward(x, y, stream=side)
+    torch.cuda.synchronize()
+    assert float(y.abs().max()) == 0.0, "capture must not execute"
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(y, want)
